@@ -1,0 +1,173 @@
+/*
+ * sfmm_gpu.h -- C ABI of the B200 (sm_100a) drop-in for the SRS-FMM apply.
+ *
+ * Replaces the reference's apply entry point
+ *     template<class K> std::vector<S> sfmm::fmm_apply(const ApplyPlan<K>&,
+ *                                                       const std::vector<S>& q,
+ *                                                       ApplyStats* = nullptr)
+ * declared at /root/reference/proj/include/sfmm/apply.hpp:91-94 and defined at
+ * /root/reference/proj/src/apply.cpp:306-337 (explicit instantiations :339-353).
+ *
+ * The reference API is a C++ template over borrowed Tree / NeighborLists /
+ * SkeletonSet objects (apply.hpp:32-42).  Across this ABI those objects travel
+ * as one flat, plain-pointer descriptor (sfmm_plan_desc) that is copied into
+ * device memory once by sfmm_gpu_plan_create and then stays resident in HBM.
+ * The header-only C++ wrapper include/sfmm_gpu.hpp builds the descriptor from
+ * a reference ApplyPlan<K> and maps the return codes back onto the
+ * reference's exceptions.
+ *
+ * No exceptions cross this boundary.  Every entry point returns an int code;
+ * sfmm_gpu_last_error() gives the thread-local message of the last failure.
+ */
+#ifndef SFMM_GPU_H_
+#define SFMM_GPU_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Kernel families, same order as sfmm::KernelFamily (kernel.hpp:12). */
+enum {
+  SFMM_LAPLACE2D = 0,   /* -log(r^2)/(4 pi)            kernel.hpp:40-44 */
+  SFMM_LAPLACE3D = 1,   /* 1/(4 pi r)                  kernel.hpp:46-50 */
+  SFMM_HELMHOLTZ2D = 2, /* (i/4) H0(kappa r)           kernel.hpp:52-60 (unsupported on GPU) */
+  SFMM_HELMHOLTZ3D = 3  /* exp(i kappa r)/(4 r)        kernel.hpp:62-71 */
+};
+
+/* Return codes.  EINVAL <-> std::invalid_argument (apply.cpp:313-314, :73-75);
+ * EDUPLICATE <-> sfmm::DuplicatePointError (apply.cpp:44-46, common.hpp:19-23). */
+enum {
+  SFMM_OK = 0,
+  SFMM_EINVAL = 1,
+  SFMM_EDUPLICATE = 2,
+  SFMM_ECUDA = 3,
+  SFMM_ENOMEM = 4,
+  SFMM_ENCCL = 5,
+  SFMM_EUNSUPPORTED = 6
+};
+
+/* Flags for sfmm_gpu_apply. */
+enum {
+  SFMM_HOST_BUFFERS = 0,   /* q and u are host pointers (pageable or pinned) */
+  SFMM_DEVICE_BUFFERS = 1  /* q and u are device pointers on the plan's device */
+};
+
+/*
+ * Flat plan descriptor.  All arrays are host memory, read once during
+ * sfmm_gpu_plan_create and not retained.  Field meanings follow the reference
+ * types one to one:
+ *   Tree            tree.hpp:323-341   (pts, perm, level_begin, boxes)
+ *   TreeBox         tree.hpp:308-321   (parent, level, begin/end, leaf)
+ *   NeighborLists   tree.hpp:357-365   (colleagues, coarse, fine)
+ *   BoxSkeleton     skeleton.hpp:260-269 (index_vec, skel_pos, red_pos,
+ *                                         interp, parent_offset)
+ * Per-box variable-length lists are CSR: off[b]..off[b+1] (n_boxes+1 entries).
+ * T is the concatenation of every box's k x r row-major interpolation matrix
+ * (BoxSkeleton::interp); T_off counts scalars, complex scalars are two
+ * interleaved doubles (re, im) as in std::complex<double>.
+ */
+typedef struct sfmm_plan_desc {
+  int32_t kernel;           /* SFMM_LAPLACE2D ... */
+  int32_t dim;              /* 2 or 3 */
+  double kappa;             /* wavenumber, Helmholtz only */
+  int64_t n_points;
+  int32_t n_boxes;
+  int32_t depth;            /* Tree::depth, root is level 0 */
+  const double* pts;        /* Tree::pts: n_points*dim, tree order, interleaved */
+  const int32_t* perm;      /* Tree::perm: tree position -> original index */
+  const int32_t* level_begin; /* depth+2 entries */
+  const int32_t* box_parent;  /* -1 for the root */
+  const int32_t* box_level;
+  const int32_t* box_begin;   /* tree-order point range of the box */
+  const int32_t* box_end;
+  const uint8_t* box_leaf;
+  const int32_t* box_parent_offset; /* BoxSkeleton::parent_offset */
+  const int64_t* iv_off;    /* index_vec CSR */
+  const int32_t* iv;
+  const int64_t* sk_off;    /* skel_pos CSR (positions into index_vec, ascending) */
+  const int32_t* skel_pos;
+  const int64_t* rd_off;    /* red_pos CSR (complement of skel_pos, ascending) */
+  const int32_t* red_pos;
+  const int64_t* T_off;     /* n_boxes+1, in scalars */
+  const double* T;
+  const int64_t* coll_off;  /* colleagues (ascending box id, self included) */
+  const int32_t* coll;
+  const int64_t* coarse_off;
+  const int32_t* coarse;
+  const int64_t* fine_off;
+  const int32_t* fine;
+} sfmm_plan_desc;
+
+/* ApplyStats (apply.hpp:12-18) plus device timings of the last apply. */
+typedef struct sfmm_gpu_stats {
+  int64_t n_ifo_pairs;
+  int64_t n_ifs_pairs;
+  int64_t n_tfo_pairs;
+  int64_t n_level1_pairs;
+  int32_t direct_fallback;
+  float ms_total;           /* device time of the apply (events on the plan stream) */
+  float ms_translate;       /* device time of the fused translation kernel K2 */
+} sfmm_gpu_stats;
+
+/* Static facts about a plan, used for roofline accounting. */
+typedef struct sfmm_gpu_plan_info {
+  int64_t n_points;
+  int32_t n_boxes;
+  int32_t depth;
+  int64_t n_slots;          /* sum over boxes of |index_vec| */
+  int64_t n_skel;           /* sum over boxes of k */
+  int64_t m_proj;           /* sum over boxes of k*r (= SkeletonSet::proj_scalars) */
+  double p_dense;           /* dense pair evaluations of one apply */
+  double p_skel;            /* skeleton pair evaluations in the reference */
+  int64_t n_tasks;          /* K2 work items */
+  int64_t device_bytes;     /* resident plan bytes */
+  int64_t n_ifo_pairs, n_ifs_pairs, n_tfo_pairs, n_level1_pairs;
+} sfmm_gpu_plan_info;
+
+typedef struct sfmm_gpu_plan sfmm_gpu_plan;
+
+/* Builds a device-resident plan on CUDA device `device`. */
+int sfmm_gpu_plan_create(const sfmm_plan_desc* desc, int device, sfmm_gpu_plan** out);
+
+/* u = A q for nrhs right-hand sides.  q and u hold n_points x nrhs scalars,
+ * column-major, in the ORIGINAL point order (apply.cpp:306-337).  Scalars are
+ * double (Laplace) or interleaved complex double (Helmholtz).  Blocks until the
+ * result is in u.  stats may be NULL. */
+int sfmm_gpu_apply(sfmm_gpu_plan* plan, const void* q, void* u, int nrhs, int flags,
+                   sfmm_gpu_stats* stats);
+
+/* Device-pointer variant that only enqueues work on `stream` (a cudaStream_t;
+ * NULL = the plan's own stream) and returns without synchronising.  The
+ * duplicate-point check of this call is reported by the next
+ * sfmm_gpu_check_status on the plan. */
+int sfmm_gpu_apply_async(sfmm_gpu_plan* plan, const void* q_dev, void* u_dev, int nrhs,
+                         void* stream);
+
+/* Synchronises the plan's pending work and returns the error code of the
+ * asynchronous applies since the last call (SFMM_EDUPLICATE if a coincident
+ * pair with distinct ids was met). */
+int sfmm_gpu_check_status(sfmm_gpu_plan* plan);
+
+int sfmm_gpu_plan_info_get(const sfmm_gpu_plan* plan, sfmm_gpu_plan_info* info);
+
+void sfmm_gpu_plan_destroy(sfmm_gpu_plan* plan);
+
+/* Dense u_i = sum_{j != i} G(x_i, x_j) q_j over the points in their given
+ * order, for the listed targets only (oracle.cpp:51-71), on the device.
+ * pts: n*dim host coords; q, u host arrays (u has n_targets scalars). */
+int sfmm_gpu_direct_sum(int kernel, double kappa, int dim, int64_t n, const double* pts,
+                        const void* q, int64_t n_targets, const int32_t* targets, void* u,
+                        int device);
+
+const char* sfmm_gpu_last_error(void);
+
+/* Library version string, and the CUDA arch it was compiled for. */
+const char* sfmm_gpu_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SFMM_GPU_H_ */

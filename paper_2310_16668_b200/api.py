@@ -1,0 +1,168 @@
+"""Python mirror of the reference apply API, running on the sm_100a library.
+
+Reference interface (C++, /root/reference/proj/include/sfmm/apply.hpp):
+    struct ApplyStats { n_ifo_pairs, n_ifs_pairs, n_tfo_pairs, n_level1_pairs,
+                        direct_fallback };                         apply.hpp:12-18
+    template<class K> std::vector<S> fmm_apply(const ApplyPlan<K>&,
+                          const std::vector<S>& q, ApplyStats* = nullptr); :91-94
+Errors: std::invalid_argument on a charge-count mismatch (apply.cpp:313-314)
+-> ValueError; sfmm::DuplicatePointError (a std::domain_error, common.hpp:19-23)
+-> DuplicatePointError.
+
+``GpuPlan`` is the device-resident counterpart of ``ApplyPlan<K>``: it is built
+once from a flat plan descriptor (tree, neighbor lists, skeletons and
+interpolation operators) and keeps everything in HBM.  ``fmm_apply`` takes and
+returns potentials in the ORIGINAL point order like the reference.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _abi
+from ._abi import PlanDescriptor
+
+
+class DuplicatePointError(ValueError):
+    """sfmm::DuplicatePointError: coincident points with distinct indices."""
+
+
+class DeviceError(RuntimeError):
+    pass
+
+
+@dataclass
+class ApplyStats:
+    n_ifo_pairs: int = 0
+    n_ifs_pairs: int = 0
+    n_tfo_pairs: int = 0
+    n_level1_pairs: int = 0
+    direct_fallback: bool = False
+    ms_total: float = 0.0       # device time of the last apply
+    ms_translate: float = 0.0   # device time of the fused translation kernel
+
+
+def _raise(rc: int) -> None:
+    if rc == _abi.SFMM_OK:
+        return
+    msg = _abi.gpu_lib().sfmm_gpu_last_error().decode()
+    if rc == _abi.SFMM_EINVAL:
+        raise ValueError(msg)
+    if rc == _abi.SFMM_EDUPLICATE:
+        raise DuplicatePointError(msg)
+    if rc == _abi.SFMM_EUNSUPPORTED:
+        raise NotImplementedError(msg)
+    if rc == _abi.SFMM_ENOMEM:
+        raise MemoryError(msg)
+    raise DeviceError(msg)
+
+
+class GpuPlan:
+    """Device-resident apply plan (operators uploaded once, resident in HBM)."""
+
+    def __init__(self, desc: PlanDescriptor, device: int = 0):
+        lib = _abi.gpu_lib()
+        self.desc = desc
+        self.device = device
+        h = C.c_void_p()
+        _raise(lib.sfmm_gpu_plan_create(C.byref(desc.struct), device, C.byref(h)))
+        self._h = h
+        self.kernel = desc.kernel
+        self.n_points = desc.n_points
+        self.is_complex = desc.is_complex
+        self.dtype = np.complex128 if self.is_complex else np.float64
+
+    @property
+    def handle(self) -> C.c_void_p:
+        if self._h is None:
+            raise ValueError("plan has been closed")
+        return self._h
+
+    def info(self) -> _abi.PlanInfo:
+        inf = _abi.PlanInfo()
+        _raise(_abi.gpu_lib().sfmm_gpu_plan_info_get(self.handle, C.byref(inf)))
+        return inf
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None:
+            _abi.gpu_lib().sfmm_gpu_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def fmm_apply(plan: GpuPlan, q, stats: ApplyStats | None = None) -> np.ndarray:
+    """u = A q (apply.cpp:306-337) on the GPU; q, u in original point order.
+
+    q has shape (N,) or (N, nrhs); each column is an independent right-hand side.
+    """
+    q = np.asarray(q)
+    one = q.ndim == 1
+    if q.ndim not in (1, 2) or q.shape[0] != plan.n_points:
+        raise ValueError("fmm_apply: charge count does not match the point count")
+    qc = np.asfortranarray(q.reshape(plan.n_points, -1), dtype=plan.dtype)
+    nrhs = qc.shape[1]
+    u = np.empty((plan.n_points, nrhs), dtype=plan.dtype, order="F")
+    st = _abi.GpuStats()
+    _raise(_abi.gpu_lib().sfmm_gpu_apply(plan.handle, qc.ctypes.data, u.ctypes.data, nrhs,
+                                         _abi.SFMM_HOST_BUFFERS, C.byref(st)))
+    if stats is not None:
+        stats.n_ifo_pairs = st.n_ifo_pairs
+        stats.n_ifs_pairs = st.n_ifs_pairs
+        stats.n_tfo_pairs = st.n_tfo_pairs
+        stats.n_level1_pairs = st.n_level1_pairs
+        stats.direct_fallback = bool(st.direct_fallback)
+        stats.ms_total = st.ms_total
+        stats.ms_translate = st.ms_translate
+    return u[:, 0] if one else u
+
+
+def fmm_apply_device(plan: GpuPlan, q_ptr: int, u_ptr: int, nrhs: int = 1, stream: int = 0) -> None:
+    """Enqueues u = A q on device buffers (raw pointers) on `stream`; no sync."""
+    _raise(_abi.gpu_lib().sfmm_gpu_apply_async(plan.handle, C.c_void_p(q_ptr), C.c_void_p(u_ptr),
+                                               nrhs, C.c_void_p(stream or None)))
+
+
+def check_status(plan: GpuPlan) -> None:
+    """Syncs and raises DuplicatePointError if an async apply met one."""
+    _raise(_abi.gpu_lib().sfmm_gpu_check_status(plan.handle))
+
+
+def direct_sum_subset(kernel: int, kappa: float, pts: np.ndarray, q: np.ndarray,
+                      targets: np.ndarray, device: int = 0) -> np.ndarray:
+    """Dense u_i = sum_{j != i} G(x_i,x_j) q_j for the listed targets, on the GPU
+    (oracle.cpp:51-71).  pts: (n, dim) in the same order as q."""
+    pts = np.ascontiguousarray(pts, dtype=np.float64)
+    n, dim = pts.shape
+    cplx = kernel in (_abi.HELMHOLTZ2D, _abi.HELMHOLTZ3D)
+    qd = np.ascontiguousarray(q, dtype=np.complex128 if cplx else np.float64)
+    t = np.ascontiguousarray(targets, dtype=np.int32)
+    u = np.empty(t.size, dtype=qd.dtype)
+    _raise(_abi.gpu_lib().sfmm_gpu_direct_sum(kernel, float(kappa), dim, n, pts.ctypes.data,
+                                              qd.ctypes.data, t.size, t.ctypes.data,
+                                              u.ctypes.data, device))
+    return u
+
+
+def max_rel_err(u: np.ndarray, ref: np.ndarray) -> float:
+    """max_i |u_i - ref_i| / max_i |ref_i| (oracle.hpp:30-41)."""
+    u = np.asarray(u)
+    ref = np.asarray(ref)
+    if u.shape != ref.shape:
+        raise ValueError("max_rel_err: length mismatch")
+    den = float(np.max(np.abs(ref))) if ref.size else 0.0
+    if den == 0.0:
+        raise ArithmeticError("max_rel_err: reference is identically zero")
+    return float(np.max(np.abs(u - ref))) / den

@@ -1,0 +1,44 @@
+// Shared device-side types of the sm_100a SRS-FMM apply.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sfmm_gpu {
+
+// Translation modes of one (target box, source box) entry of the fused
+// translation CSR.  They are the four reference phases (apply.cpp:148-266).
+enum Mode : int32_t {
+  kIFO = 0,  // colleagues, level >= 2: u_b += A(B_b,B_c) q_c ; uhat_b -= A(S_b,S_c) qhat_c
+  kIFS = 1,  // coarse leaves:          u_b += A(B_b,L_c) q_c ; uhat_b -= A(S_b,L_c) q_c
+  kTFO = 2,  // fine boxes of a leaf:   u_b += A(L_b,B_c) q_c - A(L_b,S_c) qhat_c
+  kL1 = 3    // level-1 all pairs:      u_b += A(B_b,B_c) q_c
+};
+
+// Per-box record used by the translation kernel.  Slots of a compressed box
+// are ordered [skeleton (skel_pos order) | redundant (red_pos order)], so
+// qhat/uhat of box b line up with its first k slots.
+struct BoxRec {
+  int64_t slot;   // first slot of the box in the slot arrays
+  int64_t skel;   // first entry of the box in the skeleton arrays (qhat/uhat)
+  int32_t n;      // |index_vec|
+  int32_t k;      // |skel_pos|
+};
+
+// One translation work item: rows [row0, row0+nrows) of target box `box`
+// against every CSR entry of that box.  Each row has exactly one owner, so the
+// kernel writes results with plain stores (no atomics, deterministic).
+struct Task {
+  int32_t box;
+  int32_t row0;
+  int32_t nrows;
+  int32_t pad;
+};
+
+struct EntryRange {
+  int64_t begin;
+  int32_t count;
+  int32_t pad;
+};
+
+}  // namespace sfmm_gpu

@@ -1,0 +1,400 @@
+// K2: the fused translation kernel (ifo + ifs + tfo + level-1 in one launch).
+//
+// Replaces translate_ifo / translate_ifs / translate_tfo / level1_dense and
+// their microkernel add_block (/root/reference/proj/src/apply.cpp:16-42,
+// :148-266).  The reference generates every kernel entry G(x_i, x_j) on the
+// fly for each (target box, source box) pair and runs a second, skeleton-only
+// add_block for the subtract term.  Here every subtract term is folded into
+// the dense pass: S_b is a subset of B_b with the same ids, so G is generated
+// once per (row i, source j) and accumulated into
+//     acc_u += G * a_j        (a_j = q_j, or q_j - qhat_j for tfo)
+//     acc_h += G * h_j        (h_j = qhat_j on skeleton slots for ifo, q_j for
+//                              ifs; only for tasks that own skeleton rows)
+// and the results are stored once per row: U = acc_u * c, UH = -acc_h * c.
+//
+// Scheduling: persistent warps pull cost-sorted tasks (box, 128-row tile)
+// from an atomic counter.  Each row is owned by exactly one warp, so outputs
+// are plain stores: no result atomics, deterministic, thread-count
+// independent (apply.hpp:88-90).  Sources are staged per warp through shared
+// memory in chunks of 32 and broadcast to every lane; each lane holds up to
+// four target rows in registers.
+//
+// The zero diagonal (apply.cpp:31-34) is applied by index in self blocks.  A
+// coincident pair with distinct ids makes the generated entry non-finite; a
+// non-finite row result triggers an exact re-scan of that row, which raises
+// the duplicate flag only if such a pair exists (NaN charges stay NaN, as in
+// the reference).
+#include <math.h>
+
+#include <algorithm>
+
+#include "launch.h"
+
+namespace sfmm_gpu {
+namespace {
+
+constexpr int kWarps = 4;
+constexpr int kThreads = 32 * kWarps;
+constexpr unsigned kFull = 0xffffffffu;
+constexpr double kInv4Pi = 0.0795774715459476678844418816862571810;  // 1/(4 pi)
+
+struct K2Args {
+  const BoxRec* box;
+  const EntryRange* er;
+  const int32_t* ent;
+  const Task* tasks;
+  int64_t n_tasks;
+  const double *X, *Y, *Z;
+  const int32_t* sid;
+  const double* Q;
+  const double* QH;
+  double* U;
+  double* UH;
+  int* counter;
+  int* err;
+  double kappa;
+};
+
+// rsqrt to full double precision: MUFU.RSQ64H seed + one cubic correction
+// (5 FP64 ops).  r2 == 0 yields NaN, which the diagonal select / duplicate
+// check handle.
+__device__ __forceinline__ double rsqrt_fp64(double r2) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r2));
+  const double h = y * y;
+  const double e = fma(-r2, h, 1.0);
+  const double p = fma(0.375, e, 0.5);
+  const double ye = y * e;
+  return fma(p, ye, y);
+}
+
+// Real kernels: g(r2) is proportional to G; the constant goes into `scale`.
+struct GenLaplace3d {  // kernel.hpp:46-50  1/(4 pi r)
+  static constexpr int kDim = 3;
+  static constexpr double kScale = kInv4Pi;
+  __device__ static __forceinline__ double g(double r2) { return rsqrt_fp64(r2); }
+};
+struct GenLaplace2d {  // kernel.hpp:40-44  -log(r^2)/(4 pi)
+  static constexpr int kDim = 2;
+  static constexpr double kScale = -kInv4Pi;
+  __device__ static __forceinline__ double g(double r2) { return log(r2); }
+};
+
+struct WarpSmemReal {
+  double2 xy[32];
+  double2 za[32];  // z, a-weight
+  double h[32];
+};
+
+struct WarpSmemCplx {
+  double2 xy[32];
+  double z[32];
+  double2 a[32];
+  double2 h[32];
+};
+
+// Exact re-scan of one row for coincident points with distinct ids.
+__device__ __noinline__ void verify_row(const K2Args& a, int32_t b, int32_t row, int dim) {
+  const BoxRec tb = a.box[b];
+  const int64_t s = tb.slot + row;
+  const double x = a.X[s], y = a.Y[s], z = a.Z[s];
+  const int32_t id = a.sid[s];
+  const EntryRange er = a.er[b];
+  for (int e = 0; e < er.count; ++e) {
+    const BoxRec sb = a.box[a.ent[er.begin + e] >> 2];
+    for (int j = 0; j < sb.n; ++j) {
+      const int64_t t = sb.slot + j;
+      const double dx = x - a.X[t], dy = y - a.Y[t], dz = dim == 3 ? z - a.Z[t] : 0.0;
+      const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+      if (r2 == 0.0 && a.sid[t] != id) atomicOr(a.err, 1);
+    }
+  }
+}
+
+template <class G, int R, bool H, bool SELF>
+__device__ __forceinline__ void inner_real(const WarpSmemReal& sm, int cnt, int j0,
+                                           const double (&xi)[R], const double (&yi)[R],
+                                           const double (&zi)[R], const int (&rowi)[R],
+                                           double (&au)[R], double (&ah)[R]) {
+#pragma unroll 2
+  for (int jj = 0; jj < cnt; ++jj) {
+    const double2 xy = sm.xy[jj];
+    const double2 za = sm.za[jj];
+    const double wh = H ? sm.h[jj] : 0.0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const double dx = xi[r] - xy.x;
+      const double dy = yi[r] - xy.y;
+      double r2 = fma(dy, dy, dx * dx);
+      if (G::kDim == 3) {
+        const double dz = zi[r] - za.x;
+        r2 = fma(dz, dz, r2);
+      }
+      double g = G::g(r2);
+      if (SELF) g = (rowi[r] == j0 + jj) ? 0.0 : g;
+      au[r] = fma(g, za.y, au[r]);
+      if (H) ah[r] = fma(g, wh, ah[r]);
+    }
+  }
+}
+
+template <class G, int R>
+__device__ __forceinline__ void task_real(const K2Args& a, const Task& t, WarpSmemReal& sm,
+                                          int lane) {
+  const BoxRec tb = a.box[t.box];
+  double xi[R], yi[R], zi[R], au[R], ah[R];
+  int rowi[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int row = t.row0 + r * 32 + lane;
+    rowi[r] = row;
+    const int64_t s = tb.slot + (row < t.row0 + t.nrows ? row : t.row0);
+    xi[r] = a.X[s];
+    yi[r] = a.Y[s];
+    zi[r] = G::kDim == 3 ? a.Z[s] : 0.0;
+    au[r] = 0.0;
+    ah[r] = 0.0;
+  }
+  const EntryRange er = a.er[t.box];
+  const bool skel_rows = t.row0 < tb.k;
+  for (int e = 0; e < er.count; ++e) {
+    const int32_t code = a.ent[er.begin + e];
+    const int32_t c = code >> 2;
+    const int mode = code & 3;
+    const BoxRec sb = a.box[c];
+    const bool self = c == t.box;
+    for (int j0 = 0; j0 < sb.n; j0 += 32) {
+      const int j = j0 + lane;
+      if (j < sb.n) {
+        const int64_t s = sb.slot + j;
+        const double q = a.Q[s];
+        const double qh = j < sb.k ? a.QH[sb.skel + j] : 0.0;
+        double wa = q, wh = 0.0;
+        if (mode == kIFO) wh = qh;
+        else if (mode == kIFS) wh = q;
+        else if (mode == kTFO) wa = q - qh;
+        sm.xy[lane] = make_double2(a.X[s], a.Y[s]);
+        sm.za[lane] = make_double2(G::kDim == 3 ? a.Z[s] : 0.0, wa);
+        sm.h[lane] = wh;
+      }
+      __syncwarp();
+      const int cnt = min(32, sb.n - j0);
+      const bool need_h = skel_rows && (mode == kIFS || (mode == kIFO && j0 < sb.k));
+      if (self) {
+        if (need_h) inner_real<G, R, true, true>(sm, cnt, j0, xi, yi, zi, rowi, au, ah);
+        else inner_real<G, R, false, true>(sm, cnt, j0, xi, yi, zi, rowi, au, ah);
+      } else {
+        if (need_h) inner_real<G, R, true, false>(sm, cnt, j0, xi, yi, zi, rowi, au, ah);
+        else inner_real<G, R, false, false>(sm, cnt, j0, xi, yi, zi, rowi, au, ah);
+      }
+      __syncwarp();
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int row = rowi[r];
+    if (row >= t.row0 + t.nrows) continue;
+    const bool skel_row = row < tb.k;
+    if (!isfinite(au[r]) || (skel_row && !isfinite(ah[r]))) verify_row(a, t.box, row, G::kDim);
+    a.U[tb.slot + row] = au[r] * G::kScale;
+    if (skel_row) a.UH[tb.skel + row] = -ah[r] * G::kScale;
+  }
+}
+
+template <class G>
+__global__ void __launch_bounds__(kThreads, 4) k2_translate_real(K2Args a) {
+  __shared__ WarpSmemReal smem[kWarps];
+  const int lane = threadIdx.x & 31;
+  WarpSmemReal& sm = smem[threadIdx.x >> 5];
+  for (;;) {
+    int t = 0;
+    if (lane == 0) t = atomicAdd(a.counter, 1);
+    t = __shfl_sync(kFull, t, 0);
+    if (t >= a.n_tasks) return;
+    const Task task = a.tasks[t];
+    switch ((task.nrows + 31) >> 5) {
+      case 1: task_real<G, 1>(a, task, sm, lane); break;
+      case 2: task_real<G, 2>(a, task, sm, lane); break;
+      case 3: task_real<G, 3>(a, task, sm, lane); break;
+      default: task_real<G, 4>(a, task, sm, lane); break;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Helmholtz 3D, complex FP64: G = exp(i kappa r)/(4 r) (kernel.hpp:62-71).
+// ---------------------------------------------------------------------------
+template <int R, bool H, bool SELF>
+__device__ __forceinline__ void inner_cplx(const WarpSmemCplx& sm, int cnt, int j0, double kappa,
+                                           const double (&xi)[R], const double (&yi)[R],
+                                           const double (&zi)[R], const int (&rowi)[R],
+                                           double2 (&au)[R], double2 (&ah)[R]) {
+#pragma unroll 1
+  for (int jj = 0; jj < cnt; ++jj) {
+    const double2 xy = sm.xy[jj];
+    const double zz = sm.z[jj];
+    const double2 wa = sm.a[jj];
+    const double2 wh = H ? sm.h[jj] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const double dx = xi[r] - xy.x, dy = yi[r] - xy.y, dz = zi[r] - zz;
+      const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+      const double y = rsqrt_fp64(r2);
+      double s, c;
+      sincos(kappa * (r2 * y), &s, &c);
+      double gr = c * y, gi = s * y;
+      if (SELF && rowi[r] == j0 + jj) {
+        gr = 0.0;
+        gi = 0.0;
+      }
+      au[r].x = fma(gr, wa.x, fma(-gi, wa.y, au[r].x));
+      au[r].y = fma(gr, wa.y, fma(gi, wa.x, au[r].y));
+      if (H) {
+        ah[r].x = fma(gr, wh.x, fma(-gi, wh.y, ah[r].x));
+        ah[r].y = fma(gr, wh.y, fma(gi, wh.x, ah[r].y));
+      }
+    }
+  }
+}
+
+template <int R>
+__device__ __forceinline__ void task_cplx(const K2Args& a, const Task& t, WarpSmemCplx& sm,
+                                          int lane) {
+  const double2* Q = reinterpret_cast<const double2*>(a.Q);
+  const double2* QH = reinterpret_cast<const double2*>(a.QH);
+  const BoxRec tb = a.box[t.box];
+  double xi[R], yi[R], zi[R];
+  double2 au[R], ah[R];
+  int rowi[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int row = t.row0 + r * 32 + lane;
+    rowi[r] = row;
+    const int64_t s = tb.slot + (row < t.row0 + t.nrows ? row : t.row0);
+    xi[r] = a.X[s];
+    yi[r] = a.Y[s];
+    zi[r] = a.Z[s];
+    au[r] = make_double2(0.0, 0.0);
+    ah[r] = make_double2(0.0, 0.0);
+  }
+  const EntryRange er = a.er[t.box];
+  const bool skel_rows = t.row0 < tb.k;
+  for (int e = 0; e < er.count; ++e) {
+    const int32_t code = a.ent[er.begin + e];
+    const int32_t c = code >> 2;
+    const int mode = code & 3;
+    const BoxRec sb = a.box[c];
+    const bool self = c == t.box;
+    for (int j0 = 0; j0 < sb.n; j0 += 32) {
+      const int j = j0 + lane;
+      if (j < sb.n) {
+        const int64_t s = sb.slot + j;
+        const double2 q = Q[s];
+        const double2 qh = j < sb.k ? QH[sb.skel + j] : make_double2(0.0, 0.0);
+        double2 wa = q, wh = make_double2(0.0, 0.0);
+        if (mode == kIFO) wh = qh;
+        else if (mode == kIFS) wh = q;
+        else if (mode == kTFO) wa = make_double2(q.x - qh.x, q.y - qh.y);
+        sm.xy[lane] = make_double2(a.X[s], a.Y[s]);
+        sm.z[lane] = a.Z[s];
+        sm.a[lane] = wa;
+        sm.h[lane] = wh;
+      }
+      __syncwarp();
+      const int cnt = min(32, sb.n - j0);
+      const bool need_h = skel_rows && (mode == kIFS || (mode == kIFO && j0 < sb.k));
+      if (self) {
+        if (need_h) inner_cplx<R, true, true>(sm, cnt, j0, a.kappa, xi, yi, zi, rowi, au, ah);
+        else inner_cplx<R, false, true>(sm, cnt, j0, a.kappa, xi, yi, zi, rowi, au, ah);
+      } else {
+        if (need_h) inner_cplx<R, true, false>(sm, cnt, j0, a.kappa, xi, yi, zi, rowi, au, ah);
+        else inner_cplx<R, false, false>(sm, cnt, j0, a.kappa, xi, yi, zi, rowi, au, ah);
+      }
+      __syncwarp();
+    }
+  }
+  double2* U = reinterpret_cast<double2*>(a.U);
+  double2* UH = reinterpret_cast<double2*>(a.UH);
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int row = rowi[r];
+    if (row >= t.row0 + t.nrows) continue;
+    const bool skel_row = row < tb.k;
+    if (!isfinite(au[r].x) || !isfinite(au[r].y) ||
+        (skel_row && (!isfinite(ah[r].x) || !isfinite(ah[r].y))))
+      verify_row(a, t.box, row, 3);
+    U[tb.slot + row] = make_double2(au[r].x * 0.25, au[r].y * 0.25);
+    if (skel_row) UH[tb.skel + row] = make_double2(-ah[r].x * 0.25, -ah[r].y * 0.25);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 4) k2_translate_cplx(K2Args a) {
+  __shared__ WarpSmemCplx smem[kWarps];
+  const int lane = threadIdx.x & 31;
+  WarpSmemCplx& sm = smem[threadIdx.x >> 5];
+  for (;;) {
+    int t = 0;
+    if (lane == 0) t = atomicAdd(a.counter, 1);
+    t = __shfl_sync(kFull, t, 0);
+    if (t >= a.n_tasks) return;
+    const Task task = a.tasks[t];
+    switch ((task.nrows + 31) >> 5) {
+      case 1: task_cplx<1>(a, task, sm, lane); break;
+      case 2: task_cplx<2>(a, task, sm, lane); break;
+      case 3: task_cplx<3>(a, task, sm, lane); break;
+      default: task_cplx<4>(a, task, sm, lane); break;
+    }
+  }
+}
+
+}  // namespace
+
+int configure_translate(DevPlan& p, int device) {
+  int sms = 0, per_sm = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess)
+    return -1;
+  cudaError_t e;
+  if (p.kernel == SFMM_HELMHOLTZ3D)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_translate_cplx, kThreads, 0);
+  else if (p.kernel == SFMM_LAPLACE3D)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_translate_real<GenLaplace3d>,
+                                                      kThreads, 0);
+  else
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_translate_real<GenLaplace2d>,
+                                                      kThreads, 0);
+  if (e != cudaSuccess) return -1;
+  if (per_sm < 1) per_sm = 1;
+  p.k2_grid = sms * per_sm;
+  return 0;
+}
+
+void launch_translate(const DevPlan& p, DevState& s, cudaStream_t st) {
+  if (p.n_tasks == 0) return;
+  K2Args a;
+  a.box = p.box;
+  a.er = p.ent_range;
+  a.ent = p.entries;
+  a.tasks = p.tasks;
+  a.n_tasks = p.n_tasks;
+  a.X = p.X;
+  a.Y = p.Y;
+  a.Z = p.Z;
+  a.sid = p.slot_id;
+  a.Q = s.Q;
+  a.QH = s.QH;
+  a.U = s.U;
+  a.UH = s.UH;
+  a.counter = p.counter;
+  a.err = p.err_flag;
+  a.kappa = p.kappa;
+  cudaMemsetAsync(p.counter, 0, sizeof(int), st);
+  const int grid = (int)std::min<int64_t>(p.k2_grid, (p.n_tasks + kWarps - 1) / kWarps);
+  if (p.kernel == SFMM_HELMHOLTZ3D)
+    k2_translate_cplx<<<grid, kThreads, 0, st>>>(a);
+  else if (p.kernel == SFMM_LAPLACE3D)
+    k2_translate_real<GenLaplace3d><<<grid, kThreads, 0, st>>>(a);
+  else
+    k2_translate_real<GenLaplace2d><<<grid, kThreads, 0, st>>>(a);
+}
+
+}  // namespace sfmm_gpu

@@ -1,0 +1,360 @@
+// K0/K1/K3/K4/K5: leaf gather, interpolation GEMVs, leaf scatter and the
+// dense fallback of the sm_100a SRS-FMM apply.
+//
+//   K0 gather   <- upward_pass leaf branch   apply.cpp:124-125
+//   K1 upward   <- upward_pass l >= 2        apply.cpp:126-143
+//   K3 downward <- downward_pass             apply.cpp:274-293
+//   K4 scatter  <- downward_pass leaf loop   apply.cpp:294-302
+//   K5 direct   <- fmm_apply depth < 2       apply.cpp:316-328, oracle.cpp:9-49
+//
+// K1 and K3 read every interpolation matrix T exactly once per apply with
+// coalesced row (K1) or column (K3) sweeps; they are HBM-bound.  Slots of a
+// compressed box are stored [skeleton | redundant], so the vectors they touch
+// are contiguous.
+#include <algorithm>
+
+#include "launch.h"
+
+namespace sfmm_gpu {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kUpThreads = 128;
+constexpr double kInv4Pi = 0.0795774715459476678844418816862571810;
+
+template <class S>
+__global__ void k0_gather(const int64_t* __restrict__ slot, const int32_t* __restrict__ orig,
+                          int64_t n, const S* __restrict__ q, S* __restrict__ Q) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x)
+    Q[slot[t]] = q[orig[t]];
+}
+
+template <class S>
+__global__ void k4_scatter(const int64_t* __restrict__ slot, const int32_t* __restrict__ orig,
+                           int64_t n, const S* __restrict__ U, S* __restrict__ u) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x)
+    u[orig[t]] = U[slot[t]];
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+// K1, real: qhat_i = q_S[i] + sum_j T[i,j] q_R[j] for kUpRows rows of one box.
+__global__ void __launch_bounds__(kUpThreads) k1_upward_real(
+    const LevelItem* __restrict__ items, const BoxRec* __restrict__ box,
+    const int64_t* __restrict__ T_off, const double* __restrict__ T, double* __restrict__ Q,
+    double* __restrict__ QH, const int64_t* __restrict__ up_dst) {
+  extern __shared__ double smq[];
+  const LevelItem it = items[blockIdx.x];
+  const BoxRec br = box[it.box];
+  const int k = br.k, r = br.n - br.k;
+  const double* qR = Q + br.slot + k;
+  for (int j = threadIdx.x; j < r; j += blockDim.x) smq[j] = qR[j];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const double* Tb = T + T_off[it.box];
+  const int i1 = min(it.first + kUpRows, k);
+  for (int i = it.first + w; i < i1; i += kUpThreads / 32) {
+    const double* Ti = Tb + (int64_t)i * r;
+    double acc = 0.0;
+    for (int j = lane; j < r; j += 32) acc = fma(Ti[j], smq[j], acc);
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      const double v = Q[br.slot + i] + acc;
+      QH[br.skel + i] = v;
+      Q[up_dst[br.skel + i]] = v;
+    }
+  }
+}
+
+// K1, complex.
+__global__ void __launch_bounds__(kUpThreads) k1_upward_cplx(
+    const LevelItem* __restrict__ items, const BoxRec* __restrict__ box,
+    const int64_t* __restrict__ T_off, const double2* __restrict__ T, double2* __restrict__ Q,
+    double2* __restrict__ QH, const int64_t* __restrict__ up_dst) {
+  extern __shared__ double2 smq2[];
+  const LevelItem it = items[blockIdx.x];
+  const BoxRec br = box[it.box];
+  const int k = br.k, r = br.n - br.k;
+  const double2* qR = Q + br.slot + k;
+  for (int j = threadIdx.x; j < r; j += blockDim.x) smq2[j] = qR[j];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const double2* Tb = T + T_off[it.box];
+  const int i1 = min(it.first + kUpRows, k);
+  for (int i = it.first + w; i < i1; i += kUpThreads / 32) {
+    const double2* Ti = Tb + (int64_t)i * r;
+    double ar = 0.0, ai = 0.0;
+    for (int j = lane; j < r; j += 32) {
+      const double2 t = Ti[j], x = smq2[j];
+      ar = fma(t.x, x.x, fma(-t.y, x.y, ar));
+      ai = fma(t.x, x.y, fma(t.y, x.x, ai));
+    }
+    ar = warp_sum(ar);
+    ai = warp_sum(ai);
+    if (lane == 0) {
+      const double2 q = Q[br.slot + i];
+      const double2 v = make_double2(q.x + ar, q.y + ai);
+      QH[br.skel + i] = v;
+      Q[up_dst[br.skel + i]] = v;
+    }
+  }
+}
+
+// K3, real: uhat = UH + U[parent slice]; U_S += uhat; U_R += T^T uhat.
+__global__ void __launch_bounds__(kDownCols) k3_downward_real(
+    const LevelItem* __restrict__ items, const BoxRec* __restrict__ box,
+    const int64_t* __restrict__ T_off, const double* __restrict__ T, double* __restrict__ U,
+    const double* __restrict__ UH, const int64_t* __restrict__ up_dst) {
+  extern __shared__ double smu[];
+  const LevelItem it = items[blockIdx.x];
+  const BoxRec br = box[it.box];
+  const int k = br.k, r = br.n - br.k;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    const double v = UH[br.skel + i] + U[up_dst[br.skel + i]];
+    smu[i] = v;
+    if (it.first == 0) U[br.slot + i] += v;
+  }
+  __syncthreads();
+  const int j = it.first + threadIdx.x;
+  if (j >= r) return;
+  const double* Tb = T + T_off[it.box] + j;
+  double acc = 0.0;
+#pragma unroll 4
+  for (int i = 0; i < k; ++i) acc = fma(Tb[(int64_t)i * r], smu[i], acc);
+  U[br.slot + k + j] += acc;
+}
+
+// K3, complex: U_R += conj(T)^T uhat (apply.cpp:290).
+__global__ void __launch_bounds__(kDownCols) k3_downward_cplx(
+    const LevelItem* __restrict__ items, const BoxRec* __restrict__ box,
+    const int64_t* __restrict__ T_off, const double2* __restrict__ T, double2* __restrict__ U,
+    const double2* __restrict__ UH, const int64_t* __restrict__ up_dst) {
+  extern __shared__ double2 smu2[];
+  const LevelItem it = items[blockIdx.x];
+  const BoxRec br = box[it.box];
+  const int k = br.k, r = br.n - br.k;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    const double2 a = UH[br.skel + i], b = U[up_dst[br.skel + i]];
+    const double2 v = make_double2(a.x + b.x, a.y + b.y);
+    smu2[i] = v;
+    if (it.first == 0) {
+      double2 o = U[br.slot + i];
+      U[br.slot + i] = make_double2(o.x + v.x, o.y + v.y);
+    }
+  }
+  __syncthreads();
+  const int j = it.first + threadIdx.x;
+  if (j >= r) return;
+  const double2* Tb = T + T_off[it.box] + j;
+  double ar = 0.0, ai = 0.0;
+#pragma unroll 4
+  for (int i = 0; i < k; ++i) {
+    const double2 t = Tb[(int64_t)i * r], u = smu2[i];
+    ar = fma(t.x, u.x, fma(t.y, u.y, ar));
+    ai = fma(t.x, u.y, fma(-t.y, u.x, ai));
+  }
+  double2 o = U[br.slot + k + j];
+  U[br.slot + k + j] = make_double2(o.x + ar, o.y + ai);
+}
+
+// Kernel value exactly as the reference writes it (kernel.hpp:40-71), with
+// every operation rounded separately (no FMA contraction), so the depth < 2
+// fallback reproduces direct_sum's arithmetic.
+__device__ __forceinline__ double2 ref_from_r2(int kernel, double kappa, double r2) {
+  const double pi4 = 4.0 * 3.14159265358979323846264338327950288;
+  if (kernel == SFMM_LAPLACE3D) return make_double2(__ddiv_rn(1.0, __dmul_rn(pi4, __dsqrt_rn(r2))), 0.0);
+  if (kernel == SFMM_LAPLACE2D) return make_double2(__dmul_rn(log(r2), -1.0 / pi4), 0.0);
+  const double r = __dsqrt_rn(r2);
+  const double kr = __dmul_rn(kappa, r);
+  const double r4 = __dmul_rn(4.0, r);
+  return make_double2(__ddiv_rn(cos(kr), r4), __ddiv_rn(sin(kr), r4));
+}
+
+__device__ __forceinline__ double ref_r2(const double* xi, const double* xj, int dim) {
+  double r2 = 0.0;
+  for (int k = 0; k < dim; ++k) {
+    const double dx = __dsub_rn(xi[k], xj[k]);
+    r2 = __dadd_rn(r2, __dmul_rn(dx, dx));
+  }
+  return r2;
+}
+
+// K5: one thread per target, sources ascending, j == i skipped (oracle.cpp:9-31).
+__global__ void k5_direct(int kernel, double kappa, int dim, int cplx, int64_t n,
+                          const double* __restrict__ pts, const double* __restrict__ q,
+                          double* __restrict__ u, int* err) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double xi[3];
+  for (int k = 0; k < dim; ++k) xi[k] = pts[i * dim + k];
+  double ar = 0.0, ai = 0.0;
+  for (int64_t j = 0; j < n; ++j) {
+    if (j == i) continue;
+    const double r2 = ref_r2(xi, pts + j * dim, dim);
+    if (r2 == 0.0) {
+      atomicOr(err, 1);
+      continue;
+    }
+    const double2 g = ref_from_r2(kernel, kappa, r2);
+    if (cplx) {
+      const double qr = q[2 * j], qi = q[2 * j + 1];
+      ar = __dadd_rn(ar, __dsub_rn(__dmul_rn(g.x, qr), __dmul_rn(g.y, qi)));
+      ai = __dadd_rn(ai, __dadd_rn(__dmul_rn(g.x, qi), __dmul_rn(g.y, qr)));
+    } else {
+      ar = __dadd_rn(ar, __dmul_rn(g.x, q[j]));
+    }
+  }
+  if (cplx) {
+    u[2 * i] = ar;
+    u[2 * i + 1] = ai;
+  } else {
+    u[i] = ar;
+  }
+}
+
+// Dense subset sum for accuracy checks: one CTA per target, block reduction.
+__global__ void __launch_bounds__(256) k5_direct_subset(int kernel, double kappa, int dim,
+                                                        int cplx, int64_t n,
+                                                        const double* __restrict__ pts,
+                                                        const double* __restrict__ q,
+                                                        const int32_t* __restrict__ targets,
+                                                        double* __restrict__ u, int* err) {
+  __shared__ double red[2][8];
+  const int64_t i = targets[blockIdx.x];
+  double xi[3];
+  for (int k = 0; k < dim; ++k) xi[k] = pts[i * dim + k];
+  double ar = 0.0, ai = 0.0;
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+    if (j == i) continue;
+    const double r2 = ref_r2(xi, pts + j * dim, dim);
+    if (r2 == 0.0) {
+      atomicOr(err, 1);
+      continue;
+    }
+    const double2 g = ref_from_r2(kernel, kappa, r2);
+    if (cplx) {
+      const double qr = q[2 * j], qi = q[2 * j + 1];
+      ar += g.x * qr - g.y * qi;
+      ai += g.x * qi + g.y * qr;
+    } else {
+      ar += g.x * q[j];
+    }
+  }
+  ar = warp_sum(ar);
+  ai = warp_sum(ai);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) {
+    red[0][w] = ar;
+    red[1][w] = ai;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sr = 0, si = 0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
+      sr += red[0][k];
+      si += red[1][k];
+    }
+    if (cplx) {
+      u[2 * blockIdx.x] = sr;
+      u[2 * blockIdx.x + 1] = si;
+    } else {
+      u[blockIdx.x] = sr;
+    }
+  }
+}
+
+int grid_for(int64_t n, int threads) {
+  const int64_t g = (n + threads - 1) / threads;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 32));
+}
+
+}  // namespace
+
+void launch_gather(const DevPlan& p, const double* q, DevState& s, cudaStream_t st) {
+  const int g = grid_for(p.n_points, 256);
+  if (p.cplx)
+    k0_gather<double2><<<g, 256, 0, st>>>(p.leaf_slot, p.leaf_orig, p.n_points,
+                                          reinterpret_cast<const double2*>(q),
+                                          reinterpret_cast<double2*>(s.Q));
+  else
+    k0_gather<double><<<g, 256, 0, st>>>(p.leaf_slot, p.leaf_orig, p.n_points, q, s.Q);
+}
+
+void launch_scatter(const DevPlan& p, const DevState& s, double* u, cudaStream_t st) {
+  const int g = grid_for(p.n_points, 256);
+  if (p.cplx)
+    k4_scatter<double2><<<g, 256, 0, st>>>(p.leaf_slot, p.leaf_orig, p.n_points,
+                                           reinterpret_cast<const double2*>(s.U),
+                                           reinterpret_cast<double2*>(u));
+  else
+    k4_scatter<double><<<g, 256, 0, st>>>(p.leaf_slot, p.leaf_orig, p.n_points, s.U, u);
+}
+
+void launch_upward(const DevPlan& p, const HostPlan& hp, int level, DevState& s,
+                   cudaStream_t st) {
+  const int64_t i0 = hp.up_lvl[level], i1 = hp.up_lvl[level + 1];
+  if (i1 <= i0) return;
+  if (p.cplx)
+    k1_upward_cplx<<<(unsigned)(i1 - i0), kUpThreads, p.up_smem, st>>>(
+        p.up_items + i0, p.box, p.T_off, reinterpret_cast<const double2*>(p.T),
+        reinterpret_cast<double2*>(s.Q), reinterpret_cast<double2*>(s.QH), p.up_dst);
+  else
+    k1_upward_real<<<(unsigned)(i1 - i0), kUpThreads, p.up_smem, st>>>(
+        p.up_items + i0, p.box, p.T_off, p.T, s.Q, s.QH, p.up_dst);
+}
+
+void launch_downward(const DevPlan& p, const HostPlan& hp, int level, DevState& s,
+                     cudaStream_t st) {
+  const int64_t i0 = hp.down_lvl[level], i1 = hp.down_lvl[level + 1];
+  if (i1 <= i0) return;
+  if (p.cplx)
+    k3_downward_cplx<<<(unsigned)(i1 - i0), kDownCols, p.down_smem, st>>>(
+        p.down_items + i0, p.box, p.T_off, reinterpret_cast<const double2*>(p.T),
+        reinterpret_cast<double2*>(s.U), reinterpret_cast<const double2*>(s.UH), p.up_dst);
+  else
+    k3_downward_real<<<(unsigned)(i1 - i0), kDownCols, p.down_smem, st>>>(
+        p.down_items + i0, p.box, p.T_off, p.T, s.U, s.UH, p.up_dst);
+}
+
+void launch_direct_fallback(const DevPlan& p, const double* q, double* u, cudaStream_t st) {
+  const int threads = 128;
+  const unsigned g = (unsigned)((p.n_points + threads - 1) / threads);
+  k5_direct<<<g, threads, 0, st>>>(p.kernel, p.kappa, p.dim, p.cplx, p.n_points, p.orig_pts, q,
+                                   u, p.err_flag);
+}
+
+void launch_direct_subset(int kernel, double kappa, int dim, int64_t n, const double* pts,
+                          const double* q, int64_t nt, const int32_t* targets, double* u,
+                          int* err_flag, cudaStream_t st) {
+  if (nt <= 0) return;
+  k5_direct_subset<<<(unsigned)nt, 256, 0, st>>>(kernel, kappa, dim,
+                                                 kernel == SFMM_HELMHOLTZ3D ? 1 : 0, n, pts, q,
+                                                 targets, u, err_flag);
+}
+
+int configure_tree_kernels(DevPlan& p, size_t max_r, size_t max_k) {
+  const size_t sw = p.cplx ? 16 : 8;
+  p.up_smem = std::max<size_t>(max_r * sw, 16);
+  p.down_smem = std::max<size_t>(max_k * sw, 16);
+  if (p.up_smem > 48 * 1024) {
+    if (cudaFuncSetAttribute(p.cplx ? (const void*)k1_upward_cplx : (const void*)k1_upward_real,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)p.up_smem) != cudaSuccess)
+      return -1;
+  }
+  if (p.down_smem > 48 * 1024) {
+    if (cudaFuncSetAttribute(
+            p.cplx ? (const void*)k3_downward_cplx : (const void*)k3_downward_real,
+            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.down_smem) != cudaSuccess)
+      return -1;
+  }
+  return 0;
+}
+
+}  // namespace sfmm_gpu

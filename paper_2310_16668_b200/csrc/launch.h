@@ -1,0 +1,68 @@
+// Kernel launchers of the sm_100a SRS-FMM apply (K0..K5).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "plan_build.h"
+
+namespace sfmm_gpu {
+
+// Per-apply device state for one right-hand side.  Scalars are double or
+// interleaved complex (cplx = 1).
+struct DevState {
+  double* Q;    // slot charges        (n_slots scalars)
+  double* QH;   // skeleton charges    (n_skel scalars)
+  double* U;    // slot potentials     (n_slots scalars)
+  double* UH;   // skeleton potentials (n_skel scalars)
+};
+
+struct DevPlan {
+  int kernel, dim, cplx;
+  double kappa;
+  int64_t n_points, n_slots, n_skel;
+  int32_t n_boxes, depth;
+  BoxRec* box;
+  EntryRange* ent_range;
+  int32_t* entries;
+  Task* tasks;
+  int64_t n_tasks;
+  double *X, *Y, *Z;
+  int32_t* slot_id;
+  int64_t* up_dst;
+  int64_t* leaf_slot;
+  int32_t* leaf_orig;
+  double* T;
+  int64_t* T_off;
+  LevelItem *up_items, *down_items;
+  double* orig_pts;
+  int* counter;     // K2 task counter (reset per launch)
+  int* err_flag;    // sticky duplicate-point flag
+  int k2_grid;      // persistent K2 CTAs
+  size_t up_smem, down_smem;
+};
+
+// K0: Q[leaf_slot[t]] = q[leaf_orig[t]]
+void launch_gather(const DevPlan& p, const double* q, DevState& s, cudaStream_t st);
+// K1: one tree level of the upward pass (level >= 2)
+void launch_upward(const DevPlan& p, const HostPlan& hp, int level, DevState& s, cudaStream_t st);
+// K2: fused ifo/ifs/tfo/level-1 translation, all levels in one launch
+void launch_translate(const DevPlan& p, DevState& s, cudaStream_t st);
+// K3: one tree level of the downward pass (level >= 2)
+void launch_downward(const DevPlan& p, const HostPlan& hp, int level, DevState& s,
+                     cudaStream_t st);
+// K4: u[leaf_orig[t]] = U[leaf_slot[t]]
+void launch_scatter(const DevPlan& p, const DevState& s, double* u, cudaStream_t st);
+// K5: dense sum over all points in original order (depth < 2 fallback)
+void launch_direct_fallback(const DevPlan& p, const double* q, double* u, cudaStream_t st);
+// Dense subset sum for accuracy checks: one CTA per target.
+void launch_direct_subset(int kernel, double kappa, int dim, int64_t n, const double* pts,
+                          const double* q, int64_t nt, const int32_t* targets, double* u,
+                          int* err_flag, cudaStream_t st);
+
+// Persistent-grid size and dynamic shared memory setup (called at plan creation).
+int configure_translate(DevPlan& p, int device);
+int configure_tree_kernels(DevPlan& p, size_t max_r, size_t max_k);
+
+}  // namespace sfmm_gpu

@@ -1,0 +1,255 @@
+// Descriptor validation and flattening for the device plan (see plan_build.h).
+#include "plan_build.h"
+
+#include <algorithm>
+#include <numeric>
+
+namespace sfmm_gpu {
+
+namespace {
+
+struct Fail {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void bad(const std::string& m) { throw Fail{SFMM_EINVAL, "sfmm_gpu_plan_create: " + m}; }
+
+}  // namespace
+
+int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err) {
+  try {
+    if (d.kernel == SFMM_HELMHOLTZ2D)
+      throw Fail{SFMM_EUNSUPPORTED,
+                 "sfmm_gpu_plan_create: helmholtz2d (long-double Hankel) has no device path"};
+    if (d.kernel != SFMM_LAPLACE2D && d.kernel != SFMM_LAPLACE3D && d.kernel != SFMM_HELMHOLTZ3D)
+      bad("unknown kernel id");
+    const int want_dim = d.kernel == SFMM_LAPLACE2D ? 2 : 3;
+    if (d.dim != want_dim) bad("kernel dimension mismatch");  // make_plan, apply.cpp:73
+    if (d.n_points < 1) bad("empty point set");
+    if (d.n_boxes < 1 || d.depth < 0) bad("empty tree");
+    if (!d.pts || !d.perm || !d.level_begin || !d.box_parent || !d.box_level || !d.box_begin ||
+        !d.box_end || !d.box_leaf || !d.box_parent_offset || !d.iv_off || !d.sk_off ||
+        !d.rd_off || !d.T_off || !d.coll_off || !d.coarse_off || !d.fine_off)
+      bad("null array in descriptor");
+
+    hp.kernel = d.kernel;
+    hp.dim = d.dim;
+    hp.cplx = d.kernel == SFMM_HELMHOLTZ3D ? 1 : 0;
+    hp.kappa = d.kappa;
+    hp.n_points = d.n_points;
+    hp.n_boxes = d.n_boxes;
+    hp.depth = d.depth;
+    const int64_t N = d.n_points;
+    const int32_t nb = d.n_boxes;
+    const int dim = d.dim;
+
+    hp.level_begin.assign(d.level_begin, d.level_begin + d.depth + 2);
+    if (hp.level_begin[0] != 0 || hp.level_begin[d.depth + 1] != nb) bad("level_begin");
+    for (int l = 0; l <= d.depth; ++l)
+      if (hp.level_begin[l + 1] < hp.level_begin[l]) bad("level_begin not monotone");
+    for (int64_t t = 0; t < N; ++t)
+      if (d.perm[t] < 0 || d.perm[t] >= N) bad("perm out of range");
+
+    if (d.depth < 2) {
+      // fmm_apply falls back to the dense sum on the original order
+      // (apply.cpp:316-328); only coordinates are needed.
+      hp.orig_pts.resize(N * dim);
+      for (int64_t t = 0; t < N; ++t)
+        for (int k = 0; k < dim; ++k) hp.orig_pts[(int64_t)d.perm[t] * dim + k] = d.pts[t * dim + k];
+      return SFMM_OK;
+    }
+
+    hp.box.resize(nb);
+    hp.box_parent.assign(d.box_parent, d.box_parent + nb);
+    hp.box_level.assign(d.box_level, d.box_level + nb);
+    hp.T_off.assign(d.T_off, d.T_off + nb + 1);
+    hp.n_slots = d.iv_off[nb];
+    hp.n_skel = d.sk_off[nb];
+    const int64_t S = hp.n_slots;
+
+    // slot position map: index_vec position -> offset inside the box's slots
+    std::vector<int32_t> posmap(S);
+    for (int32_t b = 0; b < nb; ++b) {
+      const int64_t n = d.iv_off[b + 1] - d.iv_off[b];
+      const int64_t k = d.sk_off[b + 1] - d.sk_off[b];
+      const int64_t r = d.rd_off[b + 1] - d.rd_off[b];
+      if (n < 0 || k < 0 || r < 0) bad("negative CSR extent");
+      if (!(k + r == n || (k == 0 && r == 0))) bad("skel_pos/red_pos do not partition index_vec");
+      if (d.T_off[b + 1] - d.T_off[b] != k * r) bad("T_off does not match k*r");
+      if (d.box_level[b] < 0 || d.box_level[b] > d.depth) bad("box level out of range");
+      BoxRec& br = hp.box[b];
+      br.slot = d.iv_off[b];
+      br.skel = d.sk_off[b];
+      br.n = (int32_t)n;
+      br.k = (int32_t)k;
+      int32_t* pm = posmap.data() + d.iv_off[b];
+      if (k + r == n && n > 0) {
+        std::vector<uint8_t> seen(n, 0);
+        for (int64_t i = 0; i < k; ++i) {
+          const int32_t p = d.skel_pos[d.sk_off[b] + i];
+          if (p < 0 || p >= n || seen[p]) bad("skel_pos out of range or repeated");
+          seen[p] = 1;
+          pm[p] = (int32_t)i;
+        }
+        for (int64_t j = 0; j < r; ++j) {
+          const int32_t p = d.red_pos[d.rd_off[b] + j];
+          if (p < 0 || p >= n || seen[p]) bad("red_pos out of range or repeated");
+          seen[p] = 1;
+          pm[p] = (int32_t)(k + j);
+        }
+      } else {
+        for (int64_t p = 0; p < n; ++p) pm[p] = (int32_t)p;
+      }
+      if (d.box_leaf[b] && d.box_end[b] - d.box_begin[b] != n)
+        bad("leaf index_vec size differs from its point range");
+      hp.m_proj += k * r;
+    }
+
+    // slot coordinates and ids
+    hp.X.resize(S);
+    hp.Y.resize(S);
+    hp.Z.assign(S, 0.0);
+    hp.slot_id.resize(S);
+    for (int32_t b = 0; b < nb; ++b) {
+      const int64_t s0 = d.iv_off[b];
+      for (int64_t p = 0; p < hp.box[b].n; ++p) {
+        const int32_t id = d.iv[s0 + p];
+        if (id < 0 || id >= N) bad("index_vec id out of range");
+        const int64_t s = s0 + posmap[s0 + p];
+        hp.slot_id[s] = id;
+        hp.X[s] = d.pts[(int64_t)id * dim];
+        hp.Y[s] = d.pts[(int64_t)id * dim + 1];
+        if (dim == 3) hp.Z[s] = d.pts[(int64_t)id * dim + 2];
+      }
+    }
+
+    // upward destinations: skeleton entry i of box b lands at
+    // parent position parent_offset + i (skeleton.cpp:204-218; apply.cpp:127-131)
+    hp.up_dst.assign(hp.n_skel, -1);
+    for (int32_t b = 0; b < nb; ++b) {
+      const int32_t p = d.box_parent[b];
+      const int32_t k = hp.box[b].k;
+      if (k == 0) continue;
+      if (p < 0) bad("compressed root box");
+      const int64_t off = d.box_parent_offset[b];
+      if (off < 0 || off + k > hp.box[p].n) bad("parent_offset out of range");
+      for (int32_t i = 0; i < k; ++i)
+        hp.up_dst[hp.box[b].skel + i] = d.iv_off[p] + posmap[d.iv_off[p] + off + i];
+    }
+
+    // leaf gather/scatter maps: slot of position i <-> q[perm[begin + i]]
+    // (apply.cpp:125, :301)
+    hp.leaf_slot.reserve(N);
+    hp.leaf_orig.reserve(N);
+    {
+      std::vector<uint8_t> hit(N, 0);
+      for (int32_t b = 0; b < nb; ++b) {
+        if (!d.box_leaf[b]) continue;
+        const int64_t s0 = d.iv_off[b];
+        std::vector<std::pair<int64_t, int32_t>> tmp(hp.box[b].n);
+        for (int32_t i = 0; i < hp.box[b].n; ++i) {
+          const int64_t t = (int64_t)d.box_begin[b] + i;
+          if (t < 0 || t >= N || hit[t]) bad("leaf point ranges overlap or exceed n_points");
+          hit[t] = 1;
+          tmp[i] = {s0 + posmap[s0 + i], d.perm[t]};
+        }
+        std::sort(tmp.begin(), tmp.end());
+        for (auto& e : tmp) {
+          hp.leaf_slot.push_back(e.first);
+          hp.leaf_orig.push_back(e.second);
+        }
+      }
+      if ((int64_t)hp.leaf_slot.size() != N) bad("leaves do not cover every point");
+    }
+
+    // translation CSR (all four phases, one list per target box)
+    hp.ent_range.resize(nb);
+    const int32_t l1b = hp.level_begin[1], l1e = hp.level_begin[2];
+    for (int32_t b = 0; b < nb; ++b) {
+      EntryRange& er = hp.ent_range[b];
+      er.begin = (int64_t)hp.entries.size();
+      const int lev = d.box_level[b];
+      auto push = [&](int32_t c, int mode) {
+        if (c < 0 || c >= nb) bad("neighbor id out of range");
+        hp.entries.push_back((c << 2) | mode);
+        const double nbn = hp.box[b].n, ncn = hp.box[c].n;
+        hp.p_dense += nbn * ncn;
+        if (mode == kIFO) hp.p_skel += (double)hp.box[b].k * hp.box[c].k;
+        if (mode == kIFS) hp.p_skel += (double)hp.box[b].k * ncn;
+        if (mode == kTFO) hp.p_skel += nbn * hp.box[c].k;
+      };
+      if (lev >= 2) {
+        for (int64_t e = d.coll_off[b]; e < d.coll_off[b + 1]; ++e) {
+          push(d.coll[e], kIFO);
+          ++hp.n_ifo;
+        }
+        for (int64_t e = d.coarse_off[b]; e < d.coarse_off[b + 1]; ++e) {
+          push(d.coarse[e], kIFS);
+          ++hp.n_ifs;
+        }
+      }
+      if (lev == 1) {
+        for (int32_t c = l1b; c < l1e; ++c) {
+          push(c, kL1);
+          ++hp.n_l1;
+        }
+      }
+      if (d.box_leaf[b] && lev >= 1) {
+        for (int64_t e = d.fine_off[b]; e < d.fine_off[b + 1]; ++e) {
+          push(d.fine[e], kTFO);
+          ++hp.n_tfo;
+        }
+      }
+      er.count = (int32_t)((int64_t)hp.entries.size() - er.begin);
+    }
+
+    // tasks: 128-row tiles, longest first (LPT) for the persistent kernel
+    {
+      std::vector<std::pair<double, Task>> tv;
+      for (int32_t b = 0; b < nb; ++b) {
+        const EntryRange& er = hp.ent_range[b];
+        if (er.count == 0 || hp.box[b].n == 0) continue;
+        double src = 0;
+        for (int64_t e = er.begin; e < er.begin + er.count; ++e) src += hp.box[hp.entries[e] >> 2].n;
+        for (int32_t r0 = 0; r0 < hp.box[b].n; r0 += kTileRows) {
+          Task t{b, r0, std::min(kTileRows, hp.box[b].n - r0), 0};
+          const double lanes_rows = 32.0 * ((t.nrows + 31) / 32);
+          tv.push_back({lanes_rows * (src + 8.0), t});
+        }
+      }
+      std::stable_sort(tv.begin(), tv.end(),
+                       [](const auto& a, const auto& b) { return a.first > b.first; });
+      hp.tasks.reserve(tv.size());
+      for (auto& e : tv) hp.tasks.push_back(e.second);
+    }
+
+    // interpolation work lists per level (levels >= 2 carry T)
+    hp.up_lvl.assign(d.depth + 2, 0);
+    hp.down_lvl.assign(d.depth + 2, 0);
+    for (int l = 0; l <= d.depth; ++l) {
+      hp.up_lvl[l] = (int64_t)hp.up_items.size();
+      hp.down_lvl[l] = (int64_t)hp.down_items.size();
+      if (l >= 2) {
+        for (int32_t b = hp.level_begin[l]; b < hp.level_begin[l + 1]; ++b) {
+          const int32_t k = hp.box[b].k, r = hp.box[b].n - hp.box[b].k;
+          if (k == 0) continue;
+          for (int32_t i = 0; i < k; i += kUpRows) hp.up_items.push_back({b, i});
+          // one item even when r == 0: it also folds uhat into the skeleton slots
+          for (int32_t j = 0; j < std::max(r, 1); j += kDownCols) hp.down_items.push_back({b, j});
+        }
+      }
+    }
+    hp.up_lvl[d.depth + 1] = (int64_t)hp.up_items.size();
+    hp.down_lvl[d.depth + 1] = (int64_t)hp.down_items.size();
+    return SFMM_OK;
+  } catch (const Fail& f) {
+    err = f.msg;
+    return f.code;
+  } catch (const std::bad_alloc&) {
+    err = "sfmm_gpu_plan_create: host allocation failed";
+    return SFMM_ENOMEM;
+  }
+}
+
+}  // namespace sfmm_gpu

@@ -1,0 +1,70 @@
+// Host-side flattening of an sfmm_plan_desc into the device layout.
+//
+// The reference keeps per-box std::vectors (ApplyPlan::x/xs/sid,
+// ExpansionState::q/u/qhat/uhat; apply.hpp:22-42) and walks the neighbor
+// lists phase by phase (apply.cpp:148-266).  The GPU plan instead owns a few
+// flat arrays that stay resident in HBM:
+//   * slot arrays (one entry per index_vec entry of every box), ordered
+//     per box as [skeleton | redundant] so qhat/uhat are the first k slots;
+//   * one translation CSR per target box covering all four phases;
+//   * a cost-sorted task list for the persistent translation kernel;
+//   * per-level work lists for the upward/downward interpolation GEMVs.
+#pragma once
+
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "sfmm_gpu.h"
+
+namespace sfmm_gpu {
+
+constexpr int kRowsPerLane = 4;                 // max rows per lane in K2
+constexpr int kTileRows = 32 * kRowsPerLane;    // rows per K2 task
+constexpr int kUpRows = 8;                      // K1 rows (skeleton entries) per CTA
+constexpr int kDownCols = 256;                  // K3 columns (redundant slots) per CTA
+
+struct LevelItem {
+  int32_t box;
+  int32_t first;  // first row (K1) / column (K3) of the chunk
+};
+
+struct HostPlan {
+  int kernel = 0, dim = 0, cplx = 0;
+  double kappa = 0;
+  int64_t n_points = 0;
+  int32_t n_boxes = 0, depth = 0;
+  int64_t n_slots = 0, n_skel = 0, m_proj = 0;
+  std::vector<int32_t> level_begin;
+  std::vector<BoxRec> box;
+  std::vector<int32_t> box_parent, box_level;
+  std::vector<int64_t> T_off;                 // scalars
+  // slot arrays
+  std::vector<double> X, Y, Z;
+  std::vector<int32_t> slot_id;               // tree-order point id
+  // skeleton arrays
+  std::vector<int64_t> up_dst;                // parent slot receiving qhat_i
+  // leaf gather / scatter
+  std::vector<int64_t> leaf_slot;
+  std::vector<int32_t> leaf_orig;
+  // translation CSR and tasks
+  std::vector<EntryRange> ent_range;
+  std::vector<int32_t> entries;               // (src box << 2) | mode
+  std::vector<Task> tasks;
+  // interpolation work lists, concatenated per level; *_lvl has depth+2 entries
+  std::vector<LevelItem> up_items, down_items;
+  std::vector<int64_t> up_lvl, down_lvl;
+  // depth < 2: coordinates in original order for the dense fallback
+  std::vector<double> orig_pts;
+  // stats
+  int64_t n_ifo = 0, n_ifs = 0, n_tfo = 0, n_l1 = 0;
+  double p_dense = 0, p_skel = 0;
+};
+
+// Validates the descriptor and fills `hp`.  Returns SFMM_OK or an error code
+// with a message in `err`.
+int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err);
+
+}  // namespace sfmm_gpu

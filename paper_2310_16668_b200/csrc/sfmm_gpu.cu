@@ -1,0 +1,376 @@
+// C ABI of the sm_100a SRS-FMM apply (include/sfmm_gpu.h).
+//
+// Orchestrates one apply exactly in the reference's phase order
+// (fmm_apply, /root/reference/proj/src/apply.cpp:306-337):
+//   K0 gather -> K1 upward (levels depth..2) -> K2 fused translation (one
+//   launch: ifo, ifs, tfo, level-1) -> K3 downward (levels 2..depth) ->
+//   K4 scatter;   depth < 2 -> K5 dense fallback.
+// The plan (geometry, index maps, interpolation operators, translation CSR,
+// task list) is uploaded once by sfmm_gpu_plan_create and stays resident.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "launch.h"
+#include "plan_build.h"
+#include "sfmm_gpu.h"
+
+using namespace sfmm_gpu;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int set_error(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+struct CudaFail {
+  int code;
+  std::string msg;
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  const int code = e == cudaErrorMemoryAllocation ? SFMM_ENOMEM : SFMM_ECUDA;
+  throw CudaFail{code, std::string(what) + ": " + cudaGetErrorString(e)};
+}
+
+}  // namespace
+
+struct sfmm_gpu_plan {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_k2a = nullptr, ev_k2b = nullptr;
+  HostPlan hp;
+  DevPlan dp{};
+  std::vector<void*> allocs;
+  int64_t device_bytes = 0;
+  // per-apply state (grown on demand, one column of scalars)
+  DevState ds{};
+  double* io_q = nullptr;
+  double* io_u = nullptr;
+  size_t io_cap = 0;  // bytes of io_q / io_u
+  std::mutex mu;
+
+  template <class T>
+  T* alloc(size_t count) {
+    void* p = nullptr;
+    const size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+    ck(cudaMalloc(&p, bytes), "cudaMalloc");
+    allocs.push_back(p);
+    device_bytes += (int64_t)bytes;
+    return static_cast<T*>(p);
+  }
+  template <class T>
+  T* upload(const T* src, size_t count) {
+    T* d = alloc<T>(count);
+    if (count) ck(cudaMemcpy(d, src, count * sizeof(T), cudaMemcpyHostToDevice), "upload");
+    return d;
+  }
+  template <class T>
+  T* upload(const std::vector<T>& v) {
+    return upload(v.data(), v.size());
+  }
+
+  ~sfmm_gpu_plan() {
+    cudaSetDevice(device);
+    if (stream) cudaStreamSynchronize(stream);
+    for (void* p : allocs) cudaFree(p);
+    if (io_q) cudaFree(io_q);
+    if (io_u) cudaFree(io_u);
+    if (ev_a) cudaEventDestroy(ev_a);
+    if (ev_b) cudaEventDestroy(ev_b);
+    if (ev_k2a) cudaEventDestroy(ev_k2a);
+    if (ev_k2b) cudaEventDestroy(ev_k2b);
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  void ensure_io(size_t bytes) {
+    if (bytes <= io_cap) return;
+    if (io_q) cudaFree(io_q);
+    if (io_u) cudaFree(io_u);
+    io_q = io_u = nullptr;
+    io_cap = 0;
+    ck(cudaMalloc(&io_q, bytes), "cudaMalloc(q)");
+    ck(cudaMalloc(&io_u, bytes), "cudaMalloc(u)");
+    io_cap = bytes;
+  }
+
+  // Enqueues one right-hand side: q, u device pointers in original order.
+  void enqueue_one(const double* q, double* u, cudaStream_t st, bool time_k2) {
+    if (hp.depth < 2) {
+      launch_direct_fallback(dp, q, u, st);
+      return;
+    }
+    launch_gather(dp, q, ds, st);
+    for (int l = hp.depth; l >= 2; --l) launch_upward(dp, hp, l, ds, st);
+    if (time_k2) ck(cudaEventRecord(ev_k2a, st), "event");
+    launch_translate(dp, ds, st);
+    if (time_k2) ck(cudaEventRecord(ev_k2b, st), "event");
+    for (int l = 2; l <= hp.depth; ++l) launch_downward(dp, hp, l, ds, st);
+    launch_scatter(dp, ds, u, st);
+  }
+
+  size_t scalar_bytes() const { return hp.cplx ? 16 : 8; }
+};
+
+extern "C" {
+
+const char* sfmm_gpu_last_error(void) { return g_last_error.c_str(); }
+
+const char* sfmm_gpu_version(void) { return "sfmm_gpu 0.1 (sm_100a, FP64)"; }
+
+int sfmm_gpu_plan_create(const sfmm_plan_desc* desc, int device, sfmm_gpu_plan** out) {
+  if (!desc || !out) return set_error(SFMM_EINVAL, "sfmm_gpu_plan_create: null argument");
+  *out = nullptr;
+  sfmm_gpu_plan* p = nullptr;
+  try {
+    p = new sfmm_gpu_plan();
+    std::string err;
+    const int rc = build_host_plan(*desc, p->hp, err);
+    if (rc != SFMM_OK) {
+      delete p;
+      return set_error(rc, err);
+    }
+    p->device = device;
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    ck(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaEventCreate(&p->ev_a), "cudaEventCreate");
+    ck(cudaEventCreate(&p->ev_b), "cudaEventCreate");
+    ck(cudaEventCreate(&p->ev_k2a), "cudaEventCreate");
+    ck(cudaEventCreate(&p->ev_k2b), "cudaEventCreate");
+    HostPlan& hp = p->hp;
+    DevPlan& dp = p->dp;
+    dp.kernel = hp.kernel;
+    dp.dim = hp.dim;
+    dp.cplx = hp.cplx;
+    dp.kappa = hp.kappa;
+    dp.n_points = hp.n_points;
+    dp.n_boxes = hp.n_boxes;
+    dp.depth = hp.depth;
+    dp.counter = p->alloc<int>(4);
+    dp.err_flag = p->alloc<int>(4);
+    ck(cudaMemset(dp.err_flag, 0, 4 * sizeof(int)), "memset");
+    const int sw = hp.cplx ? 2 : 1;
+    if (hp.depth < 2) {
+      dp.orig_pts = p->upload(hp.orig_pts);
+    } else {
+      dp.n_slots = hp.n_slots;
+      dp.n_skel = hp.n_skel;
+      dp.box = p->upload(hp.box);
+      dp.ent_range = p->upload(hp.ent_range);
+      dp.entries = p->upload(hp.entries);
+      dp.tasks = p->upload(hp.tasks);
+      dp.n_tasks = (int64_t)hp.tasks.size();
+      dp.X = p->upload(hp.X);
+      dp.Y = p->upload(hp.Y);
+      dp.Z = p->upload(hp.Z);
+      dp.slot_id = p->upload(hp.slot_id);
+      dp.up_dst = p->upload(hp.up_dst);
+      dp.leaf_slot = p->upload(hp.leaf_slot);
+      dp.leaf_orig = p->upload(hp.leaf_orig);
+      dp.T_off = p->upload(hp.T_off);
+      dp.T = p->upload(desc->T, (size_t)hp.T_off[hp.n_boxes] * sw);
+      dp.up_items = p->upload(hp.up_items);
+      dp.down_items = p->upload(hp.down_items);
+      size_t max_r = 0, max_k = 0;
+      for (const BoxRec& b : hp.box) {
+        max_r = std::max<size_t>(max_r, (size_t)(b.n - b.k));
+        max_k = std::max<size_t>(max_k, (size_t)b.k);
+      }
+      if (configure_tree_kernels(dp, max_r, max_k) != 0)
+        throw CudaFail{SFMM_EUNSUPPORTED, "interpolation block too large for shared memory"};
+      if (configure_translate(dp, device) != 0)
+        throw CudaFail{SFMM_ECUDA, "occupancy query failed"};
+      p->ds.Q = p->alloc<double>((size_t)hp.n_slots * sw);
+      p->ds.U = p->alloc<double>((size_t)hp.n_slots * sw);
+      p->ds.QH = p->alloc<double>((size_t)hp.n_skel * sw);
+      p->ds.UH = p->alloc<double>((size_t)hp.n_skel * sw);
+      // release host copies that now live on the device
+      std::vector<double>().swap(hp.X);
+      std::vector<double>().swap(hp.Y);
+      std::vector<double>().swap(hp.Z);
+      std::vector<int32_t>().swap(hp.slot_id);
+      std::vector<int64_t>().swap(hp.up_dst);
+      std::vector<int64_t>().swap(hp.leaf_slot);
+      std::vector<int32_t>().swap(hp.leaf_orig);
+      std::vector<int32_t>().swap(hp.entries);
+      std::vector<Task>().swap(hp.tasks);
+    }
+    ck(cudaDeviceSynchronize(), "plan upload");
+    *out = p;
+    return SFMM_OK;
+  } catch (const CudaFail& f) {
+    delete p;
+    return set_error(f.code, "sfmm_gpu_plan_create: " + f.msg);
+  } catch (const std::bad_alloc&) {
+    delete p;
+    return set_error(SFMM_ENOMEM, "sfmm_gpu_plan_create: host allocation failed");
+  }
+}
+
+int sfmm_gpu_apply(sfmm_gpu_plan* p, const void* q, void* u, int nrhs, int flags,
+                   sfmm_gpu_stats* stats) {
+  if (!p || (!q && p->hp.n_points) || (!u && p->hp.n_points) || nrhs < 1)
+    return set_error(SFMM_EINVAL, "fmm_apply: bad arguments");
+  std::lock_guard<std::mutex> lock(p->mu);
+  try {
+    ck(cudaSetDevice(p->device), "cudaSetDevice");
+    const size_t col = (size_t)p->hp.n_points * p->scalar_bytes();
+    const bool host = flags == SFMM_HOST_BUFFERS;
+    cudaStream_t st = p->stream;
+    if (host) p->ensure_io(col);
+    ck(cudaEventRecord(p->ev_a, st), "event");
+    for (int r = 0; r < nrhs; ++r) {
+      const char* qc = static_cast<const char*>(q) + r * col;
+      char* uc = static_cast<char*>(u) + r * col;
+      const double* qd = reinterpret_cast<const double*>(qc);
+      double* ud = reinterpret_cast<double*>(uc);
+      if (host) {
+        ck(cudaMemcpyAsync(p->io_q, qc, col, cudaMemcpyHostToDevice, st), "H2D q");
+        qd = p->io_q;
+        ud = p->io_u;
+      }
+      p->enqueue_one(qd, ud, st, r == 0);
+      ck(cudaGetLastError(), "kernel launch");
+      if (host) ck(cudaMemcpyAsync(uc, p->io_u, col, cudaMemcpyDeviceToHost, st), "D2H u");
+    }
+    ck(cudaEventRecord(p->ev_b, st), "event");
+    ck(cudaStreamSynchronize(st), "apply");
+    int flag = 0;
+    ck(cudaMemcpy(&flag, p->dp.err_flag, sizeof(int), cudaMemcpyDeviceToHost), "flag");
+    if (stats) {
+      stats->n_ifo_pairs = p->hp.n_ifo;
+      stats->n_ifs_pairs = p->hp.n_ifs;
+      stats->n_tfo_pairs = p->hp.n_tfo;
+      stats->n_level1_pairs = p->hp.n_l1;
+      stats->direct_fallback = p->hp.depth < 2 ? 1 : 0;
+      if (p->hp.depth < 2) {
+        stats->n_ifo_pairs = stats->n_ifs_pairs = stats->n_tfo_pairs = stats->n_level1_pairs = 0;
+      }
+      cudaEventElapsedTime(&stats->ms_total, p->ev_a, p->ev_b);
+      stats->ms_translate = 0;
+      if (p->hp.depth >= 2) cudaEventElapsedTime(&stats->ms_translate, p->ev_k2a, p->ev_k2b);
+    }
+    if (flag) {
+      ck(cudaMemset(p->dp.err_flag, 0, sizeof(int)), "memset");
+      return set_error(SFMM_EDUPLICATE, "fmm_apply: coincident points with distinct indices");
+    }
+    return SFMM_OK;
+  } catch (const CudaFail& f) {
+    return set_error(f.code, "fmm_apply: " + f.msg);
+  }
+}
+
+int sfmm_gpu_apply_async(sfmm_gpu_plan* p, const void* q_dev, void* u_dev, int nrhs,
+                         void* stream) {
+  if (!p || nrhs < 1) return set_error(SFMM_EINVAL, "fmm_apply: bad arguments");
+  std::lock_guard<std::mutex> lock(p->mu);
+  try {
+    ck(cudaSetDevice(p->device), "cudaSetDevice");
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : p->stream;
+    const size_t col = (size_t)p->hp.n_points * p->scalar_bytes();
+    for (int r = 0; r < nrhs; ++r) {
+      const double* qd = reinterpret_cast<const double*>(static_cast<const char*>(q_dev) + r * col);
+      double* ud = reinterpret_cast<double*>(static_cast<char*>(u_dev) + r * col);
+      p->enqueue_one(qd, ud, st, false);
+    }
+    ck(cudaGetLastError(), "kernel launch");
+    return SFMM_OK;
+  } catch (const CudaFail& f) {
+    return set_error(f.code, "fmm_apply: " + f.msg);
+  }
+}
+
+int sfmm_gpu_check_status(sfmm_gpu_plan* p) {
+  if (!p) return set_error(SFMM_EINVAL, "null plan");
+  std::lock_guard<std::mutex> lock(p->mu);
+  try {
+    ck(cudaSetDevice(p->device), "cudaSetDevice");
+    ck(cudaDeviceSynchronize(), "sync");
+    int flag = 0;
+    ck(cudaMemcpy(&flag, p->dp.err_flag, sizeof(int), cudaMemcpyDeviceToHost), "flag");
+    if (flag) {
+      ck(cudaMemset(p->dp.err_flag, 0, sizeof(int)), "memset");
+      return set_error(SFMM_EDUPLICATE, "fmm_apply: coincident points with distinct indices");
+    }
+    return SFMM_OK;
+  } catch (const CudaFail& f) {
+    return set_error(f.code, f.msg);
+  }
+}
+
+int sfmm_gpu_plan_info_get(const sfmm_gpu_plan* p, sfmm_gpu_plan_info* info) {
+  if (!p || !info) return set_error(SFMM_EINVAL, "null argument");
+  const HostPlan& hp = p->hp;
+  info->n_points = hp.n_points;
+  info->n_boxes = hp.n_boxes;
+  info->depth = hp.depth;
+  info->n_slots = hp.n_slots;
+  info->n_skel = hp.n_skel;
+  info->m_proj = hp.m_proj;
+  info->p_dense = hp.p_dense;
+  info->p_skel = hp.p_skel;
+  info->n_tasks = p->dp.n_tasks;
+  info->device_bytes = p->device_bytes;
+  info->n_ifo_pairs = hp.n_ifo;
+  info->n_ifs_pairs = hp.n_ifs;
+  info->n_tfo_pairs = hp.n_tfo;
+  info->n_level1_pairs = hp.n_l1;
+  return SFMM_OK;
+}
+
+void sfmm_gpu_plan_destroy(sfmm_gpu_plan* p) { delete p; }
+
+int sfmm_gpu_direct_sum(int kernel, double kappa, int dim, int64_t n, const double* pts,
+                        const void* q, int64_t n_targets, const int32_t* targets, void* u,
+                        int device) {
+  if (kernel == SFMM_HELMHOLTZ2D)
+    return set_error(SFMM_EUNSUPPORTED, "direct_sum_subset: helmholtz2d has no device path");
+  if (n < 1 || !pts || !q || !u || n_targets < 0)
+    return set_error(SFMM_EINVAL, "direct_sum_subset: bad arguments");
+  for (int64_t t = 0; t < n_targets; ++t)
+    if (targets[t] < 0 || targets[t] >= n)
+      return set_error(SFMM_EINVAL, "direct_sum_subset: target index out of range");
+  const size_t sb = kernel == SFMM_HELMHOLTZ3D ? 16 : 8;
+  void *dp = nullptr, *dq = nullptr, *du = nullptr, *dt = nullptr, *de = nullptr;
+  int rc = SFMM_OK;
+  try {
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    ck(cudaMalloc(&dp, n * dim * sizeof(double)), "cudaMalloc");
+    ck(cudaMalloc(&dq, n * sb), "cudaMalloc");
+    ck(cudaMalloc(&du, std::max<int64_t>(n_targets, 1) * sb), "cudaMalloc");
+    ck(cudaMalloc(&dt, std::max<int64_t>(n_targets, 1) * sizeof(int32_t)), "cudaMalloc");
+    ck(cudaMalloc(&de, sizeof(int)), "cudaMalloc");
+    ck(cudaMemset(de, 0, sizeof(int)), "memset");
+    ck(cudaMemcpy(dp, pts, n * dim * sizeof(double), cudaMemcpyHostToDevice), "H2D");
+    ck(cudaMemcpy(dq, q, n * sb, cudaMemcpyHostToDevice), "H2D");
+    ck(cudaMemcpy(dt, targets, n_targets * sizeof(int32_t), cudaMemcpyHostToDevice), "H2D");
+    launch_direct_subset(kernel, kappa, dim, n, (const double*)dp, (const double*)dq, n_targets,
+                         (const int32_t*)dt, (double*)du, (int*)de, 0);
+    ck(cudaGetLastError(), "launch");
+    ck(cudaMemcpy(u, du, n_targets * sb, cudaMemcpyDeviceToHost), "D2H");
+    int flag = 0;
+    ck(cudaMemcpy(&flag, de, sizeof(int), cudaMemcpyDeviceToHost), "flag");
+    if (flag)
+      rc = set_error(SFMM_EDUPLICATE, "direct_sum_subset: coincident points with distinct indices");
+  } catch (const CudaFail& f) {
+    rc = set_error(f.code, "direct_sum_subset: " + f.msg);
+  }
+  cudaFree(dp);
+  cudaFree(dq);
+  cudaFree(du);
+  cudaFree(dt);
+  cudaFree(de);
+  return rc;
+}
+
+}  // extern "C"
