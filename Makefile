@@ -13,12 +13,32 @@ NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -I$(SRC)
             --expt-relaxed-constexpr -Xptxas -v
 CXXFLAGS := -std=c++17 -O2 -fPIC -Iinclude -I$(SRC) -I/usr/local/cuda/include
 
-GPU_CU   := $(SRC)/kernels_translate.cu $(SRC)/kernels_tree.cu $(SRC)/sfmm_gpu.cu
+GPU_CU   := $(SRC)/kernels_translate.cu $(SRC)/kernels_tree.cu $(SRC)/kernels_probe.cu \
+            $(SRC)/sfmm_gpu.cu
 GPU_OBJS := $(patsubst $(SRC)/%.cu,$(OBJ)/%.o,$(GPU_CU)) $(OBJ)/plan_build.o
 HDRS     := include/sfmm_gpu.h $(SRC)/common.cuh $(SRC)/launch.h $(SRC)/plan_build.h
 
-.PHONY: all gpu oracle clean
-all: gpu
+.PHONY: all gpu host oracle clean
+all: gpu host
+
+HOST_SRC  := $(SRC)/host
+HOST_CPP  := $(HOST_SRC)/tree.cpp $(HOST_SRC)/skeleton.cpp $(HOST_SRC)/host_api.cpp
+HOST_OBJS := $(patsubst $(HOST_SRC)/%.cpp,$(OBJ)/host_%.o,$(HOST_CPP))
+HOSTFLAGS := -std=c++17 -O3 -march=x86-64-v3 -fopenmp -fPIC -Iinclude -I$(HOST_SRC) \
+             -fno-math-errno -fcx-limited-range -ffp-contract=off
+# skeletons need not be bit-identical to the reference (pivots are compared by
+# accuracy), so only they may use FMA contraction
+$(OBJ)/host_skeleton.o: HOSTFLAGS += -ffp-contract=fast
+
+host: $(LIB)/libsfmm_host.so
+
+$(OBJ)/host_%.o: $(HOST_SRC)/%.cpp $(HOST_SRC)/host.h include/sfmm_host.h include/sfmm_gpu.h
+	@mkdir -p $(OBJ)
+	$(CXX) $(HOSTFLAGS) -c $< -o $@
+
+$(LIB)/libsfmm_host.so: $(HOST_OBJS)
+	@mkdir -p $(LIB)
+	$(CXX) -shared -fopenmp $^ -o $@
 
 gpu: $(LIB)/libsfmm_gpu.so
 

@@ -1,0 +1,372 @@
+#!/usr/bin/env python
+"""SRS-FMM apply benchmark on B200 (one process per GPU).
+
+Workload (BASELINE.json metric): 3D Laplace, uniform unit cube, N = 1e7,
+leaf capacity 128, tolerance 1e-6, one right-hand side, synthetic inputs from
+the reference generators (points seed 1, charges seed 1 ^ 0x9e3779b97f4a7c15).
+A "step" is one apply u = A q (the reference's sfmm::fmm_apply,
+/root/reference/proj/src/apply.cpp:306-337) over the resident plan.
+
+  value   device-resident throughput: N / (device time of one apply), q and u
+          already in HBM, timed with CUDA events over K applies.
+  e2e     the same through the public host-buffer API (pinned q in, u out,
+          H2D + D2H inside every step).
+  roofline  the fused translation kernel K2 (FP64-pipe bound): algorithmic
+          flop per launch (20 per dense pair + 2 per skeleton
+          pair) / its CUDA-event duration, against the DFMA peak measured in
+          this run.
+  cpu_baseline  the unmodified reference fmm_apply (oracle/_ref) on the SAME
+          plan and charges, all host cores, one apply; it also yields the
+          relative l2 deviation of the GPU result from the CPU reference.
+
+``--impl reference`` times the reference CPU apply alone (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SRS-FMM apply Mpoints/s (3D Laplace N=1e7) & rel. err vs CPU ref at 1/2/4/8 GPU"
+UNIT = "Mpoints/s"
+CHARGE_STREAM = 0x9E3779B97F4A7C15
+KERNELS = {"laplace2d": 0, "laplace3d": 1, "helmholtz3d": 3}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=float, default=1e7)
+    ap.add_argument("--dist", default="cube")
+    ap.add_argument("--kernel", default="laplace3d", choices=list(KERNELS))
+    ap.add_argument("--kappa", type=float, default=10.0)
+    ap.add_argument("--leaf", type=int, default=128)
+    ap.add_argument("--tol", type=float, default=1e-6)
+    ap.add_argument("--check-targets", type=int, default=1000)
+    ap.add_argument("--cpu", default="full", choices=["full", "sample", "off"],
+                    help="cpu_baseline: reference apply on the full plan, on the N=1e6 "
+                         "instance, or skipped")
+    ap.add_argument("--ref-n", type=float, default=1e6,
+                    help="instance size of one --impl reference step / the 'sample' cpu baseline")
+    return ap.parse_args()
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, mx, pw, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+                pw.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "samples": len(sm),
+                "power_w_max": max(pw), "reasons": sorted(reasons)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def emit(obj):
+    print(json.dumps(obj), flush=True)
+
+
+def run_reference(args, ws, rank):
+    """--impl reference: the unmodified reference CPU apply, rank 0 only."""
+    if rank != 0:
+        return
+    from oracle import pyoracle as po
+    n = int(args.ref_n)
+    kern = KERNELS[args.kernel]
+    pts = po.generate_points(args.dist, n, 1)
+    t0 = time.perf_counter()
+    rp = po.RefPipeline.build(kern, pts, args.leaf, args.tol, args.kappa)
+    t_pre = time.perf_counter() - t0
+    cplx = kern == 3
+    q = (po.generate_charges_complex(n, 1 ^ CHARGE_STREAM) if cplx
+         else po.generate_charges(n, 1 ^ CHARGE_STREAM))
+    for _ in range(args.warmup):
+        rp.apply(q, cplx)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        rp.apply(q, cplx)
+        times.append(time.perf_counter() - t0)
+    t = statistics.median(times)
+    value = n / t / 1e6
+    threads = po.ref_lib().ref_num_threads()
+    sample = (f"reference fmm_apply (oracle/_ref, unmodified sources, -O3 OpenMP) on the "
+              f"N={n:.0e} instance of the same workload ({args.dist}, leaf {args.leaf}, tol "
+              f"{args.tol}); one apply per step, median of {args.steps}")
+    emit({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference generators, seed 1)",
+        "config": {"workload": f"{args.kernel} {args.dist} N={n:.0e} leaf={args.leaf} "
+                               f"tol={args.tol} nrhs=1", "headline_n": int(args.n)},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "precompute_s": t_pre,
+    })
+
+
+def main():
+    args = parse()
+    ws, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        return
+
+    import torch
+    from paper_2310_16668_b200 import api, host
+
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = local
+
+    n = int(args.n)
+    kern = KERNELS[args.kernel]
+    cplx = kern == 3
+    t0 = time.perf_counter()
+    pts = host.generate_points(args.dist, n, 1)
+    q = (host.generate_charges_complex(n, 1 ^ CHARGE_STREAM) if cplx
+         else host.generate_charges(n, 1 ^ CHARGE_STREAM))
+    t_gen = time.perf_counter() - t0
+    hp = host.HostPlan.build(kern, pts, args.leaf, args.tol, args.kappa)
+    hinfo = hp.info()
+    t0 = time.perf_counter()
+    plan = api.GpuPlan(hp.desc_struct(), device=dev)
+    t_upload = time.perf_counter() - t0
+    info = plan.info()
+
+    fp64_peak = api.fp64_peak_tflops(dev)
+
+    dtype = torch.complex128 if cplx else torch.float64
+    q_host = torch.from_numpy(q)
+    q_dev = q_host.to(f"cuda:{dev}")
+    u_dev = torch.empty_like(q_dev)
+    # a dedicated stream: the applies and the timing events share it
+    stream = torch.cuda.Stream(dev)
+    sp = stream.cuda_stream
+    torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        api.fmm_apply_device(plan, q_dev.data_ptr(), u_dev.data_ptr(), 1, sp)
+    api.check_status(plan)
+
+    # ---- timed region: K device-resident applies -------------------------
+    api.set_timing(plan, True)
+    clocks = ClockSampler(dev)
+    clocks.start()
+    time.sleep(0.2)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        api.fmm_apply_device(plan, q_dev.data_ptr(), u_dev.data_ptr(), 1, sp)
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    clk = clocks.stop()
+    api.check_status(plan)
+    ms_step = ev0.elapsed_time(ev1) / args.steps
+    phases = api.get_timings(plan)
+    api.set_timing(plan, False)
+    if dist:
+        tt = torch.tensor([ms_step], device=f"cuda:{dev}", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms_step = float(tt.item())
+    value = ws * n / (ms_step * 1e-3) / 1e6  # replicas: every rank applies its own plan
+
+    u_gpu = u_dev.cpu().numpy()
+
+    # ---- e2e: public host-buffer API, pinned q in / u out each step -------
+    q_pin = torch.empty(q_host.shape, dtype=dtype).pin_memory()
+    q_pin.copy_(q_host)
+    u_pin = torch.empty(q_host.shape, dtype=dtype).pin_memory()
+    e2e_steps = max(3, min(args.steps, 10))
+    api.fmm_apply(plan, q_pin.numpy(), out=u_pin.numpy())
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        u_e2e = api.fmm_apply(plan, q_pin.numpy(), out=u_pin.numpy())
+    t_e2e = (time.perf_counter() - t0) / e2e_steps
+    e2e_value = ws * n / t_e2e / 1e6
+    bytes_col = n * (16 if cplx else 8)
+
+    # ---- accuracy vs the dense sum on sampled targets (GPU direct sum) ----
+    rng = np.random.default_rng(0xC2B2AE3D27D4EB4F)
+    targets = np.sort(rng.choice(n, size=min(args.check_targets, n), replace=False)).astype(np.int32)
+    ref_t = api.direct_sum_subset(kern, args.kappa, pts, q, targets, device=dev)
+    relerr_direct = api.max_rel_err(u_gpu[targets], ref_t)
+    e2e_same = bool(np.array_equal(u_e2e, u_gpu))
+
+    # ---- roofline of the dominant kernel (K2, FP64 pipe) -------------------
+    k2_ms = float(np.mean(phases[:, 2])) if len(phases) else float("nan")
+    w_k2 = 20.0 * info.p_dense + 2.0 * info.p_skel
+    achieved = w_k2 / (k2_ms * 1e-3) / 1e12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "k2_traffic.json")
+    if os.path.exists(prof):
+        try:
+            pj = json.load(open(prof))
+            key = f"{args.kernel}_{args.dist}_{n}_{args.leaf}_{args.tol}"
+            traffic = pj.get(key)
+        except (OSError, ValueError):
+            traffic = None
+    phase_ms = {nm: float(np.mean(phases[:, i])) for i, nm in enumerate(api.PHASES)} if len(phases) else {}
+    # interpolation GEMVs: each reads T once per apply
+    sb = 16 if cplx else 8
+    t_bytes = info.m_proj * sb
+    gemv_gbs = {
+        "upward": t_bytes / (phase_ms.get("upward", float("nan")) * 1e-3) / 1e9,
+        "downward": t_bytes / (phase_ms.get("downward", float("nan")) * 1e-3) / 1e9,
+    }
+
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference generators: points seed 1, charges seed 1^0x9e3779b97f4a7c15)",
+        "config": {
+            "workload": f"{args.kernel} {args.dist} N={n:.0e} leaf={args.leaf} tol={args.tol} nrhs=1",
+            "n_points": n, "leaf_cap": args.leaf, "tol": args.tol, "nrhs": 1,
+            "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
+            "l2": "inputs larger than L2 (resident plan %.1f GB vs 126 MB L2)" % (info.device_bytes / 1e9),
+        },
+        "roofline": {
+            "bound": "fp64", "kernel": "k2_translate (fused ifo/ifs/tfo/level-1)",
+            "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+            "frac": achieved / fp64_peak if fp64_peak > 0 else None,
+            "traffic": traffic,
+            "peak_source": "DFMA loop measured in this run (MEASURED_PEAKS.json has no FP64 figure); nominal 37.2",
+            "work": "20 flop per dense pair + 2 per skeleton pair (SURVEY.md 8d)",
+            "p_dense": info.p_dense, "p_skel": info.p_skel, "k2_ms": k2_ms,
+        },
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": bytes_col,
+                "d2h_bytes_per_step": bytes_col, "ms_per_step": t_e2e * 1e3,
+                "matches_device_result": e2e_same},
+        "gpu_launches": int(info.launches_per_apply) * args.steps,
+        "clocks": clk,
+        "phase_ms": phase_ms,
+        "gemv_gbs": gemv_gbs,
+        "relerr_vs_direct": relerr_direct, "n_check": int(targets.size),
+        "precompute": {"t_generate_s": t_gen, "t_tree_s": hinfo["t_tree"],
+                       "t_skel_s": hinfo["t_skel"], "t_upload_s": t_upload,
+                       "depth": hinfo["depth"], "n_boxes": hinfo["n_boxes"],
+                       "k_max": hinfo["k_max"], "m_proj": hinfo["proj_scalars"],
+                       "host_threads": host.get_threads()},
+    }
+
+    # ---- CPU baseline: the unmodified reference apply on the same plan ----
+    if rank == 0 and ws == 1 and args.cpu != "off":
+        try:
+            from oracle import pyoracle as po
+            if args.cpu == "full":
+                rp = po.RefPipeline.from_desc(hp.desc_struct())
+                t0 = time.perf_counter()
+                u_ref, _ = rp.apply(q, cplx)
+                t_cpu = time.perf_counter() - t0
+                rp.close()
+                out["relerr_vs_cpu_ref"] = po.rel_l2(u_gpu, u_ref)
+                out["max_relerr_vs_cpu_ref"] = api.max_rel_err(u_gpu, u_ref)
+                n_cpu = n
+                sample = (f"full headline workload (N={n:.0e}), one reference fmm_apply on the "
+                          "same tree/skeletons/charges as the GPU run")
+            else:
+                n_cpu = int(args.ref_n)
+                p2 = host.generate_points(args.dist, n_cpu, 1)
+                q2 = host.generate_charges(n_cpu, 1 ^ CHARGE_STREAM)
+                rp = po.RefPipeline.build(kern, p2, args.leaf, args.tol, args.kappa)
+                t0 = time.perf_counter()
+                rp.apply(q2, cplx)
+                t_cpu = time.perf_counter() - t0
+                sample = f"N={n_cpu:.0e} instance of the same workload, one reference fmm_apply"
+            out["cpu_baseline"] = {
+                "value": n_cpu / t_cpu / 1e6, "unit": UNIT,
+                "cores": po.ref_lib().ref_num_threads(), "kind": "reference",
+                "sample": sample, "seconds": t_cpu}
+        except Exception as e:  # the checker may be absent; never the product
+            out["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": None,
+                                   "kind": "reference", "sample": f"unavailable: {e}"}
+    if rank == 0:
+        emit(out)
+    plan.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -124,6 +124,8 @@ typedef struct sfmm_gpu_plan_info {
   int64_t n_tasks;          /* K2 work items */
   int64_t device_bytes;     /* resident plan bytes */
   int64_t n_ifo_pairs, n_ifs_pairs, n_tfo_pairs, n_level1_pairs;
+  int32_t launches_per_apply; /* kernels of this library launched by one single-RHS apply */
+  int32_t k2_grid;            /* persistent CTAs of the translation kernel */
 } sfmm_gpu_plan_info;
 
 typedef struct sfmm_gpu_plan sfmm_gpu_plan;
@@ -153,6 +155,17 @@ int sfmm_gpu_check_status(sfmm_gpu_plan* plan);
 int sfmm_gpu_plan_info_get(const sfmm_gpu_plan* plan, sfmm_gpu_plan_info* info);
 
 void sfmm_gpu_plan_destroy(sfmm_gpu_plan* plan);
+
+/* Phase timing.  While enabled, every apply records CUDA events on its stream
+ * around its five phases (0 gather, 1 upward, 2 translate, 3 downward,
+ * 4 scatter).  sfmm_gpu_get_timings synchronises, writes ms[5*i + phase] for
+ * up to max_applies recorded applies, sets *n_applies and clears the record. */
+int sfmm_gpu_set_timing(sfmm_gpu_plan* plan, int enable);
+int sfmm_gpu_get_timings(sfmm_gpu_plan* plan, float* ms, int max_applies, int* n_applies);
+
+/* Measured FP64 FMA throughput of the device (TFLOP/s, 2 flop per DFMA), from
+ * a register-resident DFMA loop run on every SM for ~50 ms. */
+int sfmm_gpu_fp64_peak(int device, double* tflops);
 
 /* Dense u_i = sum_{j != i} G(x_i, x_j) q_j over the points in their given
  * order, for the listed targets only (oracle.cpp:51-71), on the device.

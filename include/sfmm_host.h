@@ -1,0 +1,86 @@
+/*
+ * sfmm_host.h -- C ABI of the host-side precompute that feeds the GPU apply.
+ *
+ * The reference keeps tree construction, neighbor lists and skeletonization on
+ * the host (north star: they "stay as they are").  This library is this
+ * repository's own C++/OpenMP implementation of those callers of the apply:
+ *   sfmm::build_tree            /root/reference/proj/src/tree.cpp:148-304
+ *   sfmm::build_neighbor_lists  /root/reference/proj/src/tree.cpp:306-355
+ *   sfmm::build_skeletons       /root/reference/proj/src/skeleton.cpp:184-260
+ *   sfmm::generate_points / generate_charges(_complex)
+ *                               /root/reference/proj/src/bench.cpp:102-161
+ * Trees (perm, box order, ranges, neighbor lists) are bit-identical to the
+ * reference's; skeletons satisfy the same ID criterion (pivot choices are
+ * rounding-sensitive, so they are compared by accuracy, not bits).
+ * The result is exported as the sfmm_plan_desc of include/sfmm_gpu.h.
+ */
+#ifndef SFMM_HOST_H_
+#define SFMM_HOST_H_
+
+#include <stdint.h>
+
+#include "sfmm_gpu.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Return codes beyond sfmm_gpu.h's: */
+enum { SFMM_EDEPTH = 7 /* sfmm::DepthExceededError */ };
+
+/* Distributions, same order as sfmm::Distribution (bench.hpp:15). */
+enum { SFMM_DIST_SQUARE = 0, SFMM_DIST_ANNULUS = 1, SFMM_DIST_CUBE = 2, SFMM_DIST_SPHERE = 3 };
+
+/* sfmm::ProxyConfig (skeleton.hpp:13-17); zero fields take the defaults
+ * 2.95 / 24 / 8. */
+typedef struct sfmm_proxy_config {
+  double radius_factor;
+  int32_t edge_points_2d;
+  int32_t face_grid_3d;
+} sfmm_proxy_config;
+
+typedef struct sfmm_host_info {
+  int32_t depth;
+  int32_t n_boxes;
+  int64_t n_leaves;
+  int32_t k_max;
+  int32_t saturated_boxes;
+  int64_t proj_scalars;     /* SkeletonSet::proj_scalars */
+  double t_tree;            /* seconds: build_tree + build_neighbor_lists */
+  double t_skel;            /* seconds: build_skeletons */
+} sfmm_host_info;
+
+typedef struct sfmm_host_plan sfmm_host_plan;
+
+int sfmm_host_generate_points(int dist, int64_t n, uint64_t seed, double* out);
+int sfmm_host_generate_charges(int64_t n, uint64_t seed, double* out);
+int sfmm_host_generate_charges_complex(int64_t n, uint64_t seed, double* out);
+
+/* Tree + neighbor lists only (skeleton fields of the descriptor stay empty,
+ * T absent).  pts: n*dim interleaved, original order. */
+int sfmm_host_build_tree(int dim, int64_t n, const double* pts, int leaf_cap,
+                         sfmm_host_plan** out);
+
+/* Full precompute: tree, neighbor lists, skeletons (build_skeletons). */
+int sfmm_host_build(int kernel, double kappa, int dim, int64_t n, const double* pts,
+                    int leaf_cap, double tol, const sfmm_proxy_config* proxy,
+                    sfmm_host_plan** out);
+
+/* Flat view of the plan; valid until sfmm_host_destroy. */
+const sfmm_plan_desc* sfmm_host_desc(sfmm_host_plan* plan);
+
+int sfmm_host_info_get(const sfmm_host_plan* plan, sfmm_host_info* info);
+
+void sfmm_host_destroy(sfmm_host_plan* plan);
+
+/* Number of OpenMP threads the precompute uses (0 keeps the default). */
+void sfmm_host_set_threads(int n);
+int sfmm_host_get_threads(void);
+
+const char* sfmm_host_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SFMM_HOST_H_ */

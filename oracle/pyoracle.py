@@ -138,9 +138,11 @@ class RefPipeline:
         return cls(h)
 
     @classmethod
-    def from_desc(cls, desc: PlanDescriptor):
+    def from_desc(cls, desc):
+        """desc: PlanDescriptor or a ctypes PlanDesc (zero-copy view)."""
+        st = desc.struct if isinstance(desc, PlanDescriptor) else desc
         h = C.c_void_p()
-        _check(ref_lib().ref_from_desc(C.byref(desc.struct), C.byref(h)))
+        _check(ref_lib().ref_from_desc(C.byref(st), C.byref(h)))
         return cls(h)
 
     def descriptor(self) -> PlanDescriptor:

@@ -93,6 +93,8 @@ class PlanInfo(C.Structure):
         ("n_ifs_pairs", C.c_int64),
         ("n_tfo_pairs", C.c_int64),
         ("n_level1_pairs", C.c_int64),
+        ("launches_per_apply", C.c_int32),
+        ("k2_grid", C.c_int32),
     ]
 
 
@@ -260,6 +262,12 @@ def gpu_lib() -> C.CDLL:
     lib.sfmm_gpu_last_error.restype = C.c_char_p
     lib.sfmm_gpu_version.argtypes = []
     lib.sfmm_gpu_version.restype = C.c_char_p
+    lib.sfmm_gpu_set_timing.argtypes = [vp, C.c_int]
+    lib.sfmm_gpu_set_timing.restype = C.c_int
+    lib.sfmm_gpu_get_timings.argtypes = [vp, vp, C.c_int, C.POINTER(C.c_int)]
+    lib.sfmm_gpu_get_timings.restype = C.c_int
+    lib.sfmm_gpu_fp64_peak.argtypes = [C.c_int, C.POINTER(C.c_double)]
+    lib.sfmm_gpu_fp64_peak.restype = C.c_int
     _gpu_lib = lib
     return lib
 
@@ -267,5 +275,6 @@ def gpu_lib() -> C.CDLL:
 GPU_SYMBOLS = [
     "sfmm_gpu_plan_create", "sfmm_gpu_apply", "sfmm_gpu_apply_async", "sfmm_gpu_check_status",
     "sfmm_gpu_plan_info_get", "sfmm_gpu_plan_destroy", "sfmm_gpu_direct_sum",
-    "sfmm_gpu_last_error", "sfmm_gpu_version",
+    "sfmm_gpu_last_error", "sfmm_gpu_version", "sfmm_gpu_set_timing", "sfmm_gpu_get_timings",
+    "sfmm_gpu_fp64_peak",
 ]

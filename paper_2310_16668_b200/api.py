@@ -62,16 +62,24 @@ def _raise(rc: int) -> None:
 class GpuPlan:
     """Device-resident apply plan (operators uploaded once, resident in HBM)."""
 
-    def __init__(self, desc: PlanDescriptor, device: int = 0):
+    def __init__(self, desc, device: int = 0):
+        """desc: a PlanDescriptor, or a ctypes PlanDesc (e.g. straight from the
+        host precompute, without copying its arrays)."""
         lib = _abi.gpu_lib()
-        self.desc = desc
         self.device = device
+        self._h = None
+        if isinstance(desc, PlanDescriptor):
+            st = desc.struct
+        elif isinstance(desc, _abi.PlanDesc):
+            st = desc
+        else:
+            raise TypeError("GpuPlan: expected a PlanDescriptor or a PlanDesc")
         h = C.c_void_p()
-        _raise(lib.sfmm_gpu_plan_create(C.byref(desc.struct), device, C.byref(h)))
+        _raise(lib.sfmm_gpu_plan_create(C.byref(st), device, C.byref(h)))
         self._h = h
-        self.kernel = desc.kernel
-        self.n_points = desc.n_points
-        self.is_complex = desc.is_complex
+        self.kernel = int(st.kernel)
+        self.n_points = int(st.n_points)
+        self.is_complex = self.kernel in (_abi.HELMHOLTZ2D, _abi.HELMHOLTZ3D)
         self.dtype = np.complex128 if self.is_complex else np.float64
 
     @property
@@ -103,10 +111,12 @@ class GpuPlan:
         self.close()
 
 
-def fmm_apply(plan: GpuPlan, q, stats: ApplyStats | None = None) -> np.ndarray:
+def fmm_apply(plan: GpuPlan, q, stats: ApplyStats | None = None,
+              out: np.ndarray | None = None) -> np.ndarray:
     """u = A q (apply.cpp:306-337) on the GPU; q, u in original point order.
 
     q has shape (N,) or (N, nrhs); each column is an independent right-hand side.
+    `out` (optional, e.g. a pinned buffer) receives u.
     """
     q = np.asarray(q)
     one = q.ndim == 1
@@ -114,7 +124,13 @@ def fmm_apply(plan: GpuPlan, q, stats: ApplyStats | None = None) -> np.ndarray:
         raise ValueError("fmm_apply: charge count does not match the point count")
     qc = np.asfortranarray(q.reshape(plan.n_points, -1), dtype=plan.dtype)
     nrhs = qc.shape[1]
-    u = np.empty((plan.n_points, nrhs), dtype=plan.dtype, order="F")
+    if out is not None:
+        if out.dtype != plan.dtype or out.size != qc.size or not (
+                out.flags.f_contiguous or out.ndim == 1):
+            raise ValueError("fmm_apply: out buffer has the wrong shape or dtype")
+        u = out.reshape(plan.n_points, nrhs, order="F")
+    else:
+        u = np.empty((plan.n_points, nrhs), dtype=plan.dtype, order="F")
     st = _abi.GpuStats()
     _raise(_abi.gpu_lib().sfmm_gpu_apply(plan.handle, qc.ctypes.data, u.ctypes.data, nrhs,
                                          _abi.SFMM_HOST_BUFFERS, C.byref(st)))
@@ -133,6 +149,29 @@ def fmm_apply_device(plan: GpuPlan, q_ptr: int, u_ptr: int, nrhs: int = 1, strea
     """Enqueues u = A q on device buffers (raw pointers) on `stream`; no sync."""
     _raise(_abi.gpu_lib().sfmm_gpu_apply_async(plan.handle, C.c_void_p(q_ptr), C.c_void_p(u_ptr),
                                                nrhs, C.c_void_p(stream or None)))
+
+
+PHASES = ("gather", "upward", "translate", "downward", "scatter")
+
+
+def set_timing(plan: GpuPlan, enable: bool = True) -> None:
+    """Record per-phase CUDA events in every subsequent apply."""
+    _raise(_abi.gpu_lib().sfmm_gpu_set_timing(plan.handle, int(enable)))
+
+
+def get_timings(plan: GpuPlan, max_applies: int = 256) -> np.ndarray:
+    """(n_applies, 5) device ms per phase of the applies recorded since set_timing."""
+    ms = np.zeros((max_applies, 5), dtype=np.float32)
+    n = C.c_int(0)
+    _raise(_abi.gpu_lib().sfmm_gpu_get_timings(plan.handle, ms.ctypes.data, max_applies, C.byref(n)))
+    return ms[: n.value].copy()
+
+
+def fp64_peak_tflops(device: int = 0) -> float:
+    """Measured DFMA throughput of the device (TFLOP/s)."""
+    v = C.c_double(0)
+    _raise(_abi.gpu_lib().sfmm_gpu_fp64_peak(device, C.byref(v)))
+    return v.value
 
 
 def check_status(plan: GpuPlan) -> None:

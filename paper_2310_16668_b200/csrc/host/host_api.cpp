@@ -1,0 +1,272 @@
+// C ABI of the host precompute (include/sfmm_host.h) and the synthetic-input
+// generators.
+#include <omp.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <random>
+#include <string>
+
+#include "host.h"
+#include "sfmm_host.h"
+
+namespace sfmm_host {
+namespace {
+
+constexpr double kPi = 3.14159265358979323846264338327950288;
+
+// Bit-to-double maps of the reference bench (bench.cpp:30-35).
+inline double unit01(std::mt19937_64& g) { return static_cast<double>(g() >> 11) * 0x1.0p-53; }
+inline double unit01_pos(std::mt19937_64& g) {
+  return static_cast<double>((g() >> 11) + 1) * 0x1.0p-53;
+}
+
+// Box-Muller pairs (bench.cpp:37-45).
+void normals(std::mt19937_64& g, double* out, int64_t n) {
+  for (int64_t i = 0; i < n; i += 2) {
+    const double u1 = unit01_pos(g);
+    const double u2 = unit01(g);
+    const double rad = std::sqrt(-2.0 * std::log(u1));
+    out[i] = rad * std::cos(2.0 * kPi * u2);
+    if (i + 1 < n) out[i + 1] = rad * std::sin(2.0 * kPi * u2);
+  }
+}
+
+}  // namespace
+
+void generate_points(int dist, int64_t n, uint64_t seed, double* out) {
+  if (n < 1) throw std::invalid_argument("generate_points: need at least one point");
+  std::mt19937_64 g(seed);
+  switch (dist) {
+    case SFMM_DIST_SQUARE:
+      for (int64_t i = 0; i < n; ++i) {
+        out[2 * i] = unit01(g);
+        out[2 * i + 1] = unit01(g);
+      }
+      break;
+    case SFMM_DIST_ANNULUS:
+      for (int64_t i = 0; i < n; ++i) {
+        const double theta = 2.0 * kPi * unit01(g);
+        const double eta = (unit01(g) - 0.5) * 0.1;
+        const double r = 1.0 + 0.25 * std::cos(5.0 * theta) + eta;
+        out[2 * i] = r * std::cos(theta);
+        out[2 * i + 1] = r * std::sin(theta);
+      }
+      break;
+    case SFMM_DIST_CUBE:
+      for (int64_t i = 0; i < n; ++i) {
+        out[3 * i] = unit01(g);
+        out[3 * i + 1] = unit01(g);
+        out[3 * i + 2] = unit01(g);
+      }
+      break;
+    case SFMM_DIST_SPHERE:
+      for (int64_t i = 0; i < n; ++i) {
+        const double z = 2.0 * unit01(g) - 1.0;
+        const double phi = 2.0 * kPi * unit01(g);
+        const double s = std::sqrt(1.0 - z * z);
+        out[3 * i] = s * std::cos(phi);
+        out[3 * i + 1] = s * std::sin(phi);
+        out[3 * i + 2] = z;
+      }
+      break;
+    default:
+      throw std::invalid_argument("generate_points: unknown distribution");
+  }
+}
+
+void generate_charges(int64_t n, uint64_t seed, double* out) {
+  std::mt19937_64 g(seed);
+  normals(g, out, n);
+}
+
+void generate_charges_complex(int64_t n, uint64_t seed, double* out) {
+  std::mt19937_64 g(seed);
+  normals(g, out, 2 * n);  // (re, im) interleaved = std::complex layout
+}
+
+}  // namespace sfmm_host
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* what) {
+  g_err = what;
+  return code;
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return SFMM_OK;
+  } catch (const sfmm_host::DuplicatePoint& e) {
+    return fail(SFMM_EDUPLICATE, e.what());
+  } catch (const sfmm_host::DepthExceeded& e) {
+    return fail(SFMM_EDEPTH, e.what());
+  } catch (const std::invalid_argument& e) {
+    return fail(SFMM_EINVAL, e.what());
+  } catch (const std::logic_error& e) {
+    return fail(SFMM_EUNSUPPORTED, e.what());
+  } catch (const std::bad_alloc&) {
+    return fail(SFMM_ENOMEM, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(SFMM_EINVAL, e.what());
+  }
+}
+
+double now() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+}  // namespace
+
+struct sfmm_host_plan {
+  int kernel = -1;
+  double kappa = 0;
+  sfmm_host::Tree tree;
+  sfmm_host::Neighbors nb;
+  sfmm_host::Skeletons sk;
+  std::vector<int32_t> parent, level, begin, end;
+  std::vector<uint8_t> leaf;
+  sfmm_plan_desc desc{};
+  sfmm_host_info info{};
+
+  void export_desc() {
+    const int32_t n_boxes = (int32_t)tree.boxes.size();
+    parent.resize(n_boxes);
+    level.resize(n_boxes);
+    begin.resize(n_boxes);
+    end.resize(n_boxes);
+    leaf.resize(n_boxes);
+    for (int32_t b = 0; b < n_boxes; ++b) {
+      const auto& x = tree.boxes[b];
+      parent[b] = x.parent;
+      level[b] = x.level;
+      begin[b] = x.begin;
+      end[b] = x.end;
+      leaf[b] = x.leaf ? 1 : 0;
+    }
+    if (sk.iv_off.empty()) {  // tree only: empty skeleton CSR
+      sk.iv_off.assign(n_boxes + 1, 0);
+      sk.sk_off.assign(n_boxes + 1, 0);
+      sk.rd_off.assign(n_boxes + 1, 0);
+      sk.T_off.assign(n_boxes + 1, 0);
+      sk.parent_offset.assign(n_boxes, 0);
+    }
+    sfmm_plan_desc& d = desc;
+    d.kernel = kernel;
+    d.dim = tree.dim;
+    d.kappa = kappa;
+    d.n_points = (int64_t)tree.perm.size();
+    d.n_boxes = n_boxes;
+    d.depth = tree.depth;
+    d.pts = tree.pts.data();
+    d.perm = tree.perm.data();
+    d.level_begin = tree.level_begin.data();
+    d.box_parent = parent.data();
+    d.box_level = level.data();
+    d.box_begin = begin.data();
+    d.box_end = end.data();
+    d.box_leaf = leaf.data();
+    d.box_parent_offset = sk.parent_offset.data();
+    d.iv_off = sk.iv_off.data();
+    d.iv = sk.iv.data();
+    d.sk_off = sk.sk_off.data();
+    d.skel_pos = sk.skel_pos.data();
+    d.rd_off = sk.rd_off.data();
+    d.red_pos = sk.red_pos.data();
+    d.T_off = sk.T_off.data();
+    d.T = sk.T.data();
+    d.coll_off = nb.coll_off.data();
+    d.coll = nb.coll.data();
+    d.coarse_off = nb.coarse_off.data();
+    d.coarse = nb.coarse.data();
+    d.fine_off = nb.fine_off.data();
+    d.fine = nb.fine.data();
+    info.depth = tree.depth;
+    info.n_boxes = n_boxes;
+    info.n_leaves = 0;
+    for (uint8_t l : leaf) info.n_leaves += l;
+    info.k_max = sk.k_max;
+    info.saturated_boxes = sk.saturated;
+    info.proj_scalars = sk.proj_scalars;
+  }
+};
+
+extern "C" {
+
+const char* sfmm_host_last_error(void) { return g_err.c_str(); }
+
+void sfmm_host_set_threads(int n) {
+  if (n > 0) omp_set_num_threads(n);
+}
+int sfmm_host_get_threads(void) { return omp_get_max_threads(); }
+
+int sfmm_host_generate_points(int dist, int64_t n, uint64_t seed, double* out) {
+  return guarded([&] { sfmm_host::generate_points(dist, n, seed, out); });
+}
+int sfmm_host_generate_charges(int64_t n, uint64_t seed, double* out) {
+  return guarded([&] { sfmm_host::generate_charges(n, seed, out); });
+}
+int sfmm_host_generate_charges_complex(int64_t n, uint64_t seed, double* out) {
+  return guarded([&] { sfmm_host::generate_charges_complex(n, seed, out); });
+}
+
+int sfmm_host_build_tree(int dim, int64_t n, const double* pts, int leaf_cap,
+                         sfmm_host_plan** out) {
+  return guarded([&] {
+    auto p = std::make_unique<sfmm_host_plan>();
+    const double t0 = now();
+    p->tree = sfmm_host::build_tree(dim, n, pts, leaf_cap);
+    p->nb = sfmm_host::build_neighbors(p->tree);
+    p->info.t_tree = now() - t0;
+    p->export_desc();
+    *out = p.release();
+  });
+}
+
+int sfmm_host_build(int kernel, double kappa, int dim, int64_t n, const double* pts,
+                    int leaf_cap, double tol, const sfmm_proxy_config* proxy,
+                    sfmm_host_plan** out) {
+  return guarded([&] {
+    if (kernel < 0 || kernel > 3) throw std::invalid_argument("sfmm_host_build: bad kernel id");
+    if (kernel == SFMM_HELMHOLTZ2D)
+      throw std::logic_error("sfmm_host_build: helmholtz2d has no device apply path");
+    if ((kernel == SFMM_HELMHOLTZ3D) && !(kappa > 0))
+      throw std::invalid_argument("sfmm_host_build: wavenumber must be positive");
+    sfmm_host::Proxy px;
+    if (proxy) {
+      if (proxy->radius_factor > 0) px.radius_factor = proxy->radius_factor;
+      if (proxy->edge_points_2d > 0) px.edge_points_2d = proxy->edge_points_2d;
+      if (proxy->face_grid_3d > 0) px.face_grid_3d = proxy->face_grid_3d;
+    }
+    auto p = std::make_unique<sfmm_host_plan>();
+    p->kernel = kernel;
+    p->kappa = kappa;
+    double t0 = now();
+    p->tree = sfmm_host::build_tree(dim, n, pts, leaf_cap);
+    p->nb = sfmm_host::build_neighbors(p->tree);
+    p->info.t_tree = now() - t0;
+    t0 = now();
+    p->sk = sfmm_host::build_skeletons(p->tree, kernel, kappa, tol, px);
+    p->info.t_skel = now() - t0;
+    p->export_desc();
+    *out = p.release();
+  });
+}
+
+const sfmm_plan_desc* sfmm_host_desc(sfmm_host_plan* p) { return p ? &p->desc : nullptr; }
+
+int sfmm_host_info_get(const sfmm_host_plan* p, sfmm_host_info* info) {
+  if (!p || !info) return fail(SFMM_EINVAL, "null argument");
+  *info = p->info;
+  return SFMM_OK;
+}
+
+void sfmm_host_destroy(sfmm_host_plan* p) { delete p; }
+
+}  // extern "C"

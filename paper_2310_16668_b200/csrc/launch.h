@@ -65,4 +65,7 @@ void launch_direct_subset(int kernel, double kappa, int dim, int64_t n, const do
 int configure_translate(DevPlan& p, int device);
 int configure_tree_kernels(DevPlan& p, size_t max_r, size_t max_k);
 
+// DFMA throughput probe (TFLOP/s), see kernels_probe.cu.
+double measure_fp64_peak(int device);
+
 }  // namespace sfmm_gpu

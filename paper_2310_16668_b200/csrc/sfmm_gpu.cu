@@ -90,6 +90,7 @@ struct sfmm_gpu_plan {
     if (ev_b) cudaEventDestroy(ev_b);
     if (ev_k2a) cudaEventDestroy(ev_k2a);
     if (ev_k2b) cudaEventDestroy(ev_k2b);
+    for (cudaEvent_t e : tev) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
   }
 
@@ -104,19 +105,47 @@ struct sfmm_gpu_plan {
     io_cap = bytes;
   }
 
+  // Phase timing: 6 events per recorded apply (phase boundaries).
+  static constexpr int kMaxTimed = 256;
+  bool timing = false;
+  std::vector<cudaEvent_t> tev;
+  int n_timed = 0;
+
+  void mark(int slot, int k, cudaStream_t st) {
+    ck(cudaEventRecord(tev[(size_t)slot * 6 + k], st), "event");
+  }
+
   // Enqueues one right-hand side: q, u device pointers in original order.
   void enqueue_one(const double* q, double* u, cudaStream_t st, bool time_k2) {
     if (hp.depth < 2) {
       launch_direct_fallback(dp, q, u, st);
       return;
     }
+    const int slot = (timing && n_timed < kMaxTimed) ? n_timed++ : -1;
+    if (slot >= 0) mark(slot, 0, st);
     launch_gather(dp, q, ds, st);
+    if (slot >= 0) mark(slot, 1, st);
     for (int l = hp.depth; l >= 2; --l) launch_upward(dp, hp, l, ds, st);
+    if (slot >= 0) mark(slot, 2, st);
     if (time_k2) ck(cudaEventRecord(ev_k2a, st), "event");
     launch_translate(dp, ds, st);
     if (time_k2) ck(cudaEventRecord(ev_k2b, st), "event");
+    if (slot >= 0) mark(slot, 3, st);
     for (int l = 2; l <= hp.depth; ++l) launch_downward(dp, hp, l, ds, st);
+    if (slot >= 0) mark(slot, 4, st);
     launch_scatter(dp, ds, u, st);
+    if (slot >= 0) mark(slot, 5, st);
+  }
+
+  int launches_per_apply() const {
+    if (hp.depth < 2) return 1;
+    int n = 3;  // gather, translate, scatter
+    for (int l = 2; l <= hp.depth; ++l) {
+      n += hp.up_lvl[l + 1] > hp.up_lvl[l] ? 1 : 0;
+      n += hp.down_lvl[l + 1] > hp.down_lvl[l] ? 1 : 0;
+    }
+    if (dp.n_tasks == 0) --n;
+    return n;
   }
 
   size_t scalar_bytes() const { return hp.cplx ? 16 : 8; }
@@ -325,7 +354,59 @@ int sfmm_gpu_plan_info_get(const sfmm_gpu_plan* p, sfmm_gpu_plan_info* info) {
   info->n_ifs_pairs = hp.n_ifs;
   info->n_tfo_pairs = hp.n_tfo;
   info->n_level1_pairs = hp.n_l1;
+  info->launches_per_apply = p->launches_per_apply();
+  info->k2_grid = p->dp.k2_grid;
   return SFMM_OK;
+}
+
+int sfmm_gpu_set_timing(sfmm_gpu_plan* p, int enable) {
+  if (!p) return set_error(SFMM_EINVAL, "null plan");
+  std::lock_guard<std::mutex> lock(p->mu);
+  try {
+    ck(cudaSetDevice(p->device), "cudaSetDevice");
+    if (enable && p->tev.empty()) {
+      p->tev.resize((size_t)sfmm_gpu_plan::kMaxTimed * 6);
+      for (cudaEvent_t& e : p->tev) ck(cudaEventCreate(&e), "cudaEventCreate");
+    }
+    p->timing = enable != 0;
+    p->n_timed = 0;
+    return SFMM_OK;
+  } catch (const CudaFail& f) {
+    return set_error(f.code, f.msg);
+  }
+}
+
+int sfmm_gpu_get_timings(sfmm_gpu_plan* p, float* ms, int max_applies, int* n_applies) {
+  if (!p || !n_applies) return set_error(SFMM_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lock(p->mu);
+  try {
+    ck(cudaSetDevice(p->device), "cudaSetDevice");
+    const int n = std::min(p->n_timed, max_applies);
+    for (int i = 0; i < n; ++i) {
+      ck(cudaEventSynchronize(p->tev[(size_t)i * 6 + 5]), "event sync");
+      for (int k = 0; k < 5; ++k)
+        ck(cudaEventElapsedTime(&ms[i * 5 + k], p->tev[(size_t)i * 6 + k],
+                                p->tev[(size_t)i * 6 + k + 1]),
+           "event time");
+    }
+    *n_applies = n;
+    p->n_timed = 0;
+    return SFMM_OK;
+  } catch (const CudaFail& f) {
+    return set_error(f.code, f.msg);
+  }
+}
+
+int sfmm_gpu_fp64_peak(int device, double* tflops) {
+  if (!tflops) return set_error(SFMM_EINVAL, "null argument");
+  try {
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    *tflops = measure_fp64_peak(device);
+    if (*tflops <= 0) return set_error(SFMM_ECUDA, "fp64 peak probe failed");
+    return SFMM_OK;
+  } catch (const CudaFail& f) {
+    return set_error(f.code, f.msg);
+  }
 }
 
 void sfmm_gpu_plan_destroy(sfmm_gpu_plan* p) { delete p; }

@@ -1,0 +1,163 @@
+"""Python handle on the host precompute library (include/sfmm_host.h).
+
+Mirrors the reference's host API that feeds the apply:
+    build_tree + build_neighbor_lists  (tree.cpp:148-355)
+    build_skeletons                     (skeleton.cpp:184-260)
+    generate_points / generate_charges  (bench.cpp:102-161)
+and exports the flat plan descriptor consumed by ``api.GpuPlan``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import _abi
+from ._abi import PlanDesc, PlanDescriptor
+
+DIST = {"square": 0, "annulus": 1, "cube": 2, "sphere": 3}
+DIST_DIM = {"square": 2, "annulus": 2, "cube": 3, "sphere": 3}
+CHARGE_STREAM = 0x9E3779B97F4A7C15  # bench.cpp:27
+DEFAULT_LEAF_CAP = {"square": 100, "annulus": 100, "cube": 320, "sphere": 200}  # bench.cpp:92-100
+SFMM_EDEPTH = 7
+
+
+class DepthExceededError(RuntimeError):
+    """sfmm::DepthExceededError (common.hpp:25-29)."""
+
+
+class HostInfo(C.Structure):
+    _fields_ = [("depth", C.c_int32), ("n_boxes", C.c_int32), ("n_leaves", C.c_int64),
+                ("k_max", C.c_int32), ("saturated_boxes", C.c_int32), ("proj_scalars", C.c_int64),
+                ("t_tree", C.c_double), ("t_skel", C.c_double)]
+
+
+class ProxyConfig(C.Structure):
+    _fields_ = [("radius_factor", C.c_double), ("edge_points_2d", C.c_int32),
+                ("face_grid_3d", C.c_int32)]
+
+
+_lib = None
+
+
+def host_lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        path = os.path.join(_abi.LIB_DIR, "libsfmm_host.so")
+        if not os.path.exists(path):
+            raise _abi.NativeLibraryMissing(f"{path} is missing; run `make`")
+        lib = C.CDLL(path)
+        vp = C.c_void_p
+        lib.sfmm_host_generate_points.argtypes = [C.c_int, C.c_int64, C.c_uint64, vp]
+        lib.sfmm_host_generate_charges.argtypes = [C.c_int64, C.c_uint64, vp]
+        lib.sfmm_host_generate_charges_complex.argtypes = [C.c_int64, C.c_uint64, vp]
+        lib.sfmm_host_build_tree.argtypes = [C.c_int, C.c_int64, vp, C.c_int, C.POINTER(vp)]
+        lib.sfmm_host_build.argtypes = [C.c_int, C.c_double, C.c_int, C.c_int64, vp, C.c_int,
+                                        C.c_double, C.POINTER(ProxyConfig), C.POINTER(vp)]
+        lib.sfmm_host_desc.argtypes = [vp]
+        lib.sfmm_host_desc.restype = C.POINTER(PlanDesc)
+        lib.sfmm_host_info_get.argtypes = [vp, C.POINTER(HostInfo)]
+        lib.sfmm_host_destroy.argtypes = [vp]
+        lib.sfmm_host_destroy.restype = None
+        lib.sfmm_host_set_threads.argtypes = [C.c_int]
+        lib.sfmm_host_set_threads.restype = None
+        lib.sfmm_host_get_threads.restype = C.c_int
+        lib.sfmm_host_last_error.restype = C.c_char_p
+        _lib = lib
+    return _lib
+
+
+def _check(rc: int) -> None:
+    if rc == 0:
+        return
+    from .api import DuplicatePointError
+    msg = host_lib().sfmm_host_last_error().decode()
+    if rc == _abi.SFMM_EDUPLICATE:
+        raise DuplicatePointError(msg)
+    if rc == SFMM_EDEPTH:
+        raise DepthExceededError(msg)
+    if rc == _abi.SFMM_EINVAL:
+        raise ValueError(msg)
+    if rc == _abi.SFMM_EUNSUPPORTED:
+        raise NotImplementedError(msg)
+    if rc == _abi.SFMM_ENOMEM:
+        raise MemoryError(msg)
+    raise RuntimeError(msg)
+
+
+def generate_points(dist: str, n: int, seed: int) -> np.ndarray:
+    out = np.empty((n, DIST_DIM[dist]), dtype=np.float64)
+    _check(host_lib().sfmm_host_generate_points(DIST[dist], n, seed, out.ctypes.data))
+    return out
+
+
+def generate_charges(n: int, seed: int) -> np.ndarray:
+    out = np.empty(n, dtype=np.float64)
+    _check(host_lib().sfmm_host_generate_charges(n, seed & 0xFFFFFFFFFFFFFFFF, out.ctypes.data))
+    return out
+
+
+def generate_charges_complex(n: int, seed: int) -> np.ndarray:
+    out = np.empty(n, dtype=np.complex128)
+    _check(host_lib().sfmm_host_generate_charges_complex(n, seed & 0xFFFFFFFFFFFFFFFF,
+                                                         out.ctypes.data))
+    return out
+
+
+class HostPlan:
+    """Tree + neighbor lists (+ skeletons) built on the host."""
+
+    def __init__(self, handle):
+        self._h = handle
+
+    @classmethod
+    def build(cls, kernel: int, pts: np.ndarray, leaf_cap: int, tol: float, kappa: float = 1.0,
+              proxy: tuple | None = None) -> "HostPlan":
+        pts = np.ascontiguousarray(pts, dtype=np.float64)
+        h = C.c_void_p()
+        px = ProxyConfig(*(proxy or (0.0, 0, 0)))
+        _check(host_lib().sfmm_host_build(kernel, kappa, pts.shape[1], pts.shape[0],
+                                          pts.ctypes.data, leaf_cap, tol, C.byref(px),
+                                          C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def build_tree(cls, pts: np.ndarray, leaf_cap: int) -> "HostPlan":
+        pts = np.ascontiguousarray(pts, dtype=np.float64)
+        h = C.c_void_p()
+        _check(host_lib().sfmm_host_build_tree(pts.shape[1], pts.shape[0], pts.ctypes.data,
+                                               leaf_cap, C.byref(h)))
+        return cls(h)
+
+    def descriptor(self) -> PlanDescriptor:
+        """Owned numpy copy of the flat descriptor."""
+        return PlanDescriptor.from_struct(host_lib().sfmm_host_desc(self._h).contents)
+
+    def desc_struct(self) -> PlanDesc:
+        """Zero-copy view of the descriptor; valid while this plan is alive."""
+        return host_lib().sfmm_host_desc(self._h).contents
+
+    def info(self) -> dict:
+        inf = HostInfo()
+        _check(host_lib().sfmm_host_info_get(self._h, C.byref(inf)))
+        return {k: getattr(inf, k) for k, _ in HostInfo._fields_}
+
+    def close(self) -> None:
+        if self._h is not None:
+            host_lib().sfmm_host_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def set_threads(n: int) -> None:
+    host_lib().sfmm_host_set_threads(n)
+
+
+def get_threads() -> int:
+    return host_lib().sfmm_host_get_threads()
