@@ -60,6 +60,21 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err) {
       return SFMM_OK;
     }
 
+    auto check_csr = [&](const int64_t* off, const int32_t* v, const char* what) {
+      if (off[0] != 0) bad(std::string(what) + " offsets must start at 0");
+      for (int32_t b = 0; b < nb; ++b)
+        if (off[b + 1] < off[b]) bad(std::string(what) + " offsets not monotone");
+      if (off[nb] > 0 && !v) bad(std::string("null ") + what);
+      for (int64_t e = 0; e < off[nb]; ++e)
+        if (v[e] < 0 || v[e] >= nb) bad(std::string(what) + " box id out of range");
+    };
+    check_csr(d.coll_off, d.coll, "colleague");
+    check_csr(d.coarse_off, d.coarse, "coarse");
+    check_csr(d.fine_off, d.fine, "fine");
+    for (int32_t b = 0; b < nb; ++b)
+      if (d.box_parent[b] < -1 || d.box_parent[b] >= nb || (b > 0 && d.box_parent[b] < 0))
+        bad("box parent out of range");
+
     hp.box.resize(nb);
     hp.box_parent.assign(d.box_parent, d.box_parent + nb);
     hp.box_level.assign(d.box_level, d.box_level + nb);

@@ -1,0 +1,203 @@
+"""GPU parity of the sm_100a apply (through the C ABI) against the reference.
+
+Mirrors /root/reference/proj/tests/test_apply.cpp and acceptance C6:
+results within rel-l2 1e-12 of the reference CPU apply on the same tree,
+skeletons and charges; within the skeletonization band of the dense sum;
+exact pair counts; linearity; exact zeros; bit-identical repeats; the depth<2
+dense fallback; coincident-point detection; multi-RHS.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import golden_files, load_golden, max_rel, rel_l2, requires_ref
+from oracle import pyoracle as po
+from paper_2310_16668_b200 import api, host
+
+pytestmark = pytest.mark.gpu
+GOLDEN = golden_files()
+PARITY = 1e-12  # north star: relative l2 vs the CPU reference apply
+
+
+@pytest.mark.parametrize("path", GOLDEN, ids=[os.path.basename(p)[:-4] for p in GOLDEN])
+def test_golden_parity(path):
+    desc, ex = load_golden(path)
+    plan = api.GpuPlan(desc)
+    st = api.ApplyStats()
+    u = api.fmm_apply(plan, ex["q"], st)
+    assert rel_l2(u, ex["u_ref"]) <= PARITY
+    assert [st.n_ifo_pairs, st.n_ifs_pairs, st.n_tfo_pairs, st.n_level1_pairs,
+            int(st.direct_fallback)] == list(ex["stats"])
+    tol = float(ex["tol"])
+    assert max_rel(u, ex["u_direct"]) <= (1e-6 if tol <= 1e-8 else 10 * tol)
+
+
+def test_depth0_fallback_bit_identical_to_direct_sum():
+    # test_apply.cpp:164-177 (two points, depth 0) -- Laplace3d arithmetic is
+    # correctly rounded on both sides, so the fallback matches bit for bit.
+    pts = np.array([[0.1, 0.2, 0.3], [0.8, 0.9, 0.4]])
+    q = np.array([1.5, -0.5])
+    hp = host.HostPlan.build(1, pts, 10, 1e-6)
+    plan = api.GpuPlan(hp.descriptor())
+    st = api.ApplyStats()
+    u = api.fmm_apply(plan, q, st)
+    assert st.direct_fallback
+    assert np.array_equal(u, po.oracle_direct_sum(1, 1.0, pts, q))
+
+
+def test_depth1_fallback_matches_direct_sum():
+    pts = host.generate_points("cube", 900, 13)
+    q = host.generate_charges(900, 13)
+    d = host.HostPlan.build(1, pts, 200, 1e-6).descriptor()
+    assert d.scalars["depth"] == 1
+    u = api.fmm_apply(api.GpuPlan(d), q)
+    assert np.array_equal(u, po.oracle_direct_sum(1, 1.0, pts, q))
+
+
+def _pipeline(kernel, dist, n, leaf, tol, seed=1, kappa=1.0):
+    pts = host.generate_points(dist, n, seed)
+    hp = host.HostPlan.build(kernel, pts, leaf, tol, kappa)
+    return pts, hp, api.GpuPlan(hp.desc_struct())
+
+
+def test_linearity():
+    # test_apply.cpp:179-196
+    n = 900
+    _, _, plan = _pipeline(0, "annulus", n, 30, 1e-6, seed=31)
+    q1, q2 = host.generate_charges(n, 32), host.generate_charges(n, 33)
+    a, b = 0.75, -1.25
+    u = api.fmm_apply(plan, a * q1 + b * q2)
+    u1, u2 = api.fmm_apply(plan, q1), api.fmm_apply(plan, q2)
+    assert np.max(np.abs(u - (a * u1 + b * u2))) <= 1e-12 * np.max(np.abs(u))
+
+
+def test_zero_charges_give_exact_zeros():
+    # test_apply.cpp:198-204
+    _, _, plan = _pipeline(1, "cube", 800, 40, 1e-4, seed=41)
+    u = api.fmm_apply(plan, np.zeros(800))
+    assert np.all(u == 0.0)
+
+
+def test_repeat_applies_bit_identical():
+    # test_apply.cpp:206-231: deterministic, no result atomics
+    n = 1200
+    _, _, plan = _pipeline(3, "sphere", n, 30, 1e-6, seed=51, kappa=2.5)
+    q = host.generate_charges_complex(n, 52)
+    u1 = api.fmm_apply(plan, q)
+    u2 = api.fmm_apply(plan, q)
+    assert np.array_equal(u1, u2)
+
+
+def test_pair_counts():
+    # test_apply.cpp:233-254
+    n = 2500
+    _, hp, plan = _pipeline(0, "annulus", n, 25, 1e-5, seed=61)
+    st = api.ApplyStats()
+    api.fmm_apply(plan, host.generate_charges(n, 62), st)
+    d = hp.descriptor()
+    a = d.arrays
+    assert not st.direct_fallback
+    assert st.n_ifo_pairs > 0 and st.n_ifs_pairs > 0
+    assert st.n_ifs_pairs == st.n_tfo_pairs
+    nl1 = a["level_begin"][2] - a["level_begin"][1]
+    assert st.n_level1_pairs == nl1 * nl1
+    lvl = a["box_level"]
+    want = sum(a["coll_off"][b + 1] - a["coll_off"][b] for b in range(d.scalars["n_boxes"])
+               if lvl[b] >= 2)
+    assert st.n_ifo_pairs == want
+
+
+def test_charge_count_mismatch():
+    _, _, plan = _pipeline(1, "cube", 500, 40, 1e-6)
+    with pytest.raises(ValueError):
+        api.fmm_apply(plan, np.ones(499))
+
+
+def test_coincident_points_raise_duplicate_error():
+    # apply.cpp:31-33: coincident points with distinct ids -> DuplicatePointError.
+    # Build a valid plan, then move one point onto another inside the same leaf.
+    pts = host.generate_points("cube", 3000, 7)
+    d = host.HostPlan.build(1, pts, 40, 1e-6).descriptor()
+    a = d.arrays
+    leaf = int(np.nonzero(a["box_leaf"] & (a["box_end"] - a["box_begin"] >= 2))[0][0])
+    t0, t1 = a["box_begin"][leaf], a["box_begin"][leaf] + 1
+    P = a["pts"].reshape(-1, 3)
+    P[t1] = P[t0]
+    d._struct = None
+    plan = api.GpuPlan(d)
+    with pytest.raises(api.DuplicatePointError):
+        api.fmm_apply(plan, host.generate_charges(3000, 1))
+    with pytest.raises(po.RefError):  # the restatement agrees
+        po.oracle_apply(d, host.generate_charges(3000, 1))
+
+
+def test_nan_charges_stay_nan_without_duplicate_error():
+    _, _, plan = _pipeline(1, "cube", 2000, 40, 1e-6)
+    q = host.generate_charges(2000, 3)
+    q[17] = np.nan
+    u = api.fmm_apply(plan, q)
+    assert np.isnan(u).any()
+
+
+def test_multi_rhs_equals_column_loop():
+    n = 3000
+    _, _, plan = _pipeline(3, "cube", n, 60, 1e-6, kappa=10.0)
+    Q = np.stack([host.generate_charges_complex(n, 100 + r) for r in range(4)], axis=1)
+    U = api.fmm_apply(plan, Q)
+    for r in range(4):
+        assert np.array_equal(U[:, r], api.fmm_apply(plan, Q[:, r]))
+
+
+def test_device_buffer_path_matches_host_path():
+    import torch
+    n = 20000
+    _, _, plan = _pipeline(1, "cube", n, 64, 1e-6)
+    q = host.generate_charges(n, 9)
+    u_host = api.fmm_apply(plan, q)
+    qd = torch.from_numpy(q).cuda()
+    ud = torch.empty_like(qd)
+    s = torch.cuda.Stream()
+    api.fmm_apply_device(plan, qd.data_ptr(), ud.data_ptr(), 1, s.cuda_stream)
+    api.check_status(plan)
+    assert np.array_equal(ud.cpu().numpy(), u_host)
+
+
+@requires_ref
+@pytest.mark.parametrize("kernel,dist,n,leaf,tol,kappa", [
+    (0, "square", 100000, 64, 1e-6, 1.0),      # config 1
+    (1, "cube", 200000, 128, 1e-6, 1.0),       # config 2 geometry, 1/5 N
+    (1, "sphere", 100000, 128, 1e-8, 1.0),     # config 3(a) geometry, adaptive
+    (3, "cube", 40000, 128, 1e-6, 10.0),       # config 4 geometry
+])
+def test_parity_vs_reference_at_scale(kernel, dist, n, leaf, tol, kappa):
+    pts, hp, plan = _pipeline(kernel, dist, n, leaf, tol, kappa=kappa)
+    q = (host.generate_charges_complex(n, 1 ^ host.CHARGE_STREAM) if kernel == 3
+         else host.generate_charges(n, 1 ^ host.CHARGE_STREAM))
+    u = api.fmm_apply(plan, q)
+    rp = po.RefPipeline.from_desc(hp.desc_struct())
+    u_ref, st = rp.apply(q, kernel == 3)
+    assert rel_l2(u, u_ref) <= PARITY
+    # sampled dense check on the GPU (oracle.cpp:51-71)
+    t = np.sort(np.random.default_rng(0).choice(n, 200, replace=False)).astype(np.int32)
+    ref_t = api.direct_sum_subset(kernel, kappa, pts, q, t)
+    assert max_rel(u[t], ref_t) <= (1e-6 if tol <= 1e-8 else 10 * tol)
+
+
+def test_direct_subset_matches_oracle():
+    pts = host.generate_points("sphere", 5000, 4)
+    q = host.generate_charges(5000, 5)
+    t = np.arange(0, 5000, 37, dtype=np.int32)
+    u = api.direct_sum_subset(1, 1.0, pts, q, t)
+    assert rel_l2(u, po.oracle_direct_sum(1, 1.0, pts, q, t)) <= 1e-14
+
+
+def test_large_linearity_and_determinism_1e6():
+    # size-independent properties at config-2 scale (3D cube, N=1e6, leaf 128)
+    n = 1000000
+    _, _, plan = _pipeline(1, "cube", n, 128, 1e-6)
+    q1, q2 = host.generate_charges(n, 1), host.generate_charges(n, 2)
+    u1, u2 = api.fmm_apply(plan, q1), api.fmm_apply(plan, q2)
+    u12 = api.fmm_apply(plan, q1 - 2.0 * q2)
+    assert np.max(np.abs(u12 - (u1 - 2.0 * u2))) <= 1e-12 * np.max(np.abs(u12))
+    assert np.array_equal(api.fmm_apply(plan, q1), u1)
