@@ -1,0 +1,77 @@
+// TEST INFRASTRUCTURE -- exercises the C++ drop-in include/sfmm_gpu.hpp the way
+// a reference user would: the reference's own pipeline (build_tree,
+// build_neighbor_lists, build_skeletons, make_plan), then the CPU
+// sfmm::fmm_apply and the GPU sfmm::gpu::fmm_apply on the same plan and
+// charges.  Prints one line per case and exits non-zero if any case misses
+// rel-l2 1e-12 or the ApplyStats differ.  Built by oracle/Makefile into
+// oracle/_ref/dropin_parity (links the reference objects and libsfmm_gpu.so).
+#include <cmath>
+#include <cstdio>
+#include <vector>
+
+#include "sfmm/apply.hpp"
+#include "sfmm/bench.hpp"
+#include "sfmm/oracle.hpp"
+#include "sfmm_gpu.hpp"
+
+using namespace sfmm;
+
+template <class T>
+double rel_l2(const std::vector<T>& u, const std::vector<T>& r) {
+  double num = 0, den = 0;
+  for (size_t i = 0; i < u.size(); ++i) {
+    num += abs_sq(u[i] - r[i]);
+    den += abs_sq(r[i]);
+  }
+  return std::sqrt(num / (den > 0 ? den : 1));
+}
+
+template <class K>
+int run(const char* name, const K& kern, Distribution dist, int64_t n, int leaf, double tol) {
+  using S = typename K::scalar;
+  const PointSet pts = generate_points(dist, n, 1);
+  const Tree tree = build_tree(pts, leaf);
+  const NeighborLists nb = build_neighbor_lists(tree);
+  const SkeletonSet<S> skel = build_skeletons(tree, kern, tol);
+  const ApplyPlan<K> plan = make_plan(kern, tree, nb, skel);
+  std::vector<S> q;
+  if constexpr (std::is_same_v<S, double>)
+    q = generate_charges(n, 2);
+  else
+    q = generate_charges_complex(n, 2);
+  ApplyStats s_cpu, s_gpu;
+  const std::vector<S> u_cpu = fmm_apply(plan, q, &s_cpu);
+  gpu::GpuPlan<K> gplan(plan);
+  const std::vector<S> u_gpu = gpu::fmm_apply(gplan, q, &s_gpu);
+  const double err = rel_l2(u_gpu, u_cpu);
+  const bool stats_ok = s_cpu.n_ifo_pairs == s_gpu.n_ifo_pairs &&
+                        s_cpu.n_ifs_pairs == s_gpu.n_ifs_pairs &&
+                        s_cpu.n_tfo_pairs == s_gpu.n_tfo_pairs &&
+                        s_cpu.n_level1_pairs == s_gpu.n_level1_pairs &&
+                        s_cpu.direct_fallback == s_gpu.direct_fallback;
+  const bool ok = err <= 1e-12 && stats_ok;
+  std::printf("%-28s n=%-7lld depth=%d rel_l2=%.3e stats=%s %s\n", name, (long long)n, tree.depth,
+              err, stats_ok ? "same" : "DIFFER", ok ? "OK" : "FAIL");
+  // the reference's exception contract survives the boundary
+  bool threw = false;
+  try {
+    std::vector<S> bad(q.begin(), q.end() - 1);
+    gpu::fmm_apply(gplan, bad);
+  } catch (const std::invalid_argument&) {
+    threw = true;
+  }
+  if (!threw) std::printf("%-28s size mismatch did not throw std::invalid_argument FAIL\n", name);
+  return ok && threw ? 0 : 1;
+}
+
+int main() {
+  int fails = 0;
+  fails += run("laplace3d cube", Laplace3d{}, Distribution::cube, 20000, 64, 1e-6);
+  fails += run("laplace3d sphere tol1e-8", Laplace3d{}, Distribution::sphere, 20000, 40, 1e-8);
+  fails += run("laplace2d square", Laplace2d{}, Distribution::square, 20000, 64, 1e-6);
+  fails += run("laplace2d annulus", Laplace2d{}, Distribution::annulus, 8000, 30, 1e-6);
+  fails += run("helmholtz3d cube k=10", Helmholtz3d{10.0}, Distribution::cube, 8000, 64, 1e-6);
+  fails += run("laplace3d depth0 fallback", Laplace3d{}, Distribution::cube, 50, 100, 1e-6);
+  std::printf("%s\n", fails ? "DROPIN PARITY FAIL" : "DROPIN PARITY OK");
+  return fails ? 1 : 0;
+}

@@ -201,3 +201,18 @@ def test_large_linearity_and_determinism_1e6():
     u12 = api.fmm_apply(plan, q1 - 2.0 * q2)
     assert np.max(np.abs(u12 - (u1 - 2.0 * u2))) <= 1e-12 * np.max(np.abs(u12))
     assert np.array_equal(api.fmm_apply(plan, q1), u1)
+
+
+DROPIN = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref",
+                      "dropin_parity")
+
+
+@pytest.mark.skipif(not os.path.exists(DROPIN), reason="oracle/_ref/dropin_parity not built")
+def test_cpp_dropin_header_against_reference():
+    # include/sfmm_gpu.hpp used exactly as a reference user would (reference
+    # pipeline -> GpuPlan<K> -> sfmm::gpu::fmm_apply) vs sfmm::fmm_apply
+    import subprocess
+    r = subprocess.run([DROPIN], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "DROPIN PARITY OK" in r.stdout
