@@ -12,8 +12,12 @@ enum Mode : int32_t {
   kIFO = 0,  // colleagues, level >= 2: u_b += A(B_b,B_c) q_c ; uhat_b -= A(S_b,S_c) qhat_c
   kIFS = 1,  // coarse leaves:          u_b += A(B_b,L_c) q_c ; uhat_b -= A(S_b,L_c) q_c
   kTFO = 2,  // fine boxes of a leaf:   u_b += A(L_b,B_c) q_c - A(L_b,S_c) qhat_c
-  kL1 = 3    // level-1 all pairs:      u_b += A(B_b,B_c) q_c
+  kL1 = 3,   // level-1 all pairs:      u_b += A(B_b,B_c) q_c
+  kSYM = 4   // IFO with a colleague c > b, evaluated once for both directions:
+             // b's rows as kIFO, c's rows (A_cb = A_bc^T) as staged column sums
 };
+constexpr int kModeBits = 3;
+constexpr int32_t kModeMask = (1 << kModeBits) - 1;
 
 // Per-box record used by the translation kernel.  Slots of a compressed box
 // are ordered [skeleton (skel_pos order) | redundant (red_pos order)], so
@@ -33,6 +37,7 @@ struct Task {
   int32_t row0;
   int32_t nrows;
   int32_t pad;
+  int64_t stage;  // first staging slot of this task's kSYM column sums
 };
 
 struct EntryRange {

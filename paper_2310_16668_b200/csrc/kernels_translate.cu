@@ -53,7 +53,12 @@ struct K2Args {
   int* counter;
   int* err;
   double kappa;
+  double* St;  // staging for kSYM column sums (unscaled)
 };
+
+// Far-away padding for partial source chunks of kSYM blocks: finite r^2,
+// negligible G, zero weights.
+constexpr double kFar = 1e100;
 
 // rsqrt to full double precision: MUFU.RSQ64H seed + one cubic correction
 // (5 FP64 ops).  r2 == 0 yields NaN, which the diagonal select / duplicate
@@ -73,11 +78,28 @@ struct GenLaplace3d {  // kernel.hpp:46-50  1/(4 pi r)
   static constexpr int kDim = 3;
   static constexpr double kScale = kInv4Pi;
   __device__ static __forceinline__ double g(double r2) { return rsqrt_fp64(r2); }
+  // M independent evaluations, stage by stage, so their dependent chains
+  // interleave in the issue stream.
+  template <int M>
+  __device__ static __forceinline__ void batch(const double* r2, double* g) {
+    double y[M], e[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y[m]) : "d"(r2[m]));
+#pragma unroll
+    for (int m = 0; m < M; ++m) e[m] = fma(-r2[m], y[m] * y[m], 1.0);
+#pragma unroll
+    for (int m = 0; m < M; ++m) g[m] = fma(fma(0.375, e[m], 0.5), y[m] * e[m], y[m]);
+  }
 };
 struct GenLaplace2d {  // kernel.hpp:40-44  -log(r^2)/(4 pi)
   static constexpr int kDim = 2;
   static constexpr double kScale = -kInv4Pi;
   __device__ static __forceinline__ double g(double r2) { return log(r2); }
+  template <int M>
+  __device__ static __forceinline__ void batch(const double* r2, double* g) {
+#pragma unroll
+    for (int m = 0; m < M; ++m) g[m] = log(r2[m]);
+  }
 };
 
 struct WarpSmemReal {
@@ -101,7 +123,7 @@ __device__ __noinline__ void verify_row(const K2Args& a, int32_t b, int32_t row,
   const int32_t id = a.sid[s];
   const EntryRange er = a.er[b];
   for (int e = 0; e < er.count; ++e) {
-    const BoxRec sb = a.box[a.ent[er.begin + e] >> 2];
+    const BoxRec sb = a.box[a.ent[er.begin + e] >> kModeBits];
     for (int j = 0; j < sb.n; ++j) {
       const int64_t t = sb.slot + j;
       const double dx = x - a.X[t], dy = y - a.Y[t], dz = dim == 3 ? z - a.Z[t] : 0.0;
@@ -138,30 +160,111 @@ __device__ __forceinline__ void inner_real(const WarpSmemReal& sm, int cnt, int 
   }
 }
 
+// One staged source chunk of a kSYM block: b's rows (registers) against 32 of
+// c's columns.  Row sums as for kIFO.  Column sums sum_i G(i,j) q_b[i] (and,
+// with H, sum_{i<k_b} G(i,j) qhat_b[i] for j < k_c) use a rotation instead of a
+// reduction: at step s lane l evaluates column (l+s) mod 32 for its R rows and
+// the running column sum moves one lane down, so after 32 steps lane l holds
+// the complete sum of column l over the warp's 32R rows.  Fixed order, no
+// butterfly, two column accumulators per lane.
+template <class G, int R, bool H>
+__device__ __forceinline__ void sym_chunk(const WarpSmemReal& sm, int j0, int n_c, int k_c,
+                                          const double (&xi)[R], const double (&yi)[R],
+                                          const double (&zi)[R], const double (&qr)[R],
+                                          const double (&qhr)[R], double (&au)[R],
+                                          double (&ah)[R], double* __restrict__ st_u,
+                                          double* __restrict__ st_h, int lane) {
+  double cp = 0.0, ch = 0.0;
+  const int from = (lane + 1) & 31;
+#pragma unroll 4
+  for (int s = 0; s < 32; ++s) {
+    const int jc = (lane + s) & 31;
+    const double2 xy = sm.xy[jc];
+    const double2 za = sm.za[jc];
+    const double wh = H ? sm.h[jc] : 0.0;
+    double r2[R], g[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const double dx = xi[r] - xy.x;
+      const double dy = yi[r] - xy.y;
+      r2[r] = fma(dy, dy, dx * dx);
+      if (G::kDim == 3) {
+        const double dz = zi[r] - za.x;
+        r2[r] = fma(dz, dz, r2[r]);
+      }
+    }
+    G::template batch<R>(r2, g);
+    double cs = 0.0, hs = 0.0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      au[r] = fma(g[r], za.y, au[r]);
+      cs = fma(g[r], qr[r], cs);
+      if (H) {
+        ah[r] = fma(g[r], wh, ah[r]);
+        hs = fma(g[r], qhr[r], hs);
+      }
+    }
+    cp = __shfl_sync(kFull, cp + cs, from);
+    if (H) ch = __shfl_sync(kFull, ch + hs, from);
+  }
+  const int col = j0 + lane;
+  if (col < n_c) st_u[col] = cp;
+  if (H && col < k_c) st_h[col] = ch;
+}
+
 template <class G, int R>
 __device__ __forceinline__ void task_real(const K2Args& a, const Task& t, WarpSmemReal& sm,
                                           int lane) {
   const BoxRec tb = a.box[t.box];
-  double xi[R], yi[R], zi[R], au[R], ah[R];
+  double xi[R], yi[R], zi[R], au[R], ah[R], qr[R], qhr[R];
   int rowi[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int row = t.row0 + r * 32 + lane;
     rowi[r] = row;
-    const int64_t s = tb.slot + (row < t.row0 + t.nrows ? row : t.row0);
+    const bool valid = row < t.row0 + t.nrows;
+    const int64_t s = tb.slot + (valid ? row : t.row0);
     xi[r] = a.X[s];
     yi[r] = a.Y[s];
     zi[r] = G::kDim == 3 ? a.Z[s] : 0.0;
+    qr[r] = valid ? a.Q[s] : 0.0;  // row charges feed kSYM column sums
+    qhr[r] = (valid && row < tb.k) ? a.QH[tb.skel + row] : 0.0;
     au[r] = 0.0;
     ah[r] = 0.0;
   }
   const EntryRange er = a.er[t.box];
   const bool skel_rows = t.row0 < tb.k;
+  int64_t stage = t.stage;
   for (int e = 0; e < er.count; ++e) {
     const int32_t code = a.ent[er.begin + e];
-    const int32_t c = code >> 2;
-    const int mode = code & 3;
+    const int32_t c = code >> kModeBits;
+    const int mode = code & kModeMask;
     const BoxRec sb = a.box[c];
+    if (mode == kSYM) {
+      double* st_u = a.St + stage;
+      double* st_h = st_u + sb.n;
+      for (int j0 = 0; j0 < sb.n; j0 += 32) {
+        const int j = j0 + lane;
+        if (j < sb.n) {
+          const int64_t s = sb.slot + j;
+          sm.xy[lane] = make_double2(a.X[s], a.Y[s]);
+          sm.za[lane] = make_double2(G::kDim == 3 ? a.Z[s] : 0.0, a.Q[s]);
+          sm.h[lane] = j < sb.k ? a.QH[sb.skel + j] : 0.0;
+        } else {
+          sm.xy[lane] = make_double2(kFar, kFar);
+          sm.za[lane] = make_double2(kFar, 0.0);
+          sm.h[lane] = 0.0;
+        }
+        __syncwarp();
+        if (skel_rows && j0 < sb.k)
+          sym_chunk<G, R, true>(sm, j0, sb.n, sb.k, xi, yi, zi, qr, qhr, au, ah, st_u, st_h, lane);
+        else
+          sym_chunk<G, R, false>(sm, j0, sb.n, sb.k, xi, yi, zi, qr, qhr, au, ah, st_u, st_h, lane);
+        __syncwarp();
+      }
+      stage += sb.n + ((skel_rows && sb.k > 0) ? sb.k : 0);
+      continue;
+    }
     const bool self = c == t.box;
     for (int j0 = 0; j0 < sb.n; j0 += 32) {
       const int j = j0 + lane;
@@ -281,8 +384,8 @@ __device__ __forceinline__ void task_cplx(const K2Args& a, const Task& t, WarpSm
   const bool skel_rows = t.row0 < tb.k;
   for (int e = 0; e < er.count; ++e) {
     const int32_t code = a.ent[er.begin + e];
-    const int32_t c = code >> 2;
-    const int mode = code & 3;
+    const int32_t c = code >> kModeBits;
+    const int mode = code & kModeMask;
     const BoxRec sb = a.box[c];
     const bool self = c == t.box;
     for (int j0 = 0; j0 < sb.n; j0 += 32) {
@@ -347,6 +450,33 @@ __global__ void __launch_bounds__(kThreads, 4) k2_translate_cplx(K2Args a) {
   }
 }
 
+// K2b: adds the staged kSYM column sums to their receiving boxes, summing the
+// contributions in the (source box, row tile) order fixed at plan time.
+__global__ void __launch_bounds__(256) k2b_reduce(const BoxRec* __restrict__ box,
+                                                  const int32_t* __restrict__ recv_box,
+                                                  const int64_t* __restrict__ recv_off,
+                                                  const int64_t* __restrict__ recv_u,
+                                                  const int64_t* __restrict__ recv_h,
+                                                  const double* __restrict__ St,
+                                                  double* __restrict__ U,
+                                                  double* __restrict__ UH, double scale) {
+  const BoxRec br = box[recv_box[blockIdx.x]];
+  const int64_t e0 = recv_off[blockIdx.x], e1 = recv_off[blockIdx.x + 1];
+  for (int i = threadIdx.x; i < br.n; i += blockDim.x) {
+    double s = 0.0;
+    for (int64_t e = e0; e < e1; ++e) s += St[recv_u[e] + i];
+    U[br.slot + i] += scale * s;
+    if (i < br.k) {
+      double h = 0.0;
+      for (int64_t e = e0; e < e1; ++e) {
+        const int64_t o = recv_h[e];
+        if (o >= 0) h += St[o + i];
+      }
+      UH[br.skel + i] -= scale * h;
+    }
+  }
+}
+
 }  // namespace
 
 int configure_translate(DevPlan& p, int device) {
@@ -387,6 +517,11 @@ void launch_translate(const DevPlan& p, DevState& s, cudaStream_t st) {
   a.counter = p.counter;
   a.err = p.err_flag;
   a.kappa = p.kappa;
+  a.St = p.stage;
+  // boxes whose every entry cancels own no task: their U/UH stay zero
+  const size_t sw = p.cplx ? 16 : 8;
+  cudaMemsetAsync(s.U, 0, (size_t)p.n_slots * sw, st);
+  cudaMemsetAsync(s.UH, 0, (size_t)p.n_skel * sw, st);
   cudaMemsetAsync(p.counter, 0, sizeof(int), st);
   const int grid = (int)std::min<int64_t>(p.k2_grid, (p.n_tasks + kWarps - 1) / kWarps);
   if (p.kernel == SFMM_HELMHOLTZ3D)
@@ -395,6 +530,11 @@ void launch_translate(const DevPlan& p, DevState& s, cudaStream_t st) {
     k2_translate_real<GenLaplace3d><<<grid, kThreads, 0, st>>>(a);
   else
     k2_translate_real<GenLaplace2d><<<grid, kThreads, 0, st>>>(a);
+  if (p.n_recv > 0) {
+    const double scale = p.kernel == SFMM_LAPLACE3D ? GenLaplace3d::kScale : GenLaplace2d::kScale;
+    k2b_reduce<<<(unsigned)p.n_recv, 256, 0, st>>>(p.box, p.recv_box, p.recv_off, p.recv_u,
+                                                   p.recv_h, p.stage, s.U, s.UH, scale);
+  }
 }
 
 }  // namespace sfmm_gpu

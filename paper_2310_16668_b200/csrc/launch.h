@@ -37,6 +37,10 @@ struct DevPlan {
   int64_t* T_off;
   LevelItem *up_items, *down_items;
   double* orig_pts;
+  double* stage;    // kSYM column-sum staging (stage_size doubles)
+  int32_t* recv_box;
+  int64_t *recv_off, *recv_u, *recv_h;
+  int64_t n_recv;
   int* counter;     // K2 task counter (reset per launch)
   int* err_flag;    // sticky duplicate-point flag
   int k2_grid;      // persistent K2 CTAs

@@ -2,6 +2,7 @@
 #include "plan_build.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <numeric>
 
 namespace sfmm_gpu {
@@ -178,65 +179,146 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err) {
       if ((int64_t)hp.leaf_slot.size() != N) bad("leaves do not cover every point");
     }
 
-    // translation CSR (all four phases, one list per target box)
+    // translation CSR (all four phases, one list per target box).
+    //
+    // Exact cancellations (in exact arithmetic) are dropped: for a box that is
+    // uncompressed (level >= 2, k = n, so S = B and qhat = q) the dense add and
+    // the skeleton subtract of its ifo/ifs entries cancel once the downward
+    // pass adds uhat back onto u (apply.cpp:286), and a tfo entry whose source
+    // is uncompressed cancels within the entry (apply.cpp:228-234).  The pair
+    // counts (ApplyStats) still count them.
+    //
+    // With `symmetric`, an ifo pair of distinct colleagues b < c is evaluated
+    // once (kSYM in b's list): b's rows are accumulated as usual and c's rows
+    // receive A_cb q_b = (A_bc)^T q_b as staged column sums.
+    const PlanOptions opt = plan_options_from_env();
+    std::vector<uint8_t> unc(nb, 0);
+    for (int32_t b = 0; b < nb; ++b)
+      unc[b] = opt.skip_cancel && d.box_level[b] >= 2 && hp.box[b].n > 0 &&
+               hp.box[b].k == hp.box[b].n;
+    hp.symmetric = opt.symmetric && !hp.cplx;
+    if (hp.symmetric) {  // the colleague relation must be symmetric to stage
+      for (int32_t b = 0; b < nb && hp.symmetric; ++b)
+        for (int64_t e = d.coll_off[b]; e < d.coll_off[b + 1]; ++e) {
+          const int32_t c = d.coll[e];
+          const int32_t* cb = d.coll + d.coll_off[c];
+          const int32_t* ce = d.coll + d.coll_off[c + 1];
+          if (d.box_level[c] != d.box_level[b] || !std::binary_search(cb, ce, b)) {
+            hp.symmetric = false;
+            break;
+          }
+        }
+    }
     hp.ent_range.resize(nb);
     const int32_t l1b = hp.level_begin[1], l1e = hp.level_begin[2];
     for (int32_t b = 0; b < nb; ++b) {
       EntryRange& er = hp.ent_range[b];
       er.begin = (int64_t)hp.entries.size();
       const int lev = d.box_level[b];
-      auto push = [&](int32_t c, int mode) {
-        if (c < 0 || c >= nb) bad("neighbor id out of range");
-        hp.entries.push_back((c << 2) | mode);
+      auto count = [&](int32_t c, int mode) {
         const double nbn = hp.box[b].n, ncn = hp.box[c].n;
         hp.p_dense += nbn * ncn;
         if (mode == kIFO) hp.p_skel += (double)hp.box[b].k * hp.box[c].k;
         if (mode == kIFS) hp.p_skel += (double)hp.box[b].k * ncn;
         if (mode == kTFO) hp.p_skel += nbn * hp.box[c].k;
       };
+      auto push = [&](int32_t c, int mode) { hp.entries.push_back((c << kModeBits) | mode); };
       if (lev >= 2) {
         for (int64_t e = d.coll_off[b]; e < d.coll_off[b + 1]; ++e) {
-          push(d.coll[e], kIFO);
+          const int32_t c = d.coll[e];
           ++hp.n_ifo;
+          count(c, kIFO);
+          if (unc[b] && unc[c]) {
+            ++hp.n_skipped_pairs;
+            continue;
+          }
+          if (hp.symmetric && c != b) {
+            if (c > b) push(c, kSYM);  // c < b arrives through c's staged column sums
+          } else {
+            push(c, kIFO);
+          }
         }
         for (int64_t e = d.coarse_off[b]; e < d.coarse_off[b + 1]; ++e) {
-          push(d.coarse[e], kIFS);
           ++hp.n_ifs;
+          count(d.coarse[e], kIFS);
+          if (unc[b]) {
+            ++hp.n_skipped_pairs;
+            continue;
+          }
+          push(d.coarse[e], kIFS);
         }
       }
       if (lev == 1) {
         for (int32_t c = l1b; c < l1e; ++c) {
-          push(c, kL1);
           ++hp.n_l1;
+          count(c, kL1);
+          push(c, kL1);
         }
       }
       if (d.box_leaf[b] && lev >= 1) {
         for (int64_t e = d.fine_off[b]; e < d.fine_off[b + 1]; ++e) {
-          push(d.fine[e], kTFO);
           ++hp.n_tfo;
+          count(d.fine[e], kTFO);
+          if (unc[d.fine[e]]) {
+            ++hp.n_skipped_pairs;
+            continue;
+          }
+          push(d.fine[e], kTFO);
         }
       }
       er.count = (int32_t)((int64_t)hp.entries.size() - er.begin);
     }
 
-    // tasks: 128-row tiles, longest first (LPT) for the persistent kernel
+    // tasks: 128-row tiles; staging slots for kSYM column sums are assigned in
+    // (box, row tile, entry) order so every receiver adds them in a fixed order
     {
+      std::vector<std::vector<std::pair<int64_t, int64_t>>> inbox(hp.symmetric ? nb : 0);
       std::vector<std::pair<double, Task>> tv;
+      int64_t cursor = 0;
       for (int32_t b = 0; b < nb; ++b) {
         const EntryRange& er = hp.ent_range[b];
         if (er.count == 0 || hp.box[b].n == 0) continue;
         double src = 0;
-        for (int64_t e = er.begin; e < er.begin + er.count; ++e) src += hp.box[hp.entries[e] >> 2].n;
+        for (int64_t e = er.begin; e < er.begin + er.count; ++e) {
+          const int32_t code = hp.entries[e];
+          const double w = (code & kModeMask) == kSYM ? 1.15 : 1.0;  // extra column accumulate
+          src += w * hp.box[code >> kModeBits].n;
+        }
         for (int32_t r0 = 0; r0 < hp.box[b].n; r0 += kTileRows) {
-          Task t{b, r0, std::min(kTileRows, hp.box[b].n - r0), 0};
+          Task t{b, r0, std::min(kTileRows, hp.box[b].n - r0), 0, cursor};
+          const bool skel_rows = r0 < hp.box[b].k;
+          for (int64_t e = er.begin; e < er.begin + er.count; ++e) {
+            const int32_t code = hp.entries[e];
+            if ((code & kModeMask) != kSYM) continue;
+            const int32_t c = code >> kModeBits;
+            const int64_t u_off = cursor;
+            cursor += hp.box[c].n;
+            int64_t h_off = -1;
+            if (skel_rows && hp.box[c].k > 0) {
+              h_off = cursor;
+              cursor += hp.box[c].k;
+            }
+            inbox[c].push_back({u_off, h_off});
+          }
           const double lanes_rows = 32.0 * ((t.nrows + 31) / 32);
           tv.push_back({lanes_rows * (src + 8.0), t});
         }
       }
+      hp.stage_size = cursor;
       std::stable_sort(tv.begin(), tv.end(),
                        [](const auto& a, const auto& b) { return a.first > b.first; });
       hp.tasks.reserve(tv.size());
       for (auto& e : tv) hp.tasks.push_back(e.second);
+      hp.recv_off.assign(1, 0);
+      for (int32_t c = 0; c < (int32_t)inbox.size(); ++c) {
+        if (inbox[c].empty()) continue;
+        hp.recv_box.push_back(c);
+        for (auto& uh : inbox[c]) {
+          hp.recv_u.push_back(uh.first);
+          hp.recv_h.push_back(uh.second);
+        }
+        hp.recv_off.push_back((int64_t)hp.recv_u.size());
+      }
     }
 
     // interpolation work lists per level (levels >= 2 carry T)
@@ -265,6 +347,13 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err) {
     err = "sfmm_gpu_plan_create: host allocation failed";
     return SFMM_ENOMEM;
   }
+}
+
+PlanOptions plan_options_from_env() {
+  PlanOptions o;
+  if (const char* v = std::getenv("SFMM_SYMMETRIC")) o.symmetric = std::atoi(v) != 0;
+  if (const char* v = std::getenv("SFMM_SKIP_CANCEL")) o.skip_cancel = std::atoi(v) != 0;
+  return o;
 }
 
 }  // namespace sfmm_gpu

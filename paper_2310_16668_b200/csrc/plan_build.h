@@ -51,8 +51,16 @@ struct HostPlan {
   std::vector<int32_t> leaf_orig;
   // translation CSR and tasks
   std::vector<EntryRange> ent_range;
-  std::vector<int32_t> entries;               // (src box << 2) | mode
+  std::vector<int32_t> entries;               // (src box << kModeBits) | mode
   std::vector<Task> tasks;
+  // symmetric colleague blocks: staged column sums and, per receiving box,
+  // the staging slots to add (u part, and uhat part or -1) in a fixed order
+  bool symmetric = false;
+  int64_t stage_size = 0;                     // doubles
+  std::vector<int32_t> recv_box;
+  std::vector<int64_t> recv_off;              // recv_box.size() + 1
+  std::vector<int64_t> recv_u, recv_h;
+  int64_t n_skipped_pairs = 0;                // cancelling pairs not evaluated
   // interpolation work lists, concatenated per level; *_lvl has depth+2 entries
   std::vector<LevelItem> up_items, down_items;
   std::vector<int64_t> up_lvl, down_lvl;
@@ -66,5 +74,13 @@ struct HostPlan {
 // Validates the descriptor and fills `hp`.  Returns SFMM_OK or an error code
 // with a message in `err`.
 int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err);
+
+// Plan options (environment SFMM_SYMMETRIC=0 / SFMM_SKIP_CANCEL=0 turn them off
+// for A/B measurements; both default on).
+struct PlanOptions {
+  bool symmetric = true;    // evaluate each off-diagonal colleague block once
+  bool skip_cancel = true;  // drop pairs whose add and subtract cancel exactly
+};
+PlanOptions plan_options_from_env();
 
 }  // namespace sfmm_gpu

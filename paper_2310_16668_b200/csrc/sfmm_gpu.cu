@@ -145,6 +145,7 @@ struct sfmm_gpu_plan {
       n += hp.down_lvl[l + 1] > hp.down_lvl[l] ? 1 : 0;
     }
     if (dp.n_tasks == 0) --n;
+    if (dp.n_recv > 0) ++n;  // k2b_reduce
     return n;
   }
 
@@ -210,6 +211,12 @@ int sfmm_gpu_plan_create(const sfmm_plan_desc* desc, int device, sfmm_gpu_plan**
       dp.T = p->upload(desc->T, (size_t)hp.T_off[hp.n_boxes] * sw);
       dp.up_items = p->upload(hp.up_items);
       dp.down_items = p->upload(hp.down_items);
+      dp.stage = p->alloc<double>((size_t)std::max<int64_t>(hp.stage_size, 1));
+      dp.n_recv = (int64_t)hp.recv_box.size();
+      dp.recv_box = p->upload(hp.recv_box);
+      dp.recv_off = p->upload(hp.recv_off);
+      dp.recv_u = p->upload(hp.recv_u);
+      dp.recv_h = p->upload(hp.recv_h);
       size_t max_r = 0, max_k = 0;
       for (const BoxRec& b : hp.box) {
         max_r = std::max<size_t>(max_r, (size_t)(b.n - b.k));
