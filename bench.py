@@ -49,7 +49,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=float, default=1e7)
+    # (not --n: torchrun's own parser would take it for --nnodes/--nproc-per-node)
+    ap.add_argument("--points", dest="n", type=float, default=1e7)
     ap.add_argument("--dist", default="cube")
     ap.add_argument("--kernel", default="laplace3d", choices=list(KERNELS))
     ap.add_argument("--kappa", type=float, default=10.0)
@@ -61,6 +62,8 @@ def parse():
                          "instance, or skipped")
     ap.add_argument("--ref-n", type=float, default=1e6,
                     help="instance size of one --impl reference step / the 'sample' cpu baseline")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="multi-rank exchange; gloo stages through host memory (test path)")
     return ap.parse_args()
 
 
@@ -176,11 +179,190 @@ def run_reference(args, ws, rank):
     })
 
 
+def _share_descriptor(hp, path):
+    """Rank 0 writes the flat plan descriptor to node-local shared memory."""
+    from paper_2310_16668_b200._abi import DESC_SCALARS, PlanDescriptor
+    d = PlanDescriptor.from_struct(hp.desc_struct())
+    os.makedirs(path, exist_ok=True)
+    for name, a in d.arrays.items():
+        np.save(os.path.join(path, name + ".npy"), a)
+    with open(os.path.join(path, "scalars.json"), "w") as f:
+        json.dump({k: d.scalars[k] for k in DESC_SCALARS}, f)
+
+
+def _load_descriptor(path):
+    from paper_2310_16668_b200._abi import DESC_ARRAYS, PlanDescriptor
+    arrays = {n: np.load(os.path.join(path, n + ".npy"), mmap_mode="r") for n, _ in DESC_ARRAYS}
+    with open(os.path.join(path, "scalars.json")) as f:
+        scalars = json.load(f)
+    return PlanDescriptor(scalars, arrays)
+
+
+def run_sharded(args, ws, rank, local):
+    """--gpus N under torchrun: strong scaling of the N=1e7 headline apply over
+    N ranks, whole level-1 subtrees per rank, ghost all-to-all over NCCL
+    overlapped with the interior translations."""
+    import shutil
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2310_16668_b200 import api, host, shard
+
+    ndev = torch.cuda.device_count()
+    dev = local % max(1, ndev)
+    torch.cuda.set_device(dev)
+    if args.backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    else:
+        dist.init_process_group("gloo")
+    n = int(args.n)
+    kern = KERNELS[args.kernel]
+    cplx = kern == 3
+    path = f"/dev/shm/sfmm_bench_{os.environ.get('MASTER_PORT', '0')}"
+    t0 = time.perf_counter()
+    pts = host.generate_points(args.dist, n, 1)
+    q = (host.generate_charges_complex(n, 1 ^ CHARGE_STREAM) if cplx
+         else host.generate_charges(n, 1 ^ CHARGE_STREAM))
+    hp = None
+    hinfo = {}
+    if rank == 0:
+        # torchrun sets OMP_NUM_THREADS=1; the other ranks wait at the barrier
+        host.set_threads(os.cpu_count() or 1)
+        hp = host.HostPlan.build(kern, pts, args.leaf, args.tol, args.kappa)
+        hinfo = hp.info()
+        _share_descriptor(hp, path)
+    dist.barrier()
+    desc = hp.desc_struct() if rank == 0 else _load_descriptor(path)
+    t_pre = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    plan = shard.ShardedPlan(desc, ws, rank, device=dev)
+    t_upload = time.perf_counter() - t0
+    dist.barrier()
+    if rank == 0:
+        shutil.rmtree(path, ignore_errors=True)
+
+    dtype = torch.complex128 if cplx else torch.float64
+    q_host = torch.from_numpy(q)
+    q_dev = q_host.to(f"cuda:{dev}")
+    u_dev = torch.zeros_like(q_dev)
+    stream = torch.cuda.Stream(dev)
+    comm = torch.cuda.Stream(dev)
+    if args.backend != "nccl":
+        # test path (several ranks on one GPU): exchange through host memory
+        def exchange_apply():
+            send, recv = plan.buffers()
+            plan.begin(q_dev, stream.cuda_stream, 0)
+            stream.synchronize()
+            s_cpu = send[: int(plan.send_counts.sum())].cpu()
+            r_cpu = torch.empty(int(plan.recv_counts.sum()), dtype=torch.float64)
+            dist.all_to_all_single(r_cpu, s_cpu, output_split_sizes=[int(x) for x in plan.recv_counts],
+                                   input_split_sizes=[int(x) for x in plan.send_counts])
+            recv[: r_cpu.numel()].copy_(r_cpu)
+            torch.cuda.synchronize(dev)
+            plan.end(q_dev, u_dev, stream.cuda_stream)
+    else:
+        def exchange_apply():
+            shard.apply_distributed(plan, q_dev, u_dev, stream=stream, comm_stream=comm)
+    torch.cuda.synchronize(dev)
+    for _ in range(args.warmup):
+        exchange_apply()
+    torch.cuda.synchronize(dev)
+
+    clocks = ClockSampler(dev)
+    clocks.start()
+    time.sleep(0.2)
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        exchange_apply()
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    clk = clocks.stop()
+    ms_local = ev0.elapsed_time(ev1) / args.steps
+    tt = torch.tensor([ms_local], dtype=torch.float64, device=f"cuda:{dev}" if args.backend == "nccl" else "cpu")
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    ms_step = float(tt.item())
+    value = n / (ms_step * 1e-3) / 1e6
+
+    # e2e: pinned q -> device, apply, device u -> pinned host, every step
+    q_pin = torch.empty(q_host.shape, dtype=dtype).pin_memory()
+    q_pin.copy_(q_host)
+    u_pin = torch.empty(q_host.shape, dtype=dtype).pin_memory()
+    e2e_steps = max(3, min(args.steps, 10))
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        with torch.cuda.stream(stream):
+            q_dev.copy_(q_pin, non_blocking=True)
+        exchange_apply()
+        with torch.cuda.stream(stream):
+            u_pin.copy_(u_dev, non_blocking=True)
+        stream.synchronize()
+    t_e2e = (time.perf_counter() - t0) / e2e_steps
+    te = torch.tensor([t_e2e], dtype=torch.float64, device=tt.device)
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    t_e2e = float(te.item())
+
+    # accuracy: assemble the owned slices (all other entries are zero)
+    if args.backend == "nccl":
+        dist.all_reduce(u_dev, op=dist.ReduceOp.SUM)
+        u_full = u_dev.cpu().numpy()
+    else:
+        uc = u_dev.cpu()
+        dist.all_reduce(uc, op=dist.ReduceOp.SUM)
+        u_full = uc.numpy()
+    out = None
+    if rank == 0:
+        rng = np.random.default_rng(0xC2B2AE3D27D4EB4F)
+        targets = np.sort(rng.choice(n, size=min(args.check_targets, n), replace=False)).astype(np.int32)
+        ref_t = api.direct_sum_subset(kern, args.kappa, pts, q, targets, device=dev)
+        relerr_direct = api.max_rel_err(u_full[targets], ref_t)
+        bytes_col = n * (16 if cplx else 8)
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference generators: points seed 1, charges seed 1^0x9e3779b97f4a7c15)",
+            "config": {
+                "workload": f"{args.kernel} {args.dist} N={n:.0e} leaf={args.leaf} tol={args.tol} nrhs=1",
+                "n_points": n, "leaf_cap": args.leaf, "tol": args.tol, "nrhs": 1,
+                "parallelism": f"level-1 subtree sharding x{ws}, ghost all-to-all over {args.backend}",
+                "l2": "inputs larger than L2",
+            },
+            "roofline": None,
+            "roofline_note": "per-kernel roofline is reported by the 1-GPU line",
+            "e2e": {"value": n / t_e2e / 1e6, "unit": UNIT, "h2d_bytes_per_step": bytes_col * ws,
+                    "d2h_bytes_per_step": bytes_col * ws, "ms_per_step": t_e2e * 1e3},
+            "gpu_launches": None,
+            "clocks": clk,
+            "relerr_vs_direct": relerr_direct, "n_check": int(targets.size),
+            "shard": {"ghost_boxes_rank0": plan.n_ghost_boxes,
+                      "owned_points_rank0": plan.n_owned_points,
+                      "send_mb_rank0": float(plan.send_counts.sum()) * 8 / 1e6},
+            "precompute": {"t_total_s": t_pre, "t_upload_s": t_upload, **{k: hinfo.get(k) for k in
+                           ("depth", "n_boxes", "k_max", "t_tree", "t_skel")}},
+            "cpu_baseline": {"value": None, "unit": UNIT, "cores": None, "kind": "reference",
+                             "sample": "reported by the 1-GPU run (rank 0 at N=1 only)"},
+        }
+        emit(out)
+    plan.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def main():
     args = parse()
     ws, rank, local = dist_env()
     if args.impl == "reference":
         run_reference(args, ws, rank)
+        return
+    if ws > 1:
+        run_sharded(args, ws, rank, local)
         return
 
     import torch

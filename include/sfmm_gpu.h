@@ -156,6 +156,45 @@ int sfmm_gpu_plan_info_get(const sfmm_gpu_plan* plan, sfmm_gpu_plan_info* info);
 
 void sfmm_gpu_plan_destroy(sfmm_gpu_plan* plan);
 
+/*
+ * Multi-GPU (one process per GPU).  Rank `rank` of `n_ranks` owns whole
+ * level-1 subtrees (Morton-contiguous; assigned by estimated translation cost)
+ * and builds its plan from the SAME full descriptor as every other rank.  One
+ * apply is
+ *   sfmm_gpu_apply_begin   gather + upward pass of the owned subtrees, pack the
+ *                          ghost boxes other ranks read (q and qhat) into
+ *                          send_dev, record `packed_event`, then start the
+ *                          translation tasks that read no ghost box;
+ *   (caller)               all-to-all of send_dev -> recv_dev with the per-peer
+ *                          counts of sfmm_gpu_shard_info (scalars; NCCL over
+ *                          NVLink, overlapped with the interior translations);
+ *   sfmm_gpu_apply_end     unpack ghosts, boundary translation tasks, staged
+ *                          column sums, downward pass, scatter of the OWNED
+ *                          points into u_dev (other entries untouched).
+ * q_dev holds all N charges (original order) on every rank.  The union over
+ * ranks of the owned entries of u is the full result.  Trees with depth < 2
+ * are computed by rank 0 alone.  Replaces nothing in the reference, which is
+ * single-process (SPEC non-goal); see DESIGN.md section 6.
+ */
+int sfmm_gpu_plan_create_sharded(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
+                                 sfmm_gpu_plan** out);
+int sfmm_gpu_shard_info(const sfmm_gpu_plan* plan, int64_t* send_counts, int64_t* recv_counts,
+                        int64_t* n_owned_points, int64_t* n_ghost_boxes);
+int sfmm_gpu_apply_begin(sfmm_gpu_plan* plan, const void* q_dev, void* send_dev, void* stream,
+                         void* packed_event);
+int sfmm_gpu_apply_end(sfmm_gpu_plan* plan, const void* q_dev, const void* recv_dev, void* u_dev,
+                       void* stream);
+
+/* Host-only view of rank `rank`'s shard (no device is touched).  counts gets
+ * 2*n_ranks + 3 values: send scalars per peer, receive scalars per peer,
+ * owned points, ghost boxes, owned boxes.  Non-NULL arrays receive the box
+ * owners (n_boxes), the ghost-exchange element indices into [q slots | qhat]
+ * (pack_idx: what this rank sends, per peer in rank order; unpack_idx: where
+ * what it receives lands) and the owned points' original indices. */
+int sfmm_gpu_shard_describe(const sfmm_plan_desc* desc, int n_ranks, int rank, int64_t* counts,
+                            int32_t* owner, int64_t* pack_idx, int64_t* unpack_idx,
+                            int32_t* owned_points);
+
 /* Phase timing.  While enabled, every apply records CUDA events on its stream
  * around its five phases (0 gather, 1 upward, 2 translate, 3 downward,
  * 4 scatter).  sfmm_gpu_get_timings synchronises, writes ms[5*i + phase] for

@@ -268,6 +268,18 @@ def gpu_lib() -> C.CDLL:
     lib.sfmm_gpu_get_timings.restype = C.c_int
     lib.sfmm_gpu_fp64_peak.argtypes = [C.c_int, C.POINTER(C.c_double)]
     lib.sfmm_gpu_fp64_peak.restype = C.c_int
+    lib.sfmm_gpu_plan_create_sharded.argtypes = [C.POINTER(PlanDesc), C.c_int, C.c_int, C.c_int,
+                                                 C.POINTER(vp)]
+    lib.sfmm_gpu_plan_create_sharded.restype = C.c_int
+    lib.sfmm_gpu_shard_info.argtypes = [vp, vp, vp, vp, vp]
+    lib.sfmm_gpu_shard_info.restype = C.c_int
+    lib.sfmm_gpu_apply_begin.argtypes = [vp, vp, vp, vp, vp]
+    lib.sfmm_gpu_apply_begin.restype = C.c_int
+    lib.sfmm_gpu_apply_end.argtypes = [vp, vp, vp, vp, vp]
+    lib.sfmm_gpu_apply_end.restype = C.c_int
+    lib.sfmm_gpu_shard_describe.argtypes = [C.POINTER(PlanDesc), C.c_int, C.c_int, vp, vp, vp, vp,
+                                            vp]
+    lib.sfmm_gpu_shard_describe.restype = C.c_int
     _gpu_lib = lib
     return lib
 
@@ -276,5 +288,6 @@ GPU_SYMBOLS = [
     "sfmm_gpu_plan_create", "sfmm_gpu_apply", "sfmm_gpu_apply_async", "sfmm_gpu_check_status",
     "sfmm_gpu_plan_info_get", "sfmm_gpu_plan_destroy", "sfmm_gpu_direct_sum",
     "sfmm_gpu_last_error", "sfmm_gpu_version", "sfmm_gpu_set_timing", "sfmm_gpu_get_timings",
-    "sfmm_gpu_fp64_peak",
+    "sfmm_gpu_fp64_peak", "sfmm_gpu_plan_create_sharded", "sfmm_gpu_shard_info",
+    "sfmm_gpu_apply_begin", "sfmm_gpu_apply_end", "sfmm_gpu_shard_describe",
 ]

@@ -498,39 +498,49 @@ int configure_translate(DevPlan& p, int device) {
   return 0;
 }
 
-void launch_translate(const DevPlan& p, DevState& s, cudaStream_t st) {
-  if (p.n_tasks == 0) return;
-  K2Args a;
-  a.box = p.box;
-  a.er = p.ent_range;
-  a.ent = p.entries;
-  a.tasks = p.tasks;
-  a.n_tasks = p.n_tasks;
-  a.X = p.X;
-  a.Y = p.Y;
-  a.Z = p.Z;
-  a.sid = p.slot_id;
-  a.Q = s.Q;
-  a.QH = s.QH;
-  a.U = s.U;
-  a.UH = s.UH;
-  a.counter = p.counter;
-  a.err = p.err_flag;
-  a.kappa = p.kappa;
-  a.St = p.stage;
-  // boxes whose every entry cancels own no task: their U/UH stay zero
+void launch_translate(const DevPlan& p, DevState& s, cudaStream_t st, TranslatePart part) {
   const size_t sw = p.cplx ? 16 : 8;
-  cudaMemsetAsync(s.U, 0, (size_t)p.n_slots * sw, st);
-  cudaMemsetAsync(s.UH, 0, (size_t)p.n_skel * sw, st);
-  cudaMemsetAsync(p.counter, 0, sizeof(int), st);
-  const int grid = (int)std::min<int64_t>(p.k2_grid, (p.n_tasks + kWarps - 1) / kWarps);
-  if (p.kernel == SFMM_HELMHOLTZ3D)
-    k2_translate_cplx<<<grid, kThreads, 0, st>>>(a);
-  else if (p.kernel == SFMM_LAPLACE3D)
-    k2_translate_real<GenLaplace3d><<<grid, kThreads, 0, st>>>(a);
-  else
-    k2_translate_real<GenLaplace2d><<<grid, kThreads, 0, st>>>(a);
-  if (p.n_recv > 0) {
+  if (part != kBoundaryTasks) {
+    // boxes whose every entry cancels own no task: their U/UH stay zero
+    cudaMemsetAsync(s.U, 0, (size_t)p.n_slots * sw, st);
+    cudaMemsetAsync(s.UH, 0, (size_t)p.n_skel * sw, st);
+  }
+  int64_t t0 = 0, t1 = p.n_tasks;
+  int* counter = p.counter;
+  if (part == kInteriorTasks) t1 = p.n_interior;
+  if (part == kBoundaryTasks) {
+    t0 = p.n_interior;
+    counter = p.counter + 1;
+  }
+  if (t1 > t0) {
+    K2Args a;
+    a.box = p.box;
+    a.er = p.ent_range;
+    a.ent = p.entries;
+    a.tasks = p.tasks + t0;
+    a.n_tasks = t1 - t0;
+    a.X = p.X;
+    a.Y = p.Y;
+    a.Z = p.Z;
+    a.sid = p.slot_id;
+    a.Q = s.Q;
+    a.QH = s.QH;
+    a.U = s.U;
+    a.UH = s.UH;
+    a.counter = counter;
+    a.err = p.err_flag;
+    a.kappa = p.kappa;
+    a.St = p.stage;
+    cudaMemsetAsync(counter, 0, sizeof(int), st);
+    const int grid = (int)std::min<int64_t>(p.k2_grid, (t1 - t0 + kWarps - 1) / kWarps);
+    if (p.kernel == SFMM_HELMHOLTZ3D)
+      k2_translate_cplx<<<grid, kThreads, 0, st>>>(a);
+    else if (p.kernel == SFMM_LAPLACE3D)
+      k2_translate_real<GenLaplace3d><<<grid, kThreads, 0, st>>>(a);
+    else
+      k2_translate_real<GenLaplace2d><<<grid, kThreads, 0, st>>>(a);
+  }
+  if (part != kInteriorTasks && p.n_recv > 0) {
     const double scale = p.kernel == SFMM_LAPLACE3D ? GenLaplace3d::kScale : GenLaplace2d::kScale;
     k2b_reduce<<<(unsigned)p.n_recv, 256, 0, st>>>(p.box, p.recv_box, p.recv_off, p.recv_u,
                                                    p.recv_h, p.stage, s.U, s.UH, scale);

@@ -277,23 +277,23 @@ int grid_for(int64_t n, int threads) {
 }  // namespace
 
 void launch_gather(const DevPlan& p, const double* q, DevState& s, cudaStream_t st) {
-  const int g = grid_for(p.n_points, 256);
+  const int g = grid_for(p.n_owned_points, 256);
   if (p.cplx)
-    k0_gather<double2><<<g, 256, 0, st>>>(p.leaf_slot, p.leaf_orig, p.n_points,
+    k0_gather<double2><<<g, 256, 0, st>>>(p.leaf_slot, p.leaf_orig, p.n_owned_points,
                                           reinterpret_cast<const double2*>(q),
                                           reinterpret_cast<double2*>(s.Q));
   else
-    k0_gather<double><<<g, 256, 0, st>>>(p.leaf_slot, p.leaf_orig, p.n_points, q, s.Q);
+    k0_gather<double><<<g, 256, 0, st>>>(p.leaf_slot, p.leaf_orig, p.n_owned_points, q, s.Q);
 }
 
 void launch_scatter(const DevPlan& p, const DevState& s, double* u, cudaStream_t st) {
-  const int g = grid_for(p.n_points, 256);
+  const int g = grid_for(p.n_owned_points, 256);
   if (p.cplx)
-    k4_scatter<double2><<<g, 256, 0, st>>>(p.leaf_slot, p.leaf_orig, p.n_points,
+    k4_scatter<double2><<<g, 256, 0, st>>>(p.leaf_slot, p.leaf_orig, p.n_owned_points,
                                            reinterpret_cast<const double2*>(s.U),
                                            reinterpret_cast<double2*>(u));
   else
-    k4_scatter<double><<<g, 256, 0, st>>>(p.leaf_slot, p.leaf_orig, p.n_points, s.U, u);
+    k4_scatter<double><<<g, 256, 0, st>>>(p.leaf_slot, p.leaf_orig, p.n_owned_points, s.U, u);
 }
 
 void launch_upward(const DevPlan& p, const HostPlan& hp, int level, DevState& s,
@@ -336,6 +336,51 @@ void launch_direct_subset(int kernel, double kappa, int dim, int64_t n, const do
   k5_direct_subset<<<(unsigned)nt, 256, 0, st>>>(kernel, kappa, dim,
                                                  kernel == SFMM_HELMHOLTZ3D ? 1 : 0, n, pts, q,
                                                  targets, u, err_flag);
+}
+
+namespace {
+
+// Ghost exchange: element i of the buffer <-> [Q | QH][idx[i]] (QH addressed
+// from n_slots on).  One thread per element, coalesced on the buffer side.
+template <class S, bool kPack>
+__global__ void k_exchange(const int64_t* __restrict__ idx, int64_t n, int64_t n_slots,
+                           S* __restrict__ Q, S* __restrict__ QH, S* __restrict__ buf) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = idx[i];
+    S* p = k < n_slots ? Q + k : QH + (k - n_slots);
+    if (kPack)
+      buf[i] = *p;
+    else
+      *p = buf[i];
+  }
+}
+
+}  // namespace
+
+void launch_pack(const DevPlan& p, const DevState& s, double* buf, cudaStream_t st) {
+  if (p.n_pack == 0) return;
+  const int g = grid_for(p.n_pack, 256);
+  if (p.cplx)
+    k_exchange<double2, true><<<g, 256, 0, st>>>(p.pack_idx, p.n_pack, p.n_slots,
+                                                  reinterpret_cast<double2*>(s.Q),
+                                                  reinterpret_cast<double2*>(s.QH),
+                                                  reinterpret_cast<double2*>(buf));
+  else
+    k_exchange<double, true><<<g, 256, 0, st>>>(p.pack_idx, p.n_pack, p.n_slots, s.Q, s.QH, buf);
+}
+
+void launch_unpack(const DevPlan& p, DevState& s, const double* buf, cudaStream_t st) {
+  if (p.n_unpack == 0) return;
+  const int g = grid_for(p.n_unpack, 256);
+  double* b = const_cast<double*>(buf);
+  if (p.cplx)
+    k_exchange<double2, false><<<g, 256, 0, st>>>(p.unpack_idx, p.n_unpack, p.n_slots,
+                                                   reinterpret_cast<double2*>(s.Q),
+                                                   reinterpret_cast<double2*>(s.QH),
+                                                   reinterpret_cast<double2*>(b));
+  else
+    k_exchange<double, false><<<g, 256, 0, st>>>(p.unpack_idx, p.n_unpack, p.n_slots, s.Q, s.QH, b);
 }
 
 int configure_tree_kernels(DevPlan& p, size_t max_r, size_t max_k) {

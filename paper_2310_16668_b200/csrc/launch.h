@@ -28,6 +28,7 @@ struct DevPlan {
   int32_t* entries;
   Task* tasks;
   int64_t n_tasks;
+  int64_t n_interior;  // tasks[0, n_interior) read no ghost box
   double *X, *Y, *Z;
   int32_t* slot_id;
   int64_t* up_dst;
@@ -41,7 +42,11 @@ struct DevPlan {
   int32_t* recv_box;
   int64_t *recv_off, *recv_u, *recv_h;
   int64_t n_recv;
-  int* counter;     // K2 task counter (reset per launch)
+  int64_t* pack_idx;    // ghost exchange element indices into [Q | QH]
+  int64_t* unpack_idx;
+  int64_t n_pack, n_unpack;
+  int64_t n_owned_points;  // entries of leaf_slot / leaf_orig
+  int* counter;     // K2 task counters (interior, boundary; reset per launch)
   int* err_flag;    // sticky duplicate-point flag
   int k2_grid;      // persistent K2 CTAs
   size_t up_smem, down_smem;
@@ -51,8 +56,14 @@ struct DevPlan {
 void launch_gather(const DevPlan& p, const double* q, DevState& s, cudaStream_t st);
 // K1: one tree level of the upward pass (level >= 2)
 void launch_upward(const DevPlan& p, const HostPlan& hp, int level, DevState& s, cudaStream_t st);
-// K2: fused ifo/ifs/tfo/level-1 translation, all levels in one launch
-void launch_translate(const DevPlan& p, DevState& s, cudaStream_t st);
+// K2: fused ifo/ifs/tfo/level-1 translation, all levels in one launch (or the
+// interior / boundary halves of a sharded plan), followed by K2b
+enum TranslatePart { kAllTasks, kInteriorTasks, kBoundaryTasks };
+void launch_translate(const DevPlan& p, DevState& s, cudaStream_t st,
+                      TranslatePart part = kAllTasks);
+// ghost exchange: buf[i] = [Q | QH][pack_idx[i]]  /  [Q | QH][unpack_idx[i]] = buf[i]
+void launch_pack(const DevPlan& p, const DevState& s, double* buf, cudaStream_t st);
+void launch_unpack(const DevPlan& p, DevState& s, const double* buf, cudaStream_t st);
 // K3: one tree level of the downward pass (level >= 2)
 void launch_downward(const DevPlan& p, const HostPlan& hp, int level, DevState& s,
                      cudaStream_t st);

@@ -18,7 +18,15 @@ struct Fail {
 
 }  // namespace
 
-int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err) {
+PlanOptions plan_options_from_env() {
+  PlanOptions o;
+  if (const char* v = std::getenv("SFMM_SYMMETRIC")) o.symmetric = std::atoi(v) != 0;
+  if (const char* v = std::getenv("SFMM_SKIP_CANCEL")) o.skip_cancel = std::atoi(v) != 0;
+  return o;
+}
+
+int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int n_ranks,
+                    int rank) {
   try {
     if (d.kernel == SFMM_HELMHOLTZ2D)
       throw Fail{SFMM_EUNSUPPORTED,
@@ -29,6 +37,7 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err) {
     if (d.dim != want_dim) bad("kernel dimension mismatch");  // make_plan, apply.cpp:73
     if (d.n_points < 1) bad("empty point set");
     if (d.n_boxes < 1 || d.depth < 0) bad("empty tree");
+    if (n_ranks < 1 || rank < 0 || rank >= n_ranks) bad("bad rank / world size");
     if (!d.pts || !d.perm || !d.level_begin || !d.box_parent || !d.box_level || !d.box_begin ||
         !d.box_end || !d.box_leaf || !d.box_parent_offset || !d.iv_off || !d.sk_off ||
         !d.rd_off || !d.T_off || !d.coll_off || !d.coarse_off || !d.fine_off)
@@ -41,6 +50,8 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err) {
     hp.n_points = d.n_points;
     hp.n_boxes = d.n_boxes;
     hp.depth = d.depth;
+    hp.n_ranks = n_ranks;
+    hp.rank = rank;
     const int64_t N = d.n_points;
     const int32_t nb = d.n_boxes;
     const int dim = d.dim;
@@ -54,10 +65,12 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err) {
 
     if (d.depth < 2) {
       // fmm_apply falls back to the dense sum on the original order
-      // (apply.cpp:316-328); only coordinates are needed.
+      // (apply.cpp:316-328); only coordinates are needed.  Sharded: rank 0
+      // owns every point.
       hp.orig_pts.resize(N * dim);
       for (int64_t t = 0; t < N; ++t)
         for (int k = 0; k < dim; ++k) hp.orig_pts[(int64_t)d.perm[t] * dim + k] = d.pts[t * dim + k];
+      hp.n_owned_points = rank == 0 ? N : 0;
       return SFMM_OK;
     }
 
@@ -72,14 +85,15 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err) {
     check_csr(d.coll_off, d.coll, "colleague");
     check_csr(d.coarse_off, d.coarse, "coarse");
     check_csr(d.fine_off, d.fine, "fine");
-    for (int32_t b = 0; b < nb; ++b)
+    for (int32_t b = 0; b < nb; ++b) {
       if (d.box_parent[b] < -1 || d.box_parent[b] >= nb || (b > 0 && d.box_parent[b] < 0))
         bad("box parent out of range");
+      if (b > 0 && d.box_parent[b] >= b) bad("parents must precede children (level-major order)");
+    }
 
     hp.box.resize(nb);
     hp.box_parent.assign(d.box_parent, d.box_parent + nb);
     hp.box_level.assign(d.box_level, d.box_level + nb);
-    hp.T_off.assign(d.T_off, d.T_off + nb + 1);
     hp.n_slots = d.iv_off[nb];
     hp.n_skel = d.sk_off[nb];
     const int64_t S = hp.n_slots;
@@ -122,7 +136,8 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err) {
       hp.m_proj += k * r;
     }
 
-    // slot coordinates and ids
+    // slot coordinates and ids (every rank keeps the full static geometry so
+    // ghost boxes need no remapping)
     hp.X.resize(S);
     hp.Y.resize(S);
     hp.Z.assign(S, 0.0);
@@ -154,12 +169,47 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err) {
         hp.up_dst[hp.box[b].skel + i] = d.iv_off[p] + posmap[d.iv_off[p] + off + i];
     }
 
-    // leaf gather/scatter maps: slot of position i <-> q[perm[begin + i]]
+    // ---- ownership: whole level-1 subtrees per rank ----------
+    const PlanOptions opt = plan_options_from_env();
+    std::vector<uint8_t> unc(nb, 0);
+    for (int32_t b = 0; b < nb; ++b)
+      unc[b] = opt.skip_cancel && d.box_level[b] >= 2 && hp.box[b].n > 0 &&
+               hp.box[b].k == hp.box[b].n;
+    const int32_t l1b = hp.level_begin[1], l1e = hp.level_begin[2];
+    hp.owner.assign(nb, 0);
+    if (n_ranks > 1) {
+      const int32_t n1 = l1e - l1b;
+      if (n_ranks > n1)
+        throw Fail{SFMM_EUNSUPPORTED, "sfmm_gpu_plan_create: more ranks than level-1 boxes"};
+      // estimated translation cost of every level-1 subtree
+      std::vector<double> cost(nb, 0.0);
+      for (int32_t b = nb - 1; b >= 1; --b) {
+        double src = 0;
+        for (int64_t e = d.coll_off[b]; e < d.coll_off[b + 1]; ++e) src += hp.box[d.coll[e]].n;
+        for (int64_t e = d.coarse_off[b]; e < d.coarse_off[b + 1]; ++e) src += hp.box[d.coarse[e]].n;
+        for (int64_t e = d.fine_off[b]; e < d.fine_off[b + 1]; ++e) src += hp.box[d.fine[e]].n;
+        cost[b] += (double)hp.box[b].n * src + 64.0 * hp.box[b].n;
+        if (d.box_parent[b] > 0) cost[d.box_parent[b]] += cost[b];
+      }
+      std::vector<int32_t> ord(n1);
+      std::iota(ord.begin(), ord.end(), l1b);
+      std::stable_sort(ord.begin(), ord.end(),
+                       [&](int32_t x, int32_t y) { return cost[x] > cost[y]; });
+      std::vector<double> load(n_ranks, 0.0);
+      for (int32_t b : ord) {
+        const int r = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+        hp.owner[b] = r;
+        load[r] += cost[b];
+      }
+      for (int32_t b = l1e; b < nb; ++b) hp.owner[b] = hp.owner[d.box_parent[b]];
+    }
+    auto mine = [&](int32_t b) { return hp.owner[b] == rank; };
+
+    // leaf gather/scatter maps (owned leaves): slot of position i <-> q[perm[begin + i]]
     // (apply.cpp:125, :301)
-    hp.leaf_slot.reserve(N);
-    hp.leaf_orig.reserve(N);
     {
       std::vector<uint8_t> hit(N, 0);
+      int64_t covered = 0;
       for (int32_t b = 0; b < nb; ++b) {
         if (!d.box_leaf[b]) continue;
         const int64_t s0 = d.iv_off[b];
@@ -170,16 +220,19 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err) {
           hit[t] = 1;
           tmp[i] = {s0 + posmap[s0 + i], d.perm[t]};
         }
+        covered += hp.box[b].n;
+        if (!mine(b)) continue;
         std::sort(tmp.begin(), tmp.end());
         for (auto& e : tmp) {
           hp.leaf_slot.push_back(e.first);
           hp.leaf_orig.push_back(e.second);
         }
       }
-      if ((int64_t)hp.leaf_slot.size() != N) bad("leaves do not cover every point");
+      if (covered != N) bad("leaves do not cover every point");
+      hp.n_owned_points = (int64_t)hp.leaf_slot.size();
     }
 
-    // translation CSR (all four phases, one list per target box).
+    // ---- translation entries --------------------------------------------
     //
     // Exact cancellations (in exact arithmetic) are dropped: for a box that is
     // uncompressed (level >= 2, k = n, so S = B and qhat = q) the dense add and
@@ -188,14 +241,10 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err) {
     // is uncompressed cancels within the entry (apply.cpp:228-234).  The pair
     // counts (ApplyStats) still count them.
     //
-    // With `symmetric`, an ifo pair of distinct colleagues b < c is evaluated
-    // once (kSYM in b's list): b's rows are accumulated as usual and c's rows
-    // receive A_cb q_b = (A_bc)^T q_b as staged column sums.
-    const PlanOptions opt = plan_options_from_env();
-    std::vector<uint8_t> unc(nb, 0);
-    for (int32_t b = 0; b < nb; ++b)
-      unc[b] = opt.skip_cancel && d.box_level[b] >= 2 && hp.box[b].n > 0 &&
-               hp.box[b].k == hp.box[b].n;
+    // With `symmetric`, an ifo pair of distinct colleagues b < c owned by the
+    // same rank is evaluated once (kSYM in b's list): b's rows are accumulated
+    // as usual and c's rows receive A_cb q_b = (A_bc)^T q_b as staged column
+    // sums.  Pairs across ranks stay kIFO on both sides.
     hp.symmetric = opt.symmetric && !hp.cplx;
     if (hp.symmetric) {  // the colleague relation must be symmetric to stage
       for (int32_t b = 0; b < nb && hp.symmetric; ++b)
@@ -209,11 +258,25 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err) {
           }
         }
     }
-    hp.ent_range.resize(nb);
-    const int32_t l1b = hp.level_begin[1], l1e = hp.level_begin[2];
+    // sources(b, f): every (source, mode) evaluated for target b, before the
+    // symmetric folding; identical on every rank.
+    auto sources = [&](int32_t b, auto&& f) {
+      const int lev = d.box_level[b];
+      if (lev >= 2) {
+        for (int64_t e = d.coll_off[b]; e < d.coll_off[b + 1]; ++e)
+          if (!(unc[b] && unc[d.coll[e]])) f(d.coll[e], (int)kIFO);
+        if (!unc[b])
+          for (int64_t e = d.coarse_off[b]; e < d.coarse_off[b + 1]; ++e) f(d.coarse[e], (int)kIFS);
+      }
+      if (lev == 1)
+        for (int32_t c = l1b; c < l1e; ++c) f(c, (int)kL1);
+      if (d.box_leaf[b] && lev >= 1)
+        for (int64_t e = d.fine_off[b]; e < d.fine_off[b + 1]; ++e)
+          if (!unc[d.fine[e]]) f(d.fine[e], (int)kTFO);
+    };
+
+    // global pair counts and work (ApplyStats, roofline): every target
     for (int32_t b = 0; b < nb; ++b) {
-      EntryRange& er = hp.ent_range[b];
-      er.begin = (int64_t)hp.entries.size();
       const int lev = d.box_level[b];
       auto count = [&](int32_t c, int mode) {
         const double nbn = hp.box[b].n, ncn = hp.box[c].n;
@@ -222,58 +285,92 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err) {
         if (mode == kIFS) hp.p_skel += (double)hp.box[b].k * ncn;
         if (mode == kTFO) hp.p_skel += nbn * hp.box[c].k;
       };
-      auto push = [&](int32_t c, int mode) { hp.entries.push_back((c << kModeBits) | mode); };
       if (lev >= 2) {
         for (int64_t e = d.coll_off[b]; e < d.coll_off[b + 1]; ++e) {
-          const int32_t c = d.coll[e];
           ++hp.n_ifo;
-          count(c, kIFO);
-          if (unc[b] && unc[c]) {
-            ++hp.n_skipped_pairs;
-            continue;
-          }
-          if (hp.symmetric && c != b) {
-            if (c > b) push(c, kSYM);  // c < b arrives through c's staged column sums
-          } else {
-            push(c, kIFO);
-          }
+          count(d.coll[e], kIFO);
+          hp.n_skipped_pairs += (unc[b] && unc[d.coll[e]]) ? 1 : 0;
         }
         for (int64_t e = d.coarse_off[b]; e < d.coarse_off[b + 1]; ++e) {
           ++hp.n_ifs;
           count(d.coarse[e], kIFS);
-          if (unc[b]) {
-            ++hp.n_skipped_pairs;
-            continue;
-          }
-          push(d.coarse[e], kIFS);
+          hp.n_skipped_pairs += unc[b] ? 1 : 0;
         }
       }
-      if (lev == 1) {
+      if (lev == 1)
         for (int32_t c = l1b; c < l1e; ++c) {
           ++hp.n_l1;
           count(c, kL1);
-          push(c, kL1);
         }
-      }
-      if (d.box_leaf[b] && lev >= 1) {
+      if (d.box_leaf[b] && lev >= 1)
         for (int64_t e = d.fine_off[b]; e < d.fine_off[b + 1]; ++e) {
           ++hp.n_tfo;
           count(d.fine[e], kTFO);
-          if (unc[d.fine[e]]) {
-            ++hp.n_skipped_pairs;
-            continue;
-          }
-          push(d.fine[e], kTFO);
+          hp.n_skipped_pairs += unc[d.fine[e]] ? 1 : 0;
         }
-      }
-      er.count = (int32_t)((int64_t)hp.entries.size() - er.begin);
     }
 
-    // tasks: 128-row tiles; staging slots for kSYM column sums are assigned in
-    // (box, row tile, entry) order so every receiver adds them in a fixed order
+    // this rank's CSR: owned targets only
+    hp.ent_range.resize(nb);
+    std::vector<uint8_t> boundary(nb, 0);
+    for (int32_t b = 0; b < nb; ++b) {
+      EntryRange& er = hp.ent_range[b];
+      er.begin = (int64_t)hp.entries.size();
+      er.count = 0;
+      if (!mine(b) || d.box_level[b] < 1) continue;
+      sources(b, [&](int32_t c, int mode) {
+        if (!mine(c)) boundary[b] = 1;
+        if (mode == kIFO && hp.symmetric && c != b && mine(c)) {
+          if (c > b) hp.entries.push_back((c << kModeBits) | kSYM);
+          return;  // c < b arrives through c's staged column sums
+        }
+        hp.entries.push_back((c << kModeBits) | mode);
+        hp.p_dense_local += (double)hp.box[b].n * hp.box[c].n;
+      });
+      er.count = (int32_t)((int64_t)hp.entries.size() - er.begin);
+      for (int64_t e = er.begin; e < er.begin + er.count; ++e)
+        if ((hp.entries[e] & kModeMask) == kSYM)
+          hp.p_dense_local += (double)hp.box[b].n * hp.box[hp.entries[e] >> kModeBits].n;
+    }
+
+    // ghost exchange lists: box c owned by p is sent to q if one of q's
+    // targets reads it.  Every rank derives the same lists.
+    if (n_ranks > 1) {
+      std::vector<std::vector<uint8_t>> need(n_ranks, std::vector<uint8_t>(nb, 0));
+      for (int32_t b = 0; b < nb; ++b) {
+        if (d.box_level[b] < 1) continue;
+        const int q = hp.owner[b];
+        sources(b, [&](int32_t c, int) {
+          if (hp.owner[c] != q) need[q][c] = 1;
+        });
+      }
+      hp.send_off.assign(n_ranks + 1, 0);
+      hp.recv_off_peer.assign(n_ranks + 1, 0);
+      const int64_t sk_base = S;  // QH entries are addressed as S + skel index
+      for (int p = 0; p < n_ranks; ++p) {
+        for (int32_t c = 0; c < nb; ++c) {
+          if (p != rank && need[p][c] && hp.owner[c] == rank) {  // I send c to p
+            for (int32_t i = 0; i < hp.box[c].n; ++i) hp.pack_idx.push_back(hp.box[c].slot + i);
+            for (int32_t i = 0; i < hp.box[c].k; ++i) hp.pack_idx.push_back(sk_base + hp.box[c].skel + i);
+          }
+          if (p != rank && need[rank][c] && hp.owner[c] == p) {  // p sends c to me
+            for (int32_t i = 0; i < hp.box[c].n; ++i) hp.unpack_idx.push_back(hp.box[c].slot + i);
+            for (int32_t i = 0; i < hp.box[c].k; ++i) hp.unpack_idx.push_back(sk_base + hp.box[c].skel + i);
+            ++hp.n_ghost_boxes;
+          }
+        }
+        hp.send_off[p + 1] = (int64_t)hp.pack_idx.size();
+        hp.recv_off_peer[p + 1] = (int64_t)hp.unpack_idx.size();
+      }
+    }
+
+    // tasks: 128-row tiles of owned targets; staging slots for kSYM column
+    // sums are assigned in (box, row tile, entry) order so every receiver adds
+    // them in a fixed order.  Interior tasks (no ghost source) come first so
+    // they can run while the ghost exchange is in flight.
     {
       std::vector<std::vector<std::pair<int64_t, int64_t>>> inbox(hp.symmetric ? nb : 0);
-      std::vector<std::pair<double, Task>> tv;
+      std::vector<std::pair<double, Task>> tv_int, tv_bnd;
       int64_t cursor = 0;
       for (int32_t b = 0; b < nb; ++b) {
         const EntryRange& er = hp.ent_range[b];
@@ -301,14 +398,17 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err) {
             inbox[c].push_back({u_off, h_off});
           }
           const double lanes_rows = 32.0 * ((t.nrows + 31) / 32);
-          tv.push_back({lanes_rows * (src + 8.0), t});
+          (boundary[b] ? tv_bnd : tv_int).push_back({lanes_rows * (src + 8.0), t});
         }
       }
       hp.stage_size = cursor;
-      std::stable_sort(tv.begin(), tv.end(),
-                       [](const auto& a, const auto& b) { return a.first > b.first; });
-      hp.tasks.reserve(tv.size());
-      for (auto& e : tv) hp.tasks.push_back(e.second);
+      auto by_cost = [](const auto& a, const auto& b) { return a.first > b.first; };
+      std::stable_sort(tv_int.begin(), tv_int.end(), by_cost);
+      std::stable_sort(tv_bnd.begin(), tv_bnd.end(), by_cost);
+      hp.tasks.reserve(tv_int.size() + tv_bnd.size());
+      for (auto& e : tv_int) hp.tasks.push_back(e.second);
+      hp.n_interior_tasks = (int64_t)tv_int.size();
+      for (auto& e : tv_bnd) hp.tasks.push_back(e.second);
       hp.recv_off.assign(1, 0);
       for (int32_t c = 0; c < (int32_t)inbox.size(); ++c) {
         if (inbox[c].empty()) continue;
@@ -321,7 +421,24 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err) {
       }
     }
 
-    // interpolation work lists per level (levels >= 2 carry T)
+    // interpolation work lists per level (owned boxes at levels >= 2 carry T);
+    // T is compacted to the owned boxes (T_off indexes the compact blob)
+    hp.T_off.assign(nb + 1, 0);
+    hp.T_runs.clear();
+    int64_t tcur = 0;
+    for (int32_t b = 0; b < nb; ++b) {
+      hp.T_off[b] = tcur;
+      const int64_t len = d.T_off[b + 1] - d.T_off[b];
+      if (len > 0 && mine(b)) {
+        if (!hp.T_runs.empty() && hp.T_runs.back().src + hp.T_runs.back().len == d.T_off[b] &&
+            hp.T_runs.back().dst + hp.T_runs.back().len == tcur)
+          hp.T_runs.back().len += len;
+        else
+          hp.T_runs.push_back({d.T_off[b], tcur, len});
+        tcur += len;
+      }
+    }
+    hp.T_off[nb] = tcur;
     hp.up_lvl.assign(d.depth + 2, 0);
     hp.down_lvl.assign(d.depth + 2, 0);
     for (int l = 0; l <= d.depth; ++l) {
@@ -329,6 +446,7 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err) {
       hp.down_lvl[l] = (int64_t)hp.down_items.size();
       if (l >= 2) {
         for (int32_t b = hp.level_begin[l]; b < hp.level_begin[l + 1]; ++b) {
+          if (!mine(b)) continue;
           const int32_t k = hp.box[b].k, r = hp.box[b].n - hp.box[b].k;
           if (k == 0) continue;
           for (int32_t i = 0; i < k; i += kUpRows) hp.up_items.push_back({b, i});
@@ -347,13 +465,6 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err) {
     err = "sfmm_gpu_plan_create: host allocation failed";
     return SFMM_ENOMEM;
   }
-}
-
-PlanOptions plan_options_from_env() {
-  PlanOptions o;
-  if (const char* v = std::getenv("SFMM_SYMMETRIC")) o.symmetric = std::atoi(v) != 0;
-  if (const char* v = std::getenv("SFMM_SKIP_CANCEL")) o.skip_cancel = std::atoi(v) != 0;
-  return o;
 }
 
 }  // namespace sfmm_gpu

@@ -61,6 +61,21 @@ struct HostPlan {
   std::vector<int64_t> recv_off;              // recv_box.size() + 1
   std::vector<int64_t> recv_u, recv_h;
   int64_t n_skipped_pairs = 0;                // cancelling pairs not evaluated
+  int64_t n_interior_tasks = 0;               // tasks[0, n_interior) read no ghost box
+  // sharding: owner rank of every box (whole level-1 subtrees)
+  int n_ranks = 1, rank = 0;
+  std::vector<int32_t> owner;
+  int64_t n_owned_points = 0;
+  double p_dense_local = 0;                   // dense pairs this rank evaluates
+  // ghost exchange: element indices into [Q | QH] (QH at offset n_slots),
+  // per peer ranges send_off[p]..send_off[p+1] / recv_off_peer[p]..
+  std::vector<int64_t> pack_idx, unpack_idx, send_off, recv_off_peer;
+  int64_t n_ghost_boxes = 0;
+  // owned interpolation blocks copied from the descriptor into a compact blob
+  struct Run {
+    int64_t src, dst, len;  // scalars
+  };
+  std::vector<Run> T_runs;
   // interpolation work lists, concatenated per level; *_lvl has depth+2 entries
   std::vector<LevelItem> up_items, down_items;
   std::vector<int64_t> up_lvl, down_lvl;
@@ -71,9 +86,11 @@ struct HostPlan {
   double p_dense = 0, p_skel = 0;
 };
 
-// Validates the descriptor and fills `hp`.  Returns SFMM_OK or an error code
-// with a message in `err`.
-int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err);
+// Validates the descriptor and fills `hp` for rank `rank` of `n_ranks`
+// (1/0: the whole tree).  Returns SFMM_OK or an error code with a message in
+// `err`.
+int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int n_ranks = 1,
+                    int rank = 0);
 
 // Plan options (environment SFMM_SYMMETRIC=0 / SFMM_SKIP_CANCEL=0 turn them off
 // for A/B measurements; both default on).

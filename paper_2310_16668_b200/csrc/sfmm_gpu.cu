@@ -158,14 +158,19 @@ const char* sfmm_gpu_last_error(void) { return g_last_error.c_str(); }
 
 const char* sfmm_gpu_version(void) { return "sfmm_gpu 0.1 (sm_100a, FP64)"; }
 
-int sfmm_gpu_plan_create(const sfmm_plan_desc* desc, int device, sfmm_gpu_plan** out) {
+}  // extern "C"
+
+namespace {
+
+int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
+                sfmm_gpu_plan** out) {
   if (!desc || !out) return set_error(SFMM_EINVAL, "sfmm_gpu_plan_create: null argument");
   *out = nullptr;
   sfmm_gpu_plan* p = nullptr;
   try {
     p = new sfmm_gpu_plan();
     std::string err;
-    const int rc = build_host_plan(*desc, p->hp, err);
+    const int rc = build_host_plan(*desc, p->hp, err, n_ranks, rank);
     if (rc != SFMM_OK) {
       delete p;
       return set_error(rc, err);
@@ -186,6 +191,7 @@ int sfmm_gpu_plan_create(const sfmm_plan_desc* desc, int device, sfmm_gpu_plan**
     dp.n_points = hp.n_points;
     dp.n_boxes = hp.n_boxes;
     dp.depth = hp.depth;
+    dp.n_owned_points = hp.n_owned_points;
     dp.counter = p->alloc<int>(4);
     dp.err_flag = p->alloc<int>(4);
     ck(cudaMemset(dp.err_flag, 0, 4 * sizeof(int)), "memset");
@@ -200,6 +206,7 @@ int sfmm_gpu_plan_create(const sfmm_plan_desc* desc, int device, sfmm_gpu_plan**
       dp.entries = p->upload(hp.entries);
       dp.tasks = p->upload(hp.tasks);
       dp.n_tasks = (int64_t)hp.tasks.size();
+      dp.n_interior = hp.n_interior_tasks;
       dp.X = p->upload(hp.X);
       dp.Y = p->upload(hp.Y);
       dp.Z = p->upload(hp.Z);
@@ -208,7 +215,12 @@ int sfmm_gpu_plan_create(const sfmm_plan_desc* desc, int device, sfmm_gpu_plan**
       dp.leaf_slot = p->upload(hp.leaf_slot);
       dp.leaf_orig = p->upload(hp.leaf_orig);
       dp.T_off = p->upload(hp.T_off);
-      dp.T = p->upload(desc->T, (size_t)hp.T_off[hp.n_boxes] * sw);
+      // interpolation operators of the owned boxes, copied run by run
+      dp.T = p->alloc<double>((size_t)hp.T_off[hp.n_boxes] * sw);
+      for (const HostPlan::Run& r : hp.T_runs)
+        ck(cudaMemcpy(dp.T + r.dst * sw, desc->T + r.src * sw, sizeof(double) * r.len * sw,
+                      cudaMemcpyHostToDevice),
+           "upload T");
       dp.up_items = p->upload(hp.up_items);
       dp.down_items = p->upload(hp.down_items);
       dp.stage = p->alloc<double>((size_t)std::max<int64_t>(hp.stage_size, 1));
@@ -217,6 +229,10 @@ int sfmm_gpu_plan_create(const sfmm_plan_desc* desc, int device, sfmm_gpu_plan**
       dp.recv_off = p->upload(hp.recv_off);
       dp.recv_u = p->upload(hp.recv_u);
       dp.recv_h = p->upload(hp.recv_h);
+      dp.pack_idx = p->upload(hp.pack_idx);
+      dp.unpack_idx = p->upload(hp.unpack_idx);
+      dp.n_pack = (int64_t)hp.pack_idx.size();
+      dp.n_unpack = (int64_t)hp.unpack_idx.size();
       size_t max_r = 0, max_k = 0;
       for (const BoxRec& b : hp.box) {
         max_r = std::max<size_t>(max_r, (size_t)(b.n - b.k));
@@ -240,6 +256,8 @@ int sfmm_gpu_plan_create(const sfmm_plan_desc* desc, int device, sfmm_gpu_plan**
       std::vector<int32_t>().swap(hp.leaf_orig);
       std::vector<int32_t>().swap(hp.entries);
       std::vector<Task>().swap(hp.tasks);
+      std::vector<int64_t>().swap(hp.pack_idx);
+      std::vector<int64_t>().swap(hp.unpack_idx);
     }
     ck(cudaDeviceSynchronize(), "plan upload");
     *out = p;
@@ -253,10 +271,122 @@ int sfmm_gpu_plan_create(const sfmm_plan_desc* desc, int device, sfmm_gpu_plan**
   }
 }
 
+}  // namespace
+
+extern "C" {
+
+int sfmm_gpu_plan_create(const sfmm_plan_desc* desc, int device, sfmm_gpu_plan** out) {
+  return create_plan(desc, device, 1, 0, out);
+}
+
+int sfmm_gpu_plan_create_sharded(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
+                                 sfmm_gpu_plan** out) {
+  return create_plan(desc, device, n_ranks, rank, out);
+}
+
+int sfmm_gpu_shard_info(const sfmm_gpu_plan* p, int64_t* send_counts, int64_t* recv_counts,
+                        int64_t* n_owned_points, int64_t* n_ghost_boxes) {
+  if (!p) return set_error(SFMM_EINVAL, "null plan");
+  const HostPlan& hp = p->hp;
+  for (int r = 0; r < hp.n_ranks; ++r) {
+    const bool have = hp.send_off.size() == (size_t)hp.n_ranks + 1;
+    if (send_counts) send_counts[r] = have ? hp.send_off[r + 1] - hp.send_off[r] : 0;
+    if (recv_counts)
+      recv_counts[r] = have ? hp.recv_off_peer[r + 1] - hp.recv_off_peer[r] : 0;
+  }
+  if (n_owned_points) *n_owned_points = hp.n_owned_points;
+  if (n_ghost_boxes) *n_ghost_boxes = hp.n_ghost_boxes;
+  return SFMM_OK;
+}
+
+int sfmm_gpu_shard_describe(const sfmm_plan_desc* desc, int n_ranks, int rank, int64_t* counts,
+                            int32_t* owner, int64_t* pack_idx, int64_t* unpack_idx,
+                            int32_t* owned_points) {
+  if (!desc || !counts) return set_error(SFMM_EINVAL, "sfmm_gpu_shard_describe: null argument");
+  HostPlan hp;
+  std::string err;
+  const int rc = build_host_plan(*desc, hp, err, n_ranks, rank);
+  if (rc != SFMM_OK) return set_error(rc, err);
+  const bool have = hp.send_off.size() == (size_t)n_ranks + 1;
+  for (int r = 0; r < n_ranks; ++r) {
+    counts[r] = have ? hp.send_off[r + 1] - hp.send_off[r] : 0;
+    counts[n_ranks + r] = have ? hp.recv_off_peer[r + 1] - hp.recv_off_peer[r] : 0;
+  }
+  counts[2 * n_ranks] = hp.n_owned_points;
+  counts[2 * n_ranks + 1] = hp.n_ghost_boxes;
+  int64_t owned_boxes = 0;
+  for (int32_t o : hp.owner) owned_boxes += o == rank ? 1 : 0;
+  counts[2 * n_ranks + 2] = hp.depth < 2 ? (rank == 0 ? hp.n_boxes : 0) : owned_boxes;
+  if (owner && !hp.owner.empty()) std::copy(hp.owner.begin(), hp.owner.end(), owner);
+  if (pack_idx) std::copy(hp.pack_idx.begin(), hp.pack_idx.end(), pack_idx);
+  if (unpack_idx) std::copy(hp.unpack_idx.begin(), hp.unpack_idx.end(), unpack_idx);
+  if (owned_points) {
+    if (hp.depth < 2) {
+      for (int64_t i = 0; i < hp.n_owned_points; ++i) owned_points[i] = (int32_t)i;
+    } else {
+      std::copy(hp.leaf_orig.begin(), hp.leaf_orig.end(), owned_points);
+    }
+  }
+  return SFMM_OK;
+}
+
+int sfmm_gpu_apply_begin(sfmm_gpu_plan* p, const void* q_dev, void* send_dev, void* stream,
+                         void* packed_event) {
+  if (!p || !q_dev) return set_error(SFMM_EINVAL, "fmm_apply: bad arguments");
+  std::lock_guard<std::mutex> lock(p->mu);
+  try {
+    ck(cudaSetDevice(p->device), "cudaSetDevice");
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : p->stream;
+    const double* q = static_cast<const double*>(q_dev);
+    if (p->hp.depth >= 2) {
+      launch_gather(p->dp, q, p->ds, st);
+      for (int l = p->hp.depth; l >= 2; --l) launch_upward(p->dp, p->hp, l, p->ds, st);
+      if (p->dp.n_pack > 0) {
+        if (!send_dev) throw CudaFail{SFMM_EINVAL, "send buffer required"};
+        launch_pack(p->dp, p->ds, static_cast<double*>(send_dev), st);
+      }
+    }
+    if (packed_event) ck(cudaEventRecord(static_cast<cudaEvent_t>(packed_event), st), "event");
+    if (p->hp.depth >= 2) launch_translate(p->dp, p->ds, st, kInteriorTasks);
+    ck(cudaGetLastError(), "kernel launch");
+    return SFMM_OK;
+  } catch (const CudaFail& f) {
+    return set_error(f.code, "fmm_apply: " + f.msg);
+  }
+}
+
+int sfmm_gpu_apply_end(sfmm_gpu_plan* p, const void* q_dev, const void* recv_dev, void* u_dev,
+                       void* stream) {
+  if (!p || !u_dev) return set_error(SFMM_EINVAL, "fmm_apply: bad arguments");
+  std::lock_guard<std::mutex> lock(p->mu);
+  try {
+    ck(cudaSetDevice(p->device), "cudaSetDevice");
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : p->stream;
+    double* u = static_cast<double*>(u_dev);
+    if (p->hp.depth < 2) {
+      if (p->hp.rank == 0) launch_direct_fallback(p->dp, static_cast<const double*>(q_dev), u, st);
+    } else {
+      if (p->dp.n_unpack > 0) {
+        if (!recv_dev) throw CudaFail{SFMM_EINVAL, "receive buffer required"};
+        launch_unpack(p->dp, p->ds, static_cast<const double*>(recv_dev), st);
+      }
+      launch_translate(p->dp, p->ds, st, kBoundaryTasks);
+      for (int l = 2; l <= p->hp.depth; ++l) launch_downward(p->dp, p->hp, l, p->ds, st);
+      launch_scatter(p->dp, p->ds, u, st);
+    }
+    ck(cudaGetLastError(), "kernel launch");
+    return SFMM_OK;
+  } catch (const CudaFail& f) {
+    return set_error(f.code, "fmm_apply: " + f.msg);
+  }
+}
+
 int sfmm_gpu_apply(sfmm_gpu_plan* p, const void* q, void* u, int nrhs, int flags,
                    sfmm_gpu_stats* stats) {
   if (!p || (!q && p->hp.n_points) || (!u && p->hp.n_points) || nrhs < 1)
     return set_error(SFMM_EINVAL, "fmm_apply: bad arguments");
+  if (p->hp.n_ranks > 1)
+    return set_error(SFMM_EINVAL, "fmm_apply: sharded plan: use sfmm_gpu_apply_begin/_end");
   std::lock_guard<std::mutex> lock(p->mu);
   try {
     ck(cudaSetDevice(p->device), "cudaSetDevice");
@@ -309,6 +439,8 @@ int sfmm_gpu_apply(sfmm_gpu_plan* p, const void* q, void* u, int nrhs, int flags
 int sfmm_gpu_apply_async(sfmm_gpu_plan* p, const void* q_dev, void* u_dev, int nrhs,
                          void* stream) {
   if (!p || nrhs < 1) return set_error(SFMM_EINVAL, "fmm_apply: bad arguments");
+  if (p->hp.n_ranks > 1)
+    return set_error(SFMM_EINVAL, "fmm_apply: sharded plan: use sfmm_gpu_apply_begin/_end");
   std::lock_guard<std::mutex> lock(p->mu);
   try {
     ck(cudaSetDevice(p->device), "cudaSetDevice");
