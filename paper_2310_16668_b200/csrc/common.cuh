@@ -16,6 +16,7 @@ enum Mode : int32_t {
   kSYM = 4   // IFO with a colleague c > b, evaluated once for both directions:
              // b's rows as kIFO, c's rows (A_cb = A_bc^T) as staged column sums
 };
+constexpr int kNRHS = 16;  // right-hand sides per multi-RHS pass (zero padded)
 constexpr int kModeBits = 3;
 constexpr int32_t kModeMask = (1 << kModeBits) - 1;
 

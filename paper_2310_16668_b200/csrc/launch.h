@@ -46,7 +46,15 @@ struct DevPlan {
   int64_t* unpack_idx;
   int64_t n_pack, n_unpack;
   int64_t n_owned_points;  // entries of leaf_slot / leaf_orig
-  int* counter;     // K2 task counters (interior, boundary; reset per launch)
+  // multi-RHS path (kernels_multi.cu)
+  EntryRange* ent_range_full;
+  int32_t* entries_full;
+  Task* tasks_m;
+  int64_t n_tasks_m;
+  LevelItem* down_m_items;
+  int k2m_grid;
+  size_t down_m_smem;
+  int* counter;     // K2 task counters (interior, boundary, multi; reset per launch)
   int* err_flag;    // sticky duplicate-point flag
   int k2_grid;      // persistent K2 CTAs
   size_t up_smem, down_smem;
@@ -79,6 +87,16 @@ void launch_direct_subset(int kernel, double kappa, int dim, int64_t n, const do
 // Persistent-grid size and dynamic shared memory setup (called at plan creation).
 int configure_translate(DevPlan& p, int device);
 int configure_tree_kernels(DevPlan& p, size_t max_r, size_t max_k);
+
+// Multi-RHS passes over kNRHS right-hand sides at once (state stride kNRHS);
+// nc <= kNRHS live columns, the rest are zero padding.
+int configure_multi(DevPlan& p, int device, size_t max_k);
+void launch_gather_m(const DevPlan& p, const double* q, int nc, DevState& s, cudaStream_t st);
+void launch_upward_m(const DevPlan& p, const HostPlan& hp, int level, DevState& s, cudaStream_t st);
+void launch_translate_m(const DevPlan& p, DevState& s, cudaStream_t st);
+void launch_downward_m(const DevPlan& p, const HostPlan& hp, int level, DevState& s,
+                       cudaStream_t st);
+void launch_scatter_m(const DevPlan& p, const DevState& s, double* u, int nc, cudaStream_t st);
 
 // DFMA throughput probe (TFLOP/s), see kernels_probe.cu.
 double measure_fp64_peak(int device);

@@ -333,6 +333,33 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
           hp.p_dense_local += (double)hp.box[b].n * hp.box[hp.entries[e] >> kModeBits].n;
     }
 
+    // multi-RHS path: the same entries without the symmetric folding, and
+    // 16-row tasks (cost sorted, interior first is not needed: the multi-RHS
+    // apply is single-rank)
+    {
+      hp.ent_range_full.resize(nb);
+      std::vector<std::pair<double, Task>> tv;
+      for (int32_t b = 0; b < nb; ++b) {
+        EntryRange& er = hp.ent_range_full[b];
+        er.begin = (int64_t)hp.entries_full.size();
+        er.count = 0;
+        if (!mine(b) || d.box_level[b] < 1) continue;
+        double src = 0;
+        sources(b, [&](int32_t c, int mode) {
+          hp.entries_full.push_back((c << kModeBits) | mode);
+          src += hp.box[c].n;
+        });
+        er.count = (int32_t)((int64_t)hp.entries_full.size() - er.begin);
+        if (er.count == 0) continue;
+        for (int32_t r0 = 0; r0 < hp.box[b].n; r0 += kMultiRows)
+          tv.push_back({src * kMultiRows + 64.0,
+                        Task{b, r0, std::min(kMultiRows, hp.box[b].n - r0), 0, 0}});
+      }
+      std::stable_sort(tv.begin(), tv.end(),
+                       [](const auto& a, const auto& b) { return a.first > b.first; });
+      for (auto& e : tv) hp.tasks_m.push_back(e.second);
+    }
+
     // ghost exchange lists: box c owned by p is sent to q if one of q's
     // targets reads it.  Every rank derives the same lists.
     if (n_ranks > 1) {
@@ -441,9 +468,11 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
     hp.T_off[nb] = tcur;
     hp.up_lvl.assign(d.depth + 2, 0);
     hp.down_lvl.assign(d.depth + 2, 0);
+    hp.down_m_lvl.assign(d.depth + 2, 0);
     for (int l = 0; l <= d.depth; ++l) {
       hp.up_lvl[l] = (int64_t)hp.up_items.size();
       hp.down_lvl[l] = (int64_t)hp.down_items.size();
+      hp.down_m_lvl[l] = (int64_t)hp.down_m_items.size();
       if (l >= 2) {
         for (int32_t b = hp.level_begin[l]; b < hp.level_begin[l + 1]; ++b) {
           if (!mine(b)) continue;
@@ -452,11 +481,13 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
           for (int32_t i = 0; i < k; i += kUpRows) hp.up_items.push_back({b, i});
           // one item even when r == 0: it also folds uhat into the skeleton slots
           for (int32_t j = 0; j < std::max(r, 1); j += kDownCols) hp.down_items.push_back({b, j});
+          for (int32_t j = 0; j < std::max(r, 1); j += kDownColsM) hp.down_m_items.push_back({b, j});
         }
       }
     }
     hp.up_lvl[d.depth + 1] = (int64_t)hp.up_items.size();
     hp.down_lvl[d.depth + 1] = (int64_t)hp.down_items.size();
+    hp.down_m_lvl[d.depth + 1] = (int64_t)hp.down_m_items.size();
     return SFMM_OK;
   } catch (const Fail& f) {
     err = f.msg;

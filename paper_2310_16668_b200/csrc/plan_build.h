@@ -25,6 +25,8 @@ constexpr int kRowsPerLane = 4;                 // max rows per lane in K2
 constexpr int kTileRows = 32 * kRowsPerLane;    // rows per K2 task
 constexpr int kUpRows = 8;                      // K1 rows (skeleton entries) per CTA
 constexpr int kDownCols = 256;                  // K3 columns (redundant slots) per CTA
+constexpr int kMultiRows = 16;                  // K2m rows per task (two 8-row DMMA tiles)
+constexpr int kDownColsM = 16;                  // K3m columns per CTA (x 16 rhs threads)
 
 struct LevelItem {
   int32_t box;
@@ -71,6 +73,12 @@ struct HostPlan {
   // per peer ranges send_off[p]..send_off[p+1] / recv_off_peer[p]..
   std::vector<int64_t> pack_idx, unpack_idx, send_off, recv_off_peer;
   int64_t n_ghost_boxes = 0;
+  // multi-RHS path: unfolded CSR (no kSYM), 16-row tasks, 16-column K3 items
+  std::vector<EntryRange> ent_range_full;
+  std::vector<int32_t> entries_full;
+  std::vector<Task> tasks_m;
+  std::vector<LevelItem> down_m_items;
+  std::vector<int64_t> down_m_lvl;
   // owned interpolation blocks copied from the descriptor into a compact blob
   struct Run {
     int64_t src, dst, len;  // scalars

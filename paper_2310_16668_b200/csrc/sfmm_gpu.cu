@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -137,6 +138,45 @@ struct sfmm_gpu_plan {
     if (slot >= 0) mark(slot, 5, st);
   }
 
+  // Multi-RHS state (kNRHS columns per pass), allocated on first use.
+  DevState dsm{};
+  bool multi_ok = true;
+
+  void ensure_multi() {
+    if (dsm.Q) return;
+    const int sw = hp.cplx ? 2 : 1;
+    dsm.Q = alloc<double>((size_t)hp.n_slots * kNRHS * sw);
+    dsm.U = alloc<double>((size_t)hp.n_slots * kNRHS * sw);
+    dsm.QH = alloc<double>((size_t)std::max<int64_t>(hp.n_skel, 1) * kNRHS * sw);
+    dsm.UH = alloc<double>((size_t)std::max<int64_t>(hp.n_skel, 1) * kNRHS * sw);
+  }
+
+  // nrhs columns (column-major, original order).  More than one column goes
+  // through the DMMA multi-RHS passes kNRHS at a time (SFMM_MULTI=0: column
+  // loop, for A/B measurements).
+  void enqueue_cols(const double* q, double* u, int nrhs, cudaStream_t st, bool time_k2) {
+    const size_t col_d = (size_t)hp.n_points * (hp.cplx ? 2 : 1);  // doubles per column
+    static const bool env_multi = [] {
+      const char* v = std::getenv("SFMM_MULTI");
+      return !(v && std::atoi(v) == 0);
+    }();
+    if (nrhs == 1 || hp.depth < 2 || !env_multi) {
+      for (int r = 0; r < nrhs; ++r) enqueue_one(q + r * col_d, u + r * col_d, st, time_k2 && r == 0);
+      return;
+    }
+    ensure_multi();
+    for (int c0 = 0; c0 < nrhs; c0 += kNRHS) {
+      const int nc = std::min(kNRHS, nrhs - c0);
+      launch_gather_m(dp, q + c0 * col_d, nc, dsm, st);
+      for (int l = hp.depth; l >= 2; --l) launch_upward_m(dp, hp, l, dsm, st);
+      if (time_k2 && c0 == 0) ck(cudaEventRecord(ev_k2a, st), "event");
+      launch_translate_m(dp, dsm, st);
+      if (time_k2 && c0 == 0) ck(cudaEventRecord(ev_k2b, st), "event");
+      for (int l = 2; l <= hp.depth; ++l) launch_downward_m(dp, hp, l, dsm, st);
+      launch_scatter_m(dp, dsm, u + c0 * col_d, nc, st);
+    }
+  }
+
   int launches_per_apply() const {
     if (hp.depth < 2) return 1;
     int n = 3;  // gather, translate, scatter
@@ -229,6 +269,11 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
       dp.recv_off = p->upload(hp.recv_off);
       dp.recv_u = p->upload(hp.recv_u);
       dp.recv_h = p->upload(hp.recv_h);
+      dp.ent_range_full = p->upload(hp.ent_range_full);
+      dp.entries_full = p->upload(hp.entries_full);
+      dp.tasks_m = p->upload(hp.tasks_m);
+      dp.n_tasks_m = (int64_t)hp.tasks_m.size();
+      dp.down_m_items = p->upload(hp.down_m_items);
       dp.pack_idx = p->upload(hp.pack_idx);
       dp.unpack_idx = p->upload(hp.unpack_idx);
       dp.n_pack = (int64_t)hp.pack_idx.size();
@@ -242,6 +287,8 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
         throw CudaFail{SFMM_EUNSUPPORTED, "interpolation block too large for shared memory"};
       if (configure_translate(dp, device) != 0)
         throw CudaFail{SFMM_ECUDA, "occupancy query failed"};
+      if (configure_multi(dp, device, max_k) != 0)
+        throw CudaFail{SFMM_EUNSUPPORTED, "multi-RHS configuration failed"};
       p->ds.Q = p->alloc<double>((size_t)hp.n_slots * sw);
       p->ds.U = p->alloc<double>((size_t)hp.n_slots * sw);
       p->ds.QH = p->alloc<double>((size_t)hp.n_skel * sw);
@@ -256,6 +303,8 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
       std::vector<int32_t>().swap(hp.leaf_orig);
       std::vector<int32_t>().swap(hp.entries);
       std::vector<Task>().swap(hp.tasks);
+      std::vector<int32_t>().swap(hp.entries_full);
+      std::vector<Task>().swap(hp.tasks_m);
       std::vector<int64_t>().swap(hp.pack_idx);
       std::vector<int64_t>().swap(hp.unpack_idx);
     }
@@ -393,22 +442,18 @@ int sfmm_gpu_apply(sfmm_gpu_plan* p, const void* q, void* u, int nrhs, int flags
     const size_t col = (size_t)p->hp.n_points * p->scalar_bytes();
     const bool host = flags == SFMM_HOST_BUFFERS;
     cudaStream_t st = p->stream;
-    if (host) p->ensure_io(col);
+    if (host) p->ensure_io(col * nrhs);
     ck(cudaEventRecord(p->ev_a, st), "event");
-    for (int r = 0; r < nrhs; ++r) {
-      const char* qc = static_cast<const char*>(q) + r * col;
-      char* uc = static_cast<char*>(u) + r * col;
-      const double* qd = reinterpret_cast<const double*>(qc);
-      double* ud = reinterpret_cast<double*>(uc);
-      if (host) {
-        ck(cudaMemcpyAsync(p->io_q, qc, col, cudaMemcpyHostToDevice, st), "H2D q");
-        qd = p->io_q;
-        ud = p->io_u;
-      }
-      p->enqueue_one(qd, ud, st, r == 0);
-      ck(cudaGetLastError(), "kernel launch");
-      if (host) ck(cudaMemcpyAsync(uc, p->io_u, col, cudaMemcpyDeviceToHost, st), "D2H u");
+    const double* qd = static_cast<const double*>(q);
+    double* ud = static_cast<double*>(u);
+    if (host) {
+      ck(cudaMemcpyAsync(p->io_q, q, col * nrhs, cudaMemcpyHostToDevice, st), "H2D q");
+      qd = p->io_q;
+      ud = p->io_u;
     }
+    p->enqueue_cols(qd, ud, nrhs, st, true);
+    ck(cudaGetLastError(), "kernel launch");
+    if (host) ck(cudaMemcpyAsync(u, p->io_u, col * nrhs, cudaMemcpyDeviceToHost, st), "D2H u");
     ck(cudaEventRecord(p->ev_b, st), "event");
     ck(cudaStreamSynchronize(st), "apply");
     int flag = 0;
@@ -445,12 +490,8 @@ int sfmm_gpu_apply_async(sfmm_gpu_plan* p, const void* q_dev, void* u_dev, int n
   try {
     ck(cudaSetDevice(p->device), "cudaSetDevice");
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : p->stream;
-    const size_t col = (size_t)p->hp.n_points * p->scalar_bytes();
-    for (int r = 0; r < nrhs; ++r) {
-      const double* qd = reinterpret_cast<const double*>(static_cast<const char*>(q_dev) + r * col);
-      double* ud = reinterpret_cast<double*>(static_cast<char*>(u_dev) + r * col);
-      p->enqueue_one(qd, ud, st, false);
-    }
+    p->enqueue_cols(static_cast<const double*>(q_dev), static_cast<double*>(u_dev), nrhs, st,
+                    false);
     ck(cudaGetLastError(), "kernel launch");
     return SFMM_OK;
   } catch (const CudaFail& f) {
