@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_DIR = os.path.join(PKG_DIR, "lib")
+LIB_DIR = os.environ.get("SFMM_LIB_DIR") or os.path.join(PKG_DIR, "lib")
 
 # kernel ids (sfmm_gpu.h; same order as sfmm::KernelFamily, kernel.hpp:12)
 LAPLACE2D, LAPLACE3D, HELMHOLTZ2D, HELMHOLTZ3D = 0, 1, 2, 3

@@ -309,7 +309,7 @@ __device__ __forceinline__ double mulr(double a, double b) { return a * b; }
 // K1m: qhat[i][r] = Q[i][r] + sum_j T[i,j] Q[k+j][r]; one CTA per (box, 8 rows),
 // thread (row, rhs); q_R streamed through shared memory in chunks of 64.
 template <class S>
-__global__ void __launch_bounds__(128) k1m_upward(const LevelItem* __restrict__ items,
+__global__ void __launch_bounds__(kUpRows * kNRHS) k1m_upward(const LevelItem* __restrict__ items,
                                                   const BoxRec* __restrict__ box,
                                                   const int64_t* __restrict__ T_off,
                                                   const S* __restrict__ T, S* __restrict__ Q,
@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(128) k1m_upward(const LevelItem* __restrict__ 
   const LevelItem it = items[blockIdx.x];
   const BoxRec br = box[it.box];
   const int k = br.k, r = br.n - br.k;
-  const int li = threadIdx.x / kNRHS, rhs = threadIdx.x % kNRHS;  // 8 rows x 16 rhs
+  const int li = threadIdx.x / kNRHS, rhs = threadIdx.x % kNRHS;  // kUpRows rows x 16 rhs
   const int i = it.first + li;
   const S* Tb = T + T_off[it.box] + (int64_t)(i < k ? i : 0) * r;
   S acc{};
@@ -470,11 +470,11 @@ void launch_upward_m(const DevPlan& p, const HostPlan& hp, int level, DevState& 
   const int64_t i0 = hp.up_lvl[level], i1 = hp.up_lvl[level + 1];
   if (i1 <= i0) return;
   if (p.cplx)
-    k1m_upward<double2><<<(unsigned)(i1 - i0), 128, 0, st>>>(
+    k1m_upward<double2><<<(unsigned)(i1 - i0), kUpRows * kNRHS, 0, st>>>(
         p.up_items + i0, p.box, p.T_off, reinterpret_cast<const double2*>(p.T),
         reinterpret_cast<double2*>(s.Q), reinterpret_cast<double2*>(s.QH), p.up_dst);
   else
-    k1m_upward<double><<<(unsigned)(i1 - i0), 128, 0, st>>>(p.up_items + i0, p.box, p.T_off, p.T,
+    k1m_upward<double><<<(unsigned)(i1 - i0), kUpRows * kNRHS, 0, st>>>(p.up_items + i0, p.box, p.T_off, p.T,
                                                              s.Q, s.QH, p.up_dst);
 }
 

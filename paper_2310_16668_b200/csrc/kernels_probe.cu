@@ -11,8 +11,12 @@ namespace {
 
 constexpr int kChains = 8;
 
-__global__ void __launch_bounds__(256) dfma_loop(double* out, int iters, double a, double b) {
+// One multiplicand comes from a uniform register (the kernel parameter) and the
+// addend from a per-thread register, so the loop is not limited by register-
+// file read bandwidth (three 64-bit register operands per DFMA measure ~92 %).
+__global__ void __launch_bounds__(256) dfma_loop(double* out, int iters, double a, double b0) {
   double x[kChains];
+  const double b = b0 * (threadIdx.x + 1);
 #pragma unroll
   for (int c = 0; c < kChains; ++c) x[c] = threadIdx.x * 1e-3 + c;
   for (int i = 0; i < iters; ++i) {
@@ -36,9 +40,9 @@ double measure_fp64_peak(int device) {
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   // 4 CTAs x 256 threads per SM, 8 independent chains each: 37.0 TFLOP/s at
-  // 1965 MHz on B200 (64 DFMA/clk/SM); ~2.6 ms per launch
+  // 1965 MHz on B200 (64 DFMA/clk/SM); ~13 ms per launch so the clocks settle
   const int blocks = sms * 4, threads = 256;
-  const int iters = 40000;
+  const int iters = 200000;
   float ms = 0;
   dfma_loop<<<blocks, threads>>>(out, iters / 10, 0.999999, 1e-7);  // warm-up
   double best = 0;

@@ -305,7 +305,10 @@ __device__ __forceinline__ void task_real(const K2Args& a, const Task& t, WarpSm
 }
 
 template <class G>
-__global__ void __launch_bounds__(kThreads, 4) k2_translate_real(K2Args a) {
+#ifndef SFMM_K2_MIN_BLOCKS
+#define SFMM_K2_MIN_BLOCKS 4
+#endif
+__global__ void __launch_bounds__(kThreads, SFMM_K2_MIN_BLOCKS) k2_translate_real(K2Args a) {
   __shared__ WarpSmemReal smem[kWarps];
   const int lane = threadIdx.x & 31;
   WarpSmemReal& sm = smem[threadIdx.x >> 5];

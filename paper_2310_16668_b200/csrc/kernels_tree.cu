@@ -19,7 +19,7 @@ namespace sfmm_gpu {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kUpThreads = 128;
+constexpr int kUpThreads = 256;
 constexpr double kInv4Pi = 0.0795774715459476678844418816862571810;
 
 template <class S>
@@ -45,6 +45,9 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // K1, real: qhat_i = q_S[i] + sum_j T[i,j] q_R[j] for kUpRows rows of one box.
+// Each warp streams 4 rows of T at once (4 independent coalesced loads per
+// lane per step) so enough bytes are in flight to run at HBM speed.
+constexpr int kUpRowsPerWarp = 4;
 __global__ void __launch_bounds__(kUpThreads) k1_upward_real(
     const LevelItem* __restrict__ items, const BoxRec* __restrict__ box,
     const int64_t* __restrict__ T_off, const double* __restrict__ T, double* __restrict__ Q,
@@ -59,15 +62,29 @@ __global__ void __launch_bounds__(kUpThreads) k1_upward_real(
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const double* Tb = T + T_off[it.box];
   const int i1 = min(it.first + kUpRows, k);
-  for (int i = it.first + w; i < i1; i += kUpThreads / 32) {
-    const double* Ti = Tb + (int64_t)i * r;
-    double acc = 0.0;
-    for (int j = lane; j < r; j += 32) acc = fma(Ti[j], smq[j], acc);
-    acc = warp_sum(acc);
-    if (lane == 0) {
-      const double v = Q[br.slot + i] + acc;
-      QH[br.skel + i] = v;
-      Q[up_dst[br.skel + i]] = v;
+  for (int i0 = it.first + w * kUpRowsPerWarp; i0 < i1; i0 += (kUpThreads / 32) * kUpRowsPerWarp) {
+    double acc[kUpRowsPerWarp];
+    const double* Ti[kUpRowsPerWarp];
+#pragma unroll
+    for (int m = 0; m < kUpRowsPerWarp; ++m) {
+      acc[m] = 0.0;
+      Ti[m] = Tb + (int64_t)min(i0 + m, i1 - 1) * r;
+    }
+#pragma unroll 2
+    for (int j = lane; j < r; j += 32) {
+      const double qj = smq[j];
+#pragma unroll
+      for (int m = 0; m < kUpRowsPerWarp; ++m) acc[m] = fma(__ldg(Ti[m] + j), qj, acc[m]);
+    }
+#pragma unroll
+    for (int m = 0; m < kUpRowsPerWarp; ++m) {
+      const double s = warp_sum(acc[m]);
+      const int i = i0 + m;
+      if (lane == 0 && i < i1) {
+        const double v = Q[br.slot + i] + s;
+        QH[br.skel + i] = v;
+        Q[up_dst[br.skel + i]] = v;
+      }
     }
   }
 }

@@ -23,7 +23,7 @@ namespace sfmm_gpu {
 
 constexpr int kRowsPerLane = 4;                 // max rows per lane in K2
 constexpr int kTileRows = 32 * kRowsPerLane;    // rows per K2 task
-constexpr int kUpRows = 8;                      // K1 rows (skeleton entries) per CTA
+constexpr int kUpRows = 32;                     // K1 rows (skeleton entries) per CTA
 constexpr int kDownCols = 256;                  // K3 columns (redundant slots) per CTA
 constexpr int kMultiRows = 16;                  // K2m rows per task (two 8-row DMMA tiles)
 constexpr int kDownColsM = 16;                  // K3m columns per CTA (x 16 rhs threads)
