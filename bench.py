@@ -64,7 +64,27 @@ def parse():
                     help="instance size of one --impl reference step / the 'sample' cpu baseline")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="multi-rank exchange; gloo stages through host memory (test path)")
-    return ap.parse_args()
+    ap.add_argument("--nrhs", type=int, default=1)
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS),
+                    help="BASELINE.json configs (secondary measurement lines; default = headline)")
+    args = ap.parse_args()
+    if args.config:
+        for k, v in CONFIGS[args.config].items():
+            setattr(args, k, v)
+    return args
+
+
+# BASELINE.json "configs" (the headline line is the default arguments above:
+# 3D Laplace, cube, N=1e7, leaf 128, tol 1e-6, one RHS)
+CONFIGS = {
+    "c1": dict(kernel="laplace2d", dist="square", n=1e5, leaf=64, tol=1e-6, nrhs=1),
+    "c2": dict(kernel="laplace3d", dist="cube", n=1e6, leaf=128, tol=1e-6, nrhs=1),
+    "c3a": dict(kernel="laplace3d", dist="sphere", n=1e7, leaf=128, tol=1e-8, nrhs=1),
+    "c3b": dict(kernel="laplace3d", dist="gaussian", n=1e7, leaf=128, tol=1e-8, nrhs=1),
+    "c4": dict(kernel="helmholtz3d", dist="cube", n=4e6, leaf=128, tol=1e-6, kappa=10.0, nrhs=16,
+               cpu="sample", ref_n=4e5),
+    "c5": dict(kernel="laplace3d", dist="cube", n=1e8, leaf=128, tol=1e-6, nrhs=1, cpu="off"),
+}
 
 
 class ClockSampler:
@@ -145,7 +165,11 @@ def run_reference(args, ws, rank):
     from oracle import pyoracle as po
     n = int(args.ref_n)
     kern = KERNELS[args.kernel]
-    pts = po.generate_points(args.dist, n, 1)
+    if args.dist in po.DIST:
+        pts = po.generate_points(args.dist, n, 1)
+    else:  # clustered Gaussian (config 3b) has no reference generator
+        from paper_2310_16668_b200 import host
+        pts = host.generate_points(args.dist, n, 1)
     t0 = time.perf_counter()
     rp = po.RefPipeline.build(kern, pts, args.leaf, args.tol, args.kappa)
     t_pre = time.perf_counter() - t0
@@ -378,10 +402,14 @@ def main():
     n = int(args.n)
     kern = KERNELS[args.kernel]
     cplx = kern == 3
+    nrhs = args.nrhs
     t0 = time.perf_counter()
     pts = host.generate_points(args.dist, n, 1)
-    q = (host.generate_charges_complex(n, 1 ^ CHARGE_STREAM) if cplx
-         else host.generate_charges(n, 1 ^ CHARGE_STREAM))
+    # right-hand side r uses the reference charge stream with seed (1 + r)
+    gen = host.generate_charges_complex if cplx else host.generate_charges
+    q = gen(n, 1 ^ CHARGE_STREAM)
+    if nrhs > 1:
+        q = np.asfortranarray(np.stack([gen(n, (1 + r) ^ CHARGE_STREAM) for r in range(nrhs)], 1))
     t_gen = time.perf_counter() - t0
     hp = host.HostPlan.build(kern, pts, args.leaf, args.tol, args.kappa)
     hinfo = hp.info()
@@ -391,7 +419,8 @@ def main():
     info = plan.info()
 
     dtype = torch.complex128 if cplx else torch.float64
-    q_host = torch.from_numpy(q)
+    # column-major n x nrhs == row-major (nrhs, n)
+    q_host = torch.from_numpy(np.ascontiguousarray(q.T) if nrhs > 1 else q)
     q_dev = q_host.to(f"cuda:{dev}")
     u_dev = torch.empty_like(q_dev)
     # a dedicated stream: the applies and the timing events share it
@@ -400,7 +429,7 @@ def main():
     torch.cuda.synchronize(dev)
 
     for _ in range(args.warmup):
-        api.fmm_apply_device(plan, q_dev.data_ptr(), u_dev.data_ptr(), 1, sp)
+        api.fmm_apply_device(plan, q_dev.data_ptr(), u_dev.data_ptr(), nrhs, sp)
     api.check_status(plan)
     # roofline denominator, measured with the clocks already up
     fp64_peak = api.fp64_peak_tflops(dev)
@@ -417,7 +446,7 @@ def main():
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     for _ in range(args.steps):
-        api.fmm_apply_device(plan, q_dev.data_ptr(), u_dev.data_ptr(), 1, sp)
+        api.fmm_apply_device(plan, q_dev.data_ptr(), u_dev.data_ptr(), nrhs, sp)
     ev1.record(stream)
     torch.cuda.synchronize(dev)
     if dist:
@@ -431,33 +460,50 @@ def main():
         tt = torch.tensor([ms_step], device=f"cuda:{dev}", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms_step = float(tt.item())
-    value = ws * n / (ms_step * 1e-3) / 1e6  # replicas: every rank applies its own plan
+    # points x right-hand sides per second (nrhs = 1 on the headline)
+    value = ws * n * nrhs / (ms_step * 1e-3) / 1e6
 
     u_gpu = u_dev.cpu().numpy()
+    if nrhs > 1:
+        u_gpu = np.asfortranarray(u_gpu.T)
+    u0 = u_gpu if nrhs == 1 else u_gpu[:, 0]
+    q0 = q if nrhs == 1 else q[:, 0]
 
     # ---- e2e: public host-buffer API, pinned q in / u out each step -------
     q_pin = torch.empty(q_host.shape, dtype=dtype).pin_memory()
     q_pin.copy_(q_host)
     u_pin = torch.empty(q_host.shape, dtype=dtype).pin_memory()
     e2e_steps = max(3, min(args.steps, 10))
-    api.fmm_apply(plan, q_pin.numpy(), out=u_pin.numpy())
+
+    def host_apply():
+        if nrhs == 1:
+            return api.fmm_apply(plan, q_pin.numpy(), out=u_pin.numpy())
+        return api.fmm_apply(plan, q_pin.numpy().T, out=u_pin.numpy().T)
+
+    host_apply()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        u_e2e = api.fmm_apply(plan, q_pin.numpy(), out=u_pin.numpy())
+        u_e2e = host_apply()
     t_e2e = (time.perf_counter() - t0) / e2e_steps
-    e2e_value = ws * n / t_e2e / 1e6
-    bytes_col = n * (16 if cplx else 8)
+    e2e_value = ws * n * nrhs / t_e2e / 1e6
+    bytes_col = n * nrhs * (16 if cplx else 8)
 
     # ---- accuracy vs the dense sum on sampled targets (GPU direct sum) ----
     rng = np.random.default_rng(0xC2B2AE3D27D4EB4F)
     targets = np.sort(rng.choice(n, size=min(args.check_targets, n), replace=False)).astype(np.int32)
-    ref_t = api.direct_sum_subset(kern, args.kappa, pts, q, targets, device=dev)
-    relerr_direct = api.max_rel_err(u_gpu[targets], ref_t)
+    ref_t = api.direct_sum_subset(kern, args.kappa, pts, q0, targets, device=dev)
+    relerr_direct = api.max_rel_err(u0[targets], ref_t)
     e2e_same = bool(np.array_equal(u_e2e, u_gpu))
 
     # ---- roofline of the dominant kernel (K2, FP64 pipe) -------------------
     k2_ms = float(np.mean(phases[:, 2])) if len(phases) else float("nan")
-    w_k2 = 20.0 * info.p_dense + 2.0 * info.p_skel
+    # W_K2 = F_K(r) P_dense + r 2 s_c P_skel, F_K(r) = G_K + 2 s_c r,
+    # G = 18 (Laplace) / 32 (Helmholtz), s_c = 1 real / 4 complex; the phase
+    # timings cover one 16-column pass of the multi-RHS path
+    r_pass = min(nrhs, 16)
+    s_c = 4.0 if cplx else 1.0
+    g_k = 32.0 if cplx else 18.0
+    w_k2 = (g_k + 2 * s_c * r_pass) * info.p_dense + r_pass * 2 * s_c * info.p_skel
     achieved = w_k2 / (k2_ms * 1e-3) / 1e12
     traffic = None
     prof = os.path.join(ROOT, "profiles", "k2_traffic.json")
@@ -483,8 +529,10 @@ def main():
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference generators: points seed 1, charges seed 1^0x9e3779b97f4a7c15)",
         "config": {
-            "workload": f"{args.kernel} {args.dist} N={n:.0e} leaf={args.leaf} tol={args.tol} nrhs=1",
-            "n_points": n, "leaf_cap": args.leaf, "tol": args.tol, "nrhs": 1,
+            "workload": f"{args.kernel} {args.dist} N={n:.0e} leaf={args.leaf} tol={args.tol} nrhs={nrhs}",
+            "n_points": n, "leaf_cap": args.leaf, "tol": args.tol, "nrhs": nrhs,
+            "baseline_config": args.config or "headline (3D Laplace cube N=1e7)",
+            "value_definition": "points x right-hand sides per second of device time",
             "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
             "l2": "inputs larger than L2 (resident plan %.1f GB vs 126 MB L2)" % (info.device_bytes / 1e9),
         },
@@ -519,23 +567,25 @@ def main():
             if args.cpu == "full":
                 rp = po.RefPipeline.from_desc(hp.desc_struct())
                 t0 = time.perf_counter()
-                u_ref, _ = rp.apply(q, cplx)
+                u_ref, _ = rp.apply(q0, cplx)  # the reference apply takes one RHS
                 t_cpu = time.perf_counter() - t0
                 rp.close()
-                out["relerr_vs_cpu_ref"] = po.rel_l2(u_gpu, u_ref)
-                out["max_relerr_vs_cpu_ref"] = api.max_rel_err(u_gpu, u_ref)
+                out["relerr_vs_cpu_ref"] = po.rel_l2(u0, u_ref)
+                out["max_relerr_vs_cpu_ref"] = api.max_rel_err(u0, u_ref)
                 n_cpu = n
-                sample = (f"full headline workload (N={n:.0e}), one reference fmm_apply on the "
+                sample = (f"full workload (N={n:.0e}), one reference fmm_apply (one RHS) on the "
                           "same tree/skeletons/charges as the GPU run")
             else:
                 n_cpu = int(args.ref_n)
                 p2 = host.generate_points(args.dist, n_cpu, 1)
-                q2 = host.generate_charges(n_cpu, 1 ^ CHARGE_STREAM)
+                q2 = (host.generate_charges_complex if cplx else host.generate_charges)(
+                    n_cpu, 1 ^ CHARGE_STREAM)
                 rp = po.RefPipeline.build(kern, p2, args.leaf, args.tol, args.kappa)
                 t0 = time.perf_counter()
                 rp.apply(q2, cplx)
                 t_cpu = time.perf_counter() - t0
-                sample = f"N={n_cpu:.0e} instance of the same workload, one reference fmm_apply"
+                sample = (f"N={n_cpu:.0e} instance of the same workload, one reference fmm_apply "
+                          "(one RHS; the reference has no multi-RHS apply)")
             out["cpu_baseline"] = {
                 "value": n_cpu / t_cpu / 1e6, "unit": UNIT,
                 "cores": po.ref_lib().ref_num_threads(), "kind": "reference",

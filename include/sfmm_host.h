@@ -28,8 +28,15 @@ extern "C" {
 /* Return codes beyond sfmm_gpu.h's: */
 enum { SFMM_EDEPTH = 7 /* sfmm::DepthExceededError */ };
 
-/* Distributions, same order as sfmm::Distribution (bench.hpp:15). */
-enum { SFMM_DIST_SQUARE = 0, SFMM_DIST_ANNULUS = 1, SFMM_DIST_CUBE = 2, SFMM_DIST_SPHERE = 3 };
+/* Distributions, same order as sfmm::Distribution (bench.hpp:15), plus the
+ * clustered Gaussian of config 3(b), which the reference does not define. */
+enum {
+  SFMM_DIST_SQUARE = 0,
+  SFMM_DIST_ANNULUS = 1,
+  SFMM_DIST_CUBE = 2,
+  SFMM_DIST_SPHERE = 3,
+  SFMM_DIST_GAUSSIAN = 4
+};
 
 /* sfmm::ProxyConfig (skeleton.hpp:13-17); zero fields take the defaults
  * 2.95 / 24 / 8. */

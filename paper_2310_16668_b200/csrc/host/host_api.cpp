@@ -72,6 +72,21 @@ void generate_points(int dist, int64_t n, uint64_t seed, double* out) {
         out[3 * i + 2] = z;
       }
       break;
+    case SFMM_DIST_GAUSSIAN: {
+      // Config 3(b) has no reference generator: 16 Gaussian
+      // clusters, sigma 0.02, centres uniform in [0.1, 0.9]^3, all from one
+      // mt19937_64 stream (centres first, then per point: cluster, 3 normals).
+      double centre[16][3];
+      for (auto& c : centre)
+        for (double& v : c) v = 0.1 + 0.8 * unit01(g);
+      for (int64_t i = 0; i < n; ++i) {
+        const int c = static_cast<int>(g() % 16);
+        double z[4];
+        normals(g, z, 4);
+        for (int k = 0; k < 3; ++k) out[3 * i + k] = centre[c][k] + 0.02 * z[k];
+      }
+      break;
+    }
     default:
       throw std::invalid_argument("generate_points: unknown distribution");
   }

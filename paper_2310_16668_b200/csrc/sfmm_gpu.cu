@@ -167,13 +167,21 @@ struct sfmm_gpu_plan {
     ensure_multi();
     for (int c0 = 0; c0 < nrhs; c0 += kNRHS) {
       const int nc = std::min(kNRHS, nrhs - c0);
+      // phase timing records the first 16-column pass of each apply
+      const int slot = (c0 == 0 && timing && n_timed < kMaxTimed) ? n_timed++ : -1;
+      if (slot >= 0) mark(slot, 0, st);
       launch_gather_m(dp, q + c0 * col_d, nc, dsm, st);
+      if (slot >= 0) mark(slot, 1, st);
       for (int l = hp.depth; l >= 2; --l) launch_upward_m(dp, hp, l, dsm, st);
+      if (slot >= 0) mark(slot, 2, st);
       if (time_k2 && c0 == 0) ck(cudaEventRecord(ev_k2a, st), "event");
       launch_translate_m(dp, dsm, st);
       if (time_k2 && c0 == 0) ck(cudaEventRecord(ev_k2b, st), "event");
+      if (slot >= 0) mark(slot, 3, st);
       for (int l = 2; l <= hp.depth; ++l) launch_downward_m(dp, hp, l, dsm, st);
+      if (slot >= 0) mark(slot, 4, st);
       launch_scatter_m(dp, dsm, u + c0 * col_d, nc, st);
+      if (slot >= 0) mark(slot, 5, st);
     }
   }
 

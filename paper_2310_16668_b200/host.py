@@ -16,8 +16,8 @@ import numpy as np
 from . import _abi
 from ._abi import PlanDesc, PlanDescriptor
 
-DIST = {"square": 0, "annulus": 1, "cube": 2, "sphere": 3}
-DIST_DIM = {"square": 2, "annulus": 2, "cube": 3, "sphere": 3}
+DIST = {"square": 0, "annulus": 1, "cube": 2, "sphere": 3, "gaussian": 4}
+DIST_DIM = {"square": 2, "annulus": 2, "cube": 3, "sphere": 3, "gaussian": 3}
 CHARGE_STREAM = 0x9E3779B97F4A7C15  # bench.cpp:27
 DEFAULT_LEAF_CAP = {"square": 100, "annulus": 100, "cube": 320, "sphere": 200}  # bench.cpp:92-100
 SFMM_EDEPTH = 7
