@@ -7,10 +7,12 @@
 // all of them: the translation step becomes a generated-matrix x (n_c x 16)
 // product issued on the FP64 tensor cores (mma.sync m8n8k4 f64 = DMMA).
 //
-// K2m task = 16 target rows (two 8-row DMMA tiles).  Per k-step (4 sources)
-// every lane generates the one G entry its A-fragment holds (row = lane/4,
-// source = lane%4) -- exactly one pair per lane, no shuffles -- and the warp
-// issues 8 DMMAs (complex) or 2 (real) per row tile.  Complex products use
+// K2m task = 64 target rows of one box on one CTA: 4 warps x two 8-row DMMA
+// tiles, sharing each staged 16-source chunk (B operands pre-arranged in
+// fragment order; the next chunk's loads are in flight during the compute).
+// Per k-step (4 sources) every lane generates the one G entry its A-fragment
+// holds (row = lane/4, source = lane%4) -- one pair per lane, no shuffles --
+// and the warp issues 8 DMMAs (complex) or 2 (real) per row tile.  Complex products use
 // U = Gr [Ar | Ai] + Gi [-Ai | Ar] so both real products accumulate into the
 // same fragments.  On B200 DMMA shares the FP64 datapath with DFMA (both
 // measured at 37 TFLOP/s, see profiles/), so the gain over scalar code is
@@ -59,14 +61,6 @@ struct K2MArgs {
   double kappa;
 };
 
-template <bool CPLX>
-struct WarpSmemM {
-  static constexpr int SW = CPLX ? 2 : 1;
-  double x[kChunk], y[kChunk], z[kChunk];
-  double a[kChunk][kNRHS * SW];
-  double h[kChunk][kNRHS * SW];
-};
-
 __device__ __noinline__ void verify_row_m(const K2MArgs& a, int32_t b, int32_t row, int dim) {
   const BoxRec tb = a.box[b];
   const int64_t s = tb.slot + row;
@@ -85,31 +79,64 @@ __device__ __noinline__ void verify_row_m(const K2MArgs& a, int32_t b, int32_t r
   }
 }
 
+// One staged 16-source chunk, shared by the CTA's 4 warps.  The B operands are
+// stored in DMMA fragment order ([k-step][B1|B2][n-block][lane]) so each lane
+// loads its fragment with one conflict-free 8-byte LDS.
+template <bool CPLX>
+struct ChunkM {
+  static constexpr int NB = CPLX ? 4 : 2;  // 8-column blocks of [Ar | Ai] or [A]
+  static constexpr int NP = CPLX ? 2 : 1;  // B1 = [Ar | Ai] and B2 = [-Ai | Ar]
+  double x[kChunk], y[kChunk], z[kChunk];
+  double a[4][NP][NB][32];
+  double h[4][NP][NB][32];
+};
+
+// Raw per-thread staging payload of one chunk (registers), so the next chunk's
+// global loads are in flight while the current one is computed.
+template <bool CPLX>
+struct StageRegs {
+  static constexpr int SW = CPLX ? 2 : 1;
+  static constexpr int ITEMS = kChunk * kNRHS / kMThreads;  // (source, rhs) per thread
+  double q[ITEMS][SW], qh[ITEMS][SW];
+  double cx, cy, cz;
+};
+
+struct ChunkPos {
+  int e, j0;  // entry index, first source of the chunk
+};
+
 // KER: 0 laplace2d, 1 laplace3d, 3 helmholtz3d
-template <int KER>
-__global__ void __launch_bounds__(kMThreads, 3) k2m_translate(K2MArgs a) {
+// WH: the launch's tasks own skeleton rows (uhat accumulators needed).  Tasks
+// without skeleton rows -- most of them -- run the lighter WH=false variant.
+template <int KER, bool WH>
+__global__ void __launch_bounds__(kMThreads, WH ? 2 : 3) k2m_translate(K2MArgs a) {
   constexpr bool CPLX = KER == SFMM_HELMHOLTZ3D;
   constexpr int SW = CPLX ? 2 : 1;
-  constexpr int NB = CPLX ? 4 : 2;  // 8-column DMMA blocks across [Ur | Ui] or [U]
+  constexpr int NB = CPLX ? 4 : 2;
   constexpr int DIM = KER == SFMM_LAPLACE2D ? 2 : 3;
-  __shared__ WarpSmemM<CPLX> smem[kMWarps];
-  WarpSmemM<CPLX>& sm = smem[threadIdx.x >> 5];
-  const int lane = threadIdx.x & 31;
+  constexpr int ITEMS = StageRegs<CPLX>::ITEMS;
+  __shared__ ChunkM<CPLX> ch;
+  __shared__ int s_task;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int rq = lane >> 2, kq = lane & 3;  // A-fragment row / k index of this lane
   for (;;) {
-    int t = 0;
-    if (lane == 0) t = atomicAdd(a.counter, 1);
-    t = __shfl_sync(0xffffffffu, t, 0);
+    __syncthreads();
+    if (tid == 0) s_task = atomicAdd(a.counter, 1);
+    __syncthreads();
+    const int t = s_task;
     if (t >= a.n_tasks) return;
     const Task task = a.tasks[t];
     const BoxRec tb = a.box[task.box];
+    const EntryRange er = a.er[task.box];
+    const int wrow0 = task.row0 + 16 * warp;  // this warp's 16 rows
+    const int rend = task.row0 + task.nrows;
     double xr[2], yr[2], zr[2];
     int rowi[2];
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) {
-      const int row = task.row0 + mt * 8 + rq;
+      const int row = wrow0 + mt * 8 + rq;
       rowi[mt] = row;
-      const int64_t s = tb.slot + (row < task.row0 + task.nrows ? row : task.row0);
+      const int64_t s = tb.slot + (row < rend ? row : task.row0);
       xr[mt] = a.X[s];
       yr[mt] = a.Y[s];
       zr[mt] = DIM == 3 ? a.Z[s] : 0.0;
@@ -119,57 +146,131 @@ __global__ void __launch_bounds__(kMThreads, 3) k2m_translate(K2MArgs a) {
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
       for (int nb = 0; nb < NB; ++nb) C[mt][nb][0] = C[mt][nb][1] = H[mt][nb][0] = H[mt][nb][1] = 0.0;
-    const bool skel_rows = task.row0 < tb.k;
-    const EntryRange er = a.er[task.box];
-    for (int e = 0; e < er.count; ++e) {
-      const int32_t code = a.ent[er.begin + e];
-      const int32_t c = code >> kModeBits;
-      const int mode = code & kModeMask;
-      const BoxRec sb = a.box[c];
-      const bool self = c == task.box;
-      for (int j0 = 0; j0 < sb.n; j0 += kChunk) {
-        // stage 16 sources: coordinates + per-mode weights for all rhs
-        __syncwarp();
-        if (lane < kChunk) {
-          const int j = j0 + lane;
-          if (j < sb.n) {
-            const int64_t s = sb.slot + j;
-            sm.x[lane] = a.X[s];
-            sm.y[lane] = a.Y[s];
-            sm.z[lane] = DIM == 3 ? a.Z[s] : 0.0;
-          } else {
-            // far away, zero weight; moderate so sincos(kappa r) stays on its
-            // fast argument-reduction path
-            sm.x[lane] = sm.y[lane] = sm.z[lane] = 1e3;
-          }
-        }
-        for (int v = lane; v < kChunk * kNRHS * SW; v += 32) {
-          const int jj = v / (kNRHS * SW), col = v % (kNRHS * SW);
-          const int j = j0 + jj;
-          double q = 0.0, qh = 0.0;
-          if (j < sb.n) {
-            q = a.Q[(sb.slot + j) * (kNRHS * SW) + col];
-            if (j < sb.k) qh = a.QH[(sb.skel + j) * (kNRHS * SW) + col];
-          }
-          double wa = q, wh = 0.0;
-          if (mode == kIFO) wh = qh;
-          else if (mode == kIFS) wh = q;
-          else if (mode == kTFO) wa = q - qh;
-          sm.a[jj][col] = wa;
-          sm.h[jj][col] = wh;
-        }
-        __syncwarp();
-        const bool need_h = skel_rows && (mode == kIFS || (mode == kIFO && j0 < sb.k));
+    const bool skel_rows = WH && task.row0 < tb.k;
+
+    // chunk iterator over (entry, first source), skipping empty source boxes
+    auto first_from = [&](int e) -> ChunkPos {
+      for (; e < er.count; ++e)
+        if (a.box[a.ent[er.begin + e] >> kModeBits].n > 0) return {e, 0};
+      return {er.count, 0};
+    };
+    auto next_of = [&](ChunkPos p) -> ChunkPos {
+      const BoxRec sb = a.box[a.ent[er.begin + p.e] >> kModeBits];
+      if (p.j0 + kChunk < sb.n) return {p.e, p.j0 + kChunk};
+      return first_from(p.e + 1);
+    };
+    // global loads of one chunk into registers (raw q and qhat)
+    // Item it of this thread is (source jj, rhs r) with the warp's 32 lanes
+    // covering one (k-step, rhs half) block in fragment-lane order, so the
+    // fragment stores below are conflict-free.
+    auto item = [&](int it, int& jj, int& r) {
+      const int g = warp + kMWarps * it;  // 0..7: (k-step, rhs half)
+      jj = 4 * (g >> 1) + (lane & 3);
+      r = 8 * (g & 1) + (lane >> 2);
+    };
+    auto load = [&](ChunkPos p, StageRegs<CPLX>& R) {
+      const BoxRec sb = a.box[a.ent[er.begin + p.e] >> kModeBits];
 #pragma unroll
-        for (int ks = 0; ks < kChunk; ks += 4) {
-          const int js = ks + kq;  // this lane's source within the chunk
+      for (int it = 0; it < ITEMS; ++it) {
+        int jj, r;
+        item(it, jj, r);
+        const int j = p.j0 + jj;
+#pragma unroll
+        for (int c = 0; c < SW; ++c) R.q[it][c] = R.qh[it][c] = 0.0;
+        if (j < sb.n) {
+          const double* qp = a.Q + ((sb.slot + j) * kNRHS + r) * SW;
+#pragma unroll
+          for (int c = 0; c < SW; ++c) R.q[it][c] = qp[c];
+          if (j < sb.k) {
+            const double* hp = a.QH + ((sb.skel + j) * kNRHS + r) * SW;
+#pragma unroll
+            for (int c = 0; c < SW; ++c) R.qh[it][c] = hp[c];
+          }
+        }
+      }
+      if (tid < kChunk) {
+        const int j = p.j0 + tid;
+        if (j < sb.n) {
+          const int64_t s = sb.slot + j;
+          R.cx = a.X[s];
+          R.cy = a.Y[s];
+          R.cz = DIM == 3 ? a.Z[s] : 0.0;
+        } else {  // far away, zero weight (moderate: sincos stays on its fast path)
+          R.cx = R.cy = R.cz = 1e3;
+        }
+      }
+    };
+    // per-mode weights, scattered into fragment order
+    auto store = [&](ChunkPos p, const StageRegs<CPLX>& R, bool need_h) {
+      const int mode = a.ent[er.begin + p.e] & kModeMask;
+#pragma unroll
+      for (int it = 0; it < ITEMS; ++it) {
+        int jj, r;
+        item(it, jj, r);
+        const int ks = jj >> 2, fl = 4 * (r & 7) + (jj & 3);  // fragment lane (== lane)
+        double wa[SW], wh[SW];
+#pragma unroll
+        for (int c = 0; c < SW; ++c) {
+          wa[c] = R.q[it][c];
+          wh[c] = 0.0;
+          if (mode == kIFO) wh[c] = R.qh[it][c];
+          else if (mode == kIFS) wh[c] = R.q[it][c];
+          else if (mode == kTFO) wa[c] = R.q[it][c] - R.qh[it][c];
+        }
+        if (CPLX) {
+          const int nb = r >> 3;
+          ch.a[ks][0][nb][fl] = wa[0];
+          ch.a[ks][0][2 + nb][fl] = wa[1];
+          ch.a[ks][CPLX ? 1 : 0][nb][fl] = -wa[1];
+          ch.a[ks][CPLX ? 1 : 0][2 + nb][fl] = wa[0];
+          if (need_h) {
+            ch.h[ks][0][nb][fl] = wh[0];
+            ch.h[ks][0][2 + nb][fl] = wh[1];
+            ch.h[ks][CPLX ? 1 : 0][nb][fl] = -wh[1];
+            ch.h[ks][CPLX ? 1 : 0][2 + nb][fl] = wh[0];
+          }
+        } else {
+          ch.a[ks][0][r >> 3][fl] = wa[0];
+          if (need_h) ch.h[ks][0][r >> 3][fl] = wh[0];
+        }
+      }
+      if (tid < kChunk) {
+        ch.x[tid] = R.cx;
+        ch.y[tid] = R.cy;
+        ch.z[tid] = R.cz;
+      }
+    };
+    auto needs_h = [&](ChunkPos p) {
+      const int32_t code = a.ent[er.begin + p.e];
+      const int mode = code & kModeMask;
+      const BoxRec sb = a.box[code >> kModeBits];
+      return skel_rows && (mode == kIFS || (mode == kIFO && p.j0 < sb.k));
+    };
+
+    ChunkPos cur = first_from(0);
+    StageRegs<CPLX> R;
+    if (cur.e < er.count) load(cur, R);
+    while (cur.e < er.count) {
+      const bool need_h = needs_h(cur);
+      __syncthreads();  // previous chunk fully consumed
+      store(cur, R, need_h);
+      __syncthreads();
+      const int32_t code = a.ent[er.begin + cur.e];
+      const bool self = (code >> kModeBits) == task.box;
+      const int j0 = cur.j0;
+      const ChunkPos nxt = next_of(cur);
+      if (nxt.e < er.count) load(nxt, R);  // in flight during the compute below
+      if (wrow0 < rend) {
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+          const int js = 4 * ks + kq;  // this lane's source within the chunk
           double gr[2], gi[2];
 #pragma unroll
           for (int mt = 0; mt < 2; ++mt) {
-            const double dx = xr[mt] - sm.x[js], dy = yr[mt] - sm.y[js];
+            const double dx = xr[mt] - ch.x[js], dy = yr[mt] - ch.y[js];
             double r2 = fma(dy, dy, dx * dx);
             if (DIM == 3) {
-              const double dz = zr[mt] - sm.z[js];
+              const double dz = zr[mt] - ch.z[js];
               r2 = fma(dz, dz, r2);
             }
             if (KER == SFMM_LAPLACE2D) {
@@ -189,59 +290,44 @@ __global__ void __launch_bounds__(kMThreads, 3) k2m_translate(K2MArgs a) {
             }
             if (self && rowi[mt] == j0 + js) gr[mt] = gi[mt] = 0.0;
           }
-          // B fragments: source js, rhs columns rq and 8 + rq
-          double b1[NB], b2[NB], h1[NB], h2[NB];
-          if (CPLX) {
-            const double ar0 = sm.a[js][2 * rq], ai0 = sm.a[js][2 * rq + 1];
-            const double ar8 = sm.a[js][2 * (8 + rq)], ai8 = sm.a[js][2 * (8 + rq) + 1];
-            b1[0] = ar0; b1[1] = ar8; b1[2] = ai0; b1[3] = ai8;
-            b2[0] = -ai0; b2[1] = -ai8; b2[2] = ar0; b2[3] = ar8;
-            if (need_h) {
-              const double hr0 = sm.h[js][2 * rq], hi0 = sm.h[js][2 * rq + 1];
-              const double hr8 = sm.h[js][2 * (8 + rq)], hi8 = sm.h[js][2 * (8 + rq) + 1];
-              h1[0] = hr0; h1[1] = hr8; h1[2] = hi0; h1[3] = hi8;
-              h2[0] = -hi0; h2[1] = -hi8; h2[2] = hr0; h2[3] = hr8;
-            }
-          } else {
-            b1[0] = sm.a[js][rq];
-            b1[1] = sm.a[js][8 + rq];
-            if (need_h) {
-              h1[0] = sm.h[js][rq];
-              h1[1] = sm.h[js][8 + rq];
+#pragma unroll
+          for (int nb = 0; nb < NB; ++nb) {
+            const double b1 = ch.a[ks][0][nb][lane];
+            const double b2 = CPLX ? ch.a[ks][CPLX ? 1 : 0][nb][lane] : 0.0;
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) {
+              dmma(C[mt][nb][0], C[mt][nb][1], gr[mt], b1);
+              if (CPLX) dmma(C[mt][nb][0], C[mt][nb][1], gi[mt], b2);
             }
           }
-#pragma unroll
-          for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-            for (int nb = 0; nb < NB; ++nb) {
-              dmma(C[mt][nb][0], C[mt][nb][1], gr[mt], b1[nb]);
-              if (CPLX) dmma(C[mt][nb][0], C[mt][nb][1], gi[mt], b2[nb]);
-            }
           if (need_h) {
 #pragma unroll
-            for (int mt = 0; mt < 2; ++mt)
+            for (int nb = 0; nb < NB; ++nb) {
+              const double b1 = ch.h[ks][0][nb][lane];
+              const double b2 = CPLX ? ch.h[ks][CPLX ? 1 : 0][nb][lane] : 0.0;
 #pragma unroll
-              for (int nb = 0; nb < NB; ++nb) {
-                dmma(H[mt][nb][0], H[mt][nb][1], gr[mt], h1[nb]);
-                if (CPLX) dmma(H[mt][nb][0], H[mt][nb][1], gi[mt], h2[nb]);
+              for (int mt = 0; mt < 2; ++mt) {
+                dmma(H[mt][nb][0], H[mt][nb][1], gr[mt], b1);
+                if (CPLX) dmma(H[mt][nb][0], H[mt][nb][1], gi[mt], b2);
               }
+            }
           }
         }
       }
+      cur = nxt;
     }
     // epilogue: lane holds rows rq (+8) and rhs columns c0, c0+1, 8+c0, 9+c0
     const double scale = CPLX ? 0.25 : (KER == SFMM_LAPLACE3D ? kInv4Pi : -kInv4Pi);
     const int c0 = kq * 2;
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) {
-      const int row = task.row0 + mt * 8 + rq;
-      // C/D fragment rows are lane/4 as well, so a lane stores its own row
+      const int row = rowi[mt];
+      if (row >= rend) continue;
       bool bad = false;
 #pragma unroll
       for (int nb = 0; nb < NB; ++nb)
         bad = bad || !isfinite(C[mt][nb][0]) || !isfinite(C[mt][nb][1]);
-      if (row < task.row0 + task.nrows && bad) verify_row_m(a, task.box, row, DIM);
-      if (row >= task.row0 + task.nrows) continue;
+      if (bad) verify_row_m(a, task.box, row, DIM);
       double* u = a.U + (tb.slot + row) * (kNRHS * SW);
       const bool skel_row = row < tb.k;
       double* uh = a.UH + (tb.skel + (skel_row ? row : 0)) * (kNRHS * SW);
@@ -419,20 +505,34 @@ int grid_m(int64_t n) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 32));
 }
 
+template <int KER, bool WH>
+int blocks_per_sm() {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2m_translate<KER, WH>, kMThreads, 0) !=
+      cudaSuccess)
+    return -1;
+  return std::max(1, per_sm);
+}
+
 }  // namespace
 
 int configure_multi(DevPlan& p, int device, size_t max_k) {
-  int sms = 0, per_sm = 0;
+  int sms = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
-  cudaError_t e;
-  if (p.kernel == SFMM_HELMHOLTZ3D)
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2m_translate<SFMM_HELMHOLTZ3D>, kMThreads, 0);
-  else if (p.kernel == SFMM_LAPLACE3D)
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2m_translate<SFMM_LAPLACE3D>, kMThreads, 0);
-  else
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2m_translate<SFMM_LAPLACE2D>, kMThreads, 0);
-  if (e != cudaSuccess) return -1;
-  p.k2m_grid = sms * std::max(1, per_sm);
+  int bh, b0;
+  if (p.kernel == SFMM_HELMHOLTZ3D) {
+    bh = blocks_per_sm<SFMM_HELMHOLTZ3D, true>();
+    b0 = blocks_per_sm<SFMM_HELMHOLTZ3D, false>();
+  } else if (p.kernel == SFMM_LAPLACE3D) {
+    bh = blocks_per_sm<SFMM_LAPLACE3D, true>();
+    b0 = blocks_per_sm<SFMM_LAPLACE3D, false>();
+  } else {
+    bh = blocks_per_sm<SFMM_LAPLACE2D, true>();
+    b0 = blocks_per_sm<SFMM_LAPLACE2D, false>();
+  }
+  if (bh < 0 || b0 < 0) return -1;
+  p.k2m_grid = sms * bh;
+  p.k2m_grid0 = sms * b0;
   const size_t sw = p.cplx ? 16 : 8;
   p.down_m_smem = std::max<size_t>(max_k * kNRHS * sw, 16);
   if (p.down_m_smem > 48 * 1024) {
@@ -500,8 +600,6 @@ void launch_translate_m(const DevPlan& p, DevState& s, cudaStream_t st) {
   a.box = p.box;
   a.er = p.ent_range_full;
   a.ent = p.entries_full;
-  a.tasks = p.tasks_m;
-  a.n_tasks = p.n_tasks_m;
   a.X = p.X;
   a.Y = p.Y;
   a.Z = p.Z;
@@ -510,17 +608,33 @@ void launch_translate_m(const DevPlan& p, DevState& s, cudaStream_t st) {
   a.QH = s.QH;
   a.U = s.U;
   a.UH = s.UH;
-  a.counter = p.counter + 2;
   a.err = p.err_flag;
   a.kappa = p.kappa;
-  cudaMemsetAsync(p.counter + 2, 0, sizeof(int), st);
-  const int grid = (int)std::min<int64_t>(p.k2m_grid, (p.n_tasks_m + kMWarps - 1) / kMWarps);
-  if (p.kernel == SFMM_HELMHOLTZ3D)
-    k2m_translate<SFMM_HELMHOLTZ3D><<<grid, kMThreads, 0, st>>>(a);
-  else if (p.kernel == SFMM_LAPLACE3D)
-    k2m_translate<SFMM_LAPLACE3D><<<grid, kMThreads, 0, st>>>(a);
-  else
-    k2m_translate<SFMM_LAPLACE2D><<<grid, kMThreads, 0, st>>>(a);
+  cudaMemsetAsync(p.counter + 2, 0, 2 * sizeof(int), st);
+  // tasks [0, n_tasks_mh) own skeleton rows, the rest do not
+  for (int part = 0; part < 2; ++part) {
+    const int64_t t0 = part == 0 ? 0 : p.n_tasks_mh;
+    const int64_t t1 = part == 0 ? p.n_tasks_mh : p.n_tasks_m;
+    if (t1 <= t0) continue;
+    a.tasks = p.tasks_m + t0;
+    a.n_tasks = t1 - t0;
+    a.counter = p.counter + 2 + part;
+    const int grid = (int)std::min<int64_t>(part == 0 ? p.k2m_grid : p.k2m_grid0, t1 - t0);
+#define SFMM_K2M_LAUNCH(KER)                                                        \
+  do {                                                                              \
+    if (part == 0)                                                                  \
+      k2m_translate<KER, true><<<grid, kMThreads, 0, st>>>(a);                      \
+    else                                                                            \
+      k2m_translate<KER, false><<<grid, kMThreads, 0, st>>>(a);                     \
+  } while (0)
+    if (p.kernel == SFMM_HELMHOLTZ3D)
+      SFMM_K2M_LAUNCH(SFMM_HELMHOLTZ3D);
+    else if (p.kernel == SFMM_LAPLACE3D)
+      SFMM_K2M_LAUNCH(SFMM_LAPLACE3D);
+    else
+      SFMM_K2M_LAUNCH(SFMM_LAPLACE2D);
+#undef SFMM_K2M_LAUNCH
+  }
 }
 
 }  // namespace sfmm_gpu

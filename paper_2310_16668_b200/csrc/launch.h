@@ -52,7 +52,8 @@ struct DevPlan {
   Task* tasks_m;
   int64_t n_tasks_m;
   LevelItem* down_m_items;
-  int k2m_grid;
+  int64_t n_tasks_mh;  // tasks_m[0, n_tasks_mh) own skeleton rows
+  int k2m_grid, k2m_grid0;
   size_t down_m_smem;
   int* counter;     // K2 task counters (interior, boundary, multi; reset per launch)
   int* err_flag;    // sticky duplicate-point flag

@@ -355,9 +355,17 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
           tv.push_back({src * kMultiRows + 64.0,
                         Task{b, r0, std::min(kMultiRows, hp.box[b].n - r0), 0, 0}});
       }
-      std::stable_sort(tv.begin(), tv.end(),
-                       [](const auto& a, const auto& b) { return a.first > b.first; });
-      for (auto& e : tv) hp.tasks_m.push_back(e.second);
+      // tasks owning skeleton rows first (they need the uhat accumulators and
+      // run a heavier kernel variant), each group longest first
+      std::stable_sort(tv.begin(), tv.end(), [&](const auto& a, const auto& b) {
+        const bool ha = a.second.row0 < hp.box[a.second.box].k;
+        const bool hb = b.second.row0 < hp.box[b.second.box].k;
+        return ha != hb ? ha : a.first > b.first;
+      });
+      for (auto& e : tv) {
+        hp.tasks_m.push_back(e.second);
+        if (e.second.row0 < hp.box[e.second.box].k) ++hp.n_tasks_mh;
+      }
     }
 
     // ghost exchange lists: box c owned by p is sent to q if one of q's

@@ -25,7 +25,7 @@ constexpr int kRowsPerLane = 4;                 // max rows per lane in K2
 constexpr int kTileRows = 32 * kRowsPerLane;    // rows per K2 task
 constexpr int kUpRows = 32;                     // K1 rows (skeleton entries) per CTA
 constexpr int kDownCols = 256;                  // K3 columns (redundant slots) per CTA
-constexpr int kMultiRows = 16;                  // K2m rows per task (two 8-row DMMA tiles)
+constexpr int kMultiRows = 64;                  // K2m rows per task (4 warps x two 8-row DMMA tiles)
 constexpr int kDownColsM = 16;                  // K3m columns per CTA (x 16 rhs threads)
 
 struct LevelItem {
@@ -77,6 +77,7 @@ struct HostPlan {
   std::vector<EntryRange> ent_range_full;
   std::vector<int32_t> entries_full;
   std::vector<Task> tasks_m;
+  int64_t n_tasks_mh = 0;                     // tasks_m[0, n_tasks_mh) own skeleton rows
   std::vector<LevelItem> down_m_items;
   std::vector<int64_t> down_m_lvl;
   // owned interpolation blocks copied from the descriptor into a compact blob

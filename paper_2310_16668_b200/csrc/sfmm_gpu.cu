@@ -281,6 +281,7 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
       dp.entries_full = p->upload(hp.entries_full);
       dp.tasks_m = p->upload(hp.tasks_m);
       dp.n_tasks_m = (int64_t)hp.tasks_m.size();
+      dp.n_tasks_mh = hp.n_tasks_mh;
       dp.down_m_items = p->upload(hp.down_m_items);
       dp.pack_idx = p->upload(hp.pack_idx);
       dp.unpack_idx = p->upload(hp.unpack_idx);
