@@ -65,6 +65,8 @@ def parse():
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="multi-rank exchange; gloo stages through host memory (test path)")
     ap.add_argument("--nrhs", type=int, default=1)
+    ap.add_argument("--precompute", default="gpu", choices=["gpu", "host"],
+                    help="skeletons from the GPU skeletonizer or the host C++ one (tree: host)")
     ap.add_argument("--config", default=None, choices=sorted(CONFIGS),
                     help="BASELINE.json configs (secondary measurement lines; default = headline)")
     args = ap.parse_args()
@@ -253,7 +255,9 @@ def run_sharded(args, ws, rank, local):
     if rank == 0:
         # torchrun sets OMP_NUM_THREADS=1; the other ranks wait at the barrier
         host.set_threads(os.cpu_count() or 1)
-        hp = host.HostPlan.build(kern, pts, args.leaf, args.tol, args.kappa)
+        hp = (host.HostPlan.build_gpu(kern, pts, args.leaf, args.tol, args.kappa)
+              if args.precompute == "gpu" else
+              host.HostPlan.build(kern, pts, args.leaf, args.tol, args.kappa))
         hinfo = hp.info()
         _share_descriptor(hp, path)
     dist.barrier()
@@ -411,7 +415,9 @@ def main():
     if nrhs > 1:
         q = np.asfortranarray(np.stack([gen(n, (1 + r) ^ CHARGE_STREAM) for r in range(nrhs)], 1))
     t_gen = time.perf_counter() - t0
-    hp = host.HostPlan.build(kern, pts, args.leaf, args.tol, args.kappa)
+    hp = (host.HostPlan.build_gpu(kern, pts, args.leaf, args.tol, args.kappa)
+              if args.precompute == "gpu" else
+              host.HostPlan.build(kern, pts, args.leaf, args.tol, args.kappa))
     hinfo = hp.info()
     t0 = time.perf_counter()
     plan = api.GpuPlan(hp.desc_struct(), device=dev)
@@ -557,7 +563,9 @@ def main():
                        "t_skel_s": hinfo["t_skel"], "t_upload_s": t_upload,
                        "depth": hinfo["depth"], "n_boxes": hinfo["n_boxes"],
                        "k_max": hinfo["k_max"], "m_proj": hinfo["proj_scalars"],
-                       "host_threads": host.get_threads()},
+                       "host_threads": host.get_threads(),
+                       "skeletons": "GPU skeletonizer (sfmm_gpu_build_skeletons)"
+                       if args.precompute == "gpu" else "host C++ skeletonizer"},
     }
 
     # ---- CPU baseline: the unmodified reference apply on the same plan ----

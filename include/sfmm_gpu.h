@@ -195,6 +195,47 @@ int sfmm_gpu_shard_describe(const sfmm_plan_desc* desc, int n_ranks, int rank, i
                             int32_t* owner, int64_t* pack_idx, int64_t* unpack_idx,
                             int32_t* owned_points);
 
+/*
+ * GPU skeletonization: the device counterpart of the
+ * reference's build_skeletons (/root/reference/proj/src/skeleton.cpp:184-260).
+ * Input: the tree (box geometry included, since proxy surfaces are built from
+ * box centres and half-widths).  Output: the skeleton fields of an
+ * sfmm_plan_desc (index_vec, skel_pos, red_pos, interp T, parent_offset), held
+ * by an opaque result until destroyed.  Same algorithm as the reference:
+ * proxy matrix from the Lobatto proxy surface (stacked with its conjugate for
+ * complex kernels), greedy Householder column-pivoted QR stopped at
+ * tol * (largest initial column norm) with the dqp3 norm downdate,
+ * T = R11^{-1} R12, positions sorted ascending.  Pivot choices are
+ * rounding-sensitive, so results are compared by accuracy, not bits.
+ */
+typedef struct sfmm_tree_desc {
+  int32_t dim;
+  int64_t n_points;
+  int32_t n_boxes;
+  int32_t depth;
+  const double* pts;          /* tree order, interleaved */
+  const int32_t* level_begin; /* depth+2 */
+  const int32_t* box_parent;
+  const int32_t* box_level;
+  const int32_t* box_begin;
+  const int32_t* box_end;
+  const uint8_t* box_leaf;
+  const double* box_center;   /* n_boxes * 3 */
+  const double* box_half;     /* n_boxes */
+} sfmm_tree_desc;
+
+typedef struct sfmm_skel_result sfmm_skel_result;
+
+int sfmm_gpu_build_skeletons(const sfmm_tree_desc* tree, int kernel, double kappa, double tol,
+                             double proxy_radius, int proxy_edge2d, int proxy_face3d, int device,
+                             sfmm_skel_result** out);
+/* Points the skeleton fields of *desc (iv_off, iv, sk_off, skel_pos, rd_off,
+ * red_pos, T_off, T, box_parent_offset) at the result's arrays and returns
+ * k_max, proj_scalars and the number of saturated boxes. */
+int sfmm_gpu_skel_fill(sfmm_skel_result* res, sfmm_plan_desc* desc, int32_t* k_max,
+                       int64_t* proj_scalars, int32_t* saturated, double* seconds);
+void sfmm_gpu_skel_destroy(sfmm_skel_result* res);
+
 /* Phase timing.  While enabled, every apply records CUDA events on its stream
  * around its five phases (0 gather, 1 upward, 2 translate, 3 downward,
  * 4 scatter).  sfmm_gpu_get_timings synchronises, writes ms[5*i + phase] for

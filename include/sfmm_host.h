@@ -76,6 +76,16 @@ int sfmm_host_build(int kernel, double kappa, int dim, int64_t n, const double* 
 /* Flat view of the plan; valid until sfmm_host_destroy. */
 const sfmm_plan_desc* sfmm_host_desc(sfmm_host_plan* plan);
 
+/* Box geometry (centre: n_boxes*3, half-width: n_boxes), needed by the GPU
+ * skeletonizer's proxy surfaces (sfmm_tree_desc in sfmm_gpu.h). */
+int sfmm_host_box_geometry(const sfmm_host_plan* plan, double* center, double* half);
+
+/* Replaces the plan's skeleton fields with externally built ones (e.g. from
+ * sfmm_gpu_build_skeletons); the arrays are copied. */
+int sfmm_host_set_skeletons(sfmm_host_plan* plan, const sfmm_plan_desc* skel, int kernel,
+                            double kappa, int32_t k_max, int64_t proj_scalars, int32_t saturated,
+                            double t_skel);
+
 int sfmm_host_info_get(const sfmm_host_plan* plan, sfmm_host_info* info);
 
 void sfmm_host_destroy(sfmm_host_plan* plan);

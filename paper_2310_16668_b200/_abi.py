@@ -98,6 +98,26 @@ class PlanInfo(C.Structure):
     ]
 
 
+class TreeDesc(C.Structure):
+    """struct sfmm_tree_desc (input of the GPU skeletonizer)."""
+
+    _fields_ = [
+        ("dim", C.c_int32),
+        ("n_points", C.c_int64),
+        ("n_boxes", C.c_int32),
+        ("depth", C.c_int32),
+        ("pts", _f64p),
+        ("level_begin", _i32p),
+        ("box_parent", _i32p),
+        ("box_level", _i32p),
+        ("box_begin", _i32p),
+        ("box_end", _i32p),
+        ("box_leaf", _u8p),
+        ("box_center", _f64p),
+        ("box_half", _f64p),
+    ]
+
+
 # (field, dtype) of every array in the descriptor, in struct order
 DESC_ARRAYS = [
     ("pts", np.float64),
@@ -280,6 +300,13 @@ def gpu_lib() -> C.CDLL:
     lib.sfmm_gpu_shard_describe.argtypes = [C.POINTER(PlanDesc), C.c_int, C.c_int, vp, vp, vp, vp,
                                             vp]
     lib.sfmm_gpu_shard_describe.restype = C.c_int
+    lib.sfmm_gpu_build_skeletons.argtypes = [C.POINTER(TreeDesc), C.c_int, C.c_double, C.c_double,
+                                             C.c_double, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]
+    lib.sfmm_gpu_build_skeletons.restype = C.c_int
+    lib.sfmm_gpu_skel_fill.argtypes = [vp, C.POINTER(PlanDesc), vp, vp, vp, vp]
+    lib.sfmm_gpu_skel_fill.restype = C.c_int
+    lib.sfmm_gpu_skel_destroy.argtypes = [vp]
+    lib.sfmm_gpu_skel_destroy.restype = None
     _gpu_lib = lib
     return lib
 
@@ -290,4 +317,5 @@ GPU_SYMBOLS = [
     "sfmm_gpu_last_error", "sfmm_gpu_version", "sfmm_gpu_set_timing", "sfmm_gpu_get_timings",
     "sfmm_gpu_fp64_peak", "sfmm_gpu_plan_create_sharded", "sfmm_gpu_shard_info",
     "sfmm_gpu_apply_begin", "sfmm_gpu_apply_end", "sfmm_gpu_shard_describe",
+    "sfmm_gpu_build_skeletons", "sfmm_gpu_skel_fill", "sfmm_gpu_skel_destroy",
 ]

@@ -276,6 +276,43 @@ int sfmm_host_build(int kernel, double kappa, int dim, int64_t n, const double* 
 
 const sfmm_plan_desc* sfmm_host_desc(sfmm_host_plan* p) { return p ? &p->desc : nullptr; }
 
+int sfmm_host_box_geometry(const sfmm_host_plan* p, double* center, double* half) {
+  if (!p || !center || !half) return fail(SFMM_EINVAL, "null argument");
+  const auto& boxes = p->tree.boxes;
+  for (size_t b = 0; b < boxes.size(); ++b) {
+    for (int k = 0; k < 3; ++k) center[3 * b + k] = boxes[b].center[k];
+    half[b] = boxes[b].half;
+  }
+  return SFMM_OK;
+}
+
+int sfmm_host_set_skeletons(sfmm_host_plan* p, const sfmm_plan_desc* s, int kernel, double kappa,
+                            int32_t k_max, int64_t proj_scalars, int32_t saturated,
+                            double t_skel) {
+  if (!p || !s) return fail(SFMM_EINVAL, "null argument");
+  return guarded([&] {
+    const int64_t nb = (int64_t)p->tree.boxes.size();
+    const int sw = kernel == SFMM_HELMHOLTZ3D || kernel == SFMM_HELMHOLTZ2D ? 2 : 1;
+    auto& k = p->sk;
+    k.iv_off.assign(s->iv_off, s->iv_off + nb + 1);
+    k.sk_off.assign(s->sk_off, s->sk_off + nb + 1);
+    k.rd_off.assign(s->rd_off, s->rd_off + nb + 1);
+    k.T_off.assign(s->T_off, s->T_off + nb + 1);
+    k.iv.assign(s->iv, s->iv + k.iv_off[nb]);
+    k.skel_pos.assign(s->skel_pos, s->skel_pos + k.sk_off[nb]);
+    k.red_pos.assign(s->red_pos, s->red_pos + k.rd_off[nb]);
+    k.T.assign(s->T, s->T + k.T_off[nb] * sw);
+    k.parent_offset.assign(s->box_parent_offset, s->box_parent_offset + nb);
+    k.k_max = k_max;
+    k.proj_scalars = proj_scalars;
+    k.saturated = saturated;
+    p->kernel = kernel;
+    p->kappa = kappa;
+    p->info.t_skel = t_skel;
+    p->export_desc();
+  });
+}
+
 int sfmm_host_info_get(const sfmm_host_plan* p, sfmm_host_info* info) {
   if (!p || !info) return fail(SFMM_EINVAL, "null argument");
   *info = p->info;

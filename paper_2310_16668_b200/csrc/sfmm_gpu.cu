@@ -25,13 +25,19 @@
 using namespace sfmm_gpu;
 
 namespace {
-
 thread_local std::string g_last_error;
+}  // namespace
 
-int set_error(int code, const std::string& msg) {
+namespace sfmm_gpu {
+int set_last_error(int code, const std::string& msg) {
   g_last_error = msg;
   return code;
 }
+}  // namespace sfmm_gpu
+
+namespace {
+
+int set_error(int code, const std::string& msg) { return sfmm_gpu::set_last_error(code, msg); }
 
 struct CudaFail {
   int code;

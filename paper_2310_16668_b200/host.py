@@ -64,6 +64,9 @@ def host_lib() -> C.CDLL:
         lib.sfmm_host_set_threads.restype = None
         lib.sfmm_host_get_threads.restype = C.c_int
         lib.sfmm_host_last_error.restype = C.c_char_p
+        lib.sfmm_host_box_geometry.argtypes = [vp, vp, vp]
+        lib.sfmm_host_set_skeletons.argtypes = [vp, C.POINTER(PlanDesc), C.c_int, C.c_double,
+                                                C.c_int32, C.c_int64, C.c_int32, C.c_double]
         _lib = lib
     return _lib
 
@@ -121,6 +124,40 @@ class HostPlan:
                                           pts.ctypes.data, leaf_cap, tol, C.byref(px),
                                           C.byref(h)))
         return cls(h)
+
+    @classmethod
+    def build_gpu(cls, kernel: int, pts: np.ndarray, leaf_cap: int, tol: float,
+                  kappa: float = 1.0, proxy: tuple | None = None, device: int = 0) -> "HostPlan":
+        """Tree and neighbor lists on the host (bit-identical to the reference),
+        skeletons on the GPU (sfmm_gpu_build_skeletons)."""
+        from .api import _raise
+        hp = cls.build_tree(pts, leaf_cap)
+        d = host_lib().sfmm_host_desc(hp._h).contents
+        nb = int(d.n_boxes)
+        center = np.zeros(3 * nb)
+        half = np.zeros(nb)
+        _check(host_lib().sfmm_host_box_geometry(hp._h, center.ctypes.data, half.ctypes.data))
+        t = _abi.TreeDesc()
+        t.dim, t.n_points, t.n_boxes, t.depth = d.dim, d.n_points, d.n_boxes, d.depth
+        for f in ("pts", "level_begin", "box_parent", "box_level", "box_begin", "box_end", "box_leaf"):
+            setattr(t, f, getattr(d, f))
+        t.box_center = center.ctypes.data_as(C.POINTER(C.c_double))
+        t.box_half = half.ctypes.data_as(C.POINTER(C.c_double))
+        px = proxy or (0.0, 0, 0)
+        res = C.c_void_p()
+        lib = _abi.gpu_lib()
+        _raise(lib.sfmm_gpu_build_skeletons(C.byref(t), kernel, kappa, tol, float(px[0]), int(px[1]),
+                                            int(px[2]), device, C.byref(res)))
+        try:
+            sk = PlanDesc()
+            kmax, proj, sat, secs = C.c_int32(), C.c_int64(), C.c_int32(), C.c_double()
+            _raise(lib.sfmm_gpu_skel_fill(res, C.byref(sk), C.byref(kmax), C.byref(proj),
+                                          C.byref(sat), C.byref(secs)))
+            _check(host_lib().sfmm_host_set_skeletons(hp._h, C.byref(sk), kernel, kappa, kmax,
+                                                      proj, sat, secs))
+        finally:
+            lib.sfmm_gpu_skel_destroy(res)
+        return hp
 
     @classmethod
     def build_tree(cls, pts: np.ndarray, leaf_cap: int) -> "HostPlan":

@@ -1,0 +1,94 @@
+"""GPU skeletonization against the reference criteria.
+
+Same checks as the host skeletonizer (tests/test_host.py) and the reference's
+own tests: accuracy of the resulting apply against the dense sum
+(test_apply.cpp:108-162), the ID far-field property and skeleton nesting
+(acceptance.cpp C6), and apply parity on the GPU-built operators.
+"""
+import numpy as np
+import pytest
+
+from conftest import max_rel, rel_l2, requires_ref
+from oracle import pyoracle as po
+from paper_2310_16668_b200 import api, host
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("kernel,dist,kappa", [
+    (0, "square", 1.0), (0, "annulus", 1.0), (1, "cube", 1.0), (1, "sphere", 1.0),
+    (3, "cube", 2.0), (3, "sphere", 2.0),
+])
+def test_gpu_skeletons_meet_tolerance(kernel, dist, kappa):
+    n, tol = 1500, 1e-6
+    pts = host.generate_points(dist, n, 100)
+    d = host.HostPlan.build_gpu(kernel, pts, 40, tol, kappa).descriptor()
+    assert d.scalars["depth"] >= 2
+    q = host.generate_charges(n, 200)
+    if kernel == 3:
+        q = q.astype(np.complex128)
+    u, _ = po.oracle_apply(d, q)
+    assert max_rel(u, po.oracle_direct_sum(kernel, kappa, pts, q)) <= 10 * tol
+
+
+@pytest.mark.parametrize("kernel,dist,n,leaf,tol", [
+    (1, "cube", 20000, 64, 1e-6), (1, "sphere", 20000, 40, 1e-8), (0, "annulus", 8000, 30, 1e-6),
+    (3, "cube", 8000, 64, 1e-6),
+])
+def test_gpu_skeleton_ranks_match_host(kernel, dist, n, leaf, tol):
+    pts = host.generate_points(dist, n, 7)
+    kappa = 10.0 if kernel == 3 else 1.0
+    ig = host.HostPlan.build_gpu(kernel, pts, leaf, tol, kappa).info()
+    ic = host.HostPlan.build(kernel, pts, leaf, tol, kappa).info()
+    # same algorithm; rounding may move a pivot, so compare totals loosely
+    assert abs(ig["k_max"] - ic["k_max"]) <= 2
+    assert abs(ig["proj_scalars"] - ic["proj_scalars"]) <= 0.01 * ic["proj_scalars"]
+
+
+def test_gpu_skeleton_id_residual_and_nesting():
+    pts = host.generate_points("annulus", 4000, 29)
+    d = host.HostPlan.build_gpu(0, pts, 50, 1e-6).descriptor()
+    a = d.arrays
+    P2 = a["pts"].reshape(-1, 2)
+    checked = 0
+    for b in range(d.scalars["n_boxes"]):
+        k = a["sk_off"][b + 1] - a["sk_off"][b]
+        r = a["rd_off"][b + 1] - a["rd_off"][b]
+        if k == 0 or r == 0:
+            continue
+        iv = a["iv"][a["iv_off"][b]:a["iv_off"][b + 1]]
+        sk = a["skel_pos"][a["sk_off"][b]:a["sk_off"][b + 1]]
+        rd = a["red_pos"][a["rd_off"][b]:a["rd_off"][b + 1]]
+        assert np.all(np.diff(sk) > 0) and np.all(np.diff(rd) > 0)
+        Tb = a["T"][a["T_off"][b]:a["T_off"][b + 1]].reshape(k, r)
+        x = P2[iv]
+        c = 0.5 * (x.min(0) + x.max(0))
+        h = 0.5 * float(np.max(x.max(0) - x.min(0)))
+        ang = np.linspace(0, 2 * np.pi, 64, endpoint=False)
+        y = c + 6 * max(h, 1e-3) * np.stack([np.cos(ang), np.sin(ang)], 1)
+        G = np.log(((y[:, None, :] - x[None, :, :]) ** 2).sum(-1)) * (-1 / (4 * np.pi))
+        assert np.abs(G[:, sk] @ Tb - G[:, rd]).max() / np.abs(G).max() <= 1e-4
+        kids = np.nonzero(a["box_parent"] == b)[0]
+        owned = []
+        for ch in kids:
+            civ = a["iv"][a["iv_off"][ch]:a["iv_off"][ch + 1]]
+            csk = a["skel_pos"][a["sk_off"][ch]:a["sk_off"][ch + 1]]
+            owned.extend(civ[csk])
+        if len(kids):
+            assert sorted(owned) == sorted(iv.tolist())
+        checked += 1
+    assert checked > 10
+
+
+@requires_ref
+@pytest.mark.parametrize("kernel,dist,n,kappa", [(1, "cube", 200000, 1.0), (3, "cube", 40000, 10.0),
+                                                 (1, "sphere", 100000, 1.0)])
+def test_apply_parity_on_gpu_skeletons(kernel, dist, n, kappa):
+    pts = host.generate_points(dist, n, 1)
+    hp = host.HostPlan.build_gpu(kernel, pts, 128, 1e-6, kappa)
+    q = host.generate_charges_complex(n, 4) if kernel == 3 else host.generate_charges(n, 4)
+    u = api.fmm_apply(api.GpuPlan(hp.desc_struct()), q)
+    u_ref, _ = po.RefPipeline.from_desc(hp.desc_struct()).apply(q, kernel == 3)
+    assert rel_l2(u, u_ref) <= 1e-12
+    t = np.arange(0, n, n // 200, dtype=np.int32)
+    assert max_rel(u[t], api.direct_sum_subset(kernel, kappa, pts, q, t)) <= 1e-5
