@@ -98,6 +98,7 @@ struct sfmm_gpu_plan {
     if (ev_k2a) cudaEventDestroy(ev_k2a);
     if (ev_k2b) cudaEventDestroy(ev_k2b);
     for (cudaEvent_t e : tev) cudaEventDestroy(e);
+    if (graph_exec) cudaGraphExecDestroy(graph_exec);
     if (stream) cudaStreamDestroy(stream);
   }
 
@@ -111,6 +112,12 @@ struct sfmm_gpu_plan {
     ck(cudaMalloc(&io_u, bytes), "cudaMalloc(u)");
     io_cap = bytes;
   }
+
+  // CUDA graph of the last (q, u, nrhs) enqueued through sfmm_gpu_apply_async
+  cudaGraphExec_t graph_exec = nullptr;
+  const double* graph_q = nullptr;
+  double* graph_u = nullptr;
+  int graph_nrhs = 0;
 
   // Phase timing: 6 events per recorded apply (phase boundaries).
   static constexpr int kMaxTimed = 256;
@@ -505,8 +512,32 @@ int sfmm_gpu_apply_async(sfmm_gpu_plan* p, const void* q_dev, void* u_dev, int n
   try {
     ck(cudaSetDevice(p->device), "cudaSetDevice");
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : p->stream;
-    p->enqueue_cols(static_cast<const double*>(q_dev), static_cast<double*>(u_dev), nrhs, st,
-                    false);
+    const double* qd = static_cast<const double*>(q_dev);
+    double* ud = static_cast<double*>(u_dev);
+    // Repeated applies on the same buffers replay one CUDA graph of the whole
+    // sequence (~15-45 launches): launch overhead matters for small trees.
+    static const bool env_graphs = [] {
+      const char* v = std::getenv("SFMM_GRAPHS");
+      return !(v && std::atoi(v) == 0);
+    }();
+    if (env_graphs && !p->timing && stream != nullptr) {
+      if (!p->graph_exec || p->graph_q != qd || p->graph_u != ud || p->graph_nrhs != nrhs) {
+        if (p->graph_exec) cudaGraphExecDestroy(p->graph_exec);
+        p->graph_exec = nullptr;
+        cudaGraph_t g = nullptr;
+        ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
+        p->enqueue_cols(qd, ud, nrhs, st, false);
+        ck(cudaStreamEndCapture(st, &g), "end capture");
+        ck(cudaGraphInstantiate(&p->graph_exec, g, 0), "graph instantiate");
+        cudaGraphDestroy(g);
+        p->graph_q = qd;
+        p->graph_u = ud;
+        p->graph_nrhs = nrhs;
+      }
+      ck(cudaGraphLaunch(p->graph_exec, st), "graph launch");
+    } else {
+      p->enqueue_cols(qd, ud, nrhs, st, false);
+    }
     ck(cudaGetLastError(), "kernel launch");
     return SFMM_OK;
   } catch (const CudaFail& f) {
