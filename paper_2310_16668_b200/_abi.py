@@ -307,6 +307,8 @@ def gpu_lib() -> C.CDLL:
     lib.sfmm_gpu_skel_fill.restype = C.c_int
     lib.sfmm_gpu_skel_destroy.argtypes = [vp]
     lib.sfmm_gpu_skel_destroy.restype = None
+    lib.sfmm_gpu_test_sincos.argtypes = [vp, C.c_int64, vp]
+    lib.sfmm_gpu_test_sincos.restype = C.c_int
     _gpu_lib = lib
     return lib
 
@@ -318,4 +320,5 @@ GPU_SYMBOLS = [
     "sfmm_gpu_fp64_peak", "sfmm_gpu_plan_create_sharded", "sfmm_gpu_shard_info",
     "sfmm_gpu_apply_begin", "sfmm_gpu_apply_end", "sfmm_gpu_shard_describe",
     "sfmm_gpu_build_skeletons", "sfmm_gpu_skel_fill", "sfmm_gpu_skel_destroy",
+    "sfmm_gpu_test_sincos",
 ]

@@ -21,6 +21,7 @@
 
 #include <algorithm>
 
+#include "fastmath.cuh"
 #include "launch.h"
 
 namespace sfmm_gpu {
@@ -280,7 +281,7 @@ __global__ void __launch_bounds__(kMThreads, WH ? 2 : 3) k2m_translate(K2MArgs a
               const double yv = rsqrt_fp64m(r2);
               if (CPLX) {
                 double sn, cs;
-                sincos(a.kappa * (r2 * yv), &sn, &cs);
+                sincos_fast(a.kappa * (r2 * yv), &sn, &cs);
                 gr[mt] = cs * yv;
                 gi[mt] = sn * yv;
               } else {

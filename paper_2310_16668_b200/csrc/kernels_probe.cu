@@ -4,9 +4,41 @@
 
 #include <algorithm>
 
+#include "fastmath.cuh"
 #include "launch.h"
+#include "sfmm_gpu.h"
 
 namespace sfmm_gpu {
+namespace {
+
+__global__ void sincos_check(const double* x, int64_t n, double* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double s, c, s_ref, c_ref;
+    sincos_fast(x[i], &s, &c);
+    sincos(x[i], &s_ref, &c_ref);
+    out[4 * i] = s;
+    out[4 * i + 1] = c;
+    out[4 * i + 2] = s_ref;
+    out[4 * i + 3] = c_ref;
+  }
+}
+
+}  // namespace
+
+int test_sincos(const double* x_host, int64_t n, double* out_host) {
+  double *dx = nullptr, *dout = nullptr;
+  if (cudaMalloc(&dx, n * sizeof(double)) != cudaSuccess) return -1;
+  if (cudaMalloc(&dout, 4 * n * sizeof(double)) != cudaSuccess) return -1;
+  cudaMemcpy(dx, x_host, n * sizeof(double), cudaMemcpyHostToDevice);
+  sincos_check<<<148 * 4, 256>>>(dx, n, dout);
+  cudaMemcpy(out_host, dout, 4 * n * sizeof(double), cudaMemcpyDeviceToHost);
+  const bool ok = cudaGetLastError() == cudaSuccess;
+  cudaFree(dx);
+  cudaFree(dout);
+  return ok ? 0 : -1;
+}
+
 namespace {
 
 constexpr int kChains = 8;

@@ -28,6 +28,7 @@
 
 #include <algorithm>
 
+#include "fastmath.cuh"
 #include "launch.h"
 
 namespace sfmm_gpu {
@@ -347,7 +348,7 @@ __device__ __forceinline__ void inner_cplx(const WarpSmemCplx& sm, int cnt, int 
       const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
       const double y = rsqrt_fp64(r2);
       double s, c;
-      sincos(kappa * (r2 * y), &s, &c);
+      sincos_fast(kappa * (r2 * y), &s, &c);
       double gr = c * y, gi = s * y;
       if (SELF && rowi[r] == j0 + jj) {
         gr = 0.0;

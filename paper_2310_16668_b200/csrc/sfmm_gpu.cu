@@ -524,9 +524,17 @@ int sfmm_gpu_apply_async(sfmm_gpu_plan* p, const void* q_dev, void* u_dev, int n
       if (!p->graph_exec || p->graph_q != qd || p->graph_u != ud || p->graph_nrhs != nrhs) {
         if (p->graph_exec) cudaGraphExecDestroy(p->graph_exec);
         p->graph_exec = nullptr;
+        // device state is allocated before the capture (no cudaMalloc inside it)
+        if (nrhs > 1) p->ensure_multi();
         cudaGraph_t g = nullptr;
         ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
-        p->enqueue_cols(qd, ud, nrhs, st, false);
+        try {
+          p->enqueue_cols(qd, ud, nrhs, st, false);
+        } catch (...) {
+          cudaStreamEndCapture(st, &g);  // leave the caller's stream usable
+          if (g) cudaGraphDestroy(g);
+          throw;
+        }
         ck(cudaStreamEndCapture(st, &g), "end capture");
         ck(cudaGraphInstantiate(&p->graph_exec, g, 0), "graph instantiate");
         cudaGraphDestroy(g);
@@ -621,6 +629,12 @@ int sfmm_gpu_get_timings(sfmm_gpu_plan* p, float* ms, int max_applies, int* n_ap
   } catch (const CudaFail& f) {
     return set_error(f.code, f.msg);
   }
+}
+
+int sfmm_gpu_test_sincos(const double* x, int64_t n, double* out) {
+  if (!x || !out || n < 0) return set_error(SFMM_EINVAL, "null argument");
+  return sfmm_gpu::test_sincos(x, n, out) == 0 ? SFMM_OK
+                                                : set_error(SFMM_ECUDA, "sincos check failed");
 }
 
 int sfmm_gpu_fp64_peak(int device, double* tflops) {

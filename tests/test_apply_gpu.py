@@ -174,6 +174,26 @@ def test_device_buffer_path_matches_host_path():
     assert np.array_equal(ud.cpu().numpy(), u_host)
 
 
+def test_device_path_graph_replay_multi_rhs():
+    """Repeated device applies on a user stream replay a captured CUDA graph;
+    the first capture of a multi-RHS apply must not allocate inside it."""
+    import torch
+    n, nrhs = 20000, 5
+    _, _, plan = _pipeline(1, "cube", n, 64, 1e-6)
+    Q = np.asfortranarray(np.stack([host.generate_charges(n, 20 + r) for r in range(nrhs)], 1))
+    U = api.fmm_apply(plan, Q)
+    qd = torch.from_numpy(Q.T.copy()).cuda()        # column-major == rows of Q.T
+    ud = torch.empty_like(qd)
+    s = torch.cuda.Stream()
+    for _ in range(3):
+        ud.zero_()
+        torch.cuda.current_stream().synchronize()
+        api.fmm_apply_device(plan, qd.data_ptr(), ud.data_ptr(), nrhs, s.cuda_stream)
+        s.synchronize()
+        api.check_status(plan)
+        assert np.array_equal(ud.cpu().numpy().T, U)
+
+
 @requires_ref
 @pytest.mark.parametrize("kernel,dist,n,leaf,tol,kappa", [
     (0, "square", 100000, 64, 1e-6, 1.0),      # config 1
