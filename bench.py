@@ -417,12 +417,14 @@ def main():
     if nrhs > 1:
         q = np.asfortranarray(np.stack([gen(n, (1 + r) ^ CHARGE_STREAM) for r in range(nrhs)], 1))
     t_gen = time.perf_counter() - t0
-    hp = (host.HostPlan.build_gpu(kern, pts, args.leaf, args.tol, args.kappa)
-              if args.precompute == "gpu" else
-              host.HostPlan.build(kern, pts, args.leaf, args.tol, args.kappa))
+    # GPU precompute keeps T in HBM: the plan takes it device-to-device
+    hp = (host.HostPlan.build_gpu(kern, pts, args.leaf, args.tol, args.kappa, device=dev,
+                                  host_T=False)
+          if args.precompute == "gpu" else
+          host.HostPlan.build(kern, pts, args.leaf, args.tol, args.kappa))
     hinfo = hp.info()
     t0 = time.perf_counter()
-    plan = api.GpuPlan(hp.desc_struct(), device=dev)
+    plan = api.GpuPlan.from_host(hp, device=dev)
     t_upload = time.perf_counter() - t0
     info = plan.info()
 
@@ -579,7 +581,10 @@ def main():
                        "k_max": hinfo["k_max"], "m_proj": hinfo["proj_scalars"],
                        "host_threads": host.get_threads(),
                        "skeletons": "GPU skeletonizer (sfmm_gpu_build_skeletons)"
-                       if args.precompute == "gpu" else "host C++ skeletonizer"},
+                       if args.precompute == "gpu" else "host C++ skeletonizer",
+                       "operators": "device-resident, plan built device-to-device "
+                       "(sfmm_gpu_plan_create_skel)" if args.precompute == "gpu"
+                       else "uploaded from the host"},
     }
 
     # ---- CPU baseline: the unmodified reference apply on the same plan ----
@@ -587,6 +592,7 @@ def main():
         try:
             from oracle import pyoracle as po
             if args.cpu == "full":
+                hp.fetch_T()  # the CPU reference needs the operators on the host
                 rp = po.RefPipeline.from_desc(hp.desc_struct())
                 t0 = time.perf_counter()
                 u_ref, _ = rp.apply(q0, cplx)  # the reference apply takes one RHS

@@ -231,10 +231,28 @@ int sfmm_gpu_build_skeletons(const sfmm_tree_desc* tree, int kernel, double kapp
                              sfmm_skel_result** out);
 /* Points the skeleton fields of *desc (iv_off, iv, sk_off, skel_pos, rd_off,
  * red_pos, T_off, T, box_parent_offset) at the result's arrays and returns
- * k_max, proj_scalars and the number of saturated boxes. */
+ * k_max, proj_scalars and the number of saturated boxes.  The interpolation
+ * operators stay resident on the device that built them; with_host_T = 0 leaves
+ * desc->T NULL (no device->host copy), with_host_T = 1 downloads them once into
+ * the result (sfmm_gpu_skel_fill = sfmm_gpu_skel_describe(.., 1, ..)). */
+int sfmm_gpu_skel_describe(sfmm_skel_result* res, sfmm_plan_desc* desc, int with_host_T,
+                           int32_t* k_max, int64_t* proj_scalars, int32_t* saturated,
+                           double* seconds);
 int sfmm_gpu_skel_fill(sfmm_skel_result* res, sfmm_plan_desc* desc, int32_t* k_max,
                        int64_t* proj_scalars, int32_t* saturated, double* seconds);
+/* Device copy of T (box order, indexed by the result's T_off; interleaved
+ * complex for Helmholtz): the device it lives on and its length in doubles. */
+const double* sfmm_gpu_skel_device_T(const sfmm_skel_result* res, int* device,
+                                     int64_t* n_scalars);
 void sfmm_gpu_skel_destroy(sfmm_skel_result* res);
+
+/* Device-side plan build: as sfmm_gpu_plan_create /
+ * _create_sharded, but the interpolation operators are taken device-to-device
+ * from `skel` (built on the same device) and desc->T is ignored, so T never
+ * leaves HBM.  desc's skeleton fields must be those of `skel`
+ * (sfmm_gpu_skel_describe).  `skel` may be destroyed after the call. */
+int sfmm_gpu_plan_create_skel(const sfmm_plan_desc* desc, const sfmm_skel_result* skel,
+                              int device, int n_ranks, int rank, sfmm_gpu_plan** out);
 
 /* Phase timing.  While enabled, every apply records CUDA events on its stream
  * around its five phases (0 gather, 1 upward, 2 translate, 3 downward,

@@ -81,10 +81,16 @@ const sfmm_plan_desc* sfmm_host_desc(sfmm_host_plan* plan);
 int sfmm_host_box_geometry(const sfmm_host_plan* plan, double* center, double* half);
 
 /* Replaces the plan's skeleton fields with externally built ones (e.g. from
- * sfmm_gpu_build_skeletons); the arrays are copied. */
+ * sfmm_gpu_build_skeletons); the arrays are copied.  skel->T may be NULL: the
+ * interpolation operators then live only on the device (the plan's desc.T is
+ * NULL until sfmm_host_set_T). */
 int sfmm_host_set_skeletons(sfmm_host_plan* plan, const sfmm_plan_desc* skel, int kernel,
                             double kappa, int32_t k_max, int64_t proj_scalars, int32_t saturated,
                             double t_skel);
+
+/* Sets (copies) the interpolation operators: n_scalars doubles, box order,
+ * matching the plan's T_off (interleaved complex for Helmholtz). */
+int sfmm_host_set_T(sfmm_host_plan* plan, const double* T, int64_t n_scalars);
 
 int sfmm_host_info_get(const sfmm_host_plan* plan, sfmm_host_info* info);
 

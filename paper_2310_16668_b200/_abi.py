@@ -219,7 +219,8 @@ class PlanDescriptor:
                 setattr(d, k, self.scalars[k])
             for name, dt in DESC_ARRAYS:
                 a = self.arrays[name]
-                setattr(d, name, a.ctypes.data_as(C.POINTER(_CTYPE[dt])))
+                # an empty array is passed as NULL (e.g. T held on the device only)
+                setattr(d, name, a.ctypes.data_as(C.POINTER(_CTYPE[dt])) if a.size else None)
             self._struct = d
         return self._struct
 
@@ -305,6 +306,13 @@ def gpu_lib() -> C.CDLL:
     lib.sfmm_gpu_build_skeletons.restype = C.c_int
     lib.sfmm_gpu_skel_fill.argtypes = [vp, C.POINTER(PlanDesc), vp, vp, vp, vp]
     lib.sfmm_gpu_skel_fill.restype = C.c_int
+    lib.sfmm_gpu_skel_describe.argtypes = [vp, C.POINTER(PlanDesc), C.c_int, vp, vp, vp, vp]
+    lib.sfmm_gpu_skel_describe.restype = C.c_int
+    lib.sfmm_gpu_skel_device_T.argtypes = [vp, vp, vp]
+    lib.sfmm_gpu_skel_device_T.restype = vp
+    lib.sfmm_gpu_plan_create_skel.argtypes = [C.POINTER(PlanDesc), vp, C.c_int, C.c_int, C.c_int,
+                                              C.POINTER(vp)]
+    lib.sfmm_gpu_plan_create_skel.restype = C.c_int
     lib.sfmm_gpu_skel_destroy.argtypes = [vp]
     lib.sfmm_gpu_skel_destroy.restype = None
     lib.sfmm_gpu_test_sincos.argtypes = [vp, C.c_int64, vp]
@@ -320,5 +328,6 @@ GPU_SYMBOLS = [
     "sfmm_gpu_fp64_peak", "sfmm_gpu_plan_create_sharded", "sfmm_gpu_shard_info",
     "sfmm_gpu_apply_begin", "sfmm_gpu_apply_end", "sfmm_gpu_shard_describe",
     "sfmm_gpu_build_skeletons", "sfmm_gpu_skel_fill", "sfmm_gpu_skel_destroy",
-    "sfmm_gpu_test_sincos",
+    "sfmm_gpu_test_sincos", "sfmm_gpu_skel_describe", "sfmm_gpu_skel_device_T",
+    "sfmm_gpu_plan_create_skel",
 ]

@@ -62,9 +62,11 @@ def _raise(rc: int) -> None:
 class GpuPlan:
     """Device-resident apply plan (operators uploaded once, resident in HBM)."""
 
-    def __init__(self, desc, device: int = 0):
+    def __init__(self, desc, device: int = 0, skeletons=None):
         """desc: a PlanDescriptor, or a ctypes PlanDesc (e.g. straight from the
-        host precompute, without copying its arrays)."""
+        host precompute, without copying its arrays).  skeletons: a device
+        skeleton result handle (host.HostPlan.device_skeletons[0]) whose T is
+        taken device-to-device instead of desc's T (sfmm_gpu_plan_create_skel)."""
         lib = _abi.gpu_lib()
         self.device = device
         self._h = None
@@ -75,12 +77,26 @@ class GpuPlan:
         else:
             raise TypeError("GpuPlan: expected a PlanDescriptor or a PlanDesc")
         h = C.c_void_p()
-        _raise(lib.sfmm_gpu_plan_create(C.byref(st), device, C.byref(h)))
+        if skeletons is not None:
+            _raise(lib.sfmm_gpu_plan_create_skel(C.byref(st), skeletons, device, 1, 0, C.byref(h)))
+        else:
+            _raise(lib.sfmm_gpu_plan_create(C.byref(st), device, C.byref(h)))
         self._h = h
         self.kernel = int(st.kernel)
         self.n_points = int(st.n_points)
         self.is_complex = self.kernel in (_abi.HELMHOLTZ2D, _abi.HELMHOLTZ3D)
         self.dtype = np.complex128 if self.is_complex else np.float64
+
+    @classmethod
+    def from_host(cls, hp, device: int | None = None) -> "GpuPlan":
+        """Plan from a host.HostPlan; device-resident skeletons (build_gpu with
+        host_T=False) are used in place, so T never crosses PCIe."""
+        ds = hp.device_skeletons
+        if ds is not None:
+            if device is not None and device != ds[1]:
+                raise ValueError("GpuPlan.from_host: skeletons live on another device")
+            return cls(hp.desc_struct(), ds[1], skeletons=ds[0])
+        return cls(hp.desc_struct(), 0 if device is None else device)
 
     @property
     def handle(self) -> C.c_void_p:

@@ -195,7 +195,7 @@ struct sfmm_host_plan {
     d.rd_off = sk.rd_off.data();
     d.red_pos = sk.red_pos.data();
     d.T_off = sk.T_off.data();
-    d.T = sk.T.data();
+    d.T = sk.T.empty() ? nullptr : sk.T.data();  // NULL: T held on the device only
     d.coll_off = nb.coll_off.data();
     d.coll = nb.coll.data();
     d.coarse_off = nb.coarse_off.data();
@@ -301,7 +301,10 @@ int sfmm_host_set_skeletons(sfmm_host_plan* p, const sfmm_plan_desc* s, int kern
     k.iv.assign(s->iv, s->iv + k.iv_off[nb]);
     k.skel_pos.assign(s->skel_pos, s->skel_pos + k.sk_off[nb]);
     k.red_pos.assign(s->red_pos, s->red_pos + k.rd_off[nb]);
-    k.T.assign(s->T, s->T + k.T_off[nb] * sw);
+    if (s->T)
+      k.T.assign(s->T, s->T + k.T_off[nb] * sw);
+    else
+      std::vector<double>().swap(k.T);  // operators stay on the device (sfmm_gpu_plan_create_skel)
     k.parent_offset.assign(s->box_parent_offset, s->box_parent_offset + nb);
     k.k_max = k_max;
     k.proj_scalars = proj_scalars;
@@ -309,6 +312,17 @@ int sfmm_host_set_skeletons(sfmm_host_plan* p, const sfmm_plan_desc* s, int kern
     p->kernel = kernel;
     p->kappa = kappa;
     p->info.t_skel = t_skel;
+    p->export_desc();
+  });
+}
+
+int sfmm_host_set_T(sfmm_host_plan* p, const double* T, int64_t n_scalars) {
+  if (!p || (!T && n_scalars)) return fail(SFMM_EINVAL, "null argument");
+  return guarded([&] {
+    const int sw = p->kernel == SFMM_HELMHOLTZ3D || p->kernel == SFMM_HELMHOLTZ2D ? 2 : 1;
+    if (p->sk.T_off.empty() || p->sk.T_off.back() * sw != n_scalars)
+      throw std::invalid_argument("set_T: length does not match T_off");
+    p->sk.T.assign(T, T + n_scalars);
     p->export_desc();
   });
 }

@@ -224,7 +224,7 @@ const char* sfmm_gpu_version(void) { return "sfmm_gpu 0.1 (sm_100a, FP64)"; }
 namespace {
 
 int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
-                sfmm_gpu_plan** out) {
+                sfmm_gpu_plan** out, const double* T_dev = nullptr) {
   if (!desc || !out) return set_error(SFMM_EINVAL, "sfmm_gpu_plan_create: null argument");
   *out = nullptr;
   sfmm_gpu_plan* p = nullptr;
@@ -278,10 +278,13 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
       dp.T_off = p->upload(hp.T_off);
       // interpolation operators of the owned boxes, copied run by run
       dp.T = p->alloc<double>((size_t)hp.T_off[hp.n_boxes] * sw);
+      const double* T_src = T_dev ? T_dev : desc->T;
+      if (!T_src && !hp.T_runs.empty()) throw CudaFail{SFMM_EINVAL, "descriptor has no T"};
       for (const HostPlan::Run& r : hp.T_runs)
-        ck(cudaMemcpy(dp.T + r.dst * sw, desc->T + r.src * sw, sizeof(double) * r.len * sw,
-                      cudaMemcpyHostToDevice),
+        ck(cudaMemcpyAsync(dp.T + r.dst * sw, T_src + r.src * sw, sizeof(double) * r.len * sw,
+                           T_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, p->stream),
            "upload T");
+      ck(cudaStreamSynchronize(p->stream), "upload T");
       dp.up_items = p->upload(hp.up_items);
       dp.down_items = p->upload(hp.down_items);
       dp.stage = p->alloc<double>((size_t)std::max<int64_t>(hp.stage_size, 1));
@@ -353,6 +356,20 @@ int sfmm_gpu_plan_create(const sfmm_plan_desc* desc, int device, sfmm_gpu_plan**
 int sfmm_gpu_plan_create_sharded(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
                                  sfmm_gpu_plan** out) {
   return create_plan(desc, device, n_ranks, rank, out);
+}
+
+int sfmm_gpu_plan_create_skel(const sfmm_plan_desc* desc, const sfmm_skel_result* skel,
+                              int device, int n_ranks, int rank, sfmm_gpu_plan** out) {
+  if (!desc || !skel || !out) return set_error(SFMM_EINVAL, "sfmm_gpu_plan_create_skel: null argument");
+  int skel_dev = -1;
+  int64_t n_scalars = 0;
+  const double* T_dev = sfmm_gpu_skel_device_T(skel, &skel_dev, &n_scalars);
+  if (skel_dev != device)
+    return set_error(SFMM_EINVAL, "sfmm_gpu_plan_create_skel: skeletons live on another device");
+  const int sw = desc->kernel == SFMM_HELMHOLTZ3D || desc->kernel == SFMM_HELMHOLTZ2D ? 2 : 1;
+  if (!desc->T_off || desc->n_boxes < 0 || desc->T_off[desc->n_boxes] * sw != n_scalars)
+    return set_error(SFMM_EINVAL, "sfmm_gpu_plan_create_skel: descriptor T_off does not match the skeletons");
+  return create_plan(desc, device, n_ranks, rank, out, T_dev);
 }
 
 int sfmm_gpu_shard_info(const sfmm_gpu_plan* p, int64_t* send_counts, int64_t* recv_counts,

@@ -24,6 +24,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -455,10 +457,37 @@ struct DevBuf {
 struct sfmm_skel_result {
   std::vector<int64_t> iv_off, sk_off, rd_off, T_off;
   std::vector<int32_t> iv, skel_pos, red_pos, poff;
+  // interpolation operators in box order (global T_off), resident on `device`;
+  // the host copy T is made on demand (sfmm_gpu_skel_fill / _describe)
+  double* d_T = nullptr;
+  int device = 0, sw = 1;
+  bool have_host_T = false;
   std::vector<double> T;
   int32_t k_max = 0, saturated = 0;
   int64_t proj = 0;
   double seconds = 0;
+  sfmm_skel_result() = default;
+  sfmm_skel_result(const sfmm_skel_result&) = delete;
+  sfmm_skel_result& operator=(const sfmm_skel_result&) = delete;
+  ~sfmm_skel_result() {
+    if (d_T) {
+      int cur = 0;
+      cudaGetDevice(&cur);
+      cudaSetDevice(device);
+      cudaFree(d_T);
+      cudaSetDevice(cur);
+    }
+  }
+  size_t t_scalars() const { return T_off.empty() ? 0 : (size_t)T_off.back() * sw; }
+  void ensure_host_T() {
+    if (have_host_T) return;
+    T.resize(t_scalars());
+    if (!T.empty()) {
+      ck(cudaSetDevice(device), "cudaSetDevice");
+      ck(cudaMemcpy(T.data(), d_T, T.size() * sizeof(double), cudaMemcpyDeviceToHost), "D2H T");
+    }
+    have_host_T = true;
+  }
 };
 
 namespace {
@@ -509,7 +538,11 @@ void run_skeletons(const sfmm_tree_desc& t, int kernel, double kappa, double tol
   std::vector<Level> L(depth + 1);
   const size_t work_cap = (size_t)12 << 30;  // bytes of proxy-matrix workspace per batch
   DevBuf<double> d_work;
+  const bool verbose = std::getenv("SFMM_SKEL_VERBOSE") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto secs = [](auto a, auto b) { return std::chrono::duration<double>(b - a).count(); };
   for (int l = depth; l >= 0; --l) {
+    const auto t_lv = now();
     Level& lv = L[l];
     const int b0 = t.level_begin[l], b1 = t.level_begin[l + 1], nl = b1 - b0;
     // index_vec sizes: leaf points or the children's k
@@ -670,6 +703,9 @@ void run_skeletons(const sfmm_tree_desc& t, int kernel, double kappa, double tol
          "D2H sat");
     }
     ck(cudaDeviceSynchronize(), "level");
+    if (verbose)
+      std::fprintf(stderr, "[skel] level %d: %d boxes, %zu batches, nmax %lld, %.3f s\n", l, nl,
+                   batch_start.size() - 1, (long long)nmax, secs(t_lv, now()));
     lv.k = kk_all;
     for (int i = 0; i < nl; ++i) {
       R.k_max = std::max(R.k_max, kk_all[i]);
@@ -678,6 +714,7 @@ void run_skeletons(const sfmm_tree_desc& t, int kernel, double kappa, double tol
     }
   }
   // assemble the global (box-order) CSR arrays on the host
+  const auto t_asm = now();
   R.iv_off.assign(nb + 1, 0);
   R.sk_off.assign(nb + 1, 0);
   R.rd_off.assign(nb + 1, 0);
@@ -697,7 +734,11 @@ void run_skeletons(const sfmm_tree_desc& t, int kernel, double kappa, double tol
   R.iv.resize(R.iv_off[nb]);
   R.skel_pos.resize(R.sk_off[nb]);
   R.red_pos.resize(R.rd_off[nb]);
-  R.T.resize((size_t)R.T_off[nb] * SW);
+  R.sw = SW;
+  R.have_host_T = false;
+  R.T.clear();
+  ck(cudaGetDevice(&R.device), "cudaGetDevice");
+  ck(cudaMalloc(&R.d_T, std::max<size_t>(R.t_scalars(), 1) * sizeof(double)), "cudaMalloc T");
   for (int l = 0; l <= depth; ++l) {
     const int b0 = t.level_begin[l], nl = t.level_begin[l + 1] - b0;
     if (nl == 0) continue;
@@ -710,10 +751,13 @@ void run_skeletons(const sfmm_tree_desc& t, int kernel, double kappa, double tol
     if (niv - nsk)
       ck(cudaMemcpy(R.red_pos.data() + R.rd_off[b0], lv.d_red.p, (niv - nsk) * 4, cudaMemcpyDeviceToHost),
          "D2H red");
-    if (nt) ck(cudaMemcpy(R.T.data() + R.T_off[b0] * SW, lv.d_T.p, nt * SW * 8, cudaMemcpyDeviceToHost), "D2H T");
+    if (nt)
+      ck(cudaMemcpy(R.d_T + R.T_off[b0] * SW, lv.d_T.p, nt * SW * 8, cudaMemcpyDeviceToDevice), "D2D T");
+    lv.d_T.alloc(0);  // release the level's (upper-bound sized) buffer early
   }
   R.poff.resize(nb);
   ck(cudaMemcpy(R.poff.data(), d_poff.p, nb * sizeof(int32_t), cudaMemcpyDeviceToHost), "D2H poff");
+  if (verbose) std::fprintf(stderr, "[skel] assemble: %.3f s\n", secs(t_asm, now()));
 }
 
 }  // namespace
@@ -760,7 +804,23 @@ int sfmm_gpu_build_skeletons(const sfmm_tree_desc* tree, int kernel, double kapp
 
 int sfmm_gpu_skel_fill(sfmm_skel_result* r, sfmm_plan_desc* d, int32_t* k_max,
                        int64_t* proj_scalars, int32_t* saturated, double* seconds) {
-  if (!r || !d) return SFMM_EINVAL;
+  return sfmm_gpu_skel_describe(r, d, 1, k_max, proj_scalars, saturated, seconds);
+}
+
+int sfmm_gpu_skel_describe(sfmm_skel_result* r, sfmm_plan_desc* d, int with_host_T,
+                           int32_t* k_max, int64_t* proj_scalars, int32_t* saturated,
+                           double* seconds) {
+  using sfmm_gpu::set_last_error;
+  if (!r || !d) return set_last_error(SFMM_EINVAL, "skel_describe: null argument");
+  if (with_host_T) {
+    try {
+      r->ensure_host_T();
+    } catch (const CudaErr& e) {
+      return set_last_error(SFMM_ECUDA, "skel_describe: " + e.msg);
+    } catch (const std::bad_alloc&) {
+      return set_last_error(SFMM_ENOMEM, "skel_describe: host allocation failed");
+    }
+  }
   d->iv_off = r->iv_off.data();
   d->iv = r->iv.data();
   d->sk_off = r->sk_off.data();
@@ -768,13 +828,20 @@ int sfmm_gpu_skel_fill(sfmm_skel_result* r, sfmm_plan_desc* d, int32_t* k_max,
   d->rd_off = r->rd_off.data();
   d->red_pos = r->red_pos.data();
   d->T_off = r->T_off.data();
-  d->T = r->T.data();
+  d->T = with_host_T ? r->T.data() : nullptr;
   d->box_parent_offset = r->poff.data();
   if (k_max) *k_max = r->k_max;
   if (proj_scalars) *proj_scalars = r->proj;
   if (saturated) *saturated = r->saturated;
   if (seconds) *seconds = r->seconds;
   return SFMM_OK;
+}
+
+const double* sfmm_gpu_skel_device_T(const sfmm_skel_result* r, int* device, int64_t* n_scalars) {
+  if (!r) return nullptr;
+  if (device) *device = r->device;
+  if (n_scalars) *n_scalars = (int64_t)r->t_scalars();
+  return r->d_T;
 }
 
 void sfmm_gpu_skel_destroy(sfmm_skel_result* r) { delete r; }

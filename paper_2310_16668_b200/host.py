@@ -67,6 +67,7 @@ def host_lib() -> C.CDLL:
         lib.sfmm_host_box_geometry.argtypes = [vp, vp, vp]
         lib.sfmm_host_set_skeletons.argtypes = [vp, C.POINTER(PlanDesc), C.c_int, C.c_double,
                                                 C.c_int32, C.c_int64, C.c_int32, C.c_double]
+        lib.sfmm_host_set_T.argtypes = [vp, vp, C.c_int64]
         _lib = lib
     return _lib
 
@@ -113,6 +114,8 @@ class HostPlan:
 
     def __init__(self, handle):
         self._h = handle
+        self._skel = None  # device-resident skeleton result (build_gpu(host_T=False))
+        self._skel_device = 0
 
     @classmethod
     def build(cls, kernel: int, pts: np.ndarray, leaf_cap: int, tol: float, kappa: float = 1.0,
@@ -127,9 +130,15 @@ class HostPlan:
 
     @classmethod
     def build_gpu(cls, kernel: int, pts: np.ndarray, leaf_cap: int, tol: float,
-                  kappa: float = 1.0, proxy: tuple | None = None, device: int = 0) -> "HostPlan":
+                  kappa: float = 1.0, proxy: tuple | None = None, device: int = 0,
+                  host_T: bool = True) -> "HostPlan":
         """Tree and neighbor lists on the host (bit-identical to the reference),
-        skeletons on the GPU (sfmm_gpu_build_skeletons)."""
+        skeletons on the GPU (sfmm_gpu_build_skeletons).
+
+        host_T=False keeps the interpolation operators on the device only
+        (SURVEY.md 8(f) row 2): the descriptor's T is NULL, api.GpuPlan.from_host
+        takes T device-to-device, and fetch_T() downloads it when a host copy is
+        needed (e.g. for the CPU reference)."""
         from .api import _raise
         hp = cls.build_tree(pts, leaf_cap)
         d = host_lib().sfmm_host_desc(hp._h).contents
@@ -148,16 +157,46 @@ class HostPlan:
         lib = _abi.gpu_lib()
         _raise(lib.sfmm_gpu_build_skeletons(C.byref(t), kernel, kappa, tol, float(px[0]), int(px[1]),
                                             int(px[2]), device, C.byref(res)))
+        keep = False
         try:
             sk = PlanDesc()
             kmax, proj, sat, secs = C.c_int32(), C.c_int64(), C.c_int32(), C.c_double()
-            _raise(lib.sfmm_gpu_skel_fill(res, C.byref(sk), C.byref(kmax), C.byref(proj),
-                                          C.byref(sat), C.byref(secs)))
+            _raise(lib.sfmm_gpu_skel_describe(res, C.byref(sk), 1 if host_T else 0, C.byref(kmax),
+                                              C.byref(proj), C.byref(sat), C.byref(secs)))
             _check(host_lib().sfmm_host_set_skeletons(hp._h, C.byref(sk), kernel, kappa, kmax,
                                                       proj, sat, secs))
+            keep = not host_T
         finally:
-            lib.sfmm_gpu_skel_destroy(res)
+            if keep:
+                hp._skel, hp._skel_device = res, device
+            else:
+                lib.sfmm_gpu_skel_destroy(res)
         return hp
+
+    @property
+    def device_skeletons(self):
+        """(handle, device) of the device-resident skeletons, or None."""
+        return (self._skel, self._skel_device) if self._skel is not None else None
+
+    def fetch_T(self) -> None:
+        """Downloads device-resident interpolation operators into this plan
+        (no-op when it already has them)."""
+        from .api import _raise
+        if self._skel is None or bool(host_lib().sfmm_host_desc(self._h).contents.T):
+            return
+        lib = _abi.gpu_lib()
+        sk = PlanDesc()
+        _raise(lib.sfmm_gpu_skel_describe(self._skel, C.byref(sk), 1, None, None, None, None))
+        n = C.c_int64()
+        lib.sfmm_gpu_skel_device_T(self._skel, None, C.byref(n))
+        _check(host_lib().sfmm_host_set_T(self._h, C.cast(sk.T, C.c_void_p), n.value))
+        self.release_device_skeletons()  # the result's host copy goes with it
+
+    def release_device_skeletons(self) -> None:
+        """Frees the device copy of T held for api.GpuPlan.from_host."""
+        if self._skel is not None:
+            _abi.gpu_lib().sfmm_gpu_skel_destroy(self._skel)
+            self._skel = None
 
     @classmethod
     def build_tree(cls, pts: np.ndarray, leaf_cap: int) -> "HostPlan":
@@ -181,6 +220,7 @@ class HostPlan:
         return {k: getattr(inf, k) for k, _ in HostInfo._fields_}
 
     def close(self) -> None:
+        self.release_device_skeletons()
         if self._h is not None:
             host_lib().sfmm_host_destroy(self._h)
             self._h = None

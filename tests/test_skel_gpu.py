@@ -92,3 +92,26 @@ def test_apply_parity_on_gpu_skeletons(kernel, dist, n, kappa):
     assert rel_l2(u, u_ref) <= 1e-12
     t = np.arange(0, n, n // 200, dtype=np.int32)
     assert max_rel(u[t], api.direct_sum_subset(kernel, kappa, pts, q, t)) <= 1e-5
+
+
+@pytest.mark.parametrize("kernel,dist,n,kappa", [(1, "cube", 60000, 1.0), (3, "sphere", 20000, 5.0),
+                                                 (0, "square", 30000, 1.0)])
+def test_device_resident_operators(kernel, dist, n, kappa):
+    """a plan built from device-resident skeletons
+    (T taken device-to-device) is bit-identical to one built from the host
+    copy of the same operators."""
+    pts = host.generate_points(dist, n, 3)
+    hp = host.HostPlan.build_gpu(kernel, pts, 64, 1e-6, kappa, host_T=False)
+    assert hp.device_skeletons is not None
+    assert not hp.desc_struct().T           # T never came to the host
+    with pytest.raises(ValueError):         # a host-only plan needs the host copy
+        api.GpuPlan(hp.desc_struct())
+    q = host.generate_charges_complex(n, 8) if kernel == 3 else host.generate_charges(n, 8)
+    u_dev = api.fmm_apply(api.GpuPlan.from_host(hp), q)
+    hp.fetch_T()
+    assert hp.device_skeletons is None and hp.desc_struct().T
+    u_host = api.fmm_apply(api.GpuPlan.from_host(hp), q)
+    assert np.array_equal(u_dev, u_host)
+    # and the operators are the skeletonizer's: accurate against the dense sum
+    t = np.arange(0, n, n // 100, dtype=np.int32)
+    assert max_rel(u_dev[t], api.direct_sum_subset(kernel, kappa, pts, q, t)) <= 1e-5
