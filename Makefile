@@ -11,7 +11,7 @@ OBJ      := build/obj
 ARCH     := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -I$(SRC) \
             --expt-relaxed-constexpr -Xptxas -v
-CXXFLAGS := -std=c++17 -O2 -fPIC -Iinclude -I$(SRC) -I/usr/local/cuda/include
+CXXFLAGS := -std=c++17 -O2 -fopenmp -fPIC -Iinclude -I$(SRC) -I/usr/local/cuda/include
 
 GPU_CU   := $(SRC)/kernels_translate.cu $(SRC)/kernels_tree.cu $(SRC)/kernels_probe.cu $(SRC)/kernels_multi.cu $(SRC)/skel_gpu.cu \
             $(SRC)/sfmm_gpu.cu
@@ -52,7 +52,7 @@ $(OBJ)/plan_build.o: $(SRC)/plan_build.cpp $(HDRS)
 
 $(LIB)/libsfmm_gpu.so: $(GPU_OBJS)
 	@mkdir -p $(LIB)
-	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart_static -lpthread -ldl -lrt
+	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart_static -lgomp -lpthread -ldl -lrt
 
 oracle:
 	$(MAKE) -C oracle

@@ -286,6 +286,46 @@ __global__ void __launch_bounds__(256) k5_direct_subset(int kernel, double kappa
   }
 }
 
+// Device-side plan build, one warp per box: slot
+// geometry and ids (make_plan's gathered coordinates, apply.cpp:70-107) and
+// the upward destinations (skeleton.cpp:204-218; apply.cpp:127-131).
+__global__ void k_build_slots(SlotBuildArgs a) {
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= a.n_boxes) return;
+  const BoxRec br = a.box[w];
+  for (int32_t p = lane; p < br.n; p += 32) {
+    const int64_t e = br.slot + p;
+    const int64_t s = br.slot + a.posmap[e];
+    const int64_t id = a.iv[e];
+    a.slot_id[s] = (int32_t)id;
+    a.X[s] = a.pts[id * a.dim];
+    a.Y[s] = a.pts[id * a.dim + 1];
+    a.Z[s] = a.dim == 3 ? a.pts[id * a.dim + 2] : 0.0;
+  }
+  if (br.k > 0) {
+    const int64_t ps = a.box[a.parent[w]].slot;
+    const int64_t off = a.parent_offset[w];
+    for (int32_t i = lane; i < br.k; i += 32) a.up_dst[br.skel + i] = ps + a.posmap[ps + off + i];
+  }
+}
+
+// Leaf gather/scatter maps, one warp per owned leaf: index_vec position p of
+// the leaf (tree-order point begin + p, original index perm[begin + p]) owns
+// slot s0 + posmap[p]; entries are written in slot order.
+__global__ void k_build_leaf_maps(SlotBuildArgs a) {
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= a.n_leaves) return;
+  const BoxRec br = a.box[a.leaf_box[w]];
+  const int64_t out = a.leaf_out[w], begin = a.leaf_begin[w];
+  for (int32_t p = lane; p < br.n; p += 32) {
+    const int32_t j = a.posmap[br.slot + p];
+    a.leaf_slot[out + j] = br.slot + j;
+    a.leaf_orig[out + j] = a.perm[begin + p];
+  }
+}
+
 int grid_for(int64_t n, int threads) {
   const int64_t g = (n + threads - 1) / threads;
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 32));
@@ -417,6 +457,14 @@ int configure_tree_kernels(DevPlan& p, size_t max_r, size_t max_k) {
       return -1;
   }
   return 0;
+}
+
+void launch_build_slots(const SlotBuildArgs& a, cudaStream_t st) {
+  constexpr int kThreads = 256, kWarps = kThreads / 32;
+  if (a.n_boxes > 0)
+    k_build_slots<<<(int)((a.n_boxes + kWarps - 1) / kWarps), kThreads, 0, st>>>(a);
+  if (a.n_leaves > 0)
+    k_build_leaf_maps<<<(int)((a.n_leaves + kWarps - 1) / kWarps), kThreads, 0, st>>>(a);
 }
 
 }  // namespace sfmm_gpu

@@ -85,6 +85,30 @@ void launch_direct_subset(int kernel, double kappa, int dim, int64_t n, const do
                           const double* q, int64_t nt, const int32_t* targets, double* u,
                           int* err_flag, cudaStream_t st);
 
+// Device-side plan build: slot geometry/ids, upward destinations and the leaf
+// maps from the uploaded index arrays (kernels_tree.cu).
+struct SlotBuildArgs {
+  const BoxRec* box;
+  int64_t n_boxes;
+  const int32_t* posmap;        // n_slots
+  const int32_t* iv;            // n_slots, tree-order point ids
+  const double* pts;            // tree order, interleaved
+  int dim;
+  const int32_t* parent;        // n_boxes
+  const int32_t* parent_offset; // n_boxes
+  const int32_t* leaf_box;      // owned leaves
+  const int64_t* leaf_begin;
+  const int64_t* leaf_out;
+  int64_t n_leaves;
+  const int32_t* perm;          // n_points
+  double *X, *Y, *Z;
+  int32_t* slot_id;
+  int64_t* up_dst;
+  int64_t* leaf_slot;
+  int32_t* leaf_orig;
+};
+void launch_build_slots(const SlotBuildArgs& a, cudaStream_t st);
+
 // Persistent-grid size and dynamic shared memory setup (called at plan creation).
 int configure_translate(DevPlan& p, int device);
 int configure_tree_kernels(DevPlan& p, size_t max_r, size_t max_k);

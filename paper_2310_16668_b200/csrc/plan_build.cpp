@@ -2,6 +2,9 @@
 #include "plan_build.h"
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <numeric>
 
@@ -16,6 +19,18 @@ struct Fail {
 
 [[noreturn]] void bad(const std::string& m) { throw Fail{SFMM_EINVAL, "sfmm_gpu_plan_create: " + m}; }
 
+// First validation failure inside an OpenMP loop, raised after the loop.
+struct ParErr {
+  std::atomic<const char*> msg{nullptr};
+  void set(const char* m) {
+    const char* none = nullptr;
+    msg.compare_exchange_strong(none, m);
+  }
+  void raise() const {
+    if (const char* m = msg.load()) bad(m);
+  }
+};
+
 }  // namespace
 
 PlanOptions plan_options_from_env() {
@@ -28,11 +43,22 @@ PlanOptions plan_options_from_env() {
 int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int n_ranks,
                     int rank) {
   try {
+    ParErr perr;
     if (d.kernel == SFMM_HELMHOLTZ2D)
       throw Fail{SFMM_EUNSUPPORTED,
                  "sfmm_gpu_plan_create: helmholtz2d (long-double Hankel) has no device path"};
     if (d.kernel != SFMM_LAPLACE2D && d.kernel != SFMM_LAPLACE3D && d.kernel != SFMM_HELMHOLTZ3D)
       bad("unknown kernel id");
+    // SFMM_PLAN_VERBOSE=1: per-phase wall time of the plan build on stderr
+    static const bool verbose = std::getenv("SFMM_PLAN_VERBOSE") != nullptr;
+    auto t_prev = std::chrono::steady_clock::now();
+    auto ptime = [&](const char* what) {
+      if (!verbose) return;
+      const auto t = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "[plan] %-20s %.3f s\n", what,
+                   std::chrono::duration<double>(t - t_prev).count());
+      t_prev = t;
+    };
     const int want_dim = d.kernel == SFMM_LAPLACE2D ? 2 : 3;
     if (d.dim != want_dim) bad("kernel dimension mismatch");  // make_plan, apply.cpp:73
     if (d.n_points < 1) bad("empty point set");
@@ -91,6 +117,7 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
       if (b > 0 && d.box_parent[b] >= b) bad("parents must precede children (level-major order)");
     }
 
+    ptime("validate");
     hp.box.resize(nb);
     hp.box_parent.assign(d.box_parent, d.box_parent + nb);
     hp.box_level.assign(d.box_level, d.box_level + nb);
@@ -99,76 +126,83 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
     const int64_t S = hp.n_slots;
 
     // slot position map: index_vec position -> offset inside the box's slots
-    std::vector<int32_t> posmap(S);
-    for (int32_t b = 0; b < nb; ++b) {
-      const int64_t n = d.iv_off[b + 1] - d.iv_off[b];
-      const int64_t k = d.sk_off[b + 1] - d.sk_off[b];
-      const int64_t r = d.rd_off[b + 1] - d.rd_off[b];
-      if (n < 0 || k < 0 || r < 0) bad("negative CSR extent");
-      if (!(k + r == n || (k == 0 && r == 0))) bad("skel_pos/red_pos do not partition index_vec");
-      if (d.T_off[b + 1] - d.T_off[b] != k * r) bad("T_off does not match k*r");
-      if (d.box_level[b] < 0 || d.box_level[b] > d.depth) bad("box level out of range");
-      BoxRec& br = hp.box[b];
-      br.slot = d.iv_off[b];
-      br.skel = d.sk_off[b];
-      br.n = (int32_t)n;
-      br.k = (int32_t)k;
-      int32_t* pm = posmap.data() + d.iv_off[b];
-      if (k + r == n && n > 0) {
-        std::vector<uint8_t> seen(n, 0);
-        for (int64_t i = 0; i < k; ++i) {
-          const int32_t p = d.skel_pos[d.sk_off[b] + i];
-          if (p < 0 || p >= n || seen[p]) bad("skel_pos out of range or repeated");
-          seen[p] = 1;
-          pm[p] = (int32_t)i;
+    hp.posmap.resize(S);
+    std::vector<int32_t>& posmap = hp.posmap;
+    int64_t m_proj = 0;
+#pragma omp parallel reduction(+ : m_proj)
+    {
+      std::vector<uint8_t> seen;
+#pragma omp for schedule(dynamic, 1024)
+      for (int32_t b = 0; b < nb; ++b) {
+        const int64_t n = d.iv_off[b + 1] - d.iv_off[b];
+        const int64_t k = d.sk_off[b + 1] - d.sk_off[b];
+        const int64_t r = d.rd_off[b + 1] - d.rd_off[b];
+        if (n < 0 || k < 0 || r < 0) { perr.set("negative CSR extent"); continue; }
+        if (!(k + r == n || (k == 0 && r == 0))) {
+          perr.set("skel_pos/red_pos do not partition index_vec");
+          continue;
         }
-        for (int64_t j = 0; j < r; ++j) {
-          const int32_t p = d.red_pos[d.rd_off[b] + j];
-          if (p < 0 || p >= n || seen[p]) bad("red_pos out of range or repeated");
-          seen[p] = 1;
-          pm[p] = (int32_t)(k + j);
+        if (d.T_off[b + 1] - d.T_off[b] != k * r) perr.set("T_off does not match k*r");
+        if (d.box_level[b] < 0 || d.box_level[b] > d.depth) perr.set("box level out of range");
+        BoxRec& br = hp.box[b];
+        br.slot = d.iv_off[b];
+        br.skel = d.sk_off[b];
+        br.n = (int32_t)n;
+        br.k = (int32_t)k;
+        int32_t* pm = posmap.data() + d.iv_off[b];
+        if (k + r == n && n > 0) {
+          seen.assign(n, 0);
+          for (int64_t i = 0; i < k; ++i) {
+            const int32_t p = d.skel_pos[d.sk_off[b] + i];
+            if (p < 0 || p >= n || seen[p]) { perr.set("skel_pos out of range or repeated"); break; }
+            seen[p] = 1;
+            pm[p] = (int32_t)i;
+          }
+          for (int64_t j = 0; j < r; ++j) {
+            const int32_t p = d.red_pos[d.rd_off[b] + j];
+            if (p < 0 || p >= n || seen[p]) { perr.set("red_pos out of range or repeated"); break; }
+            seen[p] = 1;
+            pm[p] = (int32_t)(k + j);
+          }
+        } else {
+          for (int64_t p = 0; p < n; ++p) pm[p] = (int32_t)p;
         }
-      } else {
-        for (int64_t p = 0; p < n; ++p) pm[p] = (int32_t)p;
-      }
-      if (d.box_leaf[b] && d.box_end[b] - d.box_begin[b] != n)
-        bad("leaf index_vec size differs from its point range");
-      hp.m_proj += k * r;
-    }
-
-    // slot coordinates and ids (every rank keeps the full static geometry so
-    // ghost boxes need no remapping)
-    hp.X.resize(S);
-    hp.Y.resize(S);
-    hp.Z.assign(S, 0.0);
-    hp.slot_id.resize(S);
-    for (int32_t b = 0; b < nb; ++b) {
-      const int64_t s0 = d.iv_off[b];
-      for (int64_t p = 0; p < hp.box[b].n; ++p) {
-        const int32_t id = d.iv[s0 + p];
-        if (id < 0 || id >= N) bad("index_vec id out of range");
-        const int64_t s = s0 + posmap[s0 + p];
-        hp.slot_id[s] = id;
-        hp.X[s] = d.pts[(int64_t)id * dim];
-        hp.Y[s] = d.pts[(int64_t)id * dim + 1];
-        if (dim == 3) hp.Z[s] = d.pts[(int64_t)id * dim + 2];
+        if (d.box_leaf[b] && d.box_end[b] - d.box_begin[b] != n)
+          perr.set("leaf index_vec size differs from its point range");
+        m_proj += k * r;
       }
     }
+    perr.raise();
+    hp.m_proj = m_proj;
 
+    ptime("posmap");
+    // slot coordinates and ids are gathered on the device (every rank keeps
+    // the full static geometry so ghost boxes need no remapping)
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < S; ++e)
+      if (d.iv[e] < 0 || d.iv[e] >= N) perr.set("index_vec id out of range");
+    perr.raise();
+
+    ptime("slot coords");
     // upward destinations: skeleton entry i of box b lands at
     // parent position parent_offset + i (skeleton.cpp:204-218; apply.cpp:127-131)
-    hp.up_dst.assign(hp.n_skel, -1);
+    // (computed on the device: iv_off[p] + posmap[iv_off[p] + off + i])
+    hp.parent_offset.assign(d.box_parent_offset, d.box_parent_offset + nb);
+#pragma omp parallel for schedule(static)
     for (int32_t b = 0; b < nb; ++b) {
       const int32_t p = d.box_parent[b];
       const int32_t k = hp.box[b].k;
       if (k == 0) continue;
-      if (p < 0) bad("compressed root box");
+      if (p < 0) {
+        perr.set("compressed root box");
+        continue;
+      }
       const int64_t off = d.box_parent_offset[b];
-      if (off < 0 || off + k > hp.box[p].n) bad("parent_offset out of range");
-      for (int32_t i = 0; i < k; ++i)
-        hp.up_dst[hp.box[b].skel + i] = d.iv_off[p] + posmap[d.iv_off[p] + off + i];
+      if (off < 0 || off + k > hp.box[p].n) perr.set("parent_offset out of range");
     }
+    perr.raise();
 
+    ptime("up_dst");
     // ---- ownership: whole level-1 subtrees per rank ----------
     const PlanOptions opt = plan_options_from_env();
     std::vector<uint8_t> unc(nb, 0);
@@ -205,33 +239,44 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
     }
     auto mine = [&](int32_t b) { return hp.owner[b] == rank; };
 
+    ptime("ownership");
     // leaf gather/scatter maps (owned leaves): slot of position i <-> q[perm[begin + i]]
     // (apply.cpp:125, :301)
     {
-      std::vector<uint8_t> hit(N, 0);
-      int64_t covered = 0;
-      for (int32_t b = 0; b < nb; ++b) {
-        if (!d.box_leaf[b]) continue;
-        const int64_t s0 = d.iv_off[b];
-        std::vector<std::pair<int64_t, int32_t>> tmp(hp.box[b].n);
-        for (int32_t i = 0; i < hp.box[b].n; ++i) {
-          const int64_t t = (int64_t)d.box_begin[b] + i;
-          if (t < 0 || t >= N || hit[t]) bad("leaf point ranges overlap or exceed n_points");
-          hit[t] = 1;
-          tmp[i] = {s0 + posmap[s0 + i], d.perm[t]};
+      // the leaves' point ranges must tile [0, N)
+      std::vector<int32_t> leaves;
+      for (int32_t b = 0; b < nb; ++b)
+        if (d.box_leaf[b]) leaves.push_back(b);
+      {
+        std::vector<std::pair<int64_t, int64_t>> rng;
+        rng.reserve(leaves.size());
+        for (int32_t b : leaves) rng.push_back({d.box_begin[b], d.box_end[b]});
+        std::sort(rng.begin(), rng.end());
+        int64_t cur = 0;
+        for (auto& r : rng) {
+          if (r.first != cur || r.second < r.first) {
+            if (r.first < cur || r.second < r.first)
+              bad("leaf point ranges overlap or exceed n_points");
+            bad("leaves do not cover every point");
+          }
+          cur = r.second;
         }
-        covered += hp.box[b].n;
-        if (!mine(b)) continue;
-        std::sort(tmp.begin(), tmp.end());
-        for (auto& e : tmp) {
-          hp.leaf_slot.push_back(e.first);
-          hp.leaf_orig.push_back(e.second);
-        }
+        if (cur != N) bad(cur > N ? "leaf point ranges overlap or exceed n_points"
+                                  : "leaves do not cover every point");
       }
-      if (covered != N) bad("leaves do not cover every point");
-      hp.n_owned_points = (int64_t)hp.leaf_slot.size();
+      // owned leaves; the device scatters each one's (slot, original index)
+      // pairs in slot order: position i lands at leaf_out + posmap[i]
+      hp.leaf_out.assign(1, 0);
+      for (int32_t b : leaves)
+        if (mine(b)) {
+          hp.leaf_box.push_back(b);
+          hp.leaf_begin.push_back(d.box_begin[b]);
+          hp.leaf_out.push_back(hp.leaf_out.back() + hp.box[b].n);
+        }
+      hp.n_owned_points = hp.leaf_out.back();
     }
 
+    ptime("leaf maps");
     // ---- translation entries --------------------------------------------
     //
     // Exact cancellations (in exact arithmetic) are dropped: for a box that is
@@ -247,17 +292,21 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
     // sums.  Pairs across ranks stay kIFO on both sides.
     hp.symmetric = opt.symmetric && !hp.cplx;
     if (hp.symmetric) {  // the colleague relation must be symmetric to stage
-      for (int32_t b = 0; b < nb && hp.symmetric; ++b)
+      int asym = 0;
+#pragma omp parallel for schedule(dynamic, 1024) reduction(| : asym)
+      for (int32_t b = 0; b < nb; ++b)
         for (int64_t e = d.coll_off[b]; e < d.coll_off[b + 1]; ++e) {
           const int32_t c = d.coll[e];
           const int32_t* cb = d.coll + d.coll_off[c];
           const int32_t* ce = d.coll + d.coll_off[c + 1];
           if (d.box_level[c] != d.box_level[b] || !std::binary_search(cb, ce, b)) {
-            hp.symmetric = false;
+            asym = 1;
             break;
           }
         }
+      hp.symmetric = !asym;
     }
+    ptime("sym check");
     // sources(b, f): every (source, mode) evaluated for target b, before the
     // symmetric folding; identical on every rank.
     auto sources = [&](int32_t b, auto&& f) {
@@ -310,6 +359,7 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
         }
     }
 
+    ptime("pair counts");
     // this rank's CSR: owned targets only
     hp.ent_range.resize(nb);
     std::vector<uint8_t> boundary(nb, 0);
@@ -333,6 +383,7 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
           hp.p_dense_local += (double)hp.box[b].n * hp.box[hp.entries[e] >> kModeBits].n;
     }
 
+    ptime("csr");
     // multi-RHS path: the same entries without the symmetric folding, and
     // 16-row tasks (cost sorted, interior first is not needed: the multi-RHS
     // apply is single-rank)
@@ -368,6 +419,7 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
       }
     }
 
+    ptime("multi csr");
     // ghost exchange lists: box c owned by p is sent to q if one of q's
     // targets reads it.  Every rank derives the same lists.
     if (n_ranks > 1) {
@@ -399,6 +451,7 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
       }
     }
 
+    ptime("ghost lists");
     // tasks: 128-row tiles of owned targets; staging slots for kSYM column
     // sums are assigned in (box, row tile, entry) order so every receiver adds
     // them in a fixed order.  Interior tasks (no ghost source) come first so
@@ -456,6 +509,7 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
       }
     }
 
+    ptime("tasks");
     // interpolation work lists per level (owned boxes at levels >= 2 carry T);
     // T is compacted to the owned boxes (T_off indexes the compact blob)
     hp.T_off.assign(nb + 1, 0);
@@ -493,6 +547,7 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
         }
       }
     }
+    ptime("T runs, level items");
     hp.up_lvl[d.depth + 1] = (int64_t)hp.up_items.size();
     hp.down_lvl[d.depth + 1] = (int64_t)hp.down_items.size();
     hp.down_m_lvl[d.depth + 1] = (int64_t)hp.down_m_items.size();

@@ -43,14 +43,15 @@ struct HostPlan {
   std::vector<BoxRec> box;
   std::vector<int32_t> box_parent, box_level;
   std::vector<int64_t> T_off;                 // scalars
-  // slot arrays
-  std::vector<double> X, Y, Z;
-  std::vector<int32_t> slot_id;               // tree-order point id
-  // skeleton arrays
-  std::vector<int64_t> up_dst;                // parent slot receiving qhat_i
-  // leaf gather / scatter
-  std::vector<int64_t> leaf_slot;
-  std::vector<int32_t> leaf_orig;
+  // index_vec position -> slot offset inside its box ([skeleton | redundant],
+  // a permutation per box).  The device derives the slot geometry (X, Y, Z,
+  // slot_id), the upward destinations and the leaf gather/scatter maps from it
+  // (launch_build_slots); the host never materialises them.
+  std::vector<int32_t> posmap;
+  std::vector<int32_t> parent_offset;         // box_parent_offset
+  // owned leaves: box, first tree-order point, offset into leaf_slot/leaf_orig
+  std::vector<int32_t> leaf_box;
+  std::vector<int64_t> leaf_begin, leaf_out;  // leaf_out: leaf_box.size() + 1
   // translation CSR and tasks
   std::vector<EntryRange> ent_range;
   std::vector<int32_t> entries;               // (src box << kModeBits) | mode

@@ -50,6 +50,25 @@ void ck(cudaError_t e, const char* what) {
   throw CudaFail{code, std::string(what) + ": " + cudaGetErrorString(e)};
 }
 
+// Scratch device buffers freed at scope exit.
+struct TmpDev {
+  std::vector<void*> ptrs;
+  TmpDev() = default;
+  TmpDev(const TmpDev&) = delete;
+  TmpDev& operator=(const TmpDev&) = delete;
+  ~TmpDev() {
+    for (void* p : ptrs) cudaFree(p);
+  }
+  template <class T>
+  const T* up(const T* src, size_t count) {
+    void* p = nullptr;
+    ck(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)), "cudaMalloc");
+    ptrs.push_back(p);
+    if (count) ck(cudaMemcpy(p, src, count * sizeof(T), cudaMemcpyHostToDevice), "upload");
+    return static_cast<const T*>(p);
+  }
+};
+
 }  // namespace
 
 struct sfmm_gpu_plan {
@@ -268,13 +287,42 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
       dp.tasks = p->upload(hp.tasks);
       dp.n_tasks = (int64_t)hp.tasks.size();
       dp.n_interior = hp.n_interior_tasks;
-      dp.X = p->upload(hp.X);
-      dp.Y = p->upload(hp.Y);
-      dp.Z = p->upload(hp.Z);
-      dp.slot_id = p->upload(hp.slot_id);
-      dp.up_dst = p->upload(hp.up_dst);
-      dp.leaf_slot = p->upload(hp.leaf_slot);
-      dp.leaf_orig = p->upload(hp.leaf_orig);
+      // slot geometry, upward destinations and leaf maps are built on the
+      // device from the index arrays
+      dp.X = p->alloc<double>(hp.n_slots);
+      dp.Y = p->alloc<double>(hp.n_slots);
+      dp.Z = p->alloc<double>(hp.n_slots);
+      dp.slot_id = p->alloc<int32_t>(hp.n_slots);
+      dp.up_dst = p->alloc<int64_t>(hp.n_skel);
+      dp.leaf_slot = p->alloc<int64_t>(hp.n_owned_points);
+      dp.leaf_orig = p->alloc<int32_t>(hp.n_owned_points);
+      {
+        TmpDev tmp;
+        SlotBuildArgs a{};
+        a.box = dp.box;
+        a.n_boxes = hp.n_boxes;
+        a.posmap = tmp.up(hp.posmap.data(), hp.posmap.size());
+        a.iv = tmp.up(desc->iv, (size_t)hp.n_slots);
+        a.pts = tmp.up(desc->pts, (size_t)hp.n_points * hp.dim);
+        a.dim = hp.dim;
+        a.parent = tmp.up(hp.box_parent.data(), hp.box_parent.size());
+        a.parent_offset = tmp.up(hp.parent_offset.data(), hp.parent_offset.size());
+        a.leaf_box = tmp.up(hp.leaf_box.data(), hp.leaf_box.size());
+        a.leaf_begin = tmp.up(hp.leaf_begin.data(), hp.leaf_begin.size());
+        a.leaf_out = tmp.up(hp.leaf_out.data(), hp.leaf_out.size());
+        a.n_leaves = (int64_t)hp.leaf_box.size();
+        a.perm = tmp.up(desc->perm, (size_t)hp.n_points);
+        a.X = dp.X;
+        a.Y = dp.Y;
+        a.Z = dp.Z;
+        a.slot_id = dp.slot_id;
+        a.up_dst = dp.up_dst;
+        a.leaf_slot = dp.leaf_slot;
+        a.leaf_orig = dp.leaf_orig;
+        launch_build_slots(a, p->stream);
+        ck(cudaGetLastError(), "build slots");
+        ck(cudaStreamSynchronize(p->stream), "build slots");
+      }
       dp.T_off = p->upload(hp.T_off);
       // interpolation operators of the owned boxes, copied run by run
       dp.T = p->alloc<double>((size_t)hp.T_off[hp.n_boxes] * sw);
@@ -319,13 +367,7 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
       p->ds.QH = p->alloc<double>((size_t)hp.n_skel * sw);
       p->ds.UH = p->alloc<double>((size_t)hp.n_skel * sw);
       // release host copies that now live on the device
-      std::vector<double>().swap(hp.X);
-      std::vector<double>().swap(hp.Y);
-      std::vector<double>().swap(hp.Z);
-      std::vector<int32_t>().swap(hp.slot_id);
-      std::vector<int64_t>().swap(hp.up_dst);
-      std::vector<int64_t>().swap(hp.leaf_slot);
-      std::vector<int32_t>().swap(hp.leaf_orig);
+      std::vector<int32_t>().swap(hp.posmap);
       std::vector<int32_t>().swap(hp.entries);
       std::vector<Task>().swap(hp.tasks);
       std::vector<int32_t>().swap(hp.entries_full);
@@ -412,7 +454,12 @@ int sfmm_gpu_shard_describe(const sfmm_plan_desc* desc, int n_ranks, int rank, i
     if (hp.depth < 2) {
       for (int64_t i = 0; i < hp.n_owned_points; ++i) owned_points[i] = (int32_t)i;
     } else {
-      std::copy(hp.leaf_orig.begin(), hp.leaf_orig.end(), owned_points);
+      // owned points in slot order (as the device leaf maps order them)
+      for (size_t j = 0; j < hp.leaf_box.size(); ++j) {
+        const BoxRec& br = hp.box[hp.leaf_box[j]];
+        for (int32_t i = 0; i < br.n; ++i)
+          owned_points[hp.leaf_out[j] + hp.posmap[br.slot + i]] = desc->perm[hp.leaf_begin[j] + i];
+      }
     }
   }
   return SFMM_OK;
