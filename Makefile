@@ -10,11 +10,11 @@ LIB      := $(PKG)/lib
 OBJ      := build/obj
 ARCH     := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -I$(SRC) \
-            --expt-relaxed-constexpr -Xptxas -v
+            --expt-relaxed-constexpr -Xptxas -v -Xcompiler -fopenmp
 CXXFLAGS := -std=c++17 -O2 -fopenmp -fPIC -Iinclude -I$(SRC) -I/usr/local/cuda/include
 
 GPU_CU   := $(SRC)/kernels_translate.cu $(SRC)/kernels_tree.cu $(SRC)/kernels_probe.cu $(SRC)/kernels_multi.cu $(SRC)/skel_gpu.cu \
-            $(SRC)/sfmm_gpu.cu
+            $(SRC)/tree_gpu.cu $(SRC)/sfmm_gpu.cu
 GPU_OBJS := $(patsubst $(SRC)/%.cu,$(OBJ)/%.o,$(GPU_CU)) $(OBJ)/plan_build.o
 HDRS     := include/sfmm_gpu.h $(SRC)/common.cuh $(SRC)/launch.h $(SRC)/plan_build.h
 

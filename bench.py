@@ -419,7 +419,7 @@ def main():
     t_gen = time.perf_counter() - t0
     # GPU precompute keeps T in HBM: the plan takes it device-to-device
     hp = (host.HostPlan.build_gpu(kern, pts, args.leaf, args.tol, args.kappa, device=dev,
-                                  host_T=False)
+                                  host_T=False, tree="gpu")
           if args.precompute == "gpu" else
           host.HostPlan.build(kern, pts, args.leaf, args.tol, args.kappa))
     hinfo = hp.info()
@@ -580,6 +580,8 @@ def main():
                        "depth": hinfo["depth"], "n_boxes": hinfo["n_boxes"],
                        "k_max": hinfo["k_max"], "m_proj": hinfo["proj_scalars"],
                        "host_threads": host.get_threads(),
+                       "tree": "GPU tree builder (sfmm_gpu_build_tree)"
+                       if args.precompute == "gpu" else "host C++ tree builder",
                        "skeletons": "GPU skeletonizer (sfmm_gpu_build_skeletons)"
                        if args.precompute == "gpu" else "host C++ skeletonizer",
                        "operators": "device-resident, plan built device-to-device "

@@ -45,7 +45,8 @@ enum {
   SFMM_ECUDA = 3,
   SFMM_ENOMEM = 4,
   SFMM_ENCCL = 5,
-  SFMM_EUNSUPPORTED = 6
+  SFMM_EUNSUPPORTED = 6,
+  SFMM_EDEPTH = 7 /* sfmm::DepthExceededError: leaf capacity unreachable */
 };
 
 /* Flags for sfmm_gpu_apply. */
@@ -194,6 +195,48 @@ int sfmm_gpu_apply_end(sfmm_gpu_plan* plan, const void* q_dev, const void* recv_
 int sfmm_gpu_shard_describe(const sfmm_plan_desc* desc, int n_ranks, int rank, int64_t* counts,
                             int32_t* owner, int64_t* pack_idx, int64_t* unpack_idx,
                             int32_t* owned_points);
+
+/*
+ * GPU tree and neighbor lists: the device counterpart
+ * of the reference's build_tree + build_neighbors
+ * (/root/reference/proj/src/tree.cpp:148-355), bit-identical to it: same perm,
+ * level-major Morton box order, point ranges, level_begin and colleague /
+ * coarse / fine lists.  Errors as the reference: EINVAL (bad dim, capacity,
+ * point count, non-finite coordinate), EDUPLICATE (coincident points),
+ * EDEPTH (leaf capacity unreachable at the maximum depth).
+ */
+typedef struct sfmm_tree_arrays {
+  int32_t dim, depth, leaf_cap, n_boxes;
+  int64_t n_points;
+  const int32_t* perm;        /* tree position -> original index */
+  const double* pts;          /* n_points*dim, tree order, interleaved */
+  const int32_t* level_begin; /* depth+2 */
+  const int32_t* box_parent;  /* -1 for the root */
+  const int32_t* box_child;   /* n_boxes*8, by octant, -1 = none */
+  const int32_t* box_level;
+  const uint64_t* box_morton;
+  const int64_t* box_cell;    /* n_boxes*3 */
+  const double* box_center;   /* n_boxes*3 */
+  const double* box_half;
+  const int32_t* box_begin;
+  const int32_t* box_end;
+  const uint8_t* box_leaf;
+  const int64_t* coll_off;    /* colleagues, ascending, self included */
+  const int32_t* coll;
+  const int64_t* coarse_off;
+  const int32_t* coarse;
+  const int64_t* fine_off;
+  const int32_t* fine;
+  double seconds;             /* wall time of the build */
+} sfmm_tree_arrays;
+
+typedef struct sfmm_gpu_tree sfmm_gpu_tree;
+
+int sfmm_gpu_build_tree(int dim, int64_t n, const double* pts, int leaf_cap, int device,
+                        sfmm_gpu_tree** out);
+/* Points *arrays at the result's host arrays (valid until destroyed). */
+int sfmm_gpu_tree_arrays(const sfmm_gpu_tree* tree, sfmm_tree_arrays* arrays);
+void sfmm_gpu_tree_destroy(sfmm_gpu_tree* tree);
 
 /*
  * GPU skeletonization: the device counterpart of the

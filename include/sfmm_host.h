@@ -25,8 +25,7 @@
 extern "C" {
 #endif
 
-/* Return codes beyond sfmm_gpu.h's: */
-enum { SFMM_EDEPTH = 7 /* sfmm::DepthExceededError */ };
+/* Return codes: sfmm_gpu.h (SFMM_EDEPTH = sfmm::DepthExceededError). */
 
 /* Distributions, same order as sfmm::Distribution (bench.hpp:15), plus the
  * clustered Gaussian of config 3(b), which the reference does not define. */
@@ -79,6 +78,10 @@ const sfmm_plan_desc* sfmm_host_desc(sfmm_host_plan* plan);
 /* Box geometry (centre: n_boxes*3, half-width: n_boxes), needed by the GPU
  * skeletonizer's proxy surfaces (sfmm_tree_desc in sfmm_gpu.h). */
 int sfmm_host_box_geometry(const sfmm_host_plan* plan, double* center, double* half);
+
+/* Host plan around a tree built elsewhere (e.g. sfmm_gpu_build_tree): the
+ * arrays are copied; skeletons can then be set (sfmm_host_set_skeletons). */
+int sfmm_host_adopt_tree(const sfmm_tree_arrays* tree, sfmm_host_plan** out);
 
 /* Replaces the plan's skeleton fields with externally built ones (e.g. from
  * sfmm_gpu_build_skeletons); the arrays are copied.  skel->T may be NULL: the

@@ -20,7 +20,8 @@ KERNEL_IDS = {"laplace2d": 0, "laplace3d": 1, "helmholtz2d": 2, "helmholtz3d": 3
 KERNEL_DIM = {0: 2, 1: 3, 2: 2, 3: 3}
 
 # return codes
-SFMM_OK, SFMM_EINVAL, SFMM_EDUPLICATE, SFMM_ECUDA, SFMM_ENOMEM, SFMM_ENCCL, SFMM_EUNSUPPORTED = range(7)
+(SFMM_OK, SFMM_EINVAL, SFMM_EDUPLICATE, SFMM_ECUDA, SFMM_ENOMEM, SFMM_ENCCL, SFMM_EUNSUPPORTED,
+ SFMM_EDEPTH) = range(8)
 SFMM_HOST_BUFFERS, SFMM_DEVICE_BUFFERS = 0, 1
 
 _i32p = C.POINTER(C.c_int32)
@@ -115,6 +116,22 @@ class TreeDesc(C.Structure):
         ("box_leaf", _u8p),
         ("box_center", _f64p),
         ("box_half", _f64p),
+    ]
+
+
+class TreeArrays(C.Structure):
+    """struct sfmm_tree_arrays (output of the GPU tree builder)."""
+
+    _fields_ = [
+        ("dim", C.c_int32), ("depth", C.c_int32), ("leaf_cap", C.c_int32), ("n_boxes", C.c_int32),
+        ("n_points", C.c_int64),
+        ("perm", _i32p), ("pts", _f64p), ("level_begin", _i32p), ("box_parent", _i32p),
+        ("box_child", _i32p), ("box_level", _i32p), ("box_morton", C.POINTER(C.c_uint64)),
+        ("box_cell", _i64p), ("box_center", _f64p), ("box_half", _f64p), ("box_begin", _i32p),
+        ("box_end", _i32p), ("box_leaf", _u8p),
+        ("coll_off", _i64p), ("coll", _i32p), ("coarse_off", _i64p), ("coarse", _i32p),
+        ("fine_off", _i64p), ("fine", _i32p),
+        ("seconds", C.c_double),
     ]
 
 
@@ -313,6 +330,12 @@ def gpu_lib() -> C.CDLL:
     lib.sfmm_gpu_plan_create_skel.argtypes = [C.POINTER(PlanDesc), vp, C.c_int, C.c_int, C.c_int,
                                               C.POINTER(vp)]
     lib.sfmm_gpu_plan_create_skel.restype = C.c_int
+    lib.sfmm_gpu_build_tree.argtypes = [C.c_int, C.c_int64, vp, C.c_int, C.c_int, C.POINTER(vp)]
+    lib.sfmm_gpu_build_tree.restype = C.c_int
+    lib.sfmm_gpu_tree_arrays.argtypes = [vp, C.POINTER(TreeArrays)]
+    lib.sfmm_gpu_tree_arrays.restype = C.c_int
+    lib.sfmm_gpu_tree_destroy.argtypes = [vp]
+    lib.sfmm_gpu_tree_destroy.restype = None
     lib.sfmm_gpu_skel_destroy.argtypes = [vp]
     lib.sfmm_gpu_skel_destroy.restype = None
     lib.sfmm_gpu_test_sincos.argtypes = [vp, C.c_int64, vp]
@@ -329,5 +352,6 @@ GPU_SYMBOLS = [
     "sfmm_gpu_apply_begin", "sfmm_gpu_apply_end", "sfmm_gpu_shard_describe",
     "sfmm_gpu_build_skeletons", "sfmm_gpu_skel_fill", "sfmm_gpu_skel_destroy",
     "sfmm_gpu_test_sincos", "sfmm_gpu_skel_describe", "sfmm_gpu_skel_device_T",
-    "sfmm_gpu_plan_create_skel",
+    "sfmm_gpu_plan_create_skel", "sfmm_gpu_build_tree", "sfmm_gpu_tree_arrays",
+    "sfmm_gpu_tree_destroy",
 ]

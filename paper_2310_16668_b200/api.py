@@ -56,6 +56,9 @@ def _raise(rc: int) -> None:
         raise NotImplementedError(msg)
     if rc == _abi.SFMM_ENOMEM:
         raise MemoryError(msg)
+    if rc == _abi.SFMM_EDEPTH:
+        from .host import DepthExceededError
+        raise DepthExceededError(msg)
     raise DeviceError(msg)
 
 

@@ -237,8 +237,52 @@ int sfmm_host_build_tree(int dim, int64_t n, const double* pts, int leaf_cap,
     auto p = std::make_unique<sfmm_host_plan>();
     const double t0 = now();
     p->tree = sfmm_host::build_tree(dim, n, pts, leaf_cap);
+    const double t1 = now();
     p->nb = sfmm_host::build_neighbors(p->tree);
     p->info.t_tree = now() - t0;
+    if (std::getenv("SFMM_TREE_VERBOSE")) std::fprintf(stderr, "[tree] neighbors    %.3f s\n", now() - t1);
+    p->export_desc();
+    *out = p.release();
+  });
+}
+
+int sfmm_host_adopt_tree(const sfmm_tree_arrays* a, sfmm_host_plan** out) {
+  if (!a || !out) return fail(SFMM_EINVAL, "null argument");
+  return guarded([&] {
+    auto p = std::make_unique<sfmm_host_plan>();
+    sfmm_host::Tree& t = p->tree;
+    const int32_t nb = a->n_boxes;
+    const int64_t n = a->n_points;
+    t.dim = a->dim;
+    t.depth = a->depth;
+    t.leaf_cap = a->leaf_cap;
+    t.level_begin.assign(a->level_begin, a->level_begin + a->depth + 2);
+    t.perm.assign(a->perm, a->perm + n);
+    t.pts.assign(a->pts, a->pts + n * a->dim);
+    t.boxes.resize(nb);
+    for (int32_t i = 0; i < nb; ++i) {
+      sfmm_host::Box& b = t.boxes[i];
+      b.parent = a->box_parent[i];
+      for (int c = 0; c < 8; ++c) b.child[c] = a->box_child[8 * (int64_t)i + c];
+      b.level = a->box_level[i];
+      b.morton = a->box_morton[i];
+      for (int k = 0; k < 3; ++k) {
+        b.cell[k] = a->box_cell[3 * (int64_t)i + k];
+        b.center[k] = a->box_center[3 * (int64_t)i + k];
+      }
+      b.half = a->box_half[i];
+      b.begin = a->box_begin[i];
+      b.end = a->box_end[i];
+      b.leaf = a->box_leaf[i] != 0;
+    }
+    sfmm_host::Neighbors& g = p->nb;
+    g.coll_off.assign(a->coll_off, a->coll_off + nb + 1);
+    g.coll.assign(a->coll, a->coll + g.coll_off[nb]);
+    g.coarse_off.assign(a->coarse_off, a->coarse_off + nb + 1);
+    g.coarse.assign(a->coarse, a->coarse + g.coarse_off[nb]);
+    g.fine_off.assign(a->fine_off, a->fine_off + nb + 1);
+    g.fine.assign(a->fine, a->fine + g.fine_off[nb]);
+    p->info.t_tree = a->seconds;
     p->export_desc();
     *out = p.release();
   });

@@ -12,6 +12,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <limits>
@@ -281,12 +283,26 @@ Tree build_tree(int dim, int64_t n, const double* pts, int leaf_cap) {
     throw std::invalid_argument("build_tree: point count out of range");
   for (int64_t i = 0; i < n * dim; ++i)
     if (!std::isfinite(pts[i])) throw std::invalid_argument("build_tree: non-finite coordinate");
+  // SFMM_TREE_VERBOSE=1: per-phase wall time on stderr
+  static const bool verbose = std::getenv("SFMM_TREE_VERBOSE") != nullptr;
+  double t_prev = omp_get_wtime();
+  auto mark = [&](const char* what) {
+    if (!verbose) return;
+    const double t = omp_get_wtime();
+    std::fprintf(stderr, "[tree] %-12s %.3f s\n", what, t - t_prev);
+    t_prev = t;
+  };
   reject_duplicates(dim, n, pts);
+  mark("duplicates");
   Builder b(dim, n, pts, leaf_cap);
   b.make_root();
   b.refine();
-  b.balance();
-  return b.finish();
+  mark("refine");
+  if (!std::getenv("SFMM_TREE_NO_BALANCE")) b.balance();  // debug aid: refinement only
+  mark("balance");
+  Tree t = b.finish();
+  mark("finish");
+  return t;
 }
 
 Neighbors build_neighbors(const Tree& t) {

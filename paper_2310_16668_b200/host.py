@@ -68,6 +68,7 @@ def host_lib() -> C.CDLL:
         lib.sfmm_host_set_skeletons.argtypes = [vp, C.POINTER(PlanDesc), C.c_int, C.c_double,
                                                 C.c_int32, C.c_int64, C.c_int32, C.c_double]
         lib.sfmm_host_set_T.argtypes = [vp, vp, C.c_int64]
+        lib.sfmm_host_adopt_tree.argtypes = [C.POINTER(_abi.TreeArrays), C.POINTER(vp)]
         _lib = lib
     return _lib
 
@@ -131,16 +132,19 @@ class HostPlan:
     @classmethod
     def build_gpu(cls, kernel: int, pts: np.ndarray, leaf_cap: int, tol: float,
                   kappa: float = 1.0, proxy: tuple | None = None, device: int = 0,
-                  host_T: bool = True) -> "HostPlan":
+                  host_T: bool = True, tree: str = "host") -> "HostPlan":
         """Tree and neighbor lists on the host (bit-identical to the reference),
         skeletons on the GPU (sfmm_gpu_build_skeletons).
 
         host_T=False keeps the interpolation operators on the device only
         (SURVEY.md 8(f) row 2): the descriptor's T is NULL, api.GpuPlan.from_host
         takes T device-to-device, and fetch_T() downloads it when a host copy is
-        needed (e.g. for the CPU reference)."""
+        needed (e.g. for the CPU reference).  tree="gpu" builds the tree and
+        neighbor lists on the GPU too (build_tree_gpu)."""
         from .api import _raise
-        hp = cls.build_tree(pts, leaf_cap)
+        if tree not in ("host", "gpu"):
+            raise ValueError("build_gpu: tree must be 'host' or 'gpu'")
+        hp = cls.build_tree_gpu(pts, leaf_cap, device) if tree == "gpu" else cls.build_tree(pts, leaf_cap)
         d = host_lib().sfmm_host_desc(hp._h).contents
         nb = int(d.n_boxes)
         center = np.zeros(3 * nb)
@@ -197,6 +201,27 @@ class HostPlan:
         if self._skel is not None:
             _abi.gpu_lib().sfmm_gpu_skel_destroy(self._skel)
             self._skel = None
+
+    @classmethod
+    def build_tree_gpu(cls, pts: np.ndarray, leaf_cap: int, device: int = 0) -> "HostPlan":
+        """Tree and neighbor lists built on the GPU (sfmm_gpu_build_tree,
+        SURVEY.md 8(f) row 3), bit-identical to build_tree."""
+        from .api import _raise
+        pts = np.ascontiguousarray(pts, dtype=np.float64)
+        if pts.ndim != 2:
+            raise ValueError("build_tree: points must be an (n, dim) array")
+        lib = _abi.gpu_lib()
+        t = C.c_void_p()
+        _raise(lib.sfmm_gpu_build_tree(pts.shape[1], pts.shape[0], pts.ctypes.data, leaf_cap, device,
+                                       C.byref(t)))
+        try:
+            arr = _abi.TreeArrays()
+            _raise(lib.sfmm_gpu_tree_arrays(t, C.byref(arr)))
+            h = C.c_void_p()
+            _check(host_lib().sfmm_host_adopt_tree(C.byref(arr), C.byref(h)))
+        finally:
+            lib.sfmm_gpu_tree_destroy(t)
+        return cls(h)
 
     @classmethod
     def build_tree(cls, pts: np.ndarray, leaf_cap: int) -> "HostPlan":
