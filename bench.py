@@ -257,7 +257,8 @@ def run_sharded(args, ws, rank, local):
     if rank == 0:
         # torchrun sets OMP_NUM_THREADS=1; the other ranks wait at the barrier
         host.set_threads(os.cpu_count() or 1)
-        hp = (host.HostPlan.build_gpu(kern, pts, args.leaf, args.tol, args.kappa)
+        hp = (host.HostPlan.build_gpu(kern, pts, args.leaf, args.tol, args.kappa, device=dev,
+                                      tree="gpu")
               if args.precompute == "gpu" else
               host.HostPlan.build(kern, pts, args.leaf, args.tol, args.kappa))
         hinfo = hp.info()
