@@ -12,9 +12,10 @@
 // fragment order; the next chunk's loads are in flight during the compute).
 // Per k-step (4 sources) every lane generates the one G entry its A-fragment
 // holds (row = lane/4, source = lane%4) -- one pair per lane, no shuffles --
-// and the warp issues 8 DMMAs (complex) or 2 (real) per row tile.  Complex products use
-// U = Gr [Ar | Ai] + Gi [-Ai | Ar] so both real products accumulate into the
-// same fragments.  On B200 DMMA shares the FP64 datapath with DFMA (both
+// and the warp issues 6 DMMAs (complex) or 2 (real) per row tile.  Complex products use
+// the 3-multiplication form T1 = Gr Ar, T2 = Gi Ai, T3 = (Gr + Gi)(Ar + Ai),
+// Re U = T1 - T2, Im U = T3 - T1 - T2 (25 % fewer DMMAs than the 4-product
+// form; error bound eps * sum |G||A| like it).  On B200 DMMA shares the FP64 datapath with DFMA (both
 // measured at 37 TFLOP/s, see profiles/), so the gain over scalar code is
 // issue slots and registers, not peak.
 #include <math.h>
@@ -85,8 +86,8 @@ __device__ __noinline__ void verify_row_m(const K2MArgs& a, int32_t b, int32_t r
 // loads its fragment with one conflict-free 8-byte LDS.
 template <bool CPLX>
 struct ChunkM {
-  static constexpr int NB = CPLX ? 4 : 2;  // 8-column blocks of [Ar | Ai] or [A]
-  static constexpr int NP = CPLX ? 2 : 1;  // B1 = [Ar | Ai] and B2 = [-Ai | Ar]
+  static constexpr int NB = 2;             // 8-column rhs blocks
+  static constexpr int NP = CPLX ? 3 : 1;  // B = Ar, Ai, Ar + Ai (complex) or A
   double x[kChunk], y[kChunk], z[kChunk];
   double a[4][NP][NB][32];
   double h[4][NP][NB][32];
@@ -113,7 +114,8 @@ template <int KER, bool WH>
 __global__ void __launch_bounds__(kMThreads, WH ? 2 : 3) k2m_translate(K2MArgs a) {
   constexpr bool CPLX = KER == SFMM_HELMHOLTZ3D;
   constexpr int SW = CPLX ? 2 : 1;
-  constexpr int NB = CPLX ? 4 : 2;
+  constexpr int NB = 2;             // rhs blocks of 8
+  constexpr int NP = CPLX ? 3 : 1;  // real products per complex product (3M)
   constexpr int DIM = KER == SFMM_LAPLACE2D ? 2 : 3;
   constexpr int ITEMS = StageRegs<CPLX>::ITEMS;
   __shared__ ChunkM<CPLX> ch;
@@ -142,11 +144,14 @@ __global__ void __launch_bounds__(kMThreads, WH ? 2 : 3) k2m_translate(K2MArgs a
       yr[mt] = a.Y[s];
       zr[mt] = DIM == 3 ? a.Z[s] : 0.0;
     }
-    double C[2][NB][2], H[2][NB][2];
+    double C[2][NP][NB][2], H[2][NP][NB][2];
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-      for (int nb = 0; nb < NB; ++nb) C[mt][nb][0] = C[mt][nb][1] = H[mt][nb][0] = H[mt][nb][1] = 0.0;
+      for (int pp = 0; pp < NP; ++pp)
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb)
+          C[mt][pp][nb][0] = C[mt][pp][nb][1] = H[mt][pp][nb][0] = H[mt][pp][nb][1] = 0.0;
     const bool skel_rows = WH && task.row0 < tb.k;
 
     // chunk iterator over (entry, first source), skipping empty source boxes
@@ -221,14 +226,12 @@ __global__ void __launch_bounds__(kMThreads, WH ? 2 : 3) k2m_translate(K2MArgs a
         if (CPLX) {
           const int nb = r >> 3;
           ch.a[ks][0][nb][fl] = wa[0];
-          ch.a[ks][0][2 + nb][fl] = wa[1];
-          ch.a[ks][CPLX ? 1 : 0][nb][fl] = -wa[1];
-          ch.a[ks][CPLX ? 1 : 0][2 + nb][fl] = wa[0];
+          ch.a[ks][NP - 2][nb][fl] = wa[SW - 1];
+          ch.a[ks][NP - 1][nb][fl] = wa[0] + wa[SW - 1];
           if (need_h) {
             ch.h[ks][0][nb][fl] = wh[0];
-            ch.h[ks][0][2 + nb][fl] = wh[1];
-            ch.h[ks][CPLX ? 1 : 0][nb][fl] = -wh[1];
-            ch.h[ks][CPLX ? 1 : 0][2 + nb][fl] = wh[0];
+            ch.h[ks][NP - 2][nb][fl] = wh[SW - 1];
+            ch.h[ks][NP - 1][nb][fl] = wh[0] + wh[SW - 1];
           }
         } else {
           ch.a[ks][0][r >> 3][fl] = wa[0];
@@ -291,27 +294,33 @@ __global__ void __launch_bounds__(kMThreads, WH ? 2 : 3) k2m_translate(K2MArgs a
             }
             if (self && rowi[mt] == j0 + js) gr[mt] = gi[mt] = 0.0;
           }
+          // A operands of the NP real products: Gr (, Gi, Gr + Gi)
+          double g[NP][2];
 #pragma unroll
-          for (int nb = 0; nb < NB; ++nb) {
-            const double b1 = ch.a[ks][0][nb][lane];
-            const double b2 = CPLX ? ch.a[ks][CPLX ? 1 : 0][nb][lane] : 0.0;
-#pragma unroll
-            for (int mt = 0; mt < 2; ++mt) {
-              dmma(C[mt][nb][0], C[mt][nb][1], gr[mt], b1);
-              if (CPLX) dmma(C[mt][nb][0], C[mt][nb][1], gi[mt], b2);
+          for (int mt = 0; mt < 2; ++mt) {
+            g[0][mt] = gr[mt];
+            if (CPLX) {
+              g[NP - 2][mt] = gi[mt];
+              g[NP - 1][mt] = gr[mt] + gi[mt];
             }
           }
-          if (need_h) {
+#pragma unroll
+          for (int pp = 0; pp < NP; ++pp)
 #pragma unroll
             for (int nb = 0; nb < NB; ++nb) {
-              const double b1 = ch.h[ks][0][nb][lane];
-              const double b2 = CPLX ? ch.h[ks][CPLX ? 1 : 0][nb][lane] : 0.0;
+              const double bv = ch.a[ks][pp][nb][lane];
 #pragma unroll
-              for (int mt = 0; mt < 2; ++mt) {
-                dmma(H[mt][nb][0], H[mt][nb][1], gr[mt], b1);
-                if (CPLX) dmma(H[mt][nb][0], H[mt][nb][1], gi[mt], b2);
-              }
+              for (int mt = 0; mt < 2; ++mt) dmma(C[mt][pp][nb][0], C[mt][pp][nb][1], g[pp][mt], bv);
             }
+          if (need_h) {
+#pragma unroll
+            for (int pp = 0; pp < NP; ++pp)
+#pragma unroll
+              for (int nb = 0; nb < NB; ++nb) {
+                const double bv = ch.h[ks][pp][nb][lane];
+#pragma unroll
+                for (int mt = 0; mt < 2; ++mt) dmma(H[mt][pp][nb][0], H[mt][pp][nb][1], g[pp][mt], bv);
+              }
           }
         }
       }
@@ -326,8 +335,10 @@ __global__ void __launch_bounds__(kMThreads, WH ? 2 : 3) k2m_translate(K2MArgs a
       if (row >= rend) continue;
       bool bad = false;
 #pragma unroll
-      for (int nb = 0; nb < NB; ++nb)
-        bad = bad || !isfinite(C[mt][nb][0]) || !isfinite(C[mt][nb][1]);
+      for (int pp = 0; pp < NP; ++pp)
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb)
+          bad = bad || !isfinite(C[mt][pp][nb][0]) || !isfinite(C[mt][pp][nb][1]);
       if (bad) verify_row_m(a, task.box, row, DIM);
       double* u = a.U + (tb.slot + row) * (kNRHS * SW);
       const bool skel_row = row < tb.k;
@@ -338,15 +349,17 @@ __global__ void __launch_bounds__(kMThreads, WH ? 2 : 3) k2m_translate(K2MArgs a
         for (int w = 0; w < 2; ++w) {
           const int rhs = c0 + 8 * half + w;
           if (CPLX) {
-            u[2 * rhs] = C[mt][half][w] * scale;
-            u[2 * rhs + 1] = C[mt][2 + half][w] * scale;
+            const double t1 = C[mt][0][half][w], t2 = C[mt][NP - 2][half][w];
+            u[2 * rhs] = (t1 - t2) * scale;
+            u[2 * rhs + 1] = (C[mt][NP - 1][half][w] - t1 - t2) * scale;
             if (skel_row) {
-              uh[2 * rhs] = -H[mt][half][w] * scale;
-              uh[2 * rhs + 1] = -H[mt][2 + half][w] * scale;
+              const double h1 = H[mt][0][half][w], h2 = H[mt][NP - 2][half][w];
+              uh[2 * rhs] = -(h1 - h2) * scale;
+              uh[2 * rhs + 1] = -(H[mt][NP - 1][half][w] - h1 - h2) * scale;
             }
           } else {
-            u[rhs] = C[mt][half][w] * scale;
-            if (skel_row) uh[rhs] = -H[mt][half][w] * scale;
+            u[rhs] = C[mt][0][half][w] * scale;
+            if (skel_row) uh[rhs] = -H[mt][0][half][w] * scale;
           }
         }
       }
