@@ -308,8 +308,9 @@ int sfmm_gpu_get_timings(sfmm_gpu_plan* plan, float* ms, int max_applies, int* n
  * a register-resident DFMA loop run on every SM for ~50 ms. */
 int sfmm_gpu_fp64_peak(int device, double* tflops);
 
-/* Test hook for the device sincos used by the Helmholtz kernels: for each x_i,
- * out[4i..4i+3] = (sin, cos) of the fast routine and of the CUDA library. */
+/* Test hook (device math of the Helmholtz kernels): out[6i..6i+5] = (sin, cos)
+ * of x_i from the branch-free routine, the table-driven routine and the CUDA
+ * library. */
 int sfmm_gpu_test_sincos(const double* x, int64_t n, double* out);
 
 /* Dense u_i = sum_{j != i} G(x_i, x_j) q_j over the points in their given

@@ -10,7 +10,50 @@
 // tests/test_kernels_gpu.py.
 #pragma once
 
+#include <cmath>
+
 namespace sfmm_gpu {
+
+// ---- table-driven variant (the translation kernels) ----------------------
+// x = n pi/128 + t with |t| <= pi/256 (Cody-Waite, the fdlibm pi/2 split
+// scaled by 1/64, exact for |n| < 2^20); sin t and cos t from their Taylor
+// series to degree 7 / 6 (truncation < 1e-20); then one complex product with
+// (cos, sin)(k pi/128), k = n mod 256, from a 256-entry table the caller keeps
+// in shared memory.  The scale w (1/r in the kernels) is folded into the table
+// entry.  About 16 FP64 instructions; checked in tests/test_kernels_gpu.py.
+constexpr int kSinCosTab = 256;
+constexpr double kSinCosTabMaxArg = 2.0e4;  // |n| < 2^20 with margin (2^20 pi/128 = 25736)
+
+// (cos, sin)(k pi/128), correctly rounded from long double.
+inline void fill_sincos_table(double2* out) {
+  const long double step = 3.141592653589793238462643383279502884L / 128.0L;
+  for (int k = 0; k < kSinCosTab; ++k) {
+    out[k].x = static_cast<double>(cosl(step * k));
+    out[k].y = static_cast<double>(sinl(step * k));
+  }
+}
+
+__device__ __forceinline__ void sincos_tab_scaled(const double2* __restrict__ tab, double x,
+                                                  double w, double* re, double* im) {
+  const double magic = 6755399441055744.0;  // 1.5 * 2^52: n lands in the low word
+  const double nd = fma(x, 40.74366543152520595683, magic);  // 128/pi
+  const int k = __double2loint(nd) & (kSinCosTab - 1);
+  const double n = nd - magic;
+  double t = fma(-n, 1.57079632673412561417e+00 / 64, x);
+  t = fma(-n, 6.07710050630396597660e-11 / 64, t);
+  t = fma(-n, 2.02226624879595063154e-21 / 64, t);
+  const double z = t * t;
+  double ps = fma(z, -1.0 / 5040, 1.0 / 120);
+  ps = fma(z, ps, -1.0 / 6);
+  const double s = fma(t * z, ps, t);
+  double pc = fma(z, -1.0 / 720, 1.0 / 24);
+  pc = fma(z, pc, -0.5);
+  const double c = fma(z, pc, 1.0);
+  const double2 T = tab[k];
+  const double tc = T.x * w, ts = T.y * w;
+  *re = fma(tc, c, -ts * s);
+  *im = fma(ts, c, tc * s);
+}
 
 __device__ __forceinline__ void sincos_fast(double x, double* sp, double* cp) {
   const double j = rint(x * 0.63661977236758134308);  // 2/pi

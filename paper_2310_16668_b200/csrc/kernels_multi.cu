@@ -61,6 +61,7 @@ struct K2MArgs {
   int* counter;
   int* err;
   double kappa;
+  const double2* tab;  // (cos, sin)(k pi/128), Helmholtz only
 };
 
 __device__ __noinline__ void verify_row_m(const K2MArgs& a, int32_t b, int32_t row, int dim) {
@@ -110,7 +111,8 @@ struct ChunkPos {
 // KER: 0 laplace2d, 1 laplace3d, 3 helmholtz3d
 // WH: the launch's tasks own skeleton rows (uhat accumulators needed).  Tasks
 // without skeleton rows -- most of them -- run the lighter WH=false variant.
-template <int KER, bool WH>
+// TAB: Helmholtz arguments within the sincos table's range (sincos_fast otherwise).
+template <int KER, bool WH, bool TAB>
 __global__ void __launch_bounds__(kMThreads, WH ? 2 : 3) k2m_translate(K2MArgs a) {
   constexpr bool CPLX = KER == SFMM_HELMHOLTZ3D;
   constexpr int SW = CPLX ? 2 : 1;
@@ -120,7 +122,10 @@ __global__ void __launch_bounds__(kMThreads, WH ? 2 : 3) k2m_translate(K2MArgs a
   constexpr int ITEMS = StageRegs<CPLX>::ITEMS;
   __shared__ ChunkM<CPLX> ch;
   __shared__ int s_task;
+  __shared__ double2 tab[CPLX ? kSinCosTab : 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (CPLX && TAB)
+    for (int i = tid; i < kSinCosTab; i += blockDim.x) tab[i] = a.tab[i];
   const int rq = lane >> 2, kq = lane & 3;  // A-fragment row / k index of this lane
   for (;;) {
     __syncthreads();
@@ -283,10 +288,14 @@ __global__ void __launch_bounds__(kMThreads, WH ? 2 : 3) k2m_translate(K2MArgs a
             } else {
               const double yv = rsqrt_fp64m(r2);
               if (CPLX) {
-                double sn, cs;
-                sincos_fast(a.kappa * (r2 * yv), &sn, &cs);
-                gr[mt] = cs * yv;
-                gi[mt] = sn * yv;
+                if constexpr (TAB) {
+                  sincos_tab_scaled(tab, a.kappa * (r2 * yv), yv, &gr[mt], &gi[mt]);
+                } else {
+                  double sn, cs;
+                  sincos_fast(a.kappa * (r2 * yv), &sn, &cs);
+                  gr[mt] = cs * yv;
+                  gi[mt] = sn * yv;
+                }
               } else {
                 gr[mt] = yv;
                 gi[mt] = 0.0;
@@ -522,7 +531,7 @@ int grid_m(int64_t n) {
 template <int KER, bool WH>
 int blocks_per_sm() {
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2m_translate<KER, WH>, kMThreads, 0) !=
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2m_translate<KER, WH, KER == SFMM_HELMHOLTZ3D>, kMThreads, 0) !=
       cudaSuccess)
     return -1;
   return std::max(1, per_sm);
@@ -624,6 +633,7 @@ void launch_translate_m(const DevPlan& p, DevState& s, cudaStream_t st) {
   a.UH = s.UH;
   a.err = p.err_flag;
   a.kappa = p.kappa;
+  a.tab = p.sc_tab;
   cudaMemsetAsync(p.counter + 2, 0, 2 * sizeof(int), st);
   // tasks [0, n_tasks_mh) own skeleton rows, the rest do not
   for (int part = 0; part < 2; ++part) {
@@ -634,19 +644,21 @@ void launch_translate_m(const DevPlan& p, DevState& s, cudaStream_t st) {
     a.n_tasks = t1 - t0;
     a.counter = p.counter + 2 + part;
     const int grid = (int)std::min<int64_t>(part == 0 ? p.k2m_grid : p.k2m_grid0, t1 - t0);
-#define SFMM_K2M_LAUNCH(KER)                                                        \
+#define SFMM_K2M_LAUNCH(KER, TAB)                                                   \
   do {                                                                              \
     if (part == 0)                                                                  \
-      k2m_translate<KER, true><<<grid, kMThreads, 0, st>>>(a);                      \
+      k2m_translate<KER, true, TAB><<<grid, kMThreads, 0, st>>>(a);                 \
     else                                                                            \
-      k2m_translate<KER, false><<<grid, kMThreads, 0, st>>>(a);                     \
+      k2m_translate<KER, false, TAB><<<grid, kMThreads, 0, st>>>(a);                \
   } while (0)
-    if (p.kernel == SFMM_HELMHOLTZ3D)
-      SFMM_K2M_LAUNCH(SFMM_HELMHOLTZ3D);
+    if (p.kernel == SFMM_HELMHOLTZ3D && p.sc_tab_ok)
+      SFMM_K2M_LAUNCH(SFMM_HELMHOLTZ3D, true);
+    else if (p.kernel == SFMM_HELMHOLTZ3D)
+      SFMM_K2M_LAUNCH(SFMM_HELMHOLTZ3D, false);
     else if (p.kernel == SFMM_LAPLACE3D)
-      SFMM_K2M_LAUNCH(SFMM_LAPLACE3D);
+      SFMM_K2M_LAUNCH(SFMM_LAPLACE3D, false);
     else
-      SFMM_K2M_LAUNCH(SFMM_LAPLACE2D);
+      SFMM_K2M_LAUNCH(SFMM_LAPLACE2D, false);
 #undef SFMM_K2M_LAUNCH
   }
 }

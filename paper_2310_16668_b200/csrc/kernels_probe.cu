@@ -11,16 +11,19 @@
 namespace sfmm_gpu {
 namespace {
 
-__global__ void sincos_check(const double* x, int64_t n, double* out) {
+__global__ void sincos_check(const double* x, int64_t n, const double2* tab, double* out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    double s, c, s_ref, c_ref;
+    double s, c, st, ct, s_ref, c_ref;
     sincos_fast(x[i], &s, &c);
+    sincos_tab_scaled(tab, x[i], 1.0, &ct, &st);
     sincos(x[i], &s_ref, &c_ref);
-    out[4 * i] = s;
-    out[4 * i + 1] = c;
-    out[4 * i + 2] = s_ref;
-    out[4 * i + 3] = c_ref;
+    out[6 * i] = s;
+    out[6 * i + 1] = c;
+    out[6 * i + 2] = st;
+    out[6 * i + 3] = ct;
+    out[6 * i + 4] = s_ref;
+    out[6 * i + 5] = c_ref;
   }
 }
 
@@ -28,14 +31,20 @@ __global__ void sincos_check(const double* x, int64_t n, double* out) {
 
 int test_sincos(const double* x_host, int64_t n, double* out_host) {
   double *dx = nullptr, *dout = nullptr;
+  double2* dtab = nullptr;
+  double2 tab[kSinCosTab];
+  fill_sincos_table(tab);
   if (cudaMalloc(&dx, n * sizeof(double)) != cudaSuccess) return -1;
-  if (cudaMalloc(&dout, 4 * n * sizeof(double)) != cudaSuccess) return -1;
+  if (cudaMalloc(&dout, 6 * n * sizeof(double)) != cudaSuccess) return -1;
+  if (cudaMalloc(&dtab, sizeof(tab)) != cudaSuccess) return -1;
   cudaMemcpy(dx, x_host, n * sizeof(double), cudaMemcpyHostToDevice);
-  sincos_check<<<148 * 4, 256>>>(dx, n, dout);
-  cudaMemcpy(out_host, dout, 4 * n * sizeof(double), cudaMemcpyDeviceToHost);
+  cudaMemcpy(dtab, tab, sizeof(tab), cudaMemcpyHostToDevice);
+  sincos_check<<<148 * 4, 256>>>(dx, n, dtab, dout);
+  cudaMemcpy(out_host, dout, 6 * n * sizeof(double), cudaMemcpyDeviceToHost);
   const bool ok = cudaGetLastError() == cudaSuccess;
   cudaFree(dx);
   cudaFree(dout);
+  cudaFree(dtab);
   return ok ? 0 : -1;
 }
 

@@ -55,6 +55,7 @@ struct K2Args {
   int* err;
   double kappa;
   double* St;  // staging for kSYM column sums (unscaled)
+  const double2* tab;  // (cos, sin)(k pi/128), Helmholtz only
 };
 
 // Far-away padding for partial source chunks of kSYM blocks: finite r^2,
@@ -331,8 +332,9 @@ __global__ void __launch_bounds__(kThreads, SFMM_K2_MIN_BLOCKS) k2_translate_rea
 // ---------------------------------------------------------------------------
 // Helmholtz 3D, complex FP64: G = exp(i kappa r)/(4 r) (kernel.hpp:62-71).
 // ---------------------------------------------------------------------------
-template <int R, bool H, bool SELF>
-__device__ __forceinline__ void inner_cplx(const WarpSmemCplx& sm, int cnt, int j0, double kappa,
+template <int R, bool H, bool SELF, bool TAB>
+__device__ __forceinline__ void inner_cplx(const WarpSmemCplx& sm, const double2* __restrict__ tab,
+                                           int cnt, int j0, double kappa,
                                            const double (&xi)[R], const double (&yi)[R],
                                            const double (&zi)[R], const int (&rowi)[R],
                                            double2 (&au)[R], double2 (&ah)[R]) {
@@ -347,9 +349,15 @@ __device__ __forceinline__ void inner_cplx(const WarpSmemCplx& sm, int cnt, int 
       const double dx = xi[r] - xy.x, dy = yi[r] - xy.y, dz = zi[r] - zz;
       const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
       const double y = rsqrt_fp64(r2);
-      double s, c;
-      sincos_fast(kappa * (r2 * y), &s, &c);
-      double gr = c * y, gi = s * y;
+      double gr, gi;
+      if constexpr (TAB) {
+        sincos_tab_scaled(tab, kappa * (r2 * y), y, &gr, &gi);
+      } else {  // arguments beyond the table's exact reduction range
+        double s, c;
+        sincos_fast(kappa * (r2 * y), &s, &c);
+        gr = c * y;
+        gi = s * y;
+      }
       if (SELF && rowi[r] == j0 + jj) {
         gr = 0.0;
         gi = 0.0;
@@ -364,9 +372,9 @@ __device__ __forceinline__ void inner_cplx(const WarpSmemCplx& sm, int cnt, int 
   }
 }
 
-template <int R>
+template <int R, bool TAB>
 __device__ __forceinline__ void task_cplx(const K2Args& a, const Task& t, WarpSmemCplx& sm,
-                                          int lane) {
+                                          const double2* tab, int lane) {
   const double2* Q = reinterpret_cast<const double2*>(a.Q);
   const double2* QH = reinterpret_cast<const double2*>(a.QH);
   const BoxRec tb = a.box[t.box];
@@ -411,11 +419,11 @@ __device__ __forceinline__ void task_cplx(const K2Args& a, const Task& t, WarpSm
       const int cnt = min(32, sb.n - j0);
       const bool need_h = skel_rows && (mode == kIFS || (mode == kIFO && j0 < sb.k));
       if (self) {
-        if (need_h) inner_cplx<R, true, true>(sm, cnt, j0, a.kappa, xi, yi, zi, rowi, au, ah);
-        else inner_cplx<R, false, true>(sm, cnt, j0, a.kappa, xi, yi, zi, rowi, au, ah);
+        if (need_h) inner_cplx<R, true, true, TAB>(sm, tab, cnt, j0, a.kappa, xi, yi, zi, rowi, au, ah);
+        else inner_cplx<R, false, true, TAB>(sm, tab, cnt, j0, a.kappa, xi, yi, zi, rowi, au, ah);
       } else {
-        if (need_h) inner_cplx<R, true, false>(sm, cnt, j0, a.kappa, xi, yi, zi, rowi, au, ah);
-        else inner_cplx<R, false, false>(sm, cnt, j0, a.kappa, xi, yi, zi, rowi, au, ah);
+        if (need_h) inner_cplx<R, true, false, TAB>(sm, tab, cnt, j0, a.kappa, xi, yi, zi, rowi, au, ah);
+        else inner_cplx<R, false, false, TAB>(sm, tab, cnt, j0, a.kappa, xi, yi, zi, rowi, au, ah);
       }
       __syncwarp();
     }
@@ -435,8 +443,13 @@ __device__ __forceinline__ void task_cplx(const K2Args& a, const Task& t, WarpSm
   }
 }
 
+template <bool TAB>
 __global__ void __launch_bounds__(kThreads, 4) k2_translate_cplx(K2Args a) {
   __shared__ WarpSmemCplx smem[kWarps];
+  __shared__ double2 tab[kSinCosTab];
+  if (TAB)
+    for (int i = threadIdx.x; i < kSinCosTab; i += blockDim.x) tab[i] = a.tab[i];
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   WarpSmemCplx& sm = smem[threadIdx.x >> 5];
   for (;;) {
@@ -446,10 +459,10 @@ __global__ void __launch_bounds__(kThreads, 4) k2_translate_cplx(K2Args a) {
     if (t >= a.n_tasks) return;
     const Task task = a.tasks[t];
     switch ((task.nrows + 31) >> 5) {
-      case 1: task_cplx<1>(a, task, sm, lane); break;
-      case 2: task_cplx<2>(a, task, sm, lane); break;
-      case 3: task_cplx<3>(a, task, sm, lane); break;
-      default: task_cplx<4>(a, task, sm, lane); break;
+      case 1: task_cplx<1, TAB>(a, task, sm, tab, lane); break;
+      case 2: task_cplx<2, TAB>(a, task, sm, tab, lane); break;
+      case 3: task_cplx<3, TAB>(a, task, sm, tab, lane); break;
+      default: task_cplx<4, TAB>(a, task, sm, tab, lane); break;
     }
   }
 }
@@ -489,7 +502,7 @@ int configure_translate(DevPlan& p, int device) {
     return -1;
   cudaError_t e;
   if (p.kernel == SFMM_HELMHOLTZ3D)
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_translate_cplx, kThreads, 0);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_translate_cplx<true>, kThreads, 0);
   else if (p.kernel == SFMM_LAPLACE3D)
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_translate_real<GenLaplace3d>,
                                                       kThreads, 0);
@@ -534,11 +547,15 @@ void launch_translate(const DevPlan& p, DevState& s, cudaStream_t st, TranslateP
     a.counter = counter;
     a.err = p.err_flag;
     a.kappa = p.kappa;
+    a.tab = p.sc_tab;
     a.St = p.stage;
     cudaMemsetAsync(counter, 0, sizeof(int), st);
     const int grid = (int)std::min<int64_t>(p.k2_grid, (t1 - t0 + kWarps - 1) / kWarps);
     if (p.kernel == SFMM_HELMHOLTZ3D)
-      k2_translate_cplx<<<grid, kThreads, 0, st>>>(a);
+      if (p.sc_tab_ok)
+        k2_translate_cplx<true><<<grid, kThreads, 0, st>>>(a);
+      else
+        k2_translate_cplx<false><<<grid, kThreads, 0, st>>>(a);
     else if (p.kernel == SFMM_LAPLACE3D)
       k2_translate_real<GenLaplace3d><<<grid, kThreads, 0, st>>>(a);
     else

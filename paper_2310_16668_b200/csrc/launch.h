@@ -36,6 +36,8 @@ struct DevPlan {
   int32_t* leaf_orig;
   double* T;
   int64_t* T_off;
+  double2* sc_tab;  // (cos, sin)(k pi/128), 256 entries (fastmath.cuh)
+  bool sc_tab_ok;   // kappa * (point-set diameter) within the table's reduction range
   LevelItem *up_items, *down_items;
   double* orig_pts;
   double* stage;    // kSYM column-sum staging (stage_size doubles)
@@ -123,7 +125,8 @@ void launch_downward_m(const DevPlan& p, const HostPlan& hp, int level, DevState
                        cudaStream_t st);
 void launch_scatter_m(const DevPlan& p, const DevState& s, double* u, int nc, cudaStream_t st);
 
-// Test hook: out[4i..4i+3] = sincos_fast(x_i) (s, c) and the CUDA library's (s, c).
+// Test hook: out[6i..6i+5] = sincos_fast(x_i) (s, c), the table version (s, c)
+// and the CUDA library's (s, c).
 int test_sincos(const double* x_host, int64_t n, double* out_host);
 
 // DFMA throughput probe (TFLOP/s), see kernels_probe.cu.

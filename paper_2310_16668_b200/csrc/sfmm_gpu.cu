@@ -18,6 +18,7 @@
 #include <string>
 #include <vector>
 
+#include "fastmath.cuh"
 #include "launch.h"
 #include "plan_build.h"
 #include "sfmm_gpu.h"
@@ -324,6 +325,22 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
         ck(cudaStreamSynchronize(p->stream), "build slots");
       }
       dp.T_off = p->upload(hp.T_off);
+      {
+        std::vector<double2> tab(kSinCosTab);
+        fill_sincos_table(tab.data());
+        dp.sc_tab = p->upload(tab);
+        // every kernel argument kappa * r is at most kappa * (bounding-box diagonal)
+        double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+        for (int k = 0; k < hp.dim; ++k) lo[k] = hi[k] = desc->pts[k];
+        for (int64_t i = 0; i < hp.n_points; ++i)
+          for (int k = 0; k < hp.dim; ++k) {
+            lo[k] = std::min(lo[k], desc->pts[i * hp.dim + k]);
+            hi[k] = std::max(hi[k], desc->pts[i * hp.dim + k]);
+          }
+        double d2 = 0;
+        for (int k = 0; k < hp.dim; ++k) d2 += (hi[k] - lo[k]) * (hi[k] - lo[k]);
+        dp.sc_tab_ok = std::fabs(hp.kappa) * std::sqrt(d2) <= kSinCosTabMaxArg;
+      }
       // interpolation operators of the owned boxes, copied run by run
       dp.T = p->alloc<double>((size_t)hp.T_off[hp.n_boxes] * sw);
       const double* T_src = T_dev ? T_dev : desc->T;

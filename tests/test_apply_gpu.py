@@ -145,6 +145,7 @@ def test_nan_charges_stay_nan_without_duplicate_error():
     (3, "sphere", 20, 10.0),  # 16 + a zero-padded pass of 4
     (1, "cube", 5, 1.0),
     (0, "annulus", 16, 1.0),
+    (3, "cube", 3, 2.0e4),    # kappa * diameter beyond the sincos table: sincos_fast path
 ])
 def test_multi_rhs_matches_oracle_column_loop(kernel, dist, nrhs, kappa):
     n = 6000

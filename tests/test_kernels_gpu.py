@@ -16,12 +16,16 @@ def test_fast_sincos_within_two_ulp():
     x = np.concatenate([rng.uniform(0, 20, 200000), rng.uniform(-1e3, 1e3, 200000),
                         rng.uniform(-1e6, 1e6, 50000),
                         np.arange(-64, 65) * (np.pi / 4)]).astype(np.float64)
-    out = np.zeros(4 * x.size)
+    out = np.zeros(6 * x.size)
     assert _abi.gpu_lib().sfmm_gpu_test_sincos(x.ctypes.data, x.size, out.ctypes.data) == 0
-    s, c, s_ref, c_ref = out[0::4], out[1::4], out[2::4], out[3::4]
+    s_ref, c_ref = out[4::6], out[5::6]
     assert np.allclose(s_ref, np.sin(x), atol=1e-15, rtol=0)
-    # absolute error <= 2 ulp of 1 (results are bounded by 1 in magnitude)
-    assert np.max(np.abs(s - s_ref)) <= 2 * np.spacing(1.0)
-    assert np.max(np.abs(c - c_ref)) <= 2 * np.spacing(1.0)
-    assert np.max(np.abs(s - np.sin(x))) <= 4 * np.spacing(1.0)
-    assert np.max(np.abs(c - np.cos(x))) <= 4 * np.spacing(1.0)
+    # branch-free (out[0:2]) and table-driven (out[2:4]) versions: absolute
+    # error <= 2 ulp of 1 (results are bounded by 1 in magnitude); the table
+    # version is used only for |x| <= 2e4 (kSinCosTabMaxArg)
+    tab_ok = np.abs(x) <= 2e4
+    for s, c, m in ((out[0::6], out[1::6], np.ones_like(tab_ok)), (out[2::6], out[3::6], tab_ok)):
+        assert np.max(np.abs(s - s_ref)[m]) <= 2 * np.spacing(1.0)
+        assert np.max(np.abs(c - c_ref)[m]) <= 2 * np.spacing(1.0)
+        assert np.max(np.abs(s - np.sin(x))[m]) <= 4 * np.spacing(1.0)
+        assert np.max(np.abs(c - np.cos(x))[m]) <= 4 * np.spacing(1.0)
