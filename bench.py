@@ -247,7 +247,11 @@ def run_sharded(args, ws, rank, local):
     n = int(args.n)
     kern = KERNELS[args.kernel]
     cplx = kern == 3
-    path = f"/dev/shm/sfmm_bench_{os.environ.get('MASTER_PORT', '0')}"
+    # node-local shared memory for the descriptor (~1.3 kB per point incl. T), else /tmp
+    import shutil
+    base = "/dev/shm" if (os.path.isdir("/dev/shm") and
+                          shutil.disk_usage("/dev/shm").free > 2000 * n) else "/tmp"
+    path = f"{base}/sfmm_bench_{os.environ.get('MASTER_PORT', '0')}"
     t0 = time.perf_counter()
     pts = host.generate_points(args.dist, n, 1)
     q = (host.generate_charges_complex(n, 1 ^ CHARGE_STREAM) if cplx
