@@ -44,24 +44,33 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// K1, real: qhat_i = q_S[i] + sum_j T[i,j] q_R[j] for kUpRows rows of one box.
-// Each warp streams 4 rows of T at once (4 independent coalesced loads per
-// lane per step) so enough bytes are in flight to run at HBM speed.
+// K1, real: qhat_i = q_S[i] + sum_j T[i,j] q_R[j] for up to kUpRows1 rows of
+// one box.  Each warp streams 4 rows of T at once (4 independent coalesced
+// loads per lane per step, two steps unrolled); q_R is read through the
+// read-only cache (shared by all rows of the box) so its loads overlap the T
+// stream instead of being staged behind a barrier.
 constexpr int kUpRowsPerWarp = 4;
+#ifndef SFMM_K1_SMEM
+#define SFMM_K1_SMEM 1
+#endif
 __global__ void __launch_bounds__(kUpThreads) k1_upward_real(
     const LevelItem* __restrict__ items, const BoxRec* __restrict__ box,
     const int64_t* __restrict__ T_off, const double* __restrict__ T, double* __restrict__ Q,
     double* __restrict__ QH, const int64_t* __restrict__ up_dst) {
-  extern __shared__ double smq[];
   const LevelItem it = items[blockIdx.x];
   const BoxRec br = box[it.box];
   const int k = br.k, r = br.n - br.k;
-  const double* qR = Q + br.slot + k;
-  for (int j = threadIdx.x; j < r; j += blockDim.x) smq[j] = qR[j];
+#if SFMM_K1_SMEM
+  extern __shared__ double smq[];
+  for (int j = threadIdx.x; j < r; j += blockDim.x) smq[j] = Q[br.slot + k + j];
   __syncthreads();
+  const double* qR = smq;
+#else
+  const double* qR = Q + br.slot + k;
+#endif
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const double* Tb = T + T_off[it.box];
-  const int i1 = min(it.first + kUpRows, k);
+  const int i1 = min(it.first + kUpRows1, k);
   for (int i0 = it.first + w * kUpRowsPerWarp; i0 < i1; i0 += (kUpThreads / 32) * kUpRowsPerWarp) {
     double acc[kUpRowsPerWarp];
     const double* Ti[kUpRowsPerWarp];
@@ -72,7 +81,11 @@ __global__ void __launch_bounds__(kUpThreads) k1_upward_real(
     }
 #pragma unroll 2
     for (int j = lane; j < r; j += 32) {
-      const double qj = smq[j];
+#if SFMM_K1_SMEM
+      const double qj = qR[j];
+#else
+      const double qj = __ldg(qR + j);
+#endif
 #pragma unroll
       for (int m = 0; m < kUpRowsPerWarp; ++m) acc[m] = fma(__ldg(Ti[m] + j), qj, acc[m]);
     }
@@ -94,21 +107,18 @@ __global__ void __launch_bounds__(kUpThreads) k1_upward_cplx(
     const LevelItem* __restrict__ items, const BoxRec* __restrict__ box,
     const int64_t* __restrict__ T_off, const double2* __restrict__ T, double2* __restrict__ Q,
     double2* __restrict__ QH, const int64_t* __restrict__ up_dst) {
-  extern __shared__ double2 smq2[];
   const LevelItem it = items[blockIdx.x];
   const BoxRec br = box[it.box];
   const int k = br.k, r = br.n - br.k;
   const double2* qR = Q + br.slot + k;
-  for (int j = threadIdx.x; j < r; j += blockDim.x) smq2[j] = qR[j];
-  __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const double2* Tb = T + T_off[it.box];
-  const int i1 = min(it.first + kUpRows, k);
+  const int i1 = min(it.first + kUpRows1, k);
   for (int i = it.first + w; i < i1; i += kUpThreads / 32) {
     const double2* Ti = Tb + (int64_t)i * r;
     double ar = 0.0, ai = 0.0;
     for (int j = lane; j < r; j += 32) {
-      const double2 t = Ti[j], x = smq2[j];
+      const double2 t = __ldg(Ti + j), x = __ldg(qR + j);
       ar = fma(t.x, x.x, fma(-t.y, x.y, ar));
       ai = fma(t.x, x.y, fma(t.y, x.x, ai));
     }
@@ -121,6 +131,39 @@ __global__ void __launch_bounds__(kUpThreads) k1_upward_cplx(
       Q[up_dst[br.skel + i]] = v;
     }
   }
+}
+
+// K1 / K3 for uncompressed boxes (k = n, r = 0: no interpolation block), one
+// warp per box: qhat = q (K1) and U_S += UH + U[parent slice] (K3).
+__device__ __forceinline__ double add_s(double a, double b) { return a + b; }
+__device__ __forceinline__ double2 add_s(double2 a, double2 b) {
+  return make_double2(a.x + b.x, a.y + b.y);
+}
+
+template <class S>
+__global__ void __launch_bounds__(256) k1_copy(const int32_t* __restrict__ boxes, int64_t nbox,
+                                               const BoxRec* __restrict__ box, S* __restrict__ Q,
+                                               S* __restrict__ QH, const int64_t* __restrict__ up_dst) {
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (w >= nbox) return;
+  const BoxRec br = box[boxes[w]];
+  for (int i = threadIdx.x & 31; i < br.k; i += 32) {
+    const S v = Q[br.slot + i];
+    QH[br.skel + i] = v;
+    Q[up_dst[br.skel + i]] = v;
+  }
+}
+
+template <class S>
+__global__ void __launch_bounds__(256) k3_copy(const int32_t* __restrict__ boxes, int64_t nbox,
+                                               const BoxRec* __restrict__ box, S* __restrict__ U,
+                                               const S* __restrict__ UH,
+                                               const int64_t* __restrict__ up_dst) {
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (w >= nbox) return;
+  const BoxRec br = box[boxes[w]];
+  for (int i = threadIdx.x & 31; i < br.k; i += 32)
+    U[br.slot + i] = add_s(U[br.slot + i], add_s(UH[br.skel + i], U[up_dst[br.skel + i]]));
 }
 
 // K3, real: uhat = UH + U[parent slice]; U_S += uhat; U_R += T^T uhat.
@@ -355,19 +398,39 @@ void launch_scatter(const DevPlan& p, const DevState& s, double* u, cudaStream_t
 
 void launch_upward(const DevPlan& p, const HostPlan& hp, int level, DevState& s,
                    cudaStream_t st) {
-  const int64_t i0 = hp.up_lvl[level], i1 = hp.up_lvl[level + 1];
+  const int64_t c0 = hp.copy_lvl[level], c1 = hp.copy_lvl[level + 1];
+  if (c1 > c0) {
+    const unsigned g = (unsigned)((c1 - c0 + 7) / 8);
+    if (p.cplx)
+      k1_copy<double2><<<g, 256, 0, st>>>(p.copy_boxes + c0, c1 - c0, p.box,
+                                          reinterpret_cast<double2*>(s.Q),
+                                          reinterpret_cast<double2*>(s.QH), p.up_dst);
+    else
+      k1_copy<double><<<g, 256, 0, st>>>(p.copy_boxes + c0, c1 - c0, p.box, s.Q, s.QH, p.up_dst);
+  }
+  const int64_t i0 = hp.up1_lvl[level], i1 = hp.up1_lvl[level + 1];
   if (i1 <= i0) return;
   if (p.cplx)
-    k1_upward_cplx<<<(unsigned)(i1 - i0), kUpThreads, p.up_smem, st>>>(
-        p.up_items + i0, p.box, p.T_off, reinterpret_cast<const double2*>(p.T),
+    k1_upward_cplx<<<(unsigned)(i1 - i0), kUpThreads, 0, st>>>(
+        p.up1_items + i0, p.box, p.T_off, reinterpret_cast<const double2*>(p.T),
         reinterpret_cast<double2*>(s.Q), reinterpret_cast<double2*>(s.QH), p.up_dst);
   else
-    k1_upward_real<<<(unsigned)(i1 - i0), kUpThreads, p.up_smem, st>>>(
-        p.up_items + i0, p.box, p.T_off, p.T, s.Q, s.QH, p.up_dst);
+    k1_upward_real<<<(unsigned)(i1 - i0), kUpThreads, SFMM_K1_SMEM ? p.up_smem : 0, st>>>(
+        p.up1_items + i0, p.box, p.T_off, p.T, s.Q, s.QH, p.up_dst);
 }
 
 void launch_downward(const DevPlan& p, const HostPlan& hp, int level, DevState& s,
                      cudaStream_t st) {
+  const int64_t c0 = hp.copy_lvl[level], c1 = hp.copy_lvl[level + 1];
+  if (c1 > c0) {
+    const unsigned g = (unsigned)((c1 - c0 + 7) / 8);
+    if (p.cplx)
+      k3_copy<double2><<<g, 256, 0, st>>>(p.copy_boxes + c0, c1 - c0, p.box,
+                                          reinterpret_cast<double2*>(s.U),
+                                          reinterpret_cast<const double2*>(s.UH), p.up_dst);
+    else
+      k3_copy<double><<<g, 256, 0, st>>>(p.copy_boxes + c0, c1 - c0, p.box, s.U, s.UH, p.up_dst);
+  }
   const int64_t i0 = hp.down_lvl[level], i1 = hp.down_lvl[level + 1];
   if (i1 <= i0) return;
   if (p.cplx)
@@ -443,13 +506,11 @@ void launch_unpack(const DevPlan& p, DevState& s, const double* buf, cudaStream_
 int configure_tree_kernels(DevPlan& p, size_t max_r, size_t max_k) {
   const size_t sw = p.cplx ? 16 : 8;
   p.up_smem = std::max<size_t>(max_r * sw, 16);
+  if (SFMM_K1_SMEM && !p.cplx && p.up_smem > 48 * 1024 &&
+      cudaFuncSetAttribute(k1_upward_real, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)p.up_smem) != cudaSuccess)
+    return -1;
   p.down_smem = std::max<size_t>(max_k * sw, 16);
-  if (p.up_smem > 48 * 1024) {
-    if (cudaFuncSetAttribute(p.cplx ? (const void*)k1_upward_cplx : (const void*)k1_upward_real,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)p.up_smem) != cudaSuccess)
-      return -1;
-  }
   if (p.down_smem > 48 * 1024) {
     if (cudaFuncSetAttribute(
             p.cplx ? (const void*)k3_downward_cplx : (const void*)k3_downward_real,

@@ -38,7 +38,8 @@ struct DevPlan {
   int64_t* T_off;
   double2* sc_tab;  // (cos, sin)(k pi/128), 256 entries (fastmath.cuh)
   bool sc_tab_ok;   // kappa * (point-set diameter) within the table's reduction range
-  LevelItem *up_items, *down_items;
+  LevelItem *up_items, *down_items, *up1_items;  // up1: K1 (single rhs), up: K1m
+  int32_t* copy_boxes;                            // r = 0 boxes (plan_build.h)
   double* orig_pts;
   double* stage;    // kSYM column-sum staging (stage_size doubles)
   int32_t* recv_box;

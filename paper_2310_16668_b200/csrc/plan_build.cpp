@@ -529,10 +529,14 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
     }
     hp.T_off[nb] = tcur;
     hp.up_lvl.assign(d.depth + 2, 0);
+    hp.up1_lvl.assign(d.depth + 2, 0);
+    hp.copy_lvl.assign(d.depth + 2, 0);
     hp.down_lvl.assign(d.depth + 2, 0);
     hp.down_m_lvl.assign(d.depth + 2, 0);
     for (int l = 0; l <= d.depth; ++l) {
       hp.up_lvl[l] = (int64_t)hp.up_items.size();
+      hp.up1_lvl[l] = (int64_t)hp.up1_items.size();
+      hp.copy_lvl[l] = (int64_t)hp.copy_boxes.size();
       hp.down_lvl[l] = (int64_t)hp.down_items.size();
       hp.down_m_lvl[l] = (int64_t)hp.down_m_items.size();
       if (l >= 2) {
@@ -541,14 +545,21 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
           const int32_t k = hp.box[b].k, r = hp.box[b].n - hp.box[b].k;
           if (k == 0) continue;
           for (int32_t i = 0; i < k; i += kUpRows) hp.up_items.push_back({b, i});
-          // one item even when r == 0: it also folds uhat into the skeleton slots
-          for (int32_t j = 0; j < std::max(r, 1); j += kDownCols) hp.down_items.push_back({b, j});
+          // one K3m item even when r == 0: it also folds uhat into the skeleton slots
           for (int32_t j = 0; j < std::max(r, 1); j += kDownColsM) hp.down_m_items.push_back({b, j});
+          if (r == 0) {  // uncompressed: copies only (warp per box, k1_copy / k3_copy)
+            hp.copy_boxes.push_back(b);
+            continue;
+          }
+          for (int32_t i = 0; i < k; i += kUpRows1) hp.up1_items.push_back({b, i});
+          for (int32_t j = 0; j < r; j += kDownCols) hp.down_items.push_back({b, j});
         }
       }
     }
     ptime("T runs, level items");
     hp.up_lvl[d.depth + 1] = (int64_t)hp.up_items.size();
+    hp.up1_lvl[d.depth + 1] = (int64_t)hp.up1_items.size();
+    hp.copy_lvl[d.depth + 1] = (int64_t)hp.copy_boxes.size();
     hp.down_lvl[d.depth + 1] = (int64_t)hp.down_items.size();
     hp.down_m_lvl[d.depth + 1] = (int64_t)hp.down_m_items.size();
     return SFMM_OK;

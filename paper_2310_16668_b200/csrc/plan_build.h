@@ -23,7 +23,11 @@ namespace sfmm_gpu {
 
 constexpr int kRowsPerLane = 4;                 // max rows per lane in K2
 constexpr int kTileRows = 32 * kRowsPerLane;    // rows per K2 task
-constexpr int kUpRows = 32;                     // K1 rows (skeleton entries) per CTA
+constexpr int kUpRows = 32;                     // K1m rows (skeleton entries) per CTA
+#ifndef SFMM_K1_ROWS
+#define SFMM_K1_ROWS 64
+#endif
+constexpr int kUpRows1 = SFMM_K1_ROWS;          // K1 (single rhs) rows per CTA
 constexpr int kDownCols = 256;                  // K3 columns (redundant slots) per CTA
 constexpr int kMultiRows = 64;                  // K2m rows per task (4 warps x two 8-row DMMA tiles)
 constexpr int kDownColsM = 16;                  // K3m columns per CTA (x 16 rhs threads)
@@ -87,8 +91,12 @@ struct HostPlan {
   };
   std::vector<Run> T_runs;
   // interpolation work lists, concatenated per level; *_lvl has depth+2 entries
-  std::vector<LevelItem> up_items, down_items;
-  std::vector<int64_t> up_lvl, down_lvl;
+  std::vector<LevelItem> up_items, down_items, up1_items;
+  std::vector<int64_t> up_lvl, down_lvl, up1_lvl;
+  // owned boxes with k > 0 and no redundant slots (r = 0), per level: the
+  // single-rhs passes only copy qhat / fold uhat for them (k1_copy, k3_copy)
+  std::vector<int32_t> copy_boxes;
+  std::vector<int64_t> copy_lvl;
   // depth < 2: coordinates in original order for the dense fallback
   std::vector<double> orig_pts;
   // stats

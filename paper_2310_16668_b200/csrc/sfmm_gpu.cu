@@ -222,8 +222,9 @@ struct sfmm_gpu_plan {
     if (hp.depth < 2) return 1;
     int n = 3;  // gather, translate, scatter
     for (int l = 2; l <= hp.depth; ++l) {
-      n += hp.up_lvl[l + 1] > hp.up_lvl[l] ? 1 : 0;
+      n += hp.up1_lvl[l + 1] > hp.up1_lvl[l] ? 1 : 0;
       n += hp.down_lvl[l + 1] > hp.down_lvl[l] ? 1 : 0;
+      n += hp.copy_lvl[l + 1] > hp.copy_lvl[l] ? 2 : 0;  // k1_copy + k3_copy
     }
     if (dp.n_tasks == 0) --n;
     if (dp.n_recv > 0) ++n;  // k2b_reduce
@@ -351,6 +352,8 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
            "upload T");
       ck(cudaStreamSynchronize(p->stream), "upload T");
       dp.up_items = p->upload(hp.up_items);
+      dp.up1_items = p->upload(hp.up1_items);
+      dp.copy_boxes = p->upload(hp.copy_boxes);
       dp.down_items = p->upload(hp.down_items);
       dp.stage = p->alloc<double>((size_t)std::max<int64_t>(hp.stage_size, 1));
       dp.n_recv = (int64_t)hp.recv_box.size();
