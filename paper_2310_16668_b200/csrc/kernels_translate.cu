@@ -479,15 +479,19 @@ __global__ void __launch_bounds__(256) k2b_reduce(const BoxRec* __restrict__ box
                                                   double* __restrict__ UH, double scale) {
   const BoxRec br = box[recv_box[blockIdx.x]];
   const int64_t e0 = recv_off[blockIdx.x], e1 = recv_off[blockIdx.x + 1];
+  // the sums run in the fixed e order (deterministic); unrolling lets the
+  // independent loads of several staged vectors be in flight at once
   for (int i = threadIdx.x; i < br.n; i += blockDim.x) {
     double s = 0.0;
-    for (int64_t e = e0; e < e1; ++e) s += St[recv_u[e] + i];
+#pragma unroll 8
+    for (int64_t e = e0; e < e1; ++e) s += __ldg(St + recv_u[e] + i);
     U[br.slot + i] += scale * s;
     if (i < br.k) {
       double h = 0.0;
+#pragma unroll 8
       for (int64_t e = e0; e < e1; ++e) {
         const int64_t o = recv_h[e];
-        if (o >= 0) h += St[o + i];
+        h += o >= 0 ? __ldg(St + o + i) : 0.0;
       }
       UH[br.skel + i] -= scale * h;
     }
