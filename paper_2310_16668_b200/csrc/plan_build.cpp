@@ -490,7 +490,17 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
         }
       }
       hp.stage_size = cursor;
-      auto by_cost = [](const auto& a, const auto& b) { return a.first > b.first; };
+#ifndef SFMM_TASK_GROUP_R
+#define SFMM_TASK_GROUP_R 1
+#endif
+      // Longest first (LPT), grouped by rows-per-lane R (the K2 code path) so
+      // the warps resident together mostly run one instantiation: mixing all
+      // four R variants starves instruction fetch on adaptive trees.
+      auto by_cost = [](const auto& a, const auto& b) {
+        const int ra = (a.second.nrows + 31) >> 5, rb = (b.second.nrows + 31) >> 5;
+        if (SFMM_TASK_GROUP_R && ra != rb) return ra > rb;
+        return a.first > b.first;
+      };
       std::stable_sort(tv_int.begin(), tv_int.end(), by_cost);
       std::stable_sort(tv_bnd.begin(), tv_bnd.end(), by_cost);
       hp.tasks.reserve(tv_int.size() + tv_bnd.size());
