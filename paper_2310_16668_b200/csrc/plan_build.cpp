@@ -2,6 +2,7 @@
 #include "plan_build.h"
 
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <chrono>
 #include <cstdio>
@@ -460,17 +461,50 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
       std::vector<std::vector<std::pair<int64_t, int64_t>>> inbox(hp.symmetric ? nb : 0);
       std::vector<std::pair<double, Task>> tv_int, tv_bnd;
       int64_t cursor = 0;
+      // cost model: lane-rows x (sources + 8)
+      std::vector<double> src_of(nb, 0.0);
       for (int32_t b = 0; b < nb; ++b) {
         const EntryRange& er = hp.ent_range[b];
-        if (er.count == 0 || hp.box[b].n == 0) continue;
-        double src = 0;
         for (int64_t e = er.begin; e < er.begin + er.count; ++e) {
           const int32_t code = hp.entries[e];
           const double w = (code & kModeMask) == kSYM ? 1.15 : 1.0;  // extra column accumulate
-          src += w * hp.box[code >> kModeBits].n;
+          src_of[b] += w * hp.box[code >> kModeBits].n;
         }
-        for (int32_t r0 = 0; r0 < hp.box[b].n; r0 += kTileRows) {
-          Task t{b, r0, std::min(kTileRows, hp.box[b].n - r0), 0, cursor};
+      }
+      // Row-tile height: 128 (4 rows per lane) unless the tree is so small that
+      // its largest tasks would set the persistent kernel's makespan (config-1
+      // sized plans); then 64 or 32 rows.  Smaller tiles cost a little more
+      // per pair (each staged source chunk serves fewer rows).
+      int tile = kTileRows;
+      {
+        const double warps = 148.0 * 16.0;  // resident K2 warps on a B200
+        double best = -1.0;
+        for (int T : {kTileRows, kTileRows / 2, kTileRows / 4}) {
+          double total = 0.0, longest = 0.0;
+          for (int32_t b = 0; b < nb; ++b) {
+            if (hp.ent_range[b].count == 0) continue;
+            for (int32_t r0 = 0; r0 < hp.box[b].n; r0 += T) {
+              const int32_t rows = std::min(T, hp.box[b].n - r0);
+              const double c = 32.0 * ((rows + 31) / 32) * (src_of[b] + 8.0);
+              total += c;
+              longest = std::max(longest, c);
+            }
+          }
+          const double over = T == kTileRows ? 1.0 : (T == kTileRows / 2 ? 1.08 : 1.2);
+          const double est = std::max(longest, over * total / warps);
+          if (best < 0.0 || est < 0.9 * best) {  // a smaller tile must clearly win
+            best = est;
+            tile = T;
+          }
+        }
+      }
+      hp.tile_rows = tile;
+      for (int32_t b = 0; b < nb; ++b) {
+        const EntryRange& er = hp.ent_range[b];
+        if (er.count == 0 || hp.box[b].n == 0) continue;
+        const double src = src_of[b];
+        for (int32_t r0 = 0; r0 < hp.box[b].n; r0 += tile) {
+          Task t{b, r0, std::min(tile, hp.box[b].n - r0), 0, cursor};
           const bool skel_rows = r0 < hp.box[b].k;
           for (int64_t e = er.begin; e < er.begin + er.count; ++e) {
             const int32_t code = hp.entries[e];
@@ -493,12 +527,19 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
 #ifndef SFMM_TASK_GROUP_R
 #define SFMM_TASK_GROUP_R 1
 #endif
-      // Longest first (LPT), grouped by rows-per-lane R (the K2 code path) so
-      // the warps resident together mostly run one instantiation: mixing all
-      // four R variants starves instruction fetch on adaptive trees.
-      auto by_cost = [](const auto& a, const auto& b) {
-        const int ra = (a.second.nrows + 31) >> 5, rb = (b.second.nrows + 31) >> 5;
-        if (SFMM_TASK_GROUP_R && ra != rb) return ra > rb;
+      // Longest first (LPT) by cost band (factor 1.25), and by rows-per-lane R
+      // (the K2 code path) within a band, so the warps resident together
+      // mostly run one instantiation -- mixing all four R variants starves
+      // instruction fetch on adaptive trees -- without pushing expensive
+      // partial tiles to the tail.
+      auto band = [](double c) { return (int)std::floor(std::log(c + 1.0) / std::log(1.25)); };
+      auto by_cost = [&](const auto& a, const auto& b) {
+        if (SFMM_TASK_GROUP_R) {
+          const int ba = band(a.first), bb = band(b.first);
+          if (ba != bb) return ba > bb;
+          const int ra = (a.second.nrows + 31) >> 5, rb = (b.second.nrows + 31) >> 5;
+          if (ra != rb) return ra > rb;
+        }
         return a.first > b.first;
       };
       std::stable_sort(tv_int.begin(), tv_int.end(), by_cost);

@@ -60,6 +60,7 @@ struct HostPlan {
   std::vector<EntryRange> ent_range;
   std::vector<int32_t> entries;               // (src box << kModeBits) | mode
   std::vector<Task> tasks;
+  int tile_rows = kTileRows;                  // K2 row-tile height chosen for this plan
   // symmetric colleague blocks: staged column sums and, per receiving box,
   // the staging slots to add (u part, and uhat part or -1) in a fixed order
   bool symmetric = false;
