@@ -21,4 +21,7 @@ ncu --set full --clock-control none --import-source on -k regex:k2_translate -s 
 ncu --set full --clock-control none --import-source on -k regex:k2m -s 1 -c 1 \
     -o $out/k2m_full python bench.py --config c4 --steps 1 --warmup 1 --cpu off \
     > $out/ncu_k2m.log 2>&1
+# the adaptive sphere (config 3a): K2 capture for the instruction-fetch / task-order story
+ncu --set full --clock-control none --import-source on -k regex:k2_translate -s 2 -c 1 \
+    -o $out/k2_c3a python bench.py --config c3a --steps 1 --warmup 2 --cpu off > $out/ncu_k2_c3a.log 2>&1
 ls -la $out
