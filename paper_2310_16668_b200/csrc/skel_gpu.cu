@@ -78,11 +78,6 @@ template <>
 __device__ __forceinline__ Cx zero<Cx>() { return {0.0, 0.0}; }
 __device__ __forceinline__ double shfl_xor(double v, int o) { return __shfl_xor_sync(0xffffffffu, v, o); }
 __device__ __forceinline__ Cx shfl_xor(Cx v, int o) { return {shfl_xor(v.re, o), shfl_xor(v.im, o)}; }
-__device__ __forceinline__ double shfl0(double x) { return __shfl_sync(0xffffffffu, x, 0); }
-__device__ __forceinline__ Cx shfl0(Cx x) {
-  return {__shfl_sync(0xffffffffu, x.re, 0), __shfl_sync(0xffffffffu, x.im, 0)};
-}
-
 template <class S>
 __device__ __forceinline__ S warp_sum(S v) {
 #pragma unroll
@@ -288,53 +283,7 @@ __global__ void __launch_bounds__(kSkThreads) cpqr_kernel(LevelArgs a) {
       vv = s_val;
     }
     if (tid == 0) ckp[k] = beta;
-    constexpr int KC = sizeof(S) == 8 ? 10 : 19;  // column entries per lane held in registers
-    if (vv > 0.0 && M <= 32 * KC) {
-      // register-cached trailing update: each column is read once and written
-      // once per step (the dot product, the update and a norm recompute all
-      // use the cached copy)
-      const double sc = 2.0 / vv;
-      for (int j = k + 1 + warp; j < n; j += nw) {
-        S* cj = A + (int64_t)j * M;
-        S col[KC];
-        S w = zero<S>();
-#pragma unroll
-        for (int t = 0; t < KC; ++t) {
-          const int i = k + lane + 32 * t;
-          col[t] = i < M ? cj[i] : zero<S>();
-          if (i < M) w = add(w, mul(conj_(v[i]), col[t]));
-        }
-        w = scale(warp_sum(w), sc);
-#pragma unroll
-        for (int t = 0; t < KC; ++t) {
-          const int i = k + lane + 32 * t;
-          if (i < M) {
-            col[t] = sub(col[t], mul(v[i], w));
-            cj[i] = col[t];
-          }
-        }
-        double nv = vn1[j];
-        if (nv != 0.0) {
-          const double r = sqrt(absq(shfl0(col[0])));  // row k lives in lane 0, slot 0
-          double t1 = 1.0 - (r / nv) * (r / nv);
-          if (t1 < 0) t1 = 0;
-          const double ratio = nv / vn2[j];
-          if (t1 * ratio * ratio <= 1.5e-8) {  // cancellation: recompute (dqp3 guard)
-            double sq = 0.0;
-#pragma unroll
-            for (int t = 0; t < KC; ++t) {
-              const int i = k + lane + 32 * t;
-              if (i > k && i < M) sq += absq(col[t]);
-            }
-            sq = warp_sum(sq);
-            if (lane == 0) vn1[j] = vn2[j] = sqrt(sq);
-          } else if (lane == 0) {
-            vn1[j] = nv * sqrt(t1);
-          }
-        }
-        __syncwarp();
-      }
-    } else if (vv > 0.0) {
+    if (vv > 0.0) {
       const double sc = 2.0 / vv;
       for (int j = k + 1 + warp; j < n; j += nw) {
         S* cj = A + (int64_t)j * M;
