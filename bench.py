@@ -352,11 +352,20 @@ def run_sharded(args, ws, rank, local):
         dist.all_reduce(uc, op=dist.ReduceOp.SUM)
         u_full = uc.numpy()
     out = None
+    pinfo = plan.info()
+    peak = api.fp64_peak_tflops(dev)
     if rank == 0:
         rng = np.random.default_rng(0xC2B2AE3D27D4EB4F)
         targets = np.sort(rng.choice(n, size=min(args.check_targets, n), replace=False)).astype(np.int32)
         ref_t = api.direct_sum_subset(kern, args.kappa, pts, q, targets, device=dev)
         relerr_direct = api.max_rel_err(u_full[targets], ref_t) if targets.size else None
+        # parity of the sharded result against the single-GPU plan (same operators)
+        with api.GpuPlan(desc, device=dev) as single:
+            u_single = api.fmm_apply(single, q)
+        relerr_single = float(np.linalg.norm(u_full - u_single) / np.linalg.norm(u_single))
+        # whole-job reference-equivalent K2 work over the step time, per GPU
+        w_ref = 20.0 * pinfo.p_dense + 2.0 * pinfo.p_skel
+        achieved = w_ref / (ms_step * 1e-3) / ws / 1e12
         bytes_col = n * (16 if cplx else 8)
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
@@ -369,13 +378,20 @@ def run_sharded(args, ws, rank, local):
                 "parallelism": f"level-1 subtree sharding x{ws}, ghost all-to-all over {args.backend}",
                 "l2": "inputs larger than L2",
             },
-            "roofline": None,
-            "roofline_note": "per-kernel roofline is reported by the 1-GPU line",
+            "roofline": {"bound": "fp64", "kernel": "whole sharded step (K2-equivalent work)",
+                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "work": "20 flop per dense pair + 2 per skeleton pair over all ranks, "
+                                 "divided by the max-over-ranks step time and the GPU count; the "
+                                 "per-kernel roofline is in the 1-GPU line"},
             "e2e": {"value": n / t_e2e / 1e6, "unit": UNIT, "h2d_bytes_per_step": bytes_col * ws,
                     "d2h_bytes_per_step": bytes_col * ws, "ms_per_step": t_e2e * 1e3},
-            "gpu_launches": None,
+            # per rank and apply: the single-RHS sequence, plus ghost pack and unpack and
+            # the second (boundary) translation launch
+            "gpu_launches": (int(pinfo.launches_per_apply) + 3) * args.steps,
             "clocks": clk,
             "relerr_vs_direct": relerr_direct, "n_check": int(targets.size),
+            "relerr_vs_single_gpu": relerr_single,
             "shard": {"ghost_boxes_rank0": plan.n_ghost_boxes,
                       "owned_points_rank0": plan.n_owned_points,
                       "send_mb_rank0": float(plan.send_counts.sum()) * 8 / 1e6},

@@ -82,6 +82,13 @@ class ShardedPlan:
         self.n_ghost_boxes = ghosts.value
         self._bufs = None
 
+    def info(self) -> _abi.PlanInfo:
+        """sfmm_gpu_plan_info_get of this rank's plan (pair counts are global)."""
+        from .api import _raise
+        inf = _abi.PlanInfo()
+        _raise(_abi.gpu_lib().sfmm_gpu_plan_info_get(self._h, C.byref(inf)))
+        return inf
+
     def buffers(self):
         """Device send / receive buffers (torch float64), allocated once."""
         import torch
