@@ -208,14 +208,24 @@ def run_reference(args, ws, rank):
 
 
 def _share_descriptor(hp, path):
-    """Rank 0 writes the flat plan descriptor to node-local shared memory."""
-    from paper_2310_16668_b200._abi import DESC_SCALARS, PlanDescriptor
-    d = PlanDescriptor.from_struct(hp.desc_struct())
+    """Rank 0 writes the flat plan descriptor to node-local shared memory,
+    straight from the host plan's arrays (no intermediate copy: at N=1e8 T alone
+    is ~100 GB)."""
+    import ctypes as C
+    from paper_2310_16668_b200._abi import DESC_ARRAYS, DESC_SCALARS, _array_len
+    st = hp.desc_struct()
+    sc = {k: getattr(st, k) for k in DESC_SCALARS}
     os.makedirs(path, exist_ok=True)
-    for name, a in d.arrays.items():
-        np.save(os.path.join(path, name + ".npy"), a)
+    views = {}
+    for name, dt in [(n, d) for n, d in DESC_ARRAYS if n.endswith("_off")] + \
+                    [(n, d) for n, d in DESC_ARRAYS if not n.endswith("_off")]:
+        cnt = _array_len(name, sc, lambda k: views[k])
+        ptr = getattr(st, name)
+        views[name] = (np.ctypeslib.as_array(C.cast(ptr, C.POINTER(np.ctypeslib.as_ctypes_type(dt))),
+                                             shape=(cnt,)) if cnt and ptr else np.zeros(0, dtype=dt))
+        np.save(os.path.join(path, name + ".npy"), views[name])
     with open(os.path.join(path, "scalars.json"), "w") as f:
-        json.dump({k: d.scalars[k] for k in DESC_SCALARS}, f)
+        json.dump(sc, f)
 
 
 def _load_descriptor(path):
