@@ -496,6 +496,7 @@ template <class S>
 void run_skeletons(const sfmm_tree_desc& t, int kernel, double kappa, double tol, double radius,
                    int edge2d, int face3d, sfmm_skel_result& R) {
   constexpr int SW = sizeof(S) / 8;
+  const auto t_run0 = std::chrono::steady_clock::now();
   const int nb = t.n_boxes, dim = t.dim, depth = t.depth;
   const std::vector<double> unit = unit_proxy(dim, edge2d, face3d);
   const int np = (int)unit.size() / dim;
@@ -541,6 +542,10 @@ void run_skeletons(const sfmm_tree_desc& t, int kernel, double kappa, double tol
   const bool verbose = std::getenv("SFMM_SKEL_VERBOSE") != nullptr;
   auto now = [] { return std::chrono::steady_clock::now(); };
   auto secs = [](auto a, auto b) { return std::chrono::duration<double>(b - a).count(); };
+  if (verbose) {
+    ck(cudaDeviceSynchronize(), "sync");
+    std::fprintf(stderr, "[skel] setup: %.3f s\n", secs(t_run0, now()));
+  }
   for (int l = depth; l >= 0; --l) {
     const auto t_lv = now();
     Level& lv = L[l];
@@ -757,7 +762,10 @@ void run_skeletons(const sfmm_tree_desc& t, int kernel, double kappa, double tol
   }
   R.poff.resize(nb);
   ck(cudaMemcpy(R.poff.data(), d_poff.p, nb * sizeof(int32_t), cudaMemcpyDeviceToHost), "D2H poff");
-  if (verbose) std::fprintf(stderr, "[skel] assemble: %.3f s\n", secs(t_asm, now()));
+  if (verbose) {
+    std::fprintf(stderr, "[skel] assemble: %.3f s\n", secs(t_asm, now()));
+    std::fprintf(stderr, "[skel] total: %.3f s\n", secs(t_run0, now()));
+  }
 }
 
 }  // namespace
