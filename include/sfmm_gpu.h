@@ -312,6 +312,9 @@ int sfmm_gpu_fp64_peak(int device, double* tflops);
  * of x_i from the branch-free routine, the table-driven routine and the CUDA
  * library. */
 int sfmm_gpu_test_sincos(const double* x, int64_t n, double* out);
+/* Test hook: out[2i], out[2i+1] = log(x_i) from the table-driven routine of the
+ * Laplace-2D kernels and from the CUDA library. */
+int sfmm_gpu_test_log(const double* x, int64_t n, double* out);
 
 /* Dense u_i = sum_{j != i} G(x_i, x_j) q_j over the points in their given
  * order, for the listed targets only (oracle.cpp:51-71), on the device.

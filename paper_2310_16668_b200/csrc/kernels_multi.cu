@@ -62,6 +62,7 @@ struct K2MArgs {
   int* err;
   double kappa;
   const double2* tab;  // (cos, sin)(k pi/128), Helmholtz only
+  const double* ltab;  // log table, Laplace 2D only
 };
 
 __device__ __noinline__ void verify_row_m(const K2MArgs& a, int32_t b, int32_t row, int dim) {
@@ -123,9 +124,12 @@ __global__ void __launch_bounds__(kMThreads, WH ? 2 : 3) k2m_translate(K2MArgs a
   __shared__ ChunkM<CPLX> ch;
   __shared__ int s_task;
   __shared__ double2 tab[CPLX ? kSinCosTab : 1];
+  __shared__ double ltab[KER == SFMM_LAPLACE2D ? 3 * kLogTab : 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (CPLX && TAB)
     for (int i = tid; i < kSinCosTab; i += blockDim.x) tab[i] = a.tab[i];
+  if (KER == SFMM_LAPLACE2D)
+    for (int i = tid; i < 3 * kLogTab; i += blockDim.x) ltab[i] = a.ltab[i];
   const int rq = lane >> 2, kq = lane & 3;  // A-fragment row / k index of this lane
   for (;;) {
     __syncthreads();
@@ -283,7 +287,7 @@ __global__ void __launch_bounds__(kMThreads, WH ? 2 : 3) k2m_translate(K2MArgs a
               r2 = fma(dz, dz, r2);
             }
             if (KER == SFMM_LAPLACE2D) {
-              gr[mt] = log(r2);
+              gr[mt] = log_tab(ltab, r2);
               gi[mt] = 0.0;
             } else {
               const double yv = rsqrt_fp64m(r2);
@@ -634,6 +638,7 @@ void launch_translate_m(const DevPlan& p, DevState& s, cudaStream_t st) {
   a.err = p.err_flag;
   a.kappa = p.kappa;
   a.tab = p.sc_tab;
+  a.ltab = p.log_tab;
   cudaMemsetAsync(p.counter + 2, 0, 2 * sizeof(int), st);
   // tasks [0, n_tasks_mh) own skeleton rows, the rest do not
   for (int part = 0; part < 2; ++part) {

@@ -29,6 +29,39 @@ __global__ void sincos_check(const double* x, int64_t n, const double2* tab, dou
 
 }  // namespace
 
+namespace {
+__global__ void log_check(const double* x, int64_t n, const double* tab, double* out) {
+  __shared__ double lt[3 * kLogTab];
+  for (int i = threadIdx.x; i < 3 * kLogTab; i += blockDim.x) lt[i] = tab[i];
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    out[2 * i] = log_tab(lt, x[i]);
+    out[2 * i + 1] = log(x[i]);
+  }
+}
+}  // namespace
+
+int test_log(const double* x_host, int64_t n, double* out_host) {
+  double *dx = nullptr, *dout = nullptr, *dtab = nullptr;
+  double tab[3 * kLogTab];
+  fill_log_table(tab);
+  int rc = -1;
+  if (cudaMalloc(&dx, std::max<int64_t>(n, 1) * sizeof(double)) == cudaSuccess &&
+      cudaMalloc(&dout, std::max<int64_t>(2 * n, 1) * sizeof(double)) == cudaSuccess &&
+      cudaMalloc(&dtab, sizeof(tab)) == cudaSuccess) {
+    cudaMemcpy(dx, x_host, n * sizeof(double), cudaMemcpyHostToDevice);
+    cudaMemcpy(dtab, tab, sizeof(tab), cudaMemcpyHostToDevice);
+    log_check<<<148 * 4, 256>>>(dx, n, dtab, dout);
+    cudaMemcpy(out_host, dout, 2 * n * sizeof(double), cudaMemcpyDeviceToHost);
+    rc = cudaGetLastError() == cudaSuccess ? 0 : -1;
+  }
+  cudaFree(dx);
+  cudaFree(dout);
+  cudaFree(dtab);
+  return rc;
+}
+
 int test_sincos(const double* x_host, int64_t n, double* out_host) {
   double *dx = nullptr, *dout = nullptr;
   double2* dtab = nullptr;

@@ -56,6 +56,7 @@ struct K2Args {
   double kappa;
   double* St;  // staging for kSYM column sums (unscaled)
   const double2* tab;  // (cos, sin)(k pi/128), Helmholtz only
+  const double* ltab;  // log table (fastmath.cuh), Laplace 2D only
 };
 
 // Far-away padding for partial source chunks of kSYM blocks: finite r^2,
@@ -79,11 +80,12 @@ __device__ __forceinline__ double rsqrt_fp64(double r2) {
 struct GenLaplace3d {  // kernel.hpp:46-50  1/(4 pi r)
   static constexpr int kDim = 3;
   static constexpr double kScale = kInv4Pi;
-  __device__ static __forceinline__ double g(double r2) { return rsqrt_fp64(r2); }
+  static constexpr bool kLogTable = false;
+  __device__ static __forceinline__ double g(double r2, const double*) { return rsqrt_fp64(r2); }
   // M independent evaluations, stage by stage, so their dependent chains
   // interleave in the issue stream.
   template <int M>
-  __device__ static __forceinline__ void batch(const double* r2, double* g) {
+  __device__ static __forceinline__ void batch(const double* r2, double* g, const double*) {
     double y[M], e[M];
 #pragma unroll
     for (int m = 0; m < M; ++m) asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y[m]) : "d"(r2[m]));
@@ -96,11 +98,12 @@ struct GenLaplace3d {  // kernel.hpp:46-50  1/(4 pi r)
 struct GenLaplace2d {  // kernel.hpp:40-44  -log(r^2)/(4 pi)
   static constexpr int kDim = 2;
   static constexpr double kScale = -kInv4Pi;
-  __device__ static __forceinline__ double g(double r2) { return log(r2); }
+  static constexpr bool kLogTable = true;  // log_tab with the table in shared memory
+  __device__ static __forceinline__ double g(double r2, const double* lt) { return log_tab(lt, r2); }
   template <int M>
-  __device__ static __forceinline__ void batch(const double* r2, double* g) {
+  __device__ static __forceinline__ void batch(const double* r2, double* g, const double* lt) {
 #pragma unroll
-    for (int m = 0; m < M; ++m) g[m] = log(r2[m]);
+    for (int m = 0; m < M; ++m) g[m] = log_tab(lt, r2[m]);
   }
 };
 
@@ -136,7 +139,7 @@ __device__ __noinline__ void verify_row(const K2Args& a, int32_t b, int32_t row,
 }
 
 template <class G, int R, bool H, bool SELF>
-__device__ __forceinline__ void inner_real(const WarpSmemReal& sm, int cnt, int j0,
+__device__ __forceinline__ void inner_real(const WarpSmemReal& sm, const double* lt, int cnt, int j0,
                                            const double (&xi)[R], const double (&yi)[R],
                                            const double (&zi)[R], const int (&rowi)[R],
                                            double (&au)[R], double (&ah)[R]) {
@@ -154,7 +157,7 @@ __device__ __forceinline__ void inner_real(const WarpSmemReal& sm, int cnt, int 
         const double dz = zi[r] - za.x;
         r2 = fma(dz, dz, r2);
       }
-      double g = G::g(r2);
+      double g = G::g(r2, lt);
       if (SELF) g = (rowi[r] == j0 + jj) ? 0.0 : g;
       au[r] = fma(g, za.y, au[r]);
       if (H) ah[r] = fma(g, wh, ah[r]);
@@ -170,7 +173,8 @@ __device__ __forceinline__ void inner_real(const WarpSmemReal& sm, int cnt, int 
 // the complete sum of column l over the warp's 32R rows.  Fixed order, no
 // butterfly, two column accumulators per lane.
 template <class G, int R, bool H>
-__device__ __forceinline__ void sym_chunk(const WarpSmemReal& sm, int j0, int n_c, int k_c,
+__device__ __forceinline__ void sym_chunk(const WarpSmemReal& sm, const double* lt, int j0, int n_c,
+                                          int k_c,
                                           const double (&xi)[R], const double (&yi)[R],
                                           const double (&zi)[R], const double (&qr)[R],
                                           const double (&qhr)[R], double (&au)[R],
@@ -195,7 +199,7 @@ __device__ __forceinline__ void sym_chunk(const WarpSmemReal& sm, int j0, int n_
         r2[r] = fma(dz, dz, r2[r]);
       }
     }
-    G::template batch<R>(r2, g);
+    G::template batch<R>(r2, g, lt);
     double cs = 0.0, hs = 0.0;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -216,7 +220,7 @@ __device__ __forceinline__ void sym_chunk(const WarpSmemReal& sm, int j0, int n_
 
 template <class G, int R>
 __device__ __forceinline__ void task_real(const K2Args& a, const Task& t, WarpSmemReal& sm,
-                                          int lane) {
+                                          const double* lt, int lane) {
   const BoxRec tb = a.box[t.box];
   double xi[R], yi[R], zi[R], au[R], ah[R], qr[R], qhr[R];
   int rowi[R];
@@ -259,9 +263,9 @@ __device__ __forceinline__ void task_real(const K2Args& a, const Task& t, WarpSm
         }
         __syncwarp();
         if (skel_rows && j0 < sb.k)
-          sym_chunk<G, R, true>(sm, j0, sb.n, sb.k, xi, yi, zi, qr, qhr, au, ah, st_u, st_h, lane);
+          sym_chunk<G, R, true>(sm, lt, j0, sb.n, sb.k, xi, yi, zi, qr, qhr, au, ah, st_u, st_h, lane);
         else
-          sym_chunk<G, R, false>(sm, j0, sb.n, sb.k, xi, yi, zi, qr, qhr, au, ah, st_u, st_h, lane);
+          sym_chunk<G, R, false>(sm, lt, j0, sb.n, sb.k, xi, yi, zi, qr, qhr, au, ah, st_u, st_h, lane);
         __syncwarp();
       }
       stage += sb.n + ((skel_rows && sb.k > 0) ? sb.k : 0);
@@ -286,11 +290,11 @@ __device__ __forceinline__ void task_real(const K2Args& a, const Task& t, WarpSm
       const int cnt = min(32, sb.n - j0);
       const bool need_h = skel_rows && (mode == kIFS || (mode == kIFO && j0 < sb.k));
       if (self) {
-        if (need_h) inner_real<G, R, true, true>(sm, cnt, j0, xi, yi, zi, rowi, au, ah);
-        else inner_real<G, R, false, true>(sm, cnt, j0, xi, yi, zi, rowi, au, ah);
+        if (need_h) inner_real<G, R, true, true>(sm, lt, cnt, j0, xi, yi, zi, rowi, au, ah);
+        else inner_real<G, R, false, true>(sm, lt, cnt, j0, xi, yi, zi, rowi, au, ah);
       } else {
-        if (need_h) inner_real<G, R, true, false>(sm, cnt, j0, xi, yi, zi, rowi, au, ah);
-        else inner_real<G, R, false, false>(sm, cnt, j0, xi, yi, zi, rowi, au, ah);
+        if (need_h) inner_real<G, R, true, false>(sm, lt, cnt, j0, xi, yi, zi, rowi, au, ah);
+        else inner_real<G, R, false, false>(sm, lt, cnt, j0, xi, yi, zi, rowi, au, ah);
       }
       __syncwarp();
     }
@@ -312,6 +316,11 @@ template <class G>
 #endif
 __global__ void __launch_bounds__(kThreads, SFMM_K2_MIN_BLOCKS) k2_translate_real(K2Args a) {
   __shared__ WarpSmemReal smem[kWarps];
+  __shared__ double ltab[G::kLogTable ? 3 * kLogTab : 1];
+  if (G::kLogTable) {
+    for (int i = threadIdx.x; i < 3 * kLogTab; i += blockDim.x) ltab[i] = a.ltab[i];
+    __syncthreads();
+  }
   const int lane = threadIdx.x & 31;
   WarpSmemReal& sm = smem[threadIdx.x >> 5];
   for (;;) {
@@ -321,10 +330,10 @@ __global__ void __launch_bounds__(kThreads, SFMM_K2_MIN_BLOCKS) k2_translate_rea
     if (t >= a.n_tasks) return;
     const Task task = a.tasks[t];
     switch ((task.nrows + 31) >> 5) {
-      case 1: task_real<G, 1>(a, task, sm, lane); break;
-      case 2: task_real<G, 2>(a, task, sm, lane); break;
-      case 3: task_real<G, 3>(a, task, sm, lane); break;
-      default: task_real<G, 4>(a, task, sm, lane); break;
+      case 1: task_real<G, 1>(a, task, sm, ltab, lane); break;
+      case 2: task_real<G, 2>(a, task, sm, ltab, lane); break;
+      case 3: task_real<G, 3>(a, task, sm, ltab, lane); break;
+      default: task_real<G, 4>(a, task, sm, ltab, lane); break;
     }
   }
 }
@@ -552,6 +561,7 @@ void launch_translate(const DevPlan& p, DevState& s, cudaStream_t st, TranslateP
     a.err = p.err_flag;
     a.kappa = p.kappa;
     a.tab = p.sc_tab;
+    a.ltab = p.log_tab;
     a.St = p.stage;
     cudaMemsetAsync(counter, 0, sizeof(int), st);
     const int grid = (int)std::min<int64_t>(p.k2_grid, (t1 - t0 + kWarps - 1) / kWarps);

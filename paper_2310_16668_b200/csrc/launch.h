@@ -38,6 +38,7 @@ struct DevPlan {
   int64_t* T_off;
   double2* sc_tab;  // (cos, sin)(k pi/128), 256 entries (fastmath.cuh)
   bool sc_tab_ok;   // kappa * (point-set diameter) within the table's reduction range
+  double* log_tab;  // 3 x 128 doubles (fastmath.cuh fill_log_table)
   LevelItem *up_items, *down_items, *up1_items;  // up1: K1 (single rhs), up: K1m
   int32_t* copy_boxes;                            // r = 0 boxes (plan_build.h)
   double* orig_pts;
@@ -126,6 +127,8 @@ void launch_downward_m(const DevPlan& p, const HostPlan& hp, int level, DevState
                        cudaStream_t st);
 void launch_scatter_m(const DevPlan& p, const DevState& s, double* u, int nc, cudaStream_t st);
 
+// Test hook: out[2i], out[2i+1] = log_tab(x_i) and the CUDA library's log.
+int test_log(const double* x_host, int64_t n, double* out_host);
 // Test hook: out[6i..6i+5] = sincos_fast(x_i) (s, c), the table version (s, c)
 // and the CUDA library's (s, c).
 int test_sincos(const double* x_host, int64_t n, double* out_host);

@@ -341,6 +341,9 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
         double d2 = 0;
         for (int k = 0; k < hp.dim; ++k) d2 += (hi[k] - lo[k]) * (hi[k] - lo[k]);
         dp.sc_tab_ok = std::fabs(hp.kappa) * std::sqrt(d2) <= kSinCosTabMaxArg;
+        std::vector<double> lt(3 * kLogTab);
+        fill_log_table(lt.data());
+        dp.log_tab = p->upload(lt);
       }
       // interpolation operators of the owned boxes, copied run by run
       dp.T = p->alloc<double>((size_t)hp.T_off[hp.n_boxes] * sw);
@@ -713,6 +716,11 @@ int sfmm_gpu_get_timings(sfmm_gpu_plan* p, float* ms, int max_applies, int* n_ap
   } catch (const CudaFail& f) {
     return set_error(f.code, f.msg);
   }
+}
+
+int sfmm_gpu_test_log(const double* x, int64_t n, double* out) {
+  if (!x || !out || n < 0) return set_error(SFMM_EINVAL, "test_log: bad arguments");
+  return sfmm_gpu::test_log(x, n, out) == 0 ? SFMM_OK : set_error(SFMM_ECUDA, "test_log failed");
 }
 
 int sfmm_gpu_test_sincos(const double* x, int64_t n, double* out) {

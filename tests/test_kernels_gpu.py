@@ -29,3 +29,23 @@ def test_fast_sincos_within_two_ulp():
         assert np.max(np.abs(c - c_ref)[m]) <= 2 * np.spacing(1.0)
         assert np.max(np.abs(s - np.sin(x))[m]) <= 4 * np.spacing(1.0)
         assert np.max(np.abs(c - np.cos(x))[m]) <= 4 * np.spacing(1.0)
+
+
+def test_table_log_within_two_ulp():
+    # log(r^2) of the Laplace-2D kernels: squared distances span many decades,
+    # with extra samples around 1 (no cancellation allowed there) and the
+    # special inputs that must keep the library's behaviour
+    rng = np.random.default_rng(6)
+    x = np.concatenate([10.0 ** rng.uniform(-300, 300, 200000), rng.uniform(0.5, 2.0, 200000),
+                        1.0 + rng.uniform(-1e-6, 1e-6, 50000), 1.0 + np.arange(-50, 51) * 2.0 ** -52,
+                        np.array([1.0, 2.0, 0.5, np.sqrt(2.0), 1e-310, 0.0, np.inf])])
+    out = np.zeros(2 * x.size)
+    assert _abi.gpu_lib().sfmm_gpu_test_log(x.ctypes.data, x.size, out.ctypes.data) == 0
+    got, ref = out[0::2], out[1::2]
+    with np.errstate(divide="ignore"):
+        assert np.allclose(ref, np.log(x), rtol=1e-15, atol=0, equal_nan=True)
+    fin = np.isfinite(ref) & (ref != 0)
+    rel = np.abs(got[fin] - ref[fin]) / np.abs(ref[fin])
+    assert rel.max() <= 2 * np.spacing(1.0), rel.max()
+    assert got[x == 1.0].tolist() == [0.0] * int((x == 1.0).sum())
+    assert np.isneginf(got[x == 0.0]).all() and np.isposinf(got[x == np.inf]).all()
