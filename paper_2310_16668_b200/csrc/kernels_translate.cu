@@ -329,11 +329,18 @@ __global__ void __launch_bounds__(kThreads, SFMM_K2_MIN_BLOCKS) k2_translate_rea
     t = __shfl_sync(kFull, t, 0);
     if (t >= a.n_tasks) return;
     const Task task = a.tasks[t];
+#ifndef SFMM_K2_MAX_R
+#define SFMM_K2_MAX_R 4
+#endif
     switch ((task.nrows + 31) >> 5) {
       case 1: task_real<G, 1>(a, task, sm, ltab, lane); break;
+#if SFMM_K2_MAX_R >= 2
       case 2: task_real<G, 2>(a, task, sm, ltab, lane); break;
+#endif
+#if SFMM_K2_MAX_R >= 3
       case 3: task_real<G, 3>(a, task, sm, ltab, lane); break;
-      default: task_real<G, 4>(a, task, sm, ltab, lane); break;
+#endif
+      default: task_real<G, SFMM_K2_MAX_R>(a, task, sm, ltab, lane); break;
     }
   }
 }

@@ -498,6 +498,9 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
           }
         }
       }
+#ifdef SFMM_TILE_FORCE
+      tile = SFMM_TILE_FORCE;  // dev knob (A/B of the K2 occupancy variants)
+#endif
       hp.tile_rows = tile;
       for (int32_t b = 0; b < nb; ++b) {
         const EntryRange& er = hp.ent_range[b];
