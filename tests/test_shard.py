@@ -142,6 +142,23 @@ def test_virtual_ranks_match_single_plan(n_ranks, case):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("n_ranks", [2, 3, 4])
+def test_virtual_ranks_2d(n_ranks):
+    # 2D: four level-1 quadrants, so at most four ranks
+    import torch
+    n = 40000
+    d, pts = _desc(dist="annulus", n=n, leaf=40, kernel=0, kappa=1.0)
+    q = host.generate_charges(n, 5)
+    u_ref = api.fmm_apply(api.GpuPlan(d), q)
+    plans = [shard.ShardedPlan(d, n_ranks, r) for r in range(n_ranks)]
+    qd = torch.from_numpy(q).cuda()
+    ud = torch.zeros_like(qd)
+    shard.apply_virtual(plans, qd, ud)
+    torch.cuda.synchronize()
+    assert rel_l2(ud.cpu().numpy(), u_ref) <= 1e-12
+
+
+@pytest.mark.gpu
 def test_virtual_ranks_parity_vs_oracle_1e6():
     # config-5 geometry at 1e6: 8 level-1 octants over 8 virtual ranks
     import torch
