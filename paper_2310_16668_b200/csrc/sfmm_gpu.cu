@@ -47,6 +47,7 @@ struct CudaFail {
 
 void ck(cudaError_t e, const char* what) {
   if (e == cudaSuccess) return;
+  (void)cudaGetLastError();  // reported here; do not leak into the next call
   const int code = e == cudaErrorMemoryAllocation ? SFMM_ENOMEM : SFMM_ECUDA;
   throw CudaFail{code, std::string(what) + ": " + cudaGetErrorString(e)};
 }
@@ -259,6 +260,7 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
     }
     p->device = device;
     ck(cudaSetDevice(device), "cudaSetDevice");
+    (void)cudaGetLastError();  // a stale error must not be reported by this call
     ck(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking), "cudaStreamCreate");
     ck(cudaEventCreate(&p->ev_a), "cudaEventCreate");
     ck(cudaEventCreate(&p->ev_b), "cudaEventCreate");
@@ -494,6 +496,7 @@ int sfmm_gpu_apply_begin(sfmm_gpu_plan* p, const void* q_dev, void* send_dev, vo
   std::lock_guard<std::mutex> lock(p->mu);
   try {
     ck(cudaSetDevice(p->device), "cudaSetDevice");
+    (void)cudaGetLastError();  // a stale error must not be reported by this call
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : p->stream;
     const double* q = static_cast<const double*>(q_dev);
     if (p->hp.depth >= 2) {
@@ -519,6 +522,7 @@ int sfmm_gpu_apply_end(sfmm_gpu_plan* p, const void* q_dev, const void* recv_dev
   std::lock_guard<std::mutex> lock(p->mu);
   try {
     ck(cudaSetDevice(p->device), "cudaSetDevice");
+    (void)cudaGetLastError();  // a stale error must not be reported by this call
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : p->stream;
     double* u = static_cast<double*>(u_dev);
     if (p->hp.depth < 2) {
@@ -548,6 +552,7 @@ int sfmm_gpu_apply(sfmm_gpu_plan* p, const void* q, void* u, int nrhs, int flags
   std::lock_guard<std::mutex> lock(p->mu);
   try {
     ck(cudaSetDevice(p->device), "cudaSetDevice");
+    (void)cudaGetLastError();  // a stale error must not be reported by this call
     const size_t col = (size_t)p->hp.n_points * p->scalar_bytes();
     const bool host = flags == SFMM_HOST_BUFFERS;
     cudaStream_t st = p->stream;
@@ -598,6 +603,7 @@ int sfmm_gpu_apply_async(sfmm_gpu_plan* p, const void* q_dev, void* u_dev, int n
   std::lock_guard<std::mutex> lock(p->mu);
   try {
     ck(cudaSetDevice(p->device), "cudaSetDevice");
+    (void)cudaGetLastError();  // a stale error must not be reported by this call
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : p->stream;
     const double* qd = static_cast<const double*>(q_dev);
     double* ud = static_cast<double*>(u_dev);
@@ -645,6 +651,7 @@ int sfmm_gpu_check_status(sfmm_gpu_plan* p) {
   std::lock_guard<std::mutex> lock(p->mu);
   try {
     ck(cudaSetDevice(p->device), "cudaSetDevice");
+    (void)cudaGetLastError();  // a stale error must not be reported by this call
     ck(cudaDeviceSynchronize(), "sync");
     int flag = 0;
     ck(cudaMemcpy(&flag, p->dp.err_flag, sizeof(int), cudaMemcpyDeviceToHost), "flag");
@@ -685,6 +692,7 @@ int sfmm_gpu_set_timing(sfmm_gpu_plan* p, int enable) {
   std::lock_guard<std::mutex> lock(p->mu);
   try {
     ck(cudaSetDevice(p->device), "cudaSetDevice");
+    (void)cudaGetLastError();  // a stale error must not be reported by this call
     if (enable && p->tev.empty()) {
       p->tev.resize((size_t)sfmm_gpu_plan::kMaxTimed * 6);
       for (cudaEvent_t& e : p->tev) ck(cudaEventCreate(&e), "cudaEventCreate");
@@ -702,6 +710,7 @@ int sfmm_gpu_get_timings(sfmm_gpu_plan* p, float* ms, int max_applies, int* n_ap
   std::lock_guard<std::mutex> lock(p->mu);
   try {
     ck(cudaSetDevice(p->device), "cudaSetDevice");
+    (void)cudaGetLastError();  // a stale error must not be reported by this call
     const int n = std::min(p->n_timed, max_applies);
     for (int i = 0; i < n; ++i) {
       ck(cudaEventSynchronize(p->tev[(size_t)i * 6 + 5]), "event sync");
@@ -733,6 +742,7 @@ int sfmm_gpu_fp64_peak(int device, double* tflops) {
   if (!tflops) return set_error(SFMM_EINVAL, "null argument");
   try {
     ck(cudaSetDevice(device), "cudaSetDevice");
+    (void)cudaGetLastError();  // a stale error must not be reported by this call
     *tflops = measure_fp64_peak(device);
     if (*tflops <= 0) return set_error(SFMM_ECUDA, "fp64 peak probe failed");
     return SFMM_OK;
@@ -758,6 +768,7 @@ int sfmm_gpu_direct_sum(int kernel, double kappa, int dim, int64_t n, const doub
   int rc = SFMM_OK;
   try {
     ck(cudaSetDevice(device), "cudaSetDevice");
+    (void)cudaGetLastError();  // a stale error must not be reported by this call
     ck(cudaMalloc(&dp, n * dim * sizeof(double)), "cudaMalloc");
     ck(cudaMalloc(&dq, n * sb), "cudaMalloc");
     ck(cudaMalloc(&du, std::max<int64_t>(n_targets, 1) * sb), "cudaMalloc");

@@ -46,7 +46,9 @@ struct CudaErr {
   std::string msg;
 };
 void ck(cudaError_t e, const char* what) {
-  if (e != cudaSuccess) throw CudaErr{std::string(what) + ": " + cudaGetErrorString(e)};
+  if (e == cudaSuccess) return;
+  (void)cudaGetLastError();  // reported here; do not leak into the next call
+  throw CudaErr{std::string(what) + ": " + cudaGetErrorString(e)};
 }
 
 // ---- scalar helpers (real / complex) ---------------------------------------
@@ -484,6 +486,7 @@ struct sfmm_skel_result {
     T.resize(t_scalars());
     if (!T.empty()) {
       ck(cudaSetDevice(device), "cudaSetDevice");
+    (void)cudaGetLastError();  // a stale error must not be reported by this call
       ck(cudaMemcpy(T.data(), d_T, T.size() * sizeof(double), cudaMemcpyDeviceToHost), "D2H T");
     }
     have_host_T = true;
@@ -793,6 +796,7 @@ int sfmm_gpu_build_skeletons(const sfmm_tree_desc* tree, int kernel, double kapp
   auto* R = new sfmm_skel_result();
   try {
     ck(cudaSetDevice(device), "cudaSetDevice");
+    (void)cudaGetLastError();  // a stale error must not be reported by this call
     const auto t0 = std::chrono::steady_clock::now();
     if (kernel == SFMM_HELMHOLTZ3D)
       run_skeletons<Cx>(*tree, kernel, kappa, tol, radius, edge, face, *R);

@@ -73,6 +73,7 @@ struct TreeFail {
 
 void ck(cudaError_t e, const char* what) {
   if (e == cudaSuccess) return;
+  (void)cudaGetLastError();  // reported here; do not leak into the next call
   throw TreeFail{e == cudaErrorMemoryAllocation ? SFMM_ENOMEM : SFMM_ECUDA,
                  std::string("build_tree: ") + what + ": " + cudaGetErrorString(e)};
 }
@@ -914,6 +915,7 @@ int sfmm_gpu_build_tree(int dim, int64_t n, const double* pts, int leaf_cap, int
   auto* R = new sfmm_gpu_tree();
   try {
     ck(cudaSetDevice(device), "cudaSetDevice");
+    (void)cudaGetLastError();  // a stale error must not be reported by this call
     const auto t0 = std::chrono::steady_clock::now();
     build(dim, n, pts, leaf_cap, *R);
     R->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

@@ -276,3 +276,18 @@ def test_degenerate_geometries_match_oracle(name, kernel, kappa):
     u_ref, st_ref = po.oracle_apply(d, q)
     assert rel_l2(u, u_ref) <= PARITY
     assert st.n_ifo_pairs == st_ref["n_ifo_pairs"] and st.n_tfo_pairs == st_ref["n_tfo_pairs"]
+
+
+def test_api_misuse_raises():
+    d = host.HostPlan.build(1, host.generate_points("cube", 3000, 2), 40, 1e-6).descriptor()
+    with pytest.raises((api.DeviceError, ValueError)):
+        api.GpuPlan(d, device=99)                     # no such device
+    plan = api.GpuPlan(d)
+    q = host.generate_charges(3000, 1)
+    with pytest.raises(ValueError):
+        api.fmm_apply(plan, q.reshape(3000, 1)[:, :0])  # zero right-hand sides
+    with pytest.raises(ValueError):
+        api.fmm_apply(plan, q, out=np.empty(2999))     # wrong output buffer
+    plan.close()
+    with pytest.raises(ValueError):
+        api.fmm_apply(plan, q)                        # closed plan
