@@ -71,6 +71,22 @@ struct TmpDev {
   }
 };
 
+// Makes `device` current for the scope of one ABI call and restores the
+// caller's device afterwards; clears stale (non-sticky) errors on entry.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int device) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    (void)cudaGetLastError();
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
 }  // namespace
 
 struct sfmm_gpu_plan {
@@ -109,6 +125,8 @@ struct sfmm_gpu_plan {
   }
 
   ~sfmm_gpu_plan() {
+    int prev = -1;
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
     cudaSetDevice(device);
     if (stream) cudaStreamSynchronize(stream);
     for (void* p : allocs) cudaFree(p);
@@ -121,6 +139,8 @@ struct sfmm_gpu_plan {
     for (cudaEvent_t e : tev) cudaEventDestroy(e);
     if (graph_exec) cudaGraphExecDestroy(graph_exec);
     if (stream) cudaStreamDestroy(stream);
+    (void)cudaGetLastError();
+    if (prev >= 0) cudaSetDevice(prev);  // leave the caller's current device as it was
   }
 
   void ensure_io(size_t bytes) {
@@ -259,8 +279,7 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
       return set_error(rc, err);
     }
     p->device = device;
-    ck(cudaSetDevice(device), "cudaSetDevice");
-    (void)cudaGetLastError();  // a stale error must not be reported by this call
+    DeviceGuard device_guard(device);
     ck(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking), "cudaStreamCreate");
     ck(cudaEventCreate(&p->ev_a), "cudaEventCreate");
     ck(cudaEventCreate(&p->ev_b), "cudaEventCreate");
@@ -495,8 +514,7 @@ int sfmm_gpu_apply_begin(sfmm_gpu_plan* p, const void* q_dev, void* send_dev, vo
   if (!p || !q_dev) return set_error(SFMM_EINVAL, "fmm_apply: bad arguments");
   std::lock_guard<std::mutex> lock(p->mu);
   try {
-    ck(cudaSetDevice(p->device), "cudaSetDevice");
-    (void)cudaGetLastError();  // a stale error must not be reported by this call
+    DeviceGuard device_guard(p->device);
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : p->stream;
     const double* q = static_cast<const double*>(q_dev);
     if (p->hp.depth >= 2) {
@@ -521,8 +539,7 @@ int sfmm_gpu_apply_end(sfmm_gpu_plan* p, const void* q_dev, const void* recv_dev
   if (!p || !u_dev) return set_error(SFMM_EINVAL, "fmm_apply: bad arguments");
   std::lock_guard<std::mutex> lock(p->mu);
   try {
-    ck(cudaSetDevice(p->device), "cudaSetDevice");
-    (void)cudaGetLastError();  // a stale error must not be reported by this call
+    DeviceGuard device_guard(p->device);
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : p->stream;
     double* u = static_cast<double*>(u_dev);
     if (p->hp.depth < 2) {
@@ -551,8 +568,7 @@ int sfmm_gpu_apply(sfmm_gpu_plan* p, const void* q, void* u, int nrhs, int flags
     return set_error(SFMM_EINVAL, "fmm_apply: sharded plan: use sfmm_gpu_apply_begin/_end");
   std::lock_guard<std::mutex> lock(p->mu);
   try {
-    ck(cudaSetDevice(p->device), "cudaSetDevice");
-    (void)cudaGetLastError();  // a stale error must not be reported by this call
+    DeviceGuard device_guard(p->device);
     const size_t col = (size_t)p->hp.n_points * p->scalar_bytes();
     const bool host = flags == SFMM_HOST_BUFFERS;
     cudaStream_t st = p->stream;
@@ -602,8 +618,7 @@ int sfmm_gpu_apply_async(sfmm_gpu_plan* p, const void* q_dev, void* u_dev, int n
     return set_error(SFMM_EINVAL, "fmm_apply: sharded plan: use sfmm_gpu_apply_begin/_end");
   std::lock_guard<std::mutex> lock(p->mu);
   try {
-    ck(cudaSetDevice(p->device), "cudaSetDevice");
-    (void)cudaGetLastError();  // a stale error must not be reported by this call
+    DeviceGuard device_guard(p->device);
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : p->stream;
     const double* qd = static_cast<const double*>(q_dev);
     double* ud = static_cast<double*>(u_dev);
@@ -650,8 +665,7 @@ int sfmm_gpu_check_status(sfmm_gpu_plan* p) {
   if (!p) return set_error(SFMM_EINVAL, "null plan");
   std::lock_guard<std::mutex> lock(p->mu);
   try {
-    ck(cudaSetDevice(p->device), "cudaSetDevice");
-    (void)cudaGetLastError();  // a stale error must not be reported by this call
+    DeviceGuard device_guard(p->device);
     ck(cudaDeviceSynchronize(), "sync");
     int flag = 0;
     ck(cudaMemcpy(&flag, p->dp.err_flag, sizeof(int), cudaMemcpyDeviceToHost), "flag");
@@ -691,8 +705,7 @@ int sfmm_gpu_set_timing(sfmm_gpu_plan* p, int enable) {
   if (!p) return set_error(SFMM_EINVAL, "null plan");
   std::lock_guard<std::mutex> lock(p->mu);
   try {
-    ck(cudaSetDevice(p->device), "cudaSetDevice");
-    (void)cudaGetLastError();  // a stale error must not be reported by this call
+    DeviceGuard device_guard(p->device);
     if (enable && p->tev.empty()) {
       p->tev.resize((size_t)sfmm_gpu_plan::kMaxTimed * 6);
       for (cudaEvent_t& e : p->tev) ck(cudaEventCreate(&e), "cudaEventCreate");
@@ -709,8 +722,7 @@ int sfmm_gpu_get_timings(sfmm_gpu_plan* p, float* ms, int max_applies, int* n_ap
   if (!p || !n_applies) return set_error(SFMM_EINVAL, "null argument");
   std::lock_guard<std::mutex> lock(p->mu);
   try {
-    ck(cudaSetDevice(p->device), "cudaSetDevice");
-    (void)cudaGetLastError();  // a stale error must not be reported by this call
+    DeviceGuard device_guard(p->device);
     const int n = std::min(p->n_timed, max_applies);
     for (int i = 0; i < n; ++i) {
       ck(cudaEventSynchronize(p->tev[(size_t)i * 6 + 5]), "event sync");
@@ -741,8 +753,7 @@ int sfmm_gpu_test_sincos(const double* x, int64_t n, double* out) {
 int sfmm_gpu_fp64_peak(int device, double* tflops) {
   if (!tflops) return set_error(SFMM_EINVAL, "null argument");
   try {
-    ck(cudaSetDevice(device), "cudaSetDevice");
-    (void)cudaGetLastError();  // a stale error must not be reported by this call
+    DeviceGuard device_guard(device);
     *tflops = measure_fp64_peak(device);
     if (*tflops <= 0) return set_error(SFMM_ECUDA, "fp64 peak probe failed");
     return SFMM_OK;
@@ -767,8 +778,7 @@ int sfmm_gpu_direct_sum(int kernel, double kappa, int dim, int64_t n, const doub
   void *dp = nullptr, *dq = nullptr, *du = nullptr, *dt = nullptr, *de = nullptr;
   int rc = SFMM_OK;
   try {
-    ck(cudaSetDevice(device), "cudaSetDevice");
-    (void)cudaGetLastError();  // a stale error must not be reported by this call
+    DeviceGuard device_guard(device);
     ck(cudaMalloc(&dp, n * dim * sizeof(double)), "cudaMalloc");
     ck(cudaMalloc(&dq, n * sb), "cudaMalloc");
     ck(cudaMalloc(&du, std::max<int64_t>(n_targets, 1) * sb), "cudaMalloc");

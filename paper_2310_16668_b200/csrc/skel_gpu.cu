@@ -51,6 +51,22 @@ void ck(cudaError_t e, const char* what) {
   throw CudaErr{std::string(what) + ": " + cudaGetErrorString(e)};
 }
 
+// Makes `device` current for the scope of one ABI call and restores the
+// caller's device afterwards; clears stale (non-sticky) errors on entry.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int device) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    (void)cudaGetLastError();
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
 // ---- scalar helpers (real / complex) ---------------------------------------
 struct Cx {
   double re, im;
@@ -485,8 +501,7 @@ struct sfmm_skel_result {
     if (have_host_T) return;
     T.resize(t_scalars());
     if (!T.empty()) {
-      ck(cudaSetDevice(device), "cudaSetDevice");
-    (void)cudaGetLastError();  // a stale error must not be reported by this call
+      DeviceGuard device_guard(device);
       ck(cudaMemcpy(T.data(), d_T, T.size() * sizeof(double), cudaMemcpyDeviceToHost), "D2H T");
     }
     have_host_T = true;
@@ -795,8 +810,7 @@ int sfmm_gpu_build_skeletons(const sfmm_tree_desc* tree, int kernel, double kapp
     return set_last_error(SFMM_EINVAL, "build_skeletons: bad proxy configuration");
   auto* R = new sfmm_skel_result();
   try {
-    ck(cudaSetDevice(device), "cudaSetDevice");
-    (void)cudaGetLastError();  // a stale error must not be reported by this call
+    DeviceGuard device_guard(device);
     const auto t0 = std::chrono::steady_clock::now();
     if (kernel == SFMM_HELMHOLTZ3D)
       run_skeletons<Cx>(*tree, kernel, kappa, tol, radius, edge, face, *R);

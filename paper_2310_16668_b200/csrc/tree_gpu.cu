@@ -78,6 +78,22 @@ void ck(cudaError_t e, const char* what) {
                  std::string("build_tree: ") + what + ": " + cudaGetErrorString(e)};
 }
 
+// Makes `device` current for the scope of one ABI call and restores the
+// caller's device afterwards; clears stale (non-sticky) errors on entry.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int device) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    (void)cudaGetLastError();
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
 template <class T>
 struct Dev {
   T* p = nullptr;
@@ -914,8 +930,7 @@ int sfmm_gpu_build_tree(int dim, int64_t n, const double* pts, int leaf_cap, int
   *out = nullptr;
   auto* R = new sfmm_gpu_tree();
   try {
-    ck(cudaSetDevice(device), "cudaSetDevice");
-    (void)cudaGetLastError();  // a stale error must not be reported by this call
+    DeviceGuard device_guard(device);
     const auto t0 = std::chrono::steady_clock::now();
     build(dim, n, pts, leaf_cap, *R);
     R->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
