@@ -291,3 +291,23 @@ def test_api_misuse_raises():
     plan.close()
     with pytest.raises(ValueError):
         api.fmm_apply(plan, q)                        # closed plan
+
+
+def test_sync_apply_on_device_buffers():
+    """sfmm_gpu_apply with SFMM_DEVICE_BUFFERS (synchronous, stats filled) gives
+    the host-buffer result bit for bit, single and multi-RHS."""
+    import ctypes as C
+    import torch
+    from paper_2310_16668_b200 import _abi
+    n = 15000
+    _, _, plan = _pipeline(1, "sphere", n, 50, 1e-6)
+    for nrhs in (1, 3):
+        Q = np.asfortranarray(np.stack([host.generate_charges(n, 40 + r) for r in range(nrhs)], 1))
+        U = api.fmm_apply(plan, Q)
+        qd = torch.from_numpy(Q.T.copy()).cuda()
+        ud = torch.empty_like(qd)
+        st = _abi.GpuStats()
+        api._raise(_abi.gpu_lib().sfmm_gpu_apply(plan.handle, qd.data_ptr(), ud.data_ptr(), nrhs,
+                                                 _abi.SFMM_DEVICE_BUFFERS, C.byref(st)))
+        assert np.array_equal(ud.cpu().numpy().T, U)
+        assert st.n_ifo_pairs > 0 and st.ms_total > 0
