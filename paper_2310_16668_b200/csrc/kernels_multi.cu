@@ -114,10 +114,14 @@ struct ChunkPos {
 // without skeleton rows -- most of them -- run the lighter WH=false variant.
 // TAB: Helmholtz arguments within the sincos table's range (sincos_fast otherwise).
 #ifndef SFMM_K2M_MIN_BLOCKS
-#define SFMM_K2M_MIN_BLOCKS 4  // light variant (measured: 4 > 3 on config 4); WH runs at 2
+#define SFMM_K2M_MIN_BLOCKS 4  // light variant (measured: 4 > 3 on config 4)
+#endif
+#ifndef SFMM_K2M_MIN_BLOCKS_WH
+#define SFMM_K2M_MIN_BLOCKS_WH 3  // uhat variant (measured: 3 > 2, 4)
 #endif
 template <int KER, bool WH, bool TAB>
-__global__ void __launch_bounds__(kMThreads, WH ? 2 : SFMM_K2M_MIN_BLOCKS) k2m_translate(K2MArgs a) {
+__global__ void __launch_bounds__(kMThreads, WH ? SFMM_K2M_MIN_BLOCKS_WH : SFMM_K2M_MIN_BLOCKS)
+    k2m_translate(K2MArgs a) {
   constexpr bool CPLX = KER == SFMM_HELMHOLTZ3D;
   constexpr int SW = CPLX ? 2 : 1;
   constexpr int NB = 2;             // rhs blocks of 8
