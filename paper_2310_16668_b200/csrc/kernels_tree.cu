@@ -107,10 +107,12 @@ __global__ void __launch_bounds__(kUpThreads) k1_upward_cplx(
     const LevelItem* __restrict__ items, const BoxRec* __restrict__ box,
     const int64_t* __restrict__ T_off, const double2* __restrict__ T, double2* __restrict__ Q,
     double2* __restrict__ QH, const int64_t* __restrict__ up_dst) {
+  extern __shared__ double2 smq2[];
   const LevelItem it = items[blockIdx.x];
   const BoxRec br = box[it.box];
   const int k = br.k, r = br.n - br.k;
-  const double2* qR = Q + br.slot + k;
+  for (int j = threadIdx.x; j < r; j += blockDim.x) smq2[j] = Q[br.slot + k + j];
+  __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const double2* Tb = T + T_off[it.box];
   const int i1 = min(it.first + kUpRows1, k);
@@ -118,7 +120,7 @@ __global__ void __launch_bounds__(kUpThreads) k1_upward_cplx(
     const double2* Ti = Tb + (int64_t)i * r;
     double ar = 0.0, ai = 0.0;
     for (int j = lane; j < r; j += 32) {
-      const double2 t = __ldg(Ti + j), x = __ldg(qR + j);
+      const double2 t = __ldg(Ti + j), x = smq2[j];
       ar = fma(t.x, x.x, fma(-t.y, x.y, ar));
       ai = fma(t.x, x.y, fma(t.y, x.x, ai));
     }
@@ -411,7 +413,7 @@ void launch_upward(const DevPlan& p, const HostPlan& hp, int level, DevState& s,
   const int64_t i0 = hp.up1_lvl[level], i1 = hp.up1_lvl[level + 1];
   if (i1 <= i0) return;
   if (p.cplx)
-    k1_upward_cplx<<<(unsigned)(i1 - i0), kUpThreads, 0, st>>>(
+    k1_upward_cplx<<<(unsigned)(i1 - i0), kUpThreads, p.up_smem, st>>>(
         p.up1_items + i0, p.box, p.T_off, reinterpret_cast<const double2*>(p.T),
         reinterpret_cast<double2*>(s.Q), reinterpret_cast<double2*>(s.QH), p.up_dst);
   else
@@ -506,9 +508,9 @@ void launch_unpack(const DevPlan& p, DevState& s, const double* buf, cudaStream_
 int configure_tree_kernels(DevPlan& p, size_t max_r, size_t max_k) {
   const size_t sw = p.cplx ? 16 : 8;
   p.up_smem = std::max<size_t>(max_r * sw, 16);
-  if (SFMM_K1_SMEM && !p.cplx && p.up_smem > 48 * 1024 &&
-      cudaFuncSetAttribute(k1_upward_real, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)p.up_smem) != cudaSuccess)
+  if (p.up_smem > 48 * 1024 &&
+      cudaFuncSetAttribute(p.cplx ? (const void*)k1_upward_cplx : (const void*)k1_upward_real,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.up_smem) != cudaSuccess)
     return -1;
   p.down_smem = std::max<size_t>(max_k * sw, 16);
   if (p.down_smem > 48 * 1024) {
