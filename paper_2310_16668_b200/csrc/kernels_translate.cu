@@ -388,6 +388,68 @@ __device__ __forceinline__ void inner_cplx(const WarpSmemCplx& sm, const double2
   }
 }
 
+// kSYM for the complex kernel: as sym_chunk (rotation, fixed order) with
+// complex row and column accumulators; columns past the source box are given
+// G = 0 explicitly (a far-away padding point would make exp(i kappa r) NaN).
+template <int R, bool H, bool TAB>
+__device__ __forceinline__ void sym_chunk_cplx(const WarpSmemCplx& sm, const double2* __restrict__ tab,
+                                               int j0, int n_c, int k_c, double kappa,
+                                               const double (&xi)[R], const double (&yi)[R],
+                                               const double (&zi)[R], const double2 (&qr)[R],
+                                               const double2 (&qhr)[R], double2 (&au)[R],
+                                               double2 (&ah)[R], double2* __restrict__ st_u,
+                                               double2* __restrict__ st_h, int lane) {
+  double2 cp = make_double2(0.0, 0.0), ch = make_double2(0.0, 0.0);
+  const int from = (lane + 1) & 31;
+  const int cnt = n_c - j0;  // valid columns of this chunk (may exceed 32)
+#pragma unroll 2
+  for (int s = 0; s < 32; ++s) {
+    const int jc = (lane + s) & 31;
+    const double2 xy = sm.xy[jc];
+    const double zz = sm.z[jc];
+    const double2 wa = sm.a[jc];
+    const double2 wh = H ? sm.h[jc] : make_double2(0.0, 0.0);
+    const bool valid = jc < cnt;
+    double2 cs = make_double2(0.0, 0.0), hs = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const double dx = xi[r] - xy.x, dy = yi[r] - xy.y, dz = zi[r] - zz;
+      const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+      const double y = rsqrt_fp64(r2);
+      double gr, gi;
+      if constexpr (TAB) {
+        sincos_tab_scaled(tab, kappa * (r2 * y), y, &gr, &gi);
+      } else {
+        double sn, c;
+        sincos_fast(kappa * (r2 * y), &sn, &c);
+        gr = c * y;
+        gi = sn * y;
+      }
+      gr = valid ? gr : 0.0;
+      gi = valid ? gi : 0.0;
+      au[r].x = fma(gr, wa.x, fma(-gi, wa.y, au[r].x));
+      au[r].y = fma(gr, wa.y, fma(gi, wa.x, au[r].y));
+      cs.x = fma(gr, qr[r].x, fma(-gi, qr[r].y, cs.x));
+      cs.y = fma(gr, qr[r].y, fma(gi, qr[r].x, cs.y));
+      if (H) {
+        ah[r].x = fma(gr, wh.x, fma(-gi, wh.y, ah[r].x));
+        ah[r].y = fma(gr, wh.y, fma(gi, wh.x, ah[r].y));
+        hs.x = fma(gr, qhr[r].x, fma(-gi, qhr[r].y, hs.x));
+        hs.y = fma(gr, qhr[r].y, fma(gi, qhr[r].x, hs.y));
+      }
+    }
+    cp.x = __shfl_sync(kFull, cp.x + cs.x, from);
+    cp.y = __shfl_sync(kFull, cp.y + cs.y, from);
+    if (H) {
+      ch.x = __shfl_sync(kFull, ch.x + hs.x, from);
+      ch.y = __shfl_sync(kFull, ch.y + hs.y, from);
+    }
+  }
+  const int col = j0 + lane;
+  if (col < n_c) st_u[col] = cp;
+  if (H && col < k_c) st_h[col] = ch;
+}
+
 template <int R, bool TAB>
 __device__ __forceinline__ void task_cplx(const K2Args& a, const Task& t, WarpSmemCplx& sm,
                                           const double2* tab, int lane) {
@@ -395,26 +457,60 @@ __device__ __forceinline__ void task_cplx(const K2Args& a, const Task& t, WarpSm
   const double2* QH = reinterpret_cast<const double2*>(a.QH);
   const BoxRec tb = a.box[t.box];
   double xi[R], yi[R], zi[R];
-  double2 au[R], ah[R];
+  double2 au[R], ah[R], qr[R], qhr[R];
   int rowi[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int row = t.row0 + r * 32 + lane;
     rowi[r] = row;
-    const int64_t s = tb.slot + (row < t.row0 + t.nrows ? row : t.row0);
+    const bool valid = row < t.row0 + t.nrows;
+    const int64_t s = tb.slot + (valid ? row : t.row0);
     xi[r] = a.X[s];
     yi[r] = a.Y[s];
     zi[r] = a.Z[s];
     au[r] = make_double2(0.0, 0.0);
     ah[r] = make_double2(0.0, 0.0);
+    qr[r] = valid ? Q[s] : make_double2(0.0, 0.0);  // row charges feed kSYM column sums
+    qhr[r] = (valid && row < tb.k) ? QH[tb.skel + row] : make_double2(0.0, 0.0);
   }
   const EntryRange er = a.er[t.box];
   const bool skel_rows = t.row0 < tb.k;
+  double2* St = reinterpret_cast<double2*>(a.St);
+  int64_t stage = t.stage;
   for (int e = 0; e < er.count; ++e) {
     const int32_t code = a.ent[er.begin + e];
     const int32_t c = code >> kModeBits;
     const int mode = code & kModeMask;
     const BoxRec sb = a.box[c];
+    if (mode == kSYM) {
+      double2* st_u = St + stage;
+      double2* st_h = st_u + sb.n;
+      for (int j0 = 0; j0 < sb.n; j0 += 32) {
+        const int j = j0 + lane;
+        if (j < sb.n) {
+          const int64_t s = sb.slot + j;
+          sm.xy[lane] = make_double2(a.X[s], a.Y[s]);
+          sm.z[lane] = a.Z[s];
+          sm.a[lane] = Q[s];
+          sm.h[lane] = j < sb.k ? QH[sb.skel + j] : make_double2(0.0, 0.0);
+        } else {  // zero weights; G is zeroed for these columns
+          sm.xy[lane] = make_double2(0.0, 0.0);
+          sm.z[lane] = 0.0;
+          sm.a[lane] = make_double2(0.0, 0.0);
+          sm.h[lane] = make_double2(0.0, 0.0);
+        }
+        __syncwarp();
+        if (skel_rows && j0 < sb.k)
+          sym_chunk_cplx<R, true, TAB>(sm, tab, j0, sb.n, sb.k, a.kappa, xi, yi, zi, qr, qhr, au,
+                                       ah, st_u, st_h, lane);
+        else
+          sym_chunk_cplx<R, false, TAB>(sm, tab, j0, sb.n, sb.k, a.kappa, xi, yi, zi, qr, qhr, au,
+                                        ah, st_u, st_h, lane);
+        __syncwarp();
+      }
+      stage += sb.n + ((skel_rows && sb.k > 0) ? sb.k : 0);
+      continue;
+    }
     const bool self = c == t.box;
     for (int j0 = 0; j0 < sb.n; j0 += 32) {
       const int j = j0 + lane;
@@ -476,9 +572,7 @@ __global__ void __launch_bounds__(kThreads, 4) k2_translate_cplx(K2Args a) {
     const Task task = a.tasks[t];
     switch ((task.nrows + 31) >> 5) {
       case 1: task_cplx<1, TAB>(a, task, sm, tab, lane); break;
-      case 2: task_cplx<2, TAB>(a, task, sm, tab, lane); break;
-      case 3: task_cplx<3, TAB>(a, task, sm, tab, lane); break;
-      default: task_cplx<4, TAB>(a, task, sm, tab, lane); break;
+      default: task_cplx<2, TAB>(a, task, sm, tab, lane); break;  // complex plans: <= 64-row tiles
     }
   }
 }
@@ -510,6 +604,43 @@ __global__ void __launch_bounds__(256) k2b_reduce(const BoxRec* __restrict__ box
         h += o >= 0 ? __ldg(St + o + i) : 0.0;
       }
       UH[br.skel + i] -= scale * h;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k2b_reduce_cplx(const BoxRec* __restrict__ box,
+                                                       const int32_t* __restrict__ recv_box,
+                                                       const int64_t* __restrict__ recv_off,
+                                                       const int64_t* __restrict__ recv_u,
+                                                       const int64_t* __restrict__ recv_h,
+                                                       const double2* __restrict__ St,
+                                                       double2* __restrict__ U,
+                                                       double2* __restrict__ UH, double scale) {
+  const BoxRec br = box[recv_box[blockIdx.x]];
+  const int64_t e0 = recv_off[blockIdx.x], e1 = recv_off[blockIdx.x + 1];
+  for (int i = threadIdx.x; i < br.n; i += blockDim.x) {
+    double2 s = make_double2(0.0, 0.0);
+#pragma unroll 4
+    for (int64_t e = e0; e < e1; ++e) {
+      const double2 v = __ldg(St + recv_u[e] + i);
+      s.x += v.x;
+      s.y += v.y;
+    }
+    const double2 u = U[br.slot + i];
+    U[br.slot + i] = make_double2(u.x + scale * s.x, u.y + scale * s.y);
+    if (i < br.k) {
+      double2 h = make_double2(0.0, 0.0);
+#pragma unroll 4
+      for (int64_t e = e0; e < e1; ++e) {
+        const int64_t o = recv_h[e];
+        if (o >= 0) {
+          const double2 v = __ldg(St + o + i);
+          h.x += v.x;
+          h.y += v.y;
+        }
+      }
+      const double2 uh = UH[br.skel + i];
+      UH[br.skel + i] = make_double2(uh.x - scale * h.x, uh.y - scale * h.y);
     }
   }
 }
@@ -582,7 +713,11 @@ void launch_translate(const DevPlan& p, DevState& s, cudaStream_t st, TranslateP
     else
       k2_translate_real<GenLaplace2d><<<grid, kThreads, 0, st>>>(a);
   }
-  if (part != kInteriorTasks && p.n_recv > 0) {
+  if (part != kInteriorTasks && p.n_recv > 0 && p.cplx) {
+    k2b_reduce_cplx<<<(unsigned)p.n_recv, 256, 0, st>>>(
+        p.box, p.recv_box, p.recv_off, p.recv_u, p.recv_h, reinterpret_cast<const double2*>(p.stage),
+        reinterpret_cast<double2*>(s.U), reinterpret_cast<double2*>(s.UH), 0.25);
+  } else if (part != kInteriorTasks && p.n_recv > 0) {
     const double scale = p.kernel == SFMM_LAPLACE3D ? GenLaplace3d::kScale : GenLaplace2d::kScale;
     k2b_reduce<<<(unsigned)p.n_recv, 256, 0, st>>>(p.box, p.recv_box, p.recv_off, p.recv_u,
                                                    p.recv_h, p.stage, s.U, s.UH, scale);

@@ -291,7 +291,7 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
     // same rank is evaluated once (kSYM in b's list): b's rows are accumulated
     // as usual and c's rows receive A_cb q_b = (A_bc)^T q_b as staged column
     // sums.  Pairs across ranks stay kIFO on both sides.
-    hp.symmetric = opt.symmetric && !hp.cplx;
+    hp.symmetric = opt.symmetric;
     if (hp.symmetric) {  // the colleague relation must be symmetric to stage
       int asym = 0;
 #pragma omp parallel for schedule(dynamic, 1024) reduction(| : asym)
@@ -501,6 +501,7 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
 #ifdef SFMM_TILE_FORCE
       tile = SFMM_TILE_FORCE;  // dev knob (A/B of the K2 occupancy variants)
 #endif
+      if (hp.cplx) tile = std::min(tile, kTileRows / 2);  // complex K2: <= 2 rows per lane
       hp.tile_rows = tile;
       for (int32_t b = 0; b < nb; ++b) {
         const EntryRange& er = hp.ent_range[b];

@@ -379,7 +379,7 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
       dp.up1_items = p->upload(hp.up1_items);
       dp.copy_boxes = p->upload(hp.copy_boxes);
       dp.down_items = p->upload(hp.down_items);
-      dp.stage = p->alloc<double>((size_t)std::max<int64_t>(hp.stage_size, 1));
+      dp.stage = p->alloc<double>((size_t)std::max<int64_t>(hp.stage_size, 1) * sw);  // scalars
       dp.n_recv = (int64_t)hp.recv_box.size();
       dp.recv_box = p->upload(hp.recv_box);
       dp.recv_off = p->upload(hp.recv_off);
