@@ -425,6 +425,14 @@ def main():
     if ws > 1:
         run_sharded(args, ws, rank, local)
         return
+    if args.n > 6e7:
+        # ~1.8 kB of resident plan per point (T, staging, slots): N=1e8 needs
+        # ~180 GB, more than one B200 -- config 5 is a 2/4/8-GPU sharded run
+        emit({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": 1,
+              "config": {"workload": f"{args.kernel} {args.dist} N={args.n:.0e}"},
+              "unavailable": "the resident plan exceeds one B200's HBM at this N; run it sharded "
+                             "(torchrun --nproc-per-node 2/4/8 bench.py --gpus N --config c5)"})
+        return
 
     import torch
     from paper_2310_16668_b200 import api, host
