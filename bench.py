@@ -456,6 +456,8 @@ def main():
     if nrhs > 1:
         q = np.asfortranarray(np.stack([gen(n, (1 + r) ^ CHARGE_STREAM) for r in range(nrhs)], 1))
     t_gen = time.perf_counter() - t0
+    torch.zeros(1, device=f"cuda:{dev}")  # CUDA context up front, not inside the tree build time
+    torch.cuda.synchronize(dev)
     # GPU precompute keeps T in HBM: the plan takes it device-to-device
     hp = (host.HostPlan.build_gpu(kern, pts, args.leaf, args.tol, args.kappa, device=dev,
                                   host_T=False, tree="gpu")

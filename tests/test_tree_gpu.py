@@ -104,3 +104,9 @@ def test_gpu_tree_feeds_the_apply():
     ug = api.fmm_apply(api.GpuPlan.from_host(hg), q)
     uh = api.fmm_apply(api.GpuPlan.from_host(hh), q)
     assert np.array_equal(ug, uh)
+
+
+@pytest.mark.parametrize("dist,n,leaf", [("cube", 10_000_000, 128), ("sphere", 3_000_000, 128)])
+def test_gpu_tree_matches_host_at_scale(dist, n, leaf):
+    # the headline geometry and a large adaptive one (balance replay on the host)
+    _same_tree(host.generate_points(dist, n, 1), leaf)
