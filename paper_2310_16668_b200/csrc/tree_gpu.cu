@@ -634,12 +634,14 @@ void build(int dim, int64_t n, const double* pts_host, int cap, sfmm_gpu_tree& R
   if (n < 1) throw TreeFail{SFMM_EINVAL, "build_tree: empty point set"};
   if (n > std::numeric_limits<int32_t>::max() / 2)
     throw TreeFail{SFMM_EINVAL, "build_tree: point count out of range"};
+  Timer tv;
   {
     int bad = 0;
 #pragma omp parallel for schedule(static) reduction(| : bad)
     for (int64_t i = 0; i < n * dim; ++i) bad |= !std::isfinite(pts_host[i]);
     if (bad) throw TreeFail{SFMM_EINVAL, "build_tree: non-finite coordinate"};
   }
+  tv.mark("validate");
   Timer tm;
   const int max_depth = dim == 2 ? kMaxDepth2 : kMaxDepth3;
   Dev<double> pts;
