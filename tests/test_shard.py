@@ -178,3 +178,22 @@ def test_virtual_ranks_parity_vs_oracle_1e6():
         assert rel_l2(u, u_ref) <= 1e-12
     t = np.arange(0, n, 9973, dtype=np.int32)
     assert max_rel(u[t], api.direct_sum_subset(1, 1.0, pts, q, t)) <= 1e-5
+
+
+@pytest.mark.gpu
+def test_bench_sharded_line_two_ranks_gloo(tmp_path):
+    """The N>1 bench path end to end: torchrun, two ranks (one GPU, gloo
+    exchange through host memory), the JSON line with parity vs the 1-GPU plan."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "2", "--warmup", "3",
+           "--backend", "gloo", "--points", "3e5"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["gpu_launches"] > 0
+    assert line["relerr_vs_single_gpu"] <= 1e-12
