@@ -297,6 +297,19 @@ void sfmm_gpu_skel_destroy(sfmm_skel_result* res);
 int sfmm_gpu_plan_create_skel(const sfmm_plan_desc* desc, const sfmm_skel_result* skel,
                               int device, int n_ranks, int rank, sfmm_gpu_plan** out);
 
+/*
+ * The whole pipeline on the GPU in one call: tree + neighbor
+ * lists (sfmm_gpu_build_tree, bit-identical to the reference), skeletons
+ * (sfmm_gpu_build_skeletons) and the plan, with the interpolation operators
+ * kept in HBM (sfmm_gpu_plan_create_skel) -- the device counterpart of the
+ * reference's build_tree + build_neighbor_lists + build_skeletons + make_plan
+ * followed by sfmm_gpu_plan_create.  pts: n x dim, original order; proxy
+ * parameters <= 0 take the reference defaults (2.95, 24, 8).
+ */
+int sfmm_gpu_plan_from_points(int kernel, double kappa, int dim, int64_t n, const double* pts,
+                              int leaf_cap, double tol, double proxy_radius, int proxy_edge2d,
+                              int proxy_face3d, int device, sfmm_gpu_plan** out);
+
 /* Phase timing.  While enabled, every apply records CUDA events on its stream
  * around its five phases (0 gather, 1 upward, 2 translate, 3 downward,
  * 4 scatter).  sfmm_gpu_get_timings synchronises, writes ms[5*i + phase] for

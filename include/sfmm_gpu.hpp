@@ -35,6 +35,7 @@ inline void raise(int rc, const char* what) {
   const std::string msg = std::string(what) + ": " + sfmm_gpu_last_error();
   if (rc == SFMM_EINVAL) throw std::invalid_argument(msg);
   if (rc == SFMM_EDUPLICATE) throw DuplicatePointError(msg);
+  if (rc == SFMM_EDEPTH) throw DepthExceededError(msg);
   throw std::runtime_error(msg);
 }
 
@@ -149,14 +150,34 @@ class GpuPlan {
     detail::raise(sfmm_gpu_plan_create(&d, device, &h_), "GpuPlan");
   }
 
+  // The whole pipeline on the GPU (tree, neighbor lists, skeletons, plan) from
+  // the points alone -- the device counterpart of build_tree +
+  // build_neighbor_lists + build_skeletons + make_plan (sfmm_gpu_plan_from_points).
+  // The tree is bit-identical to the reference's; skeletons meet the same ID
+  // criterion (pivots are rounding-sensitive, so not bit-identical).
+  static GpuPlan from_points(const K& kernel, const PointSet& pts, int leaf_cap, double tol,
+                             int device = 0) {
+    GpuPlan g;
+    g.n_ = pts.size();
+    detail::raise(sfmm_gpu_plan_from_points(detail::KernelId<K>::value, detail::kappa_of(kernel),
+                                            pts.dim, pts.size(), pts.coords.data(), leaf_cap, tol,
+                                            0.0, 0, 0, device, &g.h_),
+                  "GpuPlan::from_points");
+    return g;
+  }
+
+  GpuPlan(GpuPlan&& o) noexcept : n_(o.n_), h_(o.h_) { o.h_ = nullptr; }
   GpuPlan(const GpuPlan&) = delete;
   GpuPlan& operator=(const GpuPlan&) = delete;
-  ~GpuPlan() { sfmm_gpu_plan_destroy(h_); }
+  ~GpuPlan() {
+    if (h_) sfmm_gpu_plan_destroy(h_);
+  }
 
   sfmm_gpu_plan* handle() const { return h_; }
   int64_t n_points() const { return n_; }
 
  private:
+  GpuPlan() = default;
   int64_t n_ = 0;
   sfmm_gpu_plan* h_ = nullptr;
 };

@@ -61,7 +61,19 @@ int run(const char* name, const K& kern, Distribution dist, int64_t n, int leaf,
     threw = true;
   }
   if (!threw) std::printf("%-28s size mismatch did not throw std::invalid_argument FAIL\n", name);
-  return ok && threw ? 0 : 1;
+  // the whole pipeline on the GPU from the points alone: same tree (pair counts
+  // identical), own skeletons (agreement within the ID tolerance)
+  ApplyStats s_pipe;
+  gpu::GpuPlan<K> gpipe = gpu::GpuPlan<K>::from_points(kern, pts, leaf, tol);
+  const std::vector<S> u_pipe = gpu::fmm_apply(gpipe, q, &s_pipe);
+  const double err_pipe = rel_l2(u_pipe, u_cpu);
+  const bool pipe_ok = err_pipe <= 10 * tol && s_pipe.n_ifo_pairs == s_cpu.n_ifo_pairs &&
+                       s_pipe.n_ifs_pairs == s_cpu.n_ifs_pairs &&
+                       s_pipe.n_tfo_pairs == s_cpu.n_tfo_pairs &&
+                       s_pipe.n_level1_pairs == s_cpu.n_level1_pairs;
+  std::printf("%-28s GPU pipeline rel_l2 vs CPU %.3e (bar %.0e) %s\n", name, err_pipe, 10 * tol,
+              pipe_ok ? "OK" : "FAIL");
+  return ok && threw && pipe_ok ? 0 : 1;
 }
 
 int main() {

@@ -340,6 +340,10 @@ def gpu_lib() -> C.CDLL:
     lib.sfmm_gpu_skel_destroy.restype = None
     lib.sfmm_gpu_test_sincos.argtypes = [vp, C.c_int64, vp]
     lib.sfmm_gpu_test_sincos.restype = C.c_int
+    lib.sfmm_gpu_plan_from_points.argtypes = [C.c_int, C.c_double, C.c_int, C.c_int64, vp, C.c_int,
+                                              C.c_double, C.c_double, C.c_int, C.c_int, C.c_int,
+                                              C.POINTER(vp)]
+    lib.sfmm_gpu_plan_from_points.restype = C.c_int
     lib.sfmm_gpu_test_log.argtypes = [vp, C.c_int64, vp]
     lib.sfmm_gpu_test_log.restype = C.c_int
     _gpu_lib = lib
@@ -355,5 +359,5 @@ GPU_SYMBOLS = [
     "sfmm_gpu_build_skeletons", "sfmm_gpu_skel_fill", "sfmm_gpu_skel_destroy",
     "sfmm_gpu_test_sincos", "sfmm_gpu_skel_describe", "sfmm_gpu_skel_device_T",
     "sfmm_gpu_plan_create_skel", "sfmm_gpu_build_tree", "sfmm_gpu_tree_arrays",
-    "sfmm_gpu_tree_destroy", "sfmm_gpu_test_log",
+    "sfmm_gpu_tree_destroy", "sfmm_gpu_test_log", "sfmm_gpu_plan_from_points",
 ]

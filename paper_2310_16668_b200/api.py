@@ -91,6 +91,26 @@ class GpuPlan:
         self.dtype = np.complex128 if self.is_complex else np.float64
 
     @classmethod
+    def from_points(cls, kernel: int, pts, leaf_cap: int, tol: float, kappa: float = 1.0,
+                    proxy: tuple | None = None, device: int = 0) -> "GpuPlan":
+        """Tree, skeletons and plan in one call, all on the GPU
+        (sfmm_gpu_plan_from_points); pts (n, dim) in the original order."""
+        pts = np.ascontiguousarray(pts, dtype=np.float64)
+        if pts.ndim != 2:
+            raise ValueError("from_points: points must be an (n, dim) array")
+        px = proxy or (0.0, 0, 0)
+        h = C.c_void_p()
+        _raise(_abi.gpu_lib().sfmm_gpu_plan_from_points(
+            kernel, kappa, pts.shape[1], pts.shape[0], pts.ctypes.data, leaf_cap, tol,
+            float(px[0]), int(px[1]), int(px[2]), device, C.byref(h)))
+        self = cls.__new__(cls)
+        self.device, self._h = device, h
+        self.kernel, self.n_points = int(kernel), int(pts.shape[0])
+        self.is_complex = self.kernel in (_abi.HELMHOLTZ2D, _abi.HELMHOLTZ3D)
+        self.dtype = np.complex128 if self.is_complex else np.float64
+        return self
+
+    @classmethod
     def from_host(cls, hp, device: int | None = None) -> "GpuPlan":
         """Plan from a host.HostPlan; device-resident skeletons (build_gpu with
         host_T=False) are used in place, so T never crosses PCIe."""

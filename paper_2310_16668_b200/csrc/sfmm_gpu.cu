@@ -807,4 +807,69 @@ int sfmm_gpu_direct_sum(int kernel, double kappa, int dim, int64_t n, const doub
   return rc;
 }
 
+int sfmm_gpu_plan_from_points(int kernel, double kappa, int dim, int64_t n, const double* pts,
+                              int leaf_cap, double tol, double proxy_radius, int proxy_edge2d,
+                              int proxy_face3d, int device, sfmm_gpu_plan** out) {
+  if (!out) return set_error(SFMM_EINVAL, "plan_from_points: null argument");
+  *out = nullptr;
+  if (kernel == SFMM_HELMHOLTZ2D)
+    return set_error(SFMM_EUNSUPPORTED, "plan_from_points: helmholtz2d has no device path");
+  if (kernel < 0 || kernel > 3) return set_error(SFMM_EINVAL, "plan_from_points: bad kernel id");
+  if (dim != (kernel == SFMM_LAPLACE2D ? 2 : 3))
+    return set_error(SFMM_EINVAL, "plan_from_points: kernel dimension mismatch");
+  if (kernel == SFMM_HELMHOLTZ3D && !(kappa > 0))
+    return set_error(SFMM_EINVAL, "plan_from_points: wavenumber must be positive");
+  sfmm_gpu_tree* tree = nullptr;
+  int rc = sfmm_gpu_build_tree(dim, n, pts, leaf_cap, device, &tree);
+  if (rc != SFMM_OK) return rc;
+  sfmm_tree_arrays ta{};
+  sfmm_gpu_tree_arrays(tree, &ta);
+  sfmm_tree_desc td{};
+  td.dim = ta.dim;
+  td.n_points = ta.n_points;
+  td.n_boxes = ta.n_boxes;
+  td.depth = ta.depth;
+  td.pts = ta.pts;
+  td.level_begin = ta.level_begin;
+  td.box_parent = ta.box_parent;
+  td.box_level = ta.box_level;
+  td.box_begin = ta.box_begin;
+  td.box_end = ta.box_end;
+  td.box_leaf = ta.box_leaf;
+  td.box_center = ta.box_center;
+  td.box_half = ta.box_half;
+  sfmm_skel_result* skel = nullptr;
+  rc = sfmm_gpu_build_skeletons(&td, kernel, kappa, tol, proxy_radius, proxy_edge2d, proxy_face3d,
+                                device, &skel);
+  if (rc == SFMM_OK) {
+    sfmm_plan_desc d{};
+    d.kernel = kernel;
+    d.dim = dim;
+    d.kappa = kappa;
+    d.n_points = ta.n_points;
+    d.n_boxes = ta.n_boxes;
+    d.depth = ta.depth;
+    d.pts = ta.pts;
+    d.perm = ta.perm;
+    d.level_begin = ta.level_begin;
+    d.box_parent = ta.box_parent;
+    d.box_level = ta.box_level;
+    d.box_begin = ta.box_begin;
+    d.box_end = ta.box_end;
+    d.box_leaf = ta.box_leaf;
+    d.coll_off = ta.coll_off;
+    d.coll = ta.coll;
+    d.coarse_off = ta.coarse_off;
+    d.coarse = ta.coarse;
+    d.fine_off = ta.fine_off;
+    d.fine = ta.fine;
+    // skeleton fields (T stays on the device and is copied device-to-device)
+    rc = sfmm_gpu_skel_describe(skel, &d, 0, nullptr, nullptr, nullptr, nullptr);
+    if (rc == SFMM_OK) rc = sfmm_gpu_plan_create_skel(&d, skel, device, 1, 0, out);
+    sfmm_gpu_skel_destroy(skel);
+  }
+  sfmm_gpu_tree_destroy(tree);
+  return rc;
+}
+
 }  // extern "C"

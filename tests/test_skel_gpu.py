@@ -115,3 +115,28 @@ def test_device_resident_operators(kernel, dist, n, kappa):
     # and the operators are the skeletonizer's: accurate against the dense sum
     t = np.arange(0, n, n // 100, dtype=np.int32)
     assert max_rel(u_dev[t], api.direct_sum_subset(kernel, kappa, pts, q, t)) <= 1e-5
+
+
+@pytest.mark.parametrize("kernel,dist,kappa", [(1, "cube", 1.0), (3, "sphere", 4.0), (0, "annulus", 1.0)])
+def test_plan_from_points_is_the_step_by_step_pipeline(kernel, dist, kappa):
+    """sfmm_gpu_plan_from_points (one C call) = GPU tree + GPU skeletons +
+    device-side plan, bit for bit."""
+    n = 30000
+    pts = host.generate_points(dist, n, 9)
+    q = host.generate_charges_complex(n, 1) if kernel == 3 else host.generate_charges(n, 1)
+    u1 = api.fmm_apply(api.GpuPlan.from_points(kernel, pts, 64, 1e-6, kappa), q)
+    hp = host.HostPlan.build_gpu(kernel, pts, 64, 1e-6, kappa, tree="gpu", host_T=False)
+    u2 = api.fmm_apply(api.GpuPlan.from_host(hp), q)
+    assert np.array_equal(u1, u2)
+
+
+def test_plan_from_points_errors():
+    pts = host.generate_points("cube", 1000, 1)
+    with pytest.raises(ValueError):
+        api.GpuPlan.from_points(0, pts, 40, 1e-6)           # laplace2d on 3D points
+    with pytest.raises(NotImplementedError):
+        api.GpuPlan.from_points(2, pts[:, :2].copy(), 40, 1e-6)  # helmholtz2d
+    dup = pts.copy()
+    dup[5] = dup[77]
+    with pytest.raises(api.DuplicatePointError):
+        api.GpuPlan.from_points(1, dup, 40, 1e-6)
