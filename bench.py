@@ -196,7 +196,7 @@ def run_reference(args, ws, rank):
     emit({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference generators, seed 1)",
         "config": {"workload": f"{args.kernel} {args.dist} N={n:.0e} leaf={args.leaf} "
                                f"tol={args.tol} nrhs=1", "headline_n": int(args.n)},
