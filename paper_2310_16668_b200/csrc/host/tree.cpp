@@ -298,7 +298,7 @@ Tree build_tree(int dim, int64_t n, const double* pts, int leaf_cap) {
   b.make_root();
   b.refine();
   mark("refine");
-  if (!std::getenv("SFMM_TREE_NO_BALANCE")) b.balance();  // debug aid: refinement only
+  b.balance();
   mark("balance");
   Tree t = b.finish();
   mark("finish");

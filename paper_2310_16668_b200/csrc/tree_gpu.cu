@@ -800,7 +800,6 @@ void build(int dim, int64_t n, const double* pts_host, int cap, sfmm_gpu_tree& R
         if (s.mask >> c & 1) h.child[c] = level_begin[l + 1] + s.first_child + r++;
     }
   R.perm.resize(n);
-  if (std::getenv("SFMM_TREE_NO_BALANCE")) seeds.clear();  // debug aid: refinement only
   if (!seeds.empty()) {
     // order-dependent splits: the reference's sequential queue on the host
     perm.download(R.perm.data(), n);
