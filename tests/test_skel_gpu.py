@@ -140,3 +140,19 @@ def test_plan_from_points_errors():
     dup[5] = dup[77]
     with pytest.raises(api.DuplicatePointError):
         api.GpuPlan.from_points(1, dup, 40, 1e-6)
+
+
+def test_saturated_skeletons_small_proxy():
+    """A coarse proxy surface (4 x 4 per face: 56 rows) at a tight tolerance:
+    ranks hit the row count (saturated boxes, skeleton.cpp's k == rows case);
+    the operators still give the oracle's apply exactly."""
+    n = 20000
+    pts = host.generate_points("cube", n, 4)
+    hp = host.HostPlan.build_gpu(1, pts, 200, 1e-12, proxy=(0.0, 0, 4))
+    inf = hp.info()
+    assert inf["saturated_boxes"] > 0 and inf["k_max"] == 56
+    d = hp.descriptor()
+    q = host.generate_charges(n, 5)
+    u = api.fmm_apply(api.GpuPlan(d), q)
+    u_ref, _ = po.oracle_apply(d, q)
+    assert rel_l2(u, u_ref) <= 1e-12
