@@ -555,8 +555,11 @@ __device__ __forceinline__ void task_cplx(const K2Args& a, const Task& t, WarpSm
   }
 }
 
+#ifndef SFMM_K2C_MIN_BLOCKS
+#define SFMM_K2C_MIN_BLOCKS 4
+#endif
 template <bool TAB>
-__global__ void __launch_bounds__(kThreads, 4) k2_translate_cplx(K2Args a) {
+__global__ void __launch_bounds__(kThreads, SFMM_K2C_MIN_BLOCKS) k2_translate_cplx(K2Args a) {
   __shared__ WarpSmemCplx smem[kWarps];
   __shared__ double2 tab[kSinCosTab];
   if (TAB)
