@@ -1,0 +1,63 @@
+"""Projected strong scaling of the sharded apply from one GPU.
+
+Each rank's share of one apply (begin: gather, upward pass, pack, interior
+translations; end: unpack, boundary translations, K2b, downward pass, scatter)
+is timed alone on the device with CUDA events, on buffers already holding a
+complete exchange.  On N GPUs the step takes about the slowest rank's time
+plus the ghost all-to-all, which SURVEY.md 8e estimates at <0.1 % of the step
+over NVLink; it is not included.  Usage: python tools/dev_scaling_projection.py [N]
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2310_16668_b200 import api, host, shard  # noqa: E402
+
+n = int(float(sys.argv[1])) if len(sys.argv) > 1 else 10_000_000
+pts = host.generate_points("cube", n, 1)
+hp = host.HostPlan.build_gpu(1, pts, 128, 1e-6, tree="gpu")
+q = host.generate_charges(n, 1)
+qd = torch.from_numpy(q).cuda()
+ud = torch.zeros_like(qd)
+s = torch.cuda.Stream()
+
+single = api.GpuPlan(hp.desc_struct())
+for _ in range(2):
+    api.fmm_apply_device(single, qd.data_ptr(), ud.data_ptr(), 1, s.cuda_stream)
+s.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record(s)
+for _ in range(5):
+    api.fmm_apply_device(single, qd.data_ptr(), ud.data_ptr(), 1, s.cuda_stream)
+e1.record(s)
+s.synchronize()
+t1 = e0.elapsed_time(e1) / 5
+single.close()
+print(f"N={n:.0e}  1 GPU (single plan, graph replay): {t1:.2f} ms")
+
+for nr in (2, 4, 8):
+    plans = [shard.ShardedPlan(hp.desc_struct(), nr, r) for r in range(nr)]
+    shard.apply_virtual(plans, qd, ud)  # fills every rank's receive buffer once
+    torch.cuda.synchronize()
+    times = []
+    for p in plans:
+        with torch.cuda.stream(s):
+            for _ in range(2):
+                p.begin(qd, s.cuda_stream, 0)
+                p.end(qd, ud, s.cuda_stream)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            for _ in range(3):
+                p.begin(qd, s.cuda_stream, 0)
+                p.end(qd, ud, s.cuda_stream)
+            b.record(s)
+        s.synchronize()
+        times.append(a.elapsed_time(b) / 3)
+    tmax = max(times)
+    print(f"{nr} ranks: per-rank ms {np.round(times, 2).tolist()}  max {tmax:.2f}  "
+          f"projected speed-up {t1 / tmax:.2f}x  efficiency {t1 / (nr * tmax):.3f}", flush=True)
+    for p in plans:
+        p.close()
