@@ -48,16 +48,22 @@ for nr in (2, 4, 8):
             for _ in range(2):
                 p.begin(qd, s.cuda_stream, 0)
                 p.end(qd, ud, s.cuda_stream)
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(s)
-            for _ in range(3):
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
+            ev[0].record(s)
+            for i in range(3):
                 p.begin(qd, s.cuda_stream, 0)
+                ev[1 + 2 * i].record(s)
                 p.end(qd, ud, s.cuda_stream)
-            b.record(s)
+                ev[2 + 2 * i].record(s)
         s.synchronize()
-        times.append(a.elapsed_time(b) / 3)
-    tmax = max(times)
-    print(f"{nr} ranks: per-rank ms {np.round(times, 2).tolist()}  max {tmax:.2f}  "
+        tb = np.mean([ev[2 * i].elapsed_time(ev[1 + 2 * i]) for i in range(3)])
+        te = np.mean([ev[1 + 2 * i].elapsed_time(ev[2 + 2 * i]) for i in range(3)])
+        times.append((tb + te, tb, te))
+    tmax = max(t[0] for t in times)
+    print(f"{nr} ranks: per-rank ms (begin+end) {[round(t[0], 2) for t in times]}  max {tmax:.2f}  "
           f"projected speed-up {t1 / tmax:.2f}x  efficiency {t1 / (nr * tmax):.3f}", flush=True)
+    print(f"   begin (gather, upward, pack, interior K2) {[round(t[1], 2) for t in times]}", flush=True)
+    print(f"   end (unpack, boundary K2, K2b, downward, scatter) {[round(t[2], 2) for t in times]}",
+          flush=True)
     for p in plans:
         p.close()
