@@ -555,7 +555,10 @@ void run_skeletons(const sfmm_tree_desc& t, int kernel, double kappa, double tol
     DevBuf<double> d_T;
   };
   std::vector<Level> L(depth + 1);
-  const size_t work_cap = (size_t)12 << 30;  // bytes of proxy-matrix workspace per batch
+#ifndef SFMM_SKEL_WORK_GB
+#define SFMM_SKEL_WORK_GB 12
+#endif
+  const size_t work_cap = (size_t)SFMM_SKEL_WORK_GB << 30;  // proxy-matrix workspace per batch
   DevBuf<double> d_work;
   const bool verbose = std::getenv("SFMM_SKEL_VERBOSE") != nullptr;
   auto now = [] { return std::chrono::steady_clock::now(); };
