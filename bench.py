@@ -238,8 +238,8 @@ def _load_descriptor(path):
 
 def run_sharded(args, ws, rank, local):
     """--gpus N under torchrun: strong scaling of the N=1e7 headline apply over
-    N ranks, whole level-1 subtrees per rank, ghost all-to-all over NCCL
-    overlapped with the interior translations."""
+    N ranks, whole level-1 subtrees per rank, ghost all-to-all over NCCL after
+    the upward pass, one translation launch."""
     import shutil
 
     import torch

@@ -164,12 +164,13 @@ void sfmm_gpu_plan_destroy(sfmm_gpu_plan* plan);
  * apply is
  *   sfmm_gpu_apply_begin   gather + upward pass of the owned subtrees, pack the
  *                          ghost boxes other ranks read (q and qhat) into
- *                          send_dev, record `packed_event`, then start the
- *                          translation tasks that read no ghost box;
+ *                          send_dev, record `packed_event` (with
+ *                          SFMM_SHARD_OVERLAP=1 it then also starts the
+ *                          translation tasks that read no ghost box);
  *   (caller)               all-to-all of send_dev -> recv_dev with the per-peer
  *                          counts of sfmm_gpu_shard_info (scalars; NCCL over
- *                          NVLink, overlapped with the interior translations);
- *   sfmm_gpu_apply_end     unpack ghosts, boundary translation tasks, staged
+ *                          NVLink);
+ *   sfmm_gpu_apply_end     unpack ghosts, the (remaining) translation tasks, staged
  *                          column sums, downward pass, scatter of the OWNED
  *                          points into u_dev (other entries untouched).
  * q_dev holds all N charges (original order) on every rank.  The union over

@@ -38,6 +38,7 @@ PlanOptions plan_options_from_env() {
   PlanOptions o;
   if (const char* v = std::getenv("SFMM_SYMMETRIC")) o.symmetric = std::atoi(v) != 0;
   if (const char* v = std::getenv("SFMM_SKIP_CANCEL")) o.skip_cancel = std::atoi(v) != 0;
+  if (const char* v = std::getenv("SFMM_SHARD_OVERLAP")) o.overlap = std::atoi(v) != 0;
   return o;
 }
 
@@ -524,7 +525,8 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
             inbox[c].push_back({u_off, h_off});
           }
           const double lanes_rows = 32.0 * ((t.nrows + 31) / 32);
-          (boundary[b] ? tv_bnd : tv_int).push_back({lanes_rows * (src + 8.0), t});
+          // without overlap every task runs in the one launch after the exchange
+          ((boundary[b] || !opt.overlap) ? tv_bnd : tv_int).push_back({lanes_rows * (src + 8.0), t});
         }
       }
       hp.stage_size = cursor;

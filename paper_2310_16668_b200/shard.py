@@ -4,12 +4,13 @@ Every rank builds a sharded plan from the same full descriptor
 (``sfmm_gpu_plan_create_sharded``).  An apply is
 
     begin   gather + upward pass of the owned subtrees, pack the ghost boxes
-            (q and qhat) other ranks read, start the interior translations;
+            (q and qhat) other ranks read;
     exchange  all-to-all of the packed ghosts (NCCL over NVLink via
-            torch.distributed, on a side stream, overlapped with the interior
-            translation tasks);
-    end     unpack, boundary translations, staged column sums, downward pass,
-            scatter of the owned points.
+            torch.distributed, on a side stream);
+    end     unpack, the translation tasks (one launch), staged column sums,
+            downward pass, scatter of the owned points.
+(With SFMM_SHARD_OVERLAP=1, begin also starts the tasks that read no ghost box
+so they overlap the exchange; measured slower.)
 
 The reference is single-process (SPEC.md non-goal "distributed trees"); this is
 the B200-native extension described in SURVEY.md 8(e) and DESIGN.md 6.
@@ -139,7 +140,7 @@ def _work_stream(stream, device):
 
 def apply_distributed(plan: ShardedPlan, q_dev, u_dev, stream=None, comm_stream=None) -> None:
     """One sharded apply with the ghost all-to-all on torch.distributed (NCCL),
-    overlapped with the interior translation tasks.  u_dev receives the owned
+    after the upward pass (overlapping the interior tasks with SFMM_SHARD_OVERLAP=1).  u_dev receives the owned
     points (other entries untouched)."""
     import torch
     import torch.distributed as dist
