@@ -295,17 +295,25 @@ def run_sharded(args, ws, rank, local):
     comm = torch.cuda.Stream(dev)
     if args.backend != "nccl":
         # test path (several ranks on one GPU): exchange through host memory
-        def exchange_apply():
-            send, recv = plan.buffers()
-            plan.begin(q_dev, stream.cuda_stream, 0)
+        def host_exchange(bufs, send_counts, recv_counts):
+            send, recv = bufs
             stream.synchronize()
-            s_cpu = send[: int(plan.send_counts.sum())].cpu()
-            r_cpu = torch.empty(int(plan.recv_counts.sum()), dtype=torch.float64)
-            dist.all_to_all_single(r_cpu, s_cpu, output_split_sizes=[int(x) for x in plan.recv_counts],
-                                   input_split_sizes=[int(x) for x in plan.send_counts])
+            s_cpu = send[: int(send_counts.sum())].cpu()
+            r_cpu = torch.empty(int(recv_counts.sum()), dtype=torch.float64)
+            dist.all_to_all_single(r_cpu, s_cpu, output_split_sizes=[int(x) for x in recv_counts],
+                                   input_split_sizes=[int(x) for x in send_counts])
             recv[: r_cpu.numel()].copy_(r_cpu)
             torch.cuda.synchronize(dev)
-            plan.end(q_dev, u_dev, stream.cuda_stream)
+
+        def exchange_apply():
+            plan.begin(q_dev, stream.cuda_stream, 0)
+            host_exchange(plan.buffers(), plan.send_counts, plan.recv_counts)
+            if plan.cross_symmetric:
+                plan.mid(stream.cuda_stream)
+                host_exchange(plan.buffers2(), plan.send2_counts, plan.recv2_counts)
+                plan.fin(q_dev, u_dev, stream.cuda_stream)
+            else:
+                plan.end(q_dev, u_dev, stream.cuda_stream)
     else:
         def exchange_apply():
             shard.apply_distributed(plan, q_dev, u_dev, stream=stream, comm_stream=comm)
@@ -404,7 +412,8 @@ def run_sharded(args, ws, rank, local):
             "relerr_vs_single_gpu": relerr_single,
             "shard": {"ghost_boxes_rank0": plan.n_ghost_boxes,
                       "owned_points_rank0": plan.n_owned_points,
-                      "send_mb_rank0": float(plan.send_counts.sum()) * 8 / 1e6},
+                      "send_mb_rank0": float(plan.send_counts.sum()) * 8 / 1e6,
+                      "send2_mb_rank0": float(plan.send2_counts.sum()) * 8 / 1e6},
             "precompute": {"t_total_s": t_pre, "t_upload_s": t_upload, **{k: hinfo.get(k) for k in
                            ("depth", "n_boxes", "k_max", "t_tree", "t_skel")}},
             "cpu_baseline": {"value": None, "unit": UNIT, "cores": None, "kind": "reference",

@@ -173,6 +173,17 @@ void sfmm_gpu_plan_destroy(sfmm_gpu_plan* plan);
  *   sfmm_gpu_apply_end     unpack ghosts, the (remaining) translation tasks, staged
  *                          column sums, downward pass, scatter of the OWNED
  *                          points into u_dev (other entries untouched).
+ * Symmetric plans (the default) evaluate a colleague pair split across two
+ * ranks once, on one side, and return the other side's column sums in a
+ * second exchange; sfmm_gpu_shard_info2 returns 1 and its per-peer counts,
+ * and apply_end is replaced by
+ *   sfmm_gpu_apply_mid     unpack ghosts, the (remaining) translation tasks,
+ *                          pack the column sums owed to each peer into
+ *                          send2_dev, record `packed_event`;
+ *   (caller)               all-to-all of send2_dev -> recv2_dev (shard_info2
+ *                          counts);
+ *   sfmm_gpu_apply_fin     add the staged and received column sums, downward
+ *                          pass, scatter of the owned points into u_dev.
  * q_dev holds all N charges (original order) on every rank.  The union over
  * ranks of the owned entries of u is the full result.  Trees with depth < 2
  * are computed by rank 0 alone.  Replaces nothing in the reference, which is
@@ -186,10 +197,18 @@ int sfmm_gpu_apply_begin(sfmm_gpu_plan* plan, const void* q_dev, void* send_dev,
                          void* packed_event);
 int sfmm_gpu_apply_end(sfmm_gpu_plan* plan, const void* q_dev, const void* recv_dev, void* u_dev,
                        void* stream);
+/* Returns 1 when the plan has the second exchange (apply_mid/_fin), else 0;
+ * fills the per-peer scalar counts of that exchange (zeros when absent). */
+int sfmm_gpu_shard_info2(const sfmm_gpu_plan* plan, int64_t* send2_counts, int64_t* recv2_counts);
+int sfmm_gpu_apply_mid(sfmm_gpu_plan* plan, const void* recv_dev, void* send2_dev, void* stream,
+                       void* packed_event);
+int sfmm_gpu_apply_fin(sfmm_gpu_plan* plan, const void* q_dev, const void* recv2_dev, void* u_dev,
+                       void* stream);
 
 /* Host-only view of rank `rank`'s shard (no device is touched).  counts gets
- * 2*n_ranks + 3 values: send scalars per peer, receive scalars per peer,
- * owned points, ghost boxes, owned boxes.  Non-NULL arrays receive the box
+ * 4*n_ranks + 3 values: send scalars per peer, receive scalars per peer,
+ * owned points, ghost boxes, owned boxes, then the second exchange's send and
+ * receive scalars per peer.  Non-NULL arrays receive the box
  * owners (n_boxes), the ghost-exchange element indices into [q slots | qhat]
  * (pack_idx: what this rank sends, per peer in rank order; unpack_idx: where
  * what it receives lands) and the owned points' original indices. */

@@ -315,6 +315,12 @@ def gpu_lib() -> C.CDLL:
     lib.sfmm_gpu_apply_begin.restype = C.c_int
     lib.sfmm_gpu_apply_end.argtypes = [vp, vp, vp, vp, vp]
     lib.sfmm_gpu_apply_end.restype = C.c_int
+    lib.sfmm_gpu_shard_info2.argtypes = [vp, vp, vp]
+    lib.sfmm_gpu_shard_info2.restype = C.c_int
+    lib.sfmm_gpu_apply_mid.argtypes = [vp, vp, vp, vp, vp]
+    lib.sfmm_gpu_apply_mid.restype = C.c_int
+    lib.sfmm_gpu_apply_fin.argtypes = [vp, vp, vp, vp, vp]
+    lib.sfmm_gpu_apply_fin.restype = C.c_int
     lib.sfmm_gpu_shard_describe.argtypes = [C.POINTER(PlanDesc), C.c_int, C.c_int, vp, vp, vp, vp,
                                             vp]
     lib.sfmm_gpu_shard_describe.restype = C.c_int
@@ -360,4 +366,5 @@ GPU_SYMBOLS = [
     "sfmm_gpu_test_sincos", "sfmm_gpu_skel_describe", "sfmm_gpu_skel_device_T",
     "sfmm_gpu_plan_create_skel", "sfmm_gpu_build_tree", "sfmm_gpu_tree_arrays",
     "sfmm_gpu_tree_destroy", "sfmm_gpu_test_log", "sfmm_gpu_plan_from_points",
+    "sfmm_gpu_shard_info2", "sfmm_gpu_apply_mid", "sfmm_gpu_apply_fin",
 ]

@@ -669,7 +669,8 @@ int configure_translate(DevPlan& p, int device) {
   return 0;
 }
 
-void launch_translate(const DevPlan& p, DevState& s, cudaStream_t st, TranslatePart part) {
+void launch_translate(const DevPlan& p, DevState& s, cudaStream_t st, TranslatePart part,
+                      bool reduce) {
   const size_t sw = p.cplx ? 16 : 8;
   if (part != kBoundaryTasks) {
     // boxes whose every entry cancels own no task: their U/UH stay zero
@@ -716,11 +717,15 @@ void launch_translate(const DevPlan& p, DevState& s, cudaStream_t st, TranslateP
     else
       k2_translate_real<GenLaplace2d><<<grid, kThreads, 0, st>>>(a);
   }
-  if (part != kInteriorTasks && p.n_recv > 0 && p.cplx) {
+  if (part != kInteriorTasks && reduce) launch_stage_reduce(p, s, st);
+}
+
+void launch_stage_reduce(const DevPlan& p, DevState& s, cudaStream_t st) {
+  if (p.n_recv > 0 && p.cplx) {
     k2b_reduce_cplx<<<(unsigned)p.n_recv, 256, 0, st>>>(
         p.box, p.recv_box, p.recv_off, p.recv_u, p.recv_h, reinterpret_cast<const double2*>(p.stage),
         reinterpret_cast<double2*>(s.U), reinterpret_cast<double2*>(s.UH), 0.25);
-  } else if (part != kInteriorTasks && p.n_recv > 0) {
+  } else if (p.n_recv > 0) {
     const double scale = p.kernel == SFMM_LAPLACE3D ? GenLaplace3d::kScale : GenLaplace2d::kScale;
     k2b_reduce<<<(unsigned)p.n_recv, 256, 0, st>>>(p.box, p.recv_box, p.recv_off, p.recv_u,
                                                    p.recv_h, p.stage, s.U, s.UH, scale);

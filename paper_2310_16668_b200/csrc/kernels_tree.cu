@@ -467,7 +467,47 @@ __global__ void k_exchange(const int64_t* __restrict__ idx, int64_t n, int64_t n
   }
 }
 
+__device__ __forceinline__ double xadd(double a, double b) { return a + b; }
+__device__ __forceinline__ double2 xadd(double2 a, double2 b) {
+  return make_double2(a.x + b.x, a.y + b.y);
+}
+
+// Second exchange: one CTA per cross-rank pair sums the pair's staged column
+// sums over its row tiles (fixed tile order) into the send buffer.
+template <class S>
+__global__ void __launch_bounds__(256) k_xpack(const int64_t* __restrict__ tile_off,
+                                               const int64_t* __restrict__ tile_u,
+                                               const int64_t* __restrict__ tile_h,
+                                               const int64_t* __restrict__ dst,
+                                               const int32_t* __restrict__ nu,
+                                               const int32_t* __restrict__ nh,
+                                               const S* __restrict__ St, S* __restrict__ buf) {
+  const int64_t i = blockIdx.x, t0 = tile_off[i], t1 = tile_off[i + 1];
+  const int n_u = nu[i], n = n_u + nh[i];
+  S* out = buf + dst[i];
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    S s = S{};
+    for (int64_t t = t0; t < t1; ++t) {
+      const int64_t o = j < n_u ? tile_u[t] + j : (tile_h[t] >= 0 ? tile_h[t] + (j - n_u) : -1);
+      if (o >= 0) s = xadd(s, St[o]);
+    }
+    out[j] = s;
+  }
+}
+
 }  // namespace
+
+void launch_xpack(const DevPlan& p, double* buf, cudaStream_t st) {
+  if (p.n_xpairs == 0) return;
+  if (p.cplx)
+    k_xpack<double2><<<(unsigned)p.n_xpairs, 256, 0, st>>>(
+        p.xpair_tile_off, p.xtile_u, p.xtile_h, p.xpair_dst, p.xpair_nu, p.xpair_nh,
+        reinterpret_cast<const double2*>(p.stage), reinterpret_cast<double2*>(buf));
+  else
+    k_xpack<double><<<(unsigned)p.n_xpairs, 256, 0, st>>>(p.xpair_tile_off, p.xtile_u, p.xtile_h,
+                                                           p.xpair_dst, p.xpair_nu, p.xpair_nh,
+                                                           p.stage, buf);
+}
 
 void launch_pack(const DevPlan& p, const DevState& s, double* buf, cudaStream_t st) {
   if (p.n_pack == 0) return;

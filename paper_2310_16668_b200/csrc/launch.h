@@ -49,6 +49,12 @@ struct DevPlan {
   int64_t* pack_idx;    // ghost exchange element indices into [Q | QH]
   int64_t* unpack_idx;
   int64_t n_pack, n_unpack;
+  // cross-rank symmetric pairs (HostPlan::xsym): the second exchange
+  int64_t *xpair_tile_off, *xtile_u, *xtile_h, *xpair_dst;
+  int32_t *xpair_nu, *xpair_nh;
+  int64_t n_xpairs;
+  int64_t stage_size;      // local staging; received column sums follow it
+  int64_t n_send2, n_recv2;
   int64_t n_owned_points;  // entries of leaf_slot / leaf_orig
   // multi-RHS path (kernels_multi.cu)
   EntryRange* ent_range_full;
@@ -73,7 +79,12 @@ void launch_upward(const DevPlan& p, const HostPlan& hp, int level, DevState& s,
 // interior / boundary halves of a sharded plan), followed by K2b
 enum TranslatePart { kAllTasks, kInteriorTasks, kBoundaryTasks };
 void launch_translate(const DevPlan& p, DevState& s, cudaStream_t st,
-                      TranslatePart part = kAllTasks);
+                      TranslatePart part = kAllTasks, bool reduce = true);
+// K2b alone (after the second exchange of a cross-symmetric sharded plan)
+void launch_stage_reduce(const DevPlan& p, DevState& s, cudaStream_t st);
+// second exchange: buf[xpair_dst[i] + j] = sum over the pair's row tiles of
+// the staged column sums (u part, then h part)
+void launch_xpack(const DevPlan& p, double* buf, cudaStream_t st);
 // ghost exchange: buf[i] = [Q | QH][pack_idx[i]]  /  [Q | QH][unpack_idx[i]] = buf[i]
 void launch_pack(const DevPlan& p, const DevState& s, double* buf, cudaStream_t st);
 void launch_unpack(const DevPlan& p, DevState& s, const double* buf, cudaStream_t st);

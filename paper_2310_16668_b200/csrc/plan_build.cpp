@@ -39,6 +39,7 @@ PlanOptions plan_options_from_env() {
   if (const char* v = std::getenv("SFMM_SYMMETRIC")) o.symmetric = std::atoi(v) != 0;
   if (const char* v = std::getenv("SFMM_SKIP_CANCEL")) o.skip_cancel = std::atoi(v) != 0;
   if (const char* v = std::getenv("SFMM_SHARD_OVERLAP")) o.overlap = std::atoi(v) != 0;
+  if (const char* v = std::getenv("SFMM_SHARD_XSYM")) o.cross_symmetric = std::atoi(v) != 0;
   return o;
 }
 
@@ -362,6 +363,45 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
     }
 
     ptime("pair counts");
+    // Cross-rank colleague pairs (xsym): each is evaluated by one of its two
+    // owners.  The choice balances the ranks' estimated K2 work (dense pairs;
+    // a folded pair costs ~1.15 of one direction): a greedy pass over the
+    // pairs in (b < c) order gives each to the currently lighter rank.  It
+    // depends only on the descriptor, so every rank derives the same choice.
+    hp.xsym = hp.symmetric && n_ranks > 1 && opt.cross_symmetric;
+    std::vector<uint8_t> xev;  // per colleague entry (b -> c): b's owner evaluates
+    auto coll_entry = [&](int32_t b, int32_t c) {
+      const int32_t* cb = d.coll + d.coll_off[b];
+      const int32_t* ce = d.coll + d.coll_off[b + 1];
+      return d.coll_off[b] + (int64_t)(std::lower_bound(cb, ce, c) - cb);
+    };
+    if (hp.xsym) {
+      xev.assign(d.coll_off[nb], 0);
+      std::vector<double> load(n_ranks, 0.0);
+      for (int32_t b = 0; b < nb; ++b) {
+        if (d.box_level[b] < 1) continue;
+        const double nbn = hp.box[b].n;
+        sources(b, [&](int32_t c, int mode) {
+          if (mode == kIFO && hp.owner[c] != hp.owner[b]) return;
+          const double w = (mode == kIFO && c != b) ? 0.575 : 1.0;
+          load[hp.owner[b]] += w * nbn * hp.box[c].n;
+        });
+      }
+      for (int32_t b = hp.level_begin[2]; b < nb; ++b)
+        sources(b, [&](int32_t c, int mode) {
+          if (mode != kIFO || c < b || hp.owner[c] == hp.owner[b]) return;
+          const int rb = hp.owner[b], rc = hp.owner[c];
+          const bool at_b = load[rb] <= load[rc];
+          load[at_b ? rb : rc] += 1.15 * hp.box[b].n * hp.box[c].n;
+          xev[coll_entry(b, c)] = at_b ? 1 : 0;
+          xev[coll_entry(c, b)] = at_b ? 0 : 1;
+        });
+    }
+    auto evaluates = [&](int32_t b, int32_t c) { return xev[coll_entry(b, c)] != 0; };
+    // cross-rank colleague pair (b, c) that b's owner does not evaluate
+    auto folded_away = [&](int32_t b, int32_t c, int mode) {
+      return hp.xsym && mode == kIFO && hp.owner[b] != hp.owner[c] && !evaluates(b, c);
+    };
     // this rank's CSR: owned targets only
     hp.ent_range.resize(nb);
     std::vector<uint8_t> boundary(nb, 0);
@@ -371,6 +411,13 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
       er.count = 0;
       if (!mine(b) || d.box_level[b] < 1) continue;
       sources(b, [&](int32_t c, int mode) {
+        if (mode == kIFO && hp.xsym && !mine(c)) {
+          if (evaluates(b, c)) {  // evaluated here; c's side goes back to its owner
+            hp.entries.push_back((c << kModeBits) | kSYM);
+            boundary[b] = 1;
+          }
+          return;  // otherwise c's owner evaluates it and sends b's column sums
+        }
         if (!mine(c)) boundary[b] = 1;
         if (mode == kIFO && hp.symmetric && c != b && mine(c)) {
           if (c > b) hp.entries.push_back((c << kModeBits) | kSYM);
@@ -429,8 +476,8 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
       for (int32_t b = 0; b < nb; ++b) {
         if (d.box_level[b] < 1) continue;
         const int q = hp.owner[b];
-        sources(b, [&](int32_t c, int) {
-          if (hp.owner[c] != q) need[q][c] = 1;
+        sources(b, [&](int32_t c, int mode) {
+          if (hp.owner[c] != q && !folded_away(b, c, mode)) need[q][c] = 1;
         });
       }
       hp.send_off.assign(n_ranks + 1, 0);
@@ -504,13 +551,24 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
 #endif
       if (hp.cplx) tile = std::min(tile, kTileRows / 2);  // complex K2: <= 2 rows per lane
       hp.tile_rows = tile;
+      // outgoing cross-rank pairs in (b, entry) order, the staged tiles of each
+      std::vector<std::pair<int32_t, int32_t>> xpairs;
+      std::vector<std::vector<std::pair<int64_t, int64_t>>> xtiles;
       for (int32_t b = 0; b < nb; ++b) {
         const EntryRange& er = hp.ent_range[b];
+        const size_t x0 = xpairs.size();
+        for (int64_t e = er.begin; e < er.begin + er.count; ++e) {
+          const int32_t code = hp.entries[e];
+          if ((code & kModeMask) == kSYM && !mine(code >> kModeBits))
+            xpairs.push_back({b, code >> kModeBits});
+        }
+        xtiles.resize(xpairs.size());
         if (er.count == 0 || hp.box[b].n == 0) continue;
         const double src = src_of[b];
         for (int32_t r0 = 0; r0 < hp.box[b].n; r0 += tile) {
           Task t{b, r0, std::min(tile, hp.box[b].n - r0), 0, cursor};
           const bool skel_rows = r0 < hp.box[b].k;
+          size_t xi = x0;
           for (int64_t e = er.begin; e < er.begin + er.count; ++e) {
             const int32_t code = hp.entries[e];
             if ((code & kModeMask) != kSYM) continue;
@@ -522,7 +580,10 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
               h_off = cursor;
               cursor += hp.box[c].k;
             }
-            inbox[c].push_back({u_off, h_off});
+            if (mine(c))
+              inbox[c].push_back({u_off, h_off});
+            else
+              xtiles[xi++].push_back({u_off, h_off});
           }
           const double lanes_rows = 32.0 * ((t.nrows + 31) / 32);
           // without overlap every task runs in the one launch after the exchange
@@ -530,6 +591,69 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
         }
       }
       hp.stage_size = cursor;
+      // Second exchange: one vector per (peer, receiving box c) -- the column
+      // sums of every pair (b, c) this rank evaluated, summed over b and b's
+      // row tiles by k_xpack -- in ascending c per peer.  The receiver rebuilds
+      // the list from the global tree.  The h part exists iff some pair of the
+      // group has skeletons on both sides.
+      if (hp.xsym) {
+        auto has_h = [&](int32_t b, int32_t c) { return hp.box[b].k > 0 && hp.box[c].k > 0; };
+        std::vector<int32_t> ord(xpairs.size());
+        std::iota(ord.begin(), ord.end(), 0);
+        std::stable_sort(ord.begin(), ord.end(), [&](int32_t x, int32_t y) {
+          const int32_t cx = xpairs[x].second, cy = xpairs[y].second;
+          if (hp.owner[cx] != hp.owner[cy]) return hp.owner[cx] < hp.owner[cy];
+          return cx < cy;
+        });
+        hp.send2_off.assign(n_ranks + 1, 0);
+        hp.recv2_off.assign(n_ranks + 1, 0);
+        hp.xpair_tile_off.assign(1, 0);
+        int64_t dst = 0;
+        for (size_t g = 0; g < ord.size();) {
+          const int32_t c = xpairs[ord[g]].second;
+          bool h = false;
+          for (; g < ord.size() && xpairs[ord[g]].second == c; ++g) {
+            h = h || has_h(xpairs[ord[g]].first, c);
+            for (auto& uh : xtiles[ord[g]]) {
+              hp.xtile_u.push_back(uh.first);
+              hp.xtile_h.push_back(uh.second);
+            }
+          }
+          const int32_t nh = h ? hp.box[c].k : 0;
+          hp.xpair_tile_off.push_back((int64_t)hp.xtile_u.size());
+          hp.xpair_dst.push_back(dst);
+          hp.xpair_nu.push_back(hp.box[c].n);
+          hp.xpair_nh.push_back(nh);
+          dst += hp.box[c].n + nh;
+          hp.send2_off[hp.owner[c] + 1] = dst;
+        }
+        for (int p = 0; p < n_ranks; ++p)
+          hp.send2_off[p + 1] = std::max(hp.send2_off[p + 1], hp.send2_off[p]);
+        int64_t src2 = 0;
+        for (int p = 0; p < n_ranks; ++p) {
+          if (p != rank)
+            for (int32_t c = hp.level_begin[2]; c < nb; ++c) {
+              if (!mine(c)) continue;
+              bool any = false, h = false;
+              for (int64_t e = d.coll_off[c]; e < d.coll_off[c + 1]; ++e) {
+                const int32_t b = d.coll[e];
+                if (hp.owner[b] != p || (unc[b] && unc[c]) || !evaluates(b, c)) continue;
+                any = true;
+                h = h || has_h(b, c);
+              }
+              if (!any) continue;
+              const int64_t u_off = hp.stage_size + src2;
+              src2 += hp.box[c].n;
+              int64_t h_off = -1;
+              if (h) {
+                h_off = hp.stage_size + src2;
+                src2 += hp.box[c].k;
+              }
+              inbox[c].push_back({u_off, h_off});
+            }
+          hp.recv2_off[p + 1] = src2;
+        }
+      }
 #ifndef SFMM_TASK_GROUP_R
 #define SFMM_TASK_GROUP_R 1
 #endif

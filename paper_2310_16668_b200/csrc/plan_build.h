@@ -79,6 +79,18 @@ struct HostPlan {
   // per peer ranges send_off[p]..send_off[p+1] / recv_off_peer[p]..
   std::vector<int64_t> pack_idx, unpack_idx, send_off, recv_off_peer;
   int64_t n_ghost_boxes = 0;
+  // cross-rank symmetric pairs (PlanOptions::cross_symmetric).  Sender side:
+  // group i (one receiving box c of one peer) sums the staged column sums of
+  // its pairs over their row tiles xtile_u/xtile_h[xpair_tile_off[i] ..
+  // xpair_tile_off[i+1]) (h: -1 = none) into the second send buffer at
+  // xpair_dst[i] ([u: xpair_nu | h: xpair_nh] scalars), per destination rank
+  // (send2_off).  Receiver side: the peer segments land at stage_size +
+  // recv2_off[p] in the staging buffer and are listed in recv_u/recv_h after
+  // the local column sums.
+  bool xsym = false;
+  std::vector<int64_t> xpair_tile_off, xtile_u, xtile_h, xpair_dst;
+  std::vector<int32_t> xpair_nu, xpair_nh;
+  std::vector<int64_t> send2_off, recv2_off;  // n_ranks + 1 each (scalars)
   // multi-RHS path: unfolded CSR (no kSYM), 16-row tasks, 16-column K3 items
   std::vector<EntryRange> ent_range_full;
   std::vector<int32_t> entries_full;
@@ -122,6 +134,11 @@ struct PlanOptions {
   // time, N=1e7): one launch 13.4 ms vs 15.9 ms at 8 ranks -- the second
   // launch's tail costs far more than the exposed exchange (~0.1 ms).
   bool overlap = false;
+  // sharded symmetric plans: a colleague pair split across two ranks is
+  // evaluated once, by one of the two owners (chosen to balance the ranks'
+  // work), which returns the other side's column sums in a second (smaller)
+  // exchange (SFMM_SHARD_XSYM=0: both ranks evaluate it, one exchange).
+  bool cross_symmetric = true;
 };
 PlanOptions plan_options_from_env();
 

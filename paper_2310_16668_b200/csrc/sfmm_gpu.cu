@@ -379,7 +379,18 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
       dp.up1_items = p->upload(hp.up1_items);
       dp.copy_boxes = p->upload(hp.copy_boxes);
       dp.down_items = p->upload(hp.down_items);
-      dp.stage = p->alloc<double>((size_t)std::max<int64_t>(hp.stage_size, 1) * sw);  // scalars
+      const int64_t n_recv2 = hp.recv2_off.empty() ? 0 : hp.recv2_off.back();
+      dp.stage_size = hp.stage_size;
+      dp.n_recv2 = n_recv2;
+      dp.n_send2 = hp.send2_off.empty() ? 0 : hp.send2_off.back();
+      dp.stage = p->alloc<double>((size_t)std::max<int64_t>(hp.stage_size + n_recv2, 1) * sw);
+      dp.n_xpairs = (int64_t)hp.xpair_dst.size();
+      dp.xpair_tile_off = p->upload(hp.xpair_tile_off);
+      dp.xtile_u = p->upload(hp.xtile_u);
+      dp.xtile_h = p->upload(hp.xtile_h);
+      dp.xpair_dst = p->upload(hp.xpair_dst);
+      dp.xpair_nu = p->upload(hp.xpair_nu);
+      dp.xpair_nh = p->upload(hp.xpair_nh);
       dp.n_recv = (int64_t)hp.recv_box.size();
       dp.recv_box = p->upload(hp.recv_box);
       dp.recv_off = p->upload(hp.recv_off);
@@ -491,6 +502,11 @@ int sfmm_gpu_shard_describe(const sfmm_plan_desc* desc, int n_ranks, int rank, i
   int64_t owned_boxes = 0;
   for (int32_t o : hp.owner) owned_boxes += o == rank ? 1 : 0;
   counts[2 * n_ranks + 2] = hp.depth < 2 ? (rank == 0 ? hp.n_boxes : 0) : owned_boxes;
+  const bool have2 = hp.send2_off.size() == (size_t)n_ranks + 1;
+  for (int r = 0; r < n_ranks; ++r) {
+    counts[2 * n_ranks + 3 + r] = have2 ? hp.send2_off[r + 1] - hp.send2_off[r] : 0;
+    counts[3 * n_ranks + 3 + r] = have2 ? hp.recv2_off[r + 1] - hp.recv2_off[r] : 0;
+  }
   if (owner && !hp.owner.empty()) std::copy(hp.owner.begin(), hp.owner.end(), owner);
   if (pack_idx) std::copy(hp.pack_idx.begin(), hp.pack_idx.end(), pack_idx);
   if (unpack_idx) std::copy(hp.unpack_idx.begin(), hp.unpack_idx.end(), unpack_idx);
@@ -534,30 +550,103 @@ int sfmm_gpu_apply_begin(sfmm_gpu_plan* p, const void* q_dev, void* send_dev, vo
   }
 }
 
+namespace {
+
+// apply_end = mid + fin; the second exchange in between exists only for
+// cross-symmetric sharded plans
+void apply_mid_impl(sfmm_gpu_plan* p, const void* recv_dev, void* send2_dev, cudaStream_t st) {
+  if (p->hp.depth < 2) return;
+  if (p->dp.n_unpack > 0) {
+    if (!recv_dev) throw CudaFail{SFMM_EINVAL, "receive buffer required"};
+    launch_unpack(p->dp, p->ds, static_cast<const double*>(recv_dev), st);
+  }
+  launch_translate(p->dp, p->ds, st, kBoundaryTasks, false);
+  if (p->dp.n_xpairs > 0) {
+    if (!send2_dev) throw CudaFail{SFMM_EINVAL, "second send buffer required"};
+    launch_xpack(p->dp, static_cast<double*>(send2_dev), st);
+  }
+}
+
+void apply_fin_impl(sfmm_gpu_plan* p, const void* q_dev, const void* recv2_dev, void* u_dev,
+                    cudaStream_t st) {
+  double* u = static_cast<double*>(u_dev);
+  if (p->hp.depth < 2) {
+    if (p->hp.rank == 0) launch_direct_fallback(p->dp, static_cast<const double*>(q_dev), u, st);
+    return;
+  }
+  if (p->dp.n_recv2 > 0) {
+    if (!recv2_dev) throw CudaFail{SFMM_EINVAL, "second receive buffer required"};
+    const size_t sw = p->dp.cplx ? 2 : 1;
+    ck(cudaMemcpyAsync(p->dp.stage + p->dp.stage_size * sw, recv2_dev,
+                       sizeof(double) * p->dp.n_recv2 * sw, cudaMemcpyDeviceToDevice, st),
+       "second exchange");
+  }
+  launch_stage_reduce(p->dp, p->ds, st);
+  for (int l = 2; l <= p->hp.depth; ++l) launch_downward(p->dp, p->hp, l, p->ds, st);
+  launch_scatter(p->dp, p->ds, u, st);
+}
+
+}  // namespace
+
 int sfmm_gpu_apply_end(sfmm_gpu_plan* p, const void* q_dev, const void* recv_dev, void* u_dev,
+                       void* stream) {
+  if (!p || !u_dev) return set_error(SFMM_EINVAL, "fmm_apply: bad arguments");
+  if (p->dp.n_xpairs > 0 || p->dp.n_recv2 > 0)
+    return set_error(SFMM_EINVAL,
+                     "fmm_apply: plan has a second exchange: use sfmm_gpu_apply_mid/_fin");
+  std::lock_guard<std::mutex> lock(p->mu);
+  try {
+    DeviceGuard device_guard(p->device);
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : p->stream;
+    apply_mid_impl(p, recv_dev, nullptr, st);
+    apply_fin_impl(p, q_dev, nullptr, u_dev, st);
+    ck(cudaGetLastError(), "kernel launch");
+    return SFMM_OK;
+  } catch (const CudaFail& f) {
+    return set_error(f.code, "fmm_apply: " + f.msg);
+  }
+}
+
+int sfmm_gpu_apply_mid(sfmm_gpu_plan* p, const void* recv_dev, void* send2_dev, void* stream,
+                       void* packed_event) {
+  if (!p) return set_error(SFMM_EINVAL, "fmm_apply: bad arguments");
+  std::lock_guard<std::mutex> lock(p->mu);
+  try {
+    DeviceGuard device_guard(p->device);
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : p->stream;
+    apply_mid_impl(p, recv_dev, send2_dev, st);
+    if (packed_event) ck(cudaEventRecord(static_cast<cudaEvent_t>(packed_event), st), "event");
+    ck(cudaGetLastError(), "kernel launch");
+    return SFMM_OK;
+  } catch (const CudaFail& f) {
+    return set_error(f.code, "fmm_apply: " + f.msg);
+  }
+}
+
+int sfmm_gpu_apply_fin(sfmm_gpu_plan* p, const void* q_dev, const void* recv2_dev, void* u_dev,
                        void* stream) {
   if (!p || !u_dev) return set_error(SFMM_EINVAL, "fmm_apply: bad arguments");
   std::lock_guard<std::mutex> lock(p->mu);
   try {
     DeviceGuard device_guard(p->device);
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : p->stream;
-    double* u = static_cast<double*>(u_dev);
-    if (p->hp.depth < 2) {
-      if (p->hp.rank == 0) launch_direct_fallback(p->dp, static_cast<const double*>(q_dev), u, st);
-    } else {
-      if (p->dp.n_unpack > 0) {
-        if (!recv_dev) throw CudaFail{SFMM_EINVAL, "receive buffer required"};
-        launch_unpack(p->dp, p->ds, static_cast<const double*>(recv_dev), st);
-      }
-      launch_translate(p->dp, p->ds, st, kBoundaryTasks);
-      for (int l = 2; l <= p->hp.depth; ++l) launch_downward(p->dp, p->hp, l, p->ds, st);
-      launch_scatter(p->dp, p->ds, u, st);
-    }
+    apply_fin_impl(p, q_dev, recv2_dev, u_dev, st);
     ck(cudaGetLastError(), "kernel launch");
     return SFMM_OK;
   } catch (const CudaFail& f) {
     return set_error(f.code, "fmm_apply: " + f.msg);
   }
+}
+
+int sfmm_gpu_shard_info2(const sfmm_gpu_plan* p, int64_t* send2_counts, int64_t* recv2_counts) {
+  if (!p) return set_error(SFMM_EINVAL, "null plan");
+  const HostPlan& hp = p->hp;
+  for (int r = 0; r < hp.n_ranks; ++r) {
+    const bool have = hp.send2_off.size() == (size_t)hp.n_ranks + 1;
+    if (send2_counts) send2_counts[r] = have ? hp.send2_off[r + 1] - hp.send2_off[r] : 0;
+    if (recv2_counts) recv2_counts[r] = have ? hp.recv2_off[r + 1] - hp.recv2_off[r] : 0;
+  }
+  return hp.xsym ? 1 : 0;
 }
 
 int sfmm_gpu_apply(sfmm_gpu_plan* p, const void* q, void* u, int nrhs, int flags,

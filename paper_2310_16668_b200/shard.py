@@ -7,10 +7,18 @@ Every rank builds a sharded plan from the same full descriptor
             (q and qhat) other ranks read;
     exchange  all-to-all of the packed ghosts (NCCL over NVLink via
             torch.distributed, on a side stream);
-    end     unpack, the translation tasks (one launch), staged column sums,
-            downward pass, scatter of the owned points.
-(With SFMM_SHARD_OVERLAP=1, begin also starts the tasks that read no ghost box
-so they overlap the exchange; measured slower.)
+    mid     unpack, the translation tasks (one launch), pack the column sums
+            of the cross-rank colleague pairs this rank evaluated for the
+            other side;
+    exchange  all-to-all of those column sums (second, smaller exchange);
+    fin     add the staged and received column sums, downward pass, scatter of
+            the owned points.
+A colleague pair split across two ranks is evaluated once, by one of its two
+owners (chosen to balance the ranks' work, plan_build.cpp); with
+SFMM_SHARD_XSYM=0 both sides evaluate it and the second exchange disappears
+(``end`` = mid + fin).  With
+SFMM_SHARD_OVERLAP=1, begin also starts the tasks that read no ghost box so
+they overlap the first exchange; measured slower, see DESIGN.md 6.
 
 The reference is single-process (SPEC.md non-goal "distributed trees"); this is
 the B200-native extension described in SURVEY.md 8(e) and DESIGN.md 6.
@@ -38,7 +46,7 @@ def describe(desc, n_ranks: int, rank: int) -> dict:
     """Host-only shard layout of `rank` (no GPU needed)."""
     lib = _abi.gpu_lib()
     st = _struct(desc)
-    counts = np.zeros(2 * n_ranks + 3, dtype=np.int64)
+    counts = np.zeros(4 * n_ranks + 3, dtype=np.int64)
     _raise(lib.sfmm_gpu_shard_describe(C.byref(st), n_ranks, rank, counts.ctypes.data, None, None,
                                        None, None))
     send = counts[:n_ranks].copy()
@@ -54,7 +62,9 @@ def describe(desc, n_ranks: int, rank: int) -> dict:
     return {"send_counts": send, "recv_counts": recv, "n_owned_points": n_owned,
             "n_ghost_boxes": int(counts[2 * n_ranks + 1]), "n_owned_boxes": int(counts[2 * n_ranks + 2]),
             "owner": owner, "pack_idx": pack[: int(send.sum())], "unpack_idx": unpack[: int(recv.sum())],
-            "owned_points": owned[:n_owned]}
+            "owned_points": owned[:n_owned],
+            "send2_counts": counts[2 * n_ranks + 3:3 * n_ranks + 3].copy(),
+            "recv2_counts": counts[3 * n_ranks + 3:].copy()}
 
 
 class ShardedPlan:
@@ -81,7 +91,14 @@ class ShardedPlan:
         self.recv_counts = recv * self.sw
         self.n_owned_points = owned.value
         self.n_ghost_boxes = ghosts.value
+        send2 = np.zeros(n_ranks, dtype=np.int64)
+        recv2 = np.zeros(n_ranks, dtype=np.int64)
+        self.cross_symmetric = bool(lib.sfmm_gpu_shard_info2(self._h, send2.ctypes.data,
+                                                              recv2.ctypes.data))
+        self.send2_counts = send2 * self.sw  # in doubles
+        self.recv2_counts = recv2 * self.sw
         self._bufs = None
+        self._bufs2 = None
 
     def info(self) -> _abi.PlanInfo:
         """sfmm_gpu_plan_info_get of this rank's plan (pair counts are global)."""
@@ -99,6 +116,15 @@ class ShardedPlan:
                           torch.empty(max(1, int(self.recv_counts.sum())), dtype=torch.float64, device=dev))
         return self._bufs
 
+    def buffers2(self):
+        """Device send / receive buffers of the second exchange."""
+        import torch
+        if self._bufs2 is None:
+            dev = f"cuda:{self.device}"
+            self._bufs2 = (torch.empty(max(1, int(self.send2_counts.sum())), dtype=torch.float64, device=dev),
+                           torch.empty(max(1, int(self.recv2_counts.sum())), dtype=torch.float64, device=dev))
+        return self._bufs2
+
     def begin(self, q_dev, stream: int, packed_event: int = 0) -> None:
         send, _ = self.buffers()
         _raise(_abi.gpu_lib().sfmm_gpu_apply_begin(self._h, C.c_void_p(q_dev.data_ptr()),
@@ -110,6 +136,21 @@ class ShardedPlan:
         _, recv = self.buffers()
         _raise(_abi.gpu_lib().sfmm_gpu_apply_end(self._h, C.c_void_p(q_dev.data_ptr()),
                                                  C.c_void_p(recv.data_ptr()),
+                                                 C.c_void_p(u_dev.data_ptr()),
+                                                 C.c_void_p(stream or None)))
+
+    def mid(self, stream: int, packed_event: int = 0) -> None:
+        _, recv = self.buffers()
+        send2, _ = self.buffers2()
+        _raise(_abi.gpu_lib().sfmm_gpu_apply_mid(self._h, C.c_void_p(recv.data_ptr()),
+                                                 C.c_void_p(send2.data_ptr()),
+                                                 C.c_void_p(stream or None),
+                                                 C.c_void_p(packed_event or None)))
+
+    def fin(self, q_dev, u_dev, stream: int) -> None:
+        _, recv2 = self.buffers2()
+        _raise(_abi.gpu_lib().sfmm_gpu_apply_fin(self._h, C.c_void_p(q_dev.data_ptr()),
+                                                 C.c_void_p(recv2.data_ptr()),
                                                  C.c_void_p(u_dev.data_ptr()),
                                                  C.c_void_p(stream or None)))
 
@@ -138,53 +179,82 @@ def _work_stream(stream, device):
     return side, lambda: cur.wait_stream(side)
 
 
-def apply_distributed(plan: ShardedPlan, q_dev, u_dev, stream=None, comm_stream=None) -> None:
-    """One sharded apply with the ghost all-to-all on torch.distributed (NCCL),
-    after the upward pass (overlapping the interior tasks with SFMM_SHARD_OVERLAP=1).  u_dev receives the owned
-    points (other entries untouched)."""
+def _all_to_all(stream, comm_stream, ready, send, recv, send_counts, recv_counts, n_ranks):
+    """recv <- all-to-all(send) on comm_stream after `ready`; stream waits for it."""
     import torch
     import torch.distributed as dist
+    done = torch.cuda.Event()
+    with torch.cuda.stream(comm_stream):
+        comm_stream.wait_event(ready)
+        if n_ranks > 1:
+            dist.all_to_all_single(recv[: int(recv_counts.sum())], send[: int(send_counts.sum())],
+                                   output_split_sizes=[int(x) for x in recv_counts],
+                                   input_split_sizes=[int(x) for x in send_counts])
+        done.record(comm_stream)
+    stream.wait_event(done)
+
+
+def apply_distributed(plan: ShardedPlan, q_dev, u_dev, stream=None, comm_stream=None) -> None:
+    """One sharded apply with the all-to-alls on torch.distributed (NCCL) on a
+    side stream: ghosts after the upward pass, then (cross-symmetric plans)
+    the column sums after the translations.  u_dev receives the owned points
+    (other entries untouched)."""
+    import torch
     stream, fence = _work_stream(stream, plan.device)
     comm_stream = comm_stream or torch.cuda.Stream(plan.device)
     packed = torch.cuda.Event()
-    done = torch.cuda.Event()
     packed.record(stream)  # materialise the event; begin() re-records it after packing
     send, recv = plan.buffers()
-    # begin records `packed` on `stream` right after the pack kernel
     plan.begin(q_dev, stream.cuda_stream, packed.cuda_event)
-    with torch.cuda.stream(comm_stream):
-        comm_stream.wait_event(packed)
-        if plan.n_ranks > 1:
-            dist.all_to_all_single(recv[: int(plan.recv_counts.sum())],
-                                   send[: int(plan.send_counts.sum())],
-                                   output_split_sizes=[int(x) for x in plan.recv_counts],
-                                   input_split_sizes=[int(x) for x in plan.send_counts])
-        done.record(comm_stream)
-    stream.wait_event(done)
-    plan.end(q_dev, u_dev, stream.cuda_stream)
+    _all_to_all(stream, comm_stream, packed, send, recv, plan.send_counts, plan.recv_counts,
+                plan.n_ranks)
+    if plan.cross_symmetric:
+        packed2 = torch.cuda.Event()
+        packed2.record(stream)
+        send2, recv2 = plan.buffers2()
+        plan.mid(stream.cuda_stream, packed2.cuda_event)
+        _all_to_all(stream, comm_stream, packed2, send2, recv2, plan.send2_counts,
+                    plan.recv2_counts, plan.n_ranks)
+        plan.fin(q_dev, u_dev, stream.cuda_stream)
+    else:
+        plan.end(q_dev, u_dev, stream.cuda_stream)
     fence()
+
+
+def _copy_exchange(plans, send_counts, recv_counts, bufs):
+    n = len(plans)
+    send_off = [np.concatenate([[0], np.cumsum(send_counts(p))]) for p in plans]
+    recv_off = [np.concatenate([[0], np.cumsum(recv_counts(p))]) for p in plans]
+    for src in range(n):
+        for dst in range(n):
+            cnt = int(send_counts(plans[src])[dst])
+            assert cnt == int(recv_counts(plans[dst])[src])
+            if cnt == 0:
+                continue
+            s0, d0 = int(send_off[src][dst]), int(recv_off[dst][src])
+            bufs(plans[dst])[1][d0:d0 + cnt].copy_(bufs(plans[src])[0][s0:s0 + cnt])
 
 
 def apply_virtual(plans: list[ShardedPlan], q_dev, u_dev, stream=None) -> None:
     """All ranks' shards on ONE GPU, run one after another (no kernel waits on
-    another rank); the all-to-all becomes device-to-device copies.  Used to
+    another rank); the all-to-alls become device-to-device copies.  Used to
     test the sharded path where only one GPU is available."""
     import torch
     stream, fence = _work_stream(stream, plans[0].device)
     for p in plans:
         p.begin(q_dev, stream.cuda_stream, 0)
-    n = len(plans)
-    send_off = [np.concatenate([[0], np.cumsum(p.send_counts)]) for p in plans]
-    recv_off = [np.concatenate([[0], np.cumsum(p.recv_counts)]) for p in plans]
     with torch.cuda.stream(stream):
-        for src in range(n):
-            for dst in range(n):
-                cnt = int(plans[src].send_counts[dst])
-                assert cnt == int(plans[dst].recv_counts[src])
-                if cnt == 0:
-                    continue
-                s0, d0 = int(send_off[src][dst]), int(recv_off[dst][src])
-                plans[dst].buffers()[1][d0:d0 + cnt].copy_(plans[src].buffers()[0][s0:s0 + cnt])
-    for p in plans:
-        p.end(q_dev, u_dev, stream.cuda_stream)
+        _copy_exchange(plans, lambda p: p.send_counts, lambda p: p.recv_counts,
+                       lambda p: p.buffers())
+    if plans[0].cross_symmetric:
+        for p in plans:
+            p.mid(stream.cuda_stream)
+        with torch.cuda.stream(stream):
+            _copy_exchange(plans, lambda p: p.send2_counts, lambda p: p.recv2_counts,
+                           lambda p: p.buffers2())
+        for p in plans:
+            p.fin(q_dev, u_dev, stream.cuda_stream)
+    else:
+        for p in plans:
+            p.end(q_dev, u_dev, stream.cuda_stream)
     fence()

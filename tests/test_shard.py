@@ -43,6 +43,13 @@ def test_shard_layout_consistent(n_ranks, dist):
             assert np.array_equal(sent, got), (p, q)
             if p == q:
                 assert sent.size == 0
+    # second exchange (cross-rank colleague pairs evaluated on one side)
+    for p in range(n_ranks):
+        assert infos[p]["send2_counts"][p] == 0 and infos[p]["recv2_counts"][p] == 0
+        for q in range(n_ranks):
+            assert infos[p]["send2_counts"][q] == infos[q]["recv2_counts"][p], (p, q)
+    if n_ranks > 1:
+        assert sum(int(inf["send2_counts"].sum()) for inf in infos) > 0
     # ghosts are never owned by the receiver
     a = d.arrays
     n_slots = int(a["iv_off"][-1])
@@ -139,6 +146,43 @@ def test_virtual_ranks_match_single_plan(n_ranks, case):
     assert rel_l2(u, u_ref) <= 1e-12
     if n_ranks > 1:
         assert any(p.n_ghost_boxes > 0 for p in plans)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("env", [{"SFMM_SHARD_XSYM": "0"}, {"SFMM_SHARD_OVERLAP": "1"},
+                                 {"SFMM_SHARD_OVERLAP": "1", "SFMM_SHARD_XSYM": "0"}])
+def test_virtual_ranks_plan_variants(env, monkeypatch):
+    # the one-sided cross-rank pairs (default) against both sides evaluating
+    # them, and the overlapped two-launch split; all must match the single plan
+    import torch
+    n = 30000
+    d, pts = _desc(dist="sphere", n=n, leaf=64)
+    q = host.generate_charges(n, 3)
+    u_ref = api.fmm_apply(api.GpuPlan(d), q)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    plans = [shard.ShardedPlan(d, 4, r) for r in range(4)]
+    assert all(p.cross_symmetric == (env.get("SFMM_SHARD_XSYM") != "0") for p in plans)
+    qd = torch.from_numpy(q).cuda()
+    ud = torch.zeros_like(qd)
+    shard.apply_virtual(plans, qd, ud)
+    torch.cuda.synchronize()
+    assert rel_l2(ud.cpu().numpy(), u_ref) <= 1e-12
+
+
+@pytest.mark.gpu
+def test_cross_symmetric_plan_requires_mid_fin():
+    import torch
+    n = 30000
+    d, _ = _desc(n=n, leaf=64)
+    plans = [shard.ShardedPlan(d, 2, r) for r in range(2)]
+    assert all(p.cross_symmetric for p in plans)
+    assert sum(int(p.send2_counts.sum()) for p in plans) > 0
+    qd = torch.zeros(n, dtype=torch.float64, device="cuda")
+    plans[0].begin(qd, 0, 0)
+    with pytest.raises(ValueError, match="apply_mid"):
+        plans[0].end(qd, torch.zeros_like(qd), 0)
+    torch.cuda.synchronize()
 
 
 @pytest.mark.gpu

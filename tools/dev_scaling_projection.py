@@ -1,10 +1,10 @@
 """Projected strong scaling of the sharded apply from one GPU.
 
-Each rank's share of one apply (begin: gather, upward pass, pack, interior
-translations; end: unpack, boundary translations, K2b, downward pass, scatter)
+Each rank's share of one apply (begin: gather, upward pass, pack; end:
+unpack, translations, column-sum pack, K2b, downward pass, scatter)
 is timed alone on the device with CUDA events, on buffers already holding a
 complete exchange.  On N GPUs the step takes about the slowest rank's time
-plus the ghost all-to-all, which SURVEY.md 8e estimates at <0.1 % of the step
+plus the ghost all-to-alls, which SURVEY.md 8e estimates at <0.1 % of the step
 over NVLink; it is not included.  Usage: python tools/dev_scaling_projection.py [N]
 """
 import os
@@ -17,6 +17,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2310_16668_b200 import api, host, shard  # noqa: E402
 
 n = int(float(sys.argv[1])) if len(sys.argv) > 1 else 10_000_000
+REPS = 10  # timed begin/end pairs per rank (median)
 pts = host.generate_points("cube", n, 1)
 hp = host.HostPlan.build_gpu(1, pts, 128, 1e-6, tree="gpu")
 q = host.generate_charges(n, 1)
@@ -30,11 +31,11 @@ for _ in range(2):
 s.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record(s)
-for _ in range(5):
+for _ in range(REPS):
     api.fmm_apply_device(single, qd.data_ptr(), ud.data_ptr(), 1, s.cuda_stream)
 e1.record(s)
 s.synchronize()
-t1 = e0.elapsed_time(e1) / 5
+t1 = e0.elapsed_time(e1) / REPS
 single.close()
 print(f"N={n:.0e}  1 GPU (single plan, graph replay): {t1:.2f} ms")
 
@@ -45,25 +46,31 @@ for nr in (2, 4, 8):
     times = []
     for p in plans:
         with torch.cuda.stream(s):
+            def end(p=p):
+                if p.cross_symmetric:
+                    p.mid(s.cuda_stream)
+                    p.fin(qd, ud, s.cuda_stream)
+                else:
+                    p.end(qd, ud, s.cuda_stream)
             for _ in range(2):
                 p.begin(qd, s.cuda_stream, 0)
-                p.end(qd, ud, s.cuda_stream)
-            ev = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
+                end()
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * REPS + 1)]
             ev[0].record(s)
-            for i in range(3):
+            for i in range(REPS):
                 p.begin(qd, s.cuda_stream, 0)
                 ev[1 + 2 * i].record(s)
-                p.end(qd, ud, s.cuda_stream)
+                end()
                 ev[2 + 2 * i].record(s)
         s.synchronize()
-        tb = np.mean([ev[2 * i].elapsed_time(ev[1 + 2 * i]) for i in range(3)])
-        te = np.mean([ev[1 + 2 * i].elapsed_time(ev[2 + 2 * i]) for i in range(3)])
-        times.append((tb + te, tb, te))
+        tb = np.median([ev[2 * i].elapsed_time(ev[1 + 2 * i]) for i in range(REPS)])
+        te = np.median([ev[1 + 2 * i].elapsed_time(ev[2 + 2 * i]) for i in range(REPS)])
+        times.append((float(tb + te), float(tb), float(te)))
     tmax = max(t[0] for t in times)
     print(f"{nr} ranks: per-rank ms (begin+end) {[round(t[0], 2) for t in times]}  max {tmax:.2f}  "
           f"projected speed-up {t1 / tmax:.2f}x  efficiency {t1 / (nr * tmax):.3f}", flush=True)
-    print(f"   begin (gather, upward, pack, interior K2) {[round(t[1], 2) for t in times]}", flush=True)
-    print(f"   end (unpack, boundary K2, K2b, downward, scatter) {[round(t[2], 2) for t in times]}",
+    print(f"   begin (gather, upward, pack) {[round(t[1], 2) for t in times]}", flush=True)
+    print(f"   end (unpack, K2, column-sum pack, K2b, downward, scatter) {[round(t[2], 2) for t in times]}",
           flush=True)
     for p in plans:
         p.close()
