@@ -17,6 +17,11 @@ enum Mode : int32_t {
              // b's rows as kIFO, c's rows (A_cb = A_bc^T) as staged column sums
 };
 constexpr int kNRHS = 16;  // right-hand sides per multi-RHS pass (zero padded)
+// Largest rows-per-lane of the complex K2 (row tiles of complex plans are at
+// most 32 x this; plan_build.cpp and kernels_translate.cu must agree).
+#ifndef SFMM_K2C_MAX_R
+#define SFMM_K2C_MAX_R 3
+#endif
 constexpr int kModeBits = 3;
 constexpr int32_t kModeMask = (1 << kModeBits) - 1;
 

@@ -348,13 +348,20 @@ __global__ void __launch_bounds__(kThreads, SFMM_K2_MIN_BLOCKS) k2_translate_rea
 // ---------------------------------------------------------------------------
 // Helmholtz 3D, complex FP64: G = exp(i kappa r)/(4 r) (kernel.hpp:62-71).
 // ---------------------------------------------------------------------------
+// Complex K2 shape (A/B at N=2e6, kappa=10, K2 ms): rows per lane <= 2 at
+// 4 CTAs/SM 68.5; <= 3 at 3 CTAs/SM 66.1, plus two sources per loop trip 65.6
+// (adopted); <= 4 at 3 CTAs/SM 69.1; <= 3 at 4 CTAs/SM (spills) 68.1.
+#ifndef SFMM_K2C_UNROLL
+#define SFMM_K2C_UNROLL 2
+#endif
+constexpr int kK2cUnroll = SFMM_K2C_UNROLL;
 template <int R, bool H, bool SELF, bool TAB>
 __device__ __forceinline__ void inner_cplx(const WarpSmemCplx& sm, const double2* __restrict__ tab,
                                            int cnt, int j0, double kappa,
                                            const double (&xi)[R], const double (&yi)[R],
                                            const double (&zi)[R], const int (&rowi)[R],
                                            double2 (&au)[R], double2 (&ah)[R]) {
-#pragma unroll 1
+#pragma unroll kK2cUnroll
   for (int jj = 0; jj < cnt; ++jj) {
     const double2 xy = sm.xy[jj];
     const double zz = sm.z[jj];
@@ -556,7 +563,7 @@ __device__ __forceinline__ void task_cplx(const K2Args& a, const Task& t, WarpSm
 }
 
 #ifndef SFMM_K2C_MIN_BLOCKS
-#define SFMM_K2C_MIN_BLOCKS 4
+#define SFMM_K2C_MIN_BLOCKS 3
 #endif
 template <bool TAB>
 __global__ void __launch_bounds__(kThreads, SFMM_K2C_MIN_BLOCKS) k2_translate_cplx(K2Args a) {
@@ -575,7 +582,13 @@ __global__ void __launch_bounds__(kThreads, SFMM_K2C_MIN_BLOCKS) k2_translate_cp
     const Task task = a.tasks[t];
     switch ((task.nrows + 31) >> 5) {
       case 1: task_cplx<1, TAB>(a, task, sm, tab, lane); break;
-      default: task_cplx<2, TAB>(a, task, sm, tab, lane); break;  // complex plans: <= 64-row tiles
+#if SFMM_K2C_MAX_R >= 3
+      case 2: task_cplx<2, TAB>(a, task, sm, tab, lane); break;
+#endif
+#if SFMM_K2C_MAX_R >= 4
+      case 3: task_cplx<3, TAB>(a, task, sm, tab, lane); break;
+#endif
+      default: task_cplx<SFMM_K2C_MAX_R, TAB>(a, task, sm, tab, lane); break;
     }
   }
 }

@@ -549,7 +549,7 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
 #ifdef SFMM_TILE_FORCE
       tile = SFMM_TILE_FORCE;  // dev knob (A/B of the K2 occupancy variants)
 #endif
-      if (hp.cplx) tile = std::min(tile, kTileRows / 2);  // complex K2: <= 2 rows per lane
+      if (hp.cplx) tile = std::min(tile, 32 * SFMM_K2C_MAX_R);  // complex K2 rows per lane
       hp.tile_rows = tile;
       // outgoing cross-rank pairs in (b, entry) order, the staged tiles of each
       std::vector<std::pair<int32_t, int32_t>> xpairs;
