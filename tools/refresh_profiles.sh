@@ -24,4 +24,10 @@ ncu --set full --clock-control none --import-source on -k regex:k2m -s 1 -c 1 \
 # the adaptive sphere (config 3a): K2 capture for the instruction-fetch / task-order story
 ncu --set full --clock-control none --import-source on -k regex:k2_translate -s 2 -c 1 \
     -o $out/k2_c3a python bench.py --config c3a --steps 1 --warmup 2 --cpu off > $out/ncu_k2_c3a.log 2>&1
+# single-RHS Helmholtz (the reference's call shape): bench line + complex K2 capture
+python bench.py --kernel helmholtz3d --points 4e6 --steps 5 --warmup 3 --cpu off \
+    > $out/bench_h3d_4e6_1rhs.json 2> $out/bench_h3d_4e6_1rhs.err
+ncu --set full --clock-control none --import-source on -k regex:k2_translate -s 3 -c 1 \
+    -o $out/k2_h3d python bench.py --kernel helmholtz3d --points 2e6 --steps 1 --warmup 3 \
+    --cpu off --check-targets 0 > $out/ncu_k2_h3d.log 2>&1
 ls -la $out
