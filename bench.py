@@ -404,9 +404,9 @@ def run_sharded(args, ws, rank, local):
                                  "per-kernel roofline is in the 1-GPU line"},
             "e2e": {"value": n / t_e2e / 1e6, "unit": UNIT, "h2d_bytes_per_step": bytes_col * ws,
                     "d2h_bytes_per_step": bytes_col * ws, "ms_per_step": t_e2e * 1e3},
-            # per rank and apply: the single-RHS sequence, plus ghost pack and unpack and
-            # the second (boundary) translation launch
-            "gpu_launches": (int(pinfo.launches_per_apply) + 3) * args.steps,
+            # rank 0 per apply: the single-RHS sequence plus ghost pack / unpack and the
+            # column-sum pack (plan_info counts them for sharded plans)
+            "gpu_launches": int(pinfo.launches_per_apply) * args.steps,
             "clocks": clk,
             "relerr_vs_direct": relerr_direct, "n_check": int(targets.size),
             "relerr_vs_single_gpu": relerr_single,

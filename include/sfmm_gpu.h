@@ -125,7 +125,7 @@ typedef struct sfmm_gpu_plan_info {
   int64_t n_tasks;          /* K2 work items */
   int64_t device_bytes;     /* resident plan bytes */
   int64_t n_ifo_pairs, n_ifs_pairs, n_tfo_pairs, n_level1_pairs;
-  int32_t launches_per_apply; /* kernels of this library launched by one single-RHS apply */
+  int32_t launches_per_apply; /* kernels of this library launched by one single-RHS apply (this rank) */
   int32_t k2_grid;            /* persistent CTAs of the translation kernel */
 } sfmm_gpu_plan_info;
 
