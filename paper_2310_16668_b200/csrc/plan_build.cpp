@@ -294,11 +294,15 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
     // as usual and c's rows receive A_cb q_b = (A_bc)^T q_b as staged column
     // sums.  Pairs across ranks stay kIFO on both sides.
     hp.symmetric = opt.symmetric;
-    if (hp.symmetric) {  // the colleague relation must be symmetric to stage
+    if (hp.symmetric) {  // the colleague relation must be symmetric (and the lists sorted)
       int asym = 0;
 #pragma omp parallel for schedule(dynamic, 1024) reduction(| : asym)
       for (int32_t b = 0; b < nb; ++b)
         for (int64_t e = d.coll_off[b]; e < d.coll_off[b + 1]; ++e) {
+          if (e > d.coll_off[b] && d.coll[e] <= d.coll[e - 1]) {
+            asym = 1;
+            break;
+          }
           const int32_t c = d.coll[e];
           const int32_t* cb = d.coll + d.coll_off[c];
           const int32_t* ce = d.coll + d.coll_off[c + 1];

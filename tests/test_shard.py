@@ -60,6 +60,28 @@ def test_shard_layout_consistent(n_ranks, dist):
         assert np.all(owner[box_of_slot] != q)
 
 
+def _shuffled_colleagues(d, seed=7):
+    """The same descriptor with every colleague list in a random order."""
+    from paper_2310_16668_b200._abi import PlanDescriptor
+    a = {k: v.copy() for k, v in d.arrays.items()}
+    rng = np.random.default_rng(seed)
+    off, coll = a["coll_off"], a["coll"]
+    for b in range(len(off) - 1):
+        seg = coll[off[b]:off[b + 1]]
+        coll[off[b]:off[b + 1]] = seg[rng.permutation(seg.size)]
+    return PlanDescriptor(d.scalars, a)
+
+
+def test_unsorted_colleague_lists_disable_the_fold():
+    # the one-sided cross-rank pairs look pairs up in sorted colleague lists;
+    # a descriptor with unsorted lists must fall back to two-sided pairs
+    d, _ = _desc()
+    assert sum(int(shard.describe(d, 4, r)["send2_counts"].sum()) for r in range(4)) > 0
+    ds = _shuffled_colleagues(d)
+    infos = [shard.describe(ds, 4, r) for r in range(4)]
+    assert all(int(i["send2_counts"].sum()) == 0 and int(i["recv2_counts"].sum()) == 0 for i in infos)
+
+
 def test_subtrees_are_owned_whole():
     d, _ = _desc()
     owner = shard.describe(d, 4, 0)["owner"]
@@ -163,6 +185,24 @@ def test_virtual_ranks_plan_variants(env, monkeypatch):
         monkeypatch.setenv(k, v)
     plans = [shard.ShardedPlan(d, 4, r) for r in range(4)]
     assert all(p.cross_symmetric == (env.get("SFMM_SHARD_XSYM") != "0") for p in plans)
+    qd = torch.from_numpy(q).cuda()
+    ud = torch.zeros_like(qd)
+    shard.apply_virtual(plans, qd, ud)
+    torch.cuda.synchronize()
+    assert rel_l2(ud.cpu().numpy(), u_ref) <= 1e-12
+
+
+@pytest.mark.gpu
+def test_unsorted_colleague_lists_same_result():
+    import torch
+    n = 30000
+    d, _ = _desc(n=n, leaf=64)
+    ds = _shuffled_colleagues(d)
+    q = host.generate_charges(n, 3)
+    u_ref = api.fmm_apply(api.GpuPlan(d), q)
+    assert rel_l2(api.fmm_apply(api.GpuPlan(ds), q), u_ref) <= 1e-12
+    plans = [shard.ShardedPlan(ds, 4, r) for r in range(4)]
+    assert not any(p.cross_symmetric for p in plans)
     qd = torch.from_numpy(q).cuda()
     ud = torch.zeros_like(qd)
     shard.apply_virtual(plans, qd, ud)
