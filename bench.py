@@ -393,7 +393,8 @@ def run_sharded(args, ws, rank, local):
             "config": {
                 "workload": f"{args.kernel} {args.dist} N={n:.0e} leaf={args.leaf} tol={args.tol} nrhs=1",
                 "n_points": n, "leaf_cap": args.leaf, "tol": args.tol, "nrhs": 1,
-                "parallelism": f"level-1 subtree sharding x{ws}, ghost all-to-all over {args.backend}",
+                "parallelism": (f"subtree sharding x{ws} (cut level {plan.cut_level}), ghost and "
+                                f"column-sum all-to-alls over {args.backend}"),
                 "l2": "inputs larger than L2",
             },
             "roofline": {"bound": "fp64", "kernel": "whole sharded step (K2-equivalent work)",

@@ -159,7 +159,8 @@ void sfmm_gpu_plan_destroy(sfmm_gpu_plan* plan);
 
 /*
  * Multi-GPU (one process per GPU).  Rank `rank` of `n_ranks` owns whole
- * level-1 subtrees (Morton-contiguous; assigned by estimated translation cost)
+ * level-1 subtrees (assigned by estimated translation cost), or Morton ranges
+ * of level-2 subtrees when that balances clearly better (clustered inputs)
  * and builds its plan from the SAME full descriptor as every other rank.  One
  * apply is
  *   sfmm_gpu_apply_begin   gather + upward pass of the owned subtrees, pack the
@@ -198,17 +199,21 @@ int sfmm_gpu_apply_begin(sfmm_gpu_plan* plan, const void* q_dev, void* send_dev,
 int sfmm_gpu_apply_end(sfmm_gpu_plan* plan, const void* q_dev, const void* recv_dev, void* u_dev,
                        void* stream);
 /* Returns 1 when the plan has the second exchange (apply_mid/_fin), else 0;
- * fills the per-peer scalar counts of that exchange (zeros when absent). */
-int sfmm_gpu_shard_info2(const sfmm_gpu_plan* plan, int64_t* send2_counts, int64_t* recv2_counts);
+ * fills the per-peer scalar counts of that exchange (zeros when absent) and
+ * the cut level of the ownership (see sfmm_gpu_shard_describe). */
+int sfmm_gpu_shard_info2(const sfmm_gpu_plan* plan, int64_t* send2_counts, int64_t* recv2_counts,
+                         int* cut_level);
 int sfmm_gpu_apply_mid(sfmm_gpu_plan* plan, const void* recv_dev, void* send2_dev, void* stream,
                        void* packed_event);
 int sfmm_gpu_apply_fin(sfmm_gpu_plan* plan, const void* q_dev, const void* recv2_dev, void* u_dev,
                        void* stream);
 
 /* Host-only view of rank `rank`'s shard (no device is touched).  counts gets
- * 4*n_ranks + 3 values: send scalars per peer, receive scalars per peer,
- * owned points, ghost boxes, owned boxes, then the second exchange's send and
- * receive scalars per peer.  Non-NULL arrays receive the box
+ * 4*n_ranks + 4 values: send scalars per peer, receive scalars per peer,
+ * owned points, ghost boxes, owned boxes, the second exchange's send and
+ * receive scalars per peer, and the cut level (1: level-1 subtrees per rank;
+ * 2: level-2 subtrees, the internal level-1 boxes shared, owner -1).
+ * Non-NULL arrays receive the box
  * owners (n_boxes), the ghost-exchange element indices into [q slots | qhat]
  * (pack_idx: what this rank sends, per peer in rank order; unpack_idx: where
  * what it receives lands) and the owned points' original indices. */

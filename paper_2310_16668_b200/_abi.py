@@ -315,7 +315,7 @@ def gpu_lib() -> C.CDLL:
     lib.sfmm_gpu_apply_begin.restype = C.c_int
     lib.sfmm_gpu_apply_end.argtypes = [vp, vp, vp, vp, vp]
     lib.sfmm_gpu_apply_end.restype = C.c_int
-    lib.sfmm_gpu_shard_info2.argtypes = [vp, vp, vp]
+    lib.sfmm_gpu_shard_info2.argtypes = [vp, vp, vp, C.POINTER(C.c_int)]
     lib.sfmm_gpu_shard_info2.restype = C.c_int
     lib.sfmm_gpu_apply_mid.argtypes = [vp, vp, vp, vp, vp]
     lib.sfmm_gpu_apply_mid.restype = C.c_int

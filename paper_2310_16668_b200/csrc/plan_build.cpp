@@ -213,34 +213,155 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
       unc[b] = opt.skip_cancel && d.box_level[b] >= 2 && hp.box[b].n > 0 &&
                hp.box[b].k == hp.box[b].n;
     const int32_t l1b = hp.level_begin[1], l1e = hp.level_begin[2];
+    // Sharding: each rank owns whole subtrees rooted at the cut
+    // level.  Cut 1: level-1 subtrees, assigned longest-first to the least
+    // loaded rank.  Cut 2 (the level-1 split is unbalanced -- clustered
+    // inputs -- or there are more ranks than level-1 boxes): level-2 subtrees
+    // (and level-1 leaves) as Morton-contiguous ranges split to minimise the
+    // largest estimated cost, or longest-first when a few heavy subtrees make
+    // that 3 % better; the internal level-1 boxes are then shared
+    // (owner kShared): every rank evaluates their level-1 translations (~0.04 %
+    // of the pairs) and receives their slots, which the level-2 owners' upward
+    // pass fills, with the ghosts.
     hp.owner.assign(nb, 0);
+    hp.cut_level = 1;
     if (n_ranks > 1) {
-      const int32_t n1 = l1e - l1b;
-      if (n_ranks > n1)
-        throw Fail{SFMM_EUNSUPPORTED, "sfmm_gpu_plan_create: more ranks than level-1 boxes"};
-      // estimated translation cost of every level-1 subtree
+      // estimated K2 cost of every subtree, as the task cost model: lane rows
+      // x (evaluated source points + 8); cancelling pairs skipped, colleague
+      // blocks at ~0.575 (evaluated once for both directions)
       std::vector<double> cost(nb, 0.0);
       for (int32_t b = nb - 1; b >= 1; --b) {
+        const int lev = d.box_level[b];
         double src = 0;
-        for (int64_t e = d.coll_off[b]; e < d.coll_off[b + 1]; ++e) src += hp.box[d.coll[e]].n;
-        for (int64_t e = d.coarse_off[b]; e < d.coarse_off[b + 1]; ++e) src += hp.box[d.coarse[e]].n;
-        for (int64_t e = d.fine_off[b]; e < d.fine_off[b + 1]; ++e) src += hp.box[d.fine[e]].n;
-        cost[b] += (double)hp.box[b].n * src + 64.0 * hp.box[b].n;
+        if (lev >= 2) {
+          for (int64_t e = d.coll_off[b]; e < d.coll_off[b + 1]; ++e) {
+            const int32_t c = d.coll[e];
+            if (!(unc[b] && unc[c])) src += (c == b ? 1.0 : 0.575) * hp.box[c].n;
+          }
+          if (!unc[b])
+            for (int64_t e = d.coarse_off[b]; e < d.coarse_off[b + 1]; ++e) src += hp.box[d.coarse[e]].n;
+        }
+        if (lev == 1)
+          for (int32_t c = l1b; c < l1e; ++c) src += hp.box[c].n;
+        if (d.box_leaf[b] && lev >= 1)
+          for (int64_t e = d.fine_off[b]; e < d.fine_off[b + 1]; ++e)
+            if (!unc[d.fine[e]]) src += hp.box[d.fine[e]].n;
+        const double lane_rows = 32.0 * ((hp.box[b].n + 31) / 32);
+        cost[b] += src > 0.0 ? lane_rows * (src + 8.0) : 0.0;
         if (d.box_parent[b] > 0) cost[d.box_parent[b]] += cost[b];
       }
-      std::vector<int32_t> ord(n1);
-      std::iota(ord.begin(), ord.end(), l1b);
-      std::stable_sort(ord.begin(), ord.end(),
-                       [&](int32_t x, int32_t y) { return cost[x] > cost[y]; });
-      std::vector<double> load(n_ranks, 0.0);
-      for (int32_t b : ord) {
-        const int r = (int)(std::min_element(load.begin(), load.end()) - load.begin());
-        hp.owner[b] = r;
-        load[r] += cost[b];
+      const int32_t n1 = l1e - l1b;
+      double total = 0.0;
+      for (int32_t b = l1b; b < l1e; ++b) total += cost[b];
+      const double mean = total / n_ranks;
+      // cut 1: LPT over the level-1 subtrees
+      std::vector<int32_t> own1(nb, 0);
+      double max1 = 1e300;
+      if (n1 >= n_ranks) {
+        std::vector<int32_t> ord(n1);
+        std::iota(ord.begin(), ord.end(), l1b);
+        std::stable_sort(ord.begin(), ord.end(),
+                         [&](int32_t x, int32_t y) { return cost[x] > cost[y]; });
+        std::vector<double> load(n_ranks, 0.0);
+        for (int32_t b : ord) {
+          const int r = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+          own1[b] = r;
+          load[r] += cost[b];
+        }
+        max1 = *std::max_element(load.begin(), load.end());
       }
-      for (int32_t b = l1e; b < nb; ++b) hp.owner[b] = hp.owner[d.box_parent[b]];
+      // cut 2 units in Morton order: each level-1 box's level-2 children, or
+      // the level-1 box itself when it is a leaf
+      std::vector<int32_t> units;
+      const int32_t l2e = d.depth >= 2 ? hp.level_begin[3] : l1e;
+      {
+        int32_t c = l1e;
+        for (int32_t b = l1b; b < l1e; ++b) {
+          if (d.box_leaf[b]) {
+            units.push_back(b);
+            continue;
+          }
+          for (; c < l2e && d.box_parent[c] == b; ++c) units.push_back(c);
+        }
+      }
+      const int64_t nu = (int64_t)units.size();
+      // smallest feasible largest range (bisection on the bound, greedy fill)
+      auto ranges = [&](double bound, std::vector<int32_t>* own) {
+        int r = 0;
+        double acc = 0.0;
+        for (int64_t u = 0; u < nu; ++u) {
+          const double w = cost[units[u]];
+          if (acc > 0.0 && acc + w > bound) {
+            ++r;
+            acc = 0.0;
+          }
+          // leave at least one unit for every later rank
+          if (own && acc > 0.0 && nu - u <= n_ranks - 1 - r) {
+            ++r;
+            acc = 0.0;
+          }
+          acc += w;
+          if (own) (*own)[units[u]] = std::min(r, n_ranks - 1);
+        }
+        return r + 1;
+      };
+      double max2 = 1e300;
+      std::vector<int32_t> own2(nb, 0);
+      if (nu >= n_ranks) {
+        double lo = 0.0, hi = total;
+        for (int64_t u = 0; u < nu; ++u) lo = std::max(lo, cost[units[u]]);
+        lo = std::max(lo, mean);
+        for (int it = 0; it < 60 && hi - lo > 1e-9 * hi; ++it) {
+          const double mid = 0.5 * (lo + hi);
+          (ranges(mid, nullptr) <= n_ranks ? hi : lo) = mid;
+        }
+        ranges(hi, &own2);
+        std::vector<double> load(n_ranks, 0.0);
+        for (int32_t u : units) load[own2[u]] += cost[u];
+        max2 = *std::max_element(load.begin(), load.end());
+        // LPT over the same units when the contiguous ranges cannot balance
+        // (a few heavy units: clusters); the ghosts stay a small exchange
+        std::vector<int32_t> ord(units);
+        std::stable_sort(ord.begin(), ord.end(),
+                         [&](int32_t x, int32_t y) { return cost[x] > cost[y]; });
+        std::vector<double> ll(n_ranks, 0.0);
+        std::vector<int32_t> own_l(nb, 0);
+        for (int32_t u : ord) {
+          const int r = (int)(std::min_element(ll.begin(), ll.end()) - ll.begin());
+          own_l[u] = r;
+          ll[r] += cost[u];
+        }
+        const double maxl = *std::max_element(ll.begin(), ll.end());
+        if (maxl < 0.97 * max2) {
+          max2 = maxl;
+          own2.swap(own_l);
+        }
+      }
+      if (max1 >= 1e300 && max2 >= 1e300)
+        throw Fail{SFMM_EUNSUPPORTED, "sfmm_gpu_plan_create: more ranks than level-2 subtrees"};
+      // cut 2 only when it clearly balances better (cut 1 has fewer ghosts)
+      const bool cut2 = max1 >= 1e300 || (max2 < 1e300 && max2 < 0.95 * max1 && max1 > 1.02 * mean);
+      if (verbose && rank == 0) {
+        std::vector<double> l2(n_ranks, 0.0);
+        if (max2 < 1e300)
+          for (int32_t u : units) l2[own2[u]] += cost[u];
+        double umax = 0.0;
+        for (int32_t u : units) umax = std::max(umax, cost[u]);
+        fprintf(stderr, "[plan] shard cost mean %.4g  cut1 max %.4g  cut2 max %.4g (%lld units, largest %.4g)  cut2 loads:",
+                mean, max1, max2, (long long)nu, umax);
+        for (double x : l2) fprintf(stderr, " %.3g", x);
+        fprintf(stderr, "\n");
+      }
+      if (!cut2) {
+        for (int32_t b = l1b; b < l1e; ++b) hp.owner[b] = own1[b];
+      } else {
+        hp.cut_level = 2;
+        for (int32_t b = l1b; b < l1e; ++b) hp.owner[b] = d.box_leaf[b] ? own2[b] : kShared;
+        for (int32_t b = l1e; b < l2e; ++b) hp.owner[b] = own2[b];
+      }
+      for (int32_t b = cut2 ? l2e : l1e; b < nb; ++b) hp.owner[b] = hp.owner[d.box_parent[b]];
     }
-    auto mine = [&](int32_t b) { return hp.owner[b] == rank; };
+    auto mine = [&](int32_t b) { return hp.owner[b] == rank || hp.owner[b] == kShared; };
 
     ptime("ownership");
     // leaf gather/scatter maps (owned leaves): slot of position i <-> q[perm[begin + i]]
@@ -383,7 +504,7 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
       xev.assign(d.coll_off[nb], 0);
       std::vector<double> load(n_ranks, 0.0);
       for (int32_t b = 0; b < nb; ++b) {
-        if (d.box_level[b] < 1) continue;
+        if (d.box_level[b] < 1 || hp.owner[b] == kShared) continue;
         const double nbn = hp.box[b].n;
         sources(b, [&](int32_t c, int mode) {
           if (mode == kIFO && hp.owner[c] != hp.owner[b]) return;
@@ -481,9 +602,26 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
         if (d.box_level[b] < 1) continue;
         const int q = hp.owner[b];
         sources(b, [&](int32_t c, int mode) {
-          if (hp.owner[c] != q && !folded_away(b, c, mode)) need[q][c] = 1;
+          if (hp.owner[c] == kShared) return;  // every rank holds shared boxes
+          if (q == kShared) {                   // every rank evaluates b
+            for (int p = 0; p < n_ranks; ++p)
+              if (hp.owner[c] != p) need[p][c] = 1;
+          } else if (hp.owner[c] != q && !folded_away(b, c, mode)) {
+            need[q][c] = 1;
+          }
         });
       }
+      // shared boxes' slots that a child's upward pass fills (child owned by
+      // p, parent shared): p sends them to every other rank
+      std::vector<int32_t> shared_kids;
+      if (hp.cut_level > 1)
+        for (int32_t c = l1e; c < hp.level_begin[3]; ++c)
+          if (hp.owner[d.box_parent[c]] == kShared && hp.box[c].k > 0) shared_kids.push_back(c);
+      auto parent_slots = [&](int32_t c, std::vector<int64_t>& out) {
+        const int64_t ps = hp.box[d.box_parent[c]].slot;
+        for (int32_t i = 0; i < hp.box[c].k; ++i)
+          out.push_back(ps + hp.posmap[ps + d.box_parent_offset[c] + i]);
+      };
       hp.send_off.assign(n_ranks + 1, 0);
       hp.recv_off_peer.assign(n_ranks + 1, 0);
       const int64_t sk_base = S;  // QH entries are addressed as S + skel index
@@ -498,6 +636,10 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
             for (int32_t i = 0; i < hp.box[c].k; ++i) hp.unpack_idx.push_back(sk_base + hp.box[c].skel + i);
             ++hp.n_ghost_boxes;
           }
+        }
+        for (int32_t c : shared_kids) {
+          if (p != rank && hp.owner[c] == rank) parent_slots(c, hp.pack_idx);
+          if (p != rank && hp.owner[c] == p) parent_slots(c, hp.unpack_idx);
         }
         hp.send_off[p + 1] = (int64_t)hp.pack_idx.size();
         hp.recv_off_peer[p + 1] = (int64_t)hp.unpack_idx.size();

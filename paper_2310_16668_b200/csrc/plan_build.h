@@ -37,6 +37,8 @@ struct LevelItem {
   int32_t first;  // first row (K1) / column (K3) of the chunk
 };
 
+constexpr int32_t kShared = -1;  // HostPlan::owner of boxes every rank evaluates
+
 struct HostPlan {
   int kernel = 0, dim = 0, cplx = 0;
   double kappa = 0;
@@ -70,8 +72,9 @@ struct HostPlan {
   std::vector<int64_t> recv_u, recv_h;
   int64_t n_skipped_pairs = 0;                // cancelling pairs not evaluated
   int64_t n_interior_tasks = 0;               // tasks[0, n_interior) read no ghost box
-  // sharding: owner rank of every box (whole level-1 subtrees)
-  int n_ranks = 1, rank = 0;
+  // sharding: owner rank of every box (whole subtrees at the cut
+  // level; kShared: internal boxes above the cut, evaluated on every rank)
+  int n_ranks = 1, rank = 0, cut_level = 1;
   std::vector<int32_t> owner;
   int64_t n_owned_points = 0;
   double p_dense_local = 0;                   // dense pairs this rank evaluates

@@ -510,6 +510,7 @@ int sfmm_gpu_shard_describe(const sfmm_plan_desc* desc, int n_ranks, int rank, i
     counts[2 * n_ranks + 3 + r] = have2 ? hp.send2_off[r + 1] - hp.send2_off[r] : 0;
     counts[3 * n_ranks + 3 + r] = have2 ? hp.recv2_off[r + 1] - hp.recv2_off[r] : 0;
   }
+  counts[4 * n_ranks + 3] = hp.cut_level;
   if (owner && !hp.owner.empty()) std::copy(hp.owner.begin(), hp.owner.end(), owner);
   if (pack_idx) std::copy(hp.pack_idx.begin(), hp.pack_idx.end(), pack_idx);
   if (unpack_idx) std::copy(hp.unpack_idx.begin(), hp.unpack_idx.end(), unpack_idx);
@@ -641,9 +642,11 @@ int sfmm_gpu_apply_fin(sfmm_gpu_plan* p, const void* q_dev, const void* recv2_de
   }
 }
 
-int sfmm_gpu_shard_info2(const sfmm_gpu_plan* p, int64_t* send2_counts, int64_t* recv2_counts) {
+int sfmm_gpu_shard_info2(const sfmm_gpu_plan* p, int64_t* send2_counts, int64_t* recv2_counts,
+                         int* cut_level) {
   if (!p) return set_error(SFMM_EINVAL, "null plan");
   const HostPlan& hp = p->hp;
+  if (cut_level) *cut_level = hp.cut_level;
   for (int r = 0; r < hp.n_ranks; ++r) {
     const bool have = hp.send2_off.size() == (size_t)hp.n_ranks + 1;
     if (send2_counts) send2_counts[r] = have ? hp.send2_off[r + 1] - hp.send2_off[r] : 0;

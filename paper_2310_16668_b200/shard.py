@@ -46,7 +46,7 @@ def describe(desc, n_ranks: int, rank: int) -> dict:
     """Host-only shard layout of `rank` (no GPU needed)."""
     lib = _abi.gpu_lib()
     st = _struct(desc)
-    counts = np.zeros(4 * n_ranks + 3, dtype=np.int64)
+    counts = np.zeros(4 * n_ranks + 4, dtype=np.int64)
     _raise(lib.sfmm_gpu_shard_describe(C.byref(st), n_ranks, rank, counts.ctypes.data, None, None,
                                        None, None))
     send = counts[:n_ranks].copy()
@@ -64,7 +64,8 @@ def describe(desc, n_ranks: int, rank: int) -> dict:
             "owner": owner, "pack_idx": pack[: int(send.sum())], "unpack_idx": unpack[: int(recv.sum())],
             "owned_points": owned[:n_owned],
             "send2_counts": counts[2 * n_ranks + 3:3 * n_ranks + 3].copy(),
-            "recv2_counts": counts[3 * n_ranks + 3:].copy()}
+            "recv2_counts": counts[3 * n_ranks + 3:4 * n_ranks + 3].copy(),
+            "cut_level": int(counts[4 * n_ranks + 3])}
 
 
 class ShardedPlan:
@@ -93,8 +94,10 @@ class ShardedPlan:
         self.n_ghost_boxes = ghosts.value
         send2 = np.zeros(n_ranks, dtype=np.int64)
         recv2 = np.zeros(n_ranks, dtype=np.int64)
+        cut = C.c_int(1)
         self.cross_symmetric = bool(lib.sfmm_gpu_shard_info2(self._h, send2.ctypes.data,
-                                                              recv2.ctypes.data))
+                                                              recv2.ctypes.data, C.byref(cut)))
+        self.cut_level = cut.value  # 1: level-1 subtrees per rank, 2: level-2 (level 1 shared)
         self.send2_counts = send2 * self.sw  # in doubles
         self.recv2_counts = recv2 * self.sw
         self._bufs = None

@@ -29,7 +29,13 @@ def test_shard_layout_consistent(n_ranks, dist):
     owner = infos[0]["owner"]
     for inf in infos:
         assert np.array_equal(inf["owner"], owner)  # every rank derives the same split
-    assert set(np.unique(owner)) == set(range(n_ranks))
+    cut = infos[0]["cut_level"]
+    lvl = d.arrays["box_level"]
+    shared = owner == -1
+    assert set(np.unique(owner[~shared])) == set(range(n_ranks))
+    # shared boxes: the internal level-1 boxes of a level-2 cut, nothing else
+    assert np.all(lvl[shared] == 1) and (cut == 2 or not shared.any())
+    assert not np.any(d.arrays["box_leaf"][shared].astype(bool))
     # owned points partition the point set
     pts = np.concatenate([inf["owned_points"] for inf in infos])
     assert np.array_equal(np.sort(pts), np.arange(d.n_points))
@@ -82,20 +88,45 @@ def test_unsorted_colleague_lists_disable_the_fold():
     assert all(int(i["send2_counts"].sum()) == 0 and int(i["recv2_counts"].sum()) == 0 for i in infos)
 
 
-def test_subtrees_are_owned_whole():
-    d, _ = _desc()
-    owner = shard.describe(d, 4, 0)["owner"]
+@pytest.mark.parametrize("dist,n_ranks", [("cube", 4), ("cube", 8), ("gaussian", 8)])
+def test_subtrees_are_owned_whole(dist, n_ranks):
+    d, _ = _desc(dist=dist, n=40000)
+    inf = shard.describe(d, n_ranks, 0)
+    owner, cut = inf["owner"], inf["cut_level"]
     parent = d.arrays["box_parent"]
     lvl = d.arrays["box_level"]
     for b in range(1, d.scalars["n_boxes"]):
-        if lvl[b] >= 2:
+        if lvl[b] > cut:
             assert owner[b] == owner[parent[b]]
+    if cut == 2:  # every level-2 subtree has one owner; the level-1 boxes above them are shared
+        assert np.all(owner[lvl == 2] >= 0)
+
+
+def test_clustered_input_uses_the_level2_cut():
+    # 16-cluster Gaussian (config 3b geometry): level-1 subtrees are far apart
+    # in cost (max/mean 2.21 at 8 ranks); the plan cuts at level 2
+    d, _ = _desc(dist="gaussian", n=60000, tol=1e-8)
+    infos = [shard.describe(d, 8, r) for r in range(8)]
+    assert infos[0]["cut_level"] == 2
+    owner = infos[0]["owner"]
+    lvl = d.arrays["box_level"]
+    assert np.all(owner[(lvl == 1) & ~d.arrays["box_leaf"].astype(bool)] == -1)
+    assert all(i["n_owned_points"] > 0 for i in infos)
+    # every rank receives the shared level-1 slots filled by the other ranks
+    iv = d.arrays["iv_off"]
+    for r, inf in enumerate(infos):
+        idx = inf["unpack_idx"]
+        box_of = np.searchsorted(iv, idx[idx < iv[-1]], side="right") - 1
+        got_shared = np.unique(box_of[owner[box_of] == -1])
+        kids = [c for c in np.nonzero(lvl == 2)[0] if owner[c] != r]
+        assert set(got_shared) == set(d.arrays["box_parent"][kids])
 
 
 def test_too_many_ranks_is_unsupported():
-    d, _ = _desc(dist="square", kernel=0, n=5000, leaf=32)  # 2D: 4 level-1 boxes
+    d, _ = _desc(dist="square", kernel=0, n=5000, leaf=32)  # 2D: 4 level-1, <= 16 level-2 boxes
+    shard.describe(d, 8, 0)  # level-2 cut
     with pytest.raises(NotImplementedError):
-        shard.describe(d, 8, 0)
+        shard.describe(d, 64, 0)
 
 
 def _free_port():
@@ -149,13 +180,15 @@ def test_gloo_world2_exchange_plan():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("n_ranks", [1, 2, 3, 4, 8])
-@pytest.mark.parametrize("case", ["l3d_cube", "l3d_sphere", "h3d_cube"])
+@pytest.mark.parametrize("case", ["l3d_cube", "l3d_sphere", "h3d_cube", "l3d_gaussian"])
 def test_virtual_ranks_match_single_plan(n_ranks, case):
     import torch
     kern, dist, kappa = {"l3d_cube": (1, "cube", 1.0), "l3d_sphere": (1, "sphere", 1.0),
-                         "h3d_cube": (3, "cube", 5.0)}[case]
+                         "h3d_cube": (3, "cube", 5.0), "l3d_gaussian": (1, "gaussian", 1.0)}[case]
     n = 30000 if kern == 1 else 12000
     d, pts = _desc(dist=dist, n=n, leaf=64, kernel=kern, kappa=kappa)
+    if case == "l3d_gaussian" and n_ranks == 8:  # clustered: level-2 cut, shared level-1 boxes
+        assert shard.describe(d, n_ranks, 0)["cut_level"] == 2
     q = host.generate_charges_complex(n, 3) if kern == 3 else host.generate_charges(n, 3)
     u_ref = api.fmm_apply(api.GpuPlan(d), q)
     plans = [shard.ShardedPlan(d, n_ranks, r) for r in range(n_ranks)]

@@ -5,7 +5,7 @@ unpack, translations, column-sum pack, K2b, downward pass, scatter)
 is timed alone on the device with CUDA events, on buffers already holding a
 complete exchange.  On N GPUs the step takes about the slowest rank's time
 plus the ghost all-to-alls, which SURVEY.md 8e estimates at <0.1 % of the step
-over NVLink; it is not included.  Usage: python tools/dev_scaling_projection.py [N]
+over NVLink; it is not included.  Usage: python tools/dev_scaling_projection.py [N [dist [tol [ranks]]]]
 """
 import os
 import sys
@@ -17,9 +17,12 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2310_16668_b200 import api, host, shard  # noqa: E402
 
 n = int(float(sys.argv[1])) if len(sys.argv) > 1 else 10_000_000
+dist = sys.argv[2] if len(sys.argv) > 2 else "cube"
+tol = float(sys.argv[3]) if len(sys.argv) > 3 else 1e-6
+RANKS = [int(x) for x in sys.argv[4].split(",")] if len(sys.argv) > 4 else [2, 4, 8]
 REPS = 10  # timed begin/end pairs per rank (median)
-pts = host.generate_points("cube", n, 1)
-hp = host.HostPlan.build_gpu(1, pts, 128, 1e-6, tree="gpu")
+pts = host.generate_points(dist, n, 1)
+hp = host.HostPlan.build_gpu(1, pts, 128, tol, tree="gpu")
 q = host.generate_charges(n, 1)
 qd = torch.from_numpy(q).cuda()
 ud = torch.zeros_like(qd)
@@ -37,9 +40,9 @@ e1.record(s)
 s.synchronize()
 t1 = e0.elapsed_time(e1) / REPS
 single.close()
-print(f"N={n:.0e}  1 GPU (single plan, graph replay): {t1:.2f} ms")
+print(f"N={n:.0e} {dist} tol={tol:g}  1 GPU (single plan, graph replay): {t1:.2f} ms")
 
-for nr in (2, 4, 8):
+for nr in RANKS:
     plans = [shard.ShardedPlan(hp.desc_struct(), nr, r) for r in range(nr)]
     shard.apply_virtual(plans, qd, ud)  # fills every rank's receive buffer once
     torch.cuda.synchronize()
