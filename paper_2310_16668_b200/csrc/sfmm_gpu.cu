@@ -138,6 +138,8 @@ struct sfmm_gpu_plan {
     if (ev_k2b) cudaEventDestroy(ev_k2b);
     for (cudaEvent_t e : tev) cudaEventDestroy(e);
     if (graph_exec) cudaGraphExecDestroy(graph_exec);
+    for (PhaseGraph& g : phase_graph)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
     if (stream) cudaStreamDestroy(stream);
     (void)cudaGetLastError();
     if (prev >= 0) cudaSetDevice(prev);  // leave the caller's current device as it was
@@ -159,6 +161,49 @@ struct sfmm_gpu_plan {
   const double* graph_q = nullptr;
   double* graph_u = nullptr;
   int graph_nrhs = 0;
+
+  // Sharded applies: one CUDA graph per phase (begin, mid, fin), keyed on the
+  // caller's buffers; a sequence of ~10-30 small launches per phase otherwise
+  // leaves the device idle between them on deep trees.
+  struct PhaseGraph {
+    cudaGraphExec_t exec = nullptr;
+    const void* key[3] = {nullptr, nullptr, nullptr};
+  };
+  PhaseGraph phase_graph[3];
+
+  template <class F>
+  void run_phase(int which, const void* k0, const void* k1, const void* k2, void* user_stream,
+                 cudaStream_t st, F&& enqueue) {
+    static const bool env_graphs = [] {
+      const char* v = std::getenv("SFMM_GRAPHS");
+      return !(v && std::atoi(v) == 0);
+    }();
+    if (!env_graphs || timing || user_stream == nullptr || hp.depth < 2) {
+      enqueue();
+      return;
+    }
+    PhaseGraph& g = phase_graph[which];
+    if (!g.exec || g.key[0] != k0 || g.key[1] != k1 || g.key[2] != k2) {
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+      g.exec = nullptr;
+      cudaGraph_t graph = nullptr;
+      ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
+      try {
+        enqueue();
+      } catch (...) {
+        cudaStreamEndCapture(st, &graph);  // leave the caller's stream usable
+        if (graph) cudaGraphDestroy(graph);
+        throw;
+      }
+      ck(cudaStreamEndCapture(st, &graph), "end capture");
+      ck(cudaGraphInstantiate(&g.exec, graph, 0), "graph instantiate");
+      cudaGraphDestroy(graph);
+      g.key[0] = k0;
+      g.key[1] = k1;
+      g.key[2] = k2;
+    }
+    ck(cudaGraphLaunch(g.exec, st), "graph launch");
+  }
 
   // Phase timing: 6 events per recorded apply (phase boundaries).
   static constexpr int kMaxTimed = 256;
@@ -537,15 +582,16 @@ int sfmm_gpu_apply_begin(sfmm_gpu_plan* p, const void* q_dev, void* send_dev, vo
     DeviceGuard device_guard(p->device);
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : p->stream;
     const double* q = static_cast<const double*>(q_dev);
-    if (p->hp.depth >= 2) {
+    if (p->hp.depth >= 2 && p->dp.n_pack > 0 && !send_dev)
+      throw CudaFail{SFMM_EINVAL, "send buffer required"};
+    p->run_phase(0, q_dev, send_dev, nullptr, stream, st, [&] {
+      if (p->hp.depth < 2) return;
       launch_gather(p->dp, q, p->ds, st);
       for (int l = p->hp.depth; l >= 2; --l) launch_upward(p->dp, p->hp, l, p->ds, st);
-      if (p->dp.n_pack > 0) {
-        if (!send_dev) throw CudaFail{SFMM_EINVAL, "send buffer required"};
-        launch_pack(p->dp, p->ds, static_cast<double*>(send_dev), st);
-      }
-    }
+      if (p->dp.n_pack > 0) launch_pack(p->dp, p->ds, static_cast<double*>(send_dev), st);
+    });
     if (packed_event) ck(cudaEventRecord(static_cast<cudaEvent_t>(packed_event), st), "event");
+    // zeroes U / UH (and, with SFMM_SHARD_OVERLAP=1, runs the interior tasks)
     if (p->hp.depth >= 2) launch_translate(p->dp, p->ds, st, kInteriorTasks);
     ck(cudaGetLastError(), "kernel launch");
     return SFMM_OK;
@@ -602,8 +648,12 @@ int sfmm_gpu_apply_end(sfmm_gpu_plan* p, const void* q_dev, const void* recv_dev
   try {
     DeviceGuard device_guard(p->device);
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : p->stream;
-    apply_mid_impl(p, recv_dev, nullptr, st);
-    apply_fin_impl(p, q_dev, nullptr, u_dev, st);
+    if (p->hp.depth >= 2 && p->dp.n_unpack > 0 && !recv_dev)
+      throw CudaFail{SFMM_EINVAL, "receive buffer required"};
+    p->run_phase(1, recv_dev, q_dev, u_dev, stream, st, [&] {
+      apply_mid_impl(p, recv_dev, nullptr, st);
+      apply_fin_impl(p, q_dev, nullptr, u_dev, st);
+    });
     ck(cudaGetLastError(), "kernel launch");
     return SFMM_OK;
   } catch (const CudaFail& f) {
@@ -618,7 +668,12 @@ int sfmm_gpu_apply_mid(sfmm_gpu_plan* p, const void* recv_dev, void* send2_dev, 
   try {
     DeviceGuard device_guard(p->device);
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : p->stream;
-    apply_mid_impl(p, recv_dev, send2_dev, st);
+    if (p->hp.depth >= 2 && p->dp.n_unpack > 0 && !recv_dev)
+      throw CudaFail{SFMM_EINVAL, "receive buffer required"};
+    if (p->hp.depth >= 2 && p->dp.n_xpairs > 0 && !send2_dev)
+      throw CudaFail{SFMM_EINVAL, "second send buffer required"};
+    p->run_phase(1, recv_dev, send2_dev, nullptr, stream, st,
+                 [&] { apply_mid_impl(p, recv_dev, send2_dev, st); });
     if (packed_event) ck(cudaEventRecord(static_cast<cudaEvent_t>(packed_event), st), "event");
     ck(cudaGetLastError(), "kernel launch");
     return SFMM_OK;
@@ -634,7 +689,10 @@ int sfmm_gpu_apply_fin(sfmm_gpu_plan* p, const void* q_dev, const void* recv2_de
   try {
     DeviceGuard device_guard(p->device);
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : p->stream;
-    apply_fin_impl(p, q_dev, recv2_dev, u_dev, st);
+    if (p->hp.depth >= 2 && p->dp.n_recv2 > 0 && !recv2_dev)
+      throw CudaFail{SFMM_EINVAL, "second receive buffer required"};
+    p->run_phase(2, q_dev, recv2_dev, u_dev, stream, st,
+                 [&] { apply_fin_impl(p, q_dev, recv2_dev, u_dev, st); });
     ck(cudaGetLastError(), "kernel launch");
     return SFMM_OK;
   } catch (const CudaFail& f) {
