@@ -80,15 +80,36 @@ __device__ __forceinline__ double log_tab(const double* __restrict__ tab, double
   return a + b;
 }
 
+// 2-part Cody-Waite reduction in sincos_tab_scaled (A/B, complex K2 at N=2e6:
+// 65.7 -> 63.3 ms; 16-RHS K2m at 4e6: 613.8 -> 606.9 ms)
+#ifndef SFMM_SC_2PART
+#define SFMM_SC_2PART 1
+#endif
+// kappa * r from r^2 and y = 1/r: (kappa r^2) y starts before the rsqrt ends
+#ifndef SFMM_KR_EARLY
+#define SFMM_KR_EARLY 1
+#endif
+#if SFMM_KR_EARLY
+#define KR_ARG(kappa, r2, y) (((kappa) * (r2)) * (y))
+#else
+#define KR_ARG(kappa, r2, y) ((kappa) * ((r2) * (y)))
+#endif
 __device__ __forceinline__ void sincos_tab_scaled(const double2* __restrict__ tab, double x,
                                                   double w, double* re, double* im) {
   const double magic = 6755399441055744.0;  // 1.5 * 2^52: n lands in the low word
   const double nd = fma(x, 40.74366543152520595683, magic);  // 128/pi
   const int k = __double2loint(nd) & (kSinCosTab - 1);
   const double n = nd - magic;
+#if SFMM_SC_2PART
+  // |n| < 2^20 (|x| <= kSinCosTabMaxArg): the 33-bit head of pi/2 times n is
+  // exact and its 53-bit tail leaves an argument error below 1e-22
+  double t = fma(-n, 1.57079632673412561417e+00 / 64, x);
+  t = fma(-n, 6.07710050650619224932e-11 / 64, t);
+#else
   double t = fma(-n, 1.57079632673412561417e+00 / 64, x);
   t = fma(-n, 6.07710050630396597660e-11 / 64, t);
   t = fma(-n, 2.02226624879595063154e-21 / 64, t);
+#endif
   const double z = t * t;
   double ps = fma(z, -1.0 / 5040, 1.0 / 120);
   ps = fma(z, ps, -1.0 / 6);

@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(kMThreads, WH ? SFMM_K2M_MIN_BLOCKS_WH : SFMM_
               const double yv = rsqrt_fp64m(r2);
               if (CPLX) {
                 if constexpr (TAB) {
-                  sincos_tab_scaled(tab, a.kappa * (r2 * yv), yv, &gr[mt], &gi[mt]);
+                  sincos_tab_scaled(tab, KR_ARG(a.kappa, r2, yv), yv, &gr[mt], &gi[mt]);
                 } else {
                   double sn, cs;
                   sincos_fast(a.kappa * (r2 * yv), &sn, &cs);

@@ -374,7 +374,7 @@ __device__ __forceinline__ void inner_cplx(const WarpSmemCplx& sm, const double2
       const double y = rsqrt_fp64(r2);
       double gr, gi;
       if constexpr (TAB) {
-        sincos_tab_scaled(tab, kappa * (r2 * y), y, &gr, &gi);
+        sincos_tab_scaled(tab, KR_ARG(kappa, r2, y), y, &gr, &gi);
       } else {  // arguments beyond the table's exact reduction range
         double s, c;
         sincos_fast(kappa * (r2 * y), &s, &c);
@@ -425,7 +425,7 @@ __device__ __forceinline__ void sym_chunk_cplx(const WarpSmemCplx& sm, const dou
       const double y = rsqrt_fp64(r2);
       double gr, gi;
       if constexpr (TAB) {
-        sincos_tab_scaled(tab, kappa * (r2 * y), y, &gr, &gi);
+        sincos_tab_scaled(tab, KR_ARG(kappa, r2, y), y, &gr, &gi);
       } else {
         double sn, c;
         sincos_fast(kappa * (r2 * y), &sn, &c);
