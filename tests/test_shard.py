@@ -122,6 +122,33 @@ def test_clustered_input_uses_the_level2_cut():
         assert set(got_shared) == set(d.arrays["box_parent"][kids])
 
 
+def _lopsided(seed=3):
+    """A depth-2 tree: two octants split into level-2 boxes, the sparse others
+    stay level-1 leaves (2:1 balance allows leaves only next to level <= 2)."""
+    rng = np.random.default_rng(seed)
+    a = rng.uniform(0.0, 0.5, (300, 3))
+    b = rng.uniform(0.5, 1.0, (300, 3))
+    few = rng.uniform(0.0, 1.0, (200, 3))
+    return np.ascontiguousarray(np.concatenate([a, b, few]))
+
+
+def test_level1_leaves_are_units():
+    pts = _lopsided()
+    d = host.HostPlan.build(1, pts, 64, 1e-6, 1.0).descriptor()
+    leaf1 = np.nonzero((d.arrays["box_level"] == 1) & d.arrays["box_leaf"].astype(bool))[0]
+    assert leaf1.size > 0
+    infos = [shard.describe(d, 8, r) for r in range(8)]
+    assert infos[0]["cut_level"] == 2
+    owner = infos[0]["owner"]
+    assert np.all(owner[leaf1] >= 0)  # owned, not shared
+    pts_owned = np.sort(np.concatenate([i["owned_points"] for i in infos]))
+    assert np.array_equal(pts_owned, np.arange(d.n_points))
+    for p in range(8):
+        for q in range(8):
+            assert infos[p]["send_counts"][q] == infos[q]["recv_counts"][p]
+            assert infos[p]["send2_counts"][q] == infos[q]["recv2_counts"][p]
+
+
 def test_too_many_ranks_is_unsupported():
     d, _ = _desc(dist="square", kernel=0, n=5000, leaf=32)  # 2D: 4 level-1, <= 16 level-2 boxes
     shard.describe(d, 8, 0)  # level-2 cut
@@ -259,9 +286,26 @@ def test_cross_symmetric_plan_requires_mid_fin():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("n_ranks", [2, 3, 4])
+@pytest.mark.parametrize("n_ranks", [4, 8])
+def test_virtual_ranks_level1_leaves(n_ranks):
+    import torch
+    pts = _lopsided()
+    n = pts.shape[0]
+    d = host.HostPlan.build(1, pts, 64, 1e-6, 1.0).descriptor()
+    q = host.generate_charges(n, 4)
+    u_ref = api.fmm_apply(api.GpuPlan(d), q)
+    plans = [shard.ShardedPlan(d, n_ranks, r) for r in range(n_ranks)]
+    qd = torch.from_numpy(q).cuda()
+    ud = torch.zeros_like(qd)
+    shard.apply_virtual(plans, qd, ud)
+    torch.cuda.synchronize()
+    assert rel_l2(ud.cpu().numpy(), u_ref) <= 1e-12
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n_ranks", [2, 3, 4, 8])
 def test_virtual_ranks_2d(n_ranks):
-    # 2D: four level-1 quadrants, so at most four ranks
+    # 2D: four level-1 quadrants; 8 ranks take the level-2 cut
     import torch
     n = 40000
     d, pts = _desc(dist="annulus", n=n, leaf=40, kernel=0, kappa=1.0)
