@@ -208,6 +208,20 @@ int sfmm_gpu_apply_mid(sfmm_gpu_plan* plan, const void* recv_dev, void* send2_de
 int sfmm_gpu_apply_fin(sfmm_gpu_plan* plan, const void* q_dev, const void* recv2_dev, void* u_dev,
                        void* stream);
 
+/* Operators of rank `rank`'s owned boxes without the full T on every rank:
+ * sfmm_gpu_shard_T_runs (host-only) lists the runs [src, src + len) of
+ * desc->T entries (T_off units) the rank needs, in order (n_entries: their
+ * total; runs may be NULL to count); a holder of the full T on a device packs
+ * them with sfmm_gpu_copy_runs (scalars_per_entry 1 real / 2 complex) and
+ * ships the blob (NCCL); sfmm_gpu_plan_create_sharded_T builds the rank's plan
+ * from the blob in its device memory, ignoring desc->T (may be NULL). */
+int sfmm_gpu_shard_T_runs(const sfmm_plan_desc* desc, int n_ranks, int rank, int64_t* n_runs,
+                          int64_t* runs, int64_t* n_entries);
+int sfmm_gpu_copy_runs(const double* src_dev, const int64_t* runs, int64_t n_runs,
+                       int64_t scalars_per_entry, double* dst_dev, int device, void* stream);
+int sfmm_gpu_plan_create_sharded_T(const sfmm_plan_desc* desc, const void* T_owned_dev, int device,
+                                   int n_ranks, int rank, sfmm_gpu_plan** out);
+
 /* Host-only view of rank `rank`'s shard (no device is touched).  counts gets
  * 4*n_ranks + 4 values: send scalars per peer, receive scalars per peer,
  * owned points, ghost boxes, owned boxes, the second exchange's send and

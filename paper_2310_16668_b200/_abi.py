@@ -316,6 +316,13 @@ def gpu_lib() -> C.CDLL:
     lib.sfmm_gpu_apply_end.argtypes = [vp, vp, vp, vp, vp]
     lib.sfmm_gpu_apply_end.restype = C.c_int
     lib.sfmm_gpu_shard_info2.argtypes = [vp, vp, vp, C.POINTER(C.c_int)]
+    lib.sfmm_gpu_shard_T_runs.argtypes = [C.POINTER(PlanDesc), C.c_int, C.c_int, vp, vp, vp]
+    lib.sfmm_gpu_shard_T_runs.restype = C.c_int
+    lib.sfmm_gpu_copy_runs.argtypes = [vp, vp, C.c_int64, C.c_int64, vp, C.c_int, vp]
+    lib.sfmm_gpu_copy_runs.restype = C.c_int
+    lib.sfmm_gpu_plan_create_sharded_T.argtypes = [C.POINTER(PlanDesc), vp, C.c_int, C.c_int,
+                                                   C.c_int, C.POINTER(vp)]
+    lib.sfmm_gpu_plan_create_sharded_T.restype = C.c_int
     lib.sfmm_gpu_shard_info2.restype = C.c_int
     lib.sfmm_gpu_apply_mid.argtypes = [vp, vp, vp, vp, vp]
     lib.sfmm_gpu_apply_mid.restype = C.c_int
@@ -367,4 +374,5 @@ GPU_SYMBOLS = [
     "sfmm_gpu_plan_create_skel", "sfmm_gpu_build_tree", "sfmm_gpu_tree_arrays",
     "sfmm_gpu_tree_destroy", "sfmm_gpu_test_log", "sfmm_gpu_plan_from_points",
     "sfmm_gpu_shard_info2", "sfmm_gpu_apply_mid", "sfmm_gpu_apply_fin",
+    "sfmm_gpu_shard_T_runs", "sfmm_gpu_copy_runs", "sfmm_gpu_plan_create_sharded_T",
 ]

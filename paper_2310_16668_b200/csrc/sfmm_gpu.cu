@@ -313,8 +313,10 @@ const char* sfmm_gpu_version(void) { return "sfmm_gpu 0.1 (sm_100a, FP64)"; }
 
 namespace {
 
+// T_dev: the descriptor's operators in device memory (global T_off layout), or
+// with T_compact only the owned runs concatenated (sfmm_gpu_shard_T_runs order)
 int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
-                sfmm_gpu_plan** out, const double* T_dev = nullptr) {
+                sfmm_gpu_plan** out, const double* T_dev = nullptr, bool T_compact = false) {
   if (!desc || !out) return set_error(SFMM_EINVAL, "sfmm_gpu_plan_create: null argument");
   *out = nullptr;
   sfmm_gpu_plan* p = nullptr;
@@ -419,7 +421,8 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
       const double* T_src = T_dev ? T_dev : desc->T;
       if (!T_src && !hp.T_runs.empty()) throw CudaFail{SFMM_EINVAL, "descriptor has no T"};
       for (const HostPlan::Run& r : hp.T_runs)
-        ck(cudaMemcpyAsync(dp.T + r.dst * sw, T_src + r.src * sw, sizeof(double) * r.len * sw,
+        ck(cudaMemcpyAsync(dp.T + r.dst * sw, T_src + (T_compact ? r.dst : r.src) * sw,
+                           sizeof(double) * r.len * sw,
                            T_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, p->stream),
            "upload T");
       ck(cudaStreamSynchronize(p->stream), "upload T");
@@ -515,6 +518,50 @@ int sfmm_gpu_plan_create_skel(const sfmm_plan_desc* desc, const sfmm_skel_result
   if (!desc->T_off || desc->n_boxes < 0 || desc->T_off[desc->n_boxes] * sw != n_scalars)
     return set_error(SFMM_EINVAL, "sfmm_gpu_plan_create_skel: descriptor T_off does not match the skeletons");
   return create_plan(desc, device, n_ranks, rank, out, T_dev);
+}
+
+int sfmm_gpu_shard_T_runs(const sfmm_plan_desc* desc, int n_ranks, int rank, int64_t* n_runs,
+                          int64_t* runs, int64_t* n_entries) {
+  if (!desc || !n_runs) return set_error(SFMM_EINVAL, "sfmm_gpu_shard_T_runs: null argument");
+  HostPlan hp;
+  std::string err;
+  const int rc = build_host_plan(*desc, hp, err, n_ranks, rank);
+  if (rc != SFMM_OK) return set_error(rc, err);
+  *n_runs = (int64_t)hp.T_runs.size();
+  if (n_entries) *n_entries = hp.T_off.empty() ? 0 : hp.T_off.back();
+  if (runs)
+    for (size_t i = 0; i < hp.T_runs.size(); ++i) {
+      runs[2 * i] = hp.T_runs[i].src;
+      runs[2 * i + 1] = hp.T_runs[i].len;
+    }
+  return SFMM_OK;
+}
+
+int sfmm_gpu_copy_runs(const double* src_dev, const int64_t* runs, int64_t n_runs,
+                       int64_t scalars_per_entry, double* dst_dev, int device, void* stream) {
+  if ((!src_dev || !dst_dev) && n_runs > 0)
+    return set_error(SFMM_EINVAL, "sfmm_gpu_copy_runs: null argument");
+  try {
+    DeviceGuard device_guard(device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int64_t cur = 0;
+    for (int64_t i = 0; i < n_runs; ++i) {
+      const int64_t len = runs[2 * i + 1] * scalars_per_entry;
+      ck(cudaMemcpyAsync(dst_dev + cur, src_dev + runs[2 * i] * scalars_per_entry,
+                         sizeof(double) * len, cudaMemcpyDeviceToDevice, st),
+         "copy runs");
+      cur += len;
+    }
+    return SFMM_OK;
+  } catch (const CudaFail& f) {
+    return set_error(f.code, "sfmm_gpu_copy_runs: " + f.msg);
+  }
+}
+
+int sfmm_gpu_plan_create_sharded_T(const sfmm_plan_desc* desc, const void* T_owned_dev, int device,
+                                   int n_ranks, int rank, sfmm_gpu_plan** out) {
+  return create_plan(desc, device, n_ranks, rank, out, static_cast<const double*>(T_owned_dev),
+                     true);
 }
 
 int sfmm_gpu_shard_info(const sfmm_gpu_plan* p, int64_t* send_counts, int64_t* recv_counts,

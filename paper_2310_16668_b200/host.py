@@ -182,6 +182,15 @@ class HostPlan:
         """(handle, device) of the device-resident skeletons, or None."""
         return (self._skel, self._skel_device) if self._skel is not None else None
 
+    def device_T(self):
+        """(pointer, device, scalars) of the device-resident operators (global
+        T_off layout), or None."""
+        if self._skel is None:
+            return None
+        dev, n = C.c_int(), C.c_int64()
+        ptr = _abi.gpu_lib().sfmm_gpu_skel_device_T(self._skel, C.byref(dev), C.byref(n))
+        return ptr, dev.value, n.value
+
     def fetch_T(self) -> None:
         """Downloads device-resident interpolation operators into this plan
         (no-op when it already has them)."""

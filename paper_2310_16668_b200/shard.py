@@ -68,15 +68,44 @@ def describe(desc, n_ranks: int, rank: int) -> dict:
             "cut_level": int(counts[4 * n_ranks + 3])}
 
 
-class ShardedPlan:
-    """This rank's part of a sharded plan (device resident)."""
+def T_runs(desc, n_ranks: int, rank: int):
+    """Runs (src, len) of desc's T entries that `rank` owns, in the order of
+    its compact operator blob, and their total (host-only)."""
+    lib = _abi.gpu_lib()
+    st = _struct(desc)
+    nr, ne = C.c_int64(), C.c_int64()
+    _raise(lib.sfmm_gpu_shard_T_runs(C.byref(st), n_ranks, rank, C.byref(nr), None, C.byref(ne)))
+    runs = np.zeros((max(1, nr.value), 2), dtype=np.int64)
+    _raise(lib.sfmm_gpu_shard_T_runs(C.byref(st), n_ranks, rank, C.byref(nr), runs.ctypes.data,
+                                     C.byref(ne)))
+    return runs[: nr.value], ne.value
 
-    def __init__(self, desc, n_ranks: int, rank: int, device: int = 0):
+
+def pack_T(src_ptr: int, runs: np.ndarray, scalars_per_entry: int, out, device: int,
+           stream: int = 0) -> None:
+    """Copies the runs of a device-resident full T (src_ptr, e.g. the GPU
+    skeletonizer's result) into the torch float64 device tensor `out`."""
+    runs = np.ascontiguousarray(runs, dtype=np.int64)
+    _raise(_abi.gpu_lib().sfmm_gpu_copy_runs(C.c_void_p(src_ptr), runs.ctypes.data, len(runs),
+                                             scalars_per_entry, C.c_void_p(out.data_ptr()), device,
+                                             C.c_void_p(stream or None)))
+
+
+class ShardedPlan:
+    """This rank's part of a sharded plan (device resident).  T_owned: the
+    rank's operator blob on its device (pack_T / T_runs), for descriptors
+    shared without T."""
+
+    def __init__(self, desc, n_ranks: int, rank: int, device: int = 0, T_owned=None):
         lib = _abi.gpu_lib()
         st = _struct(desc)
         self._h = None
         h = C.c_void_p()
-        _raise(lib.sfmm_gpu_plan_create_sharded(C.byref(st), device, n_ranks, rank, C.byref(h)))
+        if T_owned is not None:
+            _raise(lib.sfmm_gpu_plan_create_sharded_T(C.byref(st), C.c_void_p(T_owned.data_ptr()),
+                                                      device, n_ranks, rank, C.byref(h)))
+        else:
+            _raise(lib.sfmm_gpu_plan_create_sharded(C.byref(st), device, n_ranks, rank, C.byref(h)))
         self._h = h
         self.n_ranks, self.rank, self.device = n_ranks, rank, device
         self.n_points = int(st.n_points)

@@ -253,6 +253,37 @@ def test_virtual_ranks_plan_variants(env, monkeypatch):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("kernel,n_ranks", [(1, 4), (1, 8), (3, 3)])
+def test_sharded_plans_from_device_operator_blobs(kernel, n_ranks):
+    # the descriptor travels without T; each rank's operators are packed from
+    # the device-resident skeletons (what rank 0 ships over NCCL at N=1e8)
+    import torch
+    n = 30000 if kernel == 1 else 12000
+    pts = host.generate_points("cube", n, 1)
+    hp = host.HostPlan.build_gpu(kernel, pts, 64, 1e-6, 5.0, host_T=False, tree="gpu")
+    d = hp.desc_struct()
+    assert not bool(d.T)
+    q = host.generate_charges_complex(n, 3) if kernel == 3 else host.generate_charges(n, 3)
+    u_ref = api.fmm_apply(api.GpuPlan.from_host(hp), q)
+    ptr, dev, n_scalars = hp.device_T()
+    sw = 2 if kernel == 3 else 1
+    plans, total = [], 0
+    for r in range(n_ranks):
+        runs, n_entries = shard.T_runs(d, n_ranks, r)
+        assert int(runs[:, 1].sum()) == n_entries
+        blob = torch.empty(max(1, n_entries * sw), dtype=torch.float64, device="cuda")
+        shard.pack_T(ptr, runs, sw, blob, dev)
+        plans.append(shard.ShardedPlan(d, n_ranks, r, T_owned=blob))
+        total += n_entries * sw
+    assert total <= n_scalars  # shared boxes carry no operators
+    qd = torch.from_numpy(q).cuda()
+    ud = torch.zeros_like(qd)
+    shard.apply_virtual(plans, qd, ud)
+    torch.cuda.synchronize()
+    assert rel_l2(ud.cpu().numpy(), u_ref) <= 1e-12
+
+
+@pytest.mark.gpu
 def test_unsorted_colleague_lists_same_result():
     import torch
     n = 30000
