@@ -257,10 +257,9 @@ def run_sharded(args, ws, rank, local):
     n = int(args.n)
     kern = KERNELS[args.kernel]
     cplx = kern == 3
-    # node-local shared memory for the descriptor (~1.3 kB per point incl. T), else /tmp
-    import shutil
+    # node-local shared memory for the descriptor without T (~0.1 kB per point), else /tmp
     base = "/dev/shm" if (os.path.isdir("/dev/shm") and
-                          shutil.disk_usage("/dev/shm").free > 2000 * n) else "/tmp"
+                          shutil.disk_usage("/dev/shm").free > 300 * n) else "/tmp"
     path = f"{base}/sfmm_bench_{os.environ.get('MASTER_PORT', '0')}"
     t0 = time.perf_counter()
     pts = host.generate_points(args.dist, n, 1)
@@ -268,24 +267,61 @@ def run_sharded(args, ws, rank, local):
          else host.generate_charges(n, 1 ^ CHARGE_STREAM))
     hp = None
     hinfo = {}
+    device_T = args.precompute == "gpu"
     if rank == 0:
         # torchrun sets OMP_NUM_THREADS=1; the other ranks wait at the barrier
         host.set_threads(os.cpu_count() or 1)
+        # GPU precompute keeps T on rank 0's device: the descriptor is shared
+        # without it and every rank receives only its own operators (NCCL)
         hp = (host.HostPlan.build_gpu(kern, pts, args.leaf, args.tol, args.kappa, device=dev,
-                                      tree="gpu")
-              if args.precompute == "gpu" else
+                                      host_T=False, tree="gpu")
+              if device_T else
               host.HostPlan.build(kern, pts, args.leaf, args.tol, args.kappa))
         hinfo = hp.info()
         _share_descriptor(hp, path)
     dist.barrier()
+    if rank != 0:
+        host.set_threads(max(1, (os.cpu_count() or ws) // ws))
     desc = hp.desc_struct() if rank == 0 else _load_descriptor(path)
     t_pre = time.perf_counter() - t0
     t0 = time.perf_counter()
-    plan = shard.ShardedPlan(desc, ws, rank, device=dev)
+    blob = None
+    if device_T:
+        sw = 2 if cplx else 1
+        runs, n_entries = shard.T_runs(desc, ws, rank)
+        all_runs = [None] * ws
+        dist.all_gather_object(all_runs, runs)
+        blob = torch.empty(max(1, n_entries * sw), dtype=torch.float64, device=f"cuda:{dev}")
+        if rank == 0:
+            ptr, _, _ = hp.device_T()
+            for r in range(ws):
+                if r == 0:
+                    shard.pack_T(ptr, all_runs[0], sw, blob, dev)
+                    continue
+                cnt = max(1, int(all_runs[r][:, 1].sum()) * sw)
+                buf = torch.empty(cnt, dtype=torch.float64, device=f"cuda:{dev}")
+                shard.pack_T(ptr, all_runs[r], sw, buf, dev)
+                torch.cuda.synchronize(dev)
+                dist.send(buf if args.backend == "nccl" else buf.cpu(), dst=r)
+                del buf
+        else:
+            if args.backend == "nccl":
+                dist.recv(blob, src=0)
+            else:
+                tmp = torch.empty(blob.numel(), dtype=torch.float64)
+                dist.recv(tmp, src=0)
+                blob.copy_(tmp)
+        torch.cuda.synchronize(dev)
+    plan = shard.ShardedPlan(desc, ws, rank, device=dev, T_owned=blob)
+    del blob
     t_upload = time.perf_counter() - t0
     dist.barrier()
+    # the single-GPU parity check below needs the full operators on rank 0
+    single_fits = n <= 20_000_000
     if rank == 0:
         shutil.rmtree(path, ignore_errors=True)
+        if device_T and not single_fits:
+            hp.release_device_skeletons()
 
     dtype = torch.complex128 if cplx else torch.float64
     q_host = torch.from_numpy(q)
@@ -378,9 +414,12 @@ def run_sharded(args, ws, rank, local):
         ref_t = api.direct_sum_subset(kern, args.kappa, pts, q, targets, device=dev)
         relerr_direct = api.max_rel_err(u_full[targets], ref_t) if targets.size else None
         # parity of the sharded result against the single-GPU plan (same operators)
-        with api.GpuPlan(desc, device=dev) as single:
-            u_single = api.fmm_apply(single, q)
-        relerr_single = float(np.linalg.norm(u_full - u_single) / np.linalg.norm(u_single))
+        relerr_single = None
+        if single_fits:
+            with (api.GpuPlan.from_host(hp, device=dev) if device_T else
+                  api.GpuPlan(desc, device=dev)) as single:
+                u_single = api.fmm_apply(single, q)
+            relerr_single = float(np.linalg.norm(u_full - u_single) / np.linalg.norm(u_single))
         # whole-job reference-equivalent K2 work over the step time, per GPU
         w_ref = 20.0 * pinfo.p_dense + 2.0 * pinfo.p_skel
         achieved = w_ref / (ms_step * 1e-3) / ws / 1e12

@@ -389,3 +389,4 @@ def test_bench_sharded_line_two_ranks_gloo(tmp_path):
     line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["gpu_launches"] > 0
     assert line["relerr_vs_single_gpu"] <= 1e-12
+    assert line["relerr_vs_direct"] <= 1e-4
