@@ -553,8 +553,19 @@ void run_skeletons(const sfmm_tree_desc& t, int kernel, double kappa, double tol
     DevBuf<int64_t> d_iv_off, d_sk_off, d_T_off;
     DevBuf<int32_t> d_iv, d_skel, d_red, d_k, d_colid;
     DevBuf<double> d_T;
+    std::vector<double> h_T;  // the level's T moved to the host (device memory short)
+    bool T_host = false;
   };
   std::vector<Level> L(depth + 1);
+  // Moves a level's operators to the host and frees the device buffer.
+  auto spill = [&](Level& lv, size_t nt) {
+    lv.h_T.resize(nt);
+    if (nt) ck(cudaMemcpy(lv.h_T.data(), lv.d_T.p, nt * sizeof(double), cudaMemcpyDeviceToHost), "D2H T");
+    cudaFree(lv.d_T.p);
+    lv.d_T.p = nullptr;
+    lv.d_T.n = 0;
+    lv.T_host = true;
+  };
 #ifndef SFMM_SKEL_WORK_GB
 #define SFMM_SKEL_WORK_GB 12
 #endif
@@ -733,6 +744,23 @@ void run_skeletons(const sfmm_tree_desc& t, int kernel, double kappa, double tol
       std::fprintf(stderr, "[skel] level %d: %d boxes, %zu batches, nmax %lld, %.3f s\n", l, nl,
                    batch_start.size() - 1, (long long)nmax, secs(t_lv, now()));
     lv.k = kk_all;
+    // the level's T buffer was sized for k r <= n^2/4 per box: keep only the
+    // exact part (on the host when even that no longer fits, e.g. N=1e8)
+    if (l >= 2) {
+      const size_t nt = (size_t)lv.T_off[nl] * SW;
+      if (nt < lv.d_T.n) {
+        double* exact = nullptr;
+        if (cudaMalloc(&exact, std::max<size_t>(nt, 1) * sizeof(double)) == cudaSuccess) {
+          if (nt) ck(cudaMemcpy(exact, lv.d_T.p, nt * sizeof(double), cudaMemcpyDeviceToDevice), "compact T");
+          cudaFree(lv.d_T.p);
+          lv.d_T.p = exact;
+          lv.d_T.n = nt;
+        } else {
+          (void)cudaGetLastError();
+          spill(lv, nt);
+        }
+      }
+    }
     for (int i = 0; i < nl; ++i) {
       R.k_max = std::max(R.k_max, kk_all[i]);
       R.saturated += sat_all[i];
@@ -764,7 +792,21 @@ void run_skeletons(const sfmm_tree_desc& t, int kernel, double kappa, double tol
   R.have_host_T = false;
   R.T.clear();
   ck(cudaGetDevice(&R.device), "cudaGetDevice");
-  ck(cudaMalloc(&R.d_T, std::max<size_t>(R.t_scalars(), 1) * sizeof(double)), "cudaMalloc T");
+  d_work.alloc(0);  // the proxy workspace is no longer needed
+  // the result's T; levels still on the device move to the host (largest
+  // first) until it fits
+  while (cudaMalloc(&R.d_T, std::max<size_t>(R.t_scalars(), 1) * sizeof(double)) != cudaSuccess) {
+    (void)cudaGetLastError();
+    int big = -1;
+    for (int l = 2; l <= depth; ++l)
+      if (!L[l].T_host && L[l].d_T.p && (big < 0 || L[l].d_T.n > L[big].d_T.n)) big = l;
+    if (big < 0) {
+      ck(cudaErrorMemoryAllocation, "cudaMalloc T");
+      break;
+    }
+    spill(L[big], L[big].d_T.n);
+    if (verbose) std::fprintf(stderr, "[skel] level %d operators staged on the host\n", big);
+  }
   for (int l = 0; l <= depth; ++l) {
     const int b0 = t.level_begin[l], nl = t.level_begin[l + 1] - b0;
     if (nl == 0) continue;
@@ -777,9 +819,12 @@ void run_skeletons(const sfmm_tree_desc& t, int kernel, double kappa, double tol
     if (niv - nsk)
       ck(cudaMemcpy(R.red_pos.data() + R.rd_off[b0], lv.d_red.p, (niv - nsk) * 4, cudaMemcpyDeviceToHost),
          "D2H red");
-    if (nt)
+    if (nt && lv.T_host)
+      ck(cudaMemcpy(R.d_T + R.T_off[b0] * SW, lv.h_T.data(), nt * SW * 8, cudaMemcpyHostToDevice), "H2D T");
+    else if (nt)
       ck(cudaMemcpy(R.d_T + R.T_off[b0] * SW, lv.d_T.p, nt * SW * 8, cudaMemcpyDeviceToDevice), "D2D T");
-    lv.d_T.alloc(0);  // release the level's (upper-bound sized) buffer early
+    std::vector<double>().swap(lv.h_T);
+    lv.d_T.alloc(0);  // release the level's buffer early
   }
   R.poff.resize(nb);
   ck(cudaMemcpy(R.poff.data(), d_poff.p, nb * sizeof(int32_t), cudaMemcpyDeviceToHost), "D2H poff");
