@@ -312,8 +312,10 @@ def run_sharded(args, ws, rank, local):
                 dist.recv(tmp, src=0)
                 blob.copy_(tmp)
         torch.cuda.synchronize(dev)
+        torch.cuda.empty_cache()  # rank 0's pack buffers: give the plan its memory back
     plan = shard.ShardedPlan(desc, ws, rank, device=dev, T_owned=blob)
     del blob
+    torch.cuda.empty_cache()
     t_upload = time.perf_counter() - t0
     dist.barrier()
     # the single-GPU parity check below needs the full operators on rank 0

@@ -748,7 +748,10 @@ void run_skeletons(const sfmm_tree_desc& t, int kernel, double kappa, double tol
     // exact part (on the host when even that no longer fits, e.g. N=1e8)
     if (l >= 2) {
       const size_t nt = (size_t)lv.T_off[nl] * SW;
-      if (nt < lv.d_T.n) {
+      static const bool force_host = std::getenv("SFMM_SKEL_HOST_STAGING") != nullptr;  // tests
+      if (force_host) {
+        spill(lv, nt);
+      } else if (nt < lv.d_T.n) {
         double* exact = nullptr;
         if (cudaMalloc(&exact, std::max<size_t>(nt, 1) * sizeof(double)) == cudaSuccess) {
           if (nt) ck(cudaMemcpy(exact, lv.d_T.p, nt * sizeof(double), cudaMemcpyDeviceToDevice), "compact T");

@@ -5,6 +5,8 @@ own tests: accuracy of the resulting apply against the dense sum
 (test_apply.cpp:108-162), the ID far-field property and skeleton nesting
 (acceptance.cpp C6), and apply parity on the GPU-built operators.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -156,3 +158,28 @@ def test_saturated_skeletons_small_proxy():
     u = api.fmm_apply(api.GpuPlan(d), q)
     u_ref, _ = po.oracle_apply(d, q)
     assert rel_l2(u, u_ref) <= 1e-12
+
+
+@pytest.mark.gpu
+def test_host_staged_level_operators_are_identical():
+    # N=1e8 stages level operators through host memory when the device is
+    # short (skel_gpu.cu); forced here on a small tree, the result must not move
+    import hashlib
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys, hashlib; sys.path.insert(0, %r)\n"
+            "from paper_2310_16668_b200 import host\n"
+            "pts = host.generate_points('cube', 30000, 2)\n"
+            "hp = host.HostPlan.build_gpu(1, pts, 64, 1e-6)\n"
+            "a = hp.descriptor().arrays\n"
+            "print(hashlib.sha256(a['T'].tobytes() + a['skel_pos'].tobytes()).hexdigest(), a['T'].size)\n"
+            % root)
+    outs = []
+    for extra in ({}, {"SFMM_SKEL_HOST_STAGING": "1"}):
+        env = dict(os.environ, **extra)
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                           timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(r.stdout.split())
+    assert outs[0] == outs[1] and int(outs[0][1]) > 0
