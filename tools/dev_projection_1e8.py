@@ -37,12 +37,13 @@ def rate_1gpu(n1):
             api.fmm_apply_device(p, q.data_ptr(), u.data_ptr(), 1, s.cuda_stream)
         e1.record(s)
         s.synchronize()
+        w = p.info().p_dense
     hp.release_device_skeletons()
-    return n1 / (e0.elapsed_time(e1) / REPS * 1e-3)
+    return n1 / (e0.elapsed_time(e1) / REPS * 1e-3), w
 
 
-r1 = rate_1gpu(10_000_000)
-print(f"1 GPU, N=1e7: {r1 / 1e6:.1f} Mpoints/s", flush=True)
+r1, w1 = rate_1gpu(10_000_000)
+print(f"1 GPU, N=1e7: {r1 / 1e6:.1f} Mpoints/s, {w1 / 1e7:.0f} dense pairs per point", flush=True)
 t0 = time.perf_counter()
 pts = host.generate_points("cube", n, 1)
 hp = host.HostPlan.build_gpu(1, pts, 128, 1e-6, host_T=False, tree="gpu")
@@ -85,6 +86,7 @@ for r in range(nr):
     s.synchronize()
     t = float(np.median([ev[i].elapsed_time(ev[i + 1]) for i in range(REPS)]))
     times.append(t)
+    w8 = p.info().p_dense  # global pair count (same on every rank)
     print(f"rank {r}: {p.n_owned_points} points, {p.n_ghost_boxes} ghost boxes, cut {p.cut_level}, "
           f"plan {t_plan:.1f} s, {t:.2f} ms per apply", flush=True)
     p.close()
@@ -94,3 +96,7 @@ rate = n / (tmax * 1e-3)
 print(f"{nr} GPUs, N={n:.0e}: max rank {tmax:.2f} ms (mean {np.mean(times):.2f}) -> "
       f"{rate / 1e6:.1f} Mpoints/s projected; {rate / r1:.2f}x the 1-GPU rate at 1e7 "
       f"(efficiency {rate / (nr * r1):.3f})", flush=True)
+# the deeper tree does more work per point: compare device time per dense pair
+t1_equiv = w8 / (w1 / (1e7 / r1))  # seconds one GPU would need at the 1e7 pair rate
+print(f"{w8 / n:.0f} dense pairs per point at N={n:.0e} ({w8 / n / (w1 / 1e7):.3f}x 1e7); "
+      f"work-adjusted efficiency {t1_equiv / (nr * tmax * 1e-3):.3f}", flush=True)
