@@ -214,7 +214,9 @@ int sfmm_gpu_apply_fin(sfmm_gpu_plan* plan, const void* q_dev, const void* recv2
  * total; runs may be NULL to count); a holder of the full T on a device packs
  * them with sfmm_gpu_copy_runs (scalars_per_entry 1 real / 2 complex) and
  * ships the blob (NCCL); sfmm_gpu_plan_create_sharded_T builds the rank's plan
- * from the blob in its device memory, ignoring desc->T (may be NULL). */
+ * from the blob in its device memory, ignoring desc->T (may be NULL).
+ * copy_runs with a NULL stream returns after the copies complete; plan
+ * creation waits for all outstanding device work before reading the blob. */
 int sfmm_gpu_shard_T_runs(const sfmm_plan_desc* desc, int n_ranks, int rank, int64_t* n_runs,
                           int64_t* runs, int64_t* n_entries);
 int sfmm_gpu_copy_runs(const double* src_dev, const int64_t* runs, int64_t n_runs,

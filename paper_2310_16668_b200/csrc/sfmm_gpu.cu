@@ -418,6 +418,9 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
       }
       // interpolation operators of the owned boxes, copied run by run
       dp.T = p->alloc<double>((size_t)hp.T_off[hp.n_boxes] * sw);
+      // device operators may still be in flight on another stream (a pack on
+      // the legacy stream, an NCCL receive): the plan's stream is non-blocking
+      if (T_dev) ck(cudaDeviceSynchronize(), "wait for T");
       const double* T_src = T_dev ? T_dev : desc->T;
       if (!T_src && !hp.T_runs.empty()) throw CudaFail{SFMM_EINVAL, "descriptor has no T"};
       for (const HostPlan::Run& r : hp.T_runs)
@@ -552,6 +555,7 @@ int sfmm_gpu_copy_runs(const double* src_dev, const int64_t* runs, int64_t n_run
          "copy runs");
       cur += len;
     }
+    if (!stream) ck(cudaStreamSynchronize(st), "copy runs");  // NULL stream: complete on return
     return SFMM_OK;
   } catch (const CudaFail& f) {
     return set_error(f.code, "sfmm_gpu_copy_runs: " + f.msg);
