@@ -257,9 +257,11 @@ def run_sharded(args, ws, rank, local):
     n = int(args.n)
     kern = KERNELS[args.kernel]
     cplx = kern == 3
-    # node-local shared memory for the descriptor without T (~0.1 kB per point), else /tmp
+    # node-local shared memory for the descriptor (~0.1 kB per point without T, ~1.3 kB
+    # with it), else /tmp
+    per_point = 300 if args.precompute == "gpu" else 2000
     base = "/dev/shm" if (os.path.isdir("/dev/shm") and
-                          shutil.disk_usage("/dev/shm").free > 300 * n) else "/tmp"
+                          shutil.disk_usage("/dev/shm").free > per_point * n) else "/tmp"
     path = f"{base}/sfmm_bench_{os.environ.get('MASTER_PORT', '0')}"
     t0 = time.perf_counter()
     pts = host.generate_points(args.dist, n, 1)
