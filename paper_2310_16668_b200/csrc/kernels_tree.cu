@@ -472,8 +472,10 @@ __device__ __forceinline__ double2 xadd(double2 a, double2 b) {
   return make_double2(a.x + b.x, a.y + b.y);
 }
 
-// Second exchange: one CTA per cross-rank pair sums the pair's staged column
-// sums over its row tiles (fixed tile order) into the send buffer.
+// Second exchange: one CTA per (peer, receiving box) group sums the group's
+// staged column sums over its row tiles (fixed tile order) into the send
+// buffer.  The tile offsets are staged in shared memory first so the value
+// loads of several tiles are in flight at once (the adds stay in order).
 template <class S>
 __global__ void __launch_bounds__(256) k_xpack(const int64_t* __restrict__ tile_off,
                                                const int64_t* __restrict__ tile_u,
@@ -482,16 +484,34 @@ __global__ void __launch_bounds__(256) k_xpack(const int64_t* __restrict__ tile_
                                                const int32_t* __restrict__ nu,
                                                const int32_t* __restrict__ nh,
                                                const S* __restrict__ St, S* __restrict__ buf) {
+  constexpr int kT = 128;  // tiles staged per round
+  __shared__ int64_t su[kT], sh[kT];
   const int64_t i = blockIdx.x, t0 = tile_off[i], t1 = tile_off[i + 1];
   const int n_u = nu[i], n = n_u + nh[i];
   S* out = buf + dst[i];
-  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+  for (int j0 = 0; j0 < n; j0 += blockDim.x) {
+    const int j = j0 + threadIdx.x;
     S s = S{};
-    for (int64_t t = t0; t < t1; ++t) {
-      const int64_t o = j < n_u ? tile_u[t] + j : (tile_h[t] >= 0 ? tile_h[t] + (j - n_u) : -1);
-      if (o >= 0) s = xadd(s, St[o]);
+    for (int64_t c0 = t0; c0 < t1; c0 += kT) {
+      const int cnt = (int)(t1 - c0 < kT ? t1 - c0 : kT);
+      __syncthreads();
+      for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
+        su[t] = tile_u[c0 + t];
+        sh[t] = tile_h[c0 + t];
+      }
+      __syncthreads();
+      if (j < n) {
+        if (j < n_u) {
+#pragma unroll 4
+          for (int t = 0; t < cnt; ++t) s = xadd(s, St[su[t] + j]);
+        } else {
+#pragma unroll 4
+          for (int t = 0; t < cnt; ++t)
+            if (sh[t] >= 0) s = xadd(s, St[sh[t] + (j - n_u)]);
+        }
+      }
     }
-    out[j] = s;
+    if (j < n) out[j] = s;
   }
 }
 
