@@ -355,6 +355,12 @@ __global__ void __launch_bounds__(kThreads, SFMM_K2_MIN_BLOCKS) k2_translate_rea
 #define SFMM_K2C_UNROLL 2
 #endif
 constexpr int kK2cUnroll = SFMM_K2C_UNROLL;
+// rotation steps per loop trip in sym_chunk_cplx (A/B at 2e6, K2 ms: 2 63.2,
+// 1 61.6, 4 65.5)
+#ifndef SFMM_K2C_SYM_UNROLL
+#define SFMM_K2C_SYM_UNROLL 1
+#endif
+constexpr int kSymCplxUnroll = SFMM_K2C_SYM_UNROLL;
 template <int R, bool H, bool SELF, bool TAB>
 __device__ __forceinline__ void inner_cplx(const WarpSmemCplx& sm, const double2* __restrict__ tab,
                                            int cnt, int j0, double kappa,
@@ -409,7 +415,7 @@ __device__ __forceinline__ void sym_chunk_cplx(const WarpSmemCplx& sm, const dou
   double2 cp = make_double2(0.0, 0.0), ch = make_double2(0.0, 0.0);
   const int from = (lane + 1) & 31;
   const int cnt = n_c - j0;  // valid columns of this chunk (may exceed 32)
-#pragma unroll 2
+#pragma unroll kSymCplxUnroll
   for (int s = 0; s < 32; ++s) {
     const int jc = (lane + s) & 31;
     const double2 xy = sm.xy[jc];
