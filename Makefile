@@ -16,7 +16,7 @@ CXXFLAGS := -std=c++17 -O2 -fopenmp -fPIC -Iinclude -I$(SRC) -I/usr/local/cuda/i
 GPU_CU   := $(SRC)/kernels_translate.cu $(SRC)/kernels_tree.cu $(SRC)/kernels_probe.cu $(SRC)/kernels_multi.cu $(SRC)/skel_gpu.cu \
             $(SRC)/tree_gpu.cu $(SRC)/sfmm_gpu.cu
 GPU_OBJS := $(patsubst $(SRC)/%.cu,$(OBJ)/%.o,$(GPU_CU)) $(OBJ)/plan_build.o
-HDRS     := include/sfmm_gpu.h $(SRC)/common.cuh $(SRC)/launch.h $(SRC)/plan_build.h
+HDRS     := include/sfmm_gpu.h $(SRC)/common.cuh $(SRC)/launch.h $(SRC)/plan_build.h $(SRC)/fastmath.cuh $(SRC)/log_table.inc
 
 .PHONY: all gpu host oracle clean
 all: gpu host

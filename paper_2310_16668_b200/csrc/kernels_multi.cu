@@ -131,12 +131,13 @@ __global__ void __launch_bounds__(kMThreads, WH ? SFMM_K2M_MIN_BLOCKS_WH : SFMM_
   __shared__ ChunkM<CPLX> ch;
   __shared__ int s_task;
   __shared__ double2 tab[CPLX ? kSinCosTab : 1];
-  __shared__ double ltab[KER == SFMM_LAPLACE2D ? 3 * kLogTab : 1];
+  __shared__ __align__(16) double ltab[KER == SFMM_LAPLACE2D ? kLogTabLen : 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (CPLX && TAB)
     for (int i = tid; i < kSinCosTab; i += blockDim.x) tab[i] = a.tab[i];
   if (KER == SFMM_LAPLACE2D)
-    for (int i = tid; i < 3 * kLogTab; i += blockDim.x) ltab[i] = a.ltab[i];
+    for (int i = tid; i < kLogTabLen; i += blockDim.x) ltab[i] = a.ltab[i];
+  const uint32_t lts = log_tab_addr(ltab);
   const int rq = lane >> 2, kq = lane & 3;  // A-fragment row / k index of this lane
   for (;;) {
     __syncthreads();
@@ -294,7 +295,7 @@ __global__ void __launch_bounds__(kMThreads, WH ? SFMM_K2M_MIN_BLOCKS_WH : SFMM_
               r2 = fma(dz, dz, r2);
             }
             if (KER == SFMM_LAPLACE2D) {
-              gr[mt] = log_tab(ltab, r2);
+              gr[mt] = log_tab(lts, r2);
               gi[mt] = 0.0;
             } else {
               const double yv = rsqrt_fp64m(r2);

@@ -31,12 +31,12 @@ __global__ void sincos_check(const double* x, int64_t n, const double2* tab, dou
 
 namespace {
 __global__ void log_check(const double* x, int64_t n, const double* tab, double* out) {
-  __shared__ double lt[3 * kLogTab];
-  for (int i = threadIdx.x; i < 3 * kLogTab; i += blockDim.x) lt[i] = tab[i];
+  __shared__ __align__(16) double lt[kLogTabLen];
+  for (int i = threadIdx.x; i < kLogTabLen; i += blockDim.x) lt[i] = tab[i];
   __syncthreads();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    out[2 * i] = log_tab(lt, x[i]);
+    out[2 * i] = log_tab(log_tab_addr(lt), x[i]);
     out[2 * i + 1] = log(x[i]);
   }
 }
@@ -44,7 +44,7 @@ __global__ void log_check(const double* x, int64_t n, const double* tab, double*
 
 int test_log(const double* x_host, int64_t n, double* out_host) {
   double *dx = nullptr, *dout = nullptr, *dtab = nullptr;
-  double tab[3 * kLogTab];
+  double tab[kLogTabLen];
   fill_log_table(tab);
   int rc = -1;
   if (cudaMalloc(&dx, std::max<int64_t>(n, 1) * sizeof(double)) == cudaSuccess &&

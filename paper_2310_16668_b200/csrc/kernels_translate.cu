@@ -81,11 +81,11 @@ struct GenLaplace3d {  // kernel.hpp:46-50  1/(4 pi r)
   static constexpr int kDim = 3;
   static constexpr double kScale = kInv4Pi;
   static constexpr bool kLogTable = false;
-  __device__ static __forceinline__ double g(double r2, const double*) { return rsqrt_fp64(r2); }
+  __device__ static __forceinline__ double g(double r2, uint32_t) { return rsqrt_fp64(r2); }
   // M independent evaluations, stage by stage, so their dependent chains
   // interleave in the issue stream.
   template <int M>
-  __device__ static __forceinline__ void batch(const double* r2, double* g, const double*) {
+  __device__ static __forceinline__ void batch(const double* r2, double* g, uint32_t) {
     double y[M], e[M];
 #pragma unroll
     for (int m = 0; m < M; ++m) asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y[m]) : "d"(r2[m]));
@@ -99,9 +99,9 @@ struct GenLaplace2d {  // kernel.hpp:40-44  -log(r^2)/(4 pi)
   static constexpr int kDim = 2;
   static constexpr double kScale = -kInv4Pi;
   static constexpr bool kLogTable = true;  // log_tab with the table in shared memory
-  __device__ static __forceinline__ double g(double r2, const double* lt) { return log_tab(lt, r2); }
+  __device__ static __forceinline__ double g(double r2, uint32_t lt) { return log_tab(lt, r2); }
   template <int M>
-  __device__ static __forceinline__ void batch(const double* r2, double* g, const double* lt) {
+  __device__ static __forceinline__ void batch(const double* r2, double* g, uint32_t lt) {
 #pragma unroll
     for (int m = 0; m < M; ++m) g[m] = log_tab(lt, r2[m]);
   }
@@ -139,7 +139,7 @@ __device__ __noinline__ void verify_row(const K2Args& a, int32_t b, int32_t row,
 }
 
 template <class G, int R, bool H, bool SELF>
-__device__ __forceinline__ void inner_real(const WarpSmemReal& sm, const double* lt, int cnt, int j0,
+__device__ __forceinline__ void inner_real(const WarpSmemReal& sm, uint32_t lt, int cnt, int j0,
                                            const double (&xi)[R], const double (&yi)[R],
                                            const double (&zi)[R], const int (&rowi)[R],
                                            double (&au)[R], double (&ah)[R]) {
@@ -173,7 +173,7 @@ __device__ __forceinline__ void inner_real(const WarpSmemReal& sm, const double*
 // the complete sum of column l over the warp's 32R rows.  Fixed order, no
 // butterfly, two column accumulators per lane.
 template <class G, int R, bool H>
-__device__ __forceinline__ void sym_chunk(const WarpSmemReal& sm, const double* lt, int j0, int n_c,
+__device__ __forceinline__ void sym_chunk(const WarpSmemReal& sm, uint32_t lt, int j0, int n_c,
                                           int k_c,
                                           const double (&xi)[R], const double (&yi)[R],
                                           const double (&zi)[R], const double (&qr)[R],
@@ -220,7 +220,7 @@ __device__ __forceinline__ void sym_chunk(const WarpSmemReal& sm, const double* 
 
 template <class G, int R>
 __device__ __forceinline__ void task_real(const K2Args& a, const Task& t, WarpSmemReal& sm,
-                                          const double* lt, int lane) {
+                                          uint32_t lt, int lane) {
   const BoxRec tb = a.box[t.box];
   double xi[R], yi[R], zi[R], au[R], ah[R], qr[R], qhr[R];
   int rowi[R];
@@ -316,11 +316,12 @@ template <class G>
 #endif
 __global__ void __launch_bounds__(kThreads, SFMM_K2_MIN_BLOCKS) k2_translate_real(K2Args a) {
   __shared__ WarpSmemReal smem[kWarps];
-  __shared__ double ltab[G::kLogTable ? 3 * kLogTab : 1];
+  __shared__ __align__(16) double ltab[G::kLogTable ? kLogTabLen : 1];
   if (G::kLogTable) {
-    for (int i = threadIdx.x; i < 3 * kLogTab; i += blockDim.x) ltab[i] = a.ltab[i];
+    for (int i = threadIdx.x; i < kLogTabLen; i += blockDim.x) ltab[i] = a.ltab[i];
     __syncthreads();
   }
+  const uint32_t lts = log_tab_addr(ltab);
   const int lane = threadIdx.x & 31;
   WarpSmemReal& sm = smem[threadIdx.x >> 5];
   for (;;) {
@@ -333,14 +334,14 @@ __global__ void __launch_bounds__(kThreads, SFMM_K2_MIN_BLOCKS) k2_translate_rea
 #define SFMM_K2_MAX_R 4
 #endif
     switch ((task.nrows + 31) >> 5) {
-      case 1: task_real<G, 1>(a, task, sm, ltab, lane); break;
+      case 1: task_real<G, 1>(a, task, sm, lts, lane); break;
 #if SFMM_K2_MAX_R >= 2
-      case 2: task_real<G, 2>(a, task, sm, ltab, lane); break;
+      case 2: task_real<G, 2>(a, task, sm, lts, lane); break;
 #endif
 #if SFMM_K2_MAX_R >= 3
-      case 3: task_real<G, 3>(a, task, sm, ltab, lane); break;
+      case 3: task_real<G, 3>(a, task, sm, lts, lane); break;
 #endif
-      default: task_real<G, SFMM_K2_MAX_R>(a, task, sm, ltab, lane); break;
+      default: task_real<G, SFMM_K2_MAX_R>(a, task, sm, lts, lane); break;
     }
   }
 }

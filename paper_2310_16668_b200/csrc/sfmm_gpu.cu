@@ -412,7 +412,7 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
         double d2 = 0;
         for (int k = 0; k < hp.dim; ++k) d2 += (hi[k] - lo[k]) * (hi[k] - lo[k]);
         dp.sc_tab_ok = std::fabs(hp.kappa) * std::sqrt(d2) <= kSinCosTabMaxArg;
-        std::vector<double> lt(3 * kLogTab);
+        std::vector<double> lt(kLogTabLen);
         fill_log_table(lt.data());
         dp.log_tab = p->upload(lt);
       }
