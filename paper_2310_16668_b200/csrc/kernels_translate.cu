@@ -310,11 +310,21 @@ __device__ __forceinline__ void task_real(const K2Args& a, const Task& t, WarpSm
   }
 }
 
-template <class G>
 #ifndef SFMM_K2_MIN_BLOCKS
 #define SFMM_K2_MIN_BLOCKS 4
 #endif
-__global__ void __launch_bounds__(kThreads, SFMM_K2_MIN_BLOCKS) k2_translate_real(K2Args a) {
+// Plans whose every task has <= 32 rows (small trees, config-1 sized) run a
+// 1-row-per-lane instantiation capped at 64 registers: twice the resident
+// warps to hide the dependent generation chains (the 128-register kernel
+// carries the R = 4 variant's register budget).
+#ifndef SFMM_K2_R1_MIN_BLOCKS
+#define SFMM_K2_R1_MIN_BLOCKS 8
+#endif
+#ifndef SFMM_K2_MAX_R
+#define SFMM_K2_MAX_R 4
+#endif
+template <class G, int MAXR, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k2_translate_real_t(K2Args a) {
   __shared__ WarpSmemReal smem[kWarps];
   __shared__ __align__(16) double ltab[G::kLogTable ? kLogTabLen : 1];
   if (G::kLogTable) {
@@ -330,20 +340,26 @@ __global__ void __launch_bounds__(kThreads, SFMM_K2_MIN_BLOCKS) k2_translate_rea
     t = __shfl_sync(kFull, t, 0);
     if (t >= a.n_tasks) return;
     const Task task = a.tasks[t];
-#ifndef SFMM_K2_MAX_R
-#define SFMM_K2_MAX_R 4
-#endif
-    switch ((task.nrows + 31) >> 5) {
-      case 1: task_real<G, 1>(a, task, sm, lts, lane); break;
+    if constexpr (MAXR == 1) {
+      task_real<G, 1>(a, task, sm, lts, lane);
+    } else {
+      switch ((task.nrows + 31) >> 5) {
+        case 1: task_real<G, 1>(a, task, sm, lts, lane); break;
 #if SFMM_K2_MAX_R >= 2
-      case 2: task_real<G, 2>(a, task, sm, lts, lane); break;
+        case 2: task_real<G, 2>(a, task, sm, lts, lane); break;
 #endif
 #if SFMM_K2_MAX_R >= 3
-      case 3: task_real<G, 3>(a, task, sm, lts, lane); break;
+        case 3: task_real<G, 3>(a, task, sm, lts, lane); break;
 #endif
-      default: task_real<G, SFMM_K2_MAX_R>(a, task, sm, lts, lane); break;
+        default: task_real<G, SFMM_K2_MAX_R>(a, task, sm, lts, lane); break;
+      }
     }
   }
+}
+template <class G>
+constexpr auto k2_real_kernel(bool r1) {
+  return r1 ? k2_translate_real_t<G, 1, SFMM_K2_R1_MIN_BLOCKS>
+            : k2_translate_real_t<G, SFMM_K2_MAX_R, SFMM_K2_MIN_BLOCKS>;
 }
 
 // ---------------------------------------------------------------------------
@@ -678,11 +694,11 @@ int configure_translate(DevPlan& p, int device) {
   if (p.kernel == SFMM_HELMHOLTZ3D)
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_translate_cplx<true>, kThreads, 0);
   else if (p.kernel == SFMM_LAPLACE3D)
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_translate_real<GenLaplace3d>,
-                                                      kThreads, 0);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, k2_real_kernel<GenLaplace3d>(p.k2_r1), kThreads, 0);
   else
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_translate_real<GenLaplace2d>,
-                                                      kThreads, 0);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, k2_real_kernel<GenLaplace2d>(p.k2_r1), kThreads, 0);
   if (e != cudaSuccess) return -1;
   if (per_sm < 1) per_sm = 1;
   p.k2_grid = sms * per_sm;
@@ -733,9 +749,9 @@ void launch_translate(const DevPlan& p, DevState& s, cudaStream_t st, TranslateP
       else
         k2_translate_cplx<false><<<grid, kThreads, 0, st>>>(a);
     else if (p.kernel == SFMM_LAPLACE3D)
-      k2_translate_real<GenLaplace3d><<<grid, kThreads, 0, st>>>(a);
+      k2_real_kernel<GenLaplace3d>(p.k2_r1)<<<grid, kThreads, 0, st>>>(a);
     else
-      k2_translate_real<GenLaplace2d><<<grid, kThreads, 0, st>>>(a);
+      k2_real_kernel<GenLaplace2d>(p.k2_r1)<<<grid, kThreads, 0, st>>>(a);
   }
   if (part != kInteriorTasks && reduce) launch_stage_reduce(p, s, st);
 }

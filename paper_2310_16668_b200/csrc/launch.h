@@ -68,6 +68,7 @@ struct DevPlan {
   int* counter;     // K2 task counters (interior, boundary, multi; reset per launch)
   int* err_flag;    // sticky duplicate-point flag
   int k2_grid;      // persistent K2 CTAs
+  int k2_r1 = 0;    // every K2 task has <= 32 rows: the 64-register R = 1 kernel
   size_t up_smem, down_smem;
 };
 

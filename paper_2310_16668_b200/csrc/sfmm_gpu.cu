@@ -467,6 +467,11 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
       }
       if (configure_tree_kernels(dp, max_r, max_k) != 0)
         throw CudaFail{SFMM_EUNSUPPORTED, "interpolation block too large for shared memory"};
+      {
+        int32_t max_rows = 0;
+        for (const Task& t : hp.tasks) max_rows = std::max(max_rows, t.nrows);
+        dp.k2_r1 = !hp.cplx && max_rows <= 32;
+      }
       if (configure_translate(dp, device) != 0)
         throw CudaFail{SFMM_ECUDA, "occupancy query failed"};
       if (configure_multi(dp, device, max_k) != 0)
