@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(kUpThreads) k1_upward_real(
       acc[m] = 0.0;
       Ti[m] = Tb + (int64_t)min(i0 + m, i1 - 1) * r;
     }
-#pragma unroll 2
+#pragma unroll 4
     for (int j = lane; j < r; j += 32) {
       const double qj = qR[j];
 #pragma unroll
