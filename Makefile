@@ -1,4 +1,4 @@
-# Product build: sm_100a CUDA apply library (and the host precompute library).
+# Product build: sm_100a CUDA apply library (and the host descriptor library).
 # Outputs land in-tree under paper_2310_16668_b200/lib/ so they travel to the
 # GPU box with the repo snapshot.  `make oracle` builds the test-only checkers
 # (oracle/Makefile).
@@ -13,22 +13,19 @@ NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -I$(SRC)
             --expt-relaxed-constexpr -Xptxas -v -Xcompiler -fopenmp
 CXXFLAGS := -std=c++17 -O2 -fopenmp -fPIC -Iinclude -I$(SRC) -I/usr/local/cuda/include
 
-GPU_CU   := $(SRC)/kernels_translate.cu $(SRC)/kernels_tree.cu $(SRC)/kernels_probe.cu $(SRC)/kernels_multi.cu $(SRC)/skel_gpu.cu \
+GPU_CU   := $(SRC)/kernels_translate.cu $(SRC)/kernels_tree.cu $(SRC)/kernels_multi.cu $(SRC)/skel_gpu.cu \
             $(SRC)/tree_gpu.cu $(SRC)/sfmm_gpu.cu
 GPU_OBJS := $(patsubst $(SRC)/%.cu,$(OBJ)/%.o,$(GPU_CU)) $(OBJ)/plan_build.o
 HDRS     := include/sfmm_gpu.h $(SRC)/common.cuh $(SRC)/launch.h $(SRC)/plan_build.h $(SRC)/fastmath.cuh $(SRC)/log_table.inc
 
-.PHONY: all gpu host oracle clean
-all: gpu host
+.PHONY: all gpu host probe oracle clean
+all: gpu host probe
 
 HOST_SRC  := $(SRC)/host
-HOST_CPP  := $(HOST_SRC)/tree.cpp $(HOST_SRC)/skeleton.cpp $(HOST_SRC)/host_api.cpp
+HOST_CPP  := $(HOST_SRC)/host_api.cpp
 HOST_OBJS := $(patsubst $(HOST_SRC)/%.cpp,$(OBJ)/host_%.o,$(HOST_CPP))
 HOSTFLAGS := -std=c++17 -O3 -march=x86-64-v3 -fopenmp -fPIC -Iinclude -I$(HOST_SRC) \
              -fno-math-errno -fcx-limited-range -ffp-contract=off
-# skeletons need not be bit-identical to the reference (pivots are compared by
-# accuracy), so only they may use FMA contraction
-$(OBJ)/host_skeleton.o: HOSTFLAGS += -ffp-contract=fast
 
 host: $(LIB)/libsfmm_host.so
 
@@ -53,6 +50,13 @@ $(OBJ)/plan_build.o: $(SRC)/plan_build.cpp $(HDRS)
 $(LIB)/libsfmm_gpu.so: $(GPU_OBJS)
 	@mkdir -p $(LIB)
 	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart_static -lgomp -lpthread -ldl -lrt
+
+# measurement / test hooks (include/sfmm_probe.h): not part of the apply ABI
+probe: $(LIB)/libsfmm_probe.so
+
+$(LIB)/libsfmm_probe.so: $(SRC)/probe/sfmm_probe.cu include/sfmm_probe.h $(SRC)/fastmath.cuh $(SRC)/log_table.inc
+	@mkdir -p $(LIB) $(OBJ)
+	$(NVCC) $(NVFLAGS) -shared -o $@ $< -lcudart_static -ldl -lrt -lpthread 2> $(OBJ)/probe.ptxas.txt || (cat $(OBJ)/probe.ptxas.txt; false)
 
 oracle:
 	$(MAKE) -C oracle

@@ -67,8 +67,6 @@ def parse():
     ap.add_argument("--nrhs", type=int, default=1)
     ap.add_argument("--graphs", default="auto", choices=["auto", "on", "off"],
                     help="replay the apply as a CUDA graph in the timed region (auto: small plans)")
-    ap.add_argument("--precompute", default="gpu", choices=["gpu", "host"],
-                    help="skeletons from the GPU skeletonizer or the host C++ one (tree: host)")
     ap.add_argument("--config", default=None, choices=sorted(CONFIGS),
                     help="BASELINE.json configs (secondary measurement lines; default = headline)")
     args = ap.parse_args()
@@ -259,7 +257,7 @@ def run_sharded(args, ws, rank, local):
     cplx = kern == 3
     # node-local shared memory for the descriptor (~0.1 kB per point without T, ~1.3 kB
     # with it), else /tmp
-    per_point = 300 if args.precompute == "gpu" else 2000
+    per_point = 300
     base = "/dev/shm" if (os.path.isdir("/dev/shm") and
                           shutil.disk_usage("/dev/shm").free > per_point * n) else "/tmp"
     path = f"{base}/sfmm_bench_{os.environ.get('MASTER_PORT', '0')}"
@@ -269,16 +267,14 @@ def run_sharded(args, ws, rank, local):
          else host.generate_charges(n, 1 ^ CHARGE_STREAM))
     hp = None
     hinfo = {}
-    device_T = args.precompute == "gpu"
+    device_T = True
     if rank == 0:
         # torchrun sets OMP_NUM_THREADS=1; the other ranks wait at the barrier
         host.set_threads(os.cpu_count() or 1)
         # GPU precompute keeps T on rank 0's device: the descriptor is shared
         # without it and every rank receives only its own operators (NCCL)
-        hp = (host.HostPlan.build_gpu(kern, pts, args.leaf, args.tol, args.kappa, device=dev,
-                                      host_T=False, tree="gpu")
-              if device_T else
-              host.HostPlan.build(kern, pts, args.leaf, args.tol, args.kappa))
+        hp = host.HostPlan.build_gpu(kern, pts, args.leaf, args.tol, args.kappa, device=dev,
+                                     host_T=False)
         hinfo = hp.info()
         _share_descriptor(hp, path)
     dist.barrier()
@@ -512,10 +508,8 @@ def main():
     torch.zeros(1, device=f"cuda:{dev}")  # CUDA context up front, not inside the tree build time
     torch.cuda.synchronize(dev)
     # GPU precompute keeps T in HBM: the plan takes it device-to-device
-    hp = (host.HostPlan.build_gpu(kern, pts, args.leaf, args.tol, args.kappa, device=dev,
-                                  host_T=False, tree="gpu")
-          if args.precompute == "gpu" else
-          host.HostPlan.build(kern, pts, args.leaf, args.tol, args.kappa))
+    hp = host.HostPlan.build_gpu(kern, pts, args.leaf, args.tol, args.kappa, device=dev,
+                                 host_T=False)
     hinfo = hp.info()
     t0 = time.perf_counter()
     plan = api.GpuPlan.from_host(hp, device=dev)
@@ -681,13 +675,10 @@ def main():
                        "depth": hinfo["depth"], "n_boxes": hinfo["n_boxes"],
                        "k_max": hinfo["k_max"], "m_proj": hinfo["proj_scalars"],
                        "host_threads": host.get_threads(),
-                       "tree": "GPU tree builder (sfmm_gpu_build_tree)"
-                       if args.precompute == "gpu" else "host C++ tree builder",
-                       "skeletons": "GPU skeletonizer (sfmm_gpu_build_skeletons)"
-                       if args.precompute == "gpu" else "host C++ skeletonizer",
+                       "tree": "GPU tree builder (sfmm_gpu_build_tree)",
+                       "skeletons": "GPU skeletonizer (sfmm_gpu_build_skeletons)",
                        "operators": "device-resident, plan built device-to-device "
-                       "(sfmm_gpu_plan_create_skel)" if args.precompute == "gpu"
-                       else "uploaded from the host"},
+                       "(sfmm_gpu_plan_create_skel)"},
     }
 
     # ---- CPU baseline: the unmodified reference apply on the same plan ----

@@ -59,11 +59,11 @@ enum {
  * Flat plan descriptor.  All arrays are host memory, read once during
  * sfmm_gpu_plan_create and not retained.  Field meanings follow the reference
  * types one to one:
- *   Tree            tree.hpp:323-341   (pts, perm, level_begin, boxes)
- *   TreeBox         tree.hpp:308-321   (parent, level, begin/end, leaf)
- *   NeighborLists   tree.hpp:357-365   (colleagues, coarse, fine)
- *   BoxSkeleton     skeleton.hpp:260-269 (index_vec, skel_pos, red_pos,
- *                                         interp, parent_offset)
+ *   Tree            tree.hpp:34-52     (pts, perm, level_begin, boxes)
+ *   TreeBox         tree.hpp:19-32     (parent, level, begin/end, leaf)
+ *   NeighborLists   tree.hpp:68-76     (colleagues, coarse, fine)
+ *   BoxSkeleton     skeleton.hpp:40-50 (index_vec, skel_pos, red_pos,
+ *                                       interp, parent_offset)
  * Per-box variable-length lists are CSR: off[b]..off[b+1] (n_boxes+1 entries).
  * T is the concatenation of every box's k x r row-major interpolation matrix
  * (BoxSkeleton::interp); T_off counts scalars, complex scalars are two
@@ -137,7 +137,13 @@ int sfmm_gpu_plan_create(const sfmm_plan_desc* desc, int device, sfmm_gpu_plan**
 /* u = A q for nrhs right-hand sides.  q and u hold n_points x nrhs scalars,
  * column-major, in the ORIGINAL point order (apply.cpp:306-337).  Scalars are
  * double (Laplace) or interleaved complex double (Helmholtz).  Blocks until the
- * result is in u.  stats may be NULL. */
+ * result is in u.  stats may be NULL.
+ * Ordering: applies on one plan never overlap on the device -- each waits for
+ * the previous apply on the plan (sync or async, any stream) before it touches
+ * the plan's device state, so concurrent calls from several threads are safe
+ * (the reference's guarantee, apply.hpp:88-90).  With SFMM_DEVICE_BUFFERS the
+ * apply also waits for the work already enqueued on the legacy default stream
+ * (the producer of q); work on other caller streams must be complete. */
 int sfmm_gpu_apply(sfmm_gpu_plan* plan, const void* q, void* u, int nrhs, int flags,
                    sfmm_gpu_stats* stats);
 
@@ -357,18 +363,6 @@ int sfmm_gpu_plan_from_points(int kernel, double kappa, int dim, int64_t n, cons
  * up to max_applies recorded applies, sets *n_applies and clears the record. */
 int sfmm_gpu_set_timing(sfmm_gpu_plan* plan, int enable);
 int sfmm_gpu_get_timings(sfmm_gpu_plan* plan, float* ms, int max_applies, int* n_applies);
-
-/* Measured FP64 FMA throughput of the device (TFLOP/s, 2 flop per DFMA), from
- * a register-resident DFMA loop run on every SM for ~50 ms. */
-int sfmm_gpu_fp64_peak(int device, double* tflops);
-
-/* Test hook (device math of the Helmholtz kernels): out[6i..6i+5] = (sin, cos)
- * of x_i from the branch-free routine, the table-driven routine and the CUDA
- * library. */
-int sfmm_gpu_test_sincos(const double* x, int64_t n, double* out);
-/* Test hook: out[2i], out[2i+1] = log(x_i) from the table-driven routine of the
- * Laplace-2D kernels and from the CUDA library. */
-int sfmm_gpu_test_log(const double* x, int64_t n, double* out);
 
 /* Dense u_i = sum_{j != i} G(x_i, x_j) q_j over the points in their given
  * order, for the listed targets only (oracle.cpp:51-71), on the device.

@@ -1,18 +1,17 @@
 /*
- * sfmm_host.h -- C ABI of the host-side precompute that feeds the GPU apply.
+ * sfmm_host.h -- host-side container of a plan descriptor built on the GPU.
  *
- * The reference keeps tree construction, neighbor lists and skeletonization on
- * the host (north star: they "stay as they are").  This library is this
- * repository's own C++/OpenMP implementation of those callers of the apply:
- *   sfmm::build_tree            /root/reference/proj/src/tree.cpp:148-304
- *   sfmm::build_neighbor_lists  /root/reference/proj/src/tree.cpp:306-355
- *   sfmm::build_skeletons       /root/reference/proj/src/skeleton.cpp:184-260
+ * The precompute that feeds the apply (tree, neighbor lists, skeletons) runs
+ * on the device (sfmm_gpu_build_tree / sfmm_gpu_build_skeletons, SURVEY.md
+ * 8(f)); a C++ caller of the reference keeps using the reference's own
+ * sfmm::build_tree / build_neighbor_lists / build_skeletons
+ * (/root/reference/proj/src/tree.cpp:148-355, skeleton.cpp:184-260) and the
+ * drop-in header include/sfmm_gpu.hpp.  This small library only holds the
+ * host copies of those device results as one sfmm_plan_desc
+ * (include/sfmm_gpu.h) and provides the benchmark's synthetic inputs
  *   sfmm::generate_points / generate_charges(_complex)
  *                               /root/reference/proj/src/bench.cpp:102-161
- * Trees (perm, box order, ranges, neighbor lists) are bit-identical to the
- * reference's; skeletons satisfy the same ID criterion (pivot choices are
- * rounding-sensitive, so they are compared by accuracy, not bits).
- * The result is exported as the sfmm_plan_desc of include/sfmm_gpu.h.
+ * plus the clustered Gaussian of config 3(b).
  */
 #ifndef SFMM_HOST_H_
 #define SFMM_HOST_H_
@@ -62,16 +61,6 @@ int sfmm_host_generate_points(int dist, int64_t n, uint64_t seed, double* out);
 int sfmm_host_generate_charges(int64_t n, uint64_t seed, double* out);
 int sfmm_host_generate_charges_complex(int64_t n, uint64_t seed, double* out);
 
-/* Tree + neighbor lists only (skeleton fields of the descriptor stay empty,
- * T absent).  pts: n*dim interleaved, original order. */
-int sfmm_host_build_tree(int dim, int64_t n, const double* pts, int leaf_cap,
-                         sfmm_host_plan** out);
-
-/* Full precompute: tree, neighbor lists, skeletons (build_skeletons). */
-int sfmm_host_build(int kernel, double kappa, int dim, int64_t n, const double* pts,
-                    int leaf_cap, double tol, const sfmm_proxy_config* proxy,
-                    sfmm_host_plan** out);
-
 /* Flat view of the plan; valid until sfmm_host_destroy. */
 const sfmm_plan_desc* sfmm_host_desc(sfmm_host_plan* plan);
 
@@ -99,7 +88,7 @@ int sfmm_host_info_get(const sfmm_host_plan* plan, sfmm_host_info* info);
 
 void sfmm_host_destroy(sfmm_host_plan* plan);
 
-/* Number of OpenMP threads the precompute uses (0 keeps the default). */
+/* Number of OpenMP threads the host-side copies use (0 keeps the default). */
 void sfmm_host_set_threads(int n);
 int sfmm_host_get_threads(void);
 

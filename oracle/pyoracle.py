@@ -66,9 +66,12 @@ def ref_lib() -> C.CDLL:
         lib.ref_generate_charges_complex.argtypes = [C.c_int64, C.c_uint64, vp]
         lib.ref_build.argtypes = [C.c_int, C.c_double, C.c_int, C.c_int64, vp, C.c_int, C.c_double,
                                   C.c_double, C.c_int, C.c_int, C.POINTER(vp)]
+        lib.ref_build_tree.argtypes = [C.c_int, C.c_int64, vp, C.c_int, C.POINTER(vp)]
         lib.ref_from_desc.argtypes = [C.POINTER(PlanDesc), C.POINTER(vp)]
         lib.ref_desc.argtypes = [vp]
         lib.ref_desc.restype = C.POINTER(PlanDesc)
+        lib.ref_box_geometry.argtypes = [vp, vp, vp]
+        lib.ref_box_geometry.restype = None
         lib.ref_info.argtypes = [vp, vp]
         lib.ref_info.restype = None
         lib.ref_apply.argtypes = [vp, vp, vp, vp]
@@ -138,6 +141,15 @@ class RefPipeline:
         return cls(h)
 
     @classmethod
+    def build_tree(cls, pts: np.ndarray, leaf_cap: int):
+        """build_tree + build_neighbor_lists only (empty skeleton CSR)."""
+        pts = np.ascontiguousarray(pts, dtype=np.float64)
+        h = C.c_void_p()
+        _check(ref_lib().ref_build_tree(pts.shape[1], pts.shape[0], pts.ctypes.data, leaf_cap,
+                                        C.byref(h)))
+        return cls(h)
+
+    @classmethod
     def from_desc(cls, desc):
         """desc: PlanDescriptor or a ctypes PlanDesc (zero-copy view)."""
         st = desc.struct if isinstance(desc, PlanDescriptor) else desc
@@ -147,6 +159,13 @@ class RefPipeline:
 
     def descriptor(self) -> PlanDescriptor:
         return PlanDescriptor.from_struct(ref_lib().ref_desc(self._h).contents)
+
+    def box_geometry(self):
+        """(centre (n_boxes*3,), half-width (n_boxes,)) of the reference tree."""
+        nb = int(ref_lib().ref_desc(self._h).contents.n_boxes)
+        c, h = np.zeros(3 * nb), np.zeros(nb)
+        ref_lib().ref_box_geometry(self._h, c.ctypes.data, h.ctypes.data)
+        return c, h
 
     def info(self) -> dict:
         out = np.zeros(6, dtype=np.int64)

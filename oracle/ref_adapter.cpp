@@ -136,7 +136,9 @@ struct Impl : Base {
     constexpr int sw = sfmm::is_complex_scalar<S>::value ? 2 : 1;
     for (int64_t b = 0; b < nb_; ++b) {
       const auto& bx = tree.boxes[b];
-      const auto& sk = skel.box[b];
+      // tree-only handles (ref_build_tree) have no skeletons: empty rows
+      static const sfmm::BoxSkeleton<S> kNone{};
+      const auto& sk = skel.box.empty() ? kNone : skel.box[b];
       f.parent[b] = bx.parent;
       f.level[b] = bx.level;
       f.begin[b] = bx.begin;
@@ -269,6 +271,21 @@ int ref_build(int kernel, double kappa, int dim, int64_t n, const double* pts, i
   });
 }
 
+// Reference tree + neighbor lists only (build_tree, build_neighbor_lists):
+// the descriptor's skeleton CSR is empty; apply is not available.
+int ref_build_tree(int dim, int64_t n, const double* pts, int leaf_cap, ref_handle** out) {
+  return guarded([&] {
+    sfmm::PointSet ps;
+    ps.dim = dim;
+    ps.coords.assign(pts, pts + n * dim);
+    auto impl = std::make_unique<Impl<sfmm::Laplace3d>>();
+    impl->kernel = dim == 2 ? SFMM_LAPLACE2D : SFMM_LAPLACE3D;
+    impl->tree = sfmm::build_tree(ps, leaf_cap);
+    impl->nb = sfmm::build_neighbor_lists(impl->tree);
+    *out = reinterpret_cast<ref_handle*>(static_cast<Base*>(impl.release()));
+  });
+}
+
 // Rebuilds reference objects from a flat descriptor (any producer).
 int ref_from_desc(const sfmm_plan_desc* D, ref_handle** out) {
   return guarded([&] {
@@ -344,6 +361,15 @@ const sfmm_plan_desc* ref_desc(ref_handle* h) {
 }
 
 // out: depth, n_boxes, k_max, proj_scalars, saturated_boxes, n_leaves
+// Box centres (n_boxes*3) and half-widths of the reference tree.
+void ref_box_geometry(ref_handle* h, double* center, double* half) {
+  const sfmm::Tree& t = reinterpret_cast<Base*>(h)->tree;
+  for (int64_t b = 0; b < t.n_boxes(); ++b) {
+    for (int k = 0; k < 3; ++k) center[3 * b + k] = t.boxes[b].center[k];
+    half[b] = t.boxes[b].half;
+  }
+}
+
 void ref_info(ref_handle* h, int64_t* out) { reinterpret_cast<Base*>(h)->info(out); }
 
 // The reference CPU apply, timed by the caller.  stats: ifo, ifs, tfo, l1, fallback.

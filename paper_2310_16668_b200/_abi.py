@@ -304,8 +304,6 @@ def gpu_lib() -> C.CDLL:
     lib.sfmm_gpu_set_timing.restype = C.c_int
     lib.sfmm_gpu_get_timings.argtypes = [vp, vp, C.c_int, C.POINTER(C.c_int)]
     lib.sfmm_gpu_get_timings.restype = C.c_int
-    lib.sfmm_gpu_fp64_peak.argtypes = [C.c_int, C.POINTER(C.c_double)]
-    lib.sfmm_gpu_fp64_peak.restype = C.c_int
     lib.sfmm_gpu_plan_create_sharded.argtypes = [C.POINTER(PlanDesc), C.c_int, C.c_int, C.c_int,
                                                  C.POINTER(vp)]
     lib.sfmm_gpu_plan_create_sharded.restype = C.c_int
@@ -351,14 +349,10 @@ def gpu_lib() -> C.CDLL:
     lib.sfmm_gpu_tree_destroy.restype = None
     lib.sfmm_gpu_skel_destroy.argtypes = [vp]
     lib.sfmm_gpu_skel_destroy.restype = None
-    lib.sfmm_gpu_test_sincos.argtypes = [vp, C.c_int64, vp]
-    lib.sfmm_gpu_test_sincos.restype = C.c_int
     lib.sfmm_gpu_plan_from_points.argtypes = [C.c_int, C.c_double, C.c_int, C.c_int64, vp, C.c_int,
                                               C.c_double, C.c_double, C.c_int, C.c_int, C.c_int,
                                               C.POINTER(vp)]
     lib.sfmm_gpu_plan_from_points.restype = C.c_int
-    lib.sfmm_gpu_test_log.argtypes = [vp, C.c_int64, vp]
-    lib.sfmm_gpu_test_log.restype = C.c_int
     _gpu_lib = lib
     return lib
 
@@ -367,12 +361,38 @@ GPU_SYMBOLS = [
     "sfmm_gpu_plan_create", "sfmm_gpu_apply", "sfmm_gpu_apply_async", "sfmm_gpu_check_status",
     "sfmm_gpu_plan_info_get", "sfmm_gpu_plan_destroy", "sfmm_gpu_direct_sum",
     "sfmm_gpu_last_error", "sfmm_gpu_version", "sfmm_gpu_set_timing", "sfmm_gpu_get_timings",
-    "sfmm_gpu_fp64_peak", "sfmm_gpu_plan_create_sharded", "sfmm_gpu_shard_info",
+    "sfmm_gpu_plan_create_sharded", "sfmm_gpu_shard_info",
     "sfmm_gpu_apply_begin", "sfmm_gpu_apply_end", "sfmm_gpu_shard_describe",
     "sfmm_gpu_build_skeletons", "sfmm_gpu_skel_fill", "sfmm_gpu_skel_destroy",
-    "sfmm_gpu_test_sincos", "sfmm_gpu_skel_describe", "sfmm_gpu_skel_device_T",
+    "sfmm_gpu_skel_describe", "sfmm_gpu_skel_device_T",
     "sfmm_gpu_plan_create_skel", "sfmm_gpu_build_tree", "sfmm_gpu_tree_arrays",
-    "sfmm_gpu_tree_destroy", "sfmm_gpu_test_log", "sfmm_gpu_plan_from_points",
+    "sfmm_gpu_tree_destroy", "sfmm_gpu_plan_from_points",
     "sfmm_gpu_shard_info2", "sfmm_gpu_apply_mid", "sfmm_gpu_apply_fin",
     "sfmm_gpu_shard_T_runs", "sfmm_gpu_copy_runs", "sfmm_gpu_plan_create_sharded_T",
 ]
+
+
+PROBE_SYMBOLS = ["sfmm_probe_fp64_peak", "sfmm_probe_test_sincos", "sfmm_probe_test_log"]
+
+_probe_lib = None
+
+
+def probe_lib() -> C.CDLL:
+    """Loads lib/libsfmm_probe.so: measurement and test hooks
+    (include/sfmm_probe.h), not part of the apply ABI."""
+    global _probe_lib
+    if _probe_lib is not None:
+        return _probe_lib
+    path = os.path.join(LIB_DIR, "libsfmm_probe.so")
+    if not os.path.exists(path):
+        raise NativeLibraryMissing(f"{path} is missing; run `make`")
+    lib = C.CDLL(path)
+    vp = C.c_void_p
+    lib.sfmm_probe_fp64_peak.argtypes = [C.c_int, C.POINTER(C.c_double)]
+    lib.sfmm_probe_fp64_peak.restype = C.c_int
+    lib.sfmm_probe_test_sincos.argtypes = [vp, C.c_int64, vp]
+    lib.sfmm_probe_test_sincos.restype = C.c_int
+    lib.sfmm_probe_test_log.argtypes = [vp, C.c_int64, vp]
+    lib.sfmm_probe_test_log.restype = C.c_int
+    _probe_lib = lib
+    return lib

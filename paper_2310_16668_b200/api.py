@@ -164,9 +164,11 @@ def fmm_apply(plan: GpuPlan, q, stats: ApplyStats | None = None,
     qc = np.asfortranarray(q.reshape(plan.n_points, -1), dtype=plan.dtype)
     nrhs = qc.shape[1]
     if out is not None:
-        if out.dtype != plan.dtype or out.size != qc.size or not (
-                out.flags.f_contiguous or out.ndim == 1):
-            raise ValueError("fmm_apply: out buffer has the wrong shape or dtype")
+        # the C ABI writes n*nrhs contiguous scalars (column-major): a strided
+        # view (e.g. big[::2]) would be clobbered between its elements
+        if out.dtype != plan.dtype or out.size != qc.size or not out.flags.f_contiguous:
+            raise ValueError("fmm_apply: out must be a contiguous (column-major) buffer of "
+                             "the result's size and dtype")
         u = out.reshape(plan.n_points, nrhs, order="F")
     else:
         u = np.empty((plan.n_points, nrhs), dtype=plan.dtype, order="F")
@@ -207,9 +209,12 @@ def get_timings(plan: GpuPlan, max_applies: int = 256) -> np.ndarray:
 
 
 def fp64_peak_tflops(device: int = 0) -> float:
-    """Measured DFMA throughput of the device (TFLOP/s)."""
+    """Measured DFMA throughput of the device (TFLOP/s), from the probe library
+    (include/sfmm_probe.h; not part of the apply ABI)."""
     v = C.c_double(0)
-    _raise(_abi.gpu_lib().sfmm_gpu_fp64_peak(device, C.byref(v)))
+    rc = _abi.probe_lib().sfmm_probe_fp64_peak(device, C.byref(v))
+    if rc != 0:
+        raise DeviceError(f"sfmm_probe_fp64_peak failed with code {rc}")
     return v.value
 
 

@@ -22,6 +22,13 @@ constexpr int kNRHS = 16;  // right-hand sides per multi-RHS pass (zero padded)
 #ifndef SFMM_K2C_MAX_R
 #define SFMM_K2C_MAX_R 3
 #endif
+// Largest rows-per-lane of the real K2 (a build knob, tools/build_variant.sh):
+// real row tiles are at most 32 x this (plan_build.cpp clamps them).
+#ifndef SFMM_K2_MAX_R
+#define SFMM_K2_MAX_R 4
+#endif
+static_assert(SFMM_K2_MAX_R >= 1 && SFMM_K2_MAX_R <= 4, "SFMM_K2_MAX_R must be 1..4");
+static_assert(SFMM_K2C_MAX_R >= 2 && SFMM_K2C_MAX_R <= 4, "SFMM_K2C_MAX_R must be 2..4");
 constexpr int kModeBits = 3;
 constexpr int32_t kModeMask = (1 << kModeBits) - 1;
 

@@ -1,4 +1,4 @@
-// Host precompute: adaptive Morton tree, neighbor lists, skeletons.
+// Host copies of a plan built on the GPU (tree, neighbor lists, skeletons).
 #pragma once
 
 #include <stdint.h>
@@ -9,16 +9,6 @@
 #include <vector>
 
 namespace sfmm_host {
-
-struct DuplicatePoint : std::domain_error {
-  using std::domain_error::domain_error;
-};
-struct DepthExceeded : std::runtime_error {
-  using std::runtime_error::runtime_error;
-};
-
-constexpr int kMaxDepth2 = 31;  // 64-bit Morton budget (tree.hpp:15)
-constexpr int kMaxDepth3 = 21;
 
 struct Box {
   int32_t parent = -1;
@@ -33,7 +23,7 @@ struct Box {
   int32_t npoints() const { return end - begin; }
 };
 
-// Level-major, Morton-sorted tree (same layout as sfmm::Tree, tree.hpp:323-341).
+// Level-major, Morton-sorted tree (same layout as sfmm::Tree, tree.hpp:19-52).
 struct Tree {
   int dim = 0, depth = 0, leaf_cap = 0;
   std::vector<Box> boxes;
@@ -48,15 +38,6 @@ struct Neighbors {
   std::vector<int32_t> coll, coarse, fine;
 };
 
-Tree build_tree(int dim, int64_t n, const double* pts, int leaf_cap);
-Neighbors build_neighbors(const Tree& t);
-
-struct Proxy {
-  double radius_factor = 2.95;
-  int edge_points_2d = 24;
-  int face_grid_3d = 8;
-};
-
 // Skeleton data in CSR form (the sfmm_plan_desc layout).
 struct Skeletons {
   std::vector<int64_t> iv_off, sk_off, rd_off, T_off;
@@ -66,14 +47,6 @@ struct Skeletons {
   int saturated = 0;
   int64_t proj_scalars = 0;
 };
-
-// kernel: 0 laplace2d, 1 laplace3d, 2 helmholtz2d, 3 helmholtz3d
-Skeletons build_skeletons(const Tree& t, int kernel, double kappa, double tol, const Proxy& px);
-
-// Interpolative decomposition by greedy column-pivoted QR (shared with tests).
-template <class S>
-int column_id(const S* a_colmajor, int64_t m, int64_t n, double eps, std::vector<int32_t>& skel,
-              std::vector<int32_t>& red, std::vector<S>& interp);
 
 // Synthetic inputs (bench.cpp:25-45,102-161 definitions).
 void generate_points(int dist, int64_t n, uint64_t seed, double* out);

@@ -1,5 +1,5 @@
-// C ABI of the host precompute (include/sfmm_host.h) and the synthetic-input
-// generators.
+// C ABI of the host descriptor container (include/sfmm_host.h) and the
+// synthetic-input generators.
 #include <omp.h>
 
 #include <chrono>
@@ -118,10 +118,6 @@ int guarded(F&& f) {
   try {
     f();
     return SFMM_OK;
-  } catch (const sfmm_host::DuplicatePoint& e) {
-    return fail(SFMM_EDUPLICATE, e.what());
-  } catch (const sfmm_host::DepthExceeded& e) {
-    return fail(SFMM_EDEPTH, e.what());
   } catch (const std::invalid_argument& e) {
     return fail(SFMM_EINVAL, e.what());
   } catch (const std::logic_error& e) {
@@ -231,21 +227,6 @@ int sfmm_host_generate_charges_complex(int64_t n, uint64_t seed, double* out) {
   return guarded([&] { sfmm_host::generate_charges_complex(n, seed, out); });
 }
 
-int sfmm_host_build_tree(int dim, int64_t n, const double* pts, int leaf_cap,
-                         sfmm_host_plan** out) {
-  return guarded([&] {
-    auto p = std::make_unique<sfmm_host_plan>();
-    const double t0 = now();
-    p->tree = sfmm_host::build_tree(dim, n, pts, leaf_cap);
-    const double t1 = now();
-    p->nb = sfmm_host::build_neighbors(p->tree);
-    p->info.t_tree = now() - t0;
-    if (std::getenv("SFMM_TREE_VERBOSE")) std::fprintf(stderr, "[tree] neighbors    %.3f s\n", now() - t1);
-    p->export_desc();
-    *out = p.release();
-  });
-}
-
 int sfmm_host_adopt_tree(const sfmm_tree_arrays* a, sfmm_host_plan** out) {
   if (!a || !out) return fail(SFMM_EINVAL, "null argument");
   return guarded([&] {
@@ -283,36 +264,6 @@ int sfmm_host_adopt_tree(const sfmm_tree_arrays* a, sfmm_host_plan** out) {
     g.fine_off.assign(a->fine_off, a->fine_off + nb + 1);
     g.fine.assign(a->fine, a->fine + g.fine_off[nb]);
     p->info.t_tree = a->seconds;
-    p->export_desc();
-    *out = p.release();
-  });
-}
-
-int sfmm_host_build(int kernel, double kappa, int dim, int64_t n, const double* pts,
-                    int leaf_cap, double tol, const sfmm_proxy_config* proxy,
-                    sfmm_host_plan** out) {
-  return guarded([&] {
-    if (kernel < 0 || kernel > 3) throw std::invalid_argument("sfmm_host_build: bad kernel id");
-    if (kernel == SFMM_HELMHOLTZ2D)
-      throw std::logic_error("sfmm_host_build: helmholtz2d has no device apply path");
-    if ((kernel == SFMM_HELMHOLTZ3D) && !(kappa > 0))
-      throw std::invalid_argument("sfmm_host_build: wavenumber must be positive");
-    sfmm_host::Proxy px;
-    if (proxy) {
-      if (proxy->radius_factor > 0) px.radius_factor = proxy->radius_factor;
-      if (proxy->edge_points_2d > 0) px.edge_points_2d = proxy->edge_points_2d;
-      if (proxy->face_grid_3d > 0) px.face_grid_3d = proxy->face_grid_3d;
-    }
-    auto p = std::make_unique<sfmm_host_plan>();
-    p->kernel = kernel;
-    p->kappa = kappa;
-    double t0 = now();
-    p->tree = sfmm_host::build_tree(dim, n, pts, leaf_cap);
-    p->nb = sfmm_host::build_neighbors(p->tree);
-    p->info.t_tree = now() - t0;
-    t0 = now();
-    p->sk = sfmm_host::build_skeletons(p->tree, kernel, kappa, tol, px);
-    p->info.t_skel = now() - t0;
     p->export_desc();
     *out = p.release();
   });

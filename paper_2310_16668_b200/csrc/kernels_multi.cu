@@ -279,6 +279,10 @@ __global__ void __launch_bounds__(kMThreads, WH ? SFMM_K2M_MIN_BLOCKS_WH : SFMM_
       const int32_t code = a.ent[er.begin + cur.e];
       const bool self = (code >> kModeBits) == task.box;
       const int j0 = cur.j0;
+      // sources of this chunk past the box end are padding: their G is masked
+      // below (never trusted to vanish through the zero weight: a target may
+      // sit exactly at the padding coordinate)
+      const int n_valid = a.box[code >> kModeBits].n - j0;
       const ChunkPos nxt = next_of(cur);
       if (nxt.e < er.count) load(nxt, R);  // in flight during the compute below
       if (wrow0 < rend) {
@@ -313,7 +317,7 @@ __global__ void __launch_bounds__(kMThreads, WH ? SFMM_K2M_MIN_BLOCKS_WH : SFMM_
                 gi[mt] = 0.0;
               }
             }
-            if (self && rowi[mt] == j0 + js) gr[mt] = gi[mt] = 0.0;
+            if ((self && rowi[mt] == j0 + js) || js >= n_valid) gr[mt] = gi[mt] = 0.0;
           }
           // A operands of the NP real products: Gr (, Gi, Gr + Gi)
           double g[NP][2];

@@ -320,9 +320,6 @@ __device__ __forceinline__ void task_real(const K2Args& a, const Task& t, WarpSm
 #ifndef SFMM_K2_R1_MIN_BLOCKS
 #define SFMM_K2_R1_MIN_BLOCKS 8
 #endif
-#ifndef SFMM_K2_MAX_R
-#define SFMM_K2_MAX_R 4
-#endif
 template <class G, int MAXR, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) k2_translate_real_t(K2Args a) {
   __shared__ WarpSmemReal smem[kWarps];

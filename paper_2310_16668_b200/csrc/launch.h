@@ -139,13 +139,5 @@ void launch_downward_m(const DevPlan& p, const HostPlan& hp, int level, DevState
                        cudaStream_t st);
 void launch_scatter_m(const DevPlan& p, const DevState& s, double* u, int nc, cudaStream_t st);
 
-// Test hook: out[2i], out[2i+1] = log_tab(x_i) and the CUDA library's log.
-int test_log(const double* x_host, int64_t n, double* out_host);
-// Test hook: out[6i..6i+5] = sincos_fast(x_i) (s, c), the table version (s, c)
-// and the CUDA library's (s, c).
-int test_sincos(const double* x_host, int64_t n, double* out_host);
-
-// DFMA throughput probe (TFLOP/s), see kernels_probe.cu.
-double measure_fp64_peak(int device);
 
 }  // namespace sfmm_gpu

@@ -695,7 +695,8 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
 #ifdef SFMM_TILE_FORCE
       tile = SFMM_TILE_FORCE;  // dev knob (A/B of the K2 occupancy variants)
 #endif
-      if (hp.cplx) tile = std::min(tile, 32 * SFMM_K2C_MAX_R);  // complex K2 rows per lane
+      // rows per lane of the K2 instantiations this library was built with
+      tile = std::min(tile, 32 * (hp.cplx ? SFMM_K2C_MAX_R : SFMM_K2_MAX_R));
       hp.tile_rows = tile;
       // outgoing cross-rank pairs in (b, entry) order, the staged tiles of each
       std::vector<std::pair<int32_t, int32_t>> xpairs;

@@ -1,12 +1,15 @@
-// FP64 pipe probe: the roofline denominator for the FP64-bound translation
-// kernel (MEASURED_PEAKS.json carries only HBM and bf16 peaks).
+// Measurement and test hooks (include/sfmm_probe.h), built as their own
+// library: NOT part of the drop-in apply ABI.
+//   * FP64 pipe probe: the roofline denominator for the FP64-bound
+//     translation kernel (MEASURED_PEAKS.json carries only HBM and bf16 peaks);
+//   * device-math checks of the product's table-driven log / sincos
+//     (fastmath.cuh) against the CUDA library.
 #include <cuda_runtime.h>
 
 #include <algorithm>
 
 #include "fastmath.cuh"
-#include "launch.h"
-#include "sfmm_gpu.h"
+#include "sfmm_probe.h"
 
 namespace sfmm_gpu {
 namespace {
@@ -41,6 +44,8 @@ __global__ void log_check(const double* x, int64_t n, const double* tab, double*
   }
 }
 }  // namespace
+
+namespace {
 
 int test_log(const double* x_host, int64_t n, double* out_host) {
   double *dx = nullptr, *dout = nullptr, *dtab = nullptr;
@@ -135,4 +140,29 @@ double measure_fp64_peak(int device) {
   return cudaGetLastError() == cudaSuccess ? best : -1;
 }
 
+}  // namespace
 }  // namespace sfmm_gpu
+
+extern "C" {
+
+int sfmm_probe_test_log(const double* x, int64_t n, double* out) {
+  if (!x || !out || n < 0) return 1;
+  return sfmm_gpu::test_log(x, n, out) == 0 ? 0 : 3;
+}
+
+int sfmm_probe_test_sincos(const double* x, int64_t n, double* out) {
+  if (!x || !out || n < 0) return 1;
+  return sfmm_gpu::test_sincos(x, n, out) == 0 ? 0 : 3;
+}
+
+int sfmm_probe_fp64_peak(int device, double* tflops) {
+  if (!tflops) return 1;
+  int prev = -1;
+  if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+  if (cudaSetDevice(device) != cudaSuccess) return 3;
+  *tflops = sfmm_gpu::measure_fp64_peak(device);
+  if (prev >= 0) cudaSetDevice(prev);
+  return *tflops > 0 ? 0 : 3;
+}
+
+}  // extern "C"

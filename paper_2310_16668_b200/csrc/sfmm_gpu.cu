@@ -93,6 +93,12 @@ struct sfmm_gpu_plan {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_k2a = nullptr, ev_k2b = nullptr;
+  // End of the last apply enqueued on this plan (any stream).  Every apply
+  // waits on it before touching the plan's shared device state (Q/U/QH/UH,
+  // the column-sum staging, the task counter), so applies issued on different
+  // streams -- or a sync apply on the plan stream after an async one on a
+  // caller stream -- run one after another instead of racing.
+  cudaEvent_t ev_done = nullptr;
   HostPlan hp;
   DevPlan dp{};
   std::vector<void*> allocs;
@@ -136,6 +142,7 @@ struct sfmm_gpu_plan {
     if (ev_b) cudaEventDestroy(ev_b);
     if (ev_k2a) cudaEventDestroy(ev_k2a);
     if (ev_k2b) cudaEventDestroy(ev_k2b);
+    if (ev_done) cudaEventDestroy(ev_done);
     for (cudaEvent_t e : tev) cudaEventDestroy(e);
     if (graph_exec) cudaGraphExecDestroy(graph_exec);
     for (PhaseGraph& g : phase_graph)
@@ -301,6 +308,10 @@ struct sfmm_gpu_plan {
   }
 
   size_t scalar_bytes() const { return hp.cplx ? 16 : 8; }
+
+  // Orders this apply after the previous one on the plan (see ev_done).
+  void wait_previous(cudaStream_t st) { ck(cudaStreamWaitEvent(st, ev_done, 0), "wait previous apply"); }
+  void mark_done(cudaStream_t st) { ck(cudaEventRecord(ev_done, st), "event"); }
 };
 
 extern "C" {
@@ -335,6 +346,8 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
     ck(cudaEventCreate(&p->ev_b), "cudaEventCreate");
     ck(cudaEventCreate(&p->ev_k2a), "cudaEventCreate");
     ck(cudaEventCreate(&p->ev_k2b), "cudaEventCreate");
+    ck(cudaEventCreateWithFlags(&p->ev_done, cudaEventDisableTiming), "cudaEventCreate");
+    ck(cudaEventRecord(p->ev_done, p->stream), "event");
     HostPlan& hp = p->hp;
     DevPlan& dp = p->dp;
     dp.kernel = hp.kernel;
@@ -640,6 +653,7 @@ int sfmm_gpu_apply_begin(sfmm_gpu_plan* p, const void* q_dev, void* send_dev, vo
     const double* q = static_cast<const double*>(q_dev);
     if (p->hp.depth >= 2 && p->dp.n_pack > 0 && !send_dev)
       throw CudaFail{SFMM_EINVAL, "send buffer required"};
+    p->wait_previous(st);
     p->run_phase(0, q_dev, send_dev, nullptr, stream, st, [&] {
       if (p->hp.depth < 2) return;
       launch_gather(p->dp, q, p->ds, st);
@@ -710,6 +724,7 @@ int sfmm_gpu_apply_end(sfmm_gpu_plan* p, const void* q_dev, const void* recv_dev
       apply_mid_impl(p, recv_dev, nullptr, st);
       apply_fin_impl(p, q_dev, nullptr, u_dev, st);
     });
+    p->mark_done(st);
     ck(cudaGetLastError(), "kernel launch");
     return SFMM_OK;
   } catch (const CudaFail& f) {
@@ -749,6 +764,7 @@ int sfmm_gpu_apply_fin(sfmm_gpu_plan* p, const void* q_dev, const void* recv2_de
       throw CudaFail{SFMM_EINVAL, "second receive buffer required"};
     p->run_phase(2, q_dev, recv2_dev, u_dev, stream, st,
                  [&] { apply_fin_impl(p, q_dev, recv2_dev, u_dev, st); });
+    p->mark_done(st);
     ck(cudaGetLastError(), "kernel launch");
     return SFMM_OK;
   } catch (const CudaFail& f) {
@@ -782,6 +798,13 @@ int sfmm_gpu_apply(sfmm_gpu_plan* p, const void* q, void* u, int nrhs, int flags
     const bool host = flags == SFMM_HOST_BUFFERS;
     cudaStream_t st = p->stream;
     if (host) p->ensure_io(col * nrhs);
+    p->wait_previous(st);
+    if (!host) {
+      // device buffers: q may come from work the caller enqueued on the legacy
+      // default stream, which the plan's non-blocking stream does not see
+      ck(cudaEventRecord(p->ev_a, cudaStreamLegacy), "event");
+      ck(cudaStreamWaitEvent(st, p->ev_a, 0), "wait caller");
+    }
     ck(cudaEventRecord(p->ev_a, st), "event");
     const double* qd = static_cast<const double*>(q);
     double* ud = static_cast<double*>(u);
@@ -794,6 +817,7 @@ int sfmm_gpu_apply(sfmm_gpu_plan* p, const void* q, void* u, int nrhs, int flags
     ck(cudaGetLastError(), "kernel launch");
     if (host) ck(cudaMemcpyAsync(u, p->io_u, col * nrhs, cudaMemcpyDeviceToHost, st), "D2H u");
     ck(cudaEventRecord(p->ev_b, st), "event");
+    p->mark_done(st);
     ck(cudaStreamSynchronize(st), "apply");
     int flag = 0;
     ck(cudaMemcpy(&flag, p->dp.err_flag, sizeof(int), cudaMemcpyDeviceToHost), "flag");
@@ -831,6 +855,7 @@ int sfmm_gpu_apply_async(sfmm_gpu_plan* p, const void* q_dev, void* u_dev, int n
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : p->stream;
     const double* qd = static_cast<const double*>(q_dev);
     double* ud = static_cast<double*>(u_dev);
+    p->wait_previous(st);
     // Repeated applies on the same buffers replay one CUDA graph of the whole
     // sequence (~15-45 launches): launch overhead matters for small trees.
     static const bool env_graphs = [] {
@@ -863,6 +888,7 @@ int sfmm_gpu_apply_async(sfmm_gpu_plan* p, const void* q_dev, void* u_dev, int n
     } else {
       p->enqueue_cols(qd, ud, nrhs, st, false);
     }
+    p->mark_done(st);
     ck(cudaGetLastError(), "kernel launch");
     return SFMM_OK;
   } catch (const CudaFail& f) {
@@ -942,29 +968,6 @@ int sfmm_gpu_get_timings(sfmm_gpu_plan* p, float* ms, int max_applies, int* n_ap
     }
     *n_applies = n;
     p->n_timed = 0;
-    return SFMM_OK;
-  } catch (const CudaFail& f) {
-    return set_error(f.code, f.msg);
-  }
-}
-
-int sfmm_gpu_test_log(const double* x, int64_t n, double* out) {
-  if (!x || !out || n < 0) return set_error(SFMM_EINVAL, "test_log: bad arguments");
-  return sfmm_gpu::test_log(x, n, out) == 0 ? SFMM_OK : set_error(SFMM_ECUDA, "test_log failed");
-}
-
-int sfmm_gpu_test_sincos(const double* x, int64_t n, double* out) {
-  if (!x || !out || n < 0) return set_error(SFMM_EINVAL, "null argument");
-  return sfmm_gpu::test_sincos(x, n, out) == 0 ? SFMM_OK
-                                                : set_error(SFMM_ECUDA, "sincos check failed");
-}
-
-int sfmm_gpu_fp64_peak(int device, double* tflops) {
-  if (!tflops) return set_error(SFMM_EINVAL, "null argument");
-  try {
-    DeviceGuard device_guard(device);
-    *tflops = measure_fp64_peak(device);
-    if (*tflops <= 0) return set_error(SFMM_ECUDA, "fp64 peak probe failed");
     return SFMM_OK;
   } catch (const CudaFail& f) {
     return set_error(f.code, f.msg);

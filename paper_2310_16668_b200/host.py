@@ -1,10 +1,13 @@
-"""Python handle on the host precompute library (include/sfmm_host.h).
+"""The precompute that feeds the apply, run on the GPU, and its flat descriptor.
 
-Mirrors the reference's host API that feeds the apply:
-    build_tree + build_neighbor_lists  (tree.cpp:148-355)
-    build_skeletons                     (skeleton.cpp:184-260)
-    generate_points / generate_charges  (bench.cpp:102-161)
-and exports the flat plan descriptor consumed by ``api.GpuPlan``.
+Device counterparts of the reference's host API:
+    build_tree + build_neighbor_lists  (tree.cpp:148-355)  -> sfmm_gpu_build_tree
+    build_skeletons                     (skeleton.cpp:184-260) -> sfmm_gpu_build_skeletons
+and the benchmark's synthetic inputs generate_points / generate_charges
+(bench.cpp:102-161).  The host library (include/sfmm_host.h) only holds host
+copies of the device results as the sfmm_plan_desc consumed by ``api.GpuPlan``.
+A C++ caller of the reference keeps the reference's own host precompute and
+the drop-in header include/sfmm_gpu.hpp.
 """
 from __future__ import annotations
 
@@ -52,9 +55,6 @@ def host_lib() -> C.CDLL:
         lib.sfmm_host_generate_points.argtypes = [C.c_int, C.c_int64, C.c_uint64, vp]
         lib.sfmm_host_generate_charges.argtypes = [C.c_int64, C.c_uint64, vp]
         lib.sfmm_host_generate_charges_complex.argtypes = [C.c_int64, C.c_uint64, vp]
-        lib.sfmm_host_build_tree.argtypes = [C.c_int, C.c_int64, vp, C.c_int, C.POINTER(vp)]
-        lib.sfmm_host_build.argtypes = [C.c_int, C.c_double, C.c_int, C.c_int64, vp, C.c_int,
-                                        C.c_double, C.POINTER(ProxyConfig), C.POINTER(vp)]
         lib.sfmm_host_desc.argtypes = [vp]
         lib.sfmm_host_desc.restype = C.POINTER(PlanDesc)
         lib.sfmm_host_info_get.argtypes = [vp, C.POINTER(HostInfo)]
@@ -119,32 +119,19 @@ class HostPlan:
         self._skel_device = 0
 
     @classmethod
-    def build(cls, kernel: int, pts: np.ndarray, leaf_cap: int, tol: float, kappa: float = 1.0,
-              proxy: tuple | None = None) -> "HostPlan":
-        pts = np.ascontiguousarray(pts, dtype=np.float64)
-        h = C.c_void_p()
-        px = ProxyConfig(*(proxy or (0.0, 0, 0)))
-        _check(host_lib().sfmm_host_build(kernel, kappa, pts.shape[1], pts.shape[0],
-                                          pts.ctypes.data, leaf_cap, tol, C.byref(px),
-                                          C.byref(h)))
-        return cls(h)
-
-    @classmethod
     def build_gpu(cls, kernel: int, pts: np.ndarray, leaf_cap: int, tol: float,
                   kappa: float = 1.0, proxy: tuple | None = None, device: int = 0,
-                  host_T: bool = True, tree: str = "host") -> "HostPlan":
-        """Tree and neighbor lists on the host (bit-identical to the reference),
-        skeletons on the GPU (sfmm_gpu_build_skeletons).
+                  host_T: bool = True) -> "HostPlan":
+        """Tree and neighbor lists (sfmm_gpu_build_tree, bit-identical to the
+        reference) and skeletons (sfmm_gpu_build_skeletons), all on the GPU
+        (SURVEY.md 8(f) rows 1 and 3).
 
         host_T=False keeps the interpolation operators on the device only
         (SURVEY.md 8(f) row 2): the descriptor's T is NULL, api.GpuPlan.from_host
         takes T device-to-device, and fetch_T() downloads it when a host copy is
-        needed (e.g. for the CPU reference).  tree="gpu" builds the tree and
-        neighbor lists on the GPU too (build_tree_gpu)."""
+        needed (e.g. for the CPU reference)."""
         from .api import _raise
-        if tree not in ("host", "gpu"):
-            raise ValueError("build_gpu: tree must be 'host' or 'gpu'")
-        hp = cls.build_tree_gpu(pts, leaf_cap, device) if tree == "gpu" else cls.build_tree(pts, leaf_cap)
+        hp = cls.build_tree_gpu(pts, leaf_cap, device)
         d = host_lib().sfmm_host_desc(hp._h).contents
         nb = int(d.n_boxes)
         center = np.zeros(3 * nb)
@@ -230,14 +217,6 @@ class HostPlan:
             _check(host_lib().sfmm_host_adopt_tree(C.byref(arr), C.byref(h)))
         finally:
             lib.sfmm_gpu_tree_destroy(t)
-        return cls(h)
-
-    @classmethod
-    def build_tree(cls, pts: np.ndarray, leaf_cap: int) -> "HostPlan":
-        pts = np.ascontiguousarray(pts, dtype=np.float64)
-        h = C.c_void_p()
-        _check(host_lib().sfmm_host_build_tree(pts.shape[1], pts.shape[0], pts.ctypes.data,
-                                               leaf_cap, C.byref(h)))
         return cls(h)
 
     def descriptor(self) -> PlanDescriptor:

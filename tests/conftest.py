@@ -80,6 +80,31 @@ def have_ref() -> bool:
 requires_ref = pytest.mark.skipif(not have_ref(), reason="oracle/_ref (reference build) absent")
 
 
+def ref_descriptor(kernel, pts, leaf, tol, kappa=1.0, proxy=None):
+    """Tree, neighbor lists and skeletons from the UNMODIFIED reference pipeline
+    (oracle/_ref: build_tree -> build_neighbor_lists -> build_skeletons), as the
+    flat descriptor the GPU plan takes -- the same operators the reference CPU
+    apply uses, so parity is measured on identical inputs."""
+    from oracle import pyoracle as po
+    px = proxy or (0.0, 0, 0)
+    rp = po.RefPipeline.build(kernel, np.ascontiguousarray(pts, dtype=np.float64), leaf, tol,
+                              kappa, float(px[0]), int(px[1]), int(px[2]))
+    try:
+        return rp.descriptor()
+    finally:
+        rp.close()
+
+
+def gaussian_points(n, seed=1, sigma=0.02, clusters=16):
+    """Config 3(b) input: 16 Gaussian clusters (the reference has no generator)."""
+    from paper_2310_16668_b200 import host
+    if seed == 1 and sigma == 0.02 and clusters == 16:
+        return host.generate_points("gaussian", n, 1)
+    rng = np.random.default_rng(seed)
+    centres = rng.uniform(0.1, 0.9, size=(clusters, 3))
+    return centres[rng.integers(0, clusters, n)] + sigma * rng.standard_normal((n, 3))
+
+
 def rel_l2(u, ref) -> float:
     u = np.asarray(u)
     ref = np.asarray(ref)

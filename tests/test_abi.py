@@ -9,7 +9,7 @@ import subprocess
 import numpy as np
 import pytest
 
-from conftest import ROOT, golden_files, load_golden
+from conftest import ROOT, golden_files, load_golden, ref_descriptor
 from paper_2310_16668_b200 import _abi, api, host
 
 LIB = os.path.join(ROOT, "paper_2310_16668_b200", "lib")
@@ -22,7 +22,8 @@ def declared_functions(header):
 
 
 @pytest.mark.parametrize("header,lib", [("sfmm_gpu.h", "libsfmm_gpu.so"),
-                                        ("sfmm_host.h", "libsfmm_host.so")])
+                                        ("sfmm_host.h", "libsfmm_host.so"),
+                                        ("sfmm_probe.h", "libsfmm_probe.so")])
 def test_library_exports_every_declared_symbol(header, lib):
     names = declared_functions(header)
     assert names, header
@@ -33,6 +34,13 @@ def test_library_exports_every_declared_symbol(header, lib):
 
 def test_python_binding_covers_header():
     assert set(declared_functions("sfmm_gpu.h")) == set(_abi.GPU_SYMBOLS)
+    assert set(declared_functions("sfmm_probe.h")) == set(_abi.PROBE_SYMBOLS)
+
+
+def test_probe_hooks_are_not_in_the_apply_abi():
+    so = C.CDLL(os.path.join(LIB, "libsfmm_gpu.so"))
+    for n in _abi.PROBE_SYMBOLS + ["sfmm_gpu_fp64_peak", "sfmm_gpu_test_log", "sfmm_gpu_test_sincos"]:
+        assert not hasattr(so, n), n
 
 
 def test_gpu_library_is_sm100a_code():
@@ -108,7 +116,7 @@ def test_error_mapping_to_python_exceptions():
 
 
 def test_descriptor_roundtrip_through_npz(tmp_path):
-    d = host.HostPlan.build(1, host.generate_points("cube", 800, 2), 30, 1e-6).descriptor()
+    d = ref_descriptor(1, host.generate_points("cube", 800, 2), 30, 1e-6)
     p = tmp_path / "d.npz"
     d.save(str(p))
     d2, _ = _abi.PlanDescriptor.load(str(p))

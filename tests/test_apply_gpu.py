@@ -11,7 +11,7 @@ import os
 import numpy as np
 import pytest
 
-from conftest import golden_files, load_golden, max_rel, rel_l2, requires_ref
+from conftest import golden_files, load_golden, max_rel, ref_descriptor, rel_l2, requires_ref
 from oracle import pyoracle as po
 from paper_2310_16668_b200 import api, host
 
@@ -38,8 +38,7 @@ def test_depth0_fallback_bit_identical_to_direct_sum():
     # correctly rounded on both sides, so the fallback matches bit for bit.
     pts = np.array([[0.1, 0.2, 0.3], [0.8, 0.9, 0.4]])
     q = np.array([1.5, -0.5])
-    hp = host.HostPlan.build(1, pts, 10, 1e-6)
-    plan = api.GpuPlan(hp.descriptor())
+    plan = api.GpuPlan(ref_descriptor(1, pts, 10, 1e-6))
     st = api.ApplyStats()
     u = api.fmm_apply(plan, q, st)
     assert st.direct_fallback
@@ -49,7 +48,7 @@ def test_depth0_fallback_bit_identical_to_direct_sum():
 def test_depth1_fallback_matches_direct_sum():
     pts = host.generate_points("cube", 900, 13)
     q = host.generate_charges(900, 13)
-    d = host.HostPlan.build(1, pts, 200, 1e-6).descriptor()
+    d = ref_descriptor(1, pts, 200, 1e-6)
     assert d.scalars["depth"] == 1
     u = api.fmm_apply(api.GpuPlan(d), q)
     assert np.array_equal(u, po.oracle_direct_sum(1, 1.0, pts, q))
@@ -57,8 +56,8 @@ def test_depth1_fallback_matches_direct_sum():
 
 def _pipeline(kernel, dist, n, leaf, tol, seed=1, kappa=1.0):
     pts = host.generate_points(dist, n, seed)
-    hp = host.HostPlan.build(kernel, pts, leaf, tol, kappa)
-    return pts, hp, api.GpuPlan(hp.desc_struct())
+    d = ref_descriptor(kernel, pts, leaf, tol, kappa)
+    return pts, d, api.GpuPlan(d)
 
 
 def test_linearity():
@@ -95,7 +94,7 @@ def test_pair_counts():
     _, hp, plan = _pipeline(0, "annulus", n, 25, 1e-5, seed=61)
     st = api.ApplyStats()
     api.fmm_apply(plan, host.generate_charges(n, 62), st)
-    d = hp.descriptor()
+    d = hp
     a = d.arrays
     assert not st.direct_fallback
     assert st.n_ifo_pairs > 0 and st.n_ifs_pairs > 0
@@ -118,7 +117,7 @@ def test_coincident_points_raise_duplicate_error():
     # apply.cpp:31-33: coincident points with distinct ids -> DuplicatePointError.
     # Build a valid plan, then move one point onto another inside the same leaf.
     pts = host.generate_points("cube", 3000, 7)
-    d = host.HostPlan.build(1, pts, 40, 1e-6).descriptor()
+    d = ref_descriptor(1, pts, 40, 1e-6)
     a = d.arrays
     leaf = int(np.nonzero(a["box_leaf"] & (a["box_end"] - a["box_begin"] >= 2))[0][0])
     t0, t1 = a["box_begin"][leaf], a["box_begin"][leaf] + 1
@@ -155,10 +154,27 @@ def test_multi_rhs_matches_oracle_column_loop(kernel, dist, nrhs, kappa):
     else:
         Q = np.stack([host.generate_charges(n, 100 + r) for r in range(nrhs)], axis=1)
     U = api.fmm_apply(plan, Q)
-    U_ref, _ = po.oracle_apply(hp.descriptor(), Q)
+    U_ref, _ = po.oracle_apply(hp, Q)
     assert rel_l2(U, U_ref) <= PARITY
     for r in (0, nrhs - 1):
         assert rel_l2(U[:, r], api.fmm_apply(plan, Q[:, r])) <= 1e-13
+
+
+@pytest.mark.parametrize("kernel,kappa", [(1, 1.0), (3, 10.0)])
+def test_multi_rhs_target_at_padding_coordinate(kernel, kappa):
+    """K2m pads partial source chunks with a fixed far coordinate; a real
+    target sitting exactly there must not see r2 = 0 from the padding (ADVICE
+    r1: G was masked only on the diagonal)."""
+    n = 3000
+    pts = np.concatenate([host.generate_points("cube", n - 1, 5), [[1e3, 1e3, 1e3]]])
+    d = ref_descriptor(kernel, pts, 40, 1e-6, kappa)
+    plan = api.GpuPlan(d)
+    gen = host.generate_charges_complex if kernel == 3 else host.generate_charges
+    Q = np.stack([gen(n, 300 + r) for r in range(16)], axis=1)
+    U = api.fmm_apply(plan, Q)
+    assert np.all(np.isfinite(U))
+    U_ref, _ = po.oracle_apply(d, Q)
+    assert rel_l2(U, U_ref) <= PARITY
 
 
 def test_device_buffer_path_matches_host_path():
@@ -173,6 +189,27 @@ def test_device_buffer_path_matches_host_path():
     api.fmm_apply_device(plan, qd.data_ptr(), ud.data_ptr(), 1, s.cuda_stream)
     api.check_status(plan)
     assert np.array_equal(ud.cpu().numpy(), u_host)
+
+
+def test_applies_on_different_streams_do_not_race():
+    """Two async applies on one plan from two streams, plus a sync apply right
+    after: the plan orders them (ev_done), so each result is exact."""
+    import torch
+    n = 60000
+    _, _, plan = _pipeline(1, "cube", n, 64, 1e-6)
+    qs = [host.generate_charges(n, 70 + i) for i in range(3)]
+    ref = [api.fmm_apply(plan, q) for q in qs]
+    qd = [torch.from_numpy(q).cuda() for q in qs]
+    ud = [torch.empty_like(x) for x in qd]
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    for _ in range(3):
+        api.fmm_apply_device(plan, qd[0].data_ptr(), ud[0].data_ptr(), 1, s1.cuda_stream)
+        api.fmm_apply_device(plan, qd[1].data_ptr(), ud[1].data_ptr(), 1, s2.cuda_stream)
+        u2 = api.fmm_apply(plan, qs[2])
+        api.check_status(plan)
+        assert np.array_equal(ud[0].cpu().numpy(), ref[0])
+        assert np.array_equal(ud[1].cpu().numpy(), ref[1])
+        assert np.array_equal(u2, ref[2])
 
 
 def test_device_path_graph_replay_multi_rhs():
@@ -207,7 +244,7 @@ def test_parity_vs_reference_at_scale(kernel, dist, n, leaf, tol, kappa):
     q = (host.generate_charges_complex(n, 1 ^ host.CHARGE_STREAM) if kernel == 3
          else host.generate_charges(n, 1 ^ host.CHARGE_STREAM))
     u = api.fmm_apply(plan, q)
-    rp = po.RefPipeline.from_desc(hp.desc_struct())
+    rp = po.RefPipeline.from_desc(hp)
     u_ref, st = rp.apply(q, kernel == 3)
     assert rel_l2(u, u_ref) <= PARITY
     # sampled dense check on the GPU (oracle.cpp:51-71)
@@ -268,8 +305,7 @@ def test_degenerate_geometries_match_oracle(name, kernel, kappa):
     GPU path and the C restatement agree to the parity bar."""
     pts = _degenerate_sets()[name]
     n = len(pts)
-    hp = host.HostPlan.build(kernel, pts, 32, 1e-6, kappa)
-    d = hp.descriptor()
+    d = ref_descriptor(kernel, pts, 32, 1e-6, kappa)
     q = host.generate_charges_complex(n, 3) if kernel == 3 else host.generate_charges(n, 3)
     st = api.ApplyStats()
     u = api.fmm_apply(api.GpuPlan(d), q, st)
@@ -279,7 +315,7 @@ def test_degenerate_geometries_match_oracle(name, kernel, kappa):
 
 
 def test_api_misuse_raises():
-    d = host.HostPlan.build(1, host.generate_points("cube", 3000, 2), 40, 1e-6).descriptor()
+    d = ref_descriptor(1, host.generate_points("cube", 3000, 2), 40, 1e-6)
     with pytest.raises((api.DeviceError, ValueError)):
         api.GpuPlan(d, device=99)                     # no such device
     plan = api.GpuPlan(d)
@@ -288,6 +324,11 @@ def test_api_misuse_raises():
         api.fmm_apply(plan, q.reshape(3000, 1)[:, :0])  # zero right-hand sides
     with pytest.raises(ValueError):
         api.fmm_apply(plan, q, out=np.empty(2999))     # wrong output buffer
+    with pytest.raises(ValueError):
+        api.fmm_apply(plan, q, out=np.empty(6000)[::2])  # strided output view
+    big = np.zeros(6000)
+    api.fmm_apply(plan, q, out=big[:3000])            # contiguous view: written in place
+    assert np.any(big[:3000] != 0) and not np.any(big[3000:])
     plan.close()
     with pytest.raises(ValueError):
         api.fmm_apply(plan, q)                        # closed plan

@@ -1,0 +1,136 @@
+"""Parity at every BASELINE.json configuration, against the UNMODIFIED reference.
+
+Each case builds the tree, neighbor lists and skeletons with the reference's
+own pipeline (oracle/_ref: build_tree -> build_neighbor_lists ->
+build_skeletons, as test_apply.cpp:22-34 does), hands the flat descriptor to
+the GPU plan, and compares the GPU apply with the reference CPU fmm_apply on
+the same operators and charges:
+
+* rel-l2 <= 1e-12 (north star) and identical ApplyStats pair counts;
+* max-rel vs the reference dense sum on sampled targets <= 10 * tol
+  (test_apply.cpp:108-152, acceptance.cpp:190-226).
+
+Sizes are the largest the reference CPU apply finishes in well under a minute
+on the GPU box's 16 host cores: config 1 and 2 at their full N, the
+non-uniform config 3 geometries (sphere, clustered Gaussian) at 1e6 / 3e5
+with the config's leaf 128 and tol 1e-8, the 16-RHS Helmholtz config 4 at
+N = 2e5 against the reference's column loop over all 16 columns.  bench.py
+--config cX adds the full-N relerr_vs_cpu_ref line of each config.
+"""
+import numpy as np
+import pytest
+
+from conftest import max_rel, ref_descriptor, rel_l2, requires_ref
+from oracle import pyoracle as po
+from paper_2310_16668_b200 import api, host
+
+pytestmark = [pytest.mark.gpu, requires_ref]
+
+PARITY = 1e-12
+CHARGE_STREAM = 0x9E3779B97F4A7C15
+
+
+def _leaf_levels(d):
+    a = d.arrays
+    return np.unique(a["box_level"][a["box_leaf"].astype(bool)])
+
+
+def _targets(n, m=1000, seed=0xC2B2AE3D27D4EB4F):
+    rng = np.random.default_rng(seed)
+    return np.sort(rng.choice(n, size=min(m, n), replace=False)).astype(np.int32)
+
+
+def _check_against_reference(kernel, pts, leaf, tol, kappa, q, n_check=1000):
+    """GPU apply vs the reference apply on the reference's own operators."""
+    rp = po.RefPipeline.build(kernel, pts, leaf, tol, kappa)
+    d = rp.descriptor()
+    cplx = kernel == 3
+    u_ref, st_ref = rp.apply(q, cplx)
+    plan = api.GpuPlan(d)
+    st = api.ApplyStats()
+    u = api.fmm_apply(plan, q, st)
+    err = rel_l2(u, u_ref)
+    assert err <= PARITY, err
+    assert (st.n_ifo_pairs, st.n_ifs_pairs, st.n_tfo_pairs, st.n_level1_pairs) == (
+        st_ref["n_ifo_pairs"], st_ref["n_ifs_pairs"], st_ref["n_tfo_pairs"],
+        st_ref["n_level1_pairs"])
+    t = _targets(len(q), n_check)
+    dense = po.ref_direct_sum(kernel, kappa, pts, q, t)
+    assert max_rel(u[t], dense) <= 10 * tol
+    plan.close()
+    rp.close()
+    return d, st_ref, err
+
+
+def test_config1_laplace2d_square_full_size():
+    n = 100_000
+    pts = host.generate_points("square", n, 1)
+    q = host.generate_charges(n, 1 ^ CHARGE_STREAM)
+    d, _, _ = _check_against_reference(0, pts, 64, 1e-6, 1.0, q)
+    assert d.scalars["depth"] >= 5
+
+
+def test_config2_laplace3d_cube_full_size():
+    n = 1_000_000
+    pts = host.generate_points("cube", n, 1)
+    q = host.generate_charges(n, 1 ^ CHARGE_STREAM)
+    d, _, _ = _check_against_reference(1, pts, 128, 1e-6, 1.0, q)
+    assert d.scalars["depth"] == 5
+
+
+def test_config3a_sphere_adaptive():
+    # tol 1e-8, leaf 128 (config 3a) at N = 1e6: several leaf levels, ifs/tfo pairs
+    n = 1_000_000
+    pts = host.generate_points("sphere", n, 1)
+    q = host.generate_charges(n, 1 ^ CHARGE_STREAM)
+    d, st, _ = _check_against_reference(1, pts, 128, 1e-8, 1.0, q)
+    assert len(_leaf_levels(d)) >= 3
+    assert st["n_ifs_pairs"] > 0 and st["n_tfo_pairs"] > 0
+
+
+def test_config3b_clustered_gaussian():
+    # 16 Gaussian clusters, sigma 0.02 (no reference generator),
+    # tol 1e-8, leaf 128 at N = 3e5: depth 7, four leaf levels
+    n = 300_000
+    pts = host.generate_points("gaussian", n, 1)
+    q = host.generate_charges(n, 1 ^ CHARGE_STREAM)
+    d, st, _ = _check_against_reference(1, pts, 128, 1e-8, 1.0, q)
+    assert d.scalars["depth"] >= 7
+    assert len(_leaf_levels(d)) >= 3
+    assert st["n_ifs_pairs"] > 0 and st["n_tfo_pairs"] > 0
+
+
+@pytest.mark.parametrize("fam,dist,cap", [(0, "annulus", 100), (1, "sphere", 80)])
+def test_acceptance_c5_adaptive_paths(fam, dist, cap):
+    # acceptance.cpp:190-226: N = 5e4, tol 1e-6, seed 17, >= 3 leaf levels,
+    # ifs and tfo pairs present, relerr <= 10 tol
+    n = 50_000
+    pts = host.generate_points(dist, n, 17)
+    q = host.generate_charges(n, 17 ^ CHARGE_STREAM)
+    d, st, _ = _check_against_reference(fam, pts, cap, 1e-6, 1.0, q)
+    assert len(_leaf_levels(d)) >= 3
+    assert st["n_ifs_pairs"] > 0 and st["n_tfo_pairs"] > 0
+
+
+def test_config4_helmholtz_16rhs_vs_reference_column_loop():
+    # kappa = 10, cube, leaf 128, tol 1e-6, 16 right-hand sides in one GPU
+    # apply (DMMA multi-RHS path) vs the reference's one-RHS apply per column
+    n, nrhs, kappa = 200_000, 16, 10.0
+    pts = host.generate_points("cube", n, 1)
+    Q = np.asfortranarray(np.stack(
+        [host.generate_charges_complex(n, (1 + r) ^ CHARGE_STREAM) for r in range(nrhs)], 1))
+    rp = po.RefPipeline.build(3, pts, 128, 1e-6, kappa)
+    d = rp.descriptor()
+    plan = api.GpuPlan(d)
+    U = api.fmm_apply(plan, Q)
+    worst = 0.0
+    for r in range(nrhs):
+        u_ref, _ = rp.apply(Q[:, r], True)
+        err = rel_l2(U[:, r], u_ref)
+        worst = max(worst, err)
+        assert err <= PARITY, (r, err)
+    t = _targets(n, 300)
+    dense = po.ref_direct_sum(3, kappa, pts, Q[:, 0], t)
+    assert max_rel(U[t, 0], dense) <= 10 * 1e-6
+    plan.close()
+    rp.close()

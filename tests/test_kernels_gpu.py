@@ -17,7 +17,7 @@ def test_fast_sincos_within_two_ulp():
                         rng.uniform(-1e6, 1e6, 50000),
                         np.arange(-64, 65) * (np.pi / 4)]).astype(np.float64)
     out = np.zeros(6 * x.size)
-    assert _abi.gpu_lib().sfmm_gpu_test_sincos(x.ctypes.data, x.size, out.ctypes.data) == 0
+    assert _abi.probe_lib().sfmm_probe_test_sincos(x.ctypes.data, x.size, out.ctypes.data) == 0
     s_ref, c_ref = out[4::6], out[5::6]
     assert np.allclose(s_ref, np.sin(x), atol=1e-15, rtol=0)
     # branch-free (out[0:2]) and table-driven (out[2:4]) versions: absolute
@@ -40,7 +40,7 @@ def test_table_log_within_two_ulp():
                         1.0 + rng.uniform(-1e-6, 1e-6, 50000), 1.0 + np.arange(-50, 51) * 2.0 ** -52,
                         np.array([1.0, 2.0, 0.5, np.sqrt(2.0), 1e-310, 0.0, np.inf])])
     out = np.zeros(2 * x.size)
-    assert _abi.gpu_lib().sfmm_gpu_test_log(x.ctypes.data, x.size, out.ctypes.data) == 0
+    assert _abi.probe_lib().sfmm_probe_test_log(x.ctypes.data, x.size, out.ctypes.data) == 0
     got, ref = out[0::2], out[1::2]
     with np.errstate(divide="ignore"):
         assert np.allclose(ref, np.log(x), rtol=1e-15, atol=0, equal_nan=True)

@@ -12,13 +12,13 @@ import socket
 import numpy as np
 import pytest
 
-from conftest import max_rel, rel_l2
+from conftest import max_rel, ref_descriptor, rel_l2
 from paper_2310_16668_b200 import api, host, shard
 
 
 def _desc(dist="cube", n=20000, leaf=64, kernel=1, tol=1e-6, kappa=1.0, seed=1):
     pts = host.generate_points(dist, n, seed)
-    return host.HostPlan.build(kernel, pts, leaf, tol, kappa).descriptor(), pts
+    return ref_descriptor(kernel, pts, leaf, tol, kappa), pts
 
 
 @pytest.mark.parametrize("n_ranks", [1, 2, 4, 8])
@@ -134,7 +134,7 @@ def _lopsided(seed=3):
 
 def test_level1_leaves_are_units():
     pts = _lopsided()
-    d = host.HostPlan.build(1, pts, 64, 1e-6, 1.0).descriptor()
+    d = ref_descriptor(1, pts, 64, 1e-6, 1.0)
     leaf1 = np.nonzero((d.arrays["box_level"] == 1) & d.arrays["box_leaf"].astype(bool))[0]
     assert leaf1.size > 0
     infos = [shard.describe(d, 8, r) for r in range(8)]
@@ -260,7 +260,7 @@ def test_sharded_plans_from_device_operator_blobs(kernel, n_ranks):
     import torch
     n = 30000 if kernel == 1 else 12000
     pts = host.generate_points("cube", n, 1)
-    hp = host.HostPlan.build_gpu(kernel, pts, 64, 1e-6, 5.0, host_T=False, tree="gpu")
+    hp = host.HostPlan.build_gpu(kernel, pts, 64, 1e-6, 5.0, host_T=False)
     d = hp.desc_struct()
     assert not bool(d.T)
     q = host.generate_charges_complex(n, 3) if kernel == 3 else host.generate_charges(n, 3)
@@ -322,7 +322,7 @@ def test_virtual_ranks_level1_leaves(n_ranks):
     import torch
     pts = _lopsided()
     n = pts.shape[0]
-    d = host.HostPlan.build(1, pts, 64, 1e-6, 1.0).descriptor()
+    d = ref_descriptor(1, pts, 64, 1e-6, 1.0)
     q = host.generate_charges(n, 4)
     u_ref = api.fmm_apply(api.GpuPlan(d), q)
     plans = [shard.ShardedPlan(d, n_ranks, r) for r in range(n_ranks)]
@@ -357,16 +357,16 @@ def test_virtual_ranks_parity_vs_oracle_1e6():
     from oracle import pyoracle as po
     n = 1000000
     pts = host.generate_points("cube", n, 1)
-    hp = host.HostPlan.build(1, pts, 128, 1e-6)
+    hp = ref_descriptor(1, pts, 128, 1e-6)
     q = host.generate_charges(n, 1 ^ host.CHARGE_STREAM)
-    plans = [shard.ShardedPlan(hp.desc_struct(), 8, r) for r in range(8)]
+    plans = [shard.ShardedPlan(hp, 8, r) for r in range(8)]
     qd = torch.from_numpy(q).cuda()
     ud = torch.zeros_like(qd)
     shard.apply_virtual(plans, qd, ud)
     torch.cuda.synchronize()
     u = ud.cpu().numpy()
     if po.have_ref():
-        u_ref, _ = po.RefPipeline.from_desc(hp.desc_struct()).apply(q)
+        u_ref, _ = po.RefPipeline.from_desc(hp).apply(q)
         assert rel_l2(u, u_ref) <= 1e-12
     t = np.arange(0, n, 9973, dtype=np.int32)
     assert max_rel(u[t], api.direct_sum_subset(1, 1.0, pts, q, t)) <= 1e-5

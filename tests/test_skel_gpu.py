@@ -1,7 +1,6 @@
 """GPU skeletonization against the reference criteria.
 
-Same checks as the host skeletonizer (tests/test_host.py) and the reference's
-own tests: accuracy of the resulting apply against the dense sum
+Same checks as the reference's own tests: accuracy of the resulting apply against the dense sum
 (test_apply.cpp:108-162), the ID far-field property and skeleton nesting
 (acceptance.cpp C6), and apply parity on the GPU-built operators.
 """
@@ -37,11 +36,14 @@ def test_gpu_skeletons_meet_tolerance(kernel, dist, kappa):
     (1, "cube", 20000, 64, 1e-6), (1, "sphere", 20000, 40, 1e-8), (0, "annulus", 8000, 30, 1e-6),
     (3, "cube", 8000, 64, 1e-6),
 ])
-def test_gpu_skeleton_ranks_match_host(kernel, dist, n, leaf, tol):
+@requires_ref
+def test_gpu_skeleton_ranks_match_reference(kernel, dist, n, leaf, tol):
     pts = host.generate_points(dist, n, 7)
     kappa = 10.0 if kernel == 3 else 1.0
     ig = host.HostPlan.build_gpu(kernel, pts, leaf, tol, kappa).info()
-    ic = host.HostPlan.build(kernel, pts, leaf, tol, kappa).info()
+    rp = po.RefPipeline.build(kernel, pts, leaf, tol, kappa)
+    ic = rp.info()
+    rp.close()
     # same algorithm; rounding may move a pivot, so compare totals loosely
     assert abs(ig["k_max"] - ic["k_max"]) <= 2
     assert abs(ig["proj_scalars"] - ic["proj_scalars"]) <= 0.01 * ic["proj_scalars"]
@@ -127,7 +129,7 @@ def test_plan_from_points_is_the_step_by_step_pipeline(kernel, dist, kappa):
     pts = host.generate_points(dist, n, 9)
     q = host.generate_charges_complex(n, 1) if kernel == 3 else host.generate_charges(n, 1)
     u1 = api.fmm_apply(api.GpuPlan.from_points(kernel, pts, 64, 1e-6, kappa), q)
-    hp = host.HostPlan.build_gpu(kernel, pts, 64, 1e-6, kappa, tree="gpu", host_T=False)
+    hp = host.HostPlan.build_gpu(kernel, pts, 64, 1e-6, kappa, host_T=False)
     u2 = api.fmm_apply(api.GpuPlan.from_host(hp), q)
     assert np.array_equal(u1, u2)
 

@@ -1,11 +1,11 @@
 """GPU tree and neighbor lists: bit-identical to the
-host builder (itself pinned against the reference in tests/test_host.py) and
-to the reference directly, as test_tree.cpp:168-200 pins the reference's own
-tree; error behaviour as tree.cpp:148-186."""
+unmodified reference build_tree + build_neighbor_lists (oracle/_ref), as
+test_tree.cpp:168-200 pins the reference's own tree, box geometry included;
+error behaviour as tree.cpp:148-186."""
 import numpy as np
 import pytest
 
-from conftest import requires_ref
+from conftest import gaussian_points, requires_ref
 from oracle import pyoracle as po
 from paper_2310_16668_b200 import api, host
 
@@ -24,40 +24,38 @@ def _geometry(hp):
 
 def _same_tree(pts, leaf):
     g = host.HostPlan.build_tree_gpu(pts, leaf)
-    h = host.HostPlan.build_tree(pts, leaf)
-    dg, dh = g.descriptor(), h.descriptor()
+    r = po.RefPipeline.build_tree(pts, leaf)
+    dg, dr = g.descriptor(), r.descriptor()
     for k in TREE_KEYS:
-        assert np.array_equal(dg.arrays[k], dh.arrays[k]), k
-    assert dg.scalars["depth"] == dh.scalars["depth"]
+        assert np.array_equal(dg.arrays[k], dr.arrays[k]), k
+    assert dg.scalars["depth"] == dr.scalars["depth"]
     cg, hg = _geometry(g)
-    ch, hh = _geometry(h)
-    assert np.array_equal(cg, ch) and np.array_equal(hg, hh)
+    cr, hr = r.box_geometry()
+    assert np.array_equal(cg, cr) and np.array_equal(hg, hr)
+    r.close()
     return dg
-
-
-def _gaussian(n, seed=1, sigma=0.02):
-    rng = np.random.default_rng(seed)
-    centres = rng.uniform(0.1, 0.9, size=(16, 3))
-    return centres[rng.integers(0, 16, n)] + sigma * rng.standard_normal((n, 3))
 
 
 @pytest.mark.parametrize("dist,n,leaf", [
     ("square", 4000, 20), ("annulus", 8000, 50), ("cube", 5000, 60), ("sphere", 5000, 60),
     ("sphere", 30000, 30), ("cube", 60000, 128), ("annulus", 3000, 1), ("cube", 7, 1),
     ("cube", 1, 1), ("square", 100, 1000), ("cube", 5000, 4096), ("sphere", 200000, 40),
-    ("square", 300000, 16),
+    ("square", 300000, 16), ("cube", 50000, 64), ("sphere", 40000, 30), ("annulus", 20000, 16),
 ])
-def test_gpu_tree_matches_host(dist, n, leaf):
+@requires_ref
+def test_gpu_tree_matches_reference(dist, n, leaf):
     _same_tree(host.generate_points(dist, n, 29), leaf)
 
 
 @pytest.mark.parametrize("n,leaf,sigma", [(20000, 40, 0.02), (200000, 64, 0.01), (50000, 8, 0.05)])
+@requires_ref
 def test_gpu_tree_clustered_balance_replay(n, leaf, sigma):
     # clustered input forces order-dependent 2:1 splits (the host replay path)
-    d = _same_tree(_gaussian(n, 3, sigma), leaf)
+    d = _same_tree(gaussian_points(n, 3, sigma), leaf)
     assert d.scalars["depth"] >= 5
 
 
+@requires_ref
 def test_gpu_tree_degenerate_inputs():
     # collinear, coplanar and grid points (ties on split planes)
     x = np.linspace(0, 1, 4097)
@@ -65,17 +63,6 @@ def test_gpu_tree_degenerate_inputs():
     g = np.stack(np.meshgrid(np.arange(32.0), np.arange(32.0), indexing="ij"), -1).reshape(-1, 2)
     _same_tree(g, 4)
     _same_tree(np.concatenate([g, np.zeros((len(g), 1))], 1) * -3.5, 16)
-
-
-@requires_ref
-@pytest.mark.parametrize("dist,n,leaf", [("cube", 50000, 64), ("sphere", 40000, 30),
-                                         ("annulus", 20000, 16)])
-def test_gpu_tree_bit_identical_to_reference(dist, n, leaf):
-    pts = po.generate_points(dist, n, 5)
-    mine = host.HostPlan.build_tree_gpu(pts, leaf).descriptor()
-    ref = po.RefPipeline.build(0 if pts.shape[1] == 2 else 1, pts, leaf, 1e-6).descriptor()
-    for k in TREE_KEYS:
-        assert np.array_equal(mine.arrays[k], ref.arrays[k]), k
 
 
 def test_gpu_tree_errors():
@@ -95,18 +82,8 @@ def test_gpu_tree_errors():
         host.HostPlan.build_tree_gpu(bad, 10)
 
 
-def test_gpu_tree_feeds_the_apply():
-    n = 40000
-    pts = host.generate_points("sphere", n, 2)
-    hg = host.HostPlan.build_gpu(1, pts, 64, 1e-6, tree="gpu")
-    hh = host.HostPlan.build_gpu(1, pts, 64, 1e-6, tree="host")
-    q = host.generate_charges(n, 3)
-    ug = api.fmm_apply(api.GpuPlan.from_host(hg), q)
-    uh = api.fmm_apply(api.GpuPlan.from_host(hh), q)
-    assert np.array_equal(ug, uh)
-
-
 @pytest.mark.parametrize("dist,n,leaf", [("cube", 10_000_000, 128), ("sphere", 3_000_000, 128)])
-def test_gpu_tree_matches_host_at_scale(dist, n, leaf):
+@requires_ref
+def test_gpu_tree_matches_reference_at_scale(dist, n, leaf):
     # the headline geometry and a large adaptive one (balance replay on the host)
     _same_tree(host.generate_points(dist, n, 1), leaf)

@@ -12,7 +12,7 @@ for kern, dist, n, leaf, kappa, nrhs in [(3, "cube", 20000, 64, 10.0, 16), (1, "
                                           (0, "square", 20000, 64, 1.0, 16), (3, "sphere", 30000, 64, 10.0, 20),
                                           (3, "cube", 400000, 128, 10.0, 16)]:
     pts = host.generate_points(dist, n, 1)
-    hp = host.HostPlan.build(kern, pts, leaf, 1e-6, kappa)
+    hp = host.HostPlan.build_gpu(kern, pts, leaf, 1e-6, kappa)
     plan = api.GpuPlan(hp.desc_struct())
     if kern == 3:
         Q = np.stack([host.generate_charges_complex(n, (1 + r) ^ host.CHARGE_STREAM) for r in range(nrhs)], 1)

@@ -3,7 +3,7 @@ import numpy as np, sys
 from paper_2310_16668_b200 import host
 n=int(float(sys.argv[1])); dist=sys.argv[2] if len(sys.argv)>2 else "cube"; tol=float(sys.argv[3]) if len(sys.argv)>3 else 1e-6
 pts=host.generate_points(dist,n,1)
-hp=host.HostPlan.build(1,pts,128,tol)
+hp=host.HostPlan.build_gpu(1,pts,128,tol)
 a=hp.descriptor().arrays
 nb=np.diff(a["iv_off"]).astype(np.int64); kb=np.diff(a["sk_off"]).astype(np.int64)
 lvl=a["box_level"]; unc=(lvl>=2)&(nb>0)&(kb==nb)

@@ -25,7 +25,7 @@ s = torch.cuda.Stream()
 
 def rate_1gpu(n1):
     pts = host.generate_points("cube", n1, 1)
-    hp = host.HostPlan.build_gpu(1, pts, 128, 1e-6, host_T=False, tree="gpu")
+    hp = host.HostPlan.build_gpu(1, pts, 128, 1e-6, host_T=False)
     q = torch.from_numpy(host.generate_charges(n1, 1)).cuda()
     u = torch.zeros_like(q)
     with api.GpuPlan.from_host(hp) as p:
@@ -46,7 +46,7 @@ r1, w1 = rate_1gpu(10_000_000)
 print(f"1 GPU, N=1e7: {r1 / 1e6:.1f} Mpoints/s, {w1 / 1e7:.0f} dense pairs per point", flush=True)
 t0 = time.perf_counter()
 pts = host.generate_points("cube", n, 1)
-hp = host.HostPlan.build_gpu(1, pts, 128, 1e-6, host_T=False, tree="gpu")
+hp = host.HostPlan.build_gpu(1, pts, 128, 1e-6, host_T=False)
 info = hp.info()
 print(f"N={n:.0e}: precompute {time.perf_counter() - t0:.1f} s, depth {info['depth']}, "
       f"{info['n_boxes']} boxes, k_max {info['k_max']}", flush=True)

@@ -22,7 +22,7 @@ tol = float(sys.argv[3]) if len(sys.argv) > 3 else 1e-6
 RANKS = [int(x) for x in sys.argv[4].split(",")] if len(sys.argv) > 4 else [2, 4, 8]
 REPS = 10  # timed begin/end pairs per rank (median)
 pts = host.generate_points(dist, n, 1)
-hp = host.HostPlan.build_gpu(1, pts, 128, tol, tree="gpu")
+hp = host.HostPlan.build_gpu(1, pts, 128, tol)
 q = host.generate_charges(n, 1)
 qd = torch.from_numpy(q).cuda()
 ud = torch.zeros_like(qd)

@@ -11,7 +11,7 @@ from paper_2310_16668_b200 import api, host, shard  # noqa: E402
 n = int(float(sys.argv[1])) if len(sys.argv) > 1 else 1000000
 leaf = int(sys.argv[2]) if len(sys.argv) > 2 else 128
 pts = host.generate_points("cube", n, 1)
-hp = host.HostPlan.build(1, pts, leaf, 1e-6)
+hp = host.HostPlan.build_gpu(1, pts, leaf, 1e-6)
 print("depth", hp.info()["depth"], "n_boxes", hp.info()["n_boxes"], "leaf", leaf, "env", os.environ.get("SFMM_SYMMETRIC"), os.environ.get("SFMM_SKIP_CANCEL"))
 q = host.generate_charges(n, 5)
 u_ref = api.fmm_apply(api.GpuPlan(hp.desc_struct()), q)

@@ -12,7 +12,7 @@ tol = float(sys.argv[4]) if len(sys.argv) > 4 else 1e-6
 pts = host.generate_points(dist, n, 1)
 for rep in range(2):
     t = time.perf_counter()
-    hp = host.HostPlan.build_gpu(kern, pts, 128, tol, 10.0 if kern == 3 else 1.0, host_T=False, tree="gpu")
+    hp = host.HostPlan.build_gpu(kern, pts, 128, tol, 10.0 if kern == 3 else 1.0, host_T=False)
     inf = hp.info()
     print(f"rep {rep}: total {time.perf_counter() - t:.3f} s  tree {inf['t_tree']:.3f}  skel {inf['t_skel']:.3f}"
           f"  k_max {inf['k_max']} proj {inf['proj_scalars']}", flush=True)
