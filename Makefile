@@ -14,9 +14,9 @@ NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -I$(SRC)
 CXXFLAGS := -std=c++17 -O2 -fopenmp -fPIC -Iinclude -I$(SRC) -I/usr/local/cuda/include
 
 GPU_CU   := $(SRC)/kernels_translate.cu $(SRC)/kernels_tree.cu $(SRC)/kernels_multi.cu $(SRC)/skel_gpu.cu \
-            $(SRC)/tree_gpu.cu $(SRC)/sfmm_gpu.cu
+            $(SRC)/tree_gpu.cu $(SRC)/sfmm_gpu.cu $(SRC)/sfmm_multi.cu
 GPU_OBJS := $(patsubst $(SRC)/%.cu,$(OBJ)/%.o,$(GPU_CU)) $(OBJ)/plan_build.o
-HDRS     := include/sfmm_gpu.h $(SRC)/common.cuh $(SRC)/launch.h $(SRC)/plan_build.h $(SRC)/fastmath.cuh $(SRC)/log_table.inc
+HDRS     := include/sfmm_gpu.h $(SRC)/plan.h $(SRC)/common.cuh $(SRC)/launch.h $(SRC)/plan_build.h $(SRC)/fastmath.cuh $(SRC)/log_table.inc
 
 .PHONY: all gpu host probe oracle clean
 all: gpu host probe

@@ -55,6 +55,12 @@ enum {
   SFMM_DEVICE_BUFFERS = 1  /* q and u are device pointers on the plan's device */
 };
 
+/* Output of a collective apply on an NCCL rank plan (sfmm_gpu_set_output). */
+enum {
+  SFMM_OUTPUT_FULL = 0,  /* every rank's u receives the whole result */
+  SFMM_OUTPUT_OWNED = 1  /* u receives this rank's owned points only */
+};
+
 /*
  * Flat plan descriptor.  All arrays are host memory, read once during
  * sfmm_gpu_plan_create and not retained.  Field meanings follow the reference
@@ -130,6 +136,7 @@ typedef struct sfmm_gpu_plan_info {
 } sfmm_gpu_plan_info;
 
 typedef struct sfmm_gpu_plan sfmm_gpu_plan;
+typedef struct sfmm_skel_result sfmm_skel_result; /* GPU skeletonization result (below) */
 
 /* Builds a device-resident plan on CUDA device `device`. */
 int sfmm_gpu_plan_create(const sfmm_plan_desc* desc, int device, sfmm_gpu_plan** out);
@@ -213,6 +220,45 @@ int sfmm_gpu_apply_mid(sfmm_gpu_plan* plan, const void* recv_dev, void* send2_de
                        void* packed_event);
 int sfmm_gpu_apply_fin(sfmm_gpu_plan* plan, const void* q_dev, const void* recv2_dev, void* u_dev,
                        void* stream);
+
+/*
+ * Multi-GPU with the exchanges inside this library.
+ *
+ * Single process, several GPUs: sfmm_gpu_plan_create_multi builds one sharded
+ * rank plan per entry of dev_ids (dev_ids[0] is the primary device; ids may
+ * repeat, e.g. {0,0,0,0} runs four ranks on one GPU) and returns ONE plan that
+ * sfmm_gpu_apply / sfmm_gpu_apply_async drive like a single-GPU plan: q and u
+ * (host, or device buffers on the primary) in the original order, the result
+ * bit-identical to the single-GPU plan's.  Each apply runs every rank's
+ * gather + upward pass, one cudaMemcpyPeerAsync per (sender, receiver) ghost
+ * segment over NVLink, the translations, one peer copy per column-sum segment,
+ * and the downward pass; the other devices gather q and scatter u through
+ * peer memory.  Distinct devices need peer access (SFMM_EUNSUPPORTED
+ * otherwise).  Several right-hand sides run one column at a time.
+ * _skel: operators taken device-to-device (peer copies) from a GPU
+ * skeletonization result, as sfmm_gpu_plan_create_skel.
+ */
+int sfmm_gpu_plan_create_multi(const sfmm_plan_desc* desc, int n_dev, const int* dev_ids,
+                               sfmm_gpu_plan** out);
+int sfmm_gpu_plan_create_multi_skel(const sfmm_plan_desc* desc, const sfmm_skel_result* skel,
+                                    int n_dev, const int* dev_ids, sfmm_gpu_plan** out);
+
+/*
+ * One process per GPU: after sfmm_gpu_plan_create_sharded(_T) of rank `rank`,
+ * sfmm_gpu_plan_attach_nccl joins the ranks into one NCCL communicator (rank 0
+ * makes the id with sfmm_gpu_nccl_unique_id and the caller broadcasts its 128
+ * bytes, e.g. over MPI or torch.distributed).  sfmm_gpu_apply and
+ * sfmm_gpu_apply_async on the plan are then COLLECTIVE (every rank calls them
+ * with the same q) and run both exchanges as grouped ncclSend/ncclRecv on the
+ * apply stream; u receives the full result (one in-place ncclAllReduce) or,
+ * after sfmm_gpu_set_output(plan, SFMM_OUTPUT_OWNED), only the rank's owned
+ * points.  libnccl.so.2 is loaded at run time (SFMM_NCCL_LIB overrides the
+ * path); failures return SFMM_ENCCL.
+ */
+#define SFMM_NCCL_ID_BYTES 128
+int sfmm_gpu_nccl_unique_id(void* id);
+int sfmm_gpu_plan_attach_nccl(sfmm_gpu_plan* plan, const void* id, int n_ranks, int rank);
+int sfmm_gpu_set_output(sfmm_gpu_plan* plan, int mode);
 
 /* Operators of rank `rank`'s owned boxes without the full T on every rank:
  * sfmm_gpu_shard_T_runs (host-only) lists the runs [src, src + len) of
@@ -313,8 +359,6 @@ typedef struct sfmm_tree_desc {
   const double* box_center;   /* n_boxes * 3 */
   const double* box_half;     /* n_boxes */
 } sfmm_tree_desc;
-
-typedef struct sfmm_skel_result sfmm_skel_result;
 
 int sfmm_gpu_build_skeletons(const sfmm_tree_desc* tree, int kernel, double kappa, double tol,
                              double proxy_radius, int proxy_edge2d, int proxy_face3d, int device,

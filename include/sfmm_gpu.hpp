@@ -84,6 +84,31 @@ class GpuPlan {
   using scalar = typename K::scalar;
 
   explicit GpuPlan(const ApplyPlan<K>& plan, int device = 0) : n_(plan.tree->pts.size()) {
+    with_descriptor(plan, [&](const sfmm_plan_desc& d) {
+      detail::raise(sfmm_gpu_plan_create(&d, device, &h_), "GpuPlan");
+    });
+  }
+
+  // The same plan sharded over several GPUs of this process (whole subtrees
+  // per device; ghost and column-sum exchanges by peer copies inside the
+  // library, sfmm_gpu_plan_create_multi).  devices[0] holds q and u; ids may
+  // repeat ({0, 0, 0, 0}: four ranks on one GPU).  fmm_apply is unchanged and
+  // returns the single-GPU result.
+  GpuPlan(const ApplyPlan<K>& plan, const std::vector<int>& devices) : n_(plan.tree->pts.size()) {
+    if (devices.empty()) throw std::invalid_argument("GpuPlan: empty device list");
+    with_descriptor(plan, [&](const sfmm_plan_desc& d) {
+      detail::raise(sfmm_gpu_plan_create_multi(&d, static_cast<int>(devices.size()),
+                                               devices.data(), &h_),
+                    "GpuPlan");
+    });
+  }
+
+ private:
+  // Flattens the borrowed Tree / NeighborLists / SkeletonSet into an
+  // sfmm_plan_desc (valid during the call only) and hands it to `create`.
+  template <class F>
+  static void with_descriptor(const ApplyPlan<K>& plan, F&& create) {
+    const int64_t n = plan.tree->pts.size();
     const Tree& t = *plan.tree;
     const NeighborLists& nb = *plan.nb;
     const SkeletonSet<scalar>& sk = *plan.skel;
@@ -121,7 +146,7 @@ class GpuPlan {
     d.kernel = detail::KernelId<K>::value;
     d.dim = t.dim;
     d.kappa = detail::kappa_of(plan.kernel);
-    d.n_points = n_;
+    d.n_points = n;
     d.n_boxes = static_cast<int32_t>(nbox);
     d.depth = t.depth;
     d.pts = t.pts.coords.data();
@@ -147,9 +172,10 @@ class GpuPlan {
     d.coarse = coarse.data();
     d.fine_off = fine_off.data();
     d.fine = fine.data();
-    detail::raise(sfmm_gpu_plan_create(&d, device, &h_), "GpuPlan");
+    create(d);
   }
 
+ public:
   // The whole pipeline on the GPU (tree, neighbor lists, skeletons, plan) from
   // the points alone -- the device counterpart of build_tree +
   // build_neighbor_lists + build_skeletons + make_plan (sfmm_gpu_plan_from_points).
@@ -183,7 +209,7 @@ class GpuPlan {
 };
 
 // u = A q, q and u in the original point order (apply.cpp:306-337).  Safe to
-// call concurrently on one plan (the plan serialises its device scratch).
+// call concurrently on one plan: applies on a plan never overlap on the device.
 template <class K>
 std::vector<typename K::scalar> fmm_apply(const GpuPlan<K>& plan,
                                           const std::vector<typename K::scalar>& q,

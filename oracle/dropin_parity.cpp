@@ -7,6 +7,7 @@
 // oracle/_ref/dropin_parity (links the reference objects and libsfmm_gpu.so).
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "sfmm/apply.hpp"
@@ -25,6 +26,8 @@ double rel_l2(const std::vector<T>& u, const std::vector<T>& r) {
   }
   return std::sqrt(num / (den > 0 ? den : 1));
 }
+
+static std::vector<int> g_devices = {0, 0, 0, 0};  // argv[1]: comma-separated ids
 
 template <class K>
 int run(const char* name, const K& kern, Distribution dist, int64_t n, int leaf, double tol) {
@@ -52,6 +55,18 @@ int run(const char* name, const K& kern, Distribution dist, int64_t n, int leaf,
   const bool ok = err <= 1e-12 && stats_ok;
   std::printf("%-28s n=%-7lld depth=%d rel_l2=%.3e stats=%s %s\n", name, (long long)n, tree.depth,
               err, stats_ok ? "same" : "DIFFER", ok ? "OK" : "FAIL");
+  // the same plan sharded over g_devices in this process: exchanges inside
+  // the library (peer copies), result within 1e-12 of the reference
+  ApplyStats s_multi;
+  gpu::GpuPlan<K> gmulti(plan, g_devices);
+  const std::vector<S> u_multi = gpu::fmm_apply(gmulti, q, &s_multi);
+  const double err_multi = rel_l2(u_multi, u_cpu);
+  const bool multi_ok = err_multi <= 1e-12 && s_multi.n_ifo_pairs == s_cpu.n_ifo_pairs &&
+                        s_multi.n_ifs_pairs == s_cpu.n_ifs_pairs &&
+                        s_multi.n_tfo_pairs == s_cpu.n_tfo_pairs &&
+                        s_multi.n_level1_pairs == s_cpu.n_level1_pairs;
+  std::printf("%-28s %zu-rank plan rel_l2 vs CPU %.3e %s\n", name, g_devices.size(), err_multi,
+              multi_ok ? "OK" : "FAIL");
   // the reference's exception contract survives the boundary
   bool threw = false;
   try {
@@ -73,10 +88,18 @@ int run(const char* name, const K& kern, Distribution dist, int64_t n, int leaf,
                        s_pipe.n_level1_pairs == s_cpu.n_level1_pairs;
   std::printf("%-28s GPU pipeline rel_l2 vs CPU %.3e (bar %.0e) %s\n", name, err_pipe, 10 * tol,
               pipe_ok ? "OK" : "FAIL");
-  return ok && threw && pipe_ok ? 0 : 1;
+  return ok && threw && pipe_ok && multi_ok ? 0 : 1;
 }
 
-int main() {
+int main(int argc, char** argv) {
+  if (argc > 1) {
+    g_devices.clear();
+    for (const char* c = argv[1]; *c;) {
+      g_devices.push_back(std::atoi(c));
+      while (*c && *c != ',') ++c;
+      if (*c == ',') ++c;
+    }
+  }
   int fails = 0;
   fails += run("laplace3d cube", Laplace3d{}, Distribution::cube, 20000, 64, 1e-6);
   fails += run("laplace3d sphere tol1e-8", Laplace3d{}, Distribution::sphere, 20000, 40, 1e-8);

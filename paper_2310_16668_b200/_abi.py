@@ -353,6 +353,18 @@ def gpu_lib() -> C.CDLL:
                                               C.c_double, C.c_double, C.c_int, C.c_int, C.c_int,
                                               C.POINTER(vp)]
     lib.sfmm_gpu_plan_from_points.restype = C.c_int
+    lib.sfmm_gpu_plan_create_multi.argtypes = [C.POINTER(PlanDesc), C.c_int, C.POINTER(C.c_int),
+                                               C.POINTER(vp)]
+    lib.sfmm_gpu_plan_create_multi.restype = C.c_int
+    lib.sfmm_gpu_plan_create_multi_skel.argtypes = [C.POINTER(PlanDesc), vp, C.c_int,
+                                                    C.POINTER(C.c_int), C.POINTER(vp)]
+    lib.sfmm_gpu_plan_create_multi_skel.restype = C.c_int
+    lib.sfmm_gpu_nccl_unique_id.argtypes = [vp]
+    lib.sfmm_gpu_nccl_unique_id.restype = C.c_int
+    lib.sfmm_gpu_plan_attach_nccl.argtypes = [vp, vp, C.c_int, C.c_int]
+    lib.sfmm_gpu_plan_attach_nccl.restype = C.c_int
+    lib.sfmm_gpu_set_output.argtypes = [vp, C.c_int]
+    lib.sfmm_gpu_set_output.restype = C.c_int
     _gpu_lib = lib
     return lib
 
@@ -369,7 +381,10 @@ GPU_SYMBOLS = [
     "sfmm_gpu_tree_destroy", "sfmm_gpu_plan_from_points",
     "sfmm_gpu_shard_info2", "sfmm_gpu_apply_mid", "sfmm_gpu_apply_fin",
     "sfmm_gpu_shard_T_runs", "sfmm_gpu_copy_runs", "sfmm_gpu_plan_create_sharded_T",
+    "sfmm_gpu_plan_create_multi", "sfmm_gpu_plan_create_multi_skel", "sfmm_gpu_nccl_unique_id",
+    "sfmm_gpu_plan_attach_nccl", "sfmm_gpu_set_output",
 ]
+SFMM_OUTPUT_FULL, SFMM_OUTPUT_OWNED = 0, 1
 
 
 PROBE_SYMBOLS = ["sfmm_probe_fp64_peak", "sfmm_probe_test_sincos", "sfmm_probe_test_log"]

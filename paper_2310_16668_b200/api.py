@@ -65,13 +65,17 @@ def _raise(rc: int) -> None:
 class GpuPlan:
     """Device-resident apply plan (operators uploaded once, resident in HBM)."""
 
-    def __init__(self, desc, device: int = 0, skeletons=None):
+    def __init__(self, desc, device: int = 0, skeletons=None, devices=None):
         """desc: a PlanDescriptor, or a ctypes PlanDesc (e.g. straight from the
         host precompute, without copying its arrays).  skeletons: a device
         skeleton result handle (host.HostPlan.device_skeletons[0]) whose T is
-        taken device-to-device instead of desc's T (sfmm_gpu_plan_create_skel)."""
+        taken device-to-device instead of desc's T (sfmm_gpu_plan_create_skel).
+        devices: several CUDA devices (may repeat) -> one plan sharded over them
+        in this process, exchanges by peer copies inside the library
+        (sfmm_gpu_plan_create_multi); devices[0] holds q and u."""
         lib = _abi.gpu_lib()
-        self.device = device
+        self.device = device if devices is None else int(devices[0])
+        self.devices = None if devices is None else [int(x) for x in devices]
         self._h = None
         if isinstance(desc, PlanDescriptor):
             st = desc.struct
@@ -80,7 +84,14 @@ class GpuPlan:
         else:
             raise TypeError("GpuPlan: expected a PlanDescriptor or a PlanDesc")
         h = C.c_void_p()
-        if skeletons is not None:
+        if self.devices is not None:
+            ids = (C.c_int * len(self.devices))(*self.devices)
+            if skeletons is not None:
+                _raise(lib.sfmm_gpu_plan_create_multi_skel(C.byref(st), skeletons, len(ids), ids,
+                                                           C.byref(h)))
+            else:
+                _raise(lib.sfmm_gpu_plan_create_multi(C.byref(st), len(ids), ids, C.byref(h)))
+        elif skeletons is not None:
             _raise(lib.sfmm_gpu_plan_create_skel(C.byref(st), skeletons, device, 1, 0, C.byref(h)))
         else:
             _raise(lib.sfmm_gpu_plan_create(C.byref(st), device, C.byref(h)))
@@ -111,10 +122,13 @@ class GpuPlan:
         return self
 
     @classmethod
-    def from_host(cls, hp, device: int | None = None) -> "GpuPlan":
+    def from_host(cls, hp, device: int | None = None, devices=None) -> "GpuPlan":
         """Plan from a host.HostPlan; device-resident skeletons (build_gpu with
-        host_T=False) are used in place, so T never crosses PCIe."""
+        host_T=False) are used in place, so T never crosses PCIe (peer copies
+        for a multi-device plan)."""
         ds = hp.device_skeletons
+        if devices is not None:
+            return cls(hp.desc_struct(), skeletons=None if ds is None else ds[0], devices=devices)
         if ds is not None:
             if device is not None and device != ds[1]:
                 raise ValueError("GpuPlan.from_host: skeletons live on another device")

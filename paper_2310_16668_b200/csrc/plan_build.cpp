@@ -214,8 +214,9 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
                hp.box[b].k == hp.box[b].n;
     const int32_t l1b = hp.level_begin[1], l1e = hp.level_begin[2];
     // Sharding: each rank owns whole subtrees rooted at the cut
-    // level.  Cut 1: level-1 subtrees, assigned longest-first to the least
-    // loaded rank.  Cut 2 (the level-1 split is unbalanced -- clustered
+    // level.  Cut 1: level-1 subtrees as Morton-contiguous ranges (longest-
+    // first to the least loaded rank only when the ranges cannot balance to
+    // within 2 %).  Cut 2 (the level-1 split is unbalanced -- clustered
     // inputs -- or there are more ranks than level-1 boxes): level-2 subtrees
     // (and level-1 leaves) as Morton-contiguous ranges split to minimise the
     // largest estimated cost, or longest-first when a few heavy subtrees make
@@ -254,21 +255,73 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
       double total = 0.0;
       for (int32_t b = l1b; b < l1e; ++b) total += cost[b];
       const double mean = total / n_ranks;
-      // cut 1: LPT over the level-1 subtrees
-      std::vector<int32_t> own1(nb, 0);
-      double max1 = 1e300;
-      if (n1 >= n_ranks) {
-        std::vector<int32_t> ord(n1);
-        std::iota(ord.begin(), ord.end(), l1b);
+      // Morton-contiguous split of `us` (units in Morton order) into n_ranks
+      // ranges with the smallest largest estimated cost (bisection on the
+      // bound, greedy fill); returns that largest cost, 1e300 if infeasible
+      auto contiguous = [&](const std::vector<int32_t>& us, std::vector<int32_t>& own) {
+        const int64_t nu = (int64_t)us.size();
+        if (nu < n_ranks) return 1e300;
+        auto fill = [&](double bound, bool write) {
+          int r = 0;
+          double acc = 0.0;
+          for (int64_t u = 0; u < nu; ++u) {
+            const double w = cost[us[u]];
+            if (acc > 0.0 && acc + w > bound) {
+              ++r;
+              acc = 0.0;
+            }
+            // leave at least one unit for every later rank
+            if (write && acc > 0.0 && nu - u <= n_ranks - 1 - r) {
+              ++r;
+              acc = 0.0;
+            }
+            acc += w;
+            if (write) own[us[u]] = std::min(r, n_ranks - 1);
+          }
+          return r + 1;
+        };
+        double lo = mean, hi = 0.0;
+        for (int32_t u : us) {
+          lo = std::max(lo, cost[u]);
+          hi += cost[u];
+        }
+        for (int it = 0; it < 60 && hi - lo > 1e-9 * hi; ++it) {
+          const double mid = 0.5 * (lo + hi);
+          (fill(mid, false) <= n_ranks ? hi : lo) = mid;
+        }
+        fill(hi, true);
+        std::vector<double> load(n_ranks, 0.0);
+        for (int32_t u : us) load[own[u]] += cost[u];
+        return *std::max_element(load.begin(), load.end());
+      };
+      // longest-processing-time assignment of the same units (a few heavy
+      // units: clusters); returns the largest load
+      auto lpt = [&](const std::vector<int32_t>& us, std::vector<int32_t>& own) {
+        if ((int64_t)us.size() < n_ranks) return 1e300;
+        std::vector<int32_t> ord(us);
         std::stable_sort(ord.begin(), ord.end(),
                          [&](int32_t x, int32_t y) { return cost[x] > cost[y]; });
         std::vector<double> load(n_ranks, 0.0);
-        for (int32_t b : ord) {
+        for (int32_t u : ord) {
           const int r = (int)(std::min_element(load.begin(), load.end()) - load.begin());
-          own1[b] = r;
-          load[r] += cost[b];
+          own[u] = r;
+          load[r] += cost[u];
         }
-        max1 = *std::max_element(load.begin(), load.end());
+        return *std::max_element(load.begin(), load.end());
+      };
+      // cut 1: Morton-contiguous ranges of level-1 subtrees
+      // whenever they balance to within 2 % of the mean (or as well as LPT),
+      // else LPT
+      std::vector<int32_t> l1units(n1);
+      std::iota(l1units.begin(), l1units.end(), l1b);
+      std::vector<int32_t> own1(nb, 0), own1_l(nb, 0);
+      double max1 = contiguous(l1units, own1);
+      {
+        const double maxl = lpt(l1units, own1_l);
+        if (max1 < 1e300 && max1 > 1.02 * mean && maxl < max1) {
+          max1 = maxl;
+          own1.swap(own1_l);
+        }
       }
       // cut 2 units in Morton order: each level-1 box's level-2 children, or
       // the level-1 box itself when it is a leaf
@@ -285,56 +338,15 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
         }
       }
       const int64_t nu = (int64_t)units.size();
-      // smallest feasible largest range (bisection on the bound, greedy fill)
-      auto ranges = [&](double bound, std::vector<int32_t>* own) {
-        int r = 0;
-        double acc = 0.0;
-        for (int64_t u = 0; u < nu; ++u) {
-          const double w = cost[units[u]];
-          if (acc > 0.0 && acc + w > bound) {
-            ++r;
-            acc = 0.0;
-          }
-          // leave at least one unit for every later rank
-          if (own && acc > 0.0 && nu - u <= n_ranks - 1 - r) {
-            ++r;
-            acc = 0.0;
-          }
-          acc += w;
-          if (own) (*own)[units[u]] = std::min(r, n_ranks - 1);
-        }
-        return r + 1;
-      };
-      double max2 = 1e300;
-      std::vector<int32_t> own2(nb, 0);
-      if (nu >= n_ranks) {
-        double lo = 0.0, hi = total;
-        for (int64_t u = 0; u < nu; ++u) lo = std::max(lo, cost[units[u]]);
-        lo = std::max(lo, mean);
-        for (int it = 0; it < 60 && hi - lo > 1e-9 * hi; ++it) {
-          const double mid = 0.5 * (lo + hi);
-          (ranges(mid, nullptr) <= n_ranks ? hi : lo) = mid;
-        }
-        ranges(hi, &own2);
-        std::vector<double> load(n_ranks, 0.0);
-        for (int32_t u : units) load[own2[u]] += cost[u];
-        max2 = *std::max_element(load.begin(), load.end());
-        // LPT over the same units when the contiguous ranges cannot balance
-        // (a few heavy units: clusters); the ghosts stay a small exchange
-        std::vector<int32_t> ord(units);
-        std::stable_sort(ord.begin(), ord.end(),
-                         [&](int32_t x, int32_t y) { return cost[x] > cost[y]; });
-        std::vector<double> ll(n_ranks, 0.0);
-        std::vector<int32_t> own_l(nb, 0);
-        for (int32_t u : ord) {
-          const int r = (int)(std::min_element(ll.begin(), ll.end()) - ll.begin());
-          own_l[u] = r;
-          ll[r] += cost[u];
-        }
-        const double maxl = *std::max_element(ll.begin(), ll.end());
+      std::vector<int32_t> own2(nb, 0), own2_l(nb, 0);
+      double max2 = contiguous(units, own2);
+      if (max2 < 1e300) {
+        // LPT over the same units when the contiguous ranges cannot balance;
+        // the ghosts stay a small exchange
+        const double maxl = lpt(units, own2_l);
         if (maxl < 0.97 * max2) {
           max2 = maxl;
-          own2.swap(own_l);
+          own2.swap(own2_l);
         }
       }
       if (max1 >= 1e300 && max2 >= 1e300)

@@ -7,23 +7,8 @@
 //   K4 scatter;   depth < 2 -> K5 dense fallback.
 // The plan (geometry, index maps, interpolation operators, translation CSR,
 // task list) is uploaded once by sfmm_gpu_plan_create and stays resident.
-#include <cuda_runtime.h>
-
-#include <algorithm>
-#include <cstdio>
-#include <cstdlib>
-#include <cstring>
-#include <mutex>
-#include <new>
-#include <string>
-#include <vector>
-
 #include "fastmath.cuh"
-#include "launch.h"
-#include "plan_build.h"
-#include "sfmm_gpu.h"
-
-using namespace sfmm_gpu;
+#include "plan.h"
 
 namespace {
 thread_local std::string g_last_error;
@@ -36,283 +21,6 @@ int set_last_error(int code, const std::string& msg) {
 }
 }  // namespace sfmm_gpu
 
-namespace {
-
-int set_error(int code, const std::string& msg) { return sfmm_gpu::set_last_error(code, msg); }
-
-struct CudaFail {
-  int code;
-  std::string msg;
-};
-
-void ck(cudaError_t e, const char* what) {
-  if (e == cudaSuccess) return;
-  (void)cudaGetLastError();  // reported here; do not leak into the next call
-  const int code = e == cudaErrorMemoryAllocation ? SFMM_ENOMEM : SFMM_ECUDA;
-  throw CudaFail{code, std::string(what) + ": " + cudaGetErrorString(e)};
-}
-
-// Scratch device buffers freed at scope exit.
-struct TmpDev {
-  std::vector<void*> ptrs;
-  TmpDev() = default;
-  TmpDev(const TmpDev&) = delete;
-  TmpDev& operator=(const TmpDev&) = delete;
-  ~TmpDev() {
-    for (void* p : ptrs) cudaFree(p);
-  }
-  template <class T>
-  const T* up(const T* src, size_t count) {
-    void* p = nullptr;
-    ck(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)), "cudaMalloc");
-    ptrs.push_back(p);
-    if (count) ck(cudaMemcpy(p, src, count * sizeof(T), cudaMemcpyHostToDevice), "upload");
-    return static_cast<const T*>(p);
-  }
-};
-
-// Makes `device` current for the scope of one ABI call and restores the
-// caller's device afterwards; clears stale (non-sticky) errors on entry.
-struct DeviceGuard {
-  int prev = -1;
-  explicit DeviceGuard(int device) {
-    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
-    ck(cudaSetDevice(device), "cudaSetDevice");
-    (void)cudaGetLastError();
-  }
-  DeviceGuard(const DeviceGuard&) = delete;
-  DeviceGuard& operator=(const DeviceGuard&) = delete;
-  ~DeviceGuard() {
-    if (prev >= 0) cudaSetDevice(prev);
-  }
-};
-
-}  // namespace
-
-struct sfmm_gpu_plan {
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_k2a = nullptr, ev_k2b = nullptr;
-  // End of the last apply enqueued on this plan (any stream).  Every apply
-  // waits on it before touching the plan's shared device state (Q/U/QH/UH,
-  // the column-sum staging, the task counter), so applies issued on different
-  // streams -- or a sync apply on the plan stream after an async one on a
-  // caller stream -- run one after another instead of racing.
-  cudaEvent_t ev_done = nullptr;
-  HostPlan hp;
-  DevPlan dp{};
-  std::vector<void*> allocs;
-  int64_t device_bytes = 0;
-  // per-apply state (grown on demand, one column of scalars)
-  DevState ds{};
-  double* io_q = nullptr;
-  double* io_u = nullptr;
-  size_t io_cap = 0;  // bytes of io_q / io_u
-  std::mutex mu;
-
-  template <class T>
-  T* alloc(size_t count) {
-    void* p = nullptr;
-    const size_t bytes = std::max<size_t>(count * sizeof(T), 16);
-    ck(cudaMalloc(&p, bytes), "cudaMalloc");
-    allocs.push_back(p);
-    device_bytes += (int64_t)bytes;
-    return static_cast<T*>(p);
-  }
-  template <class T>
-  T* upload(const T* src, size_t count) {
-    T* d = alloc<T>(count);
-    if (count) ck(cudaMemcpy(d, src, count * sizeof(T), cudaMemcpyHostToDevice), "upload");
-    return d;
-  }
-  template <class T>
-  T* upload(const std::vector<T>& v) {
-    return upload(v.data(), v.size());
-  }
-
-  ~sfmm_gpu_plan() {
-    int prev = -1;
-    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
-    cudaSetDevice(device);
-    if (stream) cudaStreamSynchronize(stream);
-    for (void* p : allocs) cudaFree(p);
-    if (io_q) cudaFree(io_q);
-    if (io_u) cudaFree(io_u);
-    if (ev_a) cudaEventDestroy(ev_a);
-    if (ev_b) cudaEventDestroy(ev_b);
-    if (ev_k2a) cudaEventDestroy(ev_k2a);
-    if (ev_k2b) cudaEventDestroy(ev_k2b);
-    if (ev_done) cudaEventDestroy(ev_done);
-    for (cudaEvent_t e : tev) cudaEventDestroy(e);
-    if (graph_exec) cudaGraphExecDestroy(graph_exec);
-    for (PhaseGraph& g : phase_graph)
-      if (g.exec) cudaGraphExecDestroy(g.exec);
-    if (stream) cudaStreamDestroy(stream);
-    (void)cudaGetLastError();
-    if (prev >= 0) cudaSetDevice(prev);  // leave the caller's current device as it was
-  }
-
-  void ensure_io(size_t bytes) {
-    if (bytes <= io_cap) return;
-    if (io_q) cudaFree(io_q);
-    if (io_u) cudaFree(io_u);
-    io_q = io_u = nullptr;
-    io_cap = 0;
-    ck(cudaMalloc(&io_q, bytes), "cudaMalloc(q)");
-    ck(cudaMalloc(&io_u, bytes), "cudaMalloc(u)");
-    io_cap = bytes;
-  }
-
-  // CUDA graph of the last (q, u, nrhs) enqueued through sfmm_gpu_apply_async
-  cudaGraphExec_t graph_exec = nullptr;
-  const double* graph_q = nullptr;
-  double* graph_u = nullptr;
-  int graph_nrhs = 0;
-
-  // Sharded applies: one CUDA graph per phase (begin, mid, fin), keyed on the
-  // caller's buffers; a sequence of ~10-30 small launches per phase otherwise
-  // leaves the device idle between them on deep trees.
-  struct PhaseGraph {
-    cudaGraphExec_t exec = nullptr;
-    const void* key[3] = {nullptr, nullptr, nullptr};
-  };
-  PhaseGraph phase_graph[3];
-
-  template <class F>
-  void run_phase(int which, const void* k0, const void* k1, const void* k2, void* user_stream,
-                 cudaStream_t st, F&& enqueue) {
-    static const bool env_graphs = [] {
-      const char* v = std::getenv("SFMM_GRAPHS");
-      return !(v && std::atoi(v) == 0);
-    }();
-    if (!env_graphs || timing || user_stream == nullptr || hp.depth < 2) {
-      enqueue();
-      return;
-    }
-    PhaseGraph& g = phase_graph[which];
-    if (!g.exec || g.key[0] != k0 || g.key[1] != k1 || g.key[2] != k2) {
-      if (g.exec) cudaGraphExecDestroy(g.exec);
-      g.exec = nullptr;
-      cudaGraph_t graph = nullptr;
-      ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
-      try {
-        enqueue();
-      } catch (...) {
-        cudaStreamEndCapture(st, &graph);  // leave the caller's stream usable
-        if (graph) cudaGraphDestroy(graph);
-        throw;
-      }
-      ck(cudaStreamEndCapture(st, &graph), "end capture");
-      ck(cudaGraphInstantiate(&g.exec, graph, 0), "graph instantiate");
-      cudaGraphDestroy(graph);
-      g.key[0] = k0;
-      g.key[1] = k1;
-      g.key[2] = k2;
-    }
-    ck(cudaGraphLaunch(g.exec, st), "graph launch");
-  }
-
-  // Phase timing: 6 events per recorded apply (phase boundaries).
-  static constexpr int kMaxTimed = 256;
-  bool timing = false;
-  std::vector<cudaEvent_t> tev;
-  int n_timed = 0;
-
-  void mark(int slot, int k, cudaStream_t st) {
-    ck(cudaEventRecord(tev[(size_t)slot * 6 + k], st), "event");
-  }
-
-  // Enqueues one right-hand side: q, u device pointers in original order.
-  void enqueue_one(const double* q, double* u, cudaStream_t st, bool time_k2) {
-    if (hp.depth < 2) {
-      launch_direct_fallback(dp, q, u, st);
-      return;
-    }
-    const int slot = (timing && n_timed < kMaxTimed) ? n_timed++ : -1;
-    if (slot >= 0) mark(slot, 0, st);
-    launch_gather(dp, q, ds, st);
-    if (slot >= 0) mark(slot, 1, st);
-    for (int l = hp.depth; l >= 2; --l) launch_upward(dp, hp, l, ds, st);
-    if (slot >= 0) mark(slot, 2, st);
-    if (time_k2) ck(cudaEventRecord(ev_k2a, st), "event");
-    launch_translate(dp, ds, st);
-    if (time_k2) ck(cudaEventRecord(ev_k2b, st), "event");
-    if (slot >= 0) mark(slot, 3, st);
-    for (int l = 2; l <= hp.depth; ++l) launch_downward(dp, hp, l, ds, st);
-    if (slot >= 0) mark(slot, 4, st);
-    launch_scatter(dp, ds, u, st);
-    if (slot >= 0) mark(slot, 5, st);
-  }
-
-  // Multi-RHS state (kNRHS columns per pass), allocated on first use.
-  DevState dsm{};
-  bool multi_ok = true;
-
-  void ensure_multi() {
-    if (dsm.Q) return;
-    const int sw = hp.cplx ? 2 : 1;
-    dsm.Q = alloc<double>((size_t)hp.n_slots * kNRHS * sw);
-    dsm.U = alloc<double>((size_t)hp.n_slots * kNRHS * sw);
-    dsm.QH = alloc<double>((size_t)std::max<int64_t>(hp.n_skel, 1) * kNRHS * sw);
-    dsm.UH = alloc<double>((size_t)std::max<int64_t>(hp.n_skel, 1) * kNRHS * sw);
-  }
-
-  // nrhs columns (column-major, original order).  More than one column goes
-  // through the DMMA multi-RHS passes kNRHS at a time (SFMM_MULTI=0: column
-  // loop, for A/B measurements).
-  void enqueue_cols(const double* q, double* u, int nrhs, cudaStream_t st, bool time_k2) {
-    const size_t col_d = (size_t)hp.n_points * (hp.cplx ? 2 : 1);  // doubles per column
-    static const bool env_multi = [] {
-      const char* v = std::getenv("SFMM_MULTI");
-      return !(v && std::atoi(v) == 0);
-    }();
-    if (nrhs == 1 || hp.depth < 2 || !env_multi) {
-      for (int r = 0; r < nrhs; ++r) enqueue_one(q + r * col_d, u + r * col_d, st, time_k2 && r == 0);
-      return;
-    }
-    ensure_multi();
-    for (int c0 = 0; c0 < nrhs; c0 += kNRHS) {
-      const int nc = std::min(kNRHS, nrhs - c0);
-      // phase timing records the first 16-column pass of each apply
-      const int slot = (c0 == 0 && timing && n_timed < kMaxTimed) ? n_timed++ : -1;
-      if (slot >= 0) mark(slot, 0, st);
-      launch_gather_m(dp, q + c0 * col_d, nc, dsm, st);
-      if (slot >= 0) mark(slot, 1, st);
-      for (int l = hp.depth; l >= 2; --l) launch_upward_m(dp, hp, l, dsm, st);
-      if (slot >= 0) mark(slot, 2, st);
-      if (time_k2 && c0 == 0) ck(cudaEventRecord(ev_k2a, st), "event");
-      launch_translate_m(dp, dsm, st);
-      if (time_k2 && c0 == 0) ck(cudaEventRecord(ev_k2b, st), "event");
-      if (slot >= 0) mark(slot, 3, st);
-      for (int l = 2; l <= hp.depth; ++l) launch_downward_m(dp, hp, l, dsm, st);
-      if (slot >= 0) mark(slot, 4, st);
-      launch_scatter_m(dp, dsm, u + c0 * col_d, nc, st);
-      if (slot >= 0) mark(slot, 5, st);
-    }
-  }
-
-  int launches_per_apply() const {
-    if (hp.depth < 2) return 1;
-    int n = 3;  // gather, translate, scatter
-    for (int l = 2; l <= hp.depth; ++l) {
-      n += hp.up1_lvl[l + 1] > hp.up1_lvl[l] ? 1 : 0;
-      n += hp.down_lvl[l + 1] > hp.down_lvl[l] ? 1 : 0;
-      n += hp.copy_lvl[l + 1] > hp.copy_lvl[l] ? 2 : 0;  // k1_copy + k3_copy
-    }
-    if (dp.n_tasks == 0) --n;
-    if (dp.n_recv > 0) ++n;  // k2b_reduce
-    // sharded plans: ghost pack / unpack, column-sum pack
-    n += (dp.n_pack > 0 ? 1 : 0) + (dp.n_unpack > 0 ? 1 : 0) + (dp.n_xpairs > 0 ? 1 : 0);
-    if (dp.n_interior > 0 && dp.n_interior < dp.n_tasks) ++n;  // SFMM_SHARD_OVERLAP split
-    return n;
-  }
-
-  size_t scalar_bytes() const { return hp.cplx ? 16 : 8; }
-
-  // Orders this apply after the previous one on the plan (see ev_done).
-  void wait_previous(cudaStream_t st) { ck(cudaStreamWaitEvent(st, ev_done, 0), "wait previous apply"); }
-  void mark_done(cudaStream_t st) { ck(cudaEventRecord(ev_done, st), "event"); }
-};
 
 extern "C" {
 
@@ -322,12 +30,12 @@ const char* sfmm_gpu_version(void) { return "sfmm_gpu 0.1 (sm_100a, FP64)"; }
 
 }  // extern "C"
 
-namespace {
+namespace sfmm_gpu {
 
 // T_dev: the descriptor's operators in device memory (global T_off layout), or
 // with T_compact only the owned runs concatenated (sfmm_gpu_shard_T_runs order)
 int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
-                sfmm_gpu_plan** out, const double* T_dev = nullptr, bool T_compact = false) {
+                sfmm_gpu_plan** out, const double* T_dev, bool T_compact) {
   if (!desc || !out) return set_error(SFMM_EINVAL, "sfmm_gpu_plan_create: null argument");
   *out = nullptr;
   sfmm_gpu_plan* p = nullptr;
@@ -432,14 +140,24 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
       // interpolation operators of the owned boxes, copied run by run
       dp.T = p->alloc<double>((size_t)hp.T_off[hp.n_boxes] * sw);
       // device operators may still be in flight on another stream (a pack on
-      // the legacy stream, an NCCL receive): the plan's stream is non-blocking
-      if (T_dev) ck(cudaDeviceSynchronize(), "wait for T");
+      // the legacy stream, an NCCL receive): the plan's stream is non-blocking.
+      // They may live on another device (sfmm_gpu_plan_create_multi_skel):
+      // the copies below are then peer copies (cudaMemcpyDefault, UVA).
+      if (T_dev) {
+        cudaPointerAttributes attr{};
+        if (cudaPointerGetAttributes(&attr, T_dev) == cudaSuccess && attr.device >= 0 &&
+            attr.device != device) {
+          DeviceGuard g2(attr.device);
+          ck(cudaDeviceSynchronize(), "wait for T");
+        }
+        ck(cudaDeviceSynchronize(), "wait for T");
+      }
       const double* T_src = T_dev ? T_dev : desc->T;
       if (!T_src && !hp.T_runs.empty()) throw CudaFail{SFMM_EINVAL, "descriptor has no T"};
       for (const HostPlan::Run& r : hp.T_runs)
         ck(cudaMemcpyAsync(dp.T + r.dst * sw, T_src + (T_compact ? r.dst : r.src) * sw,
                            sizeof(double) * r.len * sw,
-                           T_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, p->stream),
+                           T_dev ? cudaMemcpyDefault : cudaMemcpyHostToDevice, p->stream),
            "upload T");
       ck(cudaStreamSynchronize(p->stream), "upload T");
       dp.up_items = p->upload(hp.up_items);
@@ -514,7 +232,96 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
   }
 }
 
+}  // namespace sfmm_gpu
+
+namespace sfmm_gpu {
+namespace {
+
+// apply_end = mid + fin; the second exchange in between exists only for
+// cross-symmetric sharded plans
+void apply_mid_impl(sfmm_gpu_plan* p, const void* recv_dev, void* send2_dev, cudaStream_t st) {
+  if (p->hp.depth < 2) return;
+  if (p->dp.n_unpack > 0) {
+    if (!recv_dev) throw CudaFail{SFMM_EINVAL, "receive buffer required"};
+    launch_unpack(p->dp, p->ds, static_cast<const double*>(recv_dev), st);
+  }
+  launch_translate(p->dp, p->ds, st, kBoundaryTasks, false);
+  if (p->dp.n_xpairs > 0) {
+    if (!send2_dev) throw CudaFail{SFMM_EINVAL, "second send buffer required"};
+    launch_xpack(p->dp, static_cast<double*>(send2_dev), st);
+  }
+}
+
+void apply_fin_impl(sfmm_gpu_plan* p, const void* q_dev, const void* recv2_dev, void* u_dev,
+                    cudaStream_t st) {
+  double* u = static_cast<double*>(u_dev);
+  if (p->hp.depth < 2) {
+    if (p->hp.rank == 0) launch_direct_fallback(p->dp, static_cast<const double*>(q_dev), u, st);
+    return;
+  }
+  if (p->dp.n_recv2 > 0) {
+    if (!recv2_dev) throw CudaFail{SFMM_EINVAL, "second receive buffer required"};
+    const size_t sw = p->dp.cplx ? 2 : 1;
+    ck(cudaMemcpyAsync(p->dp.stage + p->dp.stage_size * sw, recv2_dev,
+                       sizeof(double) * p->dp.n_recv2 * sw, cudaMemcpyDeviceToDevice, st),
+       "second exchange");
+  }
+  launch_stage_reduce(p->dp, p->ds, st);
+  for (int l = 2; l <= p->hp.depth; ++l) launch_downward(p->dp, p->hp, l, p->ds, st);
+  launch_scatter(p->dp, p->ds, u, st);
+}
+
 }  // namespace
+
+// Phases of one sharded apply, shared by the C ABI's
+// begin/mid/fin/end entry points and the in-library exchanges (sfmm_multi.cu).
+// user_stream != NULL replays each phase as a CUDA graph keyed on its buffers.
+void phase_begin(sfmm_gpu_plan* p, const void* q_dev, void* send_dev, void* user_stream,
+                 cudaStream_t st, cudaEvent_t packed) {
+  const double* q = static_cast<const double*>(q_dev);
+  if (p->hp.depth >= 2 && p->dp.n_pack > 0 && !send_dev)
+    throw CudaFail{SFMM_EINVAL, "send buffer required"};
+  p->run_phase(0, q_dev, send_dev, nullptr, user_stream, st, [&] {
+    if (p->hp.depth < 2) return;
+    launch_gather(p->dp, q, p->ds, st);
+    for (int l = p->hp.depth; l >= 2; --l) launch_upward(p->dp, p->hp, l, p->ds, st);
+    if (p->dp.n_pack > 0) launch_pack(p->dp, p->ds, static_cast<double*>(send_dev), st);
+  });
+  if (packed) ck(cudaEventRecord(packed, st), "event");
+  // zeroes U / UH (and, with SFMM_SHARD_OVERLAP=1, runs the interior tasks)
+  if (p->hp.depth >= 2) launch_translate(p->dp, p->ds, st, kInteriorTasks);
+}
+
+void phase_mid(sfmm_gpu_plan* p, const void* recv_dev, void* send2_dev, void* user_stream,
+               cudaStream_t st, cudaEvent_t packed) {
+  if (p->hp.depth >= 2 && p->dp.n_unpack > 0 && !recv_dev)
+    throw CudaFail{SFMM_EINVAL, "receive buffer required"};
+  if (p->hp.depth >= 2 && p->dp.n_xpairs > 0 && !send2_dev)
+    throw CudaFail{SFMM_EINVAL, "second send buffer required"};
+  p->run_phase(1, recv_dev, send2_dev, nullptr, user_stream, st,
+               [&] { apply_mid_impl(p, recv_dev, send2_dev, st); });
+  if (packed) ck(cudaEventRecord(packed, st), "event");
+}
+
+void phase_fin(sfmm_gpu_plan* p, const void* q_dev, const void* recv2_dev, void* u_dev,
+               void* user_stream, cudaStream_t st) {
+  if (p->hp.depth >= 2 && p->dp.n_recv2 > 0 && !recv2_dev)
+    throw CudaFail{SFMM_EINVAL, "second receive buffer required"};
+  p->run_phase(2, q_dev, recv2_dev, u_dev, user_stream, st,
+               [&] { apply_fin_impl(p, q_dev, recv2_dev, u_dev, st); });
+}
+
+void phase_end(sfmm_gpu_plan* p, const void* q_dev, const void* recv_dev, void* u_dev,
+               void* user_stream, cudaStream_t st) {
+  if (p->hp.depth >= 2 && p->dp.n_unpack > 0 && !recv_dev)
+    throw CudaFail{SFMM_EINVAL, "receive buffer required"};
+  p->run_phase(1, recv_dev, q_dev, u_dev, user_stream, st, [&] {
+    apply_mid_impl(p, recv_dev, nullptr, st);
+    apply_fin_impl(p, q_dev, nullptr, u_dev, st);
+  });
+}
+
+}  // namespace sfmm_gpu
 
 extern "C" {
 
@@ -646,23 +453,14 @@ int sfmm_gpu_shard_describe(const sfmm_plan_desc* desc, int n_ranks, int rank, i
 int sfmm_gpu_apply_begin(sfmm_gpu_plan* p, const void* q_dev, void* send_dev, void* stream,
                          void* packed_event) {
   if (!p || !q_dev) return set_error(SFMM_EINVAL, "fmm_apply: bad arguments");
+  if (p->multi || p->nccl)
+    return set_error(SFMM_EINVAL, "fmm_apply: the plan runs its own exchange: use sfmm_gpu_apply");
   std::lock_guard<std::mutex> lock(p->mu);
   try {
     DeviceGuard device_guard(p->device);
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : p->stream;
-    const double* q = static_cast<const double*>(q_dev);
-    if (p->hp.depth >= 2 && p->dp.n_pack > 0 && !send_dev)
-      throw CudaFail{SFMM_EINVAL, "send buffer required"};
     p->wait_previous(st);
-    p->run_phase(0, q_dev, send_dev, nullptr, stream, st, [&] {
-      if (p->hp.depth < 2) return;
-      launch_gather(p->dp, q, p->ds, st);
-      for (int l = p->hp.depth; l >= 2; --l) launch_upward(p->dp, p->hp, l, p->ds, st);
-      if (p->dp.n_pack > 0) launch_pack(p->dp, p->ds, static_cast<double*>(send_dev), st);
-    });
-    if (packed_event) ck(cudaEventRecord(static_cast<cudaEvent_t>(packed_event), st), "event");
-    // zeroes U / UH (and, with SFMM_SHARD_OVERLAP=1, runs the interior tasks)
-    if (p->hp.depth >= 2) launch_translate(p->dp, p->ds, st, kInteriorTasks);
+    phase_begin(p, q_dev, send_dev, stream, st, static_cast<cudaEvent_t>(packed_event));
     ck(cudaGetLastError(), "kernel launch");
     return SFMM_OK;
   } catch (const CudaFail& f) {
@@ -670,47 +468,11 @@ int sfmm_gpu_apply_begin(sfmm_gpu_plan* p, const void* q_dev, void* send_dev, vo
   }
 }
 
-namespace {
-
-// apply_end = mid + fin; the second exchange in between exists only for
-// cross-symmetric sharded plans
-void apply_mid_impl(sfmm_gpu_plan* p, const void* recv_dev, void* send2_dev, cudaStream_t st) {
-  if (p->hp.depth < 2) return;
-  if (p->dp.n_unpack > 0) {
-    if (!recv_dev) throw CudaFail{SFMM_EINVAL, "receive buffer required"};
-    launch_unpack(p->dp, p->ds, static_cast<const double*>(recv_dev), st);
-  }
-  launch_translate(p->dp, p->ds, st, kBoundaryTasks, false);
-  if (p->dp.n_xpairs > 0) {
-    if (!send2_dev) throw CudaFail{SFMM_EINVAL, "second send buffer required"};
-    launch_xpack(p->dp, static_cast<double*>(send2_dev), st);
-  }
-}
-
-void apply_fin_impl(sfmm_gpu_plan* p, const void* q_dev, const void* recv2_dev, void* u_dev,
-                    cudaStream_t st) {
-  double* u = static_cast<double*>(u_dev);
-  if (p->hp.depth < 2) {
-    if (p->hp.rank == 0) launch_direct_fallback(p->dp, static_cast<const double*>(q_dev), u, st);
-    return;
-  }
-  if (p->dp.n_recv2 > 0) {
-    if (!recv2_dev) throw CudaFail{SFMM_EINVAL, "second receive buffer required"};
-    const size_t sw = p->dp.cplx ? 2 : 1;
-    ck(cudaMemcpyAsync(p->dp.stage + p->dp.stage_size * sw, recv2_dev,
-                       sizeof(double) * p->dp.n_recv2 * sw, cudaMemcpyDeviceToDevice, st),
-       "second exchange");
-  }
-  launch_stage_reduce(p->dp, p->ds, st);
-  for (int l = 2; l <= p->hp.depth; ++l) launch_downward(p->dp, p->hp, l, p->ds, st);
-  launch_scatter(p->dp, p->ds, u, st);
-}
-
-}  // namespace
-
 int sfmm_gpu_apply_end(sfmm_gpu_plan* p, const void* q_dev, const void* recv_dev, void* u_dev,
                        void* stream) {
   if (!p || !u_dev) return set_error(SFMM_EINVAL, "fmm_apply: bad arguments");
+  if (p->multi || p->nccl)
+    return set_error(SFMM_EINVAL, "fmm_apply: the plan runs its own exchange: use sfmm_gpu_apply");
   if (p->dp.n_xpairs > 0 || p->dp.n_recv2 > 0)
     return set_error(SFMM_EINVAL,
                      "fmm_apply: plan has a second exchange: use sfmm_gpu_apply_mid/_fin");
@@ -718,12 +480,7 @@ int sfmm_gpu_apply_end(sfmm_gpu_plan* p, const void* q_dev, const void* recv_dev
   try {
     DeviceGuard device_guard(p->device);
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : p->stream;
-    if (p->hp.depth >= 2 && p->dp.n_unpack > 0 && !recv_dev)
-      throw CudaFail{SFMM_EINVAL, "receive buffer required"};
-    p->run_phase(1, recv_dev, q_dev, u_dev, stream, st, [&] {
-      apply_mid_impl(p, recv_dev, nullptr, st);
-      apply_fin_impl(p, q_dev, nullptr, u_dev, st);
-    });
+    phase_end(p, q_dev, recv_dev, u_dev, stream, st);
     p->mark_done(st);
     ck(cudaGetLastError(), "kernel launch");
     return SFMM_OK;
@@ -735,17 +492,13 @@ int sfmm_gpu_apply_end(sfmm_gpu_plan* p, const void* q_dev, const void* recv_dev
 int sfmm_gpu_apply_mid(sfmm_gpu_plan* p, const void* recv_dev, void* send2_dev, void* stream,
                        void* packed_event) {
   if (!p) return set_error(SFMM_EINVAL, "fmm_apply: bad arguments");
+  if (p->multi || p->nccl)
+    return set_error(SFMM_EINVAL, "fmm_apply: the plan runs its own exchange: use sfmm_gpu_apply");
   std::lock_guard<std::mutex> lock(p->mu);
   try {
     DeviceGuard device_guard(p->device);
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : p->stream;
-    if (p->hp.depth >= 2 && p->dp.n_unpack > 0 && !recv_dev)
-      throw CudaFail{SFMM_EINVAL, "receive buffer required"};
-    if (p->hp.depth >= 2 && p->dp.n_xpairs > 0 && !send2_dev)
-      throw CudaFail{SFMM_EINVAL, "second send buffer required"};
-    p->run_phase(1, recv_dev, send2_dev, nullptr, stream, st,
-                 [&] { apply_mid_impl(p, recv_dev, send2_dev, st); });
-    if (packed_event) ck(cudaEventRecord(static_cast<cudaEvent_t>(packed_event), st), "event");
+    phase_mid(p, recv_dev, send2_dev, stream, st, static_cast<cudaEvent_t>(packed_event));
     ck(cudaGetLastError(), "kernel launch");
     return SFMM_OK;
   } catch (const CudaFail& f) {
@@ -756,14 +509,13 @@ int sfmm_gpu_apply_mid(sfmm_gpu_plan* p, const void* recv_dev, void* send2_dev, 
 int sfmm_gpu_apply_fin(sfmm_gpu_plan* p, const void* q_dev, const void* recv2_dev, void* u_dev,
                        void* stream) {
   if (!p || !u_dev) return set_error(SFMM_EINVAL, "fmm_apply: bad arguments");
+  if (p->multi || p->nccl)
+    return set_error(SFMM_EINVAL, "fmm_apply: the plan runs its own exchange: use sfmm_gpu_apply");
   std::lock_guard<std::mutex> lock(p->mu);
   try {
     DeviceGuard device_guard(p->device);
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : p->stream;
-    if (p->hp.depth >= 2 && p->dp.n_recv2 > 0 && !recv2_dev)
-      throw CudaFail{SFMM_EINVAL, "second receive buffer required"};
-    p->run_phase(2, q_dev, recv2_dev, u_dev, stream, st,
-                 [&] { apply_fin_impl(p, q_dev, recv2_dev, u_dev, st); });
+    phase_fin(p, q_dev, recv2_dev, u_dev, stream, st);
     p->mark_done(st);
     ck(cudaGetLastError(), "kernel launch");
     return SFMM_OK;
@@ -789,8 +541,9 @@ int sfmm_gpu_apply(sfmm_gpu_plan* p, const void* q, void* u, int nrhs, int flags
                    sfmm_gpu_stats* stats) {
   if (!p || (!q && p->hp.n_points) || (!u && p->hp.n_points) || nrhs < 1)
     return set_error(SFMM_EINVAL, "fmm_apply: bad arguments");
-  if (p->hp.n_ranks > 1)
-    return set_error(SFMM_EINVAL, "fmm_apply: sharded plan: use sfmm_gpu_apply_begin/_end");
+  if (p->hp.n_ranks > 1 && !p->multi && !p->nccl)
+    return set_error(SFMM_EINVAL, "fmm_apply: sharded plan without an exchange: use "
+                                  "sfmm_gpu_apply_begin/_end or sfmm_gpu_plan_attach_nccl");
   std::lock_guard<std::mutex> lock(p->mu);
   try {
     DeviceGuard device_guard(p->device);
@@ -813,14 +566,13 @@ int sfmm_gpu_apply(sfmm_gpu_plan* p, const void* q, void* u, int nrhs, int flags
       qd = p->io_q;
       ud = p->io_u;
     }
-    p->enqueue_cols(qd, ud, nrhs, st, true);
+    p->enqueue_any(qd, ud, nrhs, st, true);
     ck(cudaGetLastError(), "kernel launch");
     if (host) ck(cudaMemcpyAsync(u, p->io_u, col * nrhs, cudaMemcpyDeviceToHost, st), "D2H u");
     ck(cudaEventRecord(p->ev_b, st), "event");
     p->mark_done(st);
     ck(cudaStreamSynchronize(st), "apply");
-    int flag = 0;
-    ck(cudaMemcpy(&flag, p->dp.err_flag, sizeof(int), cudaMemcpyDeviceToHost), "flag");
+    const int flag = multi_take_error_flag(p);
     if (stats) {
       stats->n_ifo_pairs = p->hp.n_ifo;
       stats->n_ifs_pairs = p->hp.n_ifs;
@@ -832,12 +584,10 @@ int sfmm_gpu_apply(sfmm_gpu_plan* p, const void* q, void* u, int nrhs, int flags
       }
       cudaEventElapsedTime(&stats->ms_total, p->ev_a, p->ev_b);
       stats->ms_translate = 0;
-      if (p->hp.depth >= 2) cudaEventElapsedTime(&stats->ms_translate, p->ev_k2a, p->ev_k2b);
+      if (p->hp.depth >= 2 && !p->multi && !p->nccl)
+        cudaEventElapsedTime(&stats->ms_translate, p->ev_k2a, p->ev_k2b);
     }
-    if (flag) {
-      ck(cudaMemset(p->dp.err_flag, 0, sizeof(int)), "memset");
-      return set_error(SFMM_EDUPLICATE, "fmm_apply: coincident points with distinct indices");
-    }
+    if (flag) return set_error(SFMM_EDUPLICATE, "fmm_apply: coincident points with distinct indices");
     return SFMM_OK;
   } catch (const CudaFail& f) {
     return set_error(f.code, "fmm_apply: " + f.msg);
@@ -847,8 +597,9 @@ int sfmm_gpu_apply(sfmm_gpu_plan* p, const void* q, void* u, int nrhs, int flags
 int sfmm_gpu_apply_async(sfmm_gpu_plan* p, const void* q_dev, void* u_dev, int nrhs,
                          void* stream) {
   if (!p || nrhs < 1) return set_error(SFMM_EINVAL, "fmm_apply: bad arguments");
-  if (p->hp.n_ranks > 1)
-    return set_error(SFMM_EINVAL, "fmm_apply: sharded plan: use sfmm_gpu_apply_begin/_end");
+  if (p->hp.n_ranks > 1 && !p->multi && !p->nccl)
+    return set_error(SFMM_EINVAL, "fmm_apply: sharded plan without an exchange: use "
+                                  "sfmm_gpu_apply_begin/_end or sfmm_gpu_plan_attach_nccl");
   std::lock_guard<std::mutex> lock(p->mu);
   try {
     DeviceGuard device_guard(p->device);
@@ -862,7 +613,7 @@ int sfmm_gpu_apply_async(sfmm_gpu_plan* p, const void* q_dev, void* u_dev, int n
       const char* v = std::getenv("SFMM_GRAPHS");
       return !(v && std::atoi(v) == 0);
     }();
-    if (env_graphs && !p->timing && stream != nullptr) {
+    if (env_graphs && !p->timing && stream != nullptr && !p->multi && !p->nccl) {
       if (!p->graph_exec || p->graph_q != qd || p->graph_u != ud || p->graph_nrhs != nrhs) {
         if (p->graph_exec) cudaGraphExecDestroy(p->graph_exec);
         p->graph_exec = nullptr;
@@ -886,7 +637,7 @@ int sfmm_gpu_apply_async(sfmm_gpu_plan* p, const void* q_dev, void* u_dev, int n
       }
       ck(cudaGraphLaunch(p->graph_exec, st), "graph launch");
     } else {
-      p->enqueue_cols(qd, ud, nrhs, st, false);
+      p->enqueue_any(qd, ud, nrhs, st, false);
     }
     p->mark_done(st);
     ck(cudaGetLastError(), "kernel launch");
@@ -901,13 +652,10 @@ int sfmm_gpu_check_status(sfmm_gpu_plan* p) {
   std::lock_guard<std::mutex> lock(p->mu);
   try {
     DeviceGuard device_guard(p->device);
+    ck(cudaStreamSynchronize(p->stream), "sync");
     ck(cudaDeviceSynchronize(), "sync");
-    int flag = 0;
-    ck(cudaMemcpy(&flag, p->dp.err_flag, sizeof(int), cudaMemcpyDeviceToHost), "flag");
-    if (flag) {
-      ck(cudaMemset(p->dp.err_flag, 0, sizeof(int)), "memset");
+    if (multi_take_error_flag(p))
       return set_error(SFMM_EDUPLICATE, "fmm_apply: coincident points with distinct indices");
-    }
     return SFMM_OK;
   } catch (const CudaFail& f) {
     return set_error(f.code, f.msg);
@@ -933,11 +681,14 @@ int sfmm_gpu_plan_info_get(const sfmm_gpu_plan* p, sfmm_gpu_plan_info* info) {
   info->n_level1_pairs = hp.n_l1;
   info->launches_per_apply = p->launches_per_apply();
   info->k2_grid = p->dp.k2_grid;
+  if (p->multi) multi_info(p, info);
   return SFMM_OK;
 }
 
 int sfmm_gpu_set_timing(sfmm_gpu_plan* p, int enable) {
   if (!p) return set_error(SFMM_EINVAL, "null plan");
+  if (p->multi || p->nccl)
+    return set_error(SFMM_EUNSUPPORTED, "set_timing: per-phase timing is per rank plan");
   std::lock_guard<std::mutex> lock(p->mu);
   try {
     DeviceGuard device_guard(p->device);

@@ -186,6 +186,33 @@ class ShardedPlan:
                                                  C.c_void_p(u_dev.data_ptr()),
                                                  C.c_void_p(stream or None)))
 
+    # ---- exchange inside the library (NCCL, one process per GPU) ----------
+    def attach_nccl(self, unique_id: bytes) -> None:
+        """Joins this rank to the NCCL communicator of id `unique_id` (from
+        nccl_unique_id() on rank 0, broadcast by the caller); sfmm_gpu_apply /
+        apply() on this plan are then collective, both exchanges run inside the
+        library (sfmm_gpu_plan_attach_nccl)."""
+        _set_nccl_path()
+        buf = C.create_string_buffer(bytes(unique_id), NCCL_ID_BYTES)
+        _raise(_abi.gpu_lib().sfmm_gpu_plan_attach_nccl(self._h, buf, self.n_ranks, self.rank))
+
+    def set_output(self, owned_only: bool) -> None:
+        """Collective applies write the whole u on every rank (default, one
+        in-place all-reduce) or only this rank's owned points."""
+        _raise(_abi.gpu_lib().sfmm_gpu_set_output(
+            self._h, _abi.SFMM_OUTPUT_OWNED if owned_only else _abi.SFMM_OUTPUT_FULL))
+
+    def apply(self, q_dev, u_dev, stream: int) -> None:
+        """One collective apply (NCCL-attached plan) enqueued on `stream`."""
+        _raise(_abi.gpu_lib().sfmm_gpu_apply_async(self._h, C.c_void_p(q_dev.data_ptr()),
+                                                   C.c_void_p(u_dev.data_ptr()), 1,
+                                                   C.c_void_p(stream or None)))
+
+    def apply_host(self, q: np.ndarray, out: np.ndarray) -> None:
+        """Collective apply through the public host-buffer entry point."""
+        _raise(_abi.gpu_lib().sfmm_gpu_apply(self._h, q.ctypes.data, out.ctypes.data, 1,
+                                             _abi.SFMM_HOST_BUFFERS, None))
+
     def close(self) -> None:
         if self._h is not None:
             _abi.gpu_lib().sfmm_gpu_plan_destroy(self._h)
@@ -196,6 +223,32 @@ class ShardedPlan:
             self.close()
         except Exception:
             pass
+
+
+NCCL_ID_BYTES = 128
+
+
+def _set_nccl_path() -> None:
+    """Points the library's run-time NCCL load at the NCCL torch ships (the
+    one torch.distributed already uses in this process), unless set."""
+    import os
+    if os.environ.get("SFMM_NCCL_LIB"):
+        return
+    try:
+        import nvidia.nccl
+        base = os.path.join(list(nvidia.nccl.__path__)[0], "lib", "libnccl.so.2")
+        if os.path.exists(base):
+            os.environ["SFMM_NCCL_LIB"] = base
+    except ImportError:
+        pass
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh NCCL communicator id (rank 0), 128 bytes."""
+    _set_nccl_path()
+    buf = C.create_string_buffer(NCCL_ID_BYTES)
+    _raise(_abi.gpu_lib().sfmm_gpu_nccl_unique_id(buf))
+    return buf.raw
 
 
 def _work_stream(stream, device):

@@ -123,3 +123,11 @@ def test_descriptor_roundtrip_through_npz(tmp_path):
     for k in d.arrays:
         assert np.array_equal(d.arrays[k], d2.arrays[k])
     assert d.scalars == d2.scalars
+
+
+def test_nccl_unique_id_without_gpu():
+    # the library loads NCCL at run time (dlopen) for the one-process-per-GPU
+    # exchange; making a communicator id needs no device
+    from paper_2310_16668_b200 import shard
+    uid = shard.nccl_unique_id()
+    assert isinstance(uid, bytes) and len(uid) == shard.NCCL_ID_BYTES and any(uid)

@@ -7,8 +7,8 @@ the GPU plan, and compares the GPU apply with the reference CPU fmm_apply on
 the same operators and charges:
 
 * rel-l2 <= 1e-12 (north star) and identical ApplyStats pair counts;
-* max-rel vs the reference dense sum on sampled targets <= 10 * tol
-  (test_apply.cpp:108-152, acceptance.cpp:190-226).
+* max-rel vs the reference dense sum on sampled targets <= 10 * tol, or
+  1e-6 at tol 1e-8 (test_apply.cpp:108-162, acceptance.cpp:190-226).
 
 Sizes are the largest the reference CPU apply finishes in well under a minute
 on the GPU box's 16 host cores: config 1 and 2 at their full N, the
@@ -56,7 +56,10 @@ def _check_against_reference(kernel, pts, leaf, tol, kappa, q, n_check=1000):
         st_ref["n_level1_pairs"])
     t = _targets(len(q), n_check)
     dense = po.ref_direct_sum(kernel, kappa, pts, q, t)
-    assert max_rel(u[t], dense) <= 10 * tol
+    # the reference's own bars: 10 tol (test_apply.cpp:108-152), and 1e-6 at
+    # tol 1e-8 (test_apply.cpp:154-162); the reference apply meets the same
+    assert max_rel(u[t], dense) <= max(10 * tol, 1e-6)
+    assert max_rel(u_ref[t], dense) <= max(10 * tol, 1e-6)
     plan.close()
     rp.close()
     return d, st_ref, err
