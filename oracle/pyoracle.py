@@ -26,6 +26,9 @@ if ROOT not in sys.path:
 from paper_2310_16668_b200._abi import PlanDesc, PlanDescriptor  # noqa: E402
 
 REF_SO = os.path.join(HERE, "_ref", "libsfmm_ref.so")
+# the same reference sources and flags plus -march=sapphirerapids (the GPU box
+# host's -march=native): the second CPU figure of SURVEY.md 8d
+REF_NATIVE_SO = os.path.join(HERE, "_ref", "native", "libsfmm_ref.so")
 ORACLE_SO = os.path.join(HERE, "_build", "libsfmm_oracle.so")
 
 DIST = {"square": 0, "annulus": 1, "cube": 2, "sphere": 3}  # bench.hpp:15
@@ -33,7 +36,7 @@ DIST_DIM = {"square": 2, "annulus": 2, "cube": 3, "sphere": 3}
 CHARGE_STREAM = 0x9E3779B97F4A7C15  # bench.cpp:27
 CHECK_STREAM = 0xC2B2AE3D27D4EB4F   # bench.cpp:28
 
-_ref = None
+_ref = {}
 _orc = None
 
 
@@ -51,12 +54,23 @@ def have_oracle() -> bool:
     return os.path.exists(ORACLE_SO)
 
 
-def ref_lib() -> C.CDLL:
-    global _ref
-    if _ref is None:
-        if not have_ref():
-            raise FileNotFoundError(f"{REF_SO} not built (make -C oracle ref)")
-        lib = C.CDLL(REF_SO)
+def have_ref_native() -> bool:
+    """The -march build exists and this host CPU can run it (AVX-512 + AMX)."""
+    if not os.path.exists(REF_NATIVE_SO):
+        return False
+    try:
+        flags = open("/proc/cpuinfo").read()
+    except OSError:
+        return False
+    return all(f in flags for f in ("avx512f", "avx512bw", "avx512vl", "amx_tile", "avx512_fp16"))
+
+
+def ref_lib(native: bool = False) -> C.CDLL:
+    if native not in _ref:
+        path = REF_NATIVE_SO if native else REF_SO
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} not built (make -C oracle ref)")
+        lib = C.CDLL(path)
         vp = C.c_void_p
         lib.ref_last_error.restype = C.c_char_p
         lib.ref_num_threads.restype = C.c_int
@@ -80,8 +94,8 @@ def ref_lib() -> C.CDLL:
         lib.ref_direct_sum.argtypes = [C.c_int, C.c_double, C.c_int, C.c_int64, vp, vp, C.c_int64,
                                        vp, vp]
         lib.ref_eval_kernel.argtypes = [C.c_int, C.c_double, vp, vp, vp]
-        _ref = lib
-    return _ref
+        _ref[native] = lib
+    return _ref[native]
 
 
 def oracle_lib() -> C.CDLL:
@@ -127,18 +141,20 @@ def generate_charges_complex(n: int, seed: int) -> np.ndarray:
 class RefPipeline:
     """Reference objects (Tree, NeighborLists, SkeletonSet, ApplyPlan)."""
 
-    def __init__(self, handle):
+    def __init__(self, handle, native: bool = False):
         self._h = handle
+        self._lib = ref_lib(native)
 
     @classmethod
     def build(cls, kernel: int, pts: np.ndarray, leaf_cap: int, tol: float, kappa: float = 1.0,
-              proxy_radius: float = 0.0, proxy_edge2d: int = 0, proxy_face3d: int = 0):
+              proxy_radius: float = 0.0, proxy_edge2d: int = 0, proxy_face3d: int = 0,
+              native: bool = False):
         pts = np.ascontiguousarray(pts, dtype=np.float64)
         h = C.c_void_p()
-        _check(ref_lib().ref_build(kernel, kappa, pts.shape[1], pts.shape[0], pts.ctypes.data,
-                                   leaf_cap, tol, proxy_radius, proxy_edge2d, proxy_face3d,
-                                   C.byref(h)))
-        return cls(h)
+        _check(ref_lib(native).ref_build(kernel, kappa, pts.shape[1], pts.shape[0],
+                                         pts.ctypes.data, leaf_cap, tol, proxy_radius,
+                                         proxy_edge2d, proxy_face3d, C.byref(h)))
+        return cls(h, native)
 
     @classmethod
     def build_tree(cls, pts: np.ndarray, leaf_cap: int):
@@ -150,26 +166,26 @@ class RefPipeline:
         return cls(h)
 
     @classmethod
-    def from_desc(cls, desc):
+    def from_desc(cls, desc, native: bool = False):
         """desc: PlanDescriptor or a ctypes PlanDesc (zero-copy view)."""
         st = desc.struct if isinstance(desc, PlanDescriptor) else desc
         h = C.c_void_p()
-        _check(ref_lib().ref_from_desc(C.byref(st), C.byref(h)))
-        return cls(h)
+        _check(ref_lib(native).ref_from_desc(C.byref(st), C.byref(h)))
+        return cls(h, native)
 
     def descriptor(self) -> PlanDescriptor:
-        return PlanDescriptor.from_struct(ref_lib().ref_desc(self._h).contents)
+        return PlanDescriptor.from_struct(self._lib.ref_desc(self._h).contents)
 
     def box_geometry(self):
         """(centre (n_boxes*3,), half-width (n_boxes,)) of the reference tree."""
-        nb = int(ref_lib().ref_desc(self._h).contents.n_boxes)
+        nb = int(self._lib.ref_desc(self._h).contents.n_boxes)
         c, h = np.zeros(3 * nb), np.zeros(nb)
-        ref_lib().ref_box_geometry(self._h, c.ctypes.data, h.ctypes.data)
+        self._lib.ref_box_geometry(self._h, c.ctypes.data, h.ctypes.data)
         return c, h
 
     def info(self) -> dict:
         out = np.zeros(6, dtype=np.int64)
-        ref_lib().ref_info(self._h, out.ctypes.data)
+        self._lib.ref_info(self._h, out.ctypes.data)
         keys = ["depth", "n_boxes", "k_max", "proj_scalars", "saturated_boxes", "n_leaves"]
         return dict(zip(keys, (int(v) for v in out)))
 
@@ -177,13 +193,15 @@ class RefPipeline:
         q = np.ascontiguousarray(q, dtype=np.complex128 if cplx else np.float64)
         u = np.empty_like(q)
         st = np.zeros(5, dtype=np.int64)
-        _check(ref_lib().ref_apply(self._h, q.ctypes.data, u.ctypes.data, st.ctypes.data))
+        rc = self._lib.ref_apply(self._h, q.ctypes.data, u.ctypes.data, st.ctypes.data)
+        if rc != 0:
+            raise RefError(rc, self._lib.ref_last_error().decode())
         return u, dict(zip(["n_ifo_pairs", "n_ifs_pairs", "n_tfo_pairs", "n_level1_pairs",
                             "direct_fallback"], (int(v) for v in st)))
 
     def close(self):
         if self._h is not None:
-            ref_lib().ref_destroy(self._h)
+            self._lib.ref_destroy(self._h)
             self._h = None
 
     def __del__(self):

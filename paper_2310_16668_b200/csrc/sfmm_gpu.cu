@@ -679,9 +679,12 @@ int sfmm_gpu_plan_info_get(const sfmm_gpu_plan* p, sfmm_gpu_plan_info* info) {
   info->n_ifs_pairs = hp.n_ifs;
   info->n_tfo_pairs = hp.n_tfo;
   info->n_level1_pairs = hp.n_l1;
-  info->launches_per_apply = p->launches_per_apply();
-  info->k2_grid = p->dp.k2_grid;
-  if (p->multi) multi_info(p, info);
+  if (p->multi) {
+    multi_info(p, info);  // the orchestrating plan has no level lists of its own
+  } else {
+    info->launches_per_apply = p->launches_per_apply();
+    info->k2_grid = p->dp.k2_grid;
+  }
   return SFMM_OK;
 }
 
