@@ -133,8 +133,6 @@ typedef struct sfmm_gpu_plan_info {
   int64_t n_ifo_pairs, n_ifs_pairs, n_tfo_pairs, n_level1_pairs;
   int32_t launches_per_apply; /* kernels of this library launched by one single-RHS apply (this rank) */
   int32_t k2_grid;            /* persistent CTAs of the translation kernel */
-  int32_t fast_rsqrt;         /* Laplace 3D: the translation kernel uses the 3-FP64-op rsqrt
-                                 (every evaluated squared distance in [2^-120, 2^120]) */
 } sfmm_gpu_plan_info;
 
 typedef struct sfmm_gpu_plan sfmm_gpu_plan;

@@ -28,11 +28,6 @@ int sfmm_probe_test_sincos(const double* x, int64_t n, double* out);
  * Laplace-2D kernels (fastmath.cuh) and from the CUDA library. */
 int sfmm_probe_test_log(const double* x, int64_t n, double* out);
 
-/* out[2i], out[2i+1] = 1/sqrt(x_i) from the 3-FP64-instruction routine of the
- * Laplace-3D translation kernel (FP32 seed + one Newton step, fastmath.cuh)
- * and from the CUDA library (1.0 / sqrt). */
-int sfmm_probe_test_rsqrt(const double* x, int64_t n, double* out);
-
 #ifdef __cplusplus
 }
 #endif

@@ -96,7 +96,6 @@ class PlanInfo(C.Structure):
         ("n_level1_pairs", C.c_int64),
         ("launches_per_apply", C.c_int32),
         ("k2_grid", C.c_int32),
-        ("fast_rsqrt", C.c_int32),
     ]
 
 
@@ -388,8 +387,7 @@ GPU_SYMBOLS = [
 SFMM_OUTPUT_FULL, SFMM_OUTPUT_OWNED = 0, 1
 
 
-PROBE_SYMBOLS = ["sfmm_probe_fp64_peak", "sfmm_probe_test_sincos", "sfmm_probe_test_log",
-                 "sfmm_probe_test_rsqrt"]
+PROBE_SYMBOLS = ["sfmm_probe_fp64_peak", "sfmm_probe_test_sincos", "sfmm_probe_test_log"]
 
 _probe_lib = None
 
@@ -411,7 +409,5 @@ def probe_lib() -> C.CDLL:
     lib.sfmm_probe_test_sincos.restype = C.c_int
     lib.sfmm_probe_test_log.argtypes = [vp, C.c_int64, vp]
     lib.sfmm_probe_test_log.restype = C.c_int
-    lib.sfmm_probe_test_rsqrt.argtypes = [vp, C.c_int64, vp]
-    lib.sfmm_probe_test_rsqrt.restype = C.c_int
     _probe_lib = lib
     return lib

@@ -27,7 +27,6 @@
 #include <math.h>
 
 #include <algorithm>
-#include <cstring>
 
 #include "fastmath.cuh"
 #include "launch.h"
@@ -61,11 +60,8 @@ struct K2Args {
 };
 
 // Far-away padding for partial source chunks of kSYM blocks: finite r^2,
-// negligible G, zero weights.  The fast-rsqrt generator needs r^2 inside the
-// float exponent range: its plans have |coordinates| <= 2^30, so 2^40 keeps
-// r^2 < 2^83.
+// negligible G, zero weights.
 constexpr double kFar = 1e100;
-constexpr double kFarFast = 1099511627776.0;  // 2^40
 
 // rsqrt to full double precision: MUFU.RSQ64H seed + one cubic correction
 // (5 FP64 ops).  r2 == 0 yields NaN, which the diagonal select / duplicate
@@ -85,7 +81,6 @@ struct GenLaplace3d {  // kernel.hpp:46-50  1/(4 pi r)
   static constexpr int kDim = 3;
   static constexpr double kScale = kInv4Pi;
   static constexpr bool kLogTable = false;
-  static constexpr double kPad = kFar;
   __device__ static __forceinline__ double g(double r2, uint32_t) { return rsqrt_fp64(r2); }
   // M independent evaluations, stage by stage, so their dependent chains
   // interleave in the issue stream.
@@ -100,27 +95,10 @@ struct GenLaplace3d {  // kernel.hpp:46-50  1/(4 pi r)
     for (int m = 0; m < M; ++m) g[m] = fma(fma(0.375, e[m], 0.5), y[m] * e[m], y[m]);
   }
 };
-// Laplace 3D on plans whose squared distances are all in the float range
-// (DevPlan::fast_rsqrt): 3 FP64 instructions per rsqrt instead of 5.
-struct GenLaplace3dFast {
-  static constexpr int kDim = 3;
-  static constexpr double kScale = kInv4Pi;
-  static constexpr bool kLogTable = false;
-  static constexpr double kPad = kFarFast;
-  __device__ static __forceinline__ double g(double r2, uint32_t) {
-    return rsqrt_newton_f32seed(r2);
-  }
-  template <int M>
-  __device__ static __forceinline__ void batch(const double* r2, double* g, uint32_t) {
-#pragma unroll
-    for (int m = 0; m < M; ++m) g[m] = rsqrt_newton_f32seed(r2[m]);
-  }
-};
 struct GenLaplace2d {  // kernel.hpp:40-44  -log(r^2)/(4 pi)
   static constexpr int kDim = 2;
   static constexpr double kScale = -kInv4Pi;
   static constexpr bool kLogTable = true;  // log_tab with the table in shared memory
-  static constexpr double kPad = kFar;
   __device__ static __forceinline__ double g(double r2, uint32_t lt) { return log_tab(lt, r2); }
   template <int M>
   __device__ static __forceinline__ void batch(const double* r2, double* g, uint32_t lt) {
@@ -279,8 +257,8 @@ __device__ __forceinline__ void task_real(const K2Args& a, const Task& t, WarpSm
           sm.za[lane] = make_double2(G::kDim == 3 ? a.Z[s] : 0.0, a.Q[s]);
           sm.h[lane] = j < sb.k ? a.QH[sb.skel + j] : 0.0;
         } else {
-          sm.xy[lane] = make_double2(G::kPad, G::kPad);
-          sm.za[lane] = make_double2(G::kPad, 0.0);
+          sm.xy[lane] = make_double2(kFar, kFar);
+          sm.za[lane] = make_double2(kFar, 0.0);
           sm.h[lane] = 0.0;
         }
         __syncwarp();
@@ -703,72 +681,7 @@ __global__ void __launch_bounds__(256) k2b_reduce_cplx(const BoxRec* __restrict_
   }
 }
 
-// Smallest squared distance over the pairs K2 evaluates (the same task and
-// entry lists, self pairs excluded), for DevPlan::fast_rsqrt.  One warp per
-// task, sources read through L1 (a one-off pass at plan creation).
-__global__ void __launch_bounds__(256) k_min_r2(K2Args a, unsigned long long* out) {
-  const int lane = threadIdx.x & 31;
-  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  double mn = INFINITY;
-  for (int64_t t = w0; t < a.n_tasks; t += nw) {
-    const Task task = a.tasks[t];
-    const BoxRec tb = a.box[task.box];
-    const EntryRange er = a.er[task.box];
-    for (int r0 = task.row0; r0 < task.row0 + task.nrows; r0 += 32) {
-      const int row = r0 + lane;
-      const bool valid = row < task.row0 + task.nrows;
-      const int64_t s = tb.slot + (valid ? row : task.row0);
-      const double x = a.X[s], y = a.Y[s], z = a.Z[s];
-      for (int e = 0; e < er.count; ++e) {
-        const int32_t c = a.ent[er.begin + e] >> kModeBits;
-        const BoxRec sb = a.box[c];
-        const bool self = c == task.box;
-        for (int j = 0; j < sb.n; ++j) {
-          const int64_t u = sb.slot + j;
-          const double dx = x - a.X[u], dy = y - a.Y[u], dz = z - a.Z[u];
-          const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-          if (valid && !(self && j == row)) mn = fmin(mn, r2);
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mn = fmin(mn, __shfl_xor_sync(kFull, mn, o));
-  // r2 >= 0: the bit patterns order like the values
-  if (lane == 0) atomicMin(out, static_cast<unsigned long long>(__double_as_longlong(mn)));
-}
-
 }  // namespace
-
-double measure_min_r2(const DevPlan& p, cudaStream_t st) {
-  if (p.n_tasks == 0) return INFINITY;
-  unsigned long long* d = nullptr;
-  if (cudaMalloc(&d, sizeof(unsigned long long)) != cudaSuccess) return -1.0;
-  const double inf = INFINITY;
-  unsigned long long init;
-  memcpy(&init, &inf, sizeof(init));
-  cudaMemcpyAsync(d, &init, sizeof(init), cudaMemcpyHostToDevice, st);
-  K2Args a{};
-  a.box = p.box;
-  a.er = p.ent_range;
-  a.ent = p.entries;
-  a.tasks = p.tasks;
-  a.n_tasks = p.n_tasks;
-  a.X = p.X;
-  a.Y = p.Y;
-  a.Z = p.Z;
-  const int grid = (int)std::min<int64_t>(148 * 8, (p.n_tasks + 7) / 8);
-  k_min_r2<<<grid, 256, 0, st>>>(a, d);
-  unsigned long long bits = 0;
-  cudaMemcpyAsync(&bits, d, sizeof(bits), cudaMemcpyDeviceToHost, st);
-  const cudaError_t e = cudaStreamSynchronize(st);
-  cudaFree(d);
-  if (e != cudaSuccess) return -1.0;
-  double v;
-  memcpy(&v, &bits, sizeof(v));
-  return v;
-}
 
 int configure_translate(DevPlan& p, int device) {
   int sms = 0, per_sm = 0;
@@ -777,9 +690,6 @@ int configure_translate(DevPlan& p, int device) {
   cudaError_t e;
   if (p.kernel == SFMM_HELMHOLTZ3D)
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_translate_cplx<true>, kThreads, 0);
-  else if (p.kernel == SFMM_LAPLACE3D && p.fast_rsqrt)
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per_sm, k2_real_kernel<GenLaplace3dFast>(p.k2_r1), kThreads, 0);
   else if (p.kernel == SFMM_LAPLACE3D)
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
         &per_sm, k2_real_kernel<GenLaplace3d>(p.k2_r1), kThreads, 0);
@@ -835,8 +745,6 @@ void launch_translate(const DevPlan& p, DevState& s, cudaStream_t st, TranslateP
         k2_translate_cplx<true><<<grid, kThreads, 0, st>>>(a);
       else
         k2_translate_cplx<false><<<grid, kThreads, 0, st>>>(a);
-    else if (p.kernel == SFMM_LAPLACE3D && p.fast_rsqrt)
-      k2_real_kernel<GenLaplace3dFast>(p.k2_r1)<<<grid, kThreads, 0, st>>>(a);
     else if (p.kernel == SFMM_LAPLACE3D)
       k2_real_kernel<GenLaplace3d>(p.k2_r1)<<<grid, kThreads, 0, st>>>(a);
     else

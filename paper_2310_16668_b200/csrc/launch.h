@@ -69,16 +69,8 @@ struct DevPlan {
   int* err_flag;    // sticky duplicate-point flag
   int k2_grid;      // persistent K2 CTAs
   int k2_r1 = 0;    // every K2 task has <= 32 rows: the 64-register R = 1 kernel
-  // Laplace 3D: every squared distance K2 evaluates lies in [2^-120, 2^120]
-  // and |coordinates| <= 2^30 (measured once at plan creation), so K2 may
-  // use the 3-FP64-instruction rsqrt (fastmath.cuh rsqrt_newton_f32seed)
-  int fast_rsqrt = 0;
   size_t up_smem, down_smem;
 };
-
-// Smallest squared distance over every (row, source) pair K2 evaluates,
-// self pairs excluded (plan creation, synchronous; +inf when there are none).
-double measure_min_r2(const DevPlan& p, cudaStream_t st);
 
 // K0: Q[leaf_slot[t]] = q[leaf_orig[t]]
 void launch_gather(const DevPlan& p, const double* q, DevState& s, cudaStream_t st);

@@ -46,31 +46,6 @@ __global__ void log_check(const double* x, int64_t n, const double* tab, double*
 }  // namespace
 
 namespace {
-__global__ void rsqrt_check(const double* x, int64_t n, double* out) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    out[2 * i] = rsqrt_newton_f32seed(x[i]);
-    out[2 * i + 1] = 1.0 / sqrt(x[i]);
-  }
-}
-}  // namespace
-
-namespace {
-
-int test_rsqrt(const double* x_host, int64_t n, double* out_host) {
-  double *dx = nullptr, *dout = nullptr;
-  int rc = -1;
-  if (cudaMalloc(&dx, std::max<int64_t>(n, 1) * sizeof(double)) == cudaSuccess &&
-      cudaMalloc(&dout, std::max<int64_t>(2 * n, 1) * sizeof(double)) == cudaSuccess) {
-    cudaMemcpy(dx, x_host, n * sizeof(double), cudaMemcpyHostToDevice);
-    rsqrt_check<<<148 * 4, 256>>>(dx, n, dout);
-    cudaMemcpy(out_host, dout, 2 * n * sizeof(double), cudaMemcpyDeviceToHost);
-    rc = cudaGetLastError() == cudaSuccess ? 0 : -1;
-  }
-  cudaFree(dx);
-  cudaFree(dout);
-  return rc;
-}
 
 int test_log(const double* x_host, int64_t n, double* out_host) {
   double *dx = nullptr, *dout = nullptr, *dtab = nullptr;
@@ -178,11 +153,6 @@ int sfmm_probe_test_log(const double* x, int64_t n, double* out) {
 int sfmm_probe_test_sincos(const double* x, int64_t n, double* out) {
   if (!x || !out || n < 0) return 1;
   return sfmm_gpu::test_sincos(x, n, out) == 0 ? 0 : 3;
-}
-
-int sfmm_probe_test_rsqrt(const double* x, int64_t n, double* out) {
-  if (!x || !out || n < 0) return 1;
-  return sfmm_gpu::test_rsqrt(x, n, out) == 0 ? 0 : 3;
 }
 
 int sfmm_probe_fp64_peak(int device, double* tflops) {

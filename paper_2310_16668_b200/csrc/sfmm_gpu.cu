@@ -203,21 +203,6 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
         for (const Task& t : hp.tasks) max_rows = std::max(max_rows, t.nrows);
         dp.k2_r1 = !hp.cplx && max_rows <= 32;
       }
-      // Laplace 3D: the 3-instruction rsqrt needs every squared distance K2
-      // evaluates inside the float exponent range -- bounded coordinates, and
-      // no pair closer than 2^-60 (measured over the plan's own pairs once;
-      // coincident points with distinct ids fail it and keep the exact path,
-      // which reports them)
-      if (hp.kernel == SFMM_LAPLACE3D && !std::getenv("SFMM_FAST_RSQRT_OFF")) {
-        bool bounded = true;
-        for (int64_t i = 0; i < hp.n_points * hp.dim && bounded; ++i)
-          bounded = std::fabs(desc->pts[i]) <= 1073741824.0;  // 2^30
-        if (bounded) {
-          const double mn = measure_min_r2(dp, p->stream);
-          if (mn < 0) throw CudaFail{SFMM_ECUDA, "minimum distance pass failed"};
-          dp.fast_rsqrt = mn >= 0x1p-120 ? 1 : 0;
-        }
-      }
       if (configure_translate(dp, device) != 0)
         throw CudaFail{SFMM_ECUDA, "occupancy query failed"};
       if (configure_multi(dp, device, max_k) != 0)
@@ -700,7 +685,6 @@ int sfmm_gpu_plan_info_get(const sfmm_gpu_plan* p, sfmm_gpu_plan_info* info) {
     info->launches_per_apply = p->launches_per_apply();
     info->k2_grid = p->dp.k2_grid;
   }
-  info->fast_rsqrt = p->multi ? 0 : p->dp.fast_rsqrt;
   return SFMM_OK;
 }
 

@@ -352,39 +352,3 @@ def test_sync_apply_on_device_buffers():
                                                  _abi.SFMM_DEVICE_BUFFERS, C.byref(st)))
         assert np.array_equal(ud.cpu().numpy().T, U)
         assert st.n_ifo_pairs > 0 and st.ms_total > 0
-
-
-@pytest.mark.parametrize("dist,tol", [("cube", 1e-6), ("sphere", 1e-8)])
-def test_fast_rsqrt_plans_match_exact_path_and_reference(dist, tol, monkeypatch):
-    """Laplace-3D plans whose pairs all lie in the float range use the
-    3-instruction rsqrt in K2; against the exact-rsqrt path on the same plan
-    and against the reference the result stays within 1e-13 / 1e-12."""
-    n = 60000
-    pts = host.generate_points(dist, n, 11)
-    d = ref_descriptor(1, pts, 64, tol)
-    q = host.generate_charges(n, 12)
-    fast = api.GpuPlan(d)
-    assert fast.info().fast_rsqrt == 1
-    u_fast = api.fmm_apply(fast, q)
-    monkeypatch.setenv("SFMM_FAST_RSQRT_OFF", "1")
-    exact = api.GpuPlan(d)
-    assert exact.info().fast_rsqrt == 0
-    u_exact = api.fmm_apply(exact, q)
-    assert 0 < rel_l2(u_fast, u_exact) <= 1e-13
-    rp = po.RefPipeline.from_desc(d)
-    u_ref, _ = rp.apply(q)
-    rp.close()
-    assert rel_l2(u_fast, u_ref) <= PARITY
-
-
-def test_fast_rsqrt_refused_for_coincident_or_huge_coordinates():
-    pts = host.generate_points("cube", 3000, 7)
-    d = ref_descriptor(1, pts, 40, 1e-6)
-    a = d.arrays
-    leaf = int(np.nonzero(a["box_leaf"] & (a["box_end"] - a["box_begin"] >= 2))[0][0])
-    P = a["pts"].reshape(-1, 3)
-    P[a["box_begin"][leaf] + 1] = P[a["box_begin"][leaf]]
-    d._struct = None
-    assert api.GpuPlan(d).info().fast_rsqrt == 0      # r2 = 0 pair: exact path reports it
-    big = ref_descriptor(1, host.generate_points("cube", 3000, 8) * 1e10, 40, 1e-6)
-    assert api.GpuPlan(big).info().fast_rsqrt == 0    # |x| > 2^30
