@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(kMThreads, WH ? SFMM_K2M_MIN_BLOCKS_WH : SFMM_
 
 // K0m: Qm[slot][r] = q[orig + r*N] for r < nc, 0 for the padding columns.
 template <class S>
-__global__ void k0m_gather(const int64_t* __restrict__ slot, const int32_t* __restrict__ orig,
+__global__ void k0m_gather(const int32_t* __restrict__ slot, const int32_t* __restrict__ orig,
                            int64_t n_owned, int64_t N, int nc, const S* __restrict__ q,
                            S* __restrict__ Q) {
   const int64_t total = n_owned * kNRHS;
@@ -406,12 +406,12 @@ __global__ void k0m_gather(const int64_t* __restrict__ slot, const int32_t* __re
     const int r = (int)(i % kNRHS);
     S v{};
     if (r < nc) v = q[(int64_t)r * N + orig[t]];
-    Q[slot[t] * kNRHS + r] = v;
+    Q[(int64_t)slot[t] * kNRHS + r] = v;
   }
 }
 
 template <class S>
-__global__ void k4m_scatter(const int64_t* __restrict__ slot, const int32_t* __restrict__ orig,
+__global__ void k4m_scatter(const int32_t* __restrict__ slot, const int32_t* __restrict__ orig,
                             int64_t n_owned, int64_t N, int nc, const S* __restrict__ U,
                             S* __restrict__ u) {
   const int64_t total = n_owned * kNRHS;
@@ -419,7 +419,7 @@ __global__ void k4m_scatter(const int64_t* __restrict__ slot, const int32_t* __r
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t t = i / kNRHS;
     const int r = (int)(i % kNRHS);
-    if (r < nc) u[(int64_t)r * N + orig[t]] = U[slot[t] * kNRHS + r];
+    if (r < nc) u[(int64_t)r * N + orig[t]] = U[(int64_t)slot[t] * kNRHS + r];
   }
 }
 
@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(kUpRows * kNRHS) k1m_upward(const LevelItem* _
                                                   const int64_t* __restrict__ T_off,
                                                   const S* __restrict__ T, S* __restrict__ Q,
                                                   S* __restrict__ QH,
-                                                  const int64_t* __restrict__ up_dst) {
+                                                  const int32_t* __restrict__ up_dst) {
   __shared__ S sq[64][kNRHS];
   const LevelItem it = items[blockIdx.x];
   const BoxRec br = box[it.box];
@@ -478,7 +478,7 @@ __global__ void __launch_bounds__(kUpRows * kNRHS) k1m_upward(const LevelItem* _
       v += acc;
     }
     QH[(br.skel + i) * kNRHS + rhs] = v;
-    Q[up_dst[br.skel + i] * kNRHS + rhs] = v;
+    Q[(int64_t)up_dst[br.skel + i] * kNRHS + rhs] = v;
   }
 }
 
@@ -490,7 +490,7 @@ __global__ void __launch_bounds__(256) k3m_downward(const LevelItem* __restrict_
                                                     const int64_t* __restrict__ T_off,
                                                     const S* __restrict__ T, S* __restrict__ U,
                                                     const S* __restrict__ UH,
-                                                    const int64_t* __restrict__ up_dst) {
+                                                    const int32_t* __restrict__ up_dst) {
   extern __shared__ unsigned char smraw[];
   S* su = reinterpret_cast<S*>(smraw);  // [k][kNRHS]
   const LevelItem it = items[blockIdx.x];
@@ -498,7 +498,7 @@ __global__ void __launch_bounds__(256) k3m_downward(const LevelItem* __restrict_
   const int k = br.k, r = br.n - br.k;
   for (int v = threadIdx.x; v < k * kNRHS; v += blockDim.x) {
     const int i = v / kNRHS, rr = v % kNRHS;
-    S a = UH[(br.skel + i) * kNRHS + rr], b = U[up_dst[br.skel + i] * kNRHS + rr];
+    S a = UH[(br.skel + i) * kNRHS + rr], b = U[(int64_t)up_dst[br.skel + i] * kNRHS + rr];
     S s;
     if constexpr (sizeof(S) == 16) {
       s = make_double2(a.x + b.x, a.y + b.y);

@@ -12,6 +12,7 @@
 // compressed box are stored [skeleton | redundant], so the vectors they touch
 // are contiguous.
 #include <algorithm>
+#include <cstdlib>
 
 #include "launch.h"
 
@@ -22,21 +23,39 @@ constexpr unsigned kFull = 0xffffffffu;
 constexpr int kUpThreads = 256;
 constexpr double kInv4Pi = 0.0795774715459476678844418816862571810;
 
+// K0 + the leaf-level K1 copy: Q[slot] = q[orig]; for a point of an
+// uncompressed leaf (k = n: every slot is a skeleton slot) also qhat = q and
+// the parent's slot (k1_copy's work, apply.cpp:124-131, fused here so the
+// leaf charges are read once).  int32 maps: 12 B of indices per point.
 template <class S>
-__global__ void k0_gather(const int64_t* __restrict__ slot, const int32_t* __restrict__ orig,
-                          int64_t n, const S* __restrict__ q, S* __restrict__ Q) {
+__global__ void __launch_bounds__(256) k0_gather(const int32_t* __restrict__ slot,
+                                                 const int32_t* __restrict__ orig,
+                                                 const int32_t* __restrict__ hat,
+                                                 const int32_t* __restrict__ up_dst, int64_t n,
+                                                 const S* __restrict__ q, S* __restrict__ Q,
+                                                 S* __restrict__ QH) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
-       t += (int64_t)gridDim.x * blockDim.x)
-    Q[slot[t]] = q[orig[t]];
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const S v = __ldg(q + __ldg(orig + t));
+    Q[__ldg(slot + t)] = v;
+    const int32_t h = __ldg(hat + t);
+    if (h >= 0) {
+      QH[h] = v;
+      Q[__ldg(up_dst + h)] = v;
+    }
+  }
 }
 
+// K4 + the leaf-level K3 copy: u[orig] = U[slot] (+ uhat + the parent's
+// potential for a point of an uncompressed leaf, apply.cpp:284-301), in the
+// order k3_copy adds them, so the result is bit-identical to the unfused pair.
 template <class S>
-__global__ void k4_scatter(const int64_t* __restrict__ slot, const int32_t* __restrict__ orig,
-                           int64_t n, const S* __restrict__ U, S* __restrict__ u) {
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
-       t += (int64_t)gridDim.x * blockDim.x)
-    u[orig[t]] = U[slot[t]];
-}
+__global__ void __launch_bounds__(256) k4_scatter(const int32_t* __restrict__ slot,
+                                                  const int32_t* __restrict__ orig,
+                                                  const int32_t* __restrict__ hat,
+                                                  const int32_t* __restrict__ up_dst, int64_t n,
+                                                  const S* __restrict__ U,
+                                                  const S* __restrict__ UH, S* __restrict__ u);
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -54,7 +73,7 @@ constexpr int kUpRowsPerWarp = 4;
 __global__ void __launch_bounds__(kUpThreads) k1_upward_real(
     const LevelItem* __restrict__ items, const BoxRec* __restrict__ box,
     const int64_t* __restrict__ T_off, const double* __restrict__ T, double* __restrict__ Q,
-    double* __restrict__ QH, const int64_t* __restrict__ up_dst) {
+    double* __restrict__ QH, const int32_t* __restrict__ up_dst) {
   const LevelItem it = items[blockIdx.x];
   const BoxRec br = box[it.box];
   const int k = br.k, r = br.n - br.k;
@@ -92,11 +111,119 @@ __global__ void __launch_bounds__(kUpThreads) k1_upward_real(
   }
 }
 
+// K1, real, with the T rows staged by the bulk-copy engine (TMA, cp.async.bulk
+// -> SASS UBLKCP) instead of register loads: the CTA's 64-row slice of T is
+// contiguous (row-major k x r per box), so it moves as a few large copies into
+// a 3-deep ring of shared-memory stages, each completing on an mbarrier; the
+// eight warps reduce rows from shared memory.  Up to 3 x 32 KB are in flight
+// per CTA (two CTAs per SM) with no registers held for them -- the HBM
+// stream K1 is bound by (8 B per T entry).
+constexpr int kK1Stages = 3;
+constexpr int kK1StageBytes = 32 * 1024;
+constexpr int kK1MaxR = (kK1StageBytes - 16) / 8;  // longest row one stage holds
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// global -> shared bulk copy (16-byte aligned, size a multiple of 16)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__global__ void __launch_bounds__(kUpThreads) k1_upward_real_bulk(
+    const LevelItem* __restrict__ items, const BoxRec* __restrict__ box,
+    const int64_t* __restrict__ T_off, const double* __restrict__ T, double* __restrict__ Q,
+    double* __restrict__ QH, const int32_t* __restrict__ up_dst) {
+  extern __shared__ __align__(128) unsigned char k1sm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(k1sm);                       // kK1Stages
+  double* stage = reinterpret_cast<double*>(k1sm + 128);                    // kK1Stages x 32 KB
+  double* qR = reinterpret_cast<double*>(k1sm + 128 + kK1Stages * kK1StageBytes);
+  const LevelItem it = items[blockIdx.x];
+  const BoxRec br = box[it.box];
+  const int k = br.k, r = br.n - br.k;
+  const int i0 = it.first, i1 = min(it.first + kUpRows1, k);
+  const int rows_ps = max(1, min(i1 - i0, kK1MaxR / r));  // rows per stage
+  const int nch = (i1 - i0 + rows_ps - 1) / rows_ps;
+  const double* base = T + T_off[it.box] + (int64_t)i0 * r;
+  // chunk c: rows [i0 + c rows_ps, ...), copied from the 16-byte boundary at or
+  // below its first element (o = 0 or 1 leading element), size rounded up
+  auto issue = [&](int c) {
+    const int st = c % kK1Stages;
+    const int nr = min(rows_ps, i1 - i0 - c * rows_ps);
+    const double* src = base + (int64_t)c * rows_ps * r;
+    const int o = (int)((reinterpret_cast<uintptr_t>(src) >> 3) & 1);
+    const uint32_t bytes = (uint32_t)(((o + nr * r) * 8 + 15) & ~15);
+    mbar_expect_tx(&full[st], bytes);
+    bulk_g2s(stage + st * (kK1StageBytes / 8), src - o, bytes, &full[st]);
+  };
+  if (threadIdx.x == 0) {
+    for (int sidx = 0; sidx < kK1Stages; ++sidx) mbar_init(&full[sidx], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int c = 0; c < min(nch, kK1Stages); ++c) issue(c);
+  }
+  for (int j = threadIdx.x; j < r; j += blockDim.x) qR[j] = Q[br.slot + k + j];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int c = 0; c < nch; ++c) {
+    const int st = c % kK1Stages;
+    mbar_wait(&full[st], (uint32_t)((c / kK1Stages) & 1));
+    const double* src = base + (int64_t)c * rows_ps * r;
+    const int o = (int)((reinterpret_cast<uintptr_t>(src) >> 3) & 1);
+    const double* Ts = stage + st * (kK1StageBytes / 8) + o;
+    const int nr = min(rows_ps, i1 - i0 - c * rows_ps);
+    for (int m = w; m < nr; m += kUpThreads / 32) {
+      const double* row = Ts + m * r;
+      double a0 = 0.0, a1 = 0.0;
+      int j = lane;
+      for (; j + 32 < r; j += 64) {
+        a0 = fma(row[j], qR[j], a0);
+        a1 = fma(row[j + 32], qR[j + 32], a1);
+      }
+      if (j < r) a0 = fma(row[j], qR[j], a0);
+      const double sum = warp_sum(a0 + a1);
+      if (lane == 0) {
+        const int i = i0 + c * rows_ps + m;
+        const double v = Q[br.slot + i] + sum;
+        QH[br.skel + i] = v;
+        Q[up_dst[br.skel + i]] = v;
+      }
+    }
+    __syncthreads();  // stage st fully read
+    if (threadIdx.x == 0 && c + kK1Stages < nch) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(c + kK1Stages);
+    }
+  }
+}
+
 // K1, complex.
 __global__ void __launch_bounds__(kUpThreads) k1_upward_cplx(
     const LevelItem* __restrict__ items, const BoxRec* __restrict__ box,
     const int64_t* __restrict__ T_off, const double2* __restrict__ T, double2* __restrict__ Q,
-    double2* __restrict__ QH, const int64_t* __restrict__ up_dst) {
+    double2* __restrict__ QH, const int32_t* __restrict__ up_dst) {
   extern __shared__ double2 smq2[];
   const LevelItem it = items[blockIdx.x];
   const BoxRec br = box[it.box];
@@ -133,9 +260,25 @@ __device__ __forceinline__ double2 add_s(double2 a, double2 b) {
 }
 
 template <class S>
+__global__ void __launch_bounds__(256) k4_scatter(const int32_t* __restrict__ slot,
+                                                  const int32_t* __restrict__ orig,
+                                                  const int32_t* __restrict__ hat,
+                                                  const int32_t* __restrict__ up_dst, int64_t n,
+                                                  const S* __restrict__ U,
+                                                  const S* __restrict__ UH, S* __restrict__ u) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    S v = U[__ldg(slot + t)];
+    const int32_t h = __ldg(hat + t);
+    if (h >= 0) v = add_s(v, add_s(UH[h], U[__ldg(up_dst + h)]));
+    u[__ldg(orig + t)] = v;
+  }
+}
+
+template <class S>
 __global__ void __launch_bounds__(256) k1_copy(const int32_t* __restrict__ boxes, int64_t nbox,
                                                const BoxRec* __restrict__ box, S* __restrict__ Q,
-                                               S* __restrict__ QH, const int64_t* __restrict__ up_dst) {
+                                               S* __restrict__ QH, const int32_t* __restrict__ up_dst) {
   const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (w >= nbox) return;
   const BoxRec br = box[boxes[w]];
@@ -150,7 +293,7 @@ template <class S>
 __global__ void __launch_bounds__(256) k3_copy(const int32_t* __restrict__ boxes, int64_t nbox,
                                                const BoxRec* __restrict__ box, S* __restrict__ U,
                                                const S* __restrict__ UH,
-                                               const int64_t* __restrict__ up_dst) {
+                                               const int32_t* __restrict__ up_dst) {
   const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (w >= nbox) return;
   const BoxRec br = box[boxes[w]];
@@ -162,7 +305,7 @@ __global__ void __launch_bounds__(256) k3_copy(const int32_t* __restrict__ boxes
 __global__ void __launch_bounds__(kDownCols) k3_downward_real(
     const LevelItem* __restrict__ items, const BoxRec* __restrict__ box,
     const int64_t* __restrict__ T_off, const double* __restrict__ T, double* __restrict__ U,
-    const double* __restrict__ UH, const int64_t* __restrict__ up_dst) {
+    const double* __restrict__ UH, const int32_t* __restrict__ up_dst) {
   extern __shared__ double smu[];
   const LevelItem it = items[blockIdx.x];
   const BoxRec br = box[it.box];
@@ -186,7 +329,7 @@ __global__ void __launch_bounds__(kDownCols) k3_downward_real(
 __global__ void __launch_bounds__(kDownCols) k3_downward_cplx(
     const LevelItem* __restrict__ items, const BoxRec* __restrict__ box,
     const int64_t* __restrict__ T_off, const double2* __restrict__ T, double2* __restrict__ U,
-    const double2* __restrict__ UH, const int64_t* __restrict__ up_dst) {
+    const double2* __restrict__ UH, const int32_t* __restrict__ up_dst) {
   extern __shared__ double2 smu2[];
   const LevelItem it = items[blockIdx.x];
   const BoxRec br = box[it.box];
@@ -341,7 +484,8 @@ __global__ void k_build_slots(SlotBuildArgs a) {
   if (br.k > 0) {
     const int64_t ps = a.box[a.parent[w]].slot;
     const int64_t off = a.parent_offset[w];
-    for (int32_t i = lane; i < br.k; i += 32) a.up_dst[br.skel + i] = ps + a.posmap[ps + off + i];
+    for (int32_t i = lane; i < br.k; i += 32)
+      a.up_dst[br.skel + i] = (int32_t)(ps + a.posmap[ps + off + i]);
   }
 }
 
@@ -354,10 +498,12 @@ __global__ void k_build_leaf_maps(SlotBuildArgs a) {
   if (w >= a.n_leaves) return;
   const BoxRec br = a.box[a.leaf_box[w]];
   const int64_t out = a.leaf_out[w], begin = a.leaf_begin[w];
+  const bool copy = a.leaf_copy[w] != 0;
   for (int32_t p = lane; p < br.n; p += 32) {
     const int32_t j = a.posmap[br.slot + p];
-    a.leaf_slot[out + j] = br.slot + j;
+    a.leaf_slot[out + j] = (int32_t)(br.slot + j);
     a.leaf_orig[out + j] = a.perm[begin + p];
+    a.leaf_hat[out + j] = copy ? (int32_t)(br.skel + j) : -1;
   }
 }
 
@@ -371,21 +517,25 @@ int grid_for(int64_t n, int threads) {
 void launch_gather(const DevPlan& p, const double* q, DevState& s, cudaStream_t st) {
   const int g = grid_for(p.n_owned_points, 256);
   if (p.cplx)
-    k0_gather<double2><<<g, 256, 0, st>>>(p.leaf_slot, p.leaf_orig, p.n_owned_points,
-                                          reinterpret_cast<const double2*>(q),
-                                          reinterpret_cast<double2*>(s.Q));
+    k0_gather<double2><<<g, 256, 0, st>>>(p.leaf_slot, p.leaf_orig, p.leaf_hat, p.up_dst,
+                                          p.n_owned_points, reinterpret_cast<const double2*>(q),
+                                          reinterpret_cast<double2*>(s.Q),
+                                          reinterpret_cast<double2*>(s.QH));
   else
-    k0_gather<double><<<g, 256, 0, st>>>(p.leaf_slot, p.leaf_orig, p.n_owned_points, q, s.Q);
+    k0_gather<double><<<g, 256, 0, st>>>(p.leaf_slot, p.leaf_orig, p.leaf_hat, p.up_dst,
+                                         p.n_owned_points, q, s.Q, s.QH);
 }
 
 void launch_scatter(const DevPlan& p, const DevState& s, double* u, cudaStream_t st) {
   const int g = grid_for(p.n_owned_points, 256);
   if (p.cplx)
-    k4_scatter<double2><<<g, 256, 0, st>>>(p.leaf_slot, p.leaf_orig, p.n_owned_points,
-                                           reinterpret_cast<const double2*>(s.U),
+    k4_scatter<double2><<<g, 256, 0, st>>>(p.leaf_slot, p.leaf_orig, p.leaf_hat, p.up_dst,
+                                           p.n_owned_points, reinterpret_cast<const double2*>(s.U),
+                                           reinterpret_cast<const double2*>(s.UH),
                                            reinterpret_cast<double2*>(u));
   else
-    k4_scatter<double><<<g, 256, 0, st>>>(p.leaf_slot, p.leaf_orig, p.n_owned_points, s.U, u);
+    k4_scatter<double><<<g, 256, 0, st>>>(p.leaf_slot, p.leaf_orig, p.leaf_hat, p.up_dst,
+                                          p.n_owned_points, s.U, s.UH, u);
 }
 
 void launch_upward(const DevPlan& p, const HostPlan& hp, int level, DevState& s,
@@ -406,6 +556,9 @@ void launch_upward(const DevPlan& p, const HostPlan& hp, int level, DevState& s,
     k1_upward_cplx<<<(unsigned)(i1 - i0), kUpThreads, p.up_smem, st>>>(
         p.up1_items + i0, p.box, p.T_off, reinterpret_cast<const double2*>(p.T),
         reinterpret_cast<double2*>(s.Q), reinterpret_cast<double2*>(s.QH), p.up_dst);
+  else if (p.k1_bulk)
+    k1_upward_real_bulk<<<(unsigned)(i1 - i0), kUpThreads, p.up_bulk_smem, st>>>(
+        p.up1_items + i0, p.box, p.T_off, p.T, s.Q, s.QH, p.up_dst);
   else
     k1_upward_real<<<(unsigned)(i1 - i0), kUpThreads, p.up_smem, st>>>(
         p.up1_items + i0, p.box, p.T_off, p.T, s.Q, s.QH, p.up_dst);
@@ -562,6 +715,16 @@ int configure_tree_kernels(DevPlan& p, size_t max_r, size_t max_k) {
       cudaFuncSetAttribute(p.cplx ? (const void*)k1_upward_cplx : (const void*)k1_upward_real,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.up_smem) != cudaSuccess)
     return -1;
+  // real K1 through the bulk-copy ring when every T row fits one stage
+  p.k1_bulk = 0;
+  if (!p.cplx && max_r <= (size_t)kK1MaxR && !std::getenv("SFMM_K1_BULK_OFF")) {
+    p.up_bulk_smem = 128 + (size_t)kK1Stages * kK1StageBytes + ((max_r * 8 + 15) & ~(size_t)15);
+    if (cudaFuncSetAttribute((const void*)k1_upward_real_bulk,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)p.up_bulk_smem) != cudaSuccess)
+      return -1;
+    p.k1_bulk = 1;
+  }
   p.down_smem = std::max<size_t>(max_k * sw, 16);
   if (p.down_smem > 48 * 1024) {
     if (cudaFuncSetAttribute(

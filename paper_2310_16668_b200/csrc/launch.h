@@ -31,9 +31,13 @@ struct DevPlan {
   int64_t n_interior;  // tasks[0, n_interior) read no ghost box
   double *X, *Y, *Z;
   int32_t* slot_id;
-  int64_t* up_dst;
-  int64_t* leaf_slot;
-  int32_t* leaf_orig;
+  int32_t* up_dst;     // skeleton entry -> slot of the same point in the parent
+  int32_t* leaf_slot;  // owned point (slot order) -> slot
+  int32_t* leaf_orig;  // owned point -> original index
+  // owned point of an uncompressed leaf (k = n, level >= 2) -> its skeleton
+  // entry, else -1: K0 / K4 then also do that leaf's qhat copy / uhat fold
+  // (the leaf-level k1_copy / k3_copy fused into the gather / scatter)
+  int32_t* leaf_hat;
   double* T;
   int64_t* T_off;
   double2* sc_tab;  // (cos, sin)(k pi/128), 256 entries (fastmath.cuh)
@@ -70,9 +74,11 @@ struct DevPlan {
   int k2_grid;      // persistent K2 CTAs
   int k2_r1 = 0;    // every K2 task has <= 32 rows: the 64-register R = 1 kernel
   size_t up_smem, down_smem;
+  int k1_bulk = 0;          // real K1 stages T through cp.async.bulk (k1_upward_real_bulk)
+  size_t up_bulk_smem = 0;
 };
 
-// K0: Q[leaf_slot[t]] = q[leaf_orig[t]]
+// K0: Q[leaf_slot[t]] = q[leaf_orig[t]] (+ the uncompressed leaves' qhat copy)
 void launch_gather(const DevPlan& p, const double* q, DevState& s, cudaStream_t st);
 // K1: one tree level of the upward pass (level >= 2)
 void launch_upward(const DevPlan& p, const HostPlan& hp, int level, DevState& s, cudaStream_t st);
@@ -119,9 +125,11 @@ struct SlotBuildArgs {
   const int32_t* perm;          // n_points
   double *X, *Y, *Z;
   int32_t* slot_id;
-  int64_t* up_dst;
-  int64_t* leaf_slot;
+  int32_t* up_dst;
+  int32_t* leaf_slot;
   int32_t* leaf_orig;
+  int32_t* leaf_hat;
+  const uint8_t* leaf_copy;     // owned leaf is uncompressed (its copies fused into K0/K4)
 };
 void launch_build_slots(const SlotBuildArgs& a, cudaStream_t st);
 

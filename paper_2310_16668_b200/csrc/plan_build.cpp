@@ -408,6 +408,10 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
           hp.leaf_box.push_back(b);
           hp.leaf_begin.push_back(d.box_begin[b]);
           hp.leaf_out.push_back(hp.leaf_out.back() + hp.box[b].n);
+          // uncompressed leaf (k = n, level >= 2): its qhat copy / uhat fold
+          // run inside K0 / K4 (the single-RHS k1_copy / k3_copy skip it)
+          hp.leaf_copy.push_back(d.box_level[b] >= 2 && hp.box[b].k > 0 &&
+                                 hp.box[b].k == hp.box[b].n);
         }
       hp.n_owned_points = hp.leaf_out.back();
     }
@@ -887,8 +891,9 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
           for (int32_t i = 0; i < k; i += kUpRows) hp.up_items.push_back({b, i});
           // one K3m item even when r == 0: it also folds uhat into the skeleton slots
           for (int32_t j = 0; j < std::max(r, 1); j += kDownColsM) hp.down_m_items.push_back({b, j});
-          if (r == 0) {  // uncompressed: copies only (warp per box, k1_copy / k3_copy)
-            hp.copy_boxes.push_back(b);
+          if (r == 0) {  // uncompressed: copies only (warp per box, k1_copy / k3_copy;
+                         // leaves: fused into K0 / K4)
+            if (!d.box_leaf[b]) hp.copy_boxes.push_back(b);
             continue;
           }
           for (int32_t i = 0; i < k; i += kUpRows1) hp.up1_items.push_back({b, i});

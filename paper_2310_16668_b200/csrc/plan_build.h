@@ -58,6 +58,7 @@ struct HostPlan {
   // owned leaves: box, first tree-order point, offset into leaf_slot/leaf_orig
   std::vector<int32_t> leaf_box;
   std::vector<int64_t> leaf_begin, leaf_out;  // leaf_out: leaf_box.size() + 1
+  std::vector<uint8_t> leaf_copy;             // per owned leaf: uncompressed (k = n, level >= 2)
   // translation CSR and tasks
   std::vector<EntryRange> ent_range;
   std::vector<int32_t> entries;               // (src box << kModeBits) | mode

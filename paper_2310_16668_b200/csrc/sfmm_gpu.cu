@@ -87,9 +87,13 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
       dp.Y = p->alloc<double>(hp.n_slots);
       dp.Z = p->alloc<double>(hp.n_slots);
       dp.slot_id = p->alloc<int32_t>(hp.n_slots);
-      dp.up_dst = p->alloc<int64_t>(hp.n_skel);
-      dp.leaf_slot = p->alloc<int64_t>(hp.n_owned_points);
+      // slot indices are int32 on the device (12 B of maps per point in K0/K4)
+      if (hp.n_slots >= (int64_t)INT32_MAX)
+        throw CudaFail{SFMM_EUNSUPPORTED, "more than 2^31 slots in one plan: shard it"};
+      dp.up_dst = p->alloc<int32_t>(hp.n_skel);
+      dp.leaf_slot = p->alloc<int32_t>(hp.n_owned_points);
       dp.leaf_orig = p->alloc<int32_t>(hp.n_owned_points);
+      dp.leaf_hat = p->alloc<int32_t>(hp.n_owned_points);
       {
         TmpDev tmp;
         SlotBuildArgs a{};
@@ -104,6 +108,7 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
         a.leaf_box = tmp.up(hp.leaf_box.data(), hp.leaf_box.size());
         a.leaf_begin = tmp.up(hp.leaf_begin.data(), hp.leaf_begin.size());
         a.leaf_out = tmp.up(hp.leaf_out.data(), hp.leaf_out.size());
+        a.leaf_copy = tmp.up(hp.leaf_copy.data(), hp.leaf_copy.size());
         a.n_leaves = (int64_t)hp.leaf_box.size();
         a.perm = tmp.up(desc->perm, (size_t)hp.n_points);
         a.X = dp.X;
@@ -113,6 +118,7 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
         a.up_dst = dp.up_dst;
         a.leaf_slot = dp.leaf_slot;
         a.leaf_orig = dp.leaf_orig;
+        a.leaf_hat = dp.leaf_hat;
         launch_build_slots(a, p->stream);
         ck(cudaGetLastError(), "build slots");
         ck(cudaStreamSynchronize(p->stream), "build slots");
@@ -138,7 +144,8 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
         dp.log_tab = p->upload(lt);
       }
       // interpolation operators of the owned boxes, copied run by run
-      dp.T = p->alloc<double>((size_t)hp.T_off[hp.n_boxes] * sw);
+      // (+2: K1's bulk copies round each row range out to 16-byte boundaries)
+      dp.T = p->alloc<double>((size_t)hp.T_off[hp.n_boxes] * sw + 2);
       // device operators may still be in flight on another stream (a pack on
       // the legacy stream, an NCCL receive): the plan's stream is non-blocking.
       // They may live on another device (sfmm_gpu_plan_create_multi_skel):
