@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(kUpThreads) k1_upward_real(
 // eight warps reduce rows from shared memory.  Up to 3 x 32 KB are in flight
 // per CTA (two CTAs per SM) with no registers held for them -- the HBM
 // stream K1 is bound by (8 B per T entry).
-constexpr int kK1Stages = 3;
+constexpr int kK1Stages = 4;
 constexpr int kK1StageBytes = 32 * 1024;
 constexpr int kK1MaxR = (kK1StageBytes - 16) / 8;  // longest row one stage holds
 
@@ -153,69 +153,114 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-__global__ void __launch_bounds__(kUpThreads) k1_upward_real_bulk(
-    const LevelItem* __restrict__ items, const BoxRec* __restrict__ box,
+// Persistent and warp-specialized: CTA g takes items g, g + grid, ...; each
+// item (box, 64-row slice) is cut into jobs of up to rows_ps rows whose T rows
+// (contiguous) and the box's q_R arrive together in one ring stage.  A
+// producer warp (one lane) walks the job list, waits for a stage to be freed
+// (`empty` mbarrier, one arrival per consumer warp), publishes the job's
+// geometry in shared memory and issues the bulk copies onto the stage's
+// `full` mbarrier; eight consumer warps wait on `full`, reduce the rows from
+// shared memory and free the stage.  The producer's metadata loads overlap
+// the consumers' work, so the copy engine always has kK1Stages jobs queued.
+struct K1Meta {
+  int row0, nr, r, qo, to;  // first row, rows, row length, q_R / T offsets in the stage
+  int pad;
+  int64_t slot, skel;
+};
+constexpr int kK1Consumers = kUpThreads / 32;        // 8 consumer warps
+constexpr int kK1BulkThreads = kUpThreads + 32;       // + 1 producer warp
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__global__ void __launch_bounds__(kK1BulkThreads, 1) k1_upward_real_bulk(
+    const LevelItem* __restrict__ items, int64_t n_items, const BoxRec* __restrict__ box,
     const int64_t* __restrict__ T_off, const double* __restrict__ T, double* __restrict__ Q,
-    double* __restrict__ QH, const int32_t* __restrict__ up_dst) {
+    double* __restrict__ QH, const int32_t* __restrict__ up_dst, int qr_cap) {
   extern __shared__ __align__(128) unsigned char k1sm[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(k1sm);                       // kK1Stages
-  double* stage = reinterpret_cast<double*>(k1sm + 128);                    // kK1Stages x 32 KB
-  double* qR = reinterpret_cast<double*>(k1sm + 128 + kK1Stages * kK1StageBytes);
-  const LevelItem it = items[blockIdx.x];
-  const BoxRec br = box[it.box];
-  const int k = br.k, r = br.n - br.k;
-  const int i0 = it.first, i1 = min(it.first + kUpRows1, k);
-  const int rows_ps = max(1, min(i1 - i0, kK1MaxR / r));  // rows per stage
-  const int nch = (i1 - i0 + rows_ps - 1) / rows_ps;
-  const double* base = T + T_off[it.box] + (int64_t)i0 * r;
-  // chunk c: rows [i0 + c rows_ps, ...), copied from the 16-byte boundary at or
-  // below its first element (o = 0 or 1 leading element), size rounded up
-  auto issue = [&](int c) {
-    const int st = c % kK1Stages;
-    const int nr = min(rows_ps, i1 - i0 - c * rows_ps);
-    const double* src = base + (int64_t)c * rows_ps * r;
-    const int o = (int)((reinterpret_cast<uintptr_t>(src) >> 3) & 1);
-    const uint32_t bytes = (uint32_t)(((o + nr * r) * 8 + 15) & ~15);
-    mbar_expect_tx(&full[st], bytes);
-    bulk_g2s(stage + st * (kK1StageBytes / 8), src - o, bytes, &full[st]);
-  };
+  uint64_t* full = reinterpret_cast<uint64_t*>(k1sm);
+  uint64_t* empty = full + kK1Stages;
+  K1Meta* meta = reinterpret_cast<K1Meta*>(k1sm + 128);
+  double* ring = reinterpret_cast<double*>(k1sm + 128 + 64 * kK1Stages);
+  const int stage_d = qr_cap + kK1StageBytes / 8;  // doubles per stage: [q_R | T rows]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int sidx = 0; sidx < kK1Stages; ++sidx) mbar_init(&full[sidx], 1);
+    for (int st = 0; st < kK1Stages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], kK1Consumers);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int c = 0; c < min(nch, kK1Stages); ++c) issue(c);
   }
-  for (int j = threadIdx.x; j < r; j += blockDim.x) qR[j] = Q[br.slot + k + j];
   __syncthreads();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int c = 0; c < nch; ++c) {
-    const int st = c % kK1Stages;
-    mbar_wait(&full[st], (uint32_t)((c / kK1Stages) & 1));
-    const double* src = base + (int64_t)c * rows_ps * r;
-    const int o = (int)((reinterpret_cast<uintptr_t>(src) >> 3) & 1);
-    const double* Ts = stage + st * (kK1StageBytes / 8) + o;
-    const int nr = min(rows_ps, i1 - i0 - c * rows_ps);
-    for (int m = w; m < nr; m += kUpThreads / 32) {
-      const double* row = Ts + m * r;
-      double a0 = 0.0, a1 = 0.0;
-      int j = lane;
-      for (; j + 32 < r; j += 64) {
-        a0 = fma(row[j], qR[j], a0);
-        a1 = fma(row[j + 32], qR[j + 32], a1);
-      }
-      if (j < r) a0 = fma(row[j], qR[j], a0);
-      const double sum = warp_sum(a0 + a1);
-      if (lane == 0) {
-        const int i = i0 + c * rows_ps + m;
-        const double v = Q[br.slot + i] + sum;
-        QH[br.skel + i] = v;
-        Q[up_dst[br.skel + i]] = v;
+  if (warp == kK1Consumers) {  // ---- producer ----
+    if (lane != 0) return;
+    int job = 0;
+    for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const LevelItem it = items[item];
+      const BoxRec br = box[it.box];
+      const int r = br.n - br.k;
+      const int i0 = it.first, i1 = min(it.first + kUpRows1, br.k);
+      const int rows_ps = max(1, min(i1 - i0, kK1MaxR / r));
+      const double* qs = Q + br.slot + br.k;
+      const int oq = (int)((reinterpret_cast<uintptr_t>(qs) >> 3) & 1);
+      const uint32_t bq = (uint32_t)(((oq + r) * 8 + 15) & ~15);
+      const double* tb = T + T_off[it.box];
+      for (int row0 = i0; row0 < i1; row0 += rows_ps, ++job) {
+        const int st = job % kK1Stages;
+        if (job >= kK1Stages) mbar_wait(&empty[st], (uint32_t)(((job / kK1Stages) - 1) & 1));
+        const int nr = min(rows_ps, i1 - row0);
+        const double* ts = tb + (int64_t)row0 * r;
+        const int ot = (int)((reinterpret_cast<uintptr_t>(ts) >> 3) & 1);
+        const uint32_t bt = (uint32_t)(((ot + nr * r) * 8 + 15) & ~15);
+        meta[st] = K1Meta{row0, nr, r, oq, qr_cap + ot, 0, br.slot, br.skel};
+        double* dst = ring + (int64_t)st * stage_d;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&full[st], bq + bt);
+        bulk_g2s(dst, qs - oq, bq, &full[st]);
+        bulk_g2s(dst + qr_cap, ts - ot, bt, &full[st]);
       }
     }
-    __syncthreads();  // stage st fully read
-    if (threadIdx.x == 0 && c + kK1Stages < nch) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(c + kK1Stages);
+    // end marker: an empty job (nr = 0) released by a plain arrive
+    const int st = job % kK1Stages;
+    if (job >= kK1Stages) mbar_wait(&empty[st], (uint32_t)(((job / kK1Stages) - 1) & 1));
+    meta[st].nr = 0;
+    mbar_arrive(&full[st]);
+    return;
+  }
+  // ---- consumers ----
+  for (int job = 0;; ++job) {
+    const int st = job % kK1Stages;
+    mbar_wait(&full[st], (uint32_t)((job / kK1Stages) & 1));
+    const K1Meta m = meta[st];
+    if (m.nr == 0) break;
+    const double* stg = ring + (int64_t)st * stage_d;
+    const double* qR = stg + m.qo;
+    const double* Ts = stg + m.to;
+    const int r = m.r;
+    for (int m0 = warp * kUpRowsPerWarp; m0 < m.nr; m0 += kK1Consumers * kUpRowsPerWarp) {
+      double acc[kUpRowsPerWarp];
+#pragma unroll
+      for (int u = 0; u < kUpRowsPerWarp; ++u) acc[u] = 0.0;
+      for (int j = lane; j < r; j += 32) {
+        const double qj = qR[j];
+#pragma unroll
+        for (int u = 0; u < kUpRowsPerWarp; ++u)
+          acc[u] = fma(Ts[min(m0 + u, m.nr - 1) * r + j], qj, acc[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < kUpRowsPerWarp; ++u) {
+        const double sum = warp_sum(acc[u]);
+        if (lane == 0 && m0 + u < m.nr) {
+          const int i = m.row0 + m0 + u;
+          const double v = Q[m.slot + i] + sum;
+          QH[m.skel + i] = v;
+          Q[up_dst[m.skel + i]] = v;
+        }
+      }
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
   }
 }
 
@@ -557,8 +602,9 @@ void launch_upward(const DevPlan& p, const HostPlan& hp, int level, DevState& s,
         p.up1_items + i0, p.box, p.T_off, reinterpret_cast<const double2*>(p.T),
         reinterpret_cast<double2*>(s.Q), reinterpret_cast<double2*>(s.QH), p.up_dst);
   else if (p.k1_bulk)
-    k1_upward_real_bulk<<<(unsigned)(i1 - i0), kUpThreads, p.up_bulk_smem, st>>>(
-        p.up1_items + i0, p.box, p.T_off, p.T, s.Q, s.QH, p.up_dst);
+    k1_upward_real_bulk<<<(unsigned)std::min<int64_t>(i1 - i0, p.k1_bulk_grid), kK1BulkThreads,
+                          p.up_bulk_smem, st>>>(p.up1_items + i0, i1 - i0, p.box, p.T_off, p.T,
+                                                s.Q, s.QH, p.up_dst, p.up_bulk_qr);
   else
     k1_upward_real<<<(unsigned)(i1 - i0), kUpThreads, p.up_smem, st>>>(
         p.up1_items + i0, p.box, p.T_off, p.T, s.Q, s.QH, p.up_dst);
@@ -715,14 +761,21 @@ int configure_tree_kernels(DevPlan& p, size_t max_r, size_t max_k) {
       cudaFuncSetAttribute(p.cplx ? (const void*)k1_upward_cplx : (const void*)k1_upward_real,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.up_smem) != cudaSuccess)
     return -1;
-  // real K1 through the bulk-copy ring when every T row fits one stage
+  // real K1 through the bulk-copy ring (opt-in A/B: SFMM_K1_BULK=1; measured
+  // slower than the register stream) when every T row fits a stage
   p.k1_bulk = 0;
-  if (!p.cplx && max_r <= (size_t)kK1MaxR && !std::getenv("SFMM_K1_BULK_OFF")) {
-    p.up_bulk_smem = 128 + (size_t)kK1Stages * kK1StageBytes + ((max_r * 8 + 15) & ~(size_t)15);
+  if (!p.cplx && max_r <= (size_t)kK1MaxR && std::getenv("SFMM_K1_BULK")) {
+    p.up_bulk_qr = (int)(((max_r + 2) + 1) & ~(size_t)1);  // q_R doubles per stage (16-byte multiple)
+    p.up_bulk_smem = 128 + 64 * kK1Stages +
+                     (size_t)kK1Stages * ((size_t)kK1StageBytes + 8 * (size_t)p.up_bulk_qr);
     if (cudaFuncSetAttribute((const void*)k1_upward_real_bulk,
                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)p.up_bulk_smem) != cudaSuccess)
       return -1;
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    p.k1_bulk_grid = sms;  // one persistent CTA per SM (the ring takes ~160 KB)
     p.k1_bulk = 1;
   }
   p.down_smem = std::max<size_t>(max_k * sw, 16);

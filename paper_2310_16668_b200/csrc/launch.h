@@ -76,6 +76,8 @@ struct DevPlan {
   size_t up_smem, down_smem;
   int k1_bulk = 0;          // real K1 stages T through cp.async.bulk (k1_upward_real_bulk)
   size_t up_bulk_smem = 0;
+  int up_bulk_qr = 0;       // q_R doubles per ring stage
+  int k1_bulk_grid = 148;   // persistent CTAs (one per SM)
 };
 
 // K0: Q[leaf_slot[t]] = q[leaf_orig[t]] (+ the uncompressed leaves' qhat copy)

@@ -357,16 +357,16 @@ def test_sync_apply_on_device_buffers():
 @pytest.mark.parametrize("dist,tol,leaf", [("cube", 1e-6, 128), ("sphere", 1e-8, 64),
                                            ("gaussian", 1e-8, 40)])
 def test_k1_bulk_copy_path_matches_register_path(dist, tol, leaf, monkeypatch):
-    """The real K1 stages T through cp.async.bulk into a shared-memory ring;
-    the register-load kernel (SFMM_K1_BULK_OFF) must give the same result up
-    to the summation order, and both must match the reference."""
+    """The opt-in real K1 that stages T through cp.async.bulk into a
+    shared-memory ring (SFMM_K1_BULK=1) gives the register-load kernel's
+    result up to the summation order, and both match the reference."""
     n = 120000
     pts = host.generate_points(dist, n, 3)
     d = ref_descriptor(1, pts, leaf, tol)
     q = host.generate_charges(n, 4)
-    u_bulk = api.fmm_apply(api.GpuPlan(d), q)
-    monkeypatch.setenv("SFMM_K1_BULK_OFF", "1")
     u_reg = api.fmm_apply(api.GpuPlan(d), q)
+    monkeypatch.setenv("SFMM_K1_BULK", "1")
+    u_bulk = api.fmm_apply(api.GpuPlan(d), q)
     assert rel_l2(u_bulk, u_reg) <= 1e-14
     rp = po.RefPipeline.from_desc(d)
     u_ref, _ = rp.apply(q)
