@@ -655,14 +655,6 @@ def main():
         run_sharded(args, ws, rank, local)
         return
     devices = [int(x) for x in args.devices.split(",")] if args.devices else None
-    if args.n > 6e7 and not devices:
-        # ~1.3 kB of resident plan per point: N=1e8 needs more than one B200 --
-        # config 5 is a 2/4/8-GPU sharded run
-        emit({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": 1,
-              "config": workload_config(args),
-              "unavailable": "the resident plan exceeds one B200's HBM at this N; run it sharded "
-                             "(torchrun --nproc-per-node 2/4/8 bench.py --gpus N --config c5)"})
-        return
 
     import torch
     from paper_2310_16668_b200 import api, host
@@ -680,12 +672,20 @@ def main():
     torch.zeros(1, device=f"cuda:{dev}")  # CUDA context up front, not inside the tree build time
     torch.cuda.synchronize(dev)
     # GPU precompute keeps T in HBM: the plan takes it device-to-device
-    hp = host.HostPlan.build_gpu(kern, pts, args.leaf, args.tol, args.kappa, device=dev,
-                                 host_T=False)
-    hinfo = hp.info()
-    t0 = time.perf_counter()
-    plan = api.GpuPlan.from_host(hp, device=dev, devices=devices)
-    t_upload = time.perf_counter() - t0
+    try:
+        hp = host.HostPlan.build_gpu(kern, pts, args.leaf, args.tol, args.kappa, device=dev,
+                                     host_T=False)
+        hinfo = hp.info()
+        t0 = time.perf_counter()
+        plan = api.GpuPlan.from_host(hp, device=dev, devices=devices)
+        t_upload = time.perf_counter() - t0
+    except MemoryError as e:
+        # the operators alone are ~1 kB per point (N=1e8: ~97 GB); larger N is
+        # a sharded run (torchrun --nproc-per-node 2/4/8 bench.py --gpus N)
+        emit({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": 1,
+              "config": workload_config(args),
+              "unavailable": f"the plan does not fit one B200 at this N ({e}); run it sharded"})
+        return
     info = plan.info()
 
     dtype = torch.complex128 if cplx else torch.float64
@@ -823,6 +823,8 @@ def main():
                         f"one process, plan sharded over devices {devices} (peer-copy exchanges "
                         "inside the library)"),
         "resident_plan_gb": info.device_bytes / 1e9,
+        "sym_staging": {"layout": "chained per pair" if info.sym_chain else "per row tile",
+                        "gb": info.stage_bytes / 1e9},
         "roofline": roof,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": bytes_col,
                 "d2h_bytes_per_step": bytes_col, "ms_per_step": t_e2e * 1e3,

@@ -133,6 +133,9 @@ typedef struct sfmm_gpu_plan_info {
   int64_t n_ifo_pairs, n_ifs_pairs, n_tfo_pairs, n_level1_pairs;
   int32_t launches_per_apply; /* kernels of this library launched by one single-RHS apply (this rank) */
   int32_t k2_grid;            /* persistent CTAs of the translation kernel */
+  int32_t sym_chain;          /* 1: symmetric column sums chained per pair (low-memory layout,
+                                 chosen when the per-tile staging would not fit) */
+  int64_t stage_bytes;        /* column-sum staging of the symmetric colleague blocks */
 } sfmm_gpu_plan_info;
 
 typedef struct sfmm_gpu_plan sfmm_gpu_plan;

@@ -96,6 +96,8 @@ class PlanInfo(C.Structure):
         ("n_level1_pairs", C.c_int64),
         ("launches_per_apply", C.c_int32),
         ("k2_grid", C.c_int32),
+        ("sym_chain", C.c_int32),
+        ("stage_bytes", C.c_int64),
     ]
 
 

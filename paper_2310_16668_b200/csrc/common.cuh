@@ -49,8 +49,8 @@ struct Task {
   int32_t box;
   int32_t row0;
   int32_t nrows;
-  int32_t pad;
-  int64_t stage;  // first staging slot of this task's kSYM column sums
+  int32_t tile;   // row-tile index within the box (chained kSYM column sums), -1: unchained
+  int64_t stage;  // first staging slot of the box's kSYM column sums
 };
 
 struct EntryRange {

@@ -55,6 +55,7 @@ struct K2Args {
   int* err;
   double kappa;
   double* St;  // staging for kSYM column sums (unscaled)
+  unsigned* sflag;  // per 32 staged scalars: row tiles of the box that have added (chaining)
   const double2* tab;  // (cos, sin)(k pi/128), Helmholtz only
   const double* ltab;  // log table (fastmath.cuh), Laplace 2D only
 };
@@ -111,6 +112,8 @@ struct WarpSmemReal {
   double2 xy[32];
   double2 za[32];  // z, a-weight
   double h[32];
+  unsigned* fbase;  // chain flags of the current kSYM entry (kept out of registers)
+  int tile;
 };
 
 struct WarpSmemCplx {
@@ -118,7 +121,51 @@ struct WarpSmemCplx {
   double z[32];
   double2 a[32];
   double2 h[32];
+  unsigned* fbase;
+  int tile;
 };
+
+// Chained kSYM column sums: the row tiles of a box add their column sums of a
+// pair (b, c) into ONE staged vector, in tile order.  Tile t waits until the
+// chunk's flag says t tiles have added, adds its partial sums to the staged
+// ones (read through L2), stores, and publishes t + 1.  Tiles of one box are
+// claimed from the task counter in tile order (plan_build.cpp keeps them in
+// that order), so tile t - 1 is always running or done: no circular wait.
+// The order of the additions is fixed, so results stay deterministic.
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ double add_s(double a, double b) { return a + b; }
+__device__ __forceinline__ double2 add_s(double2 a, double2 b) {
+  return make_double2(a.x + b.x, a.y + b.y);
+}
+template <class S, bool H, bool CHAIN>
+__device__ __forceinline__ void chain_store(S* st_u, S* st_h, S cp, S ch, int col, int n_c,
+                                            int k_c, const unsigned* const* fbase, const int* tilep,
+                                            int j0, int lane) {
+  if constexpr (!CHAIN) {  // per-tile layout: this tile's own staged vector
+    if (col < n_c) st_u[col] = cp;
+    if (H && col < k_c) st_h[col] = ch;
+    return;
+  }
+  unsigned* flag = const_cast<unsigned*>(*fbase) + (j0 >> 5);
+  const int tile = *tilep;
+  if (tile > 0) {
+    while (ld_acquire_u32(flag) < (unsigned)tile) __nanosleep(32);
+    if (col < n_c) cp = add_s(__ldcg(st_u + col), cp);
+    if (H && col < k_c) ch = add_s(__ldcg(st_h + col), ch);
+  }
+  if (col < n_c) __stcg(st_u + col, cp);
+  if (H && col < k_c) __stcg(st_h + col, ch);
+  __threadfence();
+  __syncwarp();
+  if (lane == 0) st_release_u32(flag, (unsigned)tile + 1);
+}
 
 // Exact re-scan of one row for coincident points with distinct ids.
 __device__ __noinline__ void verify_row(const K2Args& a, int32_t b, int32_t row, int dim) {
@@ -172,7 +219,7 @@ __device__ __forceinline__ void inner_real(const WarpSmemReal& sm, uint32_t lt, 
 // the running column sum moves one lane down, so after 32 steps lane l holds
 // the complete sum of column l over the warp's 32R rows.  Fixed order, no
 // butterfly, two column accumulators per lane.
-template <class G, int R, bool H>
+template <class G, int R, bool H, bool CHAIN>
 __device__ __forceinline__ void sym_chunk(const WarpSmemReal& sm, uint32_t lt, int j0, int n_c,
                                           int k_c,
                                           const double (&xi)[R], const double (&yi)[R],
@@ -213,12 +260,11 @@ __device__ __forceinline__ void sym_chunk(const WarpSmemReal& sm, uint32_t lt, i
     cp = __shfl_sync(kFull, cp + cs, from);
     if (H) ch = __shfl_sync(kFull, ch + hs, from);
   }
-  const int col = j0 + lane;
-  if (col < n_c) st_u[col] = cp;
-  if (H && col < k_c) st_h[col] = ch;
+  chain_store<double, H, CHAIN>(st_u, st_h, cp, ch, j0 + lane, n_c, k_c, &sm.fbase, &sm.tile, j0,
+                                lane);
 }
 
-template <class G, int R>
+template <class G, int R, bool CHAIN>
 __device__ __forceinline__ void task_real(const K2Args& a, const Task& t, WarpSmemReal& sm,
                                           uint32_t lt, int lane) {
   const BoxRec tb = a.box[t.box];
@@ -249,6 +295,10 @@ __device__ __forceinline__ void task_real(const K2Args& a, const Task& t, WarpSm
     if (mode == kSYM) {
       double* st_u = a.St + stage;
       double* st_h = st_u + sb.n;
+      if (CHAIN && lane == 0) {
+        sm.fbase = a.sflag + (stage >> 5);
+        sm.tile = t.tile;
+      }
       for (int j0 = 0; j0 < sb.n; j0 += 32) {
         const int j = j0 + lane;
         if (j < sb.n) {
@@ -263,12 +313,15 @@ __device__ __forceinline__ void task_real(const K2Args& a, const Task& t, WarpSm
         }
         __syncwarp();
         if (skel_rows && j0 < sb.k)
-          sym_chunk<G, R, true>(sm, lt, j0, sb.n, sb.k, xi, yi, zi, qr, qhr, au, ah, st_u, st_h, lane);
+          sym_chunk<G, R, true, CHAIN>(sm, lt, j0, sb.n, sb.k, xi, yi, zi, qr, qhr, au, ah, st_u, st_h,
+                                lane);
         else
-          sym_chunk<G, R, false>(sm, lt, j0, sb.n, sb.k, xi, yi, zi, qr, qhr, au, ah, st_u, st_h, lane);
+          sym_chunk<G, R, false, CHAIN>(sm, lt, j0, sb.n, sb.k, xi, yi, zi, qr, qhr, au, ah, st_u, st_h,
+                                 lane);
         __syncwarp();
       }
-      stage += sb.n + ((skel_rows && sb.k > 0) ? sb.k : 0);
+      stage += (sb.n + (((CHAIN ? tb.k > 0 : skel_rows) && sb.k > 0) ? sb.k : 0) + 31) &
+               ~(int64_t)31;
       continue;
     }
     const bool self = c == t.box;
@@ -320,7 +373,7 @@ __device__ __forceinline__ void task_real(const K2Args& a, const Task& t, WarpSm
 #ifndef SFMM_K2_R1_MIN_BLOCKS
 #define SFMM_K2_R1_MIN_BLOCKS 8
 #endif
-template <class G, int MAXR, int MINB>
+template <class G, int MAXR, int MINB, bool CHAIN>
 __global__ void __launch_bounds__(kThreads, MINB) k2_translate_real_t(K2Args a) {
   __shared__ WarpSmemReal smem[kWarps];
   __shared__ __align__(16) double ltab[G::kLogTable ? kLogTabLen : 1];
@@ -338,25 +391,27 @@ __global__ void __launch_bounds__(kThreads, MINB) k2_translate_real_t(K2Args a) 
     if (t >= a.n_tasks) return;
     const Task task = a.tasks[t];
     if constexpr (MAXR == 1) {
-      task_real<G, 1>(a, task, sm, lts, lane);
+      task_real<G, 1, CHAIN>(a, task, sm, lts, lane);
     } else {
       switch ((task.nrows + 31) >> 5) {
-        case 1: task_real<G, 1>(a, task, sm, lts, lane); break;
+        case 1: task_real<G, 1, CHAIN>(a, task, sm, lts, lane); break;
 #if SFMM_K2_MAX_R >= 2
-        case 2: task_real<G, 2>(a, task, sm, lts, lane); break;
+        case 2: task_real<G, 2, CHAIN>(a, task, sm, lts, lane); break;
 #endif
 #if SFMM_K2_MAX_R >= 3
-        case 3: task_real<G, 3>(a, task, sm, lts, lane); break;
+        case 3: task_real<G, 3, CHAIN>(a, task, sm, lts, lane); break;
 #endif
-        default: task_real<G, SFMM_K2_MAX_R>(a, task, sm, lts, lane); break;
+        default: task_real<G, SFMM_K2_MAX_R, CHAIN>(a, task, sm, lts, lane); break;
       }
     }
   }
 }
 template <class G>
-constexpr auto k2_real_kernel(bool r1) {
-  return r1 ? k2_translate_real_t<G, 1, SFMM_K2_R1_MIN_BLOCKS>
-            : k2_translate_real_t<G, SFMM_K2_MAX_R, SFMM_K2_MIN_BLOCKS>;
+constexpr auto k2_real_kernel(bool r1, bool chain) {
+  return chain ? (r1 ? k2_translate_real_t<G, 1, SFMM_K2_R1_MIN_BLOCKS, true>
+                     : k2_translate_real_t<G, SFMM_K2_MAX_R, SFMM_K2_MIN_BLOCKS, true>)
+               : (r1 ? k2_translate_real_t<G, 1, SFMM_K2_R1_MIN_BLOCKS, false>
+                     : k2_translate_real_t<G, SFMM_K2_MAX_R, SFMM_K2_MIN_BLOCKS, false>);
 }
 
 // ---------------------------------------------------------------------------
@@ -418,7 +473,7 @@ __device__ __forceinline__ void inner_cplx(const WarpSmemCplx& sm, const double2
 // kSYM for the complex kernel: as sym_chunk (rotation, fixed order) with
 // complex row and column accumulators; columns past the source box are given
 // G = 0 explicitly (a far-away padding point would make exp(i kappa r) NaN).
-template <int R, bool H, bool TAB>
+template <int R, bool H, bool TAB, bool CHAIN>
 __device__ __forceinline__ void sym_chunk_cplx(const WarpSmemCplx& sm, const double2* __restrict__ tab,
                                                int j0, int n_c, int k_c, double kappa,
                                                const double (&xi)[R], const double (&yi)[R],
@@ -472,12 +527,11 @@ __device__ __forceinline__ void sym_chunk_cplx(const WarpSmemCplx& sm, const dou
       ch.y = __shfl_sync(kFull, ch.y + hs.y, from);
     }
   }
-  const int col = j0 + lane;
-  if (col < n_c) st_u[col] = cp;
-  if (H && col < k_c) st_h[col] = ch;
+  chain_store<double2, H, CHAIN>(st_u, st_h, cp, ch, j0 + lane, n_c, k_c, &sm.fbase, &sm.tile, j0,
+                                 lane);
 }
 
-template <int R, bool TAB>
+template <int R, bool TAB, bool CHAIN>
 __device__ __forceinline__ void task_cplx(const K2Args& a, const Task& t, WarpSmemCplx& sm,
                                           const double2* tab, int lane) {
   const double2* Q = reinterpret_cast<const double2*>(a.Q);
@@ -512,6 +566,10 @@ __device__ __forceinline__ void task_cplx(const K2Args& a, const Task& t, WarpSm
     if (mode == kSYM) {
       double2* st_u = St + stage;
       double2* st_h = st_u + sb.n;
+      if (CHAIN && lane == 0) {
+        sm.fbase = a.sflag + (stage >> 5);
+        sm.tile = t.tile;
+      }
       for (int j0 = 0; j0 < sb.n; j0 += 32) {
         const int j = j0 + lane;
         if (j < sb.n) {
@@ -528,14 +586,15 @@ __device__ __forceinline__ void task_cplx(const K2Args& a, const Task& t, WarpSm
         }
         __syncwarp();
         if (skel_rows && j0 < sb.k)
-          sym_chunk_cplx<R, true, TAB>(sm, tab, j0, sb.n, sb.k, a.kappa, xi, yi, zi, qr, qhr, au,
+          sym_chunk_cplx<R, true, TAB, CHAIN>(sm, tab, j0, sb.n, sb.k, a.kappa, xi, yi, zi, qr, qhr, au,
                                        ah, st_u, st_h, lane);
         else
-          sym_chunk_cplx<R, false, TAB>(sm, tab, j0, sb.n, sb.k, a.kappa, xi, yi, zi, qr, qhr, au,
+          sym_chunk_cplx<R, false, TAB, CHAIN>(sm, tab, j0, sb.n, sb.k, a.kappa, xi, yi, zi, qr, qhr, au,
                                         ah, st_u, st_h, lane);
         __syncwarp();
       }
-      stage += sb.n + ((skel_rows && sb.k > 0) ? sb.k : 0);
+      stage += (sb.n + (((CHAIN ? tb.k > 0 : skel_rows) && sb.k > 0) ? sb.k : 0) + 31) &
+               ~(int64_t)31;
       continue;
     }
     const bool self = c == t.box;
@@ -585,7 +644,7 @@ __device__ __forceinline__ void task_cplx(const K2Args& a, const Task& t, WarpSm
 #ifndef SFMM_K2C_MIN_BLOCKS
 #define SFMM_K2C_MIN_BLOCKS 3
 #endif
-template <bool TAB>
+template <bool TAB, bool CHAIN>
 __global__ void __launch_bounds__(kThreads, SFMM_K2C_MIN_BLOCKS) k2_translate_cplx(K2Args a) {
   __shared__ WarpSmemCplx smem[kWarps];
   __shared__ double2 tab[kSinCosTab];
@@ -601,14 +660,14 @@ __global__ void __launch_bounds__(kThreads, SFMM_K2C_MIN_BLOCKS) k2_translate_cp
     if (t >= a.n_tasks) return;
     const Task task = a.tasks[t];
     switch ((task.nrows + 31) >> 5) {
-      case 1: task_cplx<1, TAB>(a, task, sm, tab, lane); break;
+      case 1: task_cplx<1, TAB, CHAIN>(a, task, sm, tab, lane); break;
 #if SFMM_K2C_MAX_R >= 3
-      case 2: task_cplx<2, TAB>(a, task, sm, tab, lane); break;
+      case 2: task_cplx<2, TAB, CHAIN>(a, task, sm, tab, lane); break;
 #endif
 #if SFMM_K2C_MAX_R >= 4
-      case 3: task_cplx<3, TAB>(a, task, sm, tab, lane); break;
+      case 3: task_cplx<3, TAB, CHAIN>(a, task, sm, tab, lane); break;
 #endif
-      default: task_cplx<SFMM_K2C_MAX_R, TAB>(a, task, sm, tab, lane); break;
+      default: task_cplx<SFMM_K2C_MAX_R, TAB, CHAIN>(a, task, sm, tab, lane); break;
     }
   }
 }
@@ -689,13 +748,14 @@ int configure_translate(DevPlan& p, int device) {
     return -1;
   cudaError_t e;
   if (p.kernel == SFMM_HELMHOLTZ3D)
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_translate_cplx<true>, kThreads, 0);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_translate_cplx<true, false>,
+                                                      kThreads, 0);
   else if (p.kernel == SFMM_LAPLACE3D)
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per_sm, k2_real_kernel<GenLaplace3d>(p.k2_r1), kThreads, 0);
+        &per_sm, k2_real_kernel<GenLaplace3d>(p.k2_r1, p.sym_chain), kThreads, 0);
   else
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per_sm, k2_real_kernel<GenLaplace2d>(p.k2_r1), kThreads, 0);
+        &per_sm, k2_real_kernel<GenLaplace2d>(p.k2_r1, p.sym_chain), kThreads, 0);
   if (e != cudaSuccess) return -1;
   if (per_sm < 1) per_sm = 1;
   p.k2_grid = sms * per_sm;
@@ -709,6 +769,9 @@ void launch_translate(const DevPlan& p, DevState& s, cudaStream_t st, TranslateP
     // boxes whose every entry cancels own no task: their U/UH stay zero
     cudaMemsetAsync(s.U, 0, (size_t)p.n_slots * sw, st);
     cudaMemsetAsync(s.UH, 0, (size_t)p.n_skel * sw, st);
+    // chained kSYM column sums start from "no tile has added"
+    if (p.stage_size > 0)
+      cudaMemsetAsync(p.stage_flags, 0, sizeof(unsigned) * (size_t)(p.stage_size >> 5), st);
   }
   int64_t t0 = 0, t1 = p.n_tasks;
   int* counter = p.counter;
@@ -738,17 +801,20 @@ void launch_translate(const DevPlan& p, DevState& s, cudaStream_t st, TranslateP
     a.tab = p.sc_tab;
     a.ltab = p.log_tab;
     a.St = p.stage;
+    a.sflag = p.stage_flags;
     cudaMemsetAsync(counter, 0, sizeof(int), st);
     const int grid = (int)std::min<int64_t>(p.k2_grid, (t1 - t0 + kWarps - 1) / kWarps);
-    if (p.kernel == SFMM_HELMHOLTZ3D)
-      if (p.sc_tab_ok)
-        k2_translate_cplx<true><<<grid, kThreads, 0, st>>>(a);
-      else
-        k2_translate_cplx<false><<<grid, kThreads, 0, st>>>(a);
-    else if (p.kernel == SFMM_LAPLACE3D)
-      k2_real_kernel<GenLaplace3d>(p.k2_r1)<<<grid, kThreads, 0, st>>>(a);
-    else
-      k2_real_kernel<GenLaplace2d>(p.k2_r1)<<<grid, kThreads, 0, st>>>(a);
+    if (p.kernel == SFMM_HELMHOLTZ3D) {
+      auto kc = p.sc_tab_ok ? (p.sym_chain ? k2_translate_cplx<true, true>
+                                           : k2_translate_cplx<true, false>)
+                            : (p.sym_chain ? k2_translate_cplx<false, true>
+                                           : k2_translate_cplx<false, false>);
+      kc<<<grid, kThreads, 0, st>>>(a);
+    } else if (p.kernel == SFMM_LAPLACE3D) {
+      k2_real_kernel<GenLaplace3d>(p.k2_r1, p.sym_chain)<<<grid, kThreads, 0, st>>>(a);
+    } else {
+      k2_real_kernel<GenLaplace2d>(p.k2_r1, p.sym_chain)<<<grid, kThreads, 0, st>>>(a);
+    }
   }
   if (part != kInteriorTasks && reduce) launch_stage_reduce(p, s, st);
 }

@@ -46,7 +46,9 @@ struct DevPlan {
   LevelItem *up_items, *down_items, *up1_items;  // up1: K1 (single rhs), up: K1m
   int32_t* copy_boxes;                            // r = 0 boxes (plan_build.h)
   double* orig_pts;
-  double* stage;    // kSYM column-sum staging (stage_size doubles)
+  double* stage;    // kSYM column-sum staging (stage_size scalars; one vector per pair)
+  unsigned* stage_flags;  // stage_size / 32 chain flags (tiles that have added), zeroed per apply
+  int sym_chain = 0;      // HostPlan::sym_chain: the chained K2 instantiation
   int32_t* recv_box;
   int64_t *recv_off, *recv_u, *recv_h;
   int64_t n_recv;

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <new>
 #include <string>
@@ -93,6 +94,7 @@ struct sfmm_gpu_plan {
   HostPlan hp;
   DevPlan dp{};
   std::vector<void*> allocs;
+  std::shared_ptr<double> T_hold;  // shared operator buffer (create_plan T_share)
   int64_t device_bytes = 0;
   // per-apply state (grown on demand, one column of scalars)
   DevState ds{};
@@ -324,8 +326,13 @@ namespace sfmm_gpu {
 // Builds a device-resident plan (rank `rank` of `n_ranks`) on `device`.
 // T_dev: the descriptor's operators in device memory (any device, global
 // T_off layout), or with T_compact only the owned runs concatenated.
+// T_share: owner of T_dev (a GPU skeletonization result): a single-rank plan
+// whose operator layout is the descriptor's keeps the buffer instead of
+// copying it (skel_share_T).
 int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
-                sfmm_gpu_plan** out, const double* T_dev = nullptr, bool T_compact = false);
+                sfmm_gpu_plan** out, const double* T_dev = nullptr, bool T_compact = false,
+                std::shared_ptr<double> T_share = {});
+std::shared_ptr<double> skel_share_T(const sfmm_skel_result* r);
 
 // Phases of one sharded apply (sfmm_gpu.cu); throw CudaFail.
 void phase_begin(sfmm_gpu_plan* p, const void* q_dev, void* send_dev, void* user_stream,

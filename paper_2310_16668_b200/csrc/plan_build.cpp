@@ -40,11 +40,12 @@ PlanOptions plan_options_from_env() {
   if (const char* v = std::getenv("SFMM_SKIP_CANCEL")) o.skip_cancel = std::atoi(v) != 0;
   if (const char* v = std::getenv("SFMM_SHARD_OVERLAP")) o.overlap = std::atoi(v) != 0;
   if (const char* v = std::getenv("SFMM_SHARD_XSYM")) o.cross_symmetric = std::atoi(v) != 0;
+  if (const char* v = std::getenv("SFMM_SYM_CHAIN")) o.sym_chain = std::atoi(v) != 0;
   return o;
 }
 
 int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int n_ranks,
-                    int rank) {
+                    int rank, int sym_chain) {
   try {
     ParErr perr;
     if (d.kernel == SFMM_HELMHOLTZ2D)
@@ -207,7 +208,8 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
 
     ptime("up_dst");
     // ---- ownership: whole level-1 subtrees per rank ----------
-    const PlanOptions opt = plan_options_from_env();
+    PlanOptions opt = plan_options_from_env();
+    if (sym_chain >= 0) opt.sym_chain = sym_chain != 0;
     std::vector<uint8_t> unc(nb, 0);
     for (int32_t b = 0; b < nb; ++b)
       unc[b] = opt.skip_cancel && d.box_level[b] >= 2 && hp.box[b].n > 0 &&
@@ -431,6 +433,7 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
     // as usual and c's rows receive A_cb q_b = (A_bc)^T q_b as staged column
     // sums.  Pairs across ranks stay kIFO on both sides.
     hp.symmetric = opt.symmetric;
+    hp.sym_chain = opt.sym_chain;
     if (hp.symmetric) {  // the colleague relation must be symmetric (and the lists sorted)
       int asym = 0;
 #pragma omp parallel for schedule(dynamic, 1024) reduction(| : asym)
@@ -728,26 +731,38 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
         xtiles.resize(xpairs.size());
         if (er.count == 0 || hp.box[b].n == 0) continue;
         const double src = src_of[b];
-        for (int32_t r0 = 0; r0 < hp.box[b].n; r0 += tile) {
-          Task t{b, r0, std::min(tile, hp.box[b].n - r0), 0, cursor};
-          const bool skel_rows = r0 < hp.box[b].k;
+        // Staged [u: n_c | h: k_c] vectors of the kSYM pairs (b, c), each on a
+        // 32-scalar boundary (chain flags are offset / 32 + column / 32):
+        // one per (pair, row tile) -- the tile owning skeleton rows carries
+        // the h part -- or, with sym_chain, one per pair shared by all of b's
+        // row tiles, tile t adding to tile t - 1's in tile order.
+        auto stage_entries = [&](bool h_part) {
           size_t xi = x0;
           for (int64_t e = er.begin; e < er.begin + er.count; ++e) {
             const int32_t code = hp.entries[e];
             if ((code & kModeMask) != kSYM) continue;
             const int32_t c = code >> kModeBits;
             const int64_t u_off = cursor;
-            cursor += hp.box[c].n;
             int64_t h_off = -1;
-            if (skel_rows && hp.box[c].k > 0) {
-              h_off = cursor;
-              cursor += hp.box[c].k;
+            int64_t len = hp.box[c].n;
+            if (h_part && hp.box[c].k > 0) {
+              h_off = cursor + hp.box[c].n;
+              len += hp.box[c].k;
             }
+            cursor += (len + 31) & ~(int64_t)31;
             if (mine(c))
               inbox[c].push_back({u_off, h_off});
             else
               xtiles[xi++].push_back({u_off, h_off});
           }
+        };
+        const int64_t b_stage = cursor;
+        if (hp.sym_chain) stage_entries(hp.box[b].k > 0);
+        int32_t tile_index = 0;
+        for (int32_t r0 = 0; r0 < hp.box[b].n; r0 += tile, ++tile_index) {
+          Task t{b, r0, std::min(tile, hp.box[b].n - r0), hp.sym_chain ? tile_index : -1,
+                 hp.sym_chain ? b_stage : cursor};
+          if (!hp.sym_chain) stage_entries(r0 < hp.box[b].k);
           const double lanes_rows = 32.0 * ((t.nrows + 31) / 32);
           // without overlap every task runs in the one launch after the exchange
           ((boundary[b] || !opt.overlap) ? tv_bnd : tv_int).push_back({lanes_rows * (src + 8.0), t});

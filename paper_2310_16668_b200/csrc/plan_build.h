@@ -67,7 +67,8 @@ struct HostPlan {
   // symmetric colleague blocks: staged column sums and, per receiving box,
   // the staging slots to add (u part, and uhat part or -1) in a fixed order
   bool symmetric = false;
-  int64_t stage_size = 0;                     // doubles
+  bool sym_chain = false;                     // PlanOptions::sym_chain
+  int64_t stage_size = 0;                     // scalars, a multiple of 32
   std::vector<int32_t> recv_box;
   std::vector<int64_t> recv_off;              // recv_box.size() + 1
   std::vector<int64_t> recv_u, recv_h;
@@ -125,7 +126,7 @@ struct HostPlan {
 // (1/0: the whole tree).  Returns SFMM_OK or an error code with a message in
 // `err`.
 int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int n_ranks = 1,
-                    int rank = 0);
+                    int rank = 0, int sym_chain = -1 /* -1: SFMM_SYM_CHAIN (default 0) */);
 
 // Plan options (environment SFMM_SYMMETRIC=0 / SFMM_SKIP_CANCEL=0 turn them off
 // for A/B measurements; both default on).
@@ -143,6 +144,12 @@ struct PlanOptions {
   // work), which returns the other side's column sums in a second (smaller)
   // exchange (SFMM_SHARD_XSYM=0: both ranks evaluate it, one exchange).
   bool cross_symmetric = true;
+  // kSYM column sums of a box's row tiles chained into one staged vector per
+  // pair (tile t adds to tile t-1's, in order) instead of one vector per
+  // (pair, row tile): ~2/3 less staging memory at 1e7, but the tiles wait for
+  // each other (K2 +19 % at 1e7), so it is used only when the plan would not
+  // fit otherwise (sfmm_gpu.cu) or on request (SFMM_SYM_CHAIN=1).
+  int sym_chain = 0;
 };
 PlanOptions plan_options_from_env();
 

@@ -35,20 +35,40 @@ namespace sfmm_gpu {
 // T_dev: the descriptor's operators in device memory (global T_off layout), or
 // with T_compact only the owned runs concatenated (sfmm_gpu_shard_T_runs order)
 int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
-                sfmm_gpu_plan** out, const double* T_dev, bool T_compact) {
+                sfmm_gpu_plan** out, const double* T_dev, bool T_compact,
+                std::shared_ptr<double> T_share) {
   if (!desc || !out) return set_error(SFMM_EINVAL, "sfmm_gpu_plan_create: null argument");
   *out = nullptr;
   sfmm_gpu_plan* p = nullptr;
   try {
     p = new sfmm_gpu_plan();
     std::string err;
-    const int rc = build_host_plan(*desc, p->hp, err, n_ranks, rank);
+    int rc = build_host_plan(*desc, p->hp, err, n_ranks, rank);
     if (rc != SFMM_OK) {
       delete p;
       return set_error(rc, err);
     }
     p->device = device;
     DeviceGuard device_guard(device);
+    // Per-tile kSYM staging is the fast layout; when the plan would not fit
+    // the free device memory with it, chain the row tiles' column sums into
+    // one vector per pair instead (PlanOptions::sym_chain, ~2/3 less staging)
+    if (!p->hp.sym_chain && p->hp.stage_size > 0 && !std::getenv("SFMM_SYM_CHAIN")) {
+      size_t free_b = 0, total_b = 0;
+      if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+        const HostPlan& h = p->hp;
+        const double sw = h.cplx ? 2.0 : 1.0;
+        double need = 8.0 * sw * ((double)h.stage_size + 2.0 * h.n_slots + 2.0 * h.n_skel) +
+                      28.0 * h.n_slots + 16.0 * h.n_owned_points + 8.0 * h.n_skel +
+                      24.0 * (double)h.tasks.size() + 4.0 * (double)h.entries.size();
+        if (!(T_dev && !T_compact && n_ranks == 1)) need += 8.0 * sw * (double)h.T_off.back();
+        if (need > 0.92 * (double)free_b) {
+          HostPlan chained;
+          if (build_host_plan(*desc, chained, err, n_ranks, rank, 1) == SFMM_OK)
+            p->hp = std::move(chained);
+        }
+      }
+    }
     ck(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking), "cudaStreamCreate");
     ck(cudaEventCreate(&p->ev_a), "cudaEventCreate");
     ck(cudaEventCreate(&p->ev_b), "cudaEventCreate");
@@ -144,8 +164,20 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
         dp.log_tab = p->upload(lt);
       }
       // interpolation operators of the owned boxes, copied run by run
-      // (+2: K1's bulk copies round each row range out to 16-byte boundaries)
-      dp.T = p->alloc<double>((size_t)hp.T_off[hp.n_boxes] * sw + 2);
+      // A single-rank plan built from device operators in the descriptor's
+      // layout keeps that buffer (shared with the skeletonization result)
+      // instead of copying it: at N = 1e8 the copy alone would need ~96 GB more.
+      bool identity = T_share && T_dev && !T_compact && n_ranks == 1 &&
+                      T_share.get() == T_dev;
+      for (const HostPlan::Run& r : hp.T_runs) identity = identity && r.src == r.dst;
+      if (identity) {
+        p->T_hold = T_share;
+        dp.T = T_share.get();
+        p->device_bytes += (int64_t)(sizeof(double) * hp.T_off[hp.n_boxes] * sw);
+      } else {
+        // (+2: K1's bulk copies round each row range out to 16-byte boundaries)
+        dp.T = p->alloc<double>((size_t)hp.T_off[hp.n_boxes] * sw + 2);
+      }
       // device operators may still be in flight on another stream (a pack on
       // the legacy stream, an NCCL receive): the plan's stream is non-blocking.
       // They may live on another device (sfmm_gpu_plan_create_multi_skel):
@@ -161,11 +193,13 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
       }
       const double* T_src = T_dev ? T_dev : desc->T;
       if (!T_src && !hp.T_runs.empty()) throw CudaFail{SFMM_EINVAL, "descriptor has no T"};
-      for (const HostPlan::Run& r : hp.T_runs)
+      for (const HostPlan::Run& r : hp.T_runs) {
+        if (identity) break;
         ck(cudaMemcpyAsync(dp.T + r.dst * sw, T_src + (T_compact ? r.dst : r.src) * sw,
                            sizeof(double) * r.len * sw,
                            T_dev ? cudaMemcpyDefault : cudaMemcpyHostToDevice, p->stream),
            "upload T");
+      }
       ck(cudaStreamSynchronize(p->stream), "upload T");
       dp.up_items = p->upload(hp.up_items);
       dp.up1_items = p->upload(hp.up1_items);
@@ -173,9 +207,11 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
       dp.down_items = p->upload(hp.down_items);
       const int64_t n_recv2 = hp.recv2_off.empty() ? 0 : hp.recv2_off.back();
       dp.stage_size = hp.stage_size;
+      dp.sym_chain = hp.sym_chain ? 1 : 0;
       dp.n_recv2 = n_recv2;
       dp.n_send2 = hp.send2_off.empty() ? 0 : hp.send2_off.back();
       dp.stage = p->alloc<double>((size_t)std::max<int64_t>(hp.stage_size + n_recv2, 1) * sw);
+      dp.stage_flags = p->alloc<unsigned>((size_t)std::max<int64_t>(hp.stage_size >> 5, 1));
       dp.n_xpairs = (int64_t)hp.xpair_dst.size();
       dp.xpair_tile_off = p->upload(hp.xpair_tile_off);
       dp.xtile_u = p->upload(hp.xtile_u);
@@ -352,7 +388,7 @@ int sfmm_gpu_plan_create_skel(const sfmm_plan_desc* desc, const sfmm_skel_result
   const int sw = desc->kernel == SFMM_HELMHOLTZ3D || desc->kernel == SFMM_HELMHOLTZ2D ? 2 : 1;
   if (!desc->T_off || desc->n_boxes < 0 || desc->T_off[desc->n_boxes] * sw != n_scalars)
     return set_error(SFMM_EINVAL, "sfmm_gpu_plan_create_skel: descriptor T_off does not match the skeletons");
-  return create_plan(desc, device, n_ranks, rank, out, T_dev);
+  return create_plan(desc, device, n_ranks, rank, out, T_dev, false, skel_share_T(skel));
 }
 
 int sfmm_gpu_shard_T_runs(const sfmm_plan_desc* desc, int n_ranks, int rank, int64_t* n_runs,
@@ -686,6 +722,8 @@ int sfmm_gpu_plan_info_get(const sfmm_gpu_plan* p, sfmm_gpu_plan_info* info) {
   info->n_ifs_pairs = hp.n_ifs;
   info->n_tfo_pairs = hp.n_tfo;
   info->n_level1_pairs = hp.n_l1;
+  info->sym_chain = hp.sym_chain ? 1 : 0;
+  info->stage_bytes = (int64_t)(hp.stage_size * (hp.cplx ? 16 : 8));
   if (p->multi) {
     multi_info(p, info);  // the orchestrating plan has no level lists of its own
   } else {

@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <memory>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -479,6 +480,10 @@ struct sfmm_skel_result {
   // the host copy T is made on demand (sfmm_gpu_skel_fill / _describe)
   double* d_T = nullptr;
   int device = 0, sw = 1;
+  // owner of d_T, shared with single-rank plans built from this result
+  // (skel_share_T): the operators are not copied, and whichever of the two
+  // is destroyed last frees them
+  std::shared_ptr<double> T_owner;
   bool have_host_T = false;
   std::vector<double> T;
   int32_t k_max = 0, saturated = 0;
@@ -487,15 +492,7 @@ struct sfmm_skel_result {
   sfmm_skel_result() = default;
   sfmm_skel_result(const sfmm_skel_result&) = delete;
   sfmm_skel_result& operator=(const sfmm_skel_result&) = delete;
-  ~sfmm_skel_result() {
-    if (d_T) {
-      int cur = 0;
-      cudaGetDevice(&cur);
-      cudaSetDevice(device);
-      cudaFree(d_T);
-      cudaSetDevice(cur);
-    }
-  }
+  ~sfmm_skel_result() = default;
   size_t t_scalars() const { return T_off.empty() ? 0 : (size_t)T_off.back() * sw; }
   void ensure_host_T() {
     if (have_host_T) return;
@@ -798,7 +795,7 @@ void run_skeletons(const sfmm_tree_desc& t, int kernel, double kappa, double tol
   d_work.alloc(0);  // the proxy workspace is no longer needed
   // the result's T; levels still on the device move to the host (largest
   // first) until it fits
-  while (cudaMalloc(&R.d_T, std::max<size_t>(R.t_scalars(), 1) * sizeof(double)) != cudaSuccess) {
+  while (cudaMalloc(&R.d_T, std::max<size_t>(R.t_scalars() + 2, 1) * sizeof(double)) != cudaSuccess) {
     (void)cudaGetLastError();
     int big = -1;
     for (int l = 2; l <= depth; ++l)
@@ -809,6 +806,16 @@ void run_skeletons(const sfmm_tree_desc& t, int kernel, double kappa, double tol
     }
     spill(L[big], L[big].d_T.n);
     if (verbose) std::fprintf(stderr, "[skel] level %d operators staged on the host\n", big);
+  }
+  {
+    const int dev = R.device;
+    R.T_owner.reset(R.d_T, [dev](double* ptr) {
+      int cur = -1;
+      if (cudaGetDevice(&cur) != cudaSuccess) cur = -1;
+      cudaSetDevice(dev);
+      cudaFree(ptr);
+      if (cur >= 0) cudaSetDevice(cur);
+    });
   }
   for (int l = 0; l <= depth; ++l) {
     const int b0 = t.level_begin[l], nl = t.level_begin[l + 1] - b0;
@@ -922,5 +929,15 @@ const double* sfmm_gpu_skel_device_T(const sfmm_skel_result* r, int* device, int
 }
 
 void sfmm_gpu_skel_destroy(sfmm_skel_result* r) { delete r; }
+
+}  // extern "C"
+
+namespace sfmm_gpu {
+std::shared_ptr<double> skel_share_T(const sfmm_skel_result* r) {
+  return r ? r->T_owner : std::shared_ptr<double>();
+}
+}  // namespace sfmm_gpu
+
+extern "C" {
 
 }  // extern "C"
