@@ -110,18 +110,20 @@ struct ChunkPos {
 };
 
 // KER: 0 laplace2d, 1 laplace3d, 3 helmholtz3d
-// WH: the launch's tasks own skeleton rows (uhat accumulators needed).  Tasks
-// without skeleton rows -- most of them -- run the lighter WH=false variant.
+// HPASS: false = the u pass over every task (U = sum G a); true = the uhat
+// pass over the tasks owning skeleton rows (UH = -sum G h), visiting only the
+// chunks that carry an h weight (ifs entries, and the skeleton sources of ifo
+// entries: ~1/8 of the columns).  Round 1 accumulated both in one variant;
+// its 96 accumulator registers spilled (168 registers, ~1.3e9 local-memory
+// instructions per config-4 apply, 44 % of K2m's time for ~1/5 of the rows).
+// Two passes with one accumulator set each regenerate G for the few h chunks
+// instead.
 // TAB: Helmholtz arguments within the sincos table's range (sincos_fast otherwise).
 #ifndef SFMM_K2M_MIN_BLOCKS
-#define SFMM_K2M_MIN_BLOCKS 4  // light variant (measured: 4 > 3 on config 4)
+#define SFMM_K2M_MIN_BLOCKS 4  // measured: 4 > 3 on config 4
 #endif
-#ifndef SFMM_K2M_MIN_BLOCKS_WH
-#define SFMM_K2M_MIN_BLOCKS_WH 3  // uhat variant (measured: 3 > 2, 4)
-#endif
-template <int KER, bool WH, bool TAB>
-__global__ void __launch_bounds__(kMThreads, WH ? SFMM_K2M_MIN_BLOCKS_WH : SFMM_K2M_MIN_BLOCKS)
-    k2m_translate(K2MArgs a) {
+template <int KER, bool HPASS, bool TAB>
+__global__ void __launch_bounds__(kMThreads, SFMM_K2M_MIN_BLOCKS) k2m_translate(K2MArgs a) {
   constexpr bool CPLX = KER == SFMM_HELMHOLTZ3D;
   constexpr int SW = CPLX ? 2 : 1;
   constexpr int NB = 2;             // rhs blocks of 8
@@ -161,25 +163,31 @@ __global__ void __launch_bounds__(kMThreads, WH ? SFMM_K2M_MIN_BLOCKS_WH : SFMM_
       yr[mt] = a.Y[s];
       zr[mt] = DIM == 3 ? a.Z[s] : 0.0;
     }
-    double C[2][NP][NB][2], H[2][NP][NB][2];
+    double C[2][NP][NB][2];  // u accumulators (HPASS: uhat)
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
       for (int pp = 0; pp < NP; ++pp)
 #pragma unroll
-        for (int nb = 0; nb < NB; ++nb)
-          C[mt][pp][nb][0] = C[mt][pp][nb][1] = H[mt][pp][nb][0] = H[mt][pp][nb][1] = 0.0;
-    const bool skel_rows = WH && task.row0 < tb.k;
+        for (int nb = 0; nb < NB; ++nb) C[mt][pp][nb][0] = C[mt][pp][nb][1] = 0.0;
 
-    // chunk iterator over (entry, first source), skipping empty source boxes
+    // chunk iterator over (entry, first source), skipping empty source boxes;
+    // the uhat pass visits only chunks with an h weight (ifs: every source;
+    // ifo: the skeleton sources j < k_c)
+    auto h_limit = [&](int e) -> int {
+      const int32_t code = a.ent[er.begin + e];
+      const int mode = code & kModeMask;
+      const BoxRec sb = a.box[code >> kModeBits];
+      if (!HPASS) return sb.n;
+      return mode == kIFS ? sb.n : (mode == kIFO ? sb.k : 0);
+    };
     auto first_from = [&](int e) -> ChunkPos {
       for (; e < er.count; ++e)
-        if (a.box[a.ent[er.begin + e] >> kModeBits].n > 0) return {e, 0};
+        if (h_limit(e) > 0) return {e, 0};
       return {er.count, 0};
     };
     auto next_of = [&](ChunkPos p) -> ChunkPos {
-      const BoxRec sb = a.box[a.ent[er.begin + p.e] >> kModeBits];
-      if (p.j0 + kChunk < sb.n) return {p.e, p.j0 + kChunk};
+      if (p.j0 + kChunk < h_limit(p.e)) return {p.e, p.j0 + kChunk};
       return first_from(p.e + 1);
     };
     // global loads of one chunk into registers (raw q and qhat)
@@ -223,7 +231,8 @@ __global__ void __launch_bounds__(kMThreads, WH ? SFMM_K2M_MIN_BLOCKS_WH : SFMM_
         }
       }
     };
-    // per-mode weights, scattered into fragment order
+    // per-mode weights, scattered into fragment order (the u pass stores the
+    // a weights, the uhat pass -- need_h -- the h weights)
     auto store = [&](ChunkPos p, const StageRegs<CPLX>& R, bool need_h) {
       const int mode = a.ent[er.begin + p.e] & kModeMask;
 #pragma unroll
@@ -242,17 +251,19 @@ __global__ void __launch_bounds__(kMThreads, WH ? SFMM_K2M_MIN_BLOCKS_WH : SFMM_
         }
         if (CPLX) {
           const int nb = r >> 3;
-          ch.a[ks][0][nb][fl] = wa[0];
-          ch.a[ks][NP - 2][nb][fl] = wa[SW - 1];
-          ch.a[ks][NP - 1][nb][fl] = wa[0] + wa[SW - 1];
-          if (need_h) {
+          if (!need_h) {
+            ch.a[ks][0][nb][fl] = wa[0];
+            ch.a[ks][NP - 2][nb][fl] = wa[SW - 1];
+            ch.a[ks][NP - 1][nb][fl] = wa[0] + wa[SW - 1];
+          } else {
             ch.h[ks][0][nb][fl] = wh[0];
             ch.h[ks][NP - 2][nb][fl] = wh[SW - 1];
             ch.h[ks][NP - 1][nb][fl] = wh[0] + wh[SW - 1];
           }
-        } else {
+        } else if (!need_h) {
           ch.a[ks][0][r >> 3][fl] = wa[0];
-          if (need_h) ch.h[ks][0][r >> 3][fl] = wh[0];
+        } else {
+          ch.h[ks][0][r >> 3][fl] = wh[0];
         }
       }
       if (tid < kChunk) {
@@ -261,20 +272,12 @@ __global__ void __launch_bounds__(kMThreads, WH ? SFMM_K2M_MIN_BLOCKS_WH : SFMM_
         ch.z[tid] = R.cz;
       }
     };
-    auto needs_h = [&](ChunkPos p) {
-      const int32_t code = a.ent[er.begin + p.e];
-      const int mode = code & kModeMask;
-      const BoxRec sb = a.box[code >> kModeBits];
-      return skel_rows && (mode == kIFS || (mode == kIFO && p.j0 < sb.k));
-    };
-
     ChunkPos cur = first_from(0);
     StageRegs<CPLX> R;
     if (cur.e < er.count) load(cur, R);
     while (cur.e < er.count) {
-      const bool need_h = needs_h(cur);
       __syncthreads();  // previous chunk fully consumed
-      store(cur, R, need_h);
+      store(cur, R, HPASS);
       __syncthreads();
       const int32_t code = a.ent[er.begin + cur.e];
       const bool self = (code >> kModeBits) == task.box;
@@ -333,20 +336,10 @@ __global__ void __launch_bounds__(kMThreads, WH ? SFMM_K2M_MIN_BLOCKS_WH : SFMM_
           for (int pp = 0; pp < NP; ++pp)
 #pragma unroll
             for (int nb = 0; nb < NB; ++nb) {
-              const double bv = ch.a[ks][pp][nb][lane];
+              const double bv = HPASS ? ch.h[ks][pp][nb][lane] : ch.a[ks][pp][nb][lane];
 #pragma unroll
               for (int mt = 0; mt < 2; ++mt) dmma(C[mt][pp][nb][0], C[mt][pp][nb][1], g[pp][mt], bv);
             }
-          if (need_h) {
-#pragma unroll
-            for (int pp = 0; pp < NP; ++pp)
-#pragma unroll
-              for (int nb = 0; nb < NB; ++nb) {
-                const double bv = ch.h[ks][pp][nb][lane];
-#pragma unroll
-                for (int mt = 0; mt < 2; ++mt) dmma(H[mt][pp][nb][0], H[mt][pp][nb][1], g[pp][mt], bv);
-              }
-          }
         }
       }
       cur = nxt;
@@ -365,9 +358,11 @@ __global__ void __launch_bounds__(kMThreads, WH ? SFMM_K2M_MIN_BLOCKS_WH : SFMM_
         for (int nb = 0; nb < NB; ++nb)
           bad = bad || !isfinite(C[mt][pp][nb][0]) || !isfinite(C[mt][pp][nb][1]);
       if (bad) verify_row_m(a, task.box, row, DIM);
-      double* u = a.U + (tb.slot + row) * (kNRHS * SW);
-      const bool skel_row = row < tb.k;
-      double* uh = a.UH + (tb.skel + (skel_row ? row : 0)) * (kNRHS * SW);
+      if (HPASS && row >= tb.k) continue;  // uhat exists for skeleton rows only
+      // u pass: U = scale * acc; uhat pass: UH = -scale * acc
+      double* out = HPASS ? a.UH + (tb.skel + row) * (kNRHS * SW)
+                          : a.U + (tb.slot + row) * (kNRHS * SW);
+      const double sc = HPASS ? -scale : scale;
 #pragma unroll
       for (int half = 0; half < 2; ++half) {  // rhs block c0 + 8*half
 #pragma unroll
@@ -375,16 +370,10 @@ __global__ void __launch_bounds__(kMThreads, WH ? SFMM_K2M_MIN_BLOCKS_WH : SFMM_
           const int rhs = c0 + 8 * half + w;
           if (CPLX) {
             const double t1 = C[mt][0][half][w], t2 = C[mt][NP - 2][half][w];
-            u[2 * rhs] = (t1 - t2) * scale;
-            u[2 * rhs + 1] = (C[mt][NP - 1][half][w] - t1 - t2) * scale;
-            if (skel_row) {
-              const double h1 = H[mt][0][half][w], h2 = H[mt][NP - 2][half][w];
-              uh[2 * rhs] = -(h1 - h2) * scale;
-              uh[2 * rhs + 1] = -(H[mt][NP - 1][half][w] - h1 - h2) * scale;
-            }
+            out[2 * rhs] = (t1 - t2) * sc;
+            out[2 * rhs + 1] = (C[mt][NP - 1][half][w] - t1 - t2) * sc;
           } else {
-            u[rhs] = C[mt][0][half][w] * scale;
-            if (skel_row) uh[rhs] = -H[mt][0][half][w] * scale;
+            out[rhs] = C[mt][0][half][w] * sc;
           }
         }
       }
@@ -544,10 +533,10 @@ int grid_m(int64_t n) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 32));
 }
 
-template <int KER, bool WH>
+template <int KER, bool HPASS>
 int blocks_per_sm() {
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2m_translate<KER, WH, KER == SFMM_HELMHOLTZ3D>, kMThreads, 0) !=
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2m_translate<KER, HPASS, KER == SFMM_HELMHOLTZ3D>, kMThreads, 0) !=
       cudaSuccess)
     return -1;
   return std::max(1, per_sm);
@@ -652,18 +641,18 @@ void launch_translate_m(const DevPlan& p, DevState& s, cudaStream_t st) {
   a.tab = p.sc_tab;
   a.ltab = p.log_tab;
   cudaMemsetAsync(p.counter + 2, 0, 2 * sizeof(int), st);
-  // tasks [0, n_tasks_mh) own skeleton rows, the rest do not
+  // part 0: the u pass over every task; part 1: the uhat pass over the tasks
+  // [0, n_tasks_mh) that own skeleton rows
   for (int part = 0; part < 2; ++part) {
-    const int64_t t0 = part == 0 ? 0 : p.n_tasks_mh;
-    const int64_t t1 = part == 0 ? p.n_tasks_mh : p.n_tasks_m;
-    if (t1 <= t0) continue;
-    a.tasks = p.tasks_m + t0;
-    a.n_tasks = t1 - t0;
+    const int64_t t1 = part == 0 ? p.n_tasks_m : p.n_tasks_mh;
+    if (t1 <= 0) continue;
+    a.tasks = p.tasks_m;
+    a.n_tasks = t1;
     a.counter = p.counter + 2 + part;
-    const int grid = (int)std::min<int64_t>(part == 0 ? p.k2m_grid : p.k2m_grid0, t1 - t0);
+    const int grid = (int)std::min<int64_t>(part == 0 ? p.k2m_grid0 : p.k2m_grid, t1);
 #define SFMM_K2M_LAUNCH(KER, TAB)                                                   \
   do {                                                                              \
-    if (part == 0)                                                                  \
+    if (part == 1)                                                                  \
       k2m_translate<KER, true, TAB><<<grid, kMThreads, 0, st>>>(a);                 \
     else                                                                            \
       k2m_translate<KER, false, TAB><<<grid, kMThreads, 0, st>>>(a);                \
