@@ -130,7 +130,10 @@ __global__ void __launch_bounds__(kMThreads, SFMM_K2M_MIN_BLOCKS) k2m_translate(
   constexpr int NP = CPLX ? 3 : 1;  // real products per complex product (3M)
   constexpr int DIM = KER == SFMM_LAPLACE2D ? 2 : 3;
   constexpr int ITEMS = StageRegs<CPLX>::ITEMS;
-  __shared__ ChunkM<CPLX> ch;
+  // two chunk buffers: the next chunk is stored while the current one is
+  // read, so one barrier per chunk suffices
+  __shared__ ChunkM<CPLX> chb[2];
+  ChunkM<CPLX>* chp = &chb[0];
   __shared__ int s_task;
   __shared__ double2 tab[CPLX ? kSinCosTab : 1];
   __shared__ __align__(16) double ltab[KER == SFMM_LAPLACE2D ? kLogTabLen : 1];
@@ -252,33 +255,39 @@ __global__ void __launch_bounds__(kMThreads, SFMM_K2M_MIN_BLOCKS) k2m_translate(
         if (CPLX) {
           const int nb = r >> 3;
           if (!need_h) {
-            ch.a[ks][0][nb][fl] = wa[0];
-            ch.a[ks][NP - 2][nb][fl] = wa[SW - 1];
-            ch.a[ks][NP - 1][nb][fl] = wa[0] + wa[SW - 1];
+            chp->a[ks][0][nb][fl] = wa[0];
+            chp->a[ks][NP - 2][nb][fl] = wa[SW - 1];
+            chp->a[ks][NP - 1][nb][fl] = wa[0] + wa[SW - 1];
           } else {
-            ch.h[ks][0][nb][fl] = wh[0];
-            ch.h[ks][NP - 2][nb][fl] = wh[SW - 1];
-            ch.h[ks][NP - 1][nb][fl] = wh[0] + wh[SW - 1];
+            chp->h[ks][0][nb][fl] = wh[0];
+            chp->h[ks][NP - 2][nb][fl] = wh[SW - 1];
+            chp->h[ks][NP - 1][nb][fl] = wh[0] + wh[SW - 1];
           }
         } else if (!need_h) {
-          ch.a[ks][0][r >> 3][fl] = wa[0];
+          chp->a[ks][0][r >> 3][fl] = wa[0];
         } else {
-          ch.h[ks][0][r >> 3][fl] = wh[0];
+          chp->h[ks][0][r >> 3][fl] = wh[0];
         }
       }
       if (tid < kChunk) {
-        ch.x[tid] = R.cx;
-        ch.y[tid] = R.cy;
-        ch.z[tid] = R.cz;
+        chp->x[tid] = R.cx;
+        chp->y[tid] = R.cy;
+        chp->z[tid] = R.cz;
       }
     };
     ChunkPos cur = first_from(0);
     StageRegs<CPLX> R;
-    if (cur.e < er.count) load(cur, R);
-    while (cur.e < er.count) {
-      __syncthreads();  // previous chunk fully consumed
+    int buf = 0;
+    if (cur.e < er.count) {
+      load(cur, R);
+      chp = &chb[0];
       store(cur, R, HPASS);
-      __syncthreads();
+    }
+    __syncthreads();
+    ChunkPos nxt = cur.e < er.count ? next_of(cur) : cur;
+    if (nxt.e < er.count) load(nxt, R);  // in flight during the compute below
+    while (cur.e < er.count) {
+      chp = &chb[buf];
       const int32_t code = a.ent[er.begin + cur.e];
       const bool self = (code >> kModeBits) == task.box;
       const int j0 = cur.j0;
@@ -286,8 +295,6 @@ __global__ void __launch_bounds__(kMThreads, SFMM_K2M_MIN_BLOCKS) k2m_translate(
       // below (never trusted to vanish through the zero weight: a target may
       // sit exactly at the padding coordinate)
       const int n_valid = a.box[code >> kModeBits].n - j0;
-      const ChunkPos nxt = next_of(cur);
-      if (nxt.e < er.count) load(nxt, R);  // in flight during the compute below
       if (wrow0 < rend) {
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {
@@ -295,10 +302,10 @@ __global__ void __launch_bounds__(kMThreads, SFMM_K2M_MIN_BLOCKS) k2m_translate(
           double gr[2], gi[2];
 #pragma unroll
           for (int mt = 0; mt < 2; ++mt) {
-            const double dx = xr[mt] - ch.x[js], dy = yr[mt] - ch.y[js];
+            const double dx = xr[mt] - chp->x[js], dy = yr[mt] - chp->y[js];
             double r2 = fma(dy, dy, dx * dx);
             if (DIM == 3) {
-              const double dz = zr[mt] - ch.z[js];
+              const double dz = zr[mt] - chp->z[js];
               r2 = fma(dz, dz, r2);
             }
             if (KER == SFMM_LAPLACE2D) {
@@ -336,13 +343,23 @@ __global__ void __launch_bounds__(kMThreads, SFMM_K2M_MIN_BLOCKS) k2m_translate(
           for (int pp = 0; pp < NP; ++pp)
 #pragma unroll
             for (int nb = 0; nb < NB; ++nb) {
-              const double bv = HPASS ? ch.h[ks][pp][nb][lane] : ch.a[ks][pp][nb][lane];
+              const double bv = HPASS ? chp->h[ks][pp][nb][lane] : chp->a[ks][pp][nb][lane];
 #pragma unroll
               for (int mt = 0; mt < 2; ++mt) dmma(C[mt][pp][nb][0], C[mt][pp][nb][1], g[pp][mt], bv);
             }
         }
       }
+      if (nxt.e < er.count) {  // the other buffer was last read before the previous barrier
+        chp = &chb[buf ^ 1];
+        store(nxt, R, HPASS);
+      }
+      __syncthreads();
+      buf ^= 1;
       cur = nxt;
+      if (cur.e < er.count) {
+        nxt = next_of(cur);
+        if (nxt.e < er.count) load(nxt, R);
+      }
     }
     // epilogue: lane holds rows rq (+8) and rhs columns c0, c0+1, 8+c0, 9+c0
     const double scale = CPLX ? 0.25 : (KER == SFMM_LAPLACE3D ? kInv4Pi : -kInv4Pi);
