@@ -31,6 +31,7 @@ namespace {
 constexpr int kMWarps = 4;
 constexpr int kMThreads = 32 * kMWarps;
 constexpr int kChunk = 16;  // sources staged per chunk (4 k-steps of 4)
+constexpr int kMEntCap = 128;  // entries of a task held in shared memory (else read globally)
 constexpr double kInv4Pi = 0.0795774715459476678844418816862571810;
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
@@ -101,7 +102,9 @@ template <bool CPLX>
 struct StageRegs {
   static constexpr int SW = CPLX ? 2 : 1;
   static constexpr int ITEMS = kChunk * kNRHS / kMThreads;  // (source, rhs) per thread
-  double q[ITEMS][SW], qh[ITEMS][SW];
+  // the pass's weight (u pass: q; uhat pass: qhat for ifo, q for ifs) and,
+  // for plans with tfo entries, qhat for the u pass's tfo weight q - qhat
+  double w[ITEMS][SW], w2[ITEMS][SW];
   double cx, cy, cz;
 };
 
@@ -122,7 +125,8 @@ struct ChunkPos {
 #ifndef SFMM_K2M_MIN_BLOCKS
 #define SFMM_K2M_MIN_BLOCKS 4  // measured: 4 > 3 on config 4
 #endif
-template <int KER, bool HPASS, bool TAB>
+// TFO: the plan has tfo entries (u pass needs q and qhat of those sources).
+template <int KER, bool HPASS, bool TAB, bool TFO>
 __global__ void __launch_bounds__(kMThreads, SFMM_K2M_MIN_BLOCKS) k2m_translate(K2MArgs a) {
   constexpr bool CPLX = KER == SFMM_HELMHOLTZ3D;
   constexpr int SW = CPLX ? 2 : 1;
@@ -135,6 +139,11 @@ __global__ void __launch_bounds__(kMThreads, SFMM_K2M_MIN_BLOCKS) k2m_translate(
   __shared__ ChunkM<CPLX> chb[2];
   ChunkM<CPLX>* chp = &chb[0];
   __shared__ int s_task;
+  // the task's entry list (codes and source box records), read once per task:
+  // the chunk iterator then runs from shared memory instead of two dependent
+  // global loads per chunk on the critical path
+  __shared__ int32_t s_code[kMEntCap];
+  __shared__ BoxRec s_sb[kMEntCap];
   __shared__ double2 tab[CPLX ? kSinCosTab : 1];
   __shared__ __align__(16) double ltab[KER == SFMM_LAPLACE2D ? kLogTabLen : 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -153,6 +162,19 @@ __global__ void __launch_bounds__(kMThreads, SFMM_K2M_MIN_BLOCKS) k2m_translate(
     const Task task = a.tasks[t];
     const BoxRec tb = a.box[task.box];
     const EntryRange er = a.er[task.box];
+    const bool ent_smem = er.count <= kMEntCap;
+    if (ent_smem) {
+      for (int i = tid; i < er.count; i += kMThreads) {
+        const int32_t code = a.ent[er.begin + i];
+        s_code[i] = code;
+        s_sb[i] = a.box[code >> kModeBits];
+      }
+      __syncthreads();
+    }
+    auto ent_code = [&](int e) -> int32_t { return ent_smem ? s_code[e] : a.ent[er.begin + e]; };
+    auto ent_box = [&](int e) -> BoxRec {
+      return ent_smem ? s_sb[e] : a.box[a.ent[er.begin + e] >> kModeBits];
+    };
     const int wrow0 = task.row0 + 16 * warp;  // this warp's 16 rows
     const int rend = task.row0 + task.nrows;
     double xr[2], yr[2], zr[2];
@@ -178,9 +200,9 @@ __global__ void __launch_bounds__(kMThreads, SFMM_K2M_MIN_BLOCKS) k2m_translate(
     // the uhat pass visits only chunks with an h weight (ifs: every source;
     // ifo: the skeleton sources j < k_c)
     auto h_limit = [&](int e) -> int {
-      const int32_t code = a.ent[er.begin + e];
+      const int32_t code = ent_code(e);
       const int mode = code & kModeMask;
-      const BoxRec sb = a.box[code >> kModeBits];
+      const BoxRec sb = ent_box(e);
       if (!HPASS) return sb.n;
       return mode == kIFS ? sb.n : (mode == kIFO ? sb.k : 0);
     };
@@ -203,22 +225,33 @@ __global__ void __launch_bounds__(kMThreads, SFMM_K2M_MIN_BLOCKS) k2m_translate(
       r = 8 * (g & 1) + (lane >> 2);
     };
     auto load = [&](ChunkPos p, StageRegs<CPLX>& R) {
-      const BoxRec sb = a.box[a.ent[er.begin + p.e] >> kModeBits];
+      const BoxRec sb = ent_box(p.e);
+      const int mode = ent_code(p.e) & kModeMask;
 #pragma unroll
       for (int it = 0; it < ITEMS; ++it) {
         int jj, r;
         item(it, jj, r);
         const int j = p.j0 + jj;
 #pragma unroll
-        for (int c = 0; c < SW; ++c) R.q[it][c] = R.qh[it][c] = 0.0;
+        for (int c = 0; c < SW; ++c) R.w[it][c] = R.w2[it][c] = 0.0;
         if (j < sb.n) {
           const double* qp = a.Q + ((sb.slot + j) * kNRHS + r) * SW;
+          const double* hp = a.QH + ((sb.skel + j) * kNRHS + r) * SW;
+          if (HPASS) {
+            if (mode == kIFS) {
 #pragma unroll
-          for (int c = 0; c < SW; ++c) R.q[it][c] = qp[c];
-          if (j < sb.k) {
-            const double* hp = a.QH + ((sb.skel + j) * kNRHS + r) * SW;
+              for (int c = 0; c < SW; ++c) R.w[it][c] = qp[c];
+            } else if (j < sb.k) {  // ifo: qhat on the skeleton sources
 #pragma unroll
-            for (int c = 0; c < SW; ++c) R.qh[it][c] = hp[c];
+              for (int c = 0; c < SW; ++c) R.w[it][c] = hp[c];
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < SW; ++c) R.w[it][c] = qp[c];
+            if (TFO && mode == kTFO && j < sb.k) {
+#pragma unroll
+              for (int c = 0; c < SW; ++c) R.w2[it][c] = hp[c];
+            }
           }
         }
       }
@@ -237,7 +270,7 @@ __global__ void __launch_bounds__(kMThreads, SFMM_K2M_MIN_BLOCKS) k2m_translate(
     // per-mode weights, scattered into fragment order (the u pass stores the
     // a weights, the uhat pass -- need_h -- the h weights)
     auto store = [&](ChunkPos p, const StageRegs<CPLX>& R, bool need_h) {
-      const int mode = a.ent[er.begin + p.e] & kModeMask;
+      const int mode = ent_code(p.e) & kModeMask;
 #pragma unroll
       for (int it = 0; it < ITEMS; ++it) {
         int jj, r;
@@ -246,11 +279,9 @@ __global__ void __launch_bounds__(kMThreads, SFMM_K2M_MIN_BLOCKS) k2m_translate(
         double wa[SW], wh[SW];
 #pragma unroll
         for (int c = 0; c < SW; ++c) {
-          wa[c] = R.q[it][c];
-          wh[c] = 0.0;
-          if (mode == kIFO) wh[c] = R.qh[it][c];
-          else if (mode == kIFS) wh[c] = R.q[it][c];
-          else if (mode == kTFO) wa[c] = R.q[it][c] - R.qh[it][c];
+          wa[c] = R.w[it][c];
+          if (TFO && !HPASS && mode == kTFO) wa[c] = R.w[it][c] - R.w2[it][c];
+          wh[c] = R.w[it][c];
         }
         if (CPLX) {
           const int nb = r >> 3;
@@ -288,13 +319,13 @@ __global__ void __launch_bounds__(kMThreads, SFMM_K2M_MIN_BLOCKS) k2m_translate(
     if (nxt.e < er.count) load(nxt, R);  // in flight during the compute below
     while (cur.e < er.count) {
       chp = &chb[buf];
-      const int32_t code = a.ent[er.begin + cur.e];
+      const int32_t code = ent_code(cur.e);
       const bool self = (code >> kModeBits) == task.box;
       const int j0 = cur.j0;
       // sources of this chunk past the box end are padding: their G is masked
       // below (never trusted to vanish through the zero weight: a target may
       // sit exactly at the padding coordinate)
-      const int n_valid = a.box[code >> kModeBits].n - j0;
+      const int n_valid = ent_box(cur.e).n - j0;
       if (wrow0 < rend) {
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {
@@ -553,7 +584,7 @@ int grid_m(int64_t n) {
 template <int KER, bool HPASS>
 int blocks_per_sm() {
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2m_translate<KER, HPASS, KER == SFMM_HELMHOLTZ3D>, kMThreads, 0) !=
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2m_translate<KER, HPASS, KER == SFMM_HELMHOLTZ3D, false>, kMThreads, 0) !=
       cudaSuccess)
     return -1;
   return std::max(1, per_sm);
@@ -670,9 +701,11 @@ void launch_translate_m(const DevPlan& p, DevState& s, cudaStream_t st) {
 #define SFMM_K2M_LAUNCH(KER, TAB)                                                   \
   do {                                                                              \
     if (part == 1)                                                                  \
-      k2m_translate<KER, true, TAB><<<grid, kMThreads, 0, st>>>(a);                 \
+      k2m_translate<KER, true, TAB, false><<<grid, kMThreads, 0, st>>>(a);          \
+    else if (p.has_tfo_m)                                                           \
+      k2m_translate<KER, false, TAB, true><<<grid, kMThreads, 0, st>>>(a);          \
     else                                                                            \
-      k2m_translate<KER, false, TAB><<<grid, kMThreads, 0, st>>>(a);                \
+      k2m_translate<KER, false, TAB, false><<<grid, kMThreads, 0, st>>>(a);         \
   } while (0)
     if (p.kernel == SFMM_HELMHOLTZ3D && p.sc_tab_ok)
       SFMM_K2M_LAUNCH(SFMM_HELMHOLTZ3D, true);

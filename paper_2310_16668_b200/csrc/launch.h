@@ -69,6 +69,7 @@ struct DevPlan {
   int64_t n_tasks_m;
   LevelItem* down_m_items;
   int64_t n_tasks_mh;  // tasks_m[0, n_tasks_mh) own skeleton rows
+  int has_tfo_m = 0;   // entries_full holds tfo entries (K2m u pass needs qhat too)
   int k2m_grid, k2m_grid0;
   size_t down_m_smem;
   int* counter;     // K2 task counters (interior, boundary, multi; reset per launch)

@@ -227,6 +227,7 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
       dp.ent_range_full = p->upload(hp.ent_range_full);
       dp.entries_full = p->upload(hp.entries_full);
       dp.tasks_m = p->upload(hp.tasks_m);
+      for (int32_t c : hp.entries_full) dp.has_tfo_m |= (c & kModeMask) == kTFO ? 1 : 0;
       dp.n_tasks_m = (int64_t)hp.tasks_m.size();
       dp.n_tasks_mh = hp.n_tasks_mh;
       dp.down_m_items = p->upload(hp.down_m_items);
