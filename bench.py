@@ -112,6 +112,9 @@ def parse():
     ap.add_argument("--devices", default=None,
                     help="one process, plan sharded over these devices (e.g. 0,1,2,3; ids may "
                          "repeat), exchanges as peer copies inside the library")
+    ap.add_argument("--force-sharded", action="store_true",
+                    help="run the multi-rank path even with one rank (tests the NCCL plumbing "
+                         "on one GPU under torchrun --nproc-per-node 1)")
     ap.add_argument("--graphs", default="auto", choices=["auto", "on", "off"],
                     help="replay the apply as a CUDA graph in the timed region (auto: small plans)")
     ap.add_argument("--config", default=None, choices=sorted(CONFIGS),
@@ -651,7 +654,7 @@ def main():
     if args.impl == "reference":
         run_reference(args, ws, rank)
         return
-    if ws > 1:
+    if ws > 1 or args.force_sharded:
         run_sharded(args, ws, rank, local)
         return
     devices = [int(x) for x in args.devices.split(",")] if args.devices else None

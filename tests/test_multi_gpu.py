@@ -131,3 +131,52 @@ def test_multi_device_duplicate_points_reported():
     with api.GpuPlan(d, devices=[0, 0, 0, 0]) as plan:
         with pytest.raises(api.DuplicatePointError):
             api.fmm_apply(plan, host.generate_charges(20000, 1))
+
+
+def test_nccl_rank_plan_single_rank():
+    """The one-process-per-GPU transport on the one GPU a gpurun box has: a
+    1-rank NCCL communicator exercises the run-time NCCL load, the
+    communicator set-up and the collective apply (grouped send/recv with no
+    peers, the in-place all-reduce of the full result, the owned-only output)
+    -- everything but the peer traffic."""
+    import torch
+    d, q, _ = _case("l3d_sphere")
+    u_single = api.fmm_apply(api.GpuPlan(d), q)
+    plan = shard.ShardedPlan(d, 1, 0)
+    plan.attach_nccl(shard.nccl_unique_id())
+    qd = torch.from_numpy(q).cuda()
+    ud = torch.zeros_like(qd)
+    s = torch.cuda.Stream()
+    plan.set_output(owned_only=True)
+    plan.apply(qd, ud, s.cuda_stream)
+    s.synchronize()
+    assert rel_l2(ud.cpu().numpy(), u_single) <= PARITY
+    plan.set_output(owned_only=False)
+    out = np.empty_like(q)
+    plan.apply_host(np.ascontiguousarray(q), out)
+    assert rel_l2(out, u_single) <= PARITY
+    plan.close()
+
+
+def test_bench_sharded_path_one_rank_nccl_in_library(tmp_path):
+    """bench.py's multi-rank path (torchrun, NCCL process group, operator blobs,
+    the exchange inside the library) end to end with one rank."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.join(root, "bench.py"), "--force-sharded", "--steps", "2", "--warmup", "3",
+           "--points", "3e5", "--check-targets", "100"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["exchange_in_library"] is True, line["parallelism"]
+    assert line["relerr_vs_single_gpu"] <= 1e-12
+    assert line["value"] > 0 and line["e2e"]["value"] > 0
