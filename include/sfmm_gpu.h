@@ -136,6 +136,10 @@ typedef struct sfmm_gpu_plan_info {
   int32_t sym_chain;          /* 1: symmetric column sums chained per pair (low-memory layout,
                                  chosen when the per-tile staging would not fit) */
   int64_t stage_bytes;        /* column-sum staging of the symmetric colleague blocks */
+  int32_t multi_sym;          /* 1: multi-RHS applies generate each colleague block once
+                                 (transposed DMMA product, staged column sums) */
+  int32_t reserved0;
+  int64_t multi_stage_bytes;  /* their column-sum staging (allocated on the first multi-RHS apply) */
 } sfmm_gpu_plan_info;
 
 typedef struct sfmm_gpu_plan sfmm_gpu_plan;

@@ -98,6 +98,9 @@ class PlanInfo(C.Structure):
         ("k2_grid", C.c_int32),
         ("sym_chain", C.c_int32),
         ("stage_bytes", C.c_int64),
+        ("multi_sym", C.c_int32),
+        ("reserved0", C.c_int32),
+        ("multi_stage_bytes", C.c_int64),
     ]
 
 

@@ -30,7 +30,7 @@ namespace {
 
 constexpr int kMWarps = 4;
 constexpr int kMThreads = 32 * kMWarps;
-constexpr int kChunk = 16;  // sources staged per chunk (4 k-steps of 4)
+constexpr int kChunk = kChunkM;  // sources staged per chunk (4 k-steps of 4)
 constexpr int kMEntCap = 128;  // entries of a task held in shared memory (else read globally)
 constexpr double kInv4Pi = 0.0795774715459476678844418816862571810;
 
@@ -64,7 +64,16 @@ struct K2MArgs {
   double kappa;
   const double2* tab;  // (cos, sin)(k pi/128), Helmholtz only
   const double* ltab;  // log table, Laplace 2D only
+  const int32_t* soff; // symmetric u pass: per entry, first staged point of a kSYM entry
+  double* stage;       // symmetric u pass: staged column sums [point][kNRHS] (pre-scaled)
+  unsigned* sflag;     // symmetric u pass: per staged chunk, warps of the tiles that have added
 };
+
+__device__ __forceinline__ unsigned ld_acquire_flag(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 __device__ __noinline__ void verify_row_m(const K2MArgs& a, int32_t b, int32_t row, int dim) {
   const BoxRec tb = a.box[b];
@@ -92,9 +101,18 @@ struct ChunkM {
   static constexpr int NB = 2;             // 8-column rhs blocks
   static constexpr int NP = CPLX ? 3 : 1;  // B = Ar, Ai, Ar + Ai (complex) or A
   double x[kChunk], y[kChunk], z[kChunk];
-  double a[4][NP][NB][32];
-  double h[4][NP][NB][32];
+  double w[4][NP][NB][32];  // the pass's weights (u pass: a, uhat pass: h)
 };
+
+// Symmetric u pass (kSYM entries): the CTA's generated 64 x 16 block of a
+// chunk and the task's own charges (64 rows x kNRHS), both [row][16] in
+// shared memory with the 16-column index XOR-swizzled by the row so the
+// transposed fragment loads (4 rows x 8 columns per k-step) and the
+// generation stores are (nearly) conflict-free.
+template <bool CPLX>
+__device__ __forceinline__ int swz(int row, int col) {
+  return col ^ ((row & 3) << (CPLX ? 1 : 2));
+}
 
 // Raw per-thread staging payload of one chunk (registers), so the next chunk's
 // global loads are in flight while the current one is computed.
@@ -126,8 +144,19 @@ struct ChunkPos {
 #define SFMM_K2M_MIN_BLOCKS 4  // measured: 4 > 3 on config 4
 #endif
 // TFO: the plan has tfo entries (u pass needs q and qhat of those sources).
-template <int KER, bool HPASS, bool TAB, bool TFO>
-__global__ void __launch_bounds__(kMThreads, SFMM_K2M_MIN_BLOCKS) k2m_translate(K2MArgs a) {
+// SYM: the u pass over the folded lists (HostPlan::multi_sym): a kSYM chunk's
+// generated block is also applied transposed to the task's charges -- warp w
+// takes sources 8(w&1).. and rhs block w>>1 over all the task's rows -- and
+// the column sums go to the staging buffer (K2bm adds them).  Its shared
+// memory (two block buffers + the charges) allows 3 CTAs per SM (complex).
+#ifndef SFMM_K2M_SYM_MIN_BLOCKS
+#define SFMM_K2M_SYM_MIN_BLOCKS 3
+#endif
+template <int KER, bool HPASS, bool TAB, bool TFO, bool SYM>
+__global__ void __launch_bounds__(kMThreads, SYM ? (KER == SFMM_HELMHOLTZ3D ? SFMM_K2M_SYM_MIN_BLOCKS : 4)
+                                                 : SFMM_K2M_MIN_BLOCKS)
+    k2m_translate(K2MArgs a) {
+  static_assert(!(SYM && HPASS), "the symmetric fold is a u-pass variant");
   constexpr bool CPLX = KER == SFMM_HELMHOLTZ3D;
   constexpr int SW = CPLX ? 2 : 1;
   constexpr int NB = 2;             // rhs blocks of 8
@@ -144,6 +173,14 @@ __global__ void __launch_bounds__(kMThreads, SFMM_K2M_MIN_BLOCKS) k2m_translate(
   // global loads per chunk on the critical path
   __shared__ int32_t s_code[kMEntCap];
   __shared__ BoxRec s_sb[kMEntCap];
+  __shared__ int32_t s_soff[SYM ? kMEntCap : 1];
+  // SYM (dynamic shared memory, sym_smem_bytes): generated blocks of the
+  // current / previous kSYM chunk and the task's charges, [row][16 columns]
+  // of scalars (complex: interleaved)
+  extern __shared__ __align__(16) double k2m_dyn[];
+  using GRow = double[kChunk * SW];
+  GRow* gts0 = reinterpret_cast<GRow*>(k2m_dyn);
+  GRow* qbs = gts0 + 2 * kMultiRows;
   __shared__ double2 tab[CPLX ? kSinCosTab : 1];
   __shared__ __align__(16) double ltab[KER == SFMM_LAPLACE2D ? kLogTabLen : 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -168,10 +205,26 @@ __global__ void __launch_bounds__(kMThreads, SFMM_K2M_MIN_BLOCKS) k2m_translate(
         const int32_t code = a.ent[er.begin + i];
         s_code[i] = code;
         s_sb[i] = a.box[code >> kModeBits];
+        if (SYM) s_soff[i] = a.soff[er.begin + i];
       }
       __syncthreads();
     }
+    if constexpr (SYM) {  // the task's charges (zero past its rows); ordered by the barrier before the loop
+      for (int v = tid; v < kMultiRows * kNRHS; v += kMThreads) {
+        const int row = v / kNRHS, r = v % kNRHS;
+        const int cs = swz<CPLX>(row, r) * SW;
+        if (row < task.nrows) {
+          const double* qp = a.Q + ((tb.slot + task.row0 + row) * kNRHS + r) * SW;
+#pragma unroll
+          for (int c = 0; c < SW; ++c) qbs[row][cs + c] = qp[c];
+        } else {
+#pragma unroll
+          for (int c = 0; c < SW; ++c) qbs[row][cs + c] = 0.0;
+        }
+      }
+    }
     auto ent_code = [&](int e) -> int32_t { return ent_smem ? s_code[e] : a.ent[er.begin + e]; };
+    auto ent_soff = [&](int e) -> int32_t { return ent_smem ? s_soff[e] : a.soff[er.begin + e]; };
     auto ent_box = [&](int e) -> BoxRec {
       return ent_smem ? s_sb[e] : a.box[a.ent[er.begin + e] >> kModeBits];
     };
@@ -283,21 +336,12 @@ __global__ void __launch_bounds__(kMThreads, SFMM_K2M_MIN_BLOCKS) k2m_translate(
           if (TFO && !HPASS && mode == kTFO) wa[c] = R.w[it][c] - R.w2[it][c];
           wh[c] = R.w[it][c];
         }
+        const double w0 = need_h ? wh[0] : wa[0], w1 = need_h ? wh[SW - 1] : wa[SW - 1];
+        const int nb = r >> 3;
+        chp->w[ks][0][nb][fl] = w0;
         if (CPLX) {
-          const int nb = r >> 3;
-          if (!need_h) {
-            chp->a[ks][0][nb][fl] = wa[0];
-            chp->a[ks][NP - 2][nb][fl] = wa[SW - 1];
-            chp->a[ks][NP - 1][nb][fl] = wa[0] + wa[SW - 1];
-          } else {
-            chp->h[ks][0][nb][fl] = wh[0];
-            chp->h[ks][NP - 2][nb][fl] = wh[SW - 1];
-            chp->h[ks][NP - 1][nb][fl] = wh[0] + wh[SW - 1];
-          }
-        } else if (!need_h) {
-          chp->a[ks][0][r >> 3][fl] = wa[0];
-        } else {
-          chp->h[ks][0][r >> 3][fl] = wh[0];
+          chp->w[ks][NP - 2][nb][fl] = w1;
+          chp->w[ks][NP - 1][nb][fl] = w0 + w1;
         }
       }
       if (tid < kChunk) {
@@ -317,16 +361,24 @@ __global__ void __launch_bounds__(kMThreads, SFMM_K2M_MIN_BLOCKS) k2m_translate(
     __syncthreads();
     ChunkPos nxt = cur.e < er.count ? next_of(cur) : cur;
     if (nxt.e < er.count) load(nxt, R);  // in flight during the compute below
-    while (cur.e < er.count) {
+    // SYM: the kSYM chunk whose transposed product is still due (it runs one
+    // iteration late, reading the block buffer the previous iteration wrote)
+    ChunkPos prev{er.count, 0};
+    auto is_sym = [&](const ChunkPos& p) {
+      return SYM && p.e < er.count && (ent_code(p.e) & kModeMask) == kSYM;
+    };
+    while (cur.e < er.count || is_sym(prev)) {
       chp = &chb[buf];
-      const int32_t code = ent_code(cur.e);
-      const bool self = (code >> kModeBits) == task.box;
+      const bool live = cur.e < er.count;
+      const int32_t code = live ? ent_code(cur.e) : 0;
+      const bool self = live && (code >> kModeBits) == task.box;
+      const bool csym = SYM && live && (code & kModeMask) == kSYM;
       const int j0 = cur.j0;
       // sources of this chunk past the box end are padding: their G is masked
       // below (never trusted to vanish through the zero weight: a target may
       // sit exactly at the padding coordinate)
-      const int n_valid = ent_box(cur.e).n - j0;
-      if (wrow0 < rend) {
+      const int n_valid = live ? ent_box(cur.e).n - j0 : 0;
+      if (live && wrow0 < rend) {
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {
           const int js = 4 * ks + kq;  // this lane's source within the chunk
@@ -359,6 +411,12 @@ __global__ void __launch_bounds__(kMThreads, SFMM_K2M_MIN_BLOCKS) k2m_translate(
               }
             }
             if ((self && rowi[mt] == j0 + js) || js >= n_valid) gr[mt] = gi[mt] = 0.0;
+            if constexpr (SYM) if (csym) {  // the block, for the transposed product one iteration later
+              const int rl = 16 * warp + 8 * mt + rq;
+              double* gp = &gts0[buf * kMultiRows + rl][swz<CPLX>(rl, js) * SW];
+              gp[0] = gr[mt];
+              if (CPLX) gp[SW - 1] = gi[mt];
+            }
           }
           // A operands of the NP real products: Gr (, Gi, Gr + Gi)
           double g[NP][2];
@@ -374,11 +432,82 @@ __global__ void __launch_bounds__(kMThreads, SFMM_K2M_MIN_BLOCKS) k2m_translate(
           for (int pp = 0; pp < NP; ++pp)
 #pragma unroll
             for (int nb = 0; nb < NB; ++nb) {
-              const double bv = HPASS ? chp->h[ks][pp][nb][lane] : chp->a[ks][pp][nb][lane];
+              const double bv = chp->w[ks][pp][nb][lane];
 #pragma unroll
               for (int mt = 0; mt < 2; ++mt) dmma(C[mt][pp][nb][0], C[mt][pp][nb][1], g[pp][mt], bv);
             }
         }
+      }
+      if constexpr (SYM) if (is_sym(prev)) {
+        // column sums of the previous kSYM chunk: D (8 sources x 8 rhs) +=
+        // G^T (8 sources x 4 rows) * q_b (4 rows x 8 rhs) over the task's rows
+        const int ms = 8 * (warp & 1), nbs = 8 * (warp >> 1);
+        constexpr int NACC = CPLX ? 2 : 4;  // independent accumulator chains
+        double D[NACC][NP][2];
+#pragma unroll
+        for (int u = 0; u < NACC; ++u)
+#pragma unroll
+          for (int pp = 0; pp < NP; ++pp) D[u][pp][0] = D[u][pp][1] = 0.0;
+        const int nks = (task.nrows + 3) >> 2;
+        const GRow* gb = gts0 + (buf ^ 1) * kMultiRows;
+        for (int k0 = 0; k0 < nks; k0 += NACC) {
+#pragma unroll
+          for (int u = 0; u < NACC; ++u) {
+            if (k0 + u < nks) {
+              const int row = 4 * (k0 + u) + kq;
+              const double* gp = &gb[row][swz<CPLX>(row, ms + rq) * SW];
+              const double* qp = &qbs[row][swz<CPLX>(row, nbs + rq) * SW];
+              double ga[NP], qa[NP];
+              ga[0] = gp[0];
+              qa[0] = qp[0];
+              if (CPLX) {
+                ga[NP - 2] = gp[SW - 1];
+                ga[NP - 1] = ga[0] + ga[NP - 2];
+                qa[NP - 2] = qp[SW - 1];
+                qa[NP - 1] = qa[0] + qa[NP - 2];
+              }
+#pragma unroll
+              for (int pp = 0; pp < NP; ++pp) dmma(D[u][pp][0], D[u][pp][1], ga[pp], qa[pp]);
+            }
+          }
+        }
+        // the pair's staged vector is shared by b's row tiles: tile t adds to
+        // what tiles 0..t-1 left (in tile order: deterministic), then counts
+        // this warp into the chunk's flag (4 warps per tile)
+        const int64_t cpt = task.stage + ent_soff(prev.e) + prev.j0;  // the chunk's first point
+        unsigned* flag = a.sflag + cpt / kChunk;
+        if (task.tile > 0) {
+          if (lane == 0)
+            while (ld_acquire_flag(flag) < (unsigned)(kMWarps * task.tile)) __nanosleep(64);
+          __syncwarp();
+        }
+        const int j = prev.j0 + ms + rq;  // this lane's source (column of the block)
+        if (j < ent_box(prev.e).n) {
+          const double scale = CPLX ? 0.25 : (KER == SFMM_LAPLACE3D ? kInv4Pi : -kInv4Pi);
+          double* out = a.stage + ((cpt + ms + rq) * kNRHS + nbs + 2 * kq) * SW;
+          double o[2 * SW];
+#pragma unroll
+          for (int c = 0; c < 2 * SW; ++c) o[c] = task.tile > 0 ? __ldcg(out + c) : 0.0;
+#pragma unroll
+          for (int w = 0; w < 2; ++w) {
+            double t[NP];
+#pragma unroll
+            for (int pp = 0; pp < NP; ++pp) {
+              t[pp] = D[0][pp][w];
+#pragma unroll
+              for (int u = 1; u < NACC; ++u) t[pp] += D[u][pp][w];
+            }
+            if (CPLX) {
+              __stcg(out + 2 * w, o[2 * w] + (t[0] - t[NP - 2]) * scale);
+              __stcg(out + 2 * w + 1, o[2 * w + 1] + (t[NP - 1] - t[0] - t[NP - 2]) * scale);
+            } else {
+              __stcg(out + w, o[w] + t[0] * scale);
+            }
+          }
+        }
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicAdd(flag, 1u);
       }
       if (nxt.e < er.count) {  // the other buffer was last read before the previous barrier
         chp = &chb[buf ^ 1];
@@ -386,6 +515,7 @@ __global__ void __launch_bounds__(kMThreads, SFMM_K2M_MIN_BLOCKS) k2m_translate(
       }
       __syncthreads();
       buf ^= 1;
+      prev = cur;
       cur = nxt;
       if (cur.e < er.count) {
         nxt = next_of(cur);
@@ -466,7 +596,6 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 __device__ __forceinline__ double2 cmulc(double2 t, double2 u) {  // conj(t) * u
   return make_double2(fma(t.x, u.x, t.y * u.y), fma(t.x, u.y, -t.y * u.x));
 }
-__device__ __forceinline__ double mulr(double a, double b) { return a * b; }
 
 // K1m: qhat[i][r] = Q[i][r] + sum_j T[i,j] Q[k+j][r]; one CTA per (box, 8 rows),
 // thread (row, rhs); q_R streamed through shared memory in chunks of 64.
@@ -576,16 +705,56 @@ __global__ void __launch_bounds__(256) k3m_downward(const LevelItem* __restrict_
   }
 }
 
+// K2bm: the staged column sums of the symmetric u pass, added per receiving
+// box in the plan's fixed (b, task, entry) order (deterministic); one CTA per
+// box, consecutive threads on consecutive (point, rhs) scalars.
+template <int SW>
+__global__ void __launch_bounds__(256) k2bm_reduce(const BoxRec* __restrict__ box,
+                                                   const int32_t* __restrict__ recv_box,
+                                                   const int64_t* __restrict__ recv_off,
+                                                   const int64_t* __restrict__ recv_u,
+                                                   const double* __restrict__ St,
+                                                   double* __restrict__ U) {
+  constexpr int64_t kW = (int64_t)kNRHS * SW;  // scalars per point
+  const BoxRec br = box[recv_box[blockIdx.x]];
+  const int64_t e0 = recv_off[blockIdx.x], e1 = recv_off[blockIdx.x + 1];
+  const int64_t len = (int64_t)br.n * kW;
+  for (int64_t i = threadIdx.x; i < len; i += blockDim.x) {
+    double s = 0.0;
+#pragma unroll 8
+    for (int64_t e = e0; e < e1; ++e) s += __ldg(St + recv_u[e] * kW + i);
+    U[br.slot * kW + i] += s;
+  }
+}
+
 int grid_m(int64_t n) {
   const int64_t g = (n + 255) / 256;
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 32));
 }
 
-template <int KER, bool HPASS>
+// dynamic shared memory of the symmetric u pass: two generated blocks and the
+// task's charges, 64 rows x 16 scalars each
+constexpr size_t sym_smem_bytes(bool cplx) {
+  return (size_t)3 * kMultiRows * kChunk * (cplx ? 2 : 1) * sizeof(double);
+}
+
+template <int KER, bool TAB, bool TFO>
+bool allow_sym_smem() {
+  return cudaFuncSetAttribute(k2m_translate<KER, false, TAB, TFO, true>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)sym_smem_bytes(KER == SFMM_HELMHOLTZ3D)) == cudaSuccess;
+}
+
+template <int KER, bool HPASS, bool SYM = false>
 int blocks_per_sm() {
+  constexpr bool CPLX = KER == SFMM_HELMHOLTZ3D;
+  if (SYM && !(allow_sym_smem<KER, CPLX, false>() && allow_sym_smem<KER, CPLX, true>() &&
+               allow_sym_smem<KER, false, false>() && allow_sym_smem<KER, false, true>()))
+    return -1;
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2m_translate<KER, HPASS, KER == SFMM_HELMHOLTZ3D, false>, kMThreads, 0) !=
-      cudaSuccess)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+          &per_sm, k2m_translate<KER, HPASS, CPLX, false, SYM>, kMThreads,
+          SYM ? sym_smem_bytes(CPLX) : 0) != cudaSuccess)
     return -1;
   return std::max(1, per_sm);
 }
@@ -595,20 +764,24 @@ int blocks_per_sm() {
 int configure_multi(DevPlan& p, int device, size_t max_k) {
   int sms = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
-  int bh, b0;
+  int bh, b0, bs;
   if (p.kernel == SFMM_HELMHOLTZ3D) {
     bh = blocks_per_sm<SFMM_HELMHOLTZ3D, true>();
     b0 = blocks_per_sm<SFMM_HELMHOLTZ3D, false>();
+    bs = blocks_per_sm<SFMM_HELMHOLTZ3D, false, true>();
   } else if (p.kernel == SFMM_LAPLACE3D) {
     bh = blocks_per_sm<SFMM_LAPLACE3D, true>();
     b0 = blocks_per_sm<SFMM_LAPLACE3D, false>();
+    bs = blocks_per_sm<SFMM_LAPLACE3D, false, true>();
   } else {
     bh = blocks_per_sm<SFMM_LAPLACE2D, true>();
     b0 = blocks_per_sm<SFMM_LAPLACE2D, false>();
+    bs = blocks_per_sm<SFMM_LAPLACE2D, false, true>();
   }
-  if (bh < 0 || b0 < 0) return -1;
+  if (bh < 0 || b0 < 0 || bs < 0) return -1;
   p.k2m_grid = sms * bh;
   p.k2m_grid0 = sms * b0;
+  p.k2m_grid_sym = sms * bs;
   const size_t sw = p.cplx ? 16 : 8;
   p.down_m_smem = std::max<size_t>(max_k * kNRHS * sw, 16);
   if (p.down_m_smem > 48 * 1024) {
@@ -688,24 +861,41 @@ void launch_translate_m(const DevPlan& p, DevState& s, cudaStream_t st) {
   a.kappa = p.kappa;
   a.tab = p.sc_tab;
   a.ltab = p.log_tab;
+  a.soff = p.ent_soff_m;
+  a.stage = s.stage;
+  a.sflag = s.stage_flags;
+  const bool sym = p.multi_sym && s.stage != nullptr;
   cudaMemsetAsync(p.counter + 2, 0, 2 * sizeof(int), st);
-  // part 0: the u pass over every task; part 1: the uhat pass over the tasks
-  // [0, n_tasks_mh) that own skeleton rows
+  if (sym)
+    cudaMemsetAsync(s.stage_flags, 0,
+                    (size_t)(std::max<int64_t>(p.stage_m_points, kChunk) / kChunk) * sizeof(unsigned), st);
+  // part 0: the u pass over every task (symmetric plans: the folded lists,
+  // then K2bm); part 1: the uhat pass over the tasks [0, n_tasks_mh) that own
+  // skeleton rows (unfolded lists)
   for (int part = 0; part < 2; ++part) {
-    const int64_t t1 = part == 0 ? p.n_tasks_m : p.n_tasks_mh;
+    const int64_t t1 = part == 0 ? (sym ? p.n_tasks_msym : p.n_tasks_m) : p.n_tasks_mh;
     if (t1 <= 0) continue;
-    a.tasks = p.tasks_m;
+    const bool psym = sym && part == 0;
+    a.tasks = psym ? p.tasks_msym : p.tasks_m;
+    a.er = psym ? p.ent_range_msym : p.ent_range_full;
+    a.ent = psym ? p.entries_msym : p.entries_full;
     a.n_tasks = t1;
     a.counter = p.counter + 2 + part;
-    const int grid = (int)std::min<int64_t>(part == 0 ? p.k2m_grid0 : p.k2m_grid, t1);
+    const int grid =
+        (int)std::min<int64_t>(part == 0 ? (psym ? p.k2m_grid_sym : p.k2m_grid0) : p.k2m_grid, t1);
+    const size_t ssm = sym_smem_bytes(p.cplx != 0);
 #define SFMM_K2M_LAUNCH(KER, TAB)                                                   \
   do {                                                                              \
     if (part == 1)                                                                  \
-      k2m_translate<KER, true, TAB, false><<<grid, kMThreads, 0, st>>>(a);          \
+      k2m_translate<KER, true, TAB, false, false><<<grid, kMThreads, 0, st>>>(a);   \
+    else if (psym && p.has_tfo_m)                                                   \
+      k2m_translate<KER, false, TAB, true, true><<<grid, kMThreads, ssm, st>>>(a);  \
+    else if (psym)                                                                  \
+      k2m_translate<KER, false, TAB, false, true><<<grid, kMThreads, ssm, st>>>(a); \
     else if (p.has_tfo_m)                                                           \
-      k2m_translate<KER, false, TAB, true><<<grid, kMThreads, 0, st>>>(a);          \
+      k2m_translate<KER, false, TAB, true, false><<<grid, kMThreads, 0, st>>>(a);   \
     else                                                                            \
-      k2m_translate<KER, false, TAB, false><<<grid, kMThreads, 0, st>>>(a);         \
+      k2m_translate<KER, false, TAB, false, false><<<grid, kMThreads, 0, st>>>(a);  \
   } while (0)
     if (p.kernel == SFMM_HELMHOLTZ3D && p.sc_tab_ok)
       SFMM_K2M_LAUNCH(SFMM_HELMHOLTZ3D, true);
@@ -716,6 +906,14 @@ void launch_translate_m(const DevPlan& p, DevState& s, cudaStream_t st) {
     else
       SFMM_K2M_LAUNCH(SFMM_LAPLACE2D, false);
 #undef SFMM_K2M_LAUNCH
+    if (psym && p.n_recv_m > 0) {
+      if (p.cplx)
+        k2bm_reduce<2><<<(unsigned)p.n_recv_m, 256, 0, st>>>(p.box, p.recv_m_box, p.recv_m_off,
+                                                            p.recv_m_u, s.stage, s.U);
+      else
+        k2bm_reduce<1><<<(unsigned)p.n_recv_m, 256, 0, st>>>(p.box, p.recv_m_box, p.recv_m_off,
+                                                            p.recv_m_u, s.stage, s.U);
+    }
   }
 }
 

@@ -16,6 +16,8 @@ struct DevState {
   double* QH;   // skeleton charges    (n_skel scalars)
   double* U;    // slot potentials     (n_slots scalars)
   double* UH;   // skeleton potentials (n_skel scalars)
+  double* stage = nullptr;  // multi-RHS kSYM column sums (DevPlan::stage_m_points x kNRHS scalars)
+  unsigned* stage_flags = nullptr;  // one chain flag per kChunkM staged points, zeroed per apply
 };
 
 struct DevPlan {
@@ -72,6 +74,17 @@ struct DevPlan {
   int has_tfo_m = 0;   // entries_full holds tfo entries (K2m u pass needs qhat too)
   int k2m_grid, k2m_grid0;
   size_t down_m_smem;
+  // symmetric multi-RHS u pass (HostPlan::multi_sym; staging in DevState::stage)
+  int multi_sym = 0;
+  EntryRange* ent_range_msym;
+  int32_t *entries_msym, *ent_soff_m;
+  Task* tasks_msym;
+  int64_t n_tasks_msym = 0;
+  int64_t stage_m_points = 0;
+  int32_t* recv_m_box;
+  int64_t *recv_m_off, *recv_m_u;
+  int64_t n_recv_m = 0;
+  int k2m_grid_sym = 0;
   int* counter;     // K2 task counters (interior, boundary, multi; reset per launch)
   int* err_flag;    // sticky duplicate-point flag
   int k2_grid;      // persistent K2 CTAs

@@ -258,6 +258,25 @@ struct sfmm_gpu_plan {
     dsm.U = alloc<double>((size_t)hp.n_slots * kNRHS * sw);
     dsm.QH = alloc<double>((size_t)std::max<int64_t>(hp.n_skel, 1) * kNRHS * sw);
     dsm.UH = alloc<double>((size_t)std::max<int64_t>(hp.n_skel, 1) * kNRHS * sw);
+    if (dp.multi_sym) {
+      // staged column sums of the symmetric u pass; without the memory for
+      // them the apply runs the unfolded lists instead
+      void *st = nullptr, *fl = nullptr;
+      const int64_t pts = std::max<int64_t>(dp.stage_m_points, kChunkM);
+      const size_t bytes = (size_t)pts * kNRHS * sw * sizeof(double);
+      const size_t fbytes = (size_t)(pts / kChunkM) * sizeof(unsigned);
+      if (cudaMalloc(&st, bytes) == cudaSuccess && cudaMalloc(&fl, fbytes) == cudaSuccess) {
+        allocs.push_back(st);
+        allocs.push_back(fl);
+        device_bytes += (int64_t)(bytes + fbytes);
+        dsm.stage = static_cast<double*>(st);
+        dsm.stage_flags = static_cast<unsigned*>(fl);
+      } else {
+        cudaGetLastError();
+        if (st) cudaFree(st);
+        dp.multi_sym = 0;
+      }
+    }
   }
 
   // nrhs columns (column-major, original order).  More than one column goes

@@ -41,6 +41,7 @@ PlanOptions plan_options_from_env() {
   if (const char* v = std::getenv("SFMM_SHARD_OVERLAP")) o.overlap = std::atoi(v) != 0;
   if (const char* v = std::getenv("SFMM_SHARD_XSYM")) o.cross_symmetric = std::atoi(v) != 0;
   if (const char* v = std::getenv("SFMM_SYM_CHAIN")) o.sym_chain = std::atoi(v) != 0;
+  if (const char* v = std::getenv("SFMM_MULTI_SYM")) o.multi_sym = std::atoi(v) != 0;
   return o;
 }
 
@@ -609,6 +610,68 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
       for (auto& e : tv) {
         hp.tasks_m.push_back(e.second);
         if (e.second.row0 < hp.box[e.second.box].k) ++hp.n_tasks_mh;
+      }
+    }
+
+    // multi-RHS u pass with symmetric colleague blocks (single rank): the
+    // block of an ifo pair b < c is generated once by b's tasks, which apply
+    // it to b's rows (as kIFO) and, transposed, to b's charges for c's rows
+    // (A_cb = A_bc^T): one staged n_c x kNRHS vector per (task, pair), added
+    // by K2bm per receiving box in (b, task, entry) order -- deterministic.
+    // The uhat pass keeps the unfolded lists (it visits ~1/8 of the columns).
+    hp.multi_sym = hp.symmetric && n_ranks == 1 && opt.multi_sym;
+    if (hp.multi_sym) {
+      hp.ent_range_msym.resize(nb);
+      std::vector<std::vector<int64_t>> inbox(nb);
+      std::vector<std::pair<double, Task>> tv;
+      int64_t cursor = 0;
+      for (int32_t b = 0; b < nb; ++b) {
+        EntryRange& er = hp.ent_range_msym[b];
+        er.begin = (int64_t)hp.entries_msym.size();
+        er.count = 0;
+        if (d.box_level[b] < 1) continue;
+        double cost = 0.0;
+        int32_t soff = 0;
+        sources(b, [&](int32_t c, int mode) {
+          if (mode == kIFO && c != b) {
+            if (c < b) return;  // arrives through b = c's staged column sums
+            hp.entries_msym.push_back((c << kModeBits) | kSYM);
+            hp.ent_soff_m.push_back(soff);
+            soff += (hp.box[c].n + kChunkM - 1) / kChunkM * kChunkM;  // chunk-aligned (chain flags)
+            cost += 1.6 * hp.box[c].n;  // one generation, two DMMA products
+            return;
+          }
+          hp.entries_msym.push_back((c << kModeBits) | mode);
+          hp.ent_soff_m.push_back(-1);
+          cost += hp.box[c].n;
+        });
+        er.count = (int32_t)((int64_t)hp.entries_msym.size() - er.begin);
+        if (er.count == 0) continue;
+        // one staged vector per pair, shared by b's row tiles: tile t adds its
+        // column sums to tile t-1's, chunk by chunk (chain flags), so the
+        // staging is one n_c x kNRHS vector per pair, not per (pair, tile)
+        int32_t tile = 0;
+        for (int32_t r0 = 0; r0 < hp.box[b].n; r0 += kMultiRows, ++tile)
+          tv.push_back({cost * kMultiRows + 64.0,
+                        Task{b, r0, std::min(kMultiRows, hp.box[b].n - r0), tile, cursor}});
+        for (int64_t e = er.begin; e < er.begin + er.count; ++e)
+          if (hp.ent_soff_m[e] >= 0)
+            inbox[hp.entries_msym[e] >> kModeBits].push_back(cursor + hp.ent_soff_m[e]);
+        cursor += soff;
+      }
+      hp.stage_m_points = cursor;
+      // longest first; the tiles of a box keep their order (equal cost, stable
+      // sort), so tile t - 1 is always claimed before tile t waits on it
+      std::stable_sort(tv.begin(), tv.end(),
+                       [](const auto& x, const auto& y) { return x.first > y.first; });
+      hp.tasks_msym.reserve(tv.size());
+      for (auto& e : tv) hp.tasks_msym.push_back(e.second);
+      hp.recv_m_off.assign(1, 0);
+      for (int32_t c = 0; c < nb; ++c) {
+        if (inbox[c].empty()) continue;
+        hp.recv_m_box.push_back(c);
+        hp.recv_m_u.insert(hp.recv_m_u.end(), inbox[c].begin(), inbox[c].end());
+        hp.recv_m_off.push_back((int64_t)hp.recv_m_u.size());
       }
     }
 

@@ -29,6 +29,7 @@ constexpr int kUpRows = 32;                     // K1m rows (skeleton entries) p
 #endif
 constexpr int kUpRows1 = SFMM_K1_ROWS;          // K1 (single rhs) rows per CTA
 constexpr int kDownCols = 256;                  // K3 columns (redundant slots) per CTA
+constexpr int kChunkM = 16;                     // K2m sources per staged chunk
 constexpr int kMultiRows = 64;                  // K2m rows per task (4 warps x two 8-row DMMA tiles)
 constexpr int kDownColsM = 16;                  // K3m columns per CTA (x 16 rhs threads)
 
@@ -103,6 +104,22 @@ struct HostPlan {
   int64_t n_tasks_mh = 0;                     // tasks_m[0, n_tasks_mh) own skeleton rows
   std::vector<LevelItem> down_m_items;
   std::vector<int64_t> down_m_lvl;
+  // multi-RHS u pass with symmetric colleague blocks (single rank,
+  // PlanOptions::multi_sym): the full CSR with each ifo pair of distinct
+  // colleagues b < c folded into one kSYM entry of b; ent_soff_m[e] = first
+  // point of entry e's staged vector within b's stage block (-1: not kSYM;
+  // vectors are kChunkM-aligned).  Task::stage = b's stage block (points; each
+  // staged point carries kNRHS scalars), Task::tile = the task's row tile
+  // (tiles chain their column sums into one vector per pair).  K2bm adds, per
+  // receiving box recv_m_box[i], the staged vectors recv_m_u[recv_m_off[i] ..
+  // recv_m_off[i+1]) in that order.
+  bool multi_sym = false;
+  std::vector<EntryRange> ent_range_msym;
+  std::vector<int32_t> entries_msym, ent_soff_m;
+  std::vector<Task> tasks_msym;
+  int64_t stage_m_points = 0;
+  std::vector<int32_t> recv_m_box;
+  std::vector<int64_t> recv_m_off, recv_m_u;
   // owned interpolation blocks copied from the descriptor into a compact blob
   struct Run {
     int64_t src, dst, len;  // scalars
@@ -150,6 +167,12 @@ struct PlanOptions {
   // each other (K2 +19 % at 1e7), so it is used only when the plan would not
   // fit otherwise (sfmm_gpu.cu) or on request (SFMM_SYM_CHAIN=1).
   int sym_chain = 0;
+  // multi-RHS apply: colleague blocks generated once for both directions
+  // (the transposed DMMA product of K2m, column sums chained over b's row
+  // tiles).  Opt-in (SFMM_MULTI_SYM=1): measured slower on config 4 (DESIGN.md
+  // 3, profiles/r02/k2m_sym_ab.txt) -- K2m is DMMA-bound, the fold saves only
+  // generation and costs occupancy and the tile chain's waits.
+  bool multi_sym = false;
 };
 PlanOptions plan_options_from_env();
 

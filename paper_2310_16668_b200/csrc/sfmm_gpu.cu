@@ -231,6 +231,19 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
       dp.n_tasks_m = (int64_t)hp.tasks_m.size();
       dp.n_tasks_mh = hp.n_tasks_mh;
       dp.down_m_items = p->upload(hp.down_m_items);
+      if (hp.multi_sym) {
+        dp.multi_sym = 1;
+        dp.ent_range_msym = p->upload(hp.ent_range_msym);
+        dp.entries_msym = p->upload(hp.entries_msym);
+        dp.ent_soff_m = p->upload(hp.ent_soff_m);
+        dp.tasks_msym = p->upload(hp.tasks_msym);
+        dp.n_tasks_msym = (int64_t)hp.tasks_msym.size();
+        dp.stage_m_points = hp.stage_m_points;
+        dp.recv_m_box = p->upload(hp.recv_m_box);
+        dp.recv_m_off = p->upload(hp.recv_m_off);
+        dp.recv_m_u = p->upload(hp.recv_m_u);
+        dp.n_recv_m = (int64_t)hp.recv_m_box.size();
+      }
       dp.pack_idx = p->upload(hp.pack_idx);
       dp.unpack_idx = p->upload(hp.unpack_idx);
       dp.n_pack = (int64_t)hp.pack_idx.size();
@@ -261,6 +274,11 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
       std::vector<Task>().swap(hp.tasks);
       std::vector<int32_t>().swap(hp.entries_full);
       std::vector<Task>().swap(hp.tasks_m);
+      std::vector<EntryRange>().swap(hp.ent_range_msym);
+      std::vector<int32_t>().swap(hp.entries_msym);
+      std::vector<int32_t>().swap(hp.ent_soff_m);
+      std::vector<Task>().swap(hp.tasks_msym);
+      std::vector<int64_t>().swap(hp.recv_m_u);
       std::vector<int64_t>().swap(hp.pack_idx);
       std::vector<int64_t>().swap(hp.unpack_idx);
     }
@@ -725,6 +743,8 @@ int sfmm_gpu_plan_info_get(const sfmm_gpu_plan* p, sfmm_gpu_plan_info* info) {
   info->n_level1_pairs = hp.n_l1;
   info->sym_chain = hp.sym_chain ? 1 : 0;
   info->stage_bytes = (int64_t)(hp.stage_size * (hp.cplx ? 16 : 8));
+  info->multi_sym = p->dp.multi_sym;
+  info->multi_stage_bytes = p->dp.stage_m_points * kNRHS * (hp.cplx ? 16 : 8);
   if (p->multi) {
     multi_info(p, info);  // the orchestrating plan has no level lists of its own
   } else {

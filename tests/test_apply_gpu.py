@@ -160,6 +160,33 @@ def test_multi_rhs_matches_oracle_column_loop(kernel, dist, nrhs, kappa):
         assert rel_l2(U[:, r], api.fmm_apply(plan, Q[:, r])) <= 1e-13
 
 
+@pytest.mark.parametrize("kernel,dist,leaf", [(3, "cube", 60), (3, "sphere", 50), (1, "cube", 150),
+                                              (0, "annulus", 40)])
+def test_multi_rhs_symmetric_fold_matches_unfolded(kernel, dist, leaf, monkeypatch):
+    """The symmetric multi-RHS u pass (opt-in SFMM_MULTI_SYM=1: each colleague
+    block generated once, applied transposed through the DMMA, column sums
+    chained over the row tiles) against the unfolded lists and the reference
+    restatement; repeats are bit-identical (fixed tile order)."""
+    n, nrhs = 8000, 16
+    pts = host.generate_points(dist, n, 4)
+    d = ref_descriptor(kernel, pts, leaf, 1e-6, 10.0 if kernel == 3 else 1.0)
+    gen = host.generate_charges_complex if kernel == 3 else host.generate_charges
+    Q = np.stack([gen(n, 500 + r) for r in range(nrhs)], axis=1)
+    monkeypatch.setenv("SFMM_MULTI_SYM", "1")
+    plan = api.GpuPlan(d)
+    assert plan.info().multi_sym == 1
+    U = api.fmm_apply(plan, Q)
+    assert plan.info().multi_stage_bytes > 0
+    assert np.array_equal(U, api.fmm_apply(plan, Q))
+    monkeypatch.setenv("SFMM_MULTI_SYM", "0")
+    plain = api.GpuPlan(d)
+    assert plain.info().multi_sym == 0
+    U0 = api.fmm_apply(plain, Q)
+    assert rel_l2(U, U0) <= 1e-13
+    U_ref, _ = po.oracle_apply(d, Q)
+    assert rel_l2(U, U_ref) <= PARITY
+
+
 @pytest.mark.parametrize("kernel,kappa", [(1, 1.0), (3, 10.0)])
 def test_multi_rhs_target_at_padding_coordinate(kernel, kappa):
     """K2m pads partial source chunks with a fixed far coordinate; a real
