@@ -338,6 +338,23 @@ int sfmm_gpu_build_tree(int dim, int64_t n, const double* pts, int leaf_cap, int
 int sfmm_gpu_tree_arrays(const sfmm_gpu_tree* tree, sfmm_tree_arrays* arrays);
 void sfmm_gpu_tree_destroy(sfmm_gpu_tree* tree);
 
+/* Distributed precompute (config 5 scale: no rank holds every operator).
+ * Every rank builds the same tree (sfmm_gpu_build_tree is deterministic),
+ * sfmm_gpu_subtree_owners picks each level-1 subtree's rank from the tree
+ * alone (Morton-contiguous ranges balancing a near-field work estimate;
+ * owner gets n_boxes entries, -1 above level 1), each rank skeletonizes its
+ * subtrees (sfmm_gpu_build_skeletons_subset with mask owner[b] == rank), the
+ * ranks exchange the index data of their boxes (index_vec, skel_pos, red_pos,
+ * parent_offset: a few bytes per point) to form the full descriptor, and
+ * sfmm_gpu_plan_create_sharded_owned builds the rank plan with that ownership
+ * from the rank's own operators (the subset result's device T, box order).
+ * The rank plans are those of sfmm_gpu_plan_create_sharded_T with the same
+ * ownership: attach NCCL, apply as usual. */
+int sfmm_gpu_subtree_owners(const sfmm_tree_arrays* tree, int n_ranks, int32_t* owner);
+int sfmm_gpu_plan_create_sharded_owned(const sfmm_plan_desc* desc, const void* T_owned_dev,
+                                       int device, int n_ranks, int rank, const int32_t* owner,
+                                       sfmm_gpu_plan** out);
+
 /*
  * GPU skeletonization: the device counterpart of the
  * reference's build_skeletons (/root/reference/proj/src/skeleton.cpp:184-260).
@@ -370,6 +387,18 @@ typedef struct sfmm_tree_desc {
 int sfmm_gpu_build_skeletons(const sfmm_tree_desc* tree, int kernel, double kappa, double tol,
                              double proxy_radius, int proxy_edge2d, int proxy_face3d, int device,
                              sfmm_skel_result** out);
+/* Distributed precompute: skeletonizes only the boxes with box_mask[b] != 0
+ * (n_boxes entries; whole subtrees -- a masked box's children must be masked,
+ * else SFMM_EINVAL), e.g. the level-1 subtrees a rank owns
+ * (sfmm_gpu_subtree_owners).  The other boxes come out empty (n = k = 0, no
+ * T), so the result's T is exactly the rank's owned operators in box order --
+ * the T_owned_dev blob of sfmm_gpu_plan_create_sharded_owned.  Each masked
+ * box's skeleton is bit-identical to the full build's (it depends only on its
+ * own subtree).  box_mask = NULL is sfmm_gpu_build_skeletons. */
+int sfmm_gpu_build_skeletons_subset(const sfmm_tree_desc* tree, int kernel, double kappa,
+                                    double tol, double proxy_radius, int proxy_edge2d,
+                                    int proxy_face3d, int device, const uint8_t* box_mask,
+                                    sfmm_skel_result** out);
 /* Points the skeleton fields of *desc (iv_off, iv, sk_off, skel_pos, rd_off,
  * red_pos, T_off, T, box_parent_offset) at the result's arrays and returns
  * k_max, proj_scalars and the number of saturated boxes.  The interpolation

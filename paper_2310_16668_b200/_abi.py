@@ -370,6 +370,15 @@ def gpu_lib() -> C.CDLL:
     lib.sfmm_gpu_plan_attach_nccl.restype = C.c_int
     lib.sfmm_gpu_set_output.argtypes = [vp, C.c_int]
     lib.sfmm_gpu_set_output.restype = C.c_int
+    lib.sfmm_gpu_build_skeletons_subset.argtypes = [C.POINTER(TreeDesc), C.c_int, C.c_double,
+                                                    C.c_double, C.c_double, C.c_int, C.c_int,
+                                                    C.c_int, vp, C.POINTER(vp)]
+    lib.sfmm_gpu_build_skeletons_subset.restype = C.c_int
+    lib.sfmm_gpu_subtree_owners.argtypes = [C.POINTER(TreeArrays), C.c_int, vp]
+    lib.sfmm_gpu_subtree_owners.restype = C.c_int
+    lib.sfmm_gpu_plan_create_sharded_owned.argtypes = [C.POINTER(PlanDesc), vp, C.c_int, C.c_int,
+                                                       C.c_int, vp, C.POINTER(vp)]
+    lib.sfmm_gpu_plan_create_sharded_owned.restype = C.c_int
     _gpu_lib = lib
     return lib
 
@@ -387,7 +396,8 @@ GPU_SYMBOLS = [
     "sfmm_gpu_shard_info2", "sfmm_gpu_apply_mid", "sfmm_gpu_apply_fin",
     "sfmm_gpu_shard_T_runs", "sfmm_gpu_copy_runs", "sfmm_gpu_plan_create_sharded_T",
     "sfmm_gpu_plan_create_multi", "sfmm_gpu_plan_create_multi_skel", "sfmm_gpu_nccl_unique_id",
-    "sfmm_gpu_plan_attach_nccl", "sfmm_gpu_set_output",
+    "sfmm_gpu_plan_attach_nccl", "sfmm_gpu_set_output", "sfmm_gpu_build_skeletons_subset",
+    "sfmm_gpu_subtree_owners", "sfmm_gpu_plan_create_sharded_owned",
 ]
 SFMM_OUTPUT_FULL, SFMM_OUTPUT_OWNED = 0, 1
 

@@ -28,6 +28,22 @@ constexpr double kInv4Pi = 0.0795774715459476678844418816862571810;
 // the parent's slot (k1_copy's work, apply.cpp:124-131, fused here so the
 // leaf charges are read once).  int32 maps: 12 B of indices per point.
 template <class S>
+__device__ __forceinline__ void k0_point(int64_t t, const int32_t* __restrict__ slot,
+                                         const int32_t* __restrict__ orig,
+                                         const int32_t* __restrict__ hat,
+                                         const int32_t* __restrict__ up_dst,
+                                         const S* __restrict__ q, S* __restrict__ Q,
+                                         S* __restrict__ QH) {
+  const S v = __ldg(q + __ldg(orig + t));
+  Q[__ldg(slot + t)] = v;
+  const int32_t h = __ldg(hat + t);
+  if (h >= 0) {
+    QH[h] = v;
+    Q[__ldg(up_dst + h)] = v;
+  }
+}
+
+template <class S>
 __global__ void __launch_bounds__(256) k0_gather(const int32_t* __restrict__ slot,
                                                  const int32_t* __restrict__ orig,
                                                  const int32_t* __restrict__ hat,
@@ -35,15 +51,8 @@ __global__ void __launch_bounds__(256) k0_gather(const int32_t* __restrict__ slo
                                                  const S* __restrict__ q, S* __restrict__ Q,
                                                  S* __restrict__ QH) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const S v = __ldg(q + __ldg(orig + t));
-    Q[__ldg(slot + t)] = v;
-    const int32_t h = __ldg(hat + t);
-    if (h >= 0) {
-      QH[h] = v;
-      Q[__ldg(up_dst + h)] = v;
-    }
-  }
+       t += (int64_t)gridDim.x * blockDim.x)
+    k0_point<S>(t, slot, orig, hat, up_dst, q, Q, QH);
 }
 
 // K4 + the leaf-level K3 copy: u[orig] = U[slot] (+ uhat + the parent's
@@ -70,15 +79,16 @@ __device__ __forceinline__ double warp_sum(double v) {
 // the box) is staged in shared memory first (measured: 2.9 vs 2.3 TB/s for
 // reading it through the read-only cache).
 constexpr int kUpRowsPerWarp = 4;
-__global__ void __launch_bounds__(kUpThreads) k1_upward_real(
-    const LevelItem* __restrict__ items, const BoxRec* __restrict__ box,
-    const int64_t* __restrict__ T_off, const double* __restrict__ T, double* __restrict__ Q,
-    double* __restrict__ QH, const int32_t* __restrict__ up_dst) {
-  const LevelItem it = items[blockIdx.x];
+// Q is read through L2 (ld.cg): in the persistent tree pass the charges were
+// written by other CTAs of the same launch.
+__device__ __forceinline__ void k1_real_item(const LevelItem it, const BoxRec* __restrict__ box,
+                                             const int64_t* __restrict__ T_off,
+                                             const double* __restrict__ T, double* __restrict__ Q,
+                                             double* __restrict__ QH,
+                                             const int32_t* __restrict__ up_dst, double* smq) {
   const BoxRec br = box[it.box];
   const int k = br.k, r = br.n - br.k;
-  extern __shared__ double smq[];
-  for (int j = threadIdx.x; j < r; j += blockDim.x) smq[j] = Q[br.slot + k + j];
+  for (int j = threadIdx.x; j < r; j += blockDim.x) smq[j] = __ldcg(Q + br.slot + k + j);
   __syncthreads();
   const double* qR = smq;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -103,12 +113,20 @@ __global__ void __launch_bounds__(kUpThreads) k1_upward_real(
       const double s = warp_sum(acc[m]);
       const int i = i0 + m;
       if (lane == 0 && i < i1) {
-        const double v = Q[br.slot + i] + s;
+        const double v = __ldcg(Q + br.slot + i) + s;
         QH[br.skel + i] = v;
         Q[up_dst[br.skel + i]] = v;
       }
     }
   }
+}
+
+__global__ void __launch_bounds__(kUpThreads) k1_upward_real(
+    const LevelItem* __restrict__ items, const BoxRec* __restrict__ box,
+    const int64_t* __restrict__ T_off, const double* __restrict__ T, double* __restrict__ Q,
+    double* __restrict__ QH, const int32_t* __restrict__ up_dst) {
+  extern __shared__ double smq[];
+  k1_real_item(items[blockIdx.x], box, T_off, T, Q, QH, up_dst, smq);
 }
 
 // K1, real, with the T rows staged by the bulk-copy engine (TMA, cp.async.bulk
@@ -265,15 +283,14 @@ __global__ void __launch_bounds__(kK1BulkThreads, 1) k1_upward_real_bulk(
 }
 
 // K1, complex.
-__global__ void __launch_bounds__(kUpThreads) k1_upward_cplx(
-    const LevelItem* __restrict__ items, const BoxRec* __restrict__ box,
-    const int64_t* __restrict__ T_off, const double2* __restrict__ T, double2* __restrict__ Q,
-    double2* __restrict__ QH, const int32_t* __restrict__ up_dst) {
-  extern __shared__ double2 smq2[];
-  const LevelItem it = items[blockIdx.x];
+__device__ __forceinline__ void k1_cplx_item(const LevelItem it, const BoxRec* __restrict__ box,
+                                             const int64_t* __restrict__ T_off,
+                                             const double2* __restrict__ T,
+                                             double2* __restrict__ Q, double2* __restrict__ QH,
+                                             const int32_t* __restrict__ up_dst, double2* smq2) {
   const BoxRec br = box[it.box];
   const int k = br.k, r = br.n - br.k;
-  for (int j = threadIdx.x; j < r; j += blockDim.x) smq2[j] = Q[br.slot + k + j];
+  for (int j = threadIdx.x; j < r; j += blockDim.x) smq2[j] = __ldcg(Q + br.slot + k + j);
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const double2* Tb = T + T_off[it.box];
@@ -289,12 +306,20 @@ __global__ void __launch_bounds__(kUpThreads) k1_upward_cplx(
     ar = warp_sum(ar);
     ai = warp_sum(ai);
     if (lane == 0) {
-      const double2 q = Q[br.slot + i];
+      const double2 q = __ldcg(Q + br.slot + i);
       const double2 v = make_double2(q.x + ar, q.y + ai);
       QH[br.skel + i] = v;
       Q[up_dst[br.skel + i]] = v;
     }
   }
+}
+
+__global__ void __launch_bounds__(kUpThreads) k1_upward_cplx(
+    const LevelItem* __restrict__ items, const BoxRec* __restrict__ box,
+    const int64_t* __restrict__ T_off, const double2* __restrict__ T, double2* __restrict__ Q,
+    double2* __restrict__ QH, const int32_t* __restrict__ up_dst) {
+  extern __shared__ double2 smq2[];
+  k1_cplx_item(items[blockIdx.x], box, T_off, T, Q, QH, up_dst, smq2);
 }
 
 // K1 / K3 for uncompressed boxes (k = n, r = 0: no interpolation block), one
@@ -305,6 +330,19 @@ __device__ __forceinline__ double2 add_s(double2 a, double2 b) {
 }
 
 template <class S>
+__device__ __forceinline__ void k4_point(int64_t t, const int32_t* __restrict__ slot,
+                                         const int32_t* __restrict__ orig,
+                                         const int32_t* __restrict__ hat,
+                                         const int32_t* __restrict__ up_dst,
+                                         const S* __restrict__ U, const S* __restrict__ UH,
+                                         S* __restrict__ u) {
+  S v = __ldcg(U + __ldg(slot + t));
+  const int32_t h = __ldg(hat + t);
+  if (h >= 0) v = add_s(v, add_s(__ldcg(UH + h), __ldcg(U + __ldg(up_dst + h))));
+  u[__ldg(orig + t)] = v;
+}
+
+template <class S>
 __global__ void __launch_bounds__(256) k4_scatter(const int32_t* __restrict__ slot,
                                                   const int32_t* __restrict__ orig,
                                                   const int32_t* __restrict__ hat,
@@ -312,12 +350,27 @@ __global__ void __launch_bounds__(256) k4_scatter(const int32_t* __restrict__ sl
                                                   const S* __restrict__ U,
                                                   const S* __restrict__ UH, S* __restrict__ u) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    S v = U[__ldg(slot + t)];
-    const int32_t h = __ldg(hat + t);
-    if (h >= 0) v = add_s(v, add_s(UH[h], U[__ldg(up_dst + h)]));
-    u[__ldg(orig + t)] = v;
+       t += (int64_t)gridDim.x * blockDim.x)
+    k4_point<S>(t, slot, orig, hat, up_dst, U, UH, u);
+}
+
+template <class S>
+__device__ __forceinline__ void k1_copy_box(const BoxRec br, int lane, S* __restrict__ Q,
+                                            S* __restrict__ QH, const int32_t* __restrict__ up_dst) {
+  for (int i = lane; i < br.k; i += 32) {
+    const S v = __ldcg(Q + br.slot + i);
+    QH[br.skel + i] = v;
+    Q[up_dst[br.skel + i]] = v;
   }
+}
+
+template <class S>
+__device__ __forceinline__ void k3_copy_box(const BoxRec br, int lane, S* __restrict__ U,
+                                            const S* __restrict__ UH,
+                                            const int32_t* __restrict__ up_dst) {
+  for (int i = lane; i < br.k; i += 32)
+    U[br.slot + i] = add_s(__ldcg(U + br.slot + i),
+                           add_s(__ldcg(UH + br.skel + i), __ldcg(U + up_dst[br.skel + i])));
 }
 
 template <class S>
@@ -326,12 +379,7 @@ __global__ void __launch_bounds__(256) k1_copy(const int32_t* __restrict__ boxes
                                                S* __restrict__ QH, const int32_t* __restrict__ up_dst) {
   const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (w >= nbox) return;
-  const BoxRec br = box[boxes[w]];
-  for (int i = threadIdx.x & 31; i < br.k; i += 32) {
-    const S v = Q[br.slot + i];
-    QH[br.skel + i] = v;
-    Q[up_dst[br.skel + i]] = v;
-  }
+  k1_copy_box<S>(box[boxes[w]], threadIdx.x & 31, Q, QH, up_dst);
 }
 
 template <class S>
@@ -341,24 +389,23 @@ __global__ void __launch_bounds__(256) k3_copy(const int32_t* __restrict__ boxes
                                                const int32_t* __restrict__ up_dst) {
   const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (w >= nbox) return;
-  const BoxRec br = box[boxes[w]];
-  for (int i = threadIdx.x & 31; i < br.k; i += 32)
-    U[br.slot + i] = add_s(U[br.slot + i], add_s(UH[br.skel + i], U[up_dst[br.skel + i]]));
+  k3_copy_box<S>(box[boxes[w]], threadIdx.x & 31, U, UH, up_dst);
 }
 
 // K3, real: uhat = UH + U[parent slice]; U_S += uhat; U_R += T^T uhat.
-__global__ void __launch_bounds__(kDownCols) k3_downward_real(
-    const LevelItem* __restrict__ items, const BoxRec* __restrict__ box,
-    const int64_t* __restrict__ T_off, const double* __restrict__ T, double* __restrict__ U,
-    const double* __restrict__ UH, const int32_t* __restrict__ up_dst) {
-  extern __shared__ double smu[];
-  const LevelItem it = items[blockIdx.x];
+// U is read through L2 (ld.cg): in the persistent tree pass the parent's
+// potentials were written by other CTAs of the same launch.
+__device__ __forceinline__ void k3_real_item(const LevelItem it, const BoxRec* __restrict__ box,
+                                             const int64_t* __restrict__ T_off,
+                                             const double* __restrict__ T, double* __restrict__ U,
+                                             const double* __restrict__ UH,
+                                             const int32_t* __restrict__ up_dst, double* smu) {
   const BoxRec br = box[it.box];
   const int k = br.k, r = br.n - br.k;
   for (int i = threadIdx.x; i < k; i += blockDim.x) {
-    const double v = UH[br.skel + i] + U[up_dst[br.skel + i]];
+    const double v = __ldcg(UH + br.skel + i) + __ldcg(U + up_dst[br.skel + i]);
     smu[i] = v;
-    if (it.first == 0) U[br.slot + i] += v;
+    if (it.first == 0) U[br.slot + i] = __ldcg(U + br.slot + i) + v;
   }
   __syncthreads();
   const int j = it.first + threadIdx.x;
@@ -367,24 +414,31 @@ __global__ void __launch_bounds__(kDownCols) k3_downward_real(
   double acc = 0.0;
 #pragma unroll 4
   for (int i = 0; i < k; ++i) acc = fma(Tb[(int64_t)i * r], smu[i], acc);
-  U[br.slot + k + j] += acc;
+  U[br.slot + k + j] = __ldcg(U + br.slot + k + j) + acc;
+}
+
+__global__ void __launch_bounds__(kDownCols) k3_downward_real(
+    const LevelItem* __restrict__ items, const BoxRec* __restrict__ box,
+    const int64_t* __restrict__ T_off, const double* __restrict__ T, double* __restrict__ U,
+    const double* __restrict__ UH, const int32_t* __restrict__ up_dst) {
+  extern __shared__ double smu[];
+  k3_real_item(items[blockIdx.x], box, T_off, T, U, UH, up_dst, smu);
 }
 
 // K3, complex: U_R += conj(T)^T uhat (apply.cpp:290).
-__global__ void __launch_bounds__(kDownCols) k3_downward_cplx(
-    const LevelItem* __restrict__ items, const BoxRec* __restrict__ box,
-    const int64_t* __restrict__ T_off, const double2* __restrict__ T, double2* __restrict__ U,
-    const double2* __restrict__ UH, const int32_t* __restrict__ up_dst) {
-  extern __shared__ double2 smu2[];
-  const LevelItem it = items[blockIdx.x];
+__device__ __forceinline__ void k3_cplx_item(const LevelItem it, const BoxRec* __restrict__ box,
+                                             const int64_t* __restrict__ T_off,
+                                             const double2* __restrict__ T,
+                                             double2* __restrict__ U, const double2* __restrict__ UH,
+                                             const int32_t* __restrict__ up_dst, double2* smu2) {
   const BoxRec br = box[it.box];
   const int k = br.k, r = br.n - br.k;
   for (int i = threadIdx.x; i < k; i += blockDim.x) {
-    const double2 a = UH[br.skel + i], b = U[up_dst[br.skel + i]];
+    const double2 a = __ldcg(UH + br.skel + i), b = __ldcg(U + up_dst[br.skel + i]);
     const double2 v = make_double2(a.x + b.x, a.y + b.y);
     smu2[i] = v;
     if (it.first == 0) {
-      double2 o = U[br.slot + i];
+      double2 o = __ldcg(U + br.slot + i);
       U[br.slot + i] = make_double2(o.x + v.x, o.y + v.y);
     }
   }
@@ -399,8 +453,16 @@ __global__ void __launch_bounds__(kDownCols) k3_downward_cplx(
     ar = fma(t.x, u.x, fma(t.y, u.y, ar));
     ai = fma(t.x, u.y, fma(-t.y, u.x, ai));
   }
-  double2 o = U[br.slot + k + j];
+  double2 o = __ldcg(U + br.slot + k + j);
   U[br.slot + k + j] = make_double2(o.x + ar, o.y + ai);
+}
+
+__global__ void __launch_bounds__(kDownCols) k3_downward_cplx(
+    const LevelItem* __restrict__ items, const BoxRec* __restrict__ box,
+    const int64_t* __restrict__ T_off, const double2* __restrict__ T, double2* __restrict__ U,
+    const double2* __restrict__ UH, const int32_t* __restrict__ up_dst) {
+  extern __shared__ double2 smu2[];
+  k3_cplx_item(items[blockIdx.x], box, T_off, T, U, UH, up_dst, smu2);
 }
 
 // Kernel value exactly as the reference writes it (kernel.hpp:40-71), with
@@ -552,6 +614,100 @@ __global__ void k_build_leaf_maps(SlotBuildArgs a) {
   }
 }
 
+// ---- persistent tree passes (small, launch-bound plans) --------------------
+// One launch runs the whole upward pass (K0, then every level deepest first)
+// or the whole downward pass (every level coarsest first, then K4).  CTAs
+// claim jobs in stage order from a counter; a job of stage s waits until the
+// finished-job counter reaches the number of jobs in stages < s.  Jobs of
+// stage >= s cannot start before that, so the count is reached exactly when
+// every earlier stage is complete (empty stages included).  Deadlock-free:
+// every job waited on was claimed earlier by a running CTA.  Same arithmetic
+// as the per-level kernels (bit-identical).
+struct TreePassArgs {
+  const TreeJob* jobs;
+  int64_t n_jobs;
+  const int32_t* stage_first;  // jobs in the stages before stage s
+  int* counter;
+  int* done;                    // finished jobs
+  const LevelItem* items;
+  const int32_t* copy_boxes;
+  const BoxRec* box;
+  const int64_t* T_off;
+  const double* T;
+  const int32_t *slot, *orig, *hat, *up_dst;
+  int64_t n_points;
+  const double* q;  // up: charges in
+  double* u;        // down: potentials out
+  double *Q, *QH, *U, *UH;
+};
+
+__device__ __forceinline__ int ld_acquire_i32(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <class S, bool UP>
+__global__ void __launch_bounds__(kUpThreads) k_tree_persist(TreePassArgs a) {
+  static_assert(kUpThreads == kDownCols, "one block shape for K1 and K3 items");
+  extern __shared__ __align__(16) unsigned char tp_smem[];
+  S* sm = reinterpret_cast<S*>(tp_smem);
+  __shared__ int s_job;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (;;) {
+    if (threadIdx.x == 0) s_job = atomicAdd(a.counter, 1);
+    __syncthreads();
+    const int64_t jn = s_job;
+    if (jn >= a.n_jobs) return;
+    const TreeJob job = a.jobs[jn];
+    if (job.stage > 0 && threadIdx.x == 0)
+      while (ld_acquire_i32(a.done) < a.stage_first[job.stage]) __nanosleep(32);
+    __syncthreads();
+    if (job.kind == kJobGather || job.kind == kJobScatter) {
+      const int64_t t0 = (int64_t)job.a * kPointsPerJob;
+      const int64_t t1 = t0 + kPointsPerJob < a.n_points ? t0 + kPointsPerJob : a.n_points;
+      for (int64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
+        if (UP)
+          k0_point<S>(t, a.slot, a.orig, a.hat, a.up_dst, reinterpret_cast<const S*>(a.q),
+                      reinterpret_cast<S*>(a.Q), reinterpret_cast<S*>(a.QH));
+        else
+          k4_point<S>(t, a.slot, a.orig, a.hat, a.up_dst, reinterpret_cast<const S*>(a.U),
+                      reinterpret_cast<const S*>(a.UH), reinterpret_cast<S*>(a.u));
+      }
+    } else if (job.kind == kJobCopy) {
+      if (warp < job.b) {
+        const BoxRec br = a.box[a.copy_boxes[job.a + warp]];
+        if (UP)
+          k1_copy_box<S>(br, lane, reinterpret_cast<S*>(a.Q), reinterpret_cast<S*>(a.QH), a.up_dst);
+        else
+          k3_copy_box<S>(br, lane, reinterpret_cast<S*>(a.U), reinterpret_cast<const S*>(a.UH),
+                         a.up_dst);
+      }
+    } else {
+      const LevelItem it = a.items[job.a];
+      if constexpr (sizeof(S) == 16) {
+        if (UP)
+          k1_cplx_item(it, a.box, a.T_off, reinterpret_cast<const double2*>(a.T),
+                       reinterpret_cast<double2*>(a.Q), reinterpret_cast<double2*>(a.QH), a.up_dst,
+                       reinterpret_cast<double2*>(sm));
+        else
+          k3_cplx_item(it, a.box, a.T_off, reinterpret_cast<const double2*>(a.T),
+                       reinterpret_cast<double2*>(a.U), reinterpret_cast<const double2*>(a.UH),
+                       a.up_dst, reinterpret_cast<double2*>(sm));
+      } else {
+        if (UP)
+          k1_real_item(it, a.box, a.T_off, a.T, a.Q, a.QH, a.up_dst, reinterpret_cast<double*>(sm));
+        else
+          k3_real_item(it, a.box, a.T_off, a.T, a.U, a.UH, a.up_dst, reinterpret_cast<double*>(sm));
+      }
+    }
+    // publish this job's writes, then count it into its stage
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(a.done, 1);
+  }
+}
+
 int grid_for(int64_t n, int threads) {
   const int64_t g = (n + threads - 1) / threads;
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 32));
@@ -631,6 +787,70 @@ void launch_downward(const DevPlan& p, const HostPlan& hp, int level, DevState& 
   else
     k3_downward_real<<<(unsigned)(i1 - i0), kDownCols, p.down_smem, st>>>(
         p.down_items + i0, p.box, p.T_off, p.T, s.U, s.UH, p.up_dst);
+}
+
+namespace {
+
+TreePassArgs tree_args(const DevPlan& p, bool up, const DevState& s) {
+  TreePassArgs a;
+  a.jobs = up ? p.up_jobs : p.down_jobs;
+  a.n_jobs = up ? p.n_up_jobs : p.n_down_jobs;
+  a.stage_first = up ? p.up_stage_first : p.down_stage_first;
+  a.counter = p.tree_sync + (up ? 0 : 1);
+  a.done = p.tree_sync + (up ? 2 : 3);
+  a.items = up ? p.up1_items : p.down_items;
+  a.copy_boxes = p.copy_boxes;
+  a.box = p.box;
+  a.T_off = p.T_off;
+  a.T = p.T;
+  a.slot = p.leaf_slot;
+  a.orig = p.leaf_orig;
+  a.hat = p.leaf_hat;
+  a.up_dst = p.up_dst;
+  a.n_points = p.n_owned_points;
+  a.q = nullptr;
+  a.u = nullptr;
+  a.Q = s.Q;
+  a.QH = s.QH;
+  a.U = s.U;
+  a.UH = s.UH;
+  return a;
+}
+
+}  // namespace
+
+void launch_upward_all(const DevPlan& p, const HostPlan& hp, const double* q, DevState& s,
+                       cudaStream_t st) {
+  if (!p.tree_persist) {
+    launch_gather(p, q, s, st);
+    for (int l = hp.depth; l >= 2; --l) launch_upward(p, hp, l, s, st);
+    return;
+  }
+  // counters and done flags of both passes (the downward launch follows K2)
+  cudaMemsetAsync(p.tree_sync, 0, sizeof(int) * 4, st);
+  TreePassArgs a = tree_args(p, true, s);
+  a.q = q;
+  const unsigned g = (unsigned)std::min<int64_t>(p.persist_grid, std::max<int64_t>(p.n_up_jobs, 1));
+  if (p.cplx)
+    k_tree_persist<double2, true><<<g, kUpThreads, p.persist_smem, st>>>(a);
+  else
+    k_tree_persist<double, true><<<g, kUpThreads, p.persist_smem, st>>>(a);
+}
+
+void launch_downward_all(const DevPlan& p, const HostPlan& hp, DevState& s, double* u,
+                         cudaStream_t st) {
+  if (!p.tree_persist) {
+    for (int l = 2; l <= hp.depth; ++l) launch_downward(p, hp, l, s, st);
+    launch_scatter(p, s, u, st);
+    return;
+  }
+  TreePassArgs a = tree_args(p, false, s);
+  a.u = u;
+  const unsigned g = (unsigned)std::min<int64_t>(p.persist_grid, std::max<int64_t>(p.n_down_jobs, 1));
+  if (p.cplx)
+    k_tree_persist<double2, false><<<g, kUpThreads, p.persist_smem, st>>>(a);
+  else
+    k_tree_persist<double, false><<<g, kUpThreads, p.persist_smem, st>>>(a);
 }
 
 void launch_direct_fallback(const DevPlan& p, const double* q, double* u, cudaStream_t st) {
@@ -777,6 +997,27 @@ int configure_tree_kernels(DevPlan& p, size_t max_r, size_t max_k) {
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     p.k1_bulk_grid = sms;  // one persistent CTA per SM (the ring takes ~160 KB)
     p.k1_bulk = 1;
+  }
+  if (p.tree_persist) {
+    p.persist_smem = std::max(p.up_smem, std::max<size_t>(max_k * sw, 16));
+    const void* f[4] = {(const void*)k_tree_persist<double, true>,
+                        (const void*)k_tree_persist<double, false>,
+                        (const void*)k_tree_persist<double2, true>,
+                        (const void*)k_tree_persist<double2, false>};
+    int per_sm = 0, dev = 0, sms = 148;
+    for (const void* fn : f)
+      if (p.persist_smem > 48 * 1024 &&
+          cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)p.persist_smem) != cudaSuccess)
+        return -1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, p.cplx ? (const void*)k_tree_persist<double2, true>
+                            : (const void*)k_tree_persist<double, true>,
+            kUpThreads, p.persist_smem) != cudaSuccess)
+      return -1;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    p.persist_grid = sms * std::max(1, per_sm);
   }
   p.down_smem = std::max<size_t>(max_k * sw, 16);
   if (p.down_smem > 48 * 1024) {

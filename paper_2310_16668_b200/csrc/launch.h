@@ -94,6 +94,14 @@ struct DevPlan {
   size_t up_bulk_smem = 0;
   int up_bulk_qr = 0;       // q_R doubles per ring stage
   int k1_bulk_grid = 148;   // persistent CTAs (one per SM)
+  // persistent tree passes (HostPlan::tree_persist)
+  int tree_persist = 0;
+  TreeJob *up_jobs = nullptr, *down_jobs = nullptr;
+  int32_t *up_stage_first = nullptr, *down_stage_first = nullptr;  // jobs before each stage
+  int64_t n_up_jobs = 0, n_down_jobs = 0;
+  int* tree_sync = nullptr;  // [up counter, down counter, up done, down done]
+  int persist_grid = 0;
+  size_t persist_smem = 0;
 };
 
 // K0: Q[leaf_slot[t]] = q[leaf_orig[t]] (+ the uncompressed leaves' qhat copy)
@@ -113,6 +121,12 @@ void launch_xpack(const DevPlan& p, double* buf, cudaStream_t st);
 // ghost exchange: buf[i] = [Q | QH][pack_idx[i]]  /  [Q | QH][unpack_idx[i]] = buf[i]
 void launch_pack(const DevPlan& p, const DevState& s, double* buf, cudaStream_t st);
 void launch_unpack(const DevPlan& p, DevState& s, const double* buf, cudaStream_t st);
+// K0 + K1 of every level (one launch per level, or one persistent launch for
+// small plans) / K3 of every level + K4
+void launch_upward_all(const DevPlan& p, const HostPlan& hp, const double* q, DevState& s,
+                       cudaStream_t st);
+void launch_downward_all(const DevPlan& p, const HostPlan& hp, DevState& s, double* u,
+                         cudaStream_t st);
 // K3: one tree level of the downward pass (level >= 2)
 void launch_downward(const DevPlan& p, const HostPlan& hp, int level, DevState& s,
                      cudaStream_t st);

@@ -233,17 +233,27 @@ struct sfmm_gpu_plan {
     }
     const int slot = (timing && n_timed < kMaxTimed) ? n_timed++ : -1;
     if (slot >= 0) mark(slot, 0, st);
-    launch_gather(dp, q, ds, st);
-    if (slot >= 0) mark(slot, 1, st);
-    for (int l = hp.depth; l >= 2; --l) launch_upward(dp, hp, l, ds, st);
+    if (dp.tree_persist) {  // one launch: the gather phase reads 0, upward holds both
+      if (slot >= 0) mark(slot, 1, st);
+      launch_upward_all(dp, hp, q, ds, st);
+    } else {
+      launch_gather(dp, q, ds, st);
+      if (slot >= 0) mark(slot, 1, st);
+      for (int l = hp.depth; l >= 2; --l) launch_upward(dp, hp, l, ds, st);
+    }
     if (slot >= 0) mark(slot, 2, st);
     if (time_k2) ck(cudaEventRecord(ev_k2a, st), "event");
     launch_translate(dp, ds, st);
     if (time_k2) ck(cudaEventRecord(ev_k2b, st), "event");
     if (slot >= 0) mark(slot, 3, st);
-    for (int l = 2; l <= hp.depth; ++l) launch_downward(dp, hp, l, ds, st);
-    if (slot >= 0) mark(slot, 4, st);
-    launch_scatter(dp, ds, u, st);
+    if (dp.tree_persist) {  // one launch: downward holds the scatter, which reads 0
+      launch_downward_all(dp, hp, ds, u, st);
+      if (slot >= 0) mark(slot, 4, st);
+    } else {
+      for (int l = 2; l <= hp.depth; ++l) launch_downward(dp, hp, l, ds, st);
+      if (slot >= 0) mark(slot, 4, st);
+      launch_scatter(dp, ds, u, st);
+    }
     if (slot >= 0) mark(slot, 5, st);
   }
 
@@ -320,10 +330,14 @@ struct sfmm_gpu_plan {
   int launches_per_apply() const {
     if (hp.depth < 2) return 1;
     int n = 3;  // gather, translate, scatter
-    for (int l = 2; l <= hp.depth; ++l) {
-      n += hp.up1_lvl[l + 1] > hp.up1_lvl[l] ? 1 : 0;
-      n += hp.down_lvl[l + 1] > hp.down_lvl[l] ? 1 : 0;
-      n += hp.copy_lvl[l + 1] > hp.copy_lvl[l] ? 2 : 0;  // k1_copy + k3_copy
+    if (dp.tree_persist) {
+      n = 3;  // persistent upward (with the gather), translate, persistent downward (with the scatter)
+    } else {
+      for (int l = 2; l <= hp.depth; ++l) {
+        n += hp.up1_lvl[l + 1] > hp.up1_lvl[l] ? 1 : 0;
+        n += hp.down_lvl[l + 1] > hp.down_lvl[l] ? 1 : 0;
+        n += hp.copy_lvl[l + 1] > hp.copy_lvl[l] ? 2 : 0;  // k1_copy + k3_copy
+      }
     }
     if (dp.n_tasks == 0) --n;
     if (dp.n_recv > 0) ++n;  // k2b_reduce
@@ -350,7 +364,7 @@ namespace sfmm_gpu {
 // copying it (skel_share_T).
 int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
                 sfmm_gpu_plan** out, const double* T_dev = nullptr, bool T_compact = false,
-                std::shared_ptr<double> T_share = {});
+                std::shared_ptr<double> T_share = {}, const int32_t* l1_owner = nullptr);
 std::shared_ptr<double> skel_share_T(const sfmm_skel_result* r);
 
 // Phases of one sharded apply (sfmm_gpu.cu); throw CudaFail.

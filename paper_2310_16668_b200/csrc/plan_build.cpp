@@ -42,11 +42,72 @@ PlanOptions plan_options_from_env() {
   if (const char* v = std::getenv("SFMM_SHARD_XSYM")) o.cross_symmetric = std::atoi(v) != 0;
   if (const char* v = std::getenv("SFMM_SYM_CHAIN")) o.sym_chain = std::atoi(v) != 0;
   if (const char* v = std::getenv("SFMM_MULTI_SYM")) o.multi_sym = std::atoi(v) != 0;
+  if (const char* v = std::getenv("SFMM_TREE_PERSIST")) o.tree_persist = std::atoi(v) != 0 ? 1 : 0;
   return o;
 }
 
+int subtree_owners(int32_t nb, const int32_t* level_begin, int32_t depth,
+                   const int32_t* box_parent, const int32_t* box_begin, const int32_t* box_end,
+                   const uint8_t* box_leaf, const int64_t* coll_off, const int32_t* coll,
+                   int n_ranks, int32_t* owner, std::string& err) {
+  if (nb < 1 || depth < 1 || n_ranks < 1) {
+    err = "subtree_owners: bad arguments";
+    return SFMM_EINVAL;
+  }
+  const int32_t l1b = level_begin[1], l1e = level_begin[2], n1 = l1e - l1b;
+  if (n1 < n_ranks) {
+    err = "subtree_owners: more ranks than level-1 subtrees";
+    return SFMM_EUNSUPPORTED;
+  }
+  // near-field work of every leaf (its colleague leaves' points), summed per
+  // level-1 subtree
+  std::vector<double> cost(nb, 0.0);
+  for (int32_t b = nb - 1; b >= 1; --b) {
+    if (box_leaf[b]) {
+      double src = 0.0;
+      for (int64_t e = coll_off[b]; e < coll_off[b + 1]; ++e)
+        if (box_leaf[coll[e]]) src += box_end[coll[e]] - box_begin[coll[e]];
+      cost[b] += (double)(box_end[b] - box_begin[b]) * (src + 8.0);
+    }
+    if (box_parent[b] > 0) cost[box_parent[b]] += cost[b];
+  }
+  // Morton-contiguous ranges with the smallest largest cost (bisection on the
+  // bound, greedy fill leaving one unit per later rank)
+  double lo = 0.0, hi = 0.0;
+  for (int32_t b = l1b; b < l1e; ++b) {
+    lo = std::max(lo, cost[b]);
+    hi += cost[b];
+  }
+  lo = std::max(lo, hi / n_ranks);
+  auto fill = [&](double bound, bool write) {
+    int r = 0;
+    double acc = 0.0;
+    for (int32_t b = l1b; b < l1e; ++b) {
+      if (acc > 0.0 && acc + cost[b] > bound) {
+        ++r;
+        acc = 0.0;
+      }
+      if (write && acc > 0.0 && l1e - b <= n_ranks - 1 - r) {
+        ++r;
+        acc = 0.0;
+      }
+      acc += cost[b];
+      if (write) owner[b] = std::min(r, n_ranks - 1);
+    }
+    return r + 1;
+  };
+  for (int it = 0; it < 60 && hi - lo > 1e-9 * hi; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    (fill(mid, false) <= n_ranks ? hi : lo) = mid;
+  }
+  for (int32_t b = 0; b < l1b; ++b) owner[b] = -1;
+  fill(hi, true);
+  for (int32_t b = l1e; b < nb; ++b) owner[b] = owner[box_parent[b]];
+  return SFMM_OK;
+}
+
 int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int n_ranks,
-                    int rank, int sym_chain) {
+                    int rank, int sym_chain, const int32_t* l1_owner) {
   try {
     ParErr perr;
     if (d.kernel == SFMM_HELMHOLTZ2D)
@@ -229,7 +290,13 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
     // pass fills, with the ghosts.
     hp.owner.assign(nb, 0);
     hp.cut_level = 1;
-    if (n_ranks > 1) {
+    if (n_ranks > 1 && l1_owner) {  // given (distributed precompute): level-1 subtrees
+      for (int32_t b = l1b; b < l1e; ++b) {
+        if (l1_owner[b] < 0 || l1_owner[b] >= n_ranks) bad("l1_owner: rank out of range");
+        hp.owner[b] = l1_owner[b];
+      }
+      for (int32_t b = l1e; b < nb; ++b) hp.owner[b] = hp.owner[d.box_parent[b]];
+    } else if (n_ranks > 1) {
       // estimated K2 cost of every subtree, as the task cost model: lane rows
       // x (evaluated source points + 8); cancelling pairs skipped, colleague
       // blocks at ~0.575 (evaluated once for both directions)
@@ -985,6 +1052,36 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
     hp.copy_lvl[d.depth + 1] = (int64_t)hp.copy_boxes.size();
     hp.down_lvl[d.depth + 1] = (int64_t)hp.down_items.size();
     hp.down_m_lvl[d.depth + 1] = (int64_t)hp.down_m_items.size();
+    // persistent tree passes (opt-in A/B, plan_build.h kTreePersistPoints)
+    {
+      hp.tree_persist = opt.tree_persist >= 0 ? opt.tree_persist != 0
+                                              : (hp.n_owned_points > 0 && hp.n_owned_points <= kTreePersistPoints);
+      if (hp.tree_persist) {
+        const int32_t n_pj = (int32_t)((hp.n_owned_points + kPointsPerJob - 1) / kPointsPerJob);
+        auto level_jobs = [&](int l, const std::vector<int64_t>& lvl, std::vector<TreeJob>& jobs,
+                              int32_t stage) {
+          for (int64_t c = hp.copy_lvl[l]; c < hp.copy_lvl[l + 1]; c += 8)
+            jobs.push_back({kJobCopy, stage, (int32_t)c,
+                            (int32_t)std::min<int64_t>(8, hp.copy_lvl[l + 1] - c)});
+          for (int64_t i = lvl[l]; i < lvl[l + 1]; ++i) jobs.push_back({kJobItem, stage, (int32_t)i, 0});
+        };
+        int32_t stage = 0;
+        for (int32_t j = 0; j < n_pj; ++j) hp.up_jobs.push_back({kJobGather, 0, j, 0});
+        for (int l = d.depth; l >= 2; --l) level_jobs(l, hp.up1_lvl, hp.up_jobs, ++stage);
+        auto firsts = [](const std::vector<TreeJob>& jobs, int32_t n_stages) {
+          std::vector<int32_t> f(n_stages + 1, 0);
+          for (const TreeJob& j : jobs) ++f[j.stage + 1];
+          for (int32_t i = 0; i < n_stages; ++i) f[i + 1] += f[i];
+          return f;
+        };
+        hp.up_stage_first = firsts(hp.up_jobs, stage + 1);
+        stage = 0;
+        for (int l = 2; l <= d.depth; ++l, ++stage)
+          level_jobs(l, hp.down_lvl, hp.down_jobs, stage);
+        for (int32_t j = 0; j < n_pj; ++j) hp.down_jobs.push_back({kJobScatter, stage, j, 0});
+        hp.down_stage_first = firsts(hp.down_jobs, stage + 1);
+      }
+    }
     return SFMM_OK;
   } catch (const Fail& f) {
     err = f.msg;

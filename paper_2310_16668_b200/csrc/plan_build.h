@@ -38,6 +38,26 @@ struct LevelItem {
   int32_t first;  // first row (K1) / column (K3) of the chunk
 };
 
+// One job of the persistent tree passes (small plans, launch-bound): the
+// whole upward pass -- K0 gather, then every level deepest first -- or the
+// whole downward pass -- every level coarsest first, then K4 scatter -- in one
+// launch; a job of stage s starts once every job of stage s - 1 has finished.
+enum TreeJobKind : int32_t {
+  kJobGather = 0,   // K0 on owned points [a * kPointsPerJob, +kPointsPerJob)
+  kJobCopy = 1,     // k1_copy / k3_copy on copy_boxes[a, a + b)
+  kJobItem = 2,     // K1 on up1_items[a] / K3 on down_items[a]
+  kJobScatter = 3,  // K4 on owned points [a * kPointsPerJob, +kPointsPerJob)
+};
+constexpr int kPointsPerJob = 256;  // one point per thread
+// plans with at most this many owned points run the persistent tree passes
+// by default: none -- measured slower than the per-level launches replayed
+// from a CUDA graph even on config 1 (profiles/r02/tree_persist_ab.txt), so
+// they are an opt-in (SFMM_TREE_PERSIST=1)
+constexpr int64_t kTreePersistPoints = 0;
+struct TreeJob {
+  int32_t kind, stage, a, b;
+};
+
 constexpr int32_t kShared = -1;  // HostPlan::owner of boxes every rank evaluates
 
 struct HostPlan {
@@ -132,6 +152,11 @@ struct HostPlan {
   // single-rhs passes only copy qhat / fold uhat for them (k1_copy, k3_copy)
   std::vector<int32_t> copy_boxes;
   std::vector<int64_t> copy_lvl;
+  // persistent tree passes (PlanOptions::tree_persist): job lists in stage
+  // order and, per stage, the number of jobs in the stages before it
+  bool tree_persist = false;
+  std::vector<TreeJob> up_jobs, down_jobs;
+  std::vector<int32_t> up_stage_first, down_stage_first;
   // depth < 2: coordinates in original order for the dense fallback
   std::vector<double> orig_pts;
   // stats
@@ -142,8 +167,22 @@ struct HostPlan {
 // Validates the descriptor and fills `hp` for rank `rank` of `n_ranks`
 // (1/0: the whole tree).  Returns SFMM_OK or an error code with a message in
 // `err`.
+// l1_owner (n_boxes, may be NULL): the rank of every level-1 box -- whole
+// level-1 subtrees per rank, as chosen before the skeletons existed by a
+// distributed precompute (subtree_owners) -- instead of the cost-based choice.
 int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int n_ranks = 1,
-                    int rank = 0, int sym_chain = -1 /* -1: SFMM_SYM_CHAIN (default 0) */);
+                    int rank = 0, int sym_chain = -1 /* -1: SFMM_SYM_CHAIN (default 0) */,
+                    const int32_t* l1_owner = nullptr);
+
+// Tree-only ownership for a distributed precompute (no skeletons yet): the
+// level-1 subtrees as Morton-contiguous ranges balancing the near-field work
+// estimate sum over leaves of n_leaf * (points of its colleague leaves), so
+// every rank can skeletonize exactly the subtrees it will own.  owner gets
+// n_boxes entries (every box: its level-1 ancestor's rank; levels 0: -1).
+int subtree_owners(int32_t n_boxes, const int32_t* level_begin, int32_t depth,
+                   const int32_t* box_parent, const int32_t* box_begin, const int32_t* box_end,
+                   const uint8_t* box_leaf, const int64_t* coll_off, const int32_t* coll,
+                   int n_ranks, int32_t* owner, std::string& err);
 
 // Plan options (environment SFMM_SYMMETRIC=0 / SFMM_SKIP_CANCEL=0 turn them off
 // for A/B measurements; both default on).
@@ -173,6 +212,10 @@ struct PlanOptions {
   // 3, profiles/r02/k2m_sym_ab.txt) -- K2m is DMMA-bound, the fold saves only
   // generation and costs occupancy and the tile chain's waits.
   bool multi_sym = false;
+  // tree passes as two persistent launches (gather + upward levels, downward
+  // levels + scatter) instead of one to three launches per level: -1 = for
+  // plans of at most kTreePersistPoints points (SFMM_TREE_PERSIST=0/1 forces)
+  int tree_persist = -1;
 };
 PlanOptions plan_options_from_env();
 

@@ -36,14 +36,14 @@ namespace sfmm_gpu {
 // with T_compact only the owned runs concatenated (sfmm_gpu_shard_T_runs order)
 int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
                 sfmm_gpu_plan** out, const double* T_dev, bool T_compact,
-                std::shared_ptr<double> T_share) {
+                std::shared_ptr<double> T_share, const int32_t* l1_owner) {
   if (!desc || !out) return set_error(SFMM_EINVAL, "sfmm_gpu_plan_create: null argument");
   *out = nullptr;
   sfmm_gpu_plan* p = nullptr;
   try {
     p = new sfmm_gpu_plan();
     std::string err;
-    int rc = build_host_plan(*desc, p->hp, err, n_ranks, rank);
+    int rc = build_host_plan(*desc, p->hp, err, n_ranks, rank, -1, l1_owner);
     if (rc != SFMM_OK) {
       delete p;
       return set_error(rc, err);
@@ -64,7 +64,7 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
         if (!(T_dev && !T_compact && n_ranks == 1)) need += 8.0 * sw * (double)h.T_off.back();
         if (need > 0.92 * (double)free_b) {
           HostPlan chained;
-          if (build_host_plan(*desc, chained, err, n_ranks, rank, 1) == SFMM_OK)
+          if (build_host_plan(*desc, chained, err, n_ranks, rank, 1, l1_owner) == SFMM_OK)
             p->hp = std::move(chained);
         }
       }
@@ -205,6 +205,16 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
       dp.up1_items = p->upload(hp.up1_items);
       dp.copy_boxes = p->upload(hp.copy_boxes);
       dp.down_items = p->upload(hp.down_items);
+      if (hp.tree_persist) {
+        dp.tree_persist = 1;
+        dp.up_jobs = p->upload(hp.up_jobs);
+        dp.down_jobs = p->upload(hp.down_jobs);
+        dp.n_up_jobs = (int64_t)hp.up_jobs.size();
+        dp.n_down_jobs = (int64_t)hp.down_jobs.size();
+        dp.up_stage_first = p->upload(hp.up_stage_first);
+        dp.down_stage_first = p->upload(hp.down_stage_first);
+        dp.tree_sync = p->alloc<int>(4);
+      }
       const int64_t n_recv2 = hp.recv2_off.empty() ? 0 : hp.recv2_off.back();
       dp.stage_size = hp.stage_size;
       dp.sym_chain = hp.sym_chain ? 1 : 0;
@@ -329,8 +339,7 @@ void apply_fin_impl(sfmm_gpu_plan* p, const void* q_dev, const void* recv2_dev, 
        "second exchange");
   }
   launch_stage_reduce(p->dp, p->ds, st);
-  for (int l = 2; l <= p->hp.depth; ++l) launch_downward(p->dp, p->hp, l, p->ds, st);
-  launch_scatter(p->dp, p->ds, u, st);
+  launch_downward_all(p->dp, p->hp, p->ds, u, st);
 }
 
 }  // namespace
@@ -345,8 +354,7 @@ void phase_begin(sfmm_gpu_plan* p, const void* q_dev, void* send_dev, void* user
     throw CudaFail{SFMM_EINVAL, "send buffer required"};
   p->run_phase(0, q_dev, send_dev, nullptr, user_stream, st, [&] {
     if (p->hp.depth < 2) return;
-    launch_gather(p->dp, q, p->ds, st);
-    for (int l = p->hp.depth; l >= 2; --l) launch_upward(p->dp, p->hp, l, p->ds, st);
+    launch_upward_all(p->dp, p->hp, q, p->ds, st);
     if (p->dp.n_pack > 0) launch_pack(p->dp, p->ds, static_cast<double*>(send_dev), st);
   });
   if (packed) ck(cudaEventRecord(packed, st), "event");
@@ -453,6 +461,23 @@ int sfmm_gpu_plan_create_sharded_T(const sfmm_plan_desc* desc, const void* T_own
                                    int n_ranks, int rank, sfmm_gpu_plan** out) {
   return create_plan(desc, device, n_ranks, rank, out, static_cast<const double*>(T_owned_dev),
                      true);
+}
+
+int sfmm_gpu_subtree_owners(const sfmm_tree_arrays* tree, int n_ranks, int32_t* owner) {
+  if (!tree || !owner) return set_error(SFMM_EINVAL, "sfmm_gpu_subtree_owners: null argument");
+  std::string err;
+  const int rc = subtree_owners(tree->n_boxes, tree->level_begin, tree->depth, tree->box_parent,
+                                tree->box_begin, tree->box_end, tree->box_leaf, tree->coll_off,
+                                tree->coll, n_ranks, owner, err);
+  return rc == SFMM_OK ? SFMM_OK : set_error(rc, err);
+}
+
+int sfmm_gpu_plan_create_sharded_owned(const sfmm_plan_desc* desc, const void* T_owned_dev,
+                                       int device, int n_ranks, int rank, const int32_t* owner,
+                                       sfmm_gpu_plan** out) {
+  if (!owner) return set_error(SFMM_EINVAL, "sfmm_gpu_plan_create_sharded_owned: null owner");
+  return create_plan(desc, device, n_ranks, rank, out, static_cast<const double*>(T_owned_dev),
+                     true, {}, owner);
 }
 
 int sfmm_gpu_shard_info(const sfmm_gpu_plan* p, int64_t* send_counts, int64_t* recv_counts,

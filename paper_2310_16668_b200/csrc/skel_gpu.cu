@@ -507,9 +507,14 @@ struct sfmm_skel_result {
 
 namespace {
 
+// mask (n_boxes, may be NULL = every box): only the boxes with mask[b] != 0
+// are skeletonized; the others get an empty index_vec (n = k = 0, no T).  The
+// masked boxes must form whole subtrees (a rank's share of a sharded plan,
+// sfmm_gpu_build_skeletons_subset): each masked box's result depends only on
+// its own subtree, so it is bit-identical to the unmasked build's.
 template <class S>
 void run_skeletons(const sfmm_tree_desc& t, int kernel, double kappa, double tol, double radius,
-                   int edge2d, int face3d, sfmm_skel_result& R) {
+                   int edge2d, int face3d, const uint8_t* mask, sfmm_skel_result& R) {
   constexpr int SW = sizeof(S) / 8;
   const auto t_run0 = std::chrono::steady_clock::now();
   const int nb = t.n_boxes, dim = t.dim, depth = t.depth;
@@ -581,8 +586,15 @@ void run_skeletons(const sfmm_tree_desc& t, int kernel, double kappa, double tol
     const int b0 = t.level_begin[l], b1 = t.level_begin[l + 1], nl = b1 - b0;
     // index_vec sizes: leaf points or the children's k
     std::vector<int64_t> n(nl);
+    std::vector<int32_t> act;  // level-local indices of the boxes to skeletonize
+    act.reserve(nl);
     for (int i = 0; i < nl; ++i) {
       const int b = b0 + i;
+      if (mask && !mask[b]) {
+        n[i] = 0;
+        continue;
+      }
+      act.push_back(i);
       if (t.box_leaf[b]) {
         n[i] = t.box_end[b] - t.box_begin[b];
       } else {
@@ -631,18 +643,20 @@ void run_skeletons(const sfmm_tree_desc& t, int kernel, double kappa, double tol
     ck(cudaFuncSetAttribute(cpqr_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
        "smem attr");
     // T sizes need k: run CPQR for the whole level (batched), then solve
+    // batches: consecutive runs of `act` (positions into it)
+    const int na = (int)act.size();
     std::vector<int> batch_start{0};
     {
       int64_t acc = 0;
-      for (int i = 0; i < nl; ++i) {
-        const int64_t sz = (int64_t)rows * n[i] * sizeof(S);
+      for (int a = 0; a < na; ++a) {
+        const int64_t sz = (int64_t)rows * n[act[a]] * sizeof(S);
         if (acc > 0 && acc + sz > (int64_t)work_cap) {
-          batch_start.push_back(i);
+          batch_start.push_back(a);
           acc = 0;
         }
         acc += sz;
       }
-      batch_start.push_back(nl);
+      batch_start.push_back(na);
     }
     // the solve needs R of every box, so the level's workspace must persist
     // until its solve: process batch by batch (CPQR, k, solve)
@@ -653,21 +667,29 @@ void run_skeletons(const sfmm_tree_desc& t, int kernel, double kappa, double tol
     // first pass: CPQR + solve need level-wide sk_off/T_off, so run CPQR for
     // all batches first, keeping R only for the batch being solved; the
     // workspace is reused, so each batch is factored and solved before the next
-    std::vector<std::vector<int32_t>> k_batches;
-    for (size_t bi = 0; bi + 1 < batch_start.size(); ++bi) {
-      const int i0 = batch_start[bi], i1 = batch_start[bi + 1];
-      const int cnt = i1 - i0;
+    int filled = 0;  // level-local boxes whose sk_off / T_off prefix is final
+    for (size_t bi = 0; bi + 1 < batch_start.size() && na > 0; ++bi) {
+      const int a0 = batch_start[bi], a1 = batch_start[bi + 1];
+      const int cnt = a1 - a0;
+      // the batch's boxes are level-local indices act[a0..a1); their
+      // workspaces are packed in that order
       std::vector<int64_t> wo(cnt);
-      for (int i = 0; i < cnt; ++i) wo[i] = woff[i0 + i] - woff[i0];  // in scalars S
+      std::vector<int32_t> lb(cnt), bx(cnt);
+      int64_t wsum = 0;
+      for (int a = 0; a < cnt; ++a) {
+        const int i = act[a0 + a];
+        wo[a] = wsum;  // in scalars S
+        wsum += woff[i + 1] - woff[i];
+        lb[a] = i;
+        bx[a] = boxes[i];
+      }
       DevBuf<int64_t> d_wo;
       d_wo.upload(wo);
-      const size_t wbytes = (size_t)(woff[i1] - woff[i0]) * sizeof(S);
+      const size_t wbytes = (size_t)wsum * sizeof(S);
       if (d_work.n * sizeof(double) < wbytes) d_work.alloc(wbytes / sizeof(double) + 1);
-      std::vector<int32_t> lb(cnt);
-      std::iota(lb.begin(), lb.end(), i0);
       DevBuf<int32_t> d_lb, d_bx;
       d_lb.upload(lb);
-      d_bx.upload(std::vector<int32_t>(boxes.begin() + i0, boxes.begin() + i1));
+      d_bx.upload(bx);
       LevelArgs a{};
       a.boxes = d_bx.p;
       a.lbox = d_lb.p;
@@ -691,13 +713,20 @@ void run_skeletons(const sfmm_tree_desc& t, int kernel, double kappa, double tol
       a.sat = d_sat.p;
       cpqr_kernel<S><<<cnt, kSkThreads, smem>>>(a);
       ck(cudaGetLastError(), "cpqr");
-      std::vector<int32_t> kb;
-      ck(cudaMemcpy(kk_all.data() + i0, lv.d_k.p + i0, cnt * sizeof(int32_t), cudaMemcpyDeviceToHost),
-         "D2H k");
-      // level-local offsets are prefix sums in box order; batches run in order
-      for (int i = i0; i < i1; ++i) {
-        lv.sk_off[i + 1] = lv.sk_off[i] + kk_all[i];
-        lv.T_off[i + 1] = lv.T_off[i] + (int64_t)kk_all[i] * (n[i] - kk_all[i]);
+      {
+        std::vector<int32_t> kd(nl);
+        const int i_lo = act[a0], i_hi = act[a1 - 1] + 1;
+        ck(cudaMemcpy(kd.data() + i_lo, lv.d_k.p + i_lo, (i_hi - i_lo) * sizeof(int32_t),
+                      cudaMemcpyDeviceToHost),
+           "D2H k");
+        for (int a = a0; a < a1; ++a) kk_all[act[a]] = kd[act[a]];
+        // level-local offsets are prefix sums in box order; batches run in
+        // order, skipped boxes contribute nothing
+        for (int i = filled; i < i_hi; ++i) {
+          lv.sk_off[i + 1] = lv.sk_off[i] + kk_all[i];
+          lv.T_off[i + 1] = lv.T_off[i] + (int64_t)kk_all[i] * (n[i] - kk_all[i]);
+        }
+        filled = i_hi;
       }
       // grow the level outputs to this batch's end and solve it
       if (bi == 0) {
@@ -733,8 +762,27 @@ void run_skeletons(const sfmm_tree_desc& t, int kernel, double kappa, double tol
       s.T = lv.d_T.p;
       solve_kernel<S><<<cnt, kSkThreads, nmax * sizeof(int)>>>(s);
       ck(cudaGetLastError(), "solve");
-      ck(cudaMemcpy(sat_all.data() + i0, d_sat.p + i0, cnt * sizeof(uint8_t), cudaMemcpyDeviceToHost),
-         "D2H sat");
+      {
+        std::vector<uint8_t> sd(nl);
+        const int i_lo = act[a0], i_hi = act[a1 - 1] + 1;
+        ck(cudaMemcpy(sd.data() + i_lo, d_sat.p + i_lo, (i_hi - i_lo) * sizeof(uint8_t),
+                      cudaMemcpyDeviceToHost),
+           "D2H sat");
+        for (int a = a0; a < a1; ++a) sat_all[act[a]] = sd[act[a]];
+      }
+    }
+    // boxes after the last skeletonized one (and every box of a level with
+    // none) close the prefix sums
+    for (int i = filled; i < nl; ++i) {
+      lv.sk_off[i + 1] = lv.sk_off[i] + kk_all[i];
+      lv.T_off[i + 1] = lv.T_off[i] + (int64_t)kk_all[i] * (n[i] - kk_all[i]);
+    }
+    if (na == 0) {  // nothing of this level here: empty outputs
+      lv.d_skel.alloc(0);
+      lv.d_red.alloc(0);
+      lv.d_T.alloc(0);
+      lv.d_sk_off.upload(lv.sk_off);
+      lv.d_T_off.upload(lv.T_off);
     }
     ck(cudaDeviceSynchronize(), "level");
     if (verbose)
@@ -848,12 +896,18 @@ void run_skeletons(const sfmm_tree_desc& t, int kernel, double kappa, double tol
 
 extern "C" {
 
-int sfmm_gpu_build_skeletons(const sfmm_tree_desc* tree, int kernel, double kappa, double tol,
-                             double proxy_radius, int proxy_edge2d, int proxy_face3d, int device,
-                             sfmm_skel_result** out) {
+int sfmm_gpu_build_skeletons_subset(const sfmm_tree_desc* tree, int kernel, double kappa,
+                                    double tol, double proxy_radius, int proxy_edge2d,
+                                    int proxy_face3d, int device, const uint8_t* box_mask,
+                                    sfmm_skel_result** out) {
   using sfmm_gpu::set_last_error;
   if (!tree || !out) return set_last_error(SFMM_EINVAL, "build_skeletons: null argument");
   *out = nullptr;
+  if (box_mask)  // whole subtrees: a masked box's children are masked
+    for (int32_t b = 1; b < tree->n_boxes; ++b)
+      if (box_mask[tree->box_parent[b]] && !box_mask[b])
+        return set_last_error(SFMM_EINVAL,
+                              "build_skeletons_subset: the mask must select whole subtrees");
   if (!(tol > 0.0 && tol < 0.5))
     return set_last_error(SFMM_EINVAL, "build_skeletons: tolerance must lie in (0, 0.5)");
   if (kernel == SFMM_HELMHOLTZ2D)
@@ -871,9 +925,9 @@ int sfmm_gpu_build_skeletons(const sfmm_tree_desc* tree, int kernel, double kapp
     DeviceGuard device_guard(device);
     const auto t0 = std::chrono::steady_clock::now();
     if (kernel == SFMM_HELMHOLTZ3D)
-      run_skeletons<Cx>(*tree, kernel, kappa, tol, radius, edge, face, *R);
+      run_skeletons<Cx>(*tree, kernel, kappa, tol, radius, edge, face, box_mask, *R);
     else
-      run_skeletons<double>(*tree, kernel, kappa, tol, radius, edge, face, *R);
+      run_skeletons<double>(*tree, kernel, kappa, tol, radius, edge, face, box_mask, *R);
     R->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     *out = R;
     return SFMM_OK;
@@ -884,6 +938,13 @@ int sfmm_gpu_build_skeletons(const sfmm_tree_desc* tree, int kernel, double kapp
     delete R;
     return set_last_error(SFMM_ENOMEM, "build_skeletons: host allocation failed");
   }
+}
+
+int sfmm_gpu_build_skeletons(const sfmm_tree_desc* tree, int kernel, double kappa, double tol,
+                             double proxy_radius, int proxy_edge2d, int proxy_face3d, int device,
+                             sfmm_skel_result** out) {
+  return sfmm_gpu_build_skeletons_subset(tree, kernel, kappa, tol, proxy_radius, proxy_edge2d,
+                                         proxy_face3d, device, nullptr, out);
 }
 
 int sfmm_gpu_skel_fill(sfmm_skel_result* r, sfmm_plan_desc* d, int32_t* k_max,

@@ -121,7 +121,7 @@ class HostPlan:
     @classmethod
     def build_gpu(cls, kernel: int, pts: np.ndarray, leaf_cap: int, tol: float,
                   kappa: float = 1.0, proxy: tuple | None = None, device: int = 0,
-                  host_T: bool = True) -> "HostPlan":
+                  host_T: bool = True, box_mask=None) -> "HostPlan":
         """Tree and neighbor lists (sfmm_gpu_build_tree, bit-identical to the
         reference) and skeletons (sfmm_gpu_build_skeletons), all on the GPU
         (SURVEY.md 8(f) rows 1 and 3).
@@ -130,8 +130,18 @@ class HostPlan:
         (SURVEY.md 8(f) row 2): the descriptor's T is NULL, api.GpuPlan.from_host
         takes T device-to-device, and fetch_T() downloads it when a host copy is
         needed (e.g. for the CPU reference)."""
-        from .api import _raise
         hp = cls.build_tree_gpu(pts, leaf_cap, device)
+        hp.skeletonize(kernel, tol, kappa, proxy, device, host_T, box_mask)
+        return hp
+
+    def skeletonize(self, kernel: int, tol: float, kappa: float = 1.0, proxy: tuple | None = None,
+                    device: int = 0, host_T: bool = True, box_mask=None) -> None:
+        """Skeletons of this plan's tree on the GPU (sfmm_gpu_build_skeletons).
+        box_mask (distributed precompute): only those boxes -- whole subtrees
+        -- are skeletonized (sfmm_gpu_build_skeletons_subset); the others stay
+        empty, and the device operators are exactly the masked boxes'."""
+        from .api import _raise
+        hp = self
         d = host_lib().sfmm_host_desc(hp._h).contents
         nb = int(d.n_boxes)
         center = np.zeros(3 * nb)
@@ -146,8 +156,12 @@ class HostPlan:
         px = proxy or (0.0, 0, 0)
         res = C.c_void_p()
         lib = _abi.gpu_lib()
-        _raise(lib.sfmm_gpu_build_skeletons(C.byref(t), kernel, kappa, tol, float(px[0]), int(px[1]),
-                                            int(px[2]), device, C.byref(res)))
+        mask = None if box_mask is None else np.ascontiguousarray(box_mask, dtype=np.uint8)
+        if mask is not None and mask.size != nb:
+            raise ValueError("box_mask must have one entry per box")
+        _raise(lib.sfmm_gpu_build_skeletons_subset(
+            C.byref(t), kernel, kappa, tol, float(px[0]), int(px[1]), int(px[2]), device,
+            None if mask is None else mask.ctypes.data, C.byref(res)))
         keep = False
         try:
             sk = PlanDesc()
@@ -159,10 +173,10 @@ class HostPlan:
             keep = not host_T
         finally:
             if keep:
+                hp.release_device_skeletons()
                 hp._skel, hp._skel_device = res, device
             else:
                 lib.sfmm_gpu_skel_destroy(res)
-        return hp
 
     @property
     def device_skeletons(self):
@@ -218,6 +232,18 @@ class HostPlan:
         finally:
             lib.sfmm_gpu_tree_destroy(t)
         return cls(h)
+
+    def tree_arrays(self) -> _abi.TreeArrays:
+        """sfmm_tree_arrays view of this plan's tree (the fields the tree-only
+        helpers read: level_begin, box_parent/begin/end/leaf, colleagues);
+        valid while this plan is alive."""
+        d = self.desc_struct()
+        a = _abi.TreeArrays()
+        a.dim, a.depth, a.n_boxes, a.n_points = d.dim, d.depth, d.n_boxes, d.n_points
+        for f in ("perm", "pts", "level_begin", "box_parent", "box_level", "box_begin", "box_end",
+                  "box_leaf", "coll_off", "coll", "coarse_off", "coarse", "fine_off", "fine"):
+            setattr(a, f, getattr(d, f))
+        return a
 
     def descriptor(self) -> PlanDescriptor:
         """Owned numpy copy of the flat descriptor."""

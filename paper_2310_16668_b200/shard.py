@@ -101,7 +101,11 @@ class ShardedPlan:
         st = _struct(desc)
         self._h = None
         h = C.c_void_p()
-        if T_owned is not None:
+        if T_owned is not None and getattr(T_owned, "owner", None) is not None:
+            _raise(lib.sfmm_gpu_plan_create_sharded_owned(
+                C.byref(st), C.c_void_p(T_owned.data_ptr()), device, n_ranks, rank,
+                T_owned.owner.ctypes.data, C.byref(h)))
+        elif T_owned is not None:
             _raise(lib.sfmm_gpu_plan_create_sharded_T(C.byref(st), C.c_void_p(T_owned.data_ptr()),
                                                       device, n_ranks, rank, C.byref(h)))
         else:
@@ -343,3 +347,110 @@ def apply_virtual(plans: list[ShardedPlan], q_dev, u_dev, stream=None) -> None:
         for p in plans:
             p.end(q_dev, u_dev, stream.cuda_stream)
     fence()
+
+
+# ---------------------------------------------------------------------------
+# distributed precompute (no rank holds every operator)
+# ---------------------------------------------------------------------------
+
+def subtree_owners(hp, n_ranks: int) -> np.ndarray:
+    """Rank of every box from the tree alone (sfmm_gpu_subtree_owners):
+    Morton-contiguous ranges of level-1 subtrees; -1 above level 1."""
+    a = hp.tree_arrays()
+    owner = np.zeros(int(a.n_boxes), dtype=np.int32)
+    _raise(_abi.gpu_lib().sfmm_gpu_subtree_owners(C.byref(a), n_ranks, owner.ctypes.data))
+    return owner
+
+
+_IDX = ("iv", "skel_pos", "red_pos")
+_OFF = {"iv": "iv_off", "skel_pos": "sk_off", "red_pos": "rd_off"}
+
+
+def local_index_data(hp, owner: np.ndarray, rank: int) -> dict:
+    """This rank's share of the skeleton index data: for each box it owns
+    (ascending id) the index_vec / skel_pos / red_pos segment lengths and
+    contents and its parent_offset.  The subset build leaves every other box
+    empty, so the packed arrays are the local arrays themselves."""
+    d = hp.descriptor().arrays
+    boxes = np.nonzero(owner == rank)[0].astype(np.int32)
+    out = {"boxes": boxes, "poff": np.asarray(d["box_parent_offset"])[boxes].copy()}
+    for f in _IDX:
+        off = np.asarray(d[_OFF[f]])
+        out["len_" + f] = np.diff(off)[boxes].astype(np.int64)
+        out[f] = np.asarray(d[f]).copy()
+        assert out[f].size == int(out["len_" + f].sum()), "subset result holds unowned boxes"
+    return out
+
+
+def _place(dst: np.ndarray, dst_off: np.ndarray, boxes: np.ndarray, lens: np.ndarray,
+           src: np.ndarray) -> None:
+    if src.size == 0:
+        return
+    starts = dst_off[boxes]
+    first = np.concatenate([[0], np.cumsum(lens)[:-1]])
+    dst[np.repeat(starts - first, lens) + np.arange(src.size)] = src
+
+
+def assemble_descriptor(hp, parts: list) -> PlanDescriptor:
+    """The full plan descriptor (no T) from every rank's index data and this
+    rank's tree: what a single skeletonization of the whole tree gives, box
+    for box (each box's skeleton depends only on its own subtree)."""
+    base = hp.descriptor()
+    arrays = dict(base.arrays)
+    scalars = dict(base.scalars)
+    nb = int(scalars["n_boxes"])
+    level = np.asarray(arrays["box_level"])
+    lens = {f: np.zeros(nb, dtype=np.int64) for f in _IDX}
+    poff = np.zeros(nb, dtype=np.int32)
+    for p in parts:
+        for f in _IDX:
+            lens[f][p["boxes"]] = p["len_" + f]
+        poff[p["boxes"]] = p["poff"]
+    for f in _IDX:
+        off = np.concatenate([[0], np.cumsum(lens[f])]).astype(np.int64)
+        arrays[_OFF[f]] = off
+        dst = np.zeros(int(off[-1]), dtype=np.int32)
+        for p in parts:
+            _place(dst, off, p["boxes"], p["len_" + f], p[f])
+        arrays[f] = dst
+    n, k = lens["iv"], lens["skel_pos"]
+    arrays["T_off"] = np.concatenate([[0], np.cumsum(np.where(level >= 2, k * (n - k), 0))]).astype(np.int64)
+    arrays["box_parent_offset"] = poff
+    arrays["T"] = np.zeros(0, dtype=np.float64)
+    return PlanDescriptor(scalars, arrays)
+
+
+def distributed_precompute(kernel: int, pts: np.ndarray, leaf_cap: int, tol: float,
+                           kappa: float, n_ranks: int, rank: int, device: int, all_gather):
+    """One rank's share of the precompute: the tree (every rank builds the
+    same one), the tree-only ownership, the skeletons of this rank's level-1
+    subtrees only (operators stay on `device`), then the index data of all
+    ranks via all_gather(part) -> [part of rank 0, 1, ...] to form the full
+    descriptor.  Returns (descriptor without T, host plan holding this rank's
+    operators, owner)."""
+    from . import host
+    hp = host.HostPlan.build_tree_gpu(pts, leaf_cap, device)
+    owner = subtree_owners(hp, n_ranks)
+    hp.skeletonize(kernel, tol, kappa, device=device, host_T=False, box_mask=owner == rank)
+    parts = all_gather(local_index_data(hp, owner, rank))
+    return assemble_descriptor(hp, parts), hp, owner
+
+
+class OwnedShardedPlan(ShardedPlan):
+    """A rank plan of the distributed precompute: the ownership it was
+    skeletonized for, its operators taken from the subset build's device T
+    (sfmm_gpu_plan_create_sharded_owned)."""
+
+    def __init__(self, desc, n_ranks: int, rank: int, device: int, T_ptr: int, owner: np.ndarray):
+        self._owner = np.ascontiguousarray(owner, dtype=np.int32)
+        super().__init__(desc, n_ranks, rank, device, T_owned=_OwnedT(T_ptr, self._owner))
+
+
+class _OwnedT:
+    """T_owned for ShardedPlan: a raw device pointer plus the ownership."""
+
+    def __init__(self, ptr: int, owner: np.ndarray):
+        self.ptr, self.owner = ptr, owner
+
+    def data_ptr(self) -> int:
+        return self.ptr

@@ -187,6 +187,29 @@ def test_multi_rhs_symmetric_fold_matches_unfolded(kernel, dist, leaf, monkeypat
     assert rel_l2(U, U_ref) <= PARITY
 
 
+@pytest.mark.parametrize("kernel,dist,n,leaf", [(1, "cube", 60000, 64), (1, "sphere", 40000, 50),
+                                                (0, "square", 50000, 64), (0, "annulus", 30000, 40),
+                                                (3, "cube", 30000, 64)])
+def test_persistent_tree_passes_bit_identical(kernel, dist, n, leaf, monkeypatch):
+    """The persistent tree passes (gather + every upward level in one launch,
+    every downward level + scatter in another; small plans) give exactly the
+    per-level launches' result, and stay parity-green vs the reference."""
+    pts = host.generate_points(dist, n, 8)
+    d = ref_descriptor(kernel, pts, leaf, 1e-6, 10.0 if kernel == 3 else 1.0)
+    q = (host.generate_charges_complex if kernel == 3 else host.generate_charges)(n, 21)
+    monkeypatch.setenv("SFMM_TREE_PERSIST", "1")
+    pp = api.GpuPlan(d)
+    assert pp.info().launches_per_apply <= 4  # tree passes, translation (+ its column-sum reduce)
+    u1 = api.fmm_apply(pp, q)
+    assert np.array_equal(u1, api.fmm_apply(pp, q))
+    monkeypatch.setenv("SFMM_TREE_PERSIST", "0")
+    pl = api.GpuPlan(d)
+    assert pl.info().launches_per_apply > pp.info().launches_per_apply
+    assert np.array_equal(u1, api.fmm_apply(pl, q))
+    u_ref, _ = po.oracle_apply(d, q)
+    assert rel_l2(u1, u_ref) <= PARITY
+
+
 @pytest.mark.parametrize("kernel,kappa", [(1, 1.0), (3, 10.0)])
 def test_multi_rhs_target_at_padding_coordinate(kernel, kappa):
     """K2m pads partial source chunks with a fixed far coordinate; a real
