@@ -340,40 +340,28 @@ def run_reference(args, ws, rank):
 # multi-rank (torchrun): one process per GPU, exchanges inside the library
 # ---------------------------------------------------------------------------
 
-def _share_descriptor(hp, path):
-    """Rank 0 writes the flat plan descriptor to node-local shared memory,
-    straight from the host plan's arrays (no intermediate copy)."""
-    import ctypes as C
-    from paper_2310_16668_b200._abi import DESC_ARRAYS, DESC_SCALARS, _array_len
-    st = hp.desc_struct()
-    sc = {k: getattr(st, k) for k in DESC_SCALARS}
-    os.makedirs(path, exist_ok=True)
-    views = {}
-    for name, dt in [(n, d) for n, d in DESC_ARRAYS if n.endswith("_off")] + \
-                    [(n, d) for n, d in DESC_ARRAYS if not n.endswith("_off")]:
-        cnt = _array_len(name, sc, lambda k: views[k])
-        ptr = getattr(st, name)
-        views[name] = (np.ctypeslib.as_array(C.cast(ptr, C.POINTER(np.ctypeslib.as_ctypes_type(dt))),
-                                             shape=(cnt,)) if cnt and ptr else np.zeros(0, dtype=dt))
-        np.save(os.path.join(path, name + ".npy"), views[name])
-    with open(os.path.join(path, "scalars.json"), "w") as f:
-        json.dump(sc, f)
-
-
-def _load_descriptor(path):
-    from paper_2310_16668_b200._abi import DESC_ARRAYS, PlanDescriptor
-    arrays = {n: np.load(os.path.join(path, n + ".npy"), mmap_mode="r") for n, _ in DESC_ARRAYS}
-    with open(os.path.join(path, "scalars.json")) as f:
-        scalars = json.load(f)
-    return PlanDescriptor(scalars, arrays)
+def _shm_all_gather(path, rank, ws, dist):
+    """all_gather of one dict of numpy arrays per rank through node-local
+    files (the ranks share the node): returns the ranks' dicts in rank order."""
+    def gather(part):
+        np.savez(os.path.join(path, f"part_{rank}.npz"), **part)
+        dist.barrier()
+        out = []
+        for r in range(ws):
+            with np.load(os.path.join(path, f"part_{r}.npz")) as z:
+                out.append({k: z[k] for k in z.files})
+        dist.barrier()
+        return out
+    return gather
 
 
 def run_sharded(args, ws, rank, local):
     """--gpus N under torchrun: the apply sharded over N ranks (whole subtrees
     per rank), both exchanges inside the library as grouped
-    ncclSend/ncclRecv (sfmm_gpu_plan_attach_nccl).  torch.distributed is the
-    plumbing only: the communicator id, the operator blobs at setup, the
-    barriers and the max-over-ranks time."""
+    ncclSend/ncclRecv (sfmm_gpu_plan_attach_nccl), after a distributed
+    precompute (each rank skeletonizes only its own subtrees).
+    torch.distributed is the plumbing only: the communicator id, barriers and
+    the max-over-ranks time."""
     import shutil
 
     import torch
@@ -394,54 +382,28 @@ def run_sharded(args, ws, rank, local):
     base = "/dev/shm" if (os.path.isdir("/dev/shm") and
                           shutil.disk_usage("/dev/shm").free > 300 * n) else "/tmp"
     path = f"{base}/sfmm_bench_{os.environ.get('MASTER_PORT', '0')}"
+    if rank == 0:
+        os.makedirs(path, exist_ok=True)
+    dist.barrier()
     t0 = time.perf_counter()
     pts = gen_points(args.dist, n)
     q = gen_charges(n, 1, cplx)
-    hp = None
-    hinfo = {}
-    if rank == 0:
-        # torchrun sets OMP_NUM_THREADS=1; the other ranks wait at the barrier
-        host.set_threads(os.cpu_count() or 1)
-        # GPU precompute keeps T on rank 0's device: the descriptor is shared
-        # without it and every rank receives only its own operators
-        hp = host.HostPlan.build_gpu(kern, pts, args.leaf, args.tol, args.kappa, device=dev,
-                                     host_T=False)
-        hinfo = hp.info()
-        _share_descriptor(hp, path)
-    dist.barrier()
-    if rank != 0:
-        host.set_threads(max(1, (os.cpu_count() or ws) // ws))
-    desc = hp.desc_struct() if rank == 0 else _load_descriptor(path)
-    t_pre = time.perf_counter() - t0
+    t_gen = time.perf_counter() - t0
+    # distributed precompute: every rank builds the same tree, skeletonizes
+    # only the level-1 subtrees it owns (operators stay on its GPU) and the
+    # ranks exchange the index data to form the full descriptor
+    host.set_threads(max(1, (os.cpu_count() or ws) // ws))
+    torch.zeros(1, device=f"cuda:{dev}")
     t0 = time.perf_counter()
-    sw = 2 if cplx else 1
-    runs, n_entries = shard.T_runs(desc, ws, rank)
-    all_runs = [None] * ws
-    dist.all_gather_object(all_runs, runs)
-    blob = torch.empty(max(1, n_entries * sw), dtype=torch.float64, device=f"cuda:{dev}")
-    if rank == 0:
-        ptr, _, _ = hp.device_T()
-        for r in range(ws):
-            if r == 0:
-                shard.pack_T(ptr, all_runs[0], sw, blob, dev)
-                continue
-            cnt = max(1, int(all_runs[r][:, 1].sum()) * sw)
-            buf = torch.empty(cnt, dtype=torch.float64, device=f"cuda:{dev}")
-            shard.pack_T(ptr, all_runs[r], sw, buf, dev)
-            torch.cuda.synchronize(dev)
-            dist.send(buf if args.backend == "nccl" else buf.cpu(), dst=r)
-            del buf
-    else:
-        if args.backend == "nccl":
-            dist.recv(blob, src=0)
-        else:
-            tmp = torch.empty(blob.numel(), dtype=torch.float64)
-            dist.recv(tmp, src=0)
-            blob.copy_(tmp)
+    desc, hp_local, owner = shard.distributed_precompute(
+        kern, pts, args.leaf, args.tol, args.kappa, ws, rank, dev,
+        _shm_all_gather(path, rank, ws, dist))
+    t_pre = time.perf_counter() - t0
+    hinfo = hp_local.info()
+    t0 = time.perf_counter()
+    plan = shard.OwnedShardedPlan(desc, ws, rank, dev, hp_local.device_T()[0], owner)
+    hp_local.release_device_skeletons()  # the plan holds its own copy of the operators
     torch.cuda.synchronize(dev)
-    torch.cuda.empty_cache()
-    plan = shard.ShardedPlan(desc, ws, rank, device=dev, T_owned=blob)
-    del blob
     torch.cuda.empty_cache()
     # the exchange inside the library: one NCCL communicator for the ranks
     in_library = False
@@ -459,12 +421,14 @@ def run_sharded(args, ws, rank, local):
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)
         in_library = bool(ok.item())
     t_upload = time.perf_counter() - t0
+    pre = torch.tensor([t_pre, t_upload, hinfo["t_tree"], hinfo["t_skel"]], dtype=torch.float64,
+                       device=f"cuda:{dev}" if args.backend == "nccl" else "cpu")
+    dist.all_reduce(pre, op=dist.ReduceOp.MAX)
+    t_pre, t_upload, t_tree, t_skel = (float(x) for x in pre.tolist())
     dist.barrier()
     single_fits = n <= 20_000_000
     if rank == 0:
         shutil.rmtree(path, ignore_errors=True)
-        if not single_fits:
-            hp.release_device_skeletons()
 
     dtype = torch.complex128 if cplx else torch.float64
     q_host = torch.from_numpy(q)
@@ -571,9 +535,13 @@ def run_sharded(args, ws, rank, local):
         ref_t = api.direct_sum_subset(kern, args.kappa, pts, q, targets, device=dev)
         relerr_direct = api.max_rel_err(u_full[targets], ref_t) if targets.size else None
         relerr_single = None
-        if single_fits:
+        if single_fits:  # the whole-tree precompute on one GPU (same skeletons, bit for bit)
+            plan.close()
+            hp = host.HostPlan.build_gpu(kern, pts, args.leaf, args.tol, args.kappa, device=dev,
+                                         host_T=False)
             with api.GpuPlan.from_host(hp, device=dev) as single:
                 u_single = api.fmm_apply(single, q)
+            hp.close()
             relerr_single = float(np.linalg.norm(u_full - u_single) / np.linalg.norm(u_single))
         w_ref = 20.0 * pinfo.p_dense + 2.0 * pinfo.p_skel
         achieved = w_ref / (ms_step * 1e-3) / ws / 1e12
@@ -606,8 +574,12 @@ def run_sharded(args, ws, rank, local):
                       "owned_points_rank0": plan.n_owned_points,
                       "send_mb_rank0": float(plan.send_counts.sum()) * 8 / 1e6,
                       "send2_mb_rank0": float(plan.send2_counts.sum()) * 8 / 1e6},
-            "precompute": {"t_total_s": t_pre, "t_upload_s": t_upload, **{k: hinfo.get(k) for k in
-                           ("depth", "n_boxes", "k_max", "t_tree", "t_skel")}},
+            "precompute": {"distributed": "every rank: GPU tree, tree-only level-1 ownership, "
+                                          "skeletons of its own subtrees; index data exchanged "
+                                          "through node-local files; max over ranks",
+                           "t_generate_s": t_gen, "t_total_s": t_pre, "t_plan_s": t_upload,
+                           "t_tree_s": t_tree, "t_skel_s": t_skel, "depth": hinfo.get("depth"),
+                           "n_boxes": hinfo.get("n_boxes")},
             "cpu_baseline": {"value": None, "unit": UNIT, "cores": None, "kind": "reference",
                              "sample": "reported by the 1-GPU run (rank 0 at N=1 only)"},
         }
