@@ -31,7 +31,6 @@ namespace {
 constexpr int kMWarps = 4;
 constexpr int kMThreads = 32 * kMWarps;
 constexpr int kChunk = kChunkM;  // sources staged per chunk (4 k-steps of 4)
-constexpr int kMEntCap = 128;  // entries of a task held in shared memory (else read globally)
 constexpr double kInv4Pi = 0.0795774715459476678844418816862571810;
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
@@ -68,6 +67,11 @@ struct K2MArgs {
   double* stage;       // symmetric u pass: staged column sums [point][kNRHS] (pre-scaled)
   unsigned* sflag;     // symmetric u pass: per staged chunk, warps of the tiles that have added
 };
+
+// A task's whole entry list (source box records, codes, staged offsets) is
+// held in shared memory, so the chunk iterator never touches global memory;
+// plans with a longer list take the column loop instead (configure_multi).
+constexpr int kMEntCap = 256;
 
 __device__ __forceinline__ unsigned ld_acquire_flag(const unsigned* p) {
   unsigned v;
@@ -199,16 +203,13 @@ __global__ void __launch_bounds__(kMThreads, SYM ? (KER == SFMM_HELMHOLTZ3D ? SF
     const Task task = a.tasks[t];
     const BoxRec tb = a.box[task.box];
     const EntryRange er = a.er[task.box];
-    const bool ent_smem = er.count <= kMEntCap;
-    if (ent_smem) {
-      for (int i = tid; i < er.count; i += kMThreads) {
-        const int32_t code = a.ent[er.begin + i];
-        s_code[i] = code;
-        s_sb[i] = a.box[code >> kModeBits];
-        if (SYM) s_soff[i] = a.soff[er.begin + i];
-      }
-      __syncthreads();
+    for (int i = tid; i < er.count; i += kMThreads) {  // er.count <= kMEntCap (configure_multi)
+      const int32_t code = a.ent[er.begin + i];
+      s_code[i] = code;
+      s_sb[i] = a.box[code >> kModeBits];
+      if (SYM) s_soff[i] = a.soff[er.begin + i];
     }
+    __syncthreads();
     if constexpr (SYM) {  // the task's charges (zero past its rows); ordered by the barrier before the loop
       for (int v = tid; v < kMultiRows * kNRHS; v += kMThreads) {
         const int row = v / kNRHS, r = v % kNRHS;
@@ -223,11 +224,9 @@ __global__ void __launch_bounds__(kMThreads, SYM ? (KER == SFMM_HELMHOLTZ3D ? SF
         }
       }
     }
-    auto ent_code = [&](int e) -> int32_t { return ent_smem ? s_code[e] : a.ent[er.begin + e]; };
-    auto ent_soff = [&](int e) -> int32_t { return ent_smem ? s_soff[e] : a.soff[er.begin + e]; };
-    auto ent_box = [&](int e) -> BoxRec {
-      return ent_smem ? s_sb[e] : a.box[a.ent[er.begin + e] >> kModeBits];
-    };
+    auto ent_code = [&](int e) -> int32_t { return s_code[e]; };
+    auto ent_soff = [&](int e) -> int32_t { return s_soff[e]; };
+    auto ent_box = [&](int e) -> BoxRec { return s_sb[e]; };
     const int wrow0 = task.row0 + 16 * warp;  // this warp's 16 rows
     const int rend = task.row0 + task.nrows;
     double xr[2], yr[2], zr[2];
@@ -369,7 +368,7 @@ __global__ void __launch_bounds__(kMThreads, SYM ? (KER == SFMM_HELMHOLTZ3D ? SF
     };
     while (cur.e < er.count || is_sym(prev)) {
       chp = &chb[buf];
-      const bool live = cur.e < er.count;
+      const bool live = !SYM || cur.e < er.count;  // (without SYM the loop runs live chunks only)
       const int32_t code = live ? ent_code(cur.e) : 0;
       const bool self = live && (code >> kModeBits) == task.box;
       const bool csym = SYM && live && (code & kModeMask) == kSYM;
@@ -738,6 +737,8 @@ constexpr size_t sym_smem_bytes(bool cplx) {
   return (size_t)3 * kMultiRows * kChunk * (cplx ? 2 : 1) * sizeof(double);
 }
 
+size_t k2m_smem(bool cplx, bool sym) { return sym ? sym_smem_bytes(cplx) : 0; }
+
 template <int KER, bool TAB, bool TFO>
 bool allow_sym_smem() {
   return cudaFuncSetAttribute(k2m_translate<KER, false, TAB, TFO, true>,
@@ -745,7 +746,7 @@ bool allow_sym_smem() {
                               (int)sym_smem_bytes(KER == SFMM_HELMHOLTZ3D)) == cudaSuccess;
 }
 
-template <int KER, bool HPASS, bool SYM = false>
+template <int KER, bool HPASS, bool SYM>
 int blocks_per_sm() {
   constexpr bool CPLX = KER == SFMM_HELMHOLTZ3D;
   if (SYM && !(allow_sym_smem<KER, CPLX, false>() && allow_sym_smem<KER, CPLX, true>() &&
@@ -754,28 +755,30 @@ int blocks_per_sm() {
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
           &per_sm, k2m_translate<KER, HPASS, CPLX, false, SYM>, kMThreads,
-          SYM ? sym_smem_bytes(CPLX) : 0) != cudaSuccess)
+          k2m_smem(CPLX, SYM)) != cudaSuccess)
     return -1;
   return std::max(1, per_sm);
 }
 
 }  // namespace
 
-int configure_multi(DevPlan& p, int device, size_t max_k) {
+int configure_multi(DevPlan& p, int device, size_t max_k, int max_entries) {
   int sms = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
+  // the DMMA path holds a task's entry list in shared memory
+  p.k2m_ok = max_entries <= kMEntCap ? 1 : 0;
   int bh, b0, bs;
   if (p.kernel == SFMM_HELMHOLTZ3D) {
-    bh = blocks_per_sm<SFMM_HELMHOLTZ3D, true>();
-    b0 = blocks_per_sm<SFMM_HELMHOLTZ3D, false>();
+    bh = blocks_per_sm<SFMM_HELMHOLTZ3D, true, false>();
+    b0 = blocks_per_sm<SFMM_HELMHOLTZ3D, false, false>();
     bs = blocks_per_sm<SFMM_HELMHOLTZ3D, false, true>();
   } else if (p.kernel == SFMM_LAPLACE3D) {
-    bh = blocks_per_sm<SFMM_LAPLACE3D, true>();
-    b0 = blocks_per_sm<SFMM_LAPLACE3D, false>();
+    bh = blocks_per_sm<SFMM_LAPLACE3D, true, false>();
+    b0 = blocks_per_sm<SFMM_LAPLACE3D, false, false>();
     bs = blocks_per_sm<SFMM_LAPLACE3D, false, true>();
   } else {
-    bh = blocks_per_sm<SFMM_LAPLACE2D, true>();
-    b0 = blocks_per_sm<SFMM_LAPLACE2D, false>();
+    bh = blocks_per_sm<SFMM_LAPLACE2D, true, false>();
+    b0 = blocks_per_sm<SFMM_LAPLACE2D, false, false>();
     bs = blocks_per_sm<SFMM_LAPLACE2D, false, true>();
   }
   if (bh < 0 || b0 < 0 || bs < 0) return -1;
@@ -883,19 +886,19 @@ void launch_translate_m(const DevPlan& p, DevState& s, cudaStream_t st) {
     a.counter = p.counter + 2 + part;
     const int grid =
         (int)std::min<int64_t>(part == 0 ? (psym ? p.k2m_grid_sym : p.k2m_grid0) : p.k2m_grid, t1);
-    const size_t ssm = sym_smem_bytes(p.cplx != 0);
+    const size_t ssm = k2m_smem(p.cplx != 0, psym);
 #define SFMM_K2M_LAUNCH(KER, TAB)                                                   \
   do {                                                                              \
     if (part == 1)                                                                  \
-      k2m_translate<KER, true, TAB, false, false><<<grid, kMThreads, 0, st>>>(a);   \
+      k2m_translate<KER, true, TAB, false, false><<<grid, kMThreads, ssm, st>>>(a); \
     else if (psym && p.has_tfo_m)                                                   \
       k2m_translate<KER, false, TAB, true, true><<<grid, kMThreads, ssm, st>>>(a);  \
     else if (psym)                                                                  \
       k2m_translate<KER, false, TAB, false, true><<<grid, kMThreads, ssm, st>>>(a); \
     else if (p.has_tfo_m)                                                           \
-      k2m_translate<KER, false, TAB, true, false><<<grid, kMThreads, 0, st>>>(a);   \
+      k2m_translate<KER, false, TAB, true, false><<<grid, kMThreads, ssm, st>>>(a); \
     else                                                                            \
-      k2m_translate<KER, false, TAB, false, false><<<grid, kMThreads, 0, st>>>(a);  \
+      k2m_translate<KER, false, TAB, false, false><<<grid, kMThreads, ssm, st>>>(a);\
   } while (0)
     if (p.kernel == SFMM_HELMHOLTZ3D && p.sc_tab_ok)
       SFMM_K2M_LAUNCH(SFMM_HELMHOLTZ3D, true);

@@ -73,6 +73,7 @@ struct DevPlan {
   int64_t n_tasks_mh;  // tasks_m[0, n_tasks_mh) own skeleton rows
   int has_tfo_m = 0;   // entries_full holds tfo entries (K2m u pass needs qhat too)
   int k2m_grid, k2m_grid0;
+  int k2m_ok = 1;        // every entry list fits K2m's shared memory (else the column loop)
   size_t down_m_smem;
   // symmetric multi-RHS u pass (HostPlan::multi_sym; staging in DevState::stage)
   int multi_sym = 0;
@@ -171,7 +172,7 @@ int configure_tree_kernels(DevPlan& p, size_t max_r, size_t max_k);
 
 // Multi-RHS passes over kNRHS right-hand sides at once (state stride kNRHS);
 // nc <= kNRHS live columns, the rest are zero padding.
-int configure_multi(DevPlan& p, int device, size_t max_k);
+int configure_multi(DevPlan& p, int device, size_t max_k, int max_entries);
 void launch_gather_m(const DevPlan& p, const double* q, int nc, DevState& s, cudaStream_t st);
 void launch_upward_m(const DevPlan& p, const HostPlan& hp, int level, DevState& s, cudaStream_t st);
 void launch_translate_m(const DevPlan& p, DevState& s, cudaStream_t st);

@@ -298,7 +298,7 @@ struct sfmm_gpu_plan {
       const char* v = std::getenv("SFMM_MULTI");
       return !(v && std::atoi(v) == 0);
     }();
-    if (nrhs == 1 || hp.depth < 2 || !env_multi) {
+    if (nrhs == 1 || hp.depth < 2 || !env_multi || !dp.k2m_ok) {
       for (int r = 0; r < nrhs; ++r) enqueue_one(q + r * col_d, u + r * col_d, st, time_k2 && r == 0);
       return;
     }

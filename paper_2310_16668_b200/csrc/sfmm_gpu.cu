@@ -272,7 +272,10 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
       }
       if (configure_translate(dp, device) != 0)
         throw CudaFail{SFMM_ECUDA, "occupancy query failed"};
-      if (configure_multi(dp, device, max_k) != 0)
+      int max_entries = 0;
+      for (const EntryRange& e : hp.ent_range_full) max_entries = std::max(max_entries, e.count);
+      for (const EntryRange& e : hp.ent_range_msym) max_entries = std::max(max_entries, e.count);
+      if (configure_multi(dp, device, max_k, max_entries) != 0)
         throw CudaFail{SFMM_EUNSUPPORTED, "multi-RHS configuration failed"};
       p->ds.Q = p->alloc<double>((size_t)hp.n_slots * sw);
       p->ds.U = p->alloc<double>((size_t)hp.n_slots * sw);
