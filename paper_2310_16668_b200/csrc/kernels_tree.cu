@@ -614,6 +614,48 @@ __global__ void k_build_leaf_maps(SlotBuildArgs a) {
   }
 }
 
+// One tree level in ONE launch: blocks [0, n_copy_blocks) do the level's
+// uncompressed boxes' copies (8 boxes per block, warp per box), the rest its
+// interpolation items (K1 upward / K3 downward), so each level costs one
+// launch instead of two (launch-bound small plans).
+template <class S, bool UP>
+__global__ void __launch_bounds__(kUpThreads) k_level(const int32_t* __restrict__ copy_boxes,
+                                                     int64_t n_copy, int n_copy_blocks,
+                                                     const LevelItem* __restrict__ items,
+                                                     const BoxRec* __restrict__ box,
+                                                     const int64_t* __restrict__ T_off,
+                                                     const double* __restrict__ T,
+                                                     double* __restrict__ V, double* __restrict__ VH,
+                                                     const int32_t* __restrict__ up_dst) {
+  static_assert(kUpThreads == kDownCols, "one block shape for K1 and K3 items");
+  extern __shared__ __align__(16) unsigned char lv_smem[];
+  if ((int)blockIdx.x < n_copy_blocks) {
+    const int64_t w = (int64_t)blockIdx.x * (kUpThreads / 32) + (threadIdx.x >> 5);
+    if (w >= n_copy) return;
+    const BoxRec br = box[copy_boxes[w]];
+    if (UP)
+      k1_copy_box<S>(br, threadIdx.x & 31, reinterpret_cast<S*>(V), reinterpret_cast<S*>(VH), up_dst);
+    else
+      k3_copy_box<S>(br, threadIdx.x & 31, reinterpret_cast<S*>(V), reinterpret_cast<const S*>(VH),
+                     up_dst);
+    return;
+  }
+  const LevelItem it = items[blockIdx.x - n_copy_blocks];
+  if constexpr (sizeof(S) == 16) {
+    if (UP)
+      k1_cplx_item(it, box, T_off, reinterpret_cast<const double2*>(T), reinterpret_cast<double2*>(V),
+                   reinterpret_cast<double2*>(VH), up_dst, reinterpret_cast<double2*>(lv_smem));
+    else
+      k3_cplx_item(it, box, T_off, reinterpret_cast<const double2*>(T), reinterpret_cast<double2*>(V),
+                   reinterpret_cast<const double2*>(VH), up_dst, reinterpret_cast<double2*>(lv_smem));
+  } else {
+    if (UP)
+      k1_real_item(it, box, T_off, T, V, VH, up_dst, reinterpret_cast<double*>(lv_smem));
+    else
+      k3_real_item(it, box, T_off, T, V, VH, up_dst, reinterpret_cast<double*>(lv_smem));
+  }
+}
+
 // ---- persistent tree passes (small, launch-bound plans) --------------------
 // One launch runs the whole upward pass (K0, then every level deepest first)
 // or the whole downward pass (every level coarsest first, then K4).  CTAs
@@ -742,6 +784,18 @@ void launch_scatter(const DevPlan& p, const DevState& s, double* u, cudaStream_t
 void launch_upward(const DevPlan& p, const HostPlan& hp, int level, DevState& s,
                    cudaStream_t st) {
   const int64_t c0 = hp.copy_lvl[level], c1 = hp.copy_lvl[level + 1];
+  const int64_t j0 = hp.up1_lvl[level], j1 = hp.up1_lvl[level + 1];
+  if (c1 > c0 && j1 > j0 && !p.k1_bulk) {  // both kinds of work: one launch
+    const int ncb = (int)((c1 - c0 + 7) / 8);
+    const unsigned g = (unsigned)(ncb + (j1 - j0));
+    if (p.cplx)
+      k_level<double2, true><<<g, kUpThreads, p.up_smem, st>>>(
+          p.copy_boxes + c0, c1 - c0, ncb, p.up1_items + j0, p.box, p.T_off, p.T, s.Q, s.QH, p.up_dst);
+    else
+      k_level<double, true><<<g, kUpThreads, p.up_smem, st>>>(
+          p.copy_boxes + c0, c1 - c0, ncb, p.up1_items + j0, p.box, p.T_off, p.T, s.Q, s.QH, p.up_dst);
+    return;
+  }
   if (c1 > c0) {
     const unsigned g = (unsigned)((c1 - c0 + 7) / 8);
     if (p.cplx)
@@ -769,6 +823,18 @@ void launch_upward(const DevPlan& p, const HostPlan& hp, int level, DevState& s,
 void launch_downward(const DevPlan& p, const HostPlan& hp, int level, DevState& s,
                      cudaStream_t st) {
   const int64_t c0 = hp.copy_lvl[level], c1 = hp.copy_lvl[level + 1];
+  const int64_t j0 = hp.down_lvl[level], j1 = hp.down_lvl[level + 1];
+  if (c1 > c0 && j1 > j0) {  // both kinds of work: one launch
+    const int ncb = (int)((c1 - c0 + 7) / 8);
+    const unsigned g = (unsigned)(ncb + (j1 - j0));
+    if (p.cplx)
+      k_level<double2, false><<<g, kDownCols, p.down_smem, st>>>(
+          p.copy_boxes + c0, c1 - c0, ncb, p.down_items + j0, p.box, p.T_off, p.T, s.U, s.UH, p.up_dst);
+    else
+      k_level<double, false><<<g, kDownCols, p.down_smem, st>>>(
+          p.copy_boxes + c0, c1 - c0, ncb, p.down_items + j0, p.box, p.T_off, p.T, s.U, s.UH, p.up_dst);
+    return;
+  }
   if (c1 > c0) {
     const unsigned g = (unsigned)((c1 - c0 + 7) / 8);
     if (p.cplx)
@@ -1019,7 +1085,15 @@ int configure_tree_kernels(DevPlan& p, size_t max_r, size_t max_k) {
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     p.persist_grid = sms * std::max(1, per_sm);
   }
+  if (p.up_smem > 48 * 1024 &&
+      cudaFuncSetAttribute(p.cplx ? (const void*)k_level<double2, true> : (const void*)k_level<double, true>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.up_smem) != cudaSuccess)
+    return -1;
   p.down_smem = std::max<size_t>(max_k * sw, 16);
+  if (p.down_smem > 48 * 1024 &&
+      cudaFuncSetAttribute(p.cplx ? (const void*)k_level<double2, false> : (const void*)k_level<double, false>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.down_smem) != cudaSuccess)
+    return -1;
   if (p.down_smem > 48 * 1024) {
     if (cudaFuncSetAttribute(
             p.cplx ? (const void*)k3_downward_cplx : (const void*)k3_downward_real,

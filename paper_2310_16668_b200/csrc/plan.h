@@ -331,12 +331,13 @@ struct sfmm_gpu_plan {
     if (hp.depth < 2) return 1;
     int n = 3;  // gather, translate, scatter
     if (dp.tree_persist) {
-      n = 3;  // persistent upward (with the gather), translate, persistent downward (with the scatter)
+      n = 3;  // persistent upward (with the gather), translate, persistent downward (+ scatter)
     } else {
-      for (int l = 2; l <= hp.depth; ++l) {
-        n += hp.up1_lvl[l + 1] > hp.up1_lvl[l] ? 1 : 0;
-        n += hp.down_lvl[l + 1] > hp.down_lvl[l] ? 1 : 0;
-        n += hp.copy_lvl[l + 1] > hp.copy_lvl[l] ? 2 : 0;  // k1_copy + k3_copy
+      for (int l = 2; l <= hp.depth; ++l) {  // one launch per level and pass when both
+        const bool c = hp.copy_lvl[l + 1] > hp.copy_lvl[l];  // copies and items exist (k_level)
+        const bool u = hp.up1_lvl[l + 1] > hp.up1_lvl[l], d = hp.down_lvl[l + 1] > hp.down_lvl[l];
+        n += (c && u && !dp.k1_bulk) ? 1 : (c ? 1 : 0) + (u ? 1 : 0);
+        n += (c && d) ? 1 : (c ? 1 : 0) + (d ? 1 : 0);
       }
     }
     if (dp.n_tasks == 0) --n;
