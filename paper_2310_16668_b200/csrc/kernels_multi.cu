@@ -228,7 +228,9 @@ __global__ void __launch_bounds__(kMThreads, SYM ? (KER == SFMM_HELMHOLTZ3D ? SF
     auto ent_soff = [&](int e) -> int32_t { return s_soff[e]; };
     auto ent_box = [&](int e) -> BoxRec { return s_sb[e]; };
     const int wrow0 = task.row0 + 16 * warp;  // this warp's 16 rows
-    const int rend = task.row0 + task.nrows;
+    // the uhat pass needs the skeleton rows only: warps past them skip the chunk
+    // work entirely (a box's last skeleton tile is often mostly redundant rows)
+    const int rend = task.row0 + (HPASS ? min(task.nrows, tb.k - task.row0) : task.nrows);
     double xr[2], yr[2], zr[2];
     int rowi[2];
 #pragma unroll
@@ -873,13 +875,13 @@ void launch_translate_m(const DevPlan& p, DevState& s, cudaStream_t st) {
     cudaMemsetAsync(s.stage_flags, 0,
                     (size_t)(std::max<int64_t>(p.stage_m_points, kChunk) / kChunk) * sizeof(unsigned), st);
   // part 0: the u pass over every task (symmetric plans: the folded lists,
-  // then K2bm); part 1: the uhat pass over the tasks [0, n_tasks_mh) that own
-  // skeleton rows (unfolded lists)
+  // then K2bm); part 1: the uhat pass over the tasks that own skeleton rows
+  // (unfolded lists, its own longest-first order)
   for (int part = 0; part < 2; ++part) {
     const int64_t t1 = part == 0 ? (sym ? p.n_tasks_msym : p.n_tasks_m) : p.n_tasks_mh;
     if (t1 <= 0) continue;
     const bool psym = sym && part == 0;
-    a.tasks = psym ? p.tasks_msym : p.tasks_m;
+    a.tasks = part == 1 ? p.tasks_mh : (psym ? p.tasks_msym : p.tasks_m);
     a.er = psym ? p.ent_range_msym : p.ent_range_full;
     a.ent = psym ? p.entries_msym : p.entries_full;
     a.n_tasks = t1;

@@ -70,7 +70,8 @@ struct DevPlan {
   Task* tasks_m;
   int64_t n_tasks_m;
   LevelItem* down_m_items;
-  int64_t n_tasks_mh;  // tasks_m[0, n_tasks_mh) own skeleton rows
+  Task* tasks_mh;      // the uhat pass's tasks (own skeleton rows)
+  int64_t n_tasks_mh;
   int has_tfo_m = 0;   // entries_full holds tfo entries (K2m u pass needs qhat too)
   int k2m_grid, k2m_grid0;
   int k2m_ok = 1;        // every entry list fits K2m's shared memory (else the column loop)

@@ -651,33 +651,37 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
     {
       hp.ent_range_full.resize(nb);
       std::vector<std::pair<double, Task>> tv;
+      std::vector<std::pair<double, Task>> th;  // the uhat pass: its own costs
       for (int32_t b = 0; b < nb; ++b) {
         EntryRange& er = hp.ent_range_full[b];
         er.begin = (int64_t)hp.entries_full.size();
         er.count = 0;
         if (!mine(b) || d.box_level[b] < 1) continue;
-        double src = 0;
+        double src = 0, hsrc = 0;
         sources(b, [&](int32_t c, int mode) {
           hp.entries_full.push_back((c << kModeBits) | mode);
           src += hp.box[c].n;
+          hsrc += mode == kIFS ? hp.box[c].n : (mode == kIFO ? hp.box[c].k : 0);
         });
         er.count = (int32_t)((int64_t)hp.entries_full.size() - er.begin);
         if (er.count == 0) continue;
-        for (int32_t r0 = 0; r0 < hp.box[b].n; r0 += kMultiRows)
-          tv.push_back({src * kMultiRows + 64.0,
-                        Task{b, r0, std::min(kMultiRows, hp.box[b].n - r0), 0, 0}});
+        for (int32_t r0 = 0; r0 < hp.box[b].n; r0 += kMultiRows) {
+          const Task t{b, r0, std::min(kMultiRows, hp.box[b].n - r0), 0, 0};
+          tv.push_back({src * kMultiRows + 64.0, t});
+          if (r0 < hp.box[b].k) {  // skeleton rows (16-row warp granularity) x h-weighted sources
+            const int32_t hr = std::min(kMultiRows, hp.box[b].k - r0);
+            th.push_back({hsrc * 16.0 * ((hr + 15) / 16) + 64.0, t});
+          }
+        }
       }
-      // tasks owning skeleton rows first (they need the uhat accumulators and
-      // run a heavier kernel variant), each group longest first
-      std::stable_sort(tv.begin(), tv.end(), [&](const auto& a, const auto& b) {
-        const bool ha = a.second.row0 < hp.box[a.second.box].k;
-        const bool hb = b.second.row0 < hp.box[b.second.box].k;
-        return ha != hb ? ha : a.first > b.first;
-      });
-      for (auto& e : tv) {
-        hp.tasks_m.push_back(e.second);
-        if (e.second.row0 < hp.box[e.second.box].k) ++hp.n_tasks_mh;
-      }
+      std::stable_sort(th.begin(), th.end(),
+                       [](const auto& x, const auto& y) { return x.first > y.first; });
+      for (auto& e : th) hp.tasks_mh.push_back(e.second);
+      // the u pass: longest first
+      std::stable_sort(tv.begin(), tv.end(),
+                       [](const auto& x, const auto& y) { return x.first > y.first; });
+      for (auto& e : tv) hp.tasks_m.push_back(e.second);
+      hp.n_tasks_mh = (int64_t)hp.tasks_mh.size();
     }
 
     // multi-RHS u pass with symmetric colleague blocks (single rank): the

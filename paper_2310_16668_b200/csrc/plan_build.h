@@ -120,8 +120,9 @@ struct HostPlan {
   // multi-RHS path: unfolded CSR (no kSYM), 16-row tasks, 16-column K3 items
   std::vector<EntryRange> ent_range_full;
   std::vector<int32_t> entries_full;
-  std::vector<Task> tasks_m;
-  int64_t n_tasks_mh = 0;                     // tasks_m[0, n_tasks_mh) own skeleton rows
+  std::vector<Task> tasks_m;                  // u pass, longest first
+  std::vector<Task> tasks_mh;                 // uhat pass: the tasks owning skeleton rows,
+  int64_t n_tasks_mh = 0;                     // longest first by their uhat-pass cost
   std::vector<LevelItem> down_m_items;
   std::vector<int64_t> down_m_lvl;
   // multi-RHS u pass with symmetric colleague blocks (single rank,

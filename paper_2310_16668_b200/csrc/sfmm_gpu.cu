@@ -240,6 +240,7 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
       for (int32_t c : hp.entries_full) dp.has_tfo_m |= (c & kModeMask) == kTFO ? 1 : 0;
       dp.n_tasks_m = (int64_t)hp.tasks_m.size();
       dp.n_tasks_mh = hp.n_tasks_mh;
+      dp.tasks_mh = p->upload(hp.tasks_mh);
       dp.down_m_items = p->upload(hp.down_m_items);
       if (hp.multi_sym) {
         dp.multi_sym = 1;
@@ -287,6 +288,7 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
       std::vector<Task>().swap(hp.tasks);
       std::vector<int32_t>().swap(hp.entries_full);
       std::vector<Task>().swap(hp.tasks_m);
+      std::vector<Task>().swap(hp.tasks_mh);
       std::vector<EntryRange>().swap(hp.ent_range_msym);
       std::vector<int32_t>().swap(hp.entries_msym);
       std::vector<int32_t>().swap(hp.ent_soff_m);
