@@ -598,111 +598,185 @@ __device__ __forceinline__ double2 cmulc(double2 t, double2 u) {  // conj(t) * u
   return make_double2(fma(t.x, u.x, t.y * u.y), fma(t.x, u.y, -t.y * u.x));
 }
 
-// K1m: qhat[i][r] = Q[i][r] + sum_j T[i,j] Q[k+j][r]; one CTA per (box, 8 rows),
-// thread (row, rhs); q_R streamed through shared memory in chunks of 64.
+// ---- K1m / K3m: the interpolation operators applied to 16 right-hand sides
+// at once, a (k x r) x (r x 16) product per box on the FP64 tensor cores
+// (DMMA m8n8k4; complex via the 3-multiplication form as in K2m).  Each warp
+// owns 16 rows (two 8-row tiles) x 16 right-hand sides (two 8-column blocks):
+// A fragments come straight from T (each lane one element, rows of 4
+// consecutive entries), B fragments from the right-hand-side block staged in
+// shared memory, [row][16] with the column XOR-swizzled by the row so the
+// fragment loads (4 rows x 8 columns) are conflict-free.
 template <class S>
-__global__ void __launch_bounds__(kUpRows * kNRHS) k1m_upward(const LevelItem* __restrict__ items,
+__device__ __forceinline__ int swz_m(int row, int col) {
+  return col ^ ((row & 3) << (sizeof(S) == 16 ? 1 : 2));
+}
+
+// 3M split of a complex value into the A / B operands of the three products
+__device__ __forceinline__ void parts3(double2 v, double (&o)[3]) {
+  o[0] = v.x;
+  o[1] = v.y;
+  o[2] = v.x + v.y;
+}
+__device__ __forceinline__ void parts3(double v, double (&o)[1]) { o[0] = v; }
+
+constexpr int kUpRowsM = kUpRows;  // K1m rows per CTA: 4 warps x 16
+static_assert(kUpRowsM == 64, "K1m: four warps of 16 rows");
+
+// K1m: qhat[i][.] = Q[i][.] + sum_j T[i,j] Q[k+j][.] for the item's 64
+// skeleton rows; the q_R block is staged 64 sources at a time.
+template <class S>
+__global__ void __launch_bounds__(128) k1m_upward(const LevelItem* __restrict__ items,
                                                   const BoxRec* __restrict__ box,
                                                   const int64_t* __restrict__ T_off,
                                                   const S* __restrict__ T, S* __restrict__ Q,
                                                   S* __restrict__ QH,
                                                   const int32_t* __restrict__ up_dst) {
+  constexpr bool CPLX = sizeof(S) == 16;
+  constexpr int NP = CPLX ? 3 : 1;
   __shared__ S sq[64][kNRHS];
   const LevelItem it = items[blockIdx.x];
   const BoxRec br = box[it.box];
   const int k = br.k, r = br.n - br.k;
-  const int li = threadIdx.x / kNRHS, rhs = threadIdx.x % kNRHS;  // kUpRows rows x 16 rhs
-  const int i = it.first + li;
-  const S* Tb = T + T_off[it.box] + (int64_t)(i < k ? i : 0) * r;
-  S acc{};
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rq = lane >> 2, kq = lane & 3;
+  const S* Tb = T + T_off[it.box];
+  double C[2][NP][2][2] = {};
+  int rowi[2];
+  for (int mt = 0; mt < 2; ++mt) rowi[mt] = it.first + 16 * warp + 8 * mt + rq;
   for (int j0 = 0; j0 < r; j0 += 64) {
     __syncthreads();
     for (int v = threadIdx.x; v < 64 * kNRHS; v += blockDim.x) {
       const int jj = v / kNRHS, rr = v % kNRHS;
-      sq[jj][rr] = j0 + jj < r ? Q[(br.slot + k + j0 + jj) * kNRHS + rr] : S{};
+      sq[jj][swz_m<S>(jj, rr)] = j0 + jj < r ? Q[(br.slot + k + j0 + jj) * kNRHS + rr] : S{};
     }
     __syncthreads();
-    if (i < k) {
-      const int jn = min(64, r - j0);
-      for (int jj = 0; jj < jn; ++jj) {
-        const S t = Tb[j0 + jj];
-        if constexpr (sizeof(S) == 16) {
-          const double2 p = cmul(t, sq[jj][rhs]);
-          acc.x += p.x;
-          acc.y += p.y;
-        } else {
-          acc = fma(t, sq[jj][rhs], acc);
-        }
+    const int jn = min(64, r - j0);
+#pragma unroll 4
+    for (int jj = 0; jj < jn; jj += 4) {
+      const int jr = jj + kq;  // this lane's k index within the staged block
+      double b[2][NP];
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb) parts3(sq[jr][swz_m<S>(jr, 8 * nb + rq)], b[nb]);
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        const int i = rowi[mt], j = j0 + jr;
+        double a[NP];
+        parts3(i < k && j < r ? Tb[(int64_t)i * r + j] : S{}, a);
+#pragma unroll
+        for (int pp = 0; pp < NP; ++pp)
+#pragma unroll
+          for (int nb = 0; nb < 2; ++nb) dmma(C[mt][pp][nb][0], C[mt][pp][nb][1], a[pp], b[nb][pp]);
       }
     }
   }
-  if (i < k && i < it.first + kUpRows) {
-    S v = Q[(br.slot + i) * kNRHS + rhs];
-    if constexpr (sizeof(S) == 16) {
-      v.x += acc.x;
-      v.y += acc.y;
-    } else {
-      v += acc;
-    }
-    QH[(br.skel + i) * kNRHS + rhs] = v;
-    Q[(int64_t)up_dst[br.skel + i] * kNRHS + rhs] = v;
+  // lane holds rows rq (+8) and right-hand sides 2kq, 2kq+1 (+8)
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) {
+    const int i = rowi[mt];
+    if (i >= k || i >= it.first + kUpRowsM) continue;
+    const int64_t dst = up_dst[br.skel + i];
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+      for (int w = 0; w < 2; ++w) {
+        const int rhs = 8 * nb + 2 * kq + w;
+        S v = Q[(br.slot + i) * kNRHS + rhs];
+        if constexpr (CPLX) {
+          const double t1 = C[mt][0][nb][w], t2 = C[mt][1][nb][w];
+          v.x += t1 - t2;
+          v.y += C[mt][2][nb][w] - t1 - t2;
+        } else {
+          v += C[mt][0][nb][w];
+        }
+        QH[(br.skel + i) * kNRHS + rhs] = v;
+        Q[dst * kNRHS + rhs] = v;
+      }
   }
 }
 
-// K3m: uhat = UH + U[parent]; U_S += uhat; U_R[j][r] += sum_i conj(T[i,j]) uhat[i][r].
-// One CTA per (box, 16 columns), thread (column, rhs).
+static_assert(kDownColsM == 64, "K3m: four warps of 16 columns");
+
+// K3m: uhat = UH + U[parent]; U_S += uhat (the item with first == 0);
+// U_R[j][.] += sum_i conj(T[i,j]) uhat[i][.] for the item's 64 columns j.
 template <class S>
-__global__ void __launch_bounds__(256) k3m_downward(const LevelItem* __restrict__ items,
+__global__ void __launch_bounds__(128) k3m_downward(const LevelItem* __restrict__ items,
                                                     const BoxRec* __restrict__ box,
                                                     const int64_t* __restrict__ T_off,
                                                     const S* __restrict__ T, S* __restrict__ U,
                                                     const S* __restrict__ UH,
                                                     const int32_t* __restrict__ up_dst) {
+  constexpr bool CPLX = sizeof(S) == 16;
+  constexpr int NP = CPLX ? 3 : 1;
   extern __shared__ unsigned char smraw[];
-  S* su = reinterpret_cast<S*>(smraw);  // [k][kNRHS]
+  S* su = reinterpret_cast<S*>(smraw);  // [k rounded to 4][kNRHS], swizzled
   const LevelItem it = items[blockIdx.x];
   const BoxRec br = box[it.box];
   const int k = br.k, r = br.n - br.k;
-  for (int v = threadIdx.x; v < k * kNRHS; v += blockDim.x) {
+  const int k4 = (k + 3) & ~3;
+  for (int v = threadIdx.x; v < k4 * kNRHS; v += blockDim.x) {
     const int i = v / kNRHS, rr = v % kNRHS;
-    S a = UH[(br.skel + i) * kNRHS + rr], b = U[(int64_t)up_dst[br.skel + i] * kNRHS + rr];
-    S s;
-    if constexpr (sizeof(S) == 16) {
-      s = make_double2(a.x + b.x, a.y + b.y);
-    } else {
-      s = a + b;
-    }
-    su[v] = s;
-    if (it.first == 0) {
-      S o = U[(br.slot + i) * kNRHS + rr];
-      if constexpr (sizeof(S) == 16) {
-        U[(br.slot + i) * kNRHS + rr] = make_double2(o.x + s.x, o.y + s.y);
+    S s{};
+    if (i < k) {
+      const S a = UH[(br.skel + i) * kNRHS + rr], b = U[(int64_t)up_dst[br.skel + i] * kNRHS + rr];
+      if constexpr (CPLX) {
+        s = make_double2(a.x + b.x, a.y + b.y);
       } else {
-        U[(br.slot + i) * kNRHS + rr] = o + s;
+        s = a + b;
+      }
+      if (it.first == 0) {
+        const S o = U[(br.slot + i) * kNRHS + rr];
+        if constexpr (CPLX) {
+          U[(br.slot + i) * kNRHS + rr] = make_double2(o.x + s.x, o.y + s.y);
+        } else {
+          U[(br.slot + i) * kNRHS + rr] = o + s;
+        }
       }
     }
+    su[i * kNRHS + swz_m<S>(i, rr)] = s;
   }
   __syncthreads();
-  const int jl = threadIdx.x / kNRHS, rhs = threadIdx.x % kNRHS;
-  const int j = it.first + jl;
-  if (j >= r) return;
-  const S* Tb = T + T_off[it.box] + j;
-  S acc{};
-  for (int i = 0; i < k; ++i) {
-    const S t = Tb[(int64_t)i * r];
-    if constexpr (sizeof(S) == 16) {
-      const double2 p = cmulc(t, su[i * kNRHS + rhs]);
-      acc.x += p.x;
-      acc.y += p.y;
-    } else {
-      acc = fma(t, su[i * kNRHS + rhs], acc);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rq = lane >> 2, kq = lane & 3;
+  const int jw = it.first + 16 * warp;  // this warp's 16 columns
+  if (jw >= r) return;
+  const S* Tb = T + T_off[it.box];
+  double C[2][NP][2][2] = {};
+#pragma unroll 4
+  for (int i0 = 0; i0 < k; i0 += 4) {
+    const int i = i0 + kq;
+    double b[2][NP];
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb) parts3(su[i * kNRHS + swz_m<S>(i, 8 * nb + rq)], b[nb]);
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const int j = jw + 8 * mt + rq;
+      S t = i < k && j < r ? Tb[(int64_t)i * r + j] : S{};
+      if constexpr (CPLX) t.y = -t.y;  // conj(T)^T
+      double a[NP];
+      parts3(t, a);
+#pragma unroll
+      for (int pp = 0; pp < NP; ++pp)
+#pragma unroll
+        for (int nb = 0; nb < 2; ++nb) dmma(C[mt][pp][nb][0], C[mt][pp][nb][1], a[pp], b[nb][pp]);
     }
   }
-  S o = U[(br.slot + k + j) * kNRHS + rhs];
-  if constexpr (sizeof(S) == 16) {
-    U[(br.slot + k + j) * kNRHS + rhs] = make_double2(o.x + acc.x, o.y + acc.y);
-  } else {
-    U[(br.slot + k + j) * kNRHS + rhs] = o + acc;
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) {
+    const int j = jw + 8 * mt + rq;
+    if (j >= r) continue;
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+      for (int w = 0; w < 2; ++w) {
+        const int rhs = 8 * nb + 2 * kq + w;
+        S* o = U + (br.slot + k + j) * kNRHS + rhs;
+        if constexpr (CPLX) {
+          const double t1 = C[mt][0][nb][w], t2 = C[mt][1][nb][w];
+          *o = make_double2(o->x + (t1 - t2), o->y + (C[mt][2][nb][w] - t1 - t2));
+        } else {
+          *o += C[mt][0][nb][w];
+        }
+      }
   }
 }
 
@@ -788,7 +862,7 @@ int configure_multi(DevPlan& p, int device, size_t max_k, int max_entries) {
   p.k2m_grid0 = sms * b0;
   p.k2m_grid_sym = sms * bs;
   const size_t sw = p.cplx ? 16 : 8;
-  p.down_m_smem = std::max<size_t>(max_k * kNRHS * sw, 16);
+  p.down_m_smem = std::max<size_t>(((max_k + 3) & ~(size_t)3) * kNRHS * sw, 16);
   if (p.down_m_smem > 48 * 1024) {
     const void* f = p.cplx ? (const void*)k3m_downward<double2> : (const void*)k3m_downward<double>;
     if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.down_m_smem) !=
@@ -824,11 +898,11 @@ void launch_upward_m(const DevPlan& p, const HostPlan& hp, int level, DevState& 
   const int64_t i0 = hp.up_lvl[level], i1 = hp.up_lvl[level + 1];
   if (i1 <= i0) return;
   if (p.cplx)
-    k1m_upward<double2><<<(unsigned)(i1 - i0), kUpRows * kNRHS, 0, st>>>(
+    k1m_upward<double2><<<(unsigned)(i1 - i0), 128, 0, st>>>(
         p.up_items + i0, p.box, p.T_off, reinterpret_cast<const double2*>(p.T),
         reinterpret_cast<double2*>(s.Q), reinterpret_cast<double2*>(s.QH), p.up_dst);
   else
-    k1m_upward<double><<<(unsigned)(i1 - i0), kUpRows * kNRHS, 0, st>>>(p.up_items + i0, p.box, p.T_off, p.T,
+    k1m_upward<double><<<(unsigned)(i1 - i0), 128, 0, st>>>(p.up_items + i0, p.box, p.T_off, p.T,
                                                              s.Q, s.QH, p.up_dst);
 }
 
@@ -837,11 +911,11 @@ void launch_downward_m(const DevPlan& p, const HostPlan& hp, int level, DevState
   const int64_t i0 = hp.down_m_lvl[level], i1 = hp.down_m_lvl[level + 1];
   if (i1 <= i0) return;
   if (p.cplx)
-    k3m_downward<double2><<<(unsigned)(i1 - i0), 256, p.down_m_smem, st>>>(
+    k3m_downward<double2><<<(unsigned)(i1 - i0), 128, p.down_m_smem, st>>>(
         p.down_m_items + i0, p.box, p.T_off, reinterpret_cast<const double2*>(p.T),
         reinterpret_cast<double2*>(s.U), reinterpret_cast<const double2*>(s.UH), p.up_dst);
   else
-    k3m_downward<double><<<(unsigned)(i1 - i0), 256, p.down_m_smem, st>>>(
+    k3m_downward<double><<<(unsigned)(i1 - i0), 128, p.down_m_smem, st>>>(
         p.down_m_items + i0, p.box, p.T_off, p.T, s.U, s.UH, p.up_dst);
 }
 

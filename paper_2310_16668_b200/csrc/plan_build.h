@@ -23,7 +23,7 @@ namespace sfmm_gpu {
 
 constexpr int kRowsPerLane = 4;                 // max rows per lane in K2
 constexpr int kTileRows = 32 * kRowsPerLane;    // rows per K2 task
-constexpr int kUpRows = 32;                     // K1m rows (skeleton entries) per CTA
+constexpr int kUpRows = 64;                     // K1m rows (skeleton entries) per CTA (4 warps x 16)
 #ifndef SFMM_K1_ROWS
 #define SFMM_K1_ROWS 64
 #endif
@@ -31,7 +31,7 @@ constexpr int kUpRows1 = SFMM_K1_ROWS;          // K1 (single rhs) rows per CTA
 constexpr int kDownCols = 256;                  // K3 columns (redundant slots) per CTA
 constexpr int kChunkM = 16;                     // K2m sources per staged chunk
 constexpr int kMultiRows = 64;                  // K2m rows per task (4 warps x two 8-row DMMA tiles)
-constexpr int kDownColsM = 16;                  // K3m columns per CTA (x 16 rhs threads)
+constexpr int kDownColsM = 64;                  // K3m columns per CTA (4 warps x 16)
 
 struct LevelItem {
   int32_t box;
