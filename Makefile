@@ -19,7 +19,7 @@ GPU_OBJS := $(patsubst $(SRC)/%.cu,$(OBJ)/%.o,$(GPU_CU)) $(OBJ)/plan_build.o
 HDRS     := include/sfmm_gpu.h $(SRC)/plan.h $(SRC)/common.cuh $(SRC)/launch.h $(SRC)/plan_build.h $(SRC)/fastmath.cuh $(SRC)/log_table.inc
 
 .PHONY: all gpu host probe oracle clean
-all: gpu host probe
+all: gpu host probe check-bin
 
 HOST_SRC  := $(SRC)/host
 HOST_CPP  := $(HOST_SRC)/host_api.cpp
@@ -63,3 +63,10 @@ oracle:
 
 clean:
 	rm -rf build $(LIB)
+
+# C++ check of the distributed precompute header (run by tests/test_distributed_precompute.py)
+check-bin: build/bin/dist_precompute_check
+
+build/bin/dist_precompute_check: tests/cpp/dist_precompute_check.cpp include/sfmm_gpu_dist.hpp include/sfmm_gpu.h $(LIB)/libsfmm_gpu.so
+	@mkdir -p build/bin
+	$(CXX) -std=c++17 -O2 -Iinclude $< -L$(LIB) -lsfmm_gpu -Wl,-rpath,'$$ORIGIN/../../$(LIB)' -o $@

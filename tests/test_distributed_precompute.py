@@ -91,3 +91,20 @@ def test_sharded_apply_on_distributed_precompute(kernel, dist, n_ranks):
                                                np.asarray(descs[0].arrays["box_begin"])[b]
                                                for b in np.nonzero((owner == r) &
                                                                    (np.asarray(descs[0].arrays["box_level"]) == 1))[0]]))
+
+
+@pytest.mark.parametrize("n_ranks,n,kernel", [(8, 60000, 1), (3, 40000, 3)])
+def test_cpp_rank_precompute_header(n_ranks, n, kernel):
+    """include/sfmm_gpu_dist.hpp (the C++ host side of the same flow): every
+    virtual rank's assembled descriptor and operators equal the whole-tree
+    build, and every rank plan builds (tests/cpp/dist_precompute_check.cpp)."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "build", "bin",
+                       "dist_precompute_check")
+    if not os.path.exists(exe):
+        pytest.skip("build/bin/dist_precompute_check not built (make check-bin)")
+    r = subprocess.run([exe, str(n_ranks), str(n), str(kernel)], capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.startswith("ok")
