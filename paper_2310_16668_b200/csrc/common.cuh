@@ -51,6 +51,13 @@ struct Task {
   int32_t nrows;
   int32_t tile;   // row-tile index within the box (chained kSYM column sums), -1: unchained
   int64_t stage;  // first staging slot of the box's kSYM column sums
+  // Source-range split of a long task (small plans, plan_build.cpp): entries
+  // [e0, e1) of the box's list (e1 < 0: all), and the staging slot where a
+  // part other than the first leaves its raw row partials (-1: the task owns
+  // the rows and writes U / UH itself)
+  int32_t e0 = 0;
+  int32_t e1 = -1;
+  int64_t rstage = -1;
 };
 
 struct EntryRange {

@@ -287,7 +287,8 @@ __device__ __forceinline__ void task_real(const K2Args& a, const Task& t, WarpSm
   const EntryRange er = a.er[t.box];
   const bool skel_rows = t.row0 < tb.k;
   int64_t stage = t.stage;
-  for (int e = 0; e < er.count; ++e) {
+  const int e_end = t.e1 < 0 ? er.count : t.e1;
+  for (int e = t.e0; e < e_end; ++e) {
     const int32_t code = a.ent[er.begin + e];
     const int32_t c = code >> kModeBits;
     const int mode = code & kModeMask;
@@ -358,6 +359,13 @@ __device__ __forceinline__ void task_real(const K2Args& a, const Task& t, WarpSm
     if (row >= t.row0 + t.nrows) continue;
     const bool skel_row = row < tb.k;
     if (!isfinite(au[r]) || (skel_row && !isfinite(ah[r]))) verify_row(a, t.box, row, G::kDim);
+    if constexpr (R == 1) {  // (only 32-row tiles are ever split, plan_build.cpp)
+      if (t.rstage >= 0) {  // a later part of a split task: raw row partials, added by K2b
+        a.St[t.rstage + row] = au[r];
+        if (skel_row) a.St[t.rstage + tb.n + row] = ah[r];
+        continue;
+      }
+    }
     a.U[tb.slot + row] = au[r] * G::kScale;
     if (skel_row) a.UH[tb.skel + row] = -ah[r] * G::kScale;
   }
@@ -389,7 +397,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k2_translate_real_t(K2Args a) 
     if (lane == 0) t = atomicAdd(a.counter, 1);
     t = __shfl_sync(kFull, t, 0);
     if (t >= a.n_tasks) return;
-    const Task task = a.tasks[t];
+    // by reference: the task's fields are read where they are used instead of
+    // being held in registers through the whole task (entry range, row-partial
+    // slot of split tasks)
+    const Task& task = a.tasks[t];
     if constexpr (MAXR == 1) {
       task_real<G, 1, CHAIN>(a, task, sm, lts, lane);
     } else {

@@ -43,6 +43,8 @@ PlanOptions plan_options_from_env() {
   if (const char* v = std::getenv("SFMM_SYM_CHAIN")) o.sym_chain = std::atoi(v) != 0;
   if (const char* v = std::getenv("SFMM_MULTI_SYM")) o.multi_sym = std::atoi(v) != 0;
   if (const char* v = std::getenv("SFMM_TREE_PERSIST")) o.tree_persist = std::atoi(v) != 0 ? 1 : 0;
+  if (const char* v = std::getenv("SFMM_SPLIT")) o.split = std::atoi(v) != 0;
+  if (const char* v = std::getenv("SFMM_SPLIT_PART")) o.split_part = std::atof(v);
   return o;
 }
 
@@ -805,7 +807,7 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
     // them in a fixed order.  Interior tasks (no ghost source) come first so
     // they can run while the ghost exchange is in flight.
     {
-      std::vector<std::vector<std::pair<int64_t, int64_t>>> inbox(hp.symmetric ? nb : 0);
+      std::vector<std::vector<std::pair<int64_t, int64_t>>> inbox(nb);
       std::vector<std::pair<double, Task>> tv_int, tv_bnd;
       int64_t cursor = 0;
       // cost model: lane-rows x (sources + 8)
@@ -851,6 +853,23 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
       // rows per lane of the K2 instantiations this library was built with
       tile = std::min(tile, 32 * (hp.cplx ? SFMM_K2C_MAX_R : SFMM_K2_MAX_R));
       hp.tile_rows = tile;
+      // Source-range split (single-rank real plans of 32-row tiles, small enough
+      // for one task to set the persistent kernel's makespan, config 1): a row tile
+      // costing more than 3/4 of the per-warp share of the work is cut along
+      // its entry list into parts of about half a share.  The first part owns
+      // the rows as usual; each later part leaves raw row partials in a
+      // zero-filled [u: n_b | h: k_b] staging vector (rows outside the tile are
+      // never written) that K2b adds to the box in the fixed part order.
+      double split_share = 0.0;
+      if (n_ranks == 1 && !hp.cplx && !hp.sym_chain && opt.split && tile <= 32) {
+        double total = 0.0;
+        for (int32_t b = 0; b < nb; ++b) {
+          if (hp.ent_range[b].count == 0) continue;
+          for (int32_t r0 = 0; r0 < hp.box[b].n; r0 += tile)
+            total += 32.0 * ((std::min(tile, hp.box[b].n - r0) + 31) / 32) * (src_of[b] + 8.0);
+        }
+        split_share = total / (148.0 * 32.0);  // resident warps of the 32-row (R = 1) K2
+      }
       // outgoing cross-rank pairs in (b, entry) order, the staged tiles of each
       std::vector<std::pair<int32_t, int32_t>> xpairs;
       std::vector<std::vector<std::pair<int64_t, int64_t>>> xtiles;
@@ -870,9 +889,9 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
         // one per (pair, row tile) -- the tile owning skeleton rows carries
         // the h part -- or, with sym_chain, one per pair shared by all of b's
         // row tiles, tile t adding to tile t - 1's in tile order.
-        auto stage_entries = [&](bool h_part) {
-          size_t xi = x0;
-          for (int64_t e = er.begin; e < er.begin + er.count; ++e) {
+        auto stage_entries = [&](bool h_part, int64_t e_from = 0, int64_t e_to = -1) {
+          size_t xi = x0;  // (parts: single-rank plans only, so no cross-rank pairs)
+          for (int64_t e = er.begin + e_from; e < er.begin + (e_to < 0 ? er.count : e_to); ++e) {
             const int32_t code = hp.entries[e];
             if ((code & kModeMask) != kSYM) continue;
             const int32_t c = code >> kModeBits;
@@ -896,10 +915,37 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
         for (int32_t r0 = 0; r0 < hp.box[b].n; r0 += tile, ++tile_index) {
           Task t{b, r0, std::min(tile, hp.box[b].n - r0), hp.sym_chain ? tile_index : -1,
                  hp.sym_chain ? b_stage : cursor};
-          if (!hp.sym_chain) stage_entries(r0 < hp.box[b].k);
           const double lanes_rows = 32.0 * ((t.nrows + 31) / 32);
+          const double cost = lanes_rows * (src + 8.0);
           // without overlap every task runs in the one launch after the exchange
-          ((boundary[b] || !opt.overlap) ? tv_bnd : tv_int).push_back({lanes_rows * (src + 8.0), t});
+          auto& tv = (boundary[b] || !opt.overlap) ? tv_bnd : tv_int;
+          if (split_share > 0.0 && cost > 1.5 * opt.split_part * split_share && er.count > 1) {
+            const bool skel = r0 < hp.box[b].k;
+            int32_t e0 = 0;
+            double acc = 0.0;
+            for (int32_t e = 0; e < er.count; ++e) {
+              const int32_t code = hp.entries[er.begin + e];
+              acc += lanes_rows * ((code & kModeMask) == kSYM ? 1.15 : 1.0) * hp.box[code >> kModeBits].n;
+              if (acc < opt.split_part * split_share && e + 1 < er.count) continue;
+              Task part = t;
+              part.stage = cursor;
+              part.e0 = e0;
+              part.e1 = e + 1;
+              stage_entries(skel, e0, e + 1);
+              if (e0 > 0) {  // a later part: its row-partial vector
+                part.rstage = cursor;
+                inbox[b].push_back({cursor, skel ? cursor + hp.box[b].n : -1});
+                cursor += (hp.box[b].n + (skel ? hp.box[b].k : 0) + 31) & ~(int64_t)31;
+                ++hp.n_split_parts;
+              }
+              tv.push_back({acc + lanes_rows * 8.0, part});
+              e0 = e + 1;
+              acc = 0.0;
+            }
+            continue;
+          }
+          if (!hp.sym_chain) stage_entries(r0 < hp.box[b].k);
+          tv.push_back({cost, t});
         }
       }
       hp.stage_size = cursor;

@@ -94,6 +94,7 @@ struct HostPlan {
   std::vector<int64_t> recv_off;              // recv_box.size() + 1
   std::vector<int64_t> recv_u, recv_h;
   int64_t n_skipped_pairs = 0;                // cancelling pairs not evaluated
+  int64_t n_split_parts = 0;                  // later parts of source-range split tasks
   int64_t n_interior_tasks = 0;               // tasks[0, n_interior) read no ghost box
   // sharding: owner rank of every box (whole subtrees at the cut
   // level; kShared: internal boxes above the cut, evaluated on every rank)
@@ -217,6 +218,10 @@ struct PlanOptions {
   // levels + scatter) instead of one to three launches per level: -1 = for
   // plans of at most kTreePersistPoints points (SFMM_TREE_PERSIST=0/1 forces)
   int tree_persist = -1;
+  // small single-rank real plans: cut the row tiles that would set K2's
+  // makespan along their entry lists (SFMM_SPLIT=0 turns it off)
+  bool split = true;
+  double split_part = 0.5;  // part size as a fraction of the per-warp share (split above 1.5x it)
 };
 PlanOptions plan_options_from_env();
 

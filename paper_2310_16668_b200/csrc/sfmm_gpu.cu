@@ -221,6 +221,11 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
       dp.n_recv2 = n_recv2;
       dp.n_send2 = hp.send2_off.empty() ? 0 : hp.send2_off.back();
       dp.stage = p->alloc<double>((size_t)std::max<int64_t>(hp.stage_size + n_recv2, 1) * sw);
+      // row partials of split tasks: rows outside a part's tile are never
+      // written and must read as zero in K2b
+      if (hp.n_split_parts > 0)
+        ck(cudaMemset(dp.stage, 0, sizeof(double) * (size_t)(hp.stage_size + n_recv2) * sw),
+           "zero staging");
       dp.stage_flags = p->alloc<unsigned>((size_t)std::max<int64_t>(hp.stage_size >> 5, 1));
       dp.n_xpairs = (int64_t)hp.xpair_dst.size();
       dp.xpair_tile_off = p->upload(hp.xpair_tile_off);
