@@ -354,42 +354,90 @@ __global__ void __launch_bounds__(256) k4_scatter(const int32_t* __restrict__ sl
     k4_point<S>(t, slot, orig, hat, up_dst, U, UH, u);
 }
 
+__device__ __forceinline__ double shfl_s(double v, int src) { return __shfl_sync(kFull, v, src); }
+__device__ __forceinline__ double2 shfl_s(double2 v, int src) {
+  return make_double2(__shfl_sync(kFull, v.x, src), __shfl_sync(kFull, v.y, src));
+}
+__device__ __forceinline__ double fma_s(double t, double q, double acc) { return fma(t, q, acc); }
+__device__ __forceinline__ double2 fma_s(double2 t, double2 q, double2 acc) {  // acc + t q
+  return make_double2(fma(t.x, q.x, fma(-t.y, q.y, acc.x)), fma(t.x, q.y, fma(t.y, q.x, acc.y)));
+}
+__device__ __forceinline__ double fma_cs(double t, double u, double acc) { return fma(t, u, acc); }
+__device__ __forceinline__ double2 fma_cs(double2 t, double2 u, double2 acc) {  // acc + conj(t) u
+  return make_double2(fma(t.x, u.x, fma(t.y, u.y, acc.x)), fma(t.x, u.y, fma(-t.y, u.x, acc.y)));
+}
+
+// One box per warp (uncompressed boxes, r = 0: copies only; boxes with a
+// short interpolation block, 0 < r <= kWarpBoxR: lane = row of T, q_R held
+// one entry per lane and broadcast by shuffles -- no reduction, no idle CTA
+// threads, on adaptive trees most boxes of the deepest levels).
 template <class S>
-__device__ __forceinline__ void k1_copy_box(const BoxRec br, int lane, S* __restrict__ Q,
-                                            S* __restrict__ QH, const int32_t* __restrict__ up_dst) {
-  for (int i = lane; i < br.k; i += 32) {
-    const S v = __ldcg(Q + br.slot + i);
-    QH[br.skel + i] = v;
-    Q[up_dst[br.skel + i]] = v;
+__device__ __forceinline__ void k1_copy_box(const BoxRec br, int lane, const S* __restrict__ Tb,
+                                            S* __restrict__ Q, S* __restrict__ QH,
+                                            const int32_t* __restrict__ up_dst) {
+  const int k = br.k, r = br.n - br.k;
+  const S qr = lane < r ? __ldcg(Q + br.slot + k + lane) : S{};
+  for (int i0 = 0; i0 < k; i0 += 32) {
+    const int i = i0 + lane;
+    S acc{};
+    for (int j = 0; j < r; ++j) {
+      const S q = shfl_s(qr, j);
+      if (i < k) acc = fma_s(Tb[(int64_t)i * r + j], q, acc);
+    }
+    if (i < k) {
+      const S q = __ldcg(Q + br.slot + i);
+      const S v = r > 0 ? add_s(q, acc) : q;
+      QH[br.skel + i] = v;
+      Q[up_dst[br.skel + i]] = v;
+    }
   }
 }
 
 template <class S>
-__device__ __forceinline__ void k3_copy_box(const BoxRec br, int lane, S* __restrict__ U,
-                                            const S* __restrict__ UH,
+__device__ __forceinline__ void k3_copy_box(const BoxRec br, int lane, const S* __restrict__ Tb,
+                                            S* __restrict__ U, const S* __restrict__ UH,
                                             const int32_t* __restrict__ up_dst) {
-  for (int i = lane; i < br.k; i += 32)
-    U[br.slot + i] = add_s(__ldcg(U + br.slot + i),
-                           add_s(__ldcg(UH + br.skel + i), __ldcg(U + up_dst[br.skel + i])));
+  const int k = br.k, r = br.n - br.k;
+  S acc{};  // lane j < r: U_R[j] += sum_i conj(T[i,j]) uhat[i]
+  for (int i0 = 0; i0 < k; i0 += 32) {
+    const int i = i0 + lane;
+    S uh{};
+    if (i < k) {
+      uh = add_s(__ldcg(UH + br.skel + i), __ldcg(U + up_dst[br.skel + i]));
+      U[br.slot + i] = add_s(__ldcg(U + br.slot + i), uh);
+    }
+    const int cnt = min(32, k - i0);
+    for (int ii = 0; ii < cnt && r > 0; ++ii) {
+      const S u = shfl_s(uh, ii);
+      if (lane < r) acc = fma_cs(Tb[(int64_t)(i0 + ii) * r + lane], u, acc);
+    }
+  }
+  if (lane < r) U[br.slot + k + lane] = add_s(__ldcg(U + br.slot + k + lane), acc);
 }
 
 template <class S>
 __global__ void __launch_bounds__(256) k1_copy(const int32_t* __restrict__ boxes, int64_t nbox,
-                                               const BoxRec* __restrict__ box, S* __restrict__ Q,
+                                               const BoxRec* __restrict__ box,
+                                               const int64_t* __restrict__ T_off,
+                                               const S* __restrict__ T, S* __restrict__ Q,
                                                S* __restrict__ QH, const int32_t* __restrict__ up_dst) {
   const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (w >= nbox) return;
-  k1_copy_box<S>(box[boxes[w]], threadIdx.x & 31, Q, QH, up_dst);
+  const int32_t b = boxes[w];
+  k1_copy_box<S>(box[b], threadIdx.x & 31, T + T_off[b], Q, QH, up_dst);
 }
 
 template <class S>
 __global__ void __launch_bounds__(256) k3_copy(const int32_t* __restrict__ boxes, int64_t nbox,
-                                               const BoxRec* __restrict__ box, S* __restrict__ U,
+                                               const BoxRec* __restrict__ box,
+                                               const int64_t* __restrict__ T_off,
+                                               const S* __restrict__ T, S* __restrict__ U,
                                                const S* __restrict__ UH,
                                                const int32_t* __restrict__ up_dst) {
   const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (w >= nbox) return;
-  k3_copy_box<S>(box[boxes[w]], threadIdx.x & 31, U, UH, up_dst);
+  const int32_t b = boxes[w];
+  k3_copy_box<S>(box[b], threadIdx.x & 31, T + T_off[b], U, UH, up_dst);
 }
 
 // K3, real: uhat = UH + U[parent slice]; U_S += uhat; U_R += T^T uhat.
@@ -632,12 +680,14 @@ __global__ void __launch_bounds__(kUpThreads) k_level(const int32_t* __restrict_
   if ((int)blockIdx.x < n_copy_blocks) {
     const int64_t w = (int64_t)blockIdx.x * (kUpThreads / 32) + (threadIdx.x >> 5);
     if (w >= n_copy) return;
-    const BoxRec br = box[copy_boxes[w]];
+    const int32_t b = copy_boxes[w];
+    const S* Tb = reinterpret_cast<const S*>(T) + T_off[b];
     if (UP)
-      k1_copy_box<S>(br, threadIdx.x & 31, reinterpret_cast<S*>(V), reinterpret_cast<S*>(VH), up_dst);
-    else
-      k3_copy_box<S>(br, threadIdx.x & 31, reinterpret_cast<S*>(V), reinterpret_cast<const S*>(VH),
+      k1_copy_box<S>(box[b], threadIdx.x & 31, Tb, reinterpret_cast<S*>(V), reinterpret_cast<S*>(VH),
                      up_dst);
+    else
+      k3_copy_box<S>(box[b], threadIdx.x & 31, Tb, reinterpret_cast<S*>(V),
+                     reinterpret_cast<const S*>(VH), up_dst);
     return;
   }
   const LevelItem it = items[blockIdx.x - n_copy_blocks];
@@ -718,12 +768,14 @@ __global__ void __launch_bounds__(kUpThreads) k_tree_persist(TreePassArgs a) {
       }
     } else if (job.kind == kJobCopy) {
       if (warp < job.b) {
-        const BoxRec br = a.box[a.copy_boxes[job.a + warp]];
+        const int32_t b = a.copy_boxes[job.a + warp];
+        const S* Tb = reinterpret_cast<const S*>(a.T) + a.T_off[b];
         if (UP)
-          k1_copy_box<S>(br, lane, reinterpret_cast<S*>(a.Q), reinterpret_cast<S*>(a.QH), a.up_dst);
-        else
-          k3_copy_box<S>(br, lane, reinterpret_cast<S*>(a.U), reinterpret_cast<const S*>(a.UH),
+          k1_copy_box<S>(a.box[b], lane, Tb, reinterpret_cast<S*>(a.Q), reinterpret_cast<S*>(a.QH),
                          a.up_dst);
+        else
+          k3_copy_box<S>(a.box[b], lane, Tb, reinterpret_cast<S*>(a.U),
+                         reinterpret_cast<const S*>(a.UH), a.up_dst);
       }
     } else {
       const LevelItem it = a.items[job.a];
@@ -785,7 +837,7 @@ void launch_upward(const DevPlan& p, const HostPlan& hp, int level, DevState& s,
                    cudaStream_t st) {
   const int64_t c0 = hp.copy_lvl[level], c1 = hp.copy_lvl[level + 1];
   const int64_t j0 = hp.up1_lvl[level], j1 = hp.up1_lvl[level + 1];
-  if (c1 > c0 && j1 > j0 && !p.k1_bulk) {  // both kinds of work: one launch
+  if (SFMM_K1_MERGE && c1 > c0 && j1 > j0 && !p.k1_bulk) {  // both kinds of work: one launch
     const int ncb = (int)((c1 - c0 + 7) / 8);
     const unsigned g = (unsigned)(ncb + (j1 - j0));
     if (p.cplx)
@@ -799,11 +851,13 @@ void launch_upward(const DevPlan& p, const HostPlan& hp, int level, DevState& s,
   if (c1 > c0) {
     const unsigned g = (unsigned)((c1 - c0 + 7) / 8);
     if (p.cplx)
-      k1_copy<double2><<<g, 256, 0, st>>>(p.copy_boxes + c0, c1 - c0, p.box,
+      k1_copy<double2><<<g, 256, 0, st>>>(p.copy_boxes + c0, c1 - c0, p.box, p.T_off,
+                                          reinterpret_cast<const double2*>(p.T),
                                           reinterpret_cast<double2*>(s.Q),
                                           reinterpret_cast<double2*>(s.QH), p.up_dst);
     else
-      k1_copy<double><<<g, 256, 0, st>>>(p.copy_boxes + c0, c1 - c0, p.box, s.Q, s.QH, p.up_dst);
+      k1_copy<double><<<g, 256, 0, st>>>(p.copy_boxes + c0, c1 - c0, p.box, p.T_off, p.T, s.Q, s.QH,
+                                         p.up_dst);
   }
   const int64_t i0 = hp.up1_lvl[level], i1 = hp.up1_lvl[level + 1];
   if (i1 <= i0) return;
@@ -822,27 +876,31 @@ void launch_upward(const DevPlan& p, const HostPlan& hp, int level, DevState& s,
 
 void launch_downward(const DevPlan& p, const HostPlan& hp, int level, DevState& s,
                      cudaStream_t st) {
-  const int64_t c0 = hp.copy_lvl[level], c1 = hp.copy_lvl[level + 1];
+  const int64_t c0 = hp.copy_dn_lvl[level], c1 = hp.copy_dn_lvl[level + 1];
   const int64_t j0 = hp.down_lvl[level], j1 = hp.down_lvl[level + 1];
-  if (c1 > c0 && j1 > j0) {  // both kinds of work: one launch
+  // (SFMM_K3_MERGE, plan_build.h: off -- the merged downward launch measured
+  // slower on adaptive trees, config 3a 1.42 vs 1.36 ms, 3b 2.47 vs 2.35 ms)
+  if (SFMM_K3_MERGE && c1 > c0 && j1 > j0) {  // both kinds of work: one launch
     const int ncb = (int)((c1 - c0 + 7) / 8);
     const unsigned g = (unsigned)(ncb + (j1 - j0));
     if (p.cplx)
       k_level<double2, false><<<g, kDownCols, p.down_smem, st>>>(
-          p.copy_boxes + c0, c1 - c0, ncb, p.down_items + j0, p.box, p.T_off, p.T, s.U, s.UH, p.up_dst);
+          p.copy_boxes_dn + c0, c1 - c0, ncb, p.down_items + j0, p.box, p.T_off, p.T, s.U, s.UH, p.up_dst);
     else
       k_level<double, false><<<g, kDownCols, p.down_smem, st>>>(
-          p.copy_boxes + c0, c1 - c0, ncb, p.down_items + j0, p.box, p.T_off, p.T, s.U, s.UH, p.up_dst);
+          p.copy_boxes_dn + c0, c1 - c0, ncb, p.down_items + j0, p.box, p.T_off, p.T, s.U, s.UH, p.up_dst);
     return;
   }
   if (c1 > c0) {
     const unsigned g = (unsigned)((c1 - c0 + 7) / 8);
     if (p.cplx)
-      k3_copy<double2><<<g, 256, 0, st>>>(p.copy_boxes + c0, c1 - c0, p.box,
+      k3_copy<double2><<<g, 256, 0, st>>>(p.copy_boxes_dn + c0, c1 - c0, p.box, p.T_off,
+                                          reinterpret_cast<const double2*>(p.T),
                                           reinterpret_cast<double2*>(s.U),
                                           reinterpret_cast<const double2*>(s.UH), p.up_dst);
     else
-      k3_copy<double><<<g, 256, 0, st>>>(p.copy_boxes + c0, c1 - c0, p.box, s.U, s.UH, p.up_dst);
+      k3_copy<double><<<g, 256, 0, st>>>(p.copy_boxes_dn + c0, c1 - c0, p.box, p.T_off, p.T, s.U, s.UH,
+                                         p.up_dst);
   }
   const int64_t i0 = hp.down_lvl[level], i1 = hp.down_lvl[level + 1];
   if (i1 <= i0) return;
@@ -865,7 +923,7 @@ TreePassArgs tree_args(const DevPlan& p, bool up, const DevState& s) {
   a.counter = p.tree_sync + (up ? 0 : 1);
   a.done = p.tree_sync + (up ? 2 : 3);
   a.items = up ? p.up1_items : p.down_items;
-  a.copy_boxes = p.copy_boxes;
+  a.copy_boxes = up ? p.copy_boxes : p.copy_boxes_dn;
   a.box = p.box;
   a.T_off = p.T_off;
   a.T = p.T;

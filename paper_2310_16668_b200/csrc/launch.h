@@ -46,7 +46,8 @@ struct DevPlan {
   bool sc_tab_ok;   // kappa * (point-set diameter) within the table's reduction range
   double* log_tab;  // 3 x 128 doubles (fastmath.cuh fill_log_table)
   LevelItem *up_items, *down_items, *up1_items;  // up1: K1 (single rhs), up: K1m
-  int32_t* copy_boxes;                            // r = 0 boxes (plan_build.h)
+  int32_t* copy_boxes;                            // warp-per-box lists (plan_build.h): upward
+  int32_t* copy_boxes_dn;                         //   and downward
   double* orig_pts;
   double* stage;    // kSYM column-sum staging (stage_size scalars; one vector per pair)
   unsigned* stage_flags;  // stage_size / 32 chain flags (tiles that have added), zeroed per apply

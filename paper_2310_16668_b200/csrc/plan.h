@@ -334,10 +334,11 @@ struct sfmm_gpu_plan {
       n = 3;  // persistent upward (with the gather), translate, persistent downward (+ scatter)
     } else {
       for (int l = 2; l <= hp.depth; ++l) {  // one launch per level and pass when both
-        const bool c = hp.copy_lvl[l + 1] > hp.copy_lvl[l];  // copies and items exist (k_level)
+        const bool c = hp.copy_lvl[l + 1] > hp.copy_lvl[l];  // warp boxes and items exist (k_level)
+        const bool cd = hp.copy_dn_lvl[l + 1] > hp.copy_dn_lvl[l];
         const bool u = hp.up1_lvl[l + 1] > hp.up1_lvl[l], d = hp.down_lvl[l + 1] > hp.down_lvl[l];
-        n += (c && u && !dp.k1_bulk) ? 1 : (c ? 1 : 0) + (u ? 1 : 0);
-        n += (c && d) ? 1 : (c ? 1 : 0) + (d ? 1 : 0);
+        n += (SFMM_K1_MERGE && c && u && !dp.k1_bulk) ? 1 : (c ? 1 : 0) + (u ? 1 : 0);
+        n += (SFMM_K3_MERGE && cd && d) ? 1 : (cd ? 1 : 0) + (d ? 1 : 0);
       }
     }
     if (dp.n_tasks == 0) --n;

@@ -1070,12 +1070,14 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
     hp.up_lvl.assign(d.depth + 2, 0);
     hp.up1_lvl.assign(d.depth + 2, 0);
     hp.copy_lvl.assign(d.depth + 2, 0);
+    hp.copy_dn_lvl.assign(d.depth + 2, 0);
     hp.down_lvl.assign(d.depth + 2, 0);
     hp.down_m_lvl.assign(d.depth + 2, 0);
     for (int l = 0; l <= d.depth; ++l) {
       hp.up_lvl[l] = (int64_t)hp.up_items.size();
       hp.up1_lvl[l] = (int64_t)hp.up1_items.size();
       hp.copy_lvl[l] = (int64_t)hp.copy_boxes.size();
+      hp.copy_dn_lvl[l] = (int64_t)hp.copy_boxes_dn.size();
       hp.down_lvl[l] = (int64_t)hp.down_items.size();
       hp.down_m_lvl[l] = (int64_t)hp.down_m_items.size();
       if (l >= 2) {
@@ -1088,7 +1090,15 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
           for (int32_t j = 0; j < std::max(r, 1); j += kDownColsM) hp.down_m_items.push_back({b, j});
           if (r == 0) {  // uncompressed: copies only (warp per box, k1_copy / k3_copy;
                          // leaves: fused into K0 / K4)
-            if (!d.box_leaf[b]) hp.copy_boxes.push_back(b);
+            if (!d.box_leaf[b]) {
+              hp.copy_boxes.push_back(b);
+              hp.copy_boxes_dn.push_back(b);
+            }
+            continue;
+          }
+          if (r <= kWarpBoxR) {  // short interpolation block: warp per box upward
+            hp.copy_boxes.push_back(b);
+            for (int32_t j = 0; j < r; j += kDownCols) hp.down_items.push_back({b, j});
             continue;
           }
           for (int32_t i = 0; i < k; i += kUpRows1) hp.up1_items.push_back({b, i});
@@ -1100,6 +1110,7 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
     hp.up_lvl[d.depth + 1] = (int64_t)hp.up_items.size();
     hp.up1_lvl[d.depth + 1] = (int64_t)hp.up1_items.size();
     hp.copy_lvl[d.depth + 1] = (int64_t)hp.copy_boxes.size();
+    hp.copy_dn_lvl[d.depth + 1] = (int64_t)hp.copy_boxes_dn.size();
     hp.down_lvl[d.depth + 1] = (int64_t)hp.down_items.size();
     hp.down_m_lvl[d.depth + 1] = (int64_t)hp.down_m_items.size();
     // persistent tree passes (opt-in A/B, plan_build.h kTreePersistPoints)
@@ -1110,9 +1121,9 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
         const int32_t n_pj = (int32_t)((hp.n_owned_points + kPointsPerJob - 1) / kPointsPerJob);
         auto level_jobs = [&](int l, const std::vector<int64_t>& lvl, std::vector<TreeJob>& jobs,
                               int32_t stage) {
-          for (int64_t c = hp.copy_lvl[l]; c < hp.copy_lvl[l + 1]; c += 8)
-            jobs.push_back({kJobCopy, stage, (int32_t)c,
-                            (int32_t)std::min<int64_t>(8, hp.copy_lvl[l + 1] - c)});
+          const std::vector<int64_t>& cl = &lvl == &hp.up1_lvl ? hp.copy_lvl : hp.copy_dn_lvl;
+          for (int64_t c = cl[l]; c < cl[l + 1]; c += 8)
+            jobs.push_back({kJobCopy, stage, (int32_t)c, (int32_t)std::min<int64_t>(8, cl[l + 1] - c)});
           for (int64_t i = lvl[l]; i < lvl[l + 1]; ++i) jobs.push_back({kJobItem, stage, (int32_t)i, 0});
         };
         int32_t stage = 0;

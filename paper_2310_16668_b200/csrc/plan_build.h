@@ -30,6 +30,15 @@ constexpr int kUpRows = 64;                     // K1m rows (skeleton entries) p
 constexpr int kUpRows1 = SFMM_K1_ROWS;          // K1 (single rhs) rows per CTA
 constexpr int kDownCols = 256;                  // K3 columns (redundant slots) per CTA
 constexpr int kChunkM = 16;                     // K2m sources per staged chunk
+constexpr int kWarpBoxR = 32;                   // K1/K3: boxes with r <= this run warp per box
+// a tree level's warp-per-box work and interpolation items in one launch
+// (k_level): upward yes, downward no (measured, kernels_tree.cu)
+#ifndef SFMM_K1_MERGE
+#define SFMM_K1_MERGE 1
+#endif
+#ifndef SFMM_K3_MERGE
+#define SFMM_K3_MERGE 0
+#endif
 constexpr int kMultiRows = 64;                  // K2m rows per task (4 warps x two 8-row DMMA tiles)
 constexpr int kDownColsM = 64;                  // K3m columns per CTA (4 warps x 16)
 
@@ -150,10 +159,15 @@ struct HostPlan {
   // interpolation work lists, concatenated per level; *_lvl has depth+2 entries
   std::vector<LevelItem> up_items, down_items, up1_items;
   std::vector<int64_t> up_lvl, down_lvl, up1_lvl;
-  // owned boxes with k > 0 and no redundant slots (r = 0), per level: the
-  // single-rhs passes only copy qhat / fold uhat for them (k1_copy, k3_copy)
+  // owned boxes with k > 0 and no redundant slots (r = 0; the single-rhs
+  // passes only copy qhat / fold uhat for them) or a short block
+  // (r <= kWarpBoxR), per level: one warp per box (k1_copy, k3_copy)
   std::vector<int32_t> copy_boxes;
   std::vector<int64_t> copy_lvl;
+  // the downward pass's warp-per-box list: uncompressed boxes only (a short
+  // block's K3 keeps the column-per-thread CTA, measured faster there)
+  std::vector<int32_t> copy_boxes_dn;
+  std::vector<int64_t> copy_dn_lvl;
   // persistent tree passes (PlanOptions::tree_persist): job lists in stage
   // order and, per stage, the number of jobs in the stages before it
   bool tree_persist = false;

@@ -204,6 +204,7 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
       dp.up_items = p->upload(hp.up_items);
       dp.up1_items = p->upload(hp.up1_items);
       dp.copy_boxes = p->upload(hp.copy_boxes);
+      dp.copy_boxes_dn = p->upload(hp.copy_boxes_dn);
       dp.down_items = p->upload(hp.down_items);
       if (hp.tree_persist) {
         dp.tree_persist = 1;
