@@ -627,6 +627,7 @@ __global__ void k_build_slots(SlotBuildArgs a) {
   const int lane = threadIdx.x & 31;
   if (w >= a.n_boxes) return;
   const BoxRec br = a.box[w];
+  if (br.slot < 0) return;  // not on this rank (compact slot space of a sharded plan)
   for (int32_t p = lane; p < br.n; p += 32) {
     const int64_t e = br.slot + p;
     const int64_t s = br.slot + a.posmap[e];
@@ -636,7 +637,7 @@ __global__ void k_build_slots(SlotBuildArgs a) {
     a.Y[s] = a.pts[id * a.dim + 1];
     a.Z[s] = a.dim == 3 ? a.pts[id * a.dim + 2] : 0.0;
   }
-  if (br.k > 0) {
+  if (br.k > 0 && a.box[a.parent[w]].slot >= 0) {  // (a ghost box's parent may be absent)
     const int64_t ps = a.box[a.parent[w]].slot;
     const int64_t off = a.parent_offset[w];
     for (int32_t i = lane; i < br.k; i += 32)

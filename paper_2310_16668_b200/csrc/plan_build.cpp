@@ -45,6 +45,7 @@ PlanOptions plan_options_from_env() {
   if (const char* v = std::getenv("SFMM_TREE_PERSIST")) o.tree_persist = std::atoi(v) != 0 ? 1 : 0;
   if (const char* v = std::getenv("SFMM_SPLIT")) o.split = std::atoi(v) != 0;
   if (const char* v = std::getenv("SFMM_SPLIT_PART")) o.split_part = std::atof(v);
+  if (const char* v = std::getenv("SFMM_SHARD_COMPACT")) o.compact = std::atoi(v) != 0;
   return o;
 }
 
@@ -616,6 +617,45 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
     auto folded_away = [&](int32_t b, int32_t c, int mode) {
       return hp.xsym && mode == kIFO && hp.owner[b] != hp.owner[c] && !evaluates(b, c);
     };
+    // Compact slot space (sharded plans): only the boxes this rank touches --
+    // its own (and shared) boxes and the sources its targets read -- keep
+    // slots, renumbered into one contiguous range, so the slot geometry and
+    // state (coordinates, ids, Q / U, QH / UH: ~50 B per slot) scale with the
+    // rank's share instead of N.  Every other box gets slot = skel = -1 and is
+    // never touched.  Slot offsets are only reached through the box records,
+    // the exchange index lists and the leaf maps, all built from here on.
+    hp.global_slot.clear();
+    if (n_ranks > 1 && opt.compact) {
+      std::vector<uint8_t> present(nb, 0);
+      for (int32_t b = 0; b < nb; ++b) {
+        if (!mine(b)) continue;
+        present[b] = 1;
+        if (d.box_level[b] >= 1) sources(b, [&](int32_t c, int) { present[c] = 1; });
+      }
+      std::vector<int32_t> pm;
+      int64_t cs = 0, ck = 0;
+      hp.global_slot.assign(nb, -1);
+      hp.global_skel.assign(nb, -1);
+      for (int32_t b = 0; b < nb; ++b) {
+        BoxRec& br = hp.box[b];
+        hp.global_slot[b] = br.slot;
+        hp.global_skel[b] = br.skel;
+        if (!present[b]) {
+          br.slot = -1;
+          br.skel = -1;
+          continue;
+        }
+        pm.insert(pm.end(), hp.posmap.begin() + br.slot, hp.posmap.begin() + br.slot + br.n);
+        hp.iv_runs.push_back({br.slot, cs, br.n});
+        br.slot = cs;
+        br.skel = ck;
+        cs += br.n;
+        ck += br.k;
+      }
+      hp.posmap.swap(pm);
+      hp.n_slots = cs;
+      hp.n_skel = ck;
+    }
     // this rank's CSR: owned targets only
     hp.ent_range.resize(nb);
     std::vector<uint8_t> boundary(nb, 0);
@@ -777,24 +817,49 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
         for (int32_t i = 0; i < hp.box[c].k; ++i)
           out.push_back(ps + hp.posmap[ps + d.box_parent_offset[c] + i]);
       };
+      auto parent_slots_global = [&](int32_t c, std::vector<int64_t>& out) {
+        const int32_t pb = d.box_parent[c];
+        const int64_t ps = hp.box[pb].slot, gs = hp.global_slot[pb];
+        for (int32_t i = 0; i < hp.box[c].k; ++i)
+          out.push_back(gs + hp.posmap[ps + d.box_parent_offset[c] + i]);
+      };
       hp.send_off.assign(n_ranks + 1, 0);
       hp.recv_off_peer.assign(n_ranks + 1, 0);
-      const int64_t sk_base = S;  // QH entries are addressed as S + skel index
+      const int64_t sk_base = hp.n_slots;  // QH entries are addressed as n_slots + skel index
+      // the same lists in the descriptor's (global) numbering, for the
+      // host-only view (sfmm_gpu_shard_describe): they agree across ranks
+      const bool compact = !hp.global_slot.empty();
+      auto gslot = [&](int32_t c) { return compact ? hp.global_slot[c] : hp.box[c].slot; };
+      auto gskel = [&](int32_t c) { return compact ? hp.global_skel[c] : hp.box[c].skel; };
       for (int p = 0; p < n_ranks; ++p) {
         for (int32_t c = 0; c < nb; ++c) {
           if (p != rank && need[p][c] && hp.owner[c] == rank) {  // I send c to p
             for (int32_t i = 0; i < hp.box[c].n; ++i) hp.pack_idx.push_back(hp.box[c].slot + i);
             for (int32_t i = 0; i < hp.box[c].k; ++i) hp.pack_idx.push_back(sk_base + hp.box[c].skel + i);
+            if (compact) {
+              for (int32_t i = 0; i < hp.box[c].n; ++i) hp.pack_idx_global.push_back(gslot(c) + i);
+              for (int32_t i = 0; i < hp.box[c].k; ++i) hp.pack_idx_global.push_back(S + gskel(c) + i);
+            }
           }
           if (p != rank && need[rank][c] && hp.owner[c] == p) {  // p sends c to me
             for (int32_t i = 0; i < hp.box[c].n; ++i) hp.unpack_idx.push_back(hp.box[c].slot + i);
             for (int32_t i = 0; i < hp.box[c].k; ++i) hp.unpack_idx.push_back(sk_base + hp.box[c].skel + i);
+            if (compact) {
+              for (int32_t i = 0; i < hp.box[c].n; ++i) hp.unpack_idx_global.push_back(gslot(c) + i);
+              for (int32_t i = 0; i < hp.box[c].k; ++i) hp.unpack_idx_global.push_back(S + gskel(c) + i);
+            }
             ++hp.n_ghost_boxes;
           }
         }
         for (int32_t c : shared_kids) {
-          if (p != rank && hp.owner[c] == rank) parent_slots(c, hp.pack_idx);
-          if (p != rank && hp.owner[c] == p) parent_slots(c, hp.unpack_idx);
+          if (p != rank && hp.owner[c] == rank) {
+            parent_slots(c, hp.pack_idx);
+            if (compact) parent_slots_global(c, hp.pack_idx_global);
+          }
+          if (p != rank && hp.owner[c] == p) {
+            parent_slots(c, hp.unpack_idx);
+            if (compact) parent_slots_global(c, hp.unpack_idx_global);
+          }
         }
         hp.send_off[p + 1] = (int64_t)hp.pack_idx.size();
         hp.recv_off_peer[p + 1] = (int64_t)hp.unpack_idx.size();

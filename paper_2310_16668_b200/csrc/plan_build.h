@@ -114,6 +114,16 @@ struct HostPlan {
   // ghost exchange: element indices into [Q | QH] (QH at offset n_slots),
   // per peer ranges send_off[p]..send_off[p+1] / recv_off_peer[p]..
   std::vector<int64_t> pack_idx, unpack_idx, send_off, recv_off_peer;
+  // compact slot space (PlanOptions::compact, sharded plans): the descriptor's
+  // slot / skeleton offset of every box (empty when not compacted), the runs
+  // (global offset, compact offset, length) of index_vec entries to upload,
+  // and the exchange lists in the descriptor's numbering (for describe)
+  std::vector<int64_t> global_slot, global_skel;
+  struct IvRun {
+    int64_t src, dst, len;
+  };
+  std::vector<IvRun> iv_runs;
+  std::vector<int64_t> pack_idx_global, unpack_idx_global;
   int64_t n_ghost_boxes = 0;
   // cross-rank symmetric pairs (PlanOptions::cross_symmetric).  Sender side:
   // group i (one receiving box c of one peer) sums the staged column sums of
@@ -236,6 +246,8 @@ struct PlanOptions {
   // makespan along their entry lists (SFMM_SPLIT=0 turns it off)
   bool split = true;
   double split_part = 0.5;  // part size as a fraction of the per-warp share (split above 1.5x it)
+  // sharded plans: slots only for the boxes the rank touches (SFMM_SHARD_COMPACT=0: all N)
+  bool compact = true;
 };
 PlanOptions plan_options_from_env();
 

@@ -120,7 +120,14 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
         a.box = dp.box;
         a.n_boxes = hp.n_boxes;
         a.posmap = tmp.up(hp.posmap.data(), hp.posmap.size());
-        a.iv = tmp.up(desc->iv, (size_t)hp.n_slots);
+        if (hp.iv_runs.empty()) {
+          a.iv = tmp.up(desc->iv, (size_t)hp.n_slots);
+        } else {  // compact slot space: the present boxes' index_vec runs
+          std::vector<int32_t> iv((size_t)hp.n_slots);
+          for (const HostPlan::IvRun& r : hp.iv_runs)
+            std::copy(desc->iv + r.src, desc->iv + r.src + r.len, iv.begin() + r.dst);
+          a.iv = tmp.up(iv.data(), iv.size());
+        }
         a.pts = tmp.up(desc->pts, (size_t)hp.n_points * hp.dim);
         a.dim = hp.dim;
         a.parent = tmp.up(hp.box_parent.data(), hp.box_parent.size());
@@ -531,8 +538,12 @@ int sfmm_gpu_shard_describe(const sfmm_plan_desc* desc, int n_ranks, int rank, i
   }
   counts[4 * n_ranks + 3] = hp.cut_level;
   if (owner && !hp.owner.empty()) std::copy(hp.owner.begin(), hp.owner.end(), owner);
-  if (pack_idx) std::copy(hp.pack_idx.begin(), hp.pack_idx.end(), pack_idx);
-  if (unpack_idx) std::copy(hp.unpack_idx.begin(), hp.unpack_idx.end(), unpack_idx);
+  // exchange lists in the descriptor's numbering (a compacted rank plan keeps
+  // its own; the element order is the same)
+  const std::vector<int64_t>& pk = hp.global_slot.empty() ? hp.pack_idx : hp.pack_idx_global;
+  const std::vector<int64_t>& uk = hp.global_slot.empty() ? hp.unpack_idx : hp.unpack_idx_global;
+  if (pack_idx) std::copy(pk.begin(), pk.end(), pack_idx);
+  if (unpack_idx) std::copy(uk.begin(), uk.end(), unpack_idx);
   if (owned_points) {
     if (hp.depth < 2) {
       for (int64_t i = 0; i < hp.n_owned_points; ++i) owned_points[i] = (int32_t)i;

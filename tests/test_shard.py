@@ -390,3 +390,35 @@ def test_bench_sharded_line_two_ranks_gloo(tmp_path):
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["gpu_launches"] > 0
     assert line["relerr_vs_single_gpu"] <= 1e-12
     assert line["relerr_vs_direct"] <= 1e-4
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", [("cube", 1, 8), ("sphere", 1, 4), ("gaussian", 1, 4), ("square", 0, 4)])
+def test_compact_slot_space_bit_identical(case, monkeypatch):
+    """Sharded rank plans keep slots only for the boxes the rank touches (its
+    own and shared boxes, the sources its targets read): each rank's slot
+    space shrinks with its share, and the sharded result is bit-identical to
+    the plans that keep all N slots (SFMM_SHARD_COMPACT=0)."""
+    import torch
+    dist, kernel, n_ranks = case
+    n = 120000
+    pts = host.generate_points(dist, n, 3)
+    d = ref_descriptor(kernel, pts, 64, 1e-6)
+    q = host.generate_charges(n, 9)
+    qd = torch.from_numpy(q).cuda()
+    out = {}
+    for comp in ("1", "0"):
+        monkeypatch.setenv("SFMM_SHARD_COMPACT", comp)
+        plans = [shard.ShardedPlan(d, n_ranks, r) for r in range(n_ranks)]
+        ud = torch.zeros_like(qd)
+        shard.apply_virtual(plans, qd, ud)
+        torch.cuda.synchronize()
+        out[comp] = (ud.cpu().numpy(), [p.info().n_slots for p in plans])
+        for p in plans:
+            p.close()
+    assert np.array_equal(out["1"][0], out["0"][0])
+    full = int(d.arrays["iv_off"][-1])
+    assert all(s == full for s in out["0"][1])
+    # each rank keeps its share plus a ghost layer (a large fraction at these
+    # small N; surface / volume at config-5 sizes)
+    assert max(out["1"][1]) < full
