@@ -64,6 +64,10 @@ struct MultiRank {
   sfmm_gpu_plan* plan = nullptr;  // owned sharded rank plan
   double *send = nullptr, *recv = nullptr, *send2 = nullptr, *recv2 = nullptr;
   cudaEvent_t packed = nullptr, packed2 = nullptr, done = nullptr;
+  // the ghost exchange's own stream (receiver side), so the peer copies run
+  // while the rank's interior tasks do (plans split with SFMM_SHARD_OVERLAP=1)
+  cudaStream_t xs = nullptr;
+  cudaEvent_t xdone = nullptr;
   std::vector<int64_t> soff, roff, soff2, roff2;  // per-peer segments (scalars)
 };
 
@@ -82,8 +86,9 @@ void destroy_multi(MultiPlan* m) {
     if (!r.plan) continue;
     cudaSetDevice(r.plan->device);
     cudaStreamSynchronize(r.plan->stream);
-    for (cudaEvent_t e : {r.packed, r.packed2, r.done})
+    for (cudaEvent_t e : {r.packed, r.packed2, r.done, r.xdone})
       if (e) cudaEventDestroy(e);
+    if (r.xs) cudaStreamDestroy(r.xs);
     delete r.plan;
   }
   for (auto& b : m->buffers) {
@@ -103,11 +108,14 @@ namespace {
 // sender's pack.
 void peer_exchange(MultiPlan& m, double* MultiRank::*send, double* MultiRank::*recv,
                    std::vector<int64_t> MultiRank::*soff, std::vector<int64_t> MultiRank::*roff,
-                   cudaEvent_t MultiRank::*packed, size_t sw) {
+                   cudaEvent_t MultiRank::*packed, size_t sw, bool side) {
   const int n = (int)m.rank.size();
   for (int p = 0; p < n; ++p) {
     MultiRank& dst = m.rank[p];
     DeviceGuard g(dst.plan->device);
+    // the ghost exchange of a split plan runs on the receiver's exchange
+    // stream, concurrently with its interior tasks; the rank stream joins it
+    cudaStream_t xst = side ? dst.xs : dst.plan->stream;
     for (int r = 0; r < n; ++r) {
       if (r == p) continue;
       MultiRank& src = m.rank[r];
@@ -115,13 +123,23 @@ void peer_exchange(MultiPlan& m, double* MultiRank::*send, double* MultiRank::*r
       if (cnt == 0) continue;
       if ((dst.*roff)[r + 1] - (dst.*roff)[r] != cnt)
         throw CudaFail{SFMM_EINVAL, "exchange: peer segment sizes disagree"};
-      ck(cudaStreamWaitEvent(dst.plan->stream, src.*packed, 0), "wait pack");
+      ck(cudaStreamWaitEvent(xst, src.*packed, 0), "wait pack");
       ck(cudaMemcpyPeerAsync(dst.*recv + (dst.*roff)[r] * sw, dst.plan->device,
                              src.*send + (src.*soff)[p] * sw, src.plan->device,
-                             sizeof(double) * cnt * sw, dst.plan->stream),
+                             sizeof(double) * cnt * sw, xst),
          "peer copy");
     }
+    if (side) {
+      ck(cudaEventRecord(dst.xdone, xst), "event");
+      ck(cudaStreamWaitEvent(dst.plan->stream, dst.xdone, 0), "join exchange");
+    }
   }
+}
+
+// a plan whose translation tasks are split into interior (launched before the
+// ghost exchange) and boundary ones (SFMM_SHARD_OVERLAP=1)
+bool split_plan(const sfmm_gpu_plan* p) {
+  return p->dp.n_interior > 0 && p->dp.n_interior < p->dp.n_tasks;
 }
 
 }  // namespace
@@ -139,15 +157,17 @@ void multi_enqueue(sfmm_gpu_plan* p, const double* q, double* u, cudaStream_t st
     ck(cudaStreamWaitEvent(rs, m.ev_in, 0), "wait input");
     phase_begin(r.plan, q, r.send, rs, rs, r.packed);
   }
+  bool side = false;
+  for (MultiRank& r : m.rank) side = side || split_plan(r.plan);
   peer_exchange(m, &MultiRank::send, &MultiRank::recv, &MultiRank::soff, &MultiRank::roff,
-                &MultiRank::packed, sw);
+                &MultiRank::packed, sw, side);
   if (m.xsym) {
     for (MultiRank& r : m.rank) {
       DeviceGuard g(r.plan->device);
       phase_mid(r.plan, r.recv, r.send2, r.plan->stream, r.plan->stream, r.packed2);
     }
     peer_exchange(m, &MultiRank::send2, &MultiRank::recv2, &MultiRank::soff2, &MultiRank::roff2,
-                  &MultiRank::packed2, sw);
+                  &MultiRank::packed2, sw, false);
     for (MultiRank& r : m.rank) {
       DeviceGuard g(r.plan->device);
       phase_fin(r.plan, q, r.recv2, u, r.plan->stream, r.plan->stream);
@@ -287,8 +307,9 @@ int create_multi(const sfmm_plan_desc* desc, int n_dev, const int* dev_ids, sfmm
       mr.send2 = dev_alloc(d, mr.soff2.back() * sw, m.buffers);
       mr.recv2 = dev_alloc(d, mr.roff2.back() * sw, m.buffers);
       DeviceGuard gd(d);
-      for (cudaEvent_t* e : {&mr.packed, &mr.packed2, &mr.done})
+      for (cudaEvent_t* e : {&mr.packed, &mr.packed2, &mr.done, &mr.xdone})
         ck(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "cudaEventCreate");
+      ck(cudaStreamCreateWithFlags(&mr.xs, cudaStreamNonBlocking), "cudaStreamCreate");
       p->device_bytes += mr.plan->device_bytes +
                          (int64_t)sizeof(double) * sw *
                              (mr.soff.back() + mr.roff.back() + mr.soff2.back() + mr.roff2.back());
@@ -368,6 +389,10 @@ void nck(ncclResult_t r, const char* what) {
 struct NcclRank {
   ncclComm_t comm = nullptr;
   int n_ranks = 1, rank = 0;
+  // split plans (SFMM_SHARD_OVERLAP=1): the ghost exchange on its own stream,
+  // concurrent with the interior tasks on the apply stream
+  cudaStream_t xs = nullptr;
+  cudaEvent_t packed = nullptr, xdone = nullptr;
   double *send = nullptr, *recv = nullptr, *send2 = nullptr, *recv2 = nullptr;
   std::vector<int64_t> soff, roff, soff2, roff2;
   std::vector<std::pair<int, void*>> buffers;
@@ -376,6 +401,9 @@ struct NcclRank {
 void destroy_nccl(NcclRank* n) {
   if (!n) return;
   if (n->comm && nccl_api().CommDestroy) nccl_api().CommDestroy(n->comm);
+  if (n->xs) cudaStreamDestroy(n->xs);
+  for (cudaEvent_t e : {n->packed, n->xdone})
+    if (e) cudaEventDestroy(e);
   int prev = -1;
   if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
   for (auto& b : n->buffers) {
@@ -409,8 +437,16 @@ void nccl_enqueue(sfmm_gpu_plan* p, const double* q, double* u, cudaStream_t st)
   const size_t sw = scalar_doubles(p);
   const bool full = p->output_mode == SFMM_OUTPUT_FULL;
   if (full) ck(cudaMemsetAsync(u, 0, sizeof(double) * sw * p->hp.n_points, st), "zero u");
-  phase_begin(p, q, c.send, st, st, nullptr);
-  nccl_exchange(c, c.send, c.recv, c.soff, c.roff, sw, st);
+  if (split_plan(p)) {  // exchange on the side stream while the interior tasks run
+    phase_begin(p, q, c.send, st, st, c.packed);
+    ck(cudaStreamWaitEvent(c.xs, c.packed, 0), "wait pack");
+    nccl_exchange(c, c.send, c.recv, c.soff, c.roff, sw, c.xs);
+    ck(cudaEventRecord(c.xdone, c.xs), "event");
+    ck(cudaStreamWaitEvent(st, c.xdone, 0), "join exchange");
+  } else {
+    phase_begin(p, q, c.send, st, st, nullptr);
+    nccl_exchange(c, c.send, c.recv, c.soff, c.roff, sw, st);
+  }
   if (p->hp.xsym) {
     phase_mid(p, c.recv, c.send2, st, st, nullptr);
     nccl_exchange(c, c.send2, c.recv2, c.soff2, c.roff2, sw, st);
@@ -486,6 +522,9 @@ int sfmm_gpu_plan_attach_nccl(sfmm_gpu_plan* p, const void* id, int n_ranks, int
     c->recv = dev_alloc(p->device, c->roff.back() * sw, c->buffers);
     c->send2 = dev_alloc(p->device, c->soff2.back() * sw, c->buffers);
     c->recv2 = dev_alloc(p->device, c->roff2.back() * sw, c->buffers);
+    ck(cudaStreamCreateWithFlags(&c->xs, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaEventCreateWithFlags(&c->packed, cudaEventDisableTiming), "cudaEventCreate");
+    ck(cudaEventCreateWithFlags(&c->xdone, cudaEventDisableTiming), "cudaEventCreate");
     ncclUniqueId uid;
     std::memcpy(&uid, id, sizeof(uid));
     nck(api.CommInitRank(&c->comm, n_ranks, uid, rank), "ncclCommInitRank");
