@@ -798,7 +798,9 @@ def main():
                         f"one process, plan sharded over devices {devices} (peer-copy exchanges "
                         "inside the library)"),
         "resident_plan_gb": info.device_bytes / 1e9,
-        "sym_staging": {"layout": "chained per pair" if info.sym_chain else "per row tile",
+        "sym_staging": {"layout": ("chained per pair" if info.sym_chain else
+                                   f"per row tile, {info.merged_tasks} merged multi-tile tasks"
+                                   if info.merged_tasks else "per row tile"),
                         "gb": info.stage_bytes / 1e9},
         "roofline": roof,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": bytes_col,

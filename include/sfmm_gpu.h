@@ -138,7 +138,8 @@ typedef struct sfmm_gpu_plan_info {
   int64_t stage_bytes;        /* column-sum staging of the symmetric colleague blocks */
   int32_t multi_sym;          /* 1: multi-RHS applies generate each colleague block once
                                  (transposed DMMA product, staged column sums) */
-  int32_t reserved0;
+  int32_t merged_tasks;       /* K2 tasks that run all row tiles of one box (the low-memory
+                                 staging layout tried first when a plan would not fit) */
   int64_t multi_stage_bytes;  /* their column-sum staging (allocated on the first multi-RHS apply) */
 } sfmm_gpu_plan_info;
 

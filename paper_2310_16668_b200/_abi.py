@@ -99,7 +99,7 @@ class PlanInfo(C.Structure):
         ("sym_chain", C.c_int32),
         ("stage_bytes", C.c_int64),
         ("multi_sym", C.c_int32),
-        ("reserved0", C.c_int32),
+        ("merged_tasks", C.c_int32),
         ("multi_stage_bytes", C.c_int64),
     ]
 

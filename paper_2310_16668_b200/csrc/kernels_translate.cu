@@ -112,8 +112,14 @@ struct WarpSmemReal {
   double2 xy[32];
   double2 za[32];  // z, a-weight
   double h[32];
+  // per-tile layout: the rotation's starting column sums (a merged task's
+  // later tiles: the earlier tiles' sums of the pair's staged vector, else 0)
+  double pu[32], ph[32];
   unsigned* fbase;  // chain flags of the current kSYM entry (kept out of registers)
   int tile;
+  // the current tile of the task (merged tasks: one of the box's tiles) and
+  // the merged task's next tile, kept out of registers
+  int row0, nrows, pend_t, pend_r0;
 };
 
 struct WarpSmemCplx {
@@ -123,6 +129,7 @@ struct WarpSmemCplx {
   double2 h[32];
   unsigned* fbase;
   int tile;
+  int row0, nrows, pend_t, pend_r0;
 };
 
 // Chained kSYM column sums: the row tiles of a box add their column sums of a
@@ -141,6 +148,7 @@ __device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ double add_s(double a, double b) { return a + b; }
+
 __device__ __forceinline__ double2 add_s(double2 a, double2 b) {
   return make_double2(a.x + b.x, a.y + b.y);
 }
@@ -148,7 +156,7 @@ template <class S, bool H, bool CHAIN>
 __device__ __forceinline__ void chain_store(S* st_u, S* st_h, S cp, S ch, int col, int n_c,
                                             int k_c, const unsigned* const* fbase, const int* tilep,
                                             int j0, int lane) {
-  if constexpr (!CHAIN) {  // per-tile layout: this tile's own staged vector
+  if constexpr (!CHAIN) {  // this tile's own staged vector (merged tasks: see sym_chunk)
     if (col < n_c) st_u[col] = cp;
     if (H && col < k_c) st_h[col] = ch;
     return;
@@ -219,7 +227,7 @@ __device__ __forceinline__ void inner_real(const WarpSmemReal& sm, uint32_t lt, 
 // the running column sum moves one lane down, so after 32 steps lane l holds
 // the complete sum of column l over the warp's 32R rows.  Fixed order, no
 // butterfly, two column accumulators per lane.
-template <class G, int R, bool H, bool CHAIN>
+template <class G, int R, bool H, bool CHAIN, bool MERGE>
 __device__ __forceinline__ void sym_chunk(const WarpSmemReal& sm, uint32_t lt, int j0, int n_c,
                                           int k_c,
                                           const double (&xi)[R], const double (&yi)[R],
@@ -228,6 +236,13 @@ __device__ __forceinline__ void sym_chunk(const WarpSmemReal& sm, uint32_t lt, i
                                           double (&ah)[R], double* __restrict__ st_u,
                                           double* __restrict__ st_h, int lane) {
   double cp = 0.0, ch = 0.0;
+  // a merged task's later tiles start the rotation from the earlier tiles'
+  // sums of their column (stored by this same thread: the running sum ends
+  // in the lane it started in), so the pair keeps one staged vector
+  if (MERGE) {
+    cp = sm.pu[lane];
+    if (H) ch = sm.ph[lane];
+  }
   const int from = (lane + 1) & 31;
 #pragma unroll 4
   for (int s = 0; s < 32; ++s) {
@@ -264,18 +279,22 @@ __device__ __forceinline__ void sym_chunk(const WarpSmemReal& sm, uint32_t lt, i
                                 lane);
 }
 
-template <class G, int R, bool CHAIN>
+// Rows [row0, row0 + nrows) of task t: the task's tile, or one tile of a
+// merged task (all row tiles of a box in one task, plan_build.cpp), whose
+// kSYM column sums share one staged vector per pair (as the chained layout).
+template <class G, int R, bool CHAIN, bool MERGE>
 __device__ __forceinline__ void task_real(const K2Args& a, const Task& t, WarpSmemReal& sm,
                                           uint32_t lt, int lane) {
+  const int row0 = MERGE ? sm.row0 : t.row0;
   const BoxRec tb = a.box[t.box];
   double xi[R], yi[R], zi[R], au[R], ah[R], qr[R], qhr[R];
   int rowi[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    const int row = t.row0 + r * 32 + lane;
+    const int row = row0 + r * 32 + lane;
     rowi[r] = row;
-    const bool valid = row < t.row0 + t.nrows;
-    const int64_t s = tb.slot + (valid ? row : t.row0);
+    const bool valid = row < row0 + (MERGE ? sm.nrows : t.nrows);
+    const int64_t s = tb.slot + (valid ? row : row0);
     xi[r] = a.X[s];
     yi[r] = a.Y[s];
     zi[r] = G::kDim == 3 ? a.Z[s] : 0.0;
@@ -285,7 +304,9 @@ __device__ __forceinline__ void task_real(const K2Args& a, const Task& t, WarpSm
     ah[r] = 0.0;
   }
   const EntryRange er = a.er[t.box];
-  const bool skel_rows = t.row0 < tb.k;
+  const bool skel_rows = row0 < tb.k;
+  // one staged vector per pair for every row tile: chained or merged layout
+  const bool pair_stage = CHAIN || (MERGE && t.nrows > sm.nrows);
   int64_t stage = t.stage;
   const int e_end = t.e1 < 0 ? er.count : t.e1;
   for (int e = t.e0; e < e_end; ++e) {
@@ -312,16 +333,21 @@ __device__ __forceinline__ void task_real(const K2Args& a, const Task& t, WarpSm
           sm.za[lane] = make_double2(kFar, 0.0);
           sm.h[lane] = 0.0;
         }
+        if (MERGE) {  // a merged task's later tiles continue the pair's sums
+          const bool acc = sm.tile > 0;
+          sm.pu[lane] = acc && j < sb.n ? st_u[j] : 0.0;
+          sm.ph[lane] = acc && j < sb.k ? st_h[j] : 0.0;
+        }
         __syncwarp();
         if (skel_rows && j0 < sb.k)
-          sym_chunk<G, R, true, CHAIN>(sm, lt, j0, sb.n, sb.k, xi, yi, zi, qr, qhr, au, ah, st_u, st_h,
+          sym_chunk<G, R, true, CHAIN, MERGE>(sm, lt, j0, sb.n, sb.k, xi, yi, zi, qr, qhr, au, ah, st_u, st_h,
                                 lane);
         else
-          sym_chunk<G, R, false, CHAIN>(sm, lt, j0, sb.n, sb.k, xi, yi, zi, qr, qhr, au, ah, st_u, st_h,
+          sym_chunk<G, R, false, CHAIN, MERGE>(sm, lt, j0, sb.n, sb.k, xi, yi, zi, qr, qhr, au, ah, st_u, st_h,
                                  lane);
         __syncwarp();
       }
-      stage += (sb.n + (((CHAIN ? tb.k > 0 : skel_rows) && sb.k > 0) ? sb.k : 0) + 31) &
+      stage += (sb.n + (((pair_stage ? tb.k > 0 : skel_rows) && sb.k > 0) ? sb.k : 0) + 31) &
                ~(int64_t)31;
       continue;
     }
@@ -356,7 +382,7 @@ __device__ __forceinline__ void task_real(const K2Args& a, const Task& t, WarpSm
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int row = rowi[r];
-    if (row >= t.row0 + t.nrows) continue;
+    if (row >= (MERGE ? sm.row0 + sm.nrows : t.row0 + t.nrows)) continue;
     const bool skel_row = row < tb.k;
     if (!isfinite(au[r]) || (skel_row && !isfinite(ah[r]))) verify_row(a, t.box, row, G::kDim);
     if constexpr (R == 1) {  // (only 32-row tiles are ever split, plan_build.cpp)
@@ -381,7 +407,7 @@ __device__ __forceinline__ void task_real(const K2Args& a, const Task& t, WarpSm
 #ifndef SFMM_K2_R1_MIN_BLOCKS
 #define SFMM_K2_R1_MIN_BLOCKS 8
 #endif
-template <class G, int MAXR, int MINB, bool CHAIN>
+template <class G, int MAXR, int MINB, bool CHAIN, bool MERGE>
 __global__ void __launch_bounds__(kThreads, MINB) k2_translate_real_t(K2Args a) {
   __shared__ WarpSmemReal smem[kWarps];
   __shared__ __align__(16) double ltab[G::kLogTable ? kLogTabLen : 1];
@@ -392,37 +418,84 @@ __global__ void __launch_bounds__(kThreads, MINB) k2_translate_real_t(K2Args a) 
   const uint32_t lts = log_tab_addr(ltab);
   const int lane = threadIdx.x & 31;
   WarpSmemReal& sm = smem[threadIdx.x >> 5];
-  for (;;) {
-    int t = 0;
-    if (lane == 0) t = atomicAdd(a.counter, 1);
-    t = __shfl_sync(kFull, t, 0);
-    if (t >= a.n_tasks) return;
-    // by reference: the task's fields are read where they are used instead of
-    // being held in registers through the whole task (entry range, row-partial
-    // slot of split tasks)
-    const Task& task = a.tasks[t];
-    if constexpr (MAXR == 1) {
-      task_real<G, 1, CHAIN>(a, task, sm, lts, lane);
-    } else {
-      switch ((task.nrows + 31) >> 5) {
-        case 1: task_real<G, 1, CHAIN>(a, task, sm, lts, lane); break;
+  if constexpr (MERGE) {
+    if (lane == 0) sm.pend_t = -1;
+    for (;;) {
+      // the next tile: a merged task's next one (its box's row tiles in order,
+      // plan_build.cpp), else a new task from the counter; the tile's rows
+      // are handed over in shared memory (kept out of registers)
+      int t = 0;
+      if (lane == 0) {
+        int r0 = 0;
+        if (sm.pend_t >= 0) {
+          t = sm.pend_t;
+          r0 = sm.pend_r0;
+        } else {
+          t = atomicAdd(a.counter, 1);
+        }
+        sm.pend_t = -1;
+        if (t < a.n_tasks) {
+          constexpr int kTile = 32 * MAXR;
+          const int nr = a.tasks[t].nrows;
+          sm.row0 = a.tasks[t].row0 + r0;
+          sm.nrows = min(kTile, nr - r0);
+          sm.tile = r0 / kTile;
+          if (r0 + kTile < nr) {
+            sm.pend_t = t;
+            sm.pend_r0 = r0 + kTile;
+          }
+        }
+      }
+      t = __shfl_sync(kFull, t, 0);  // (also orders lane 0's tile fields for the warp)
+      if (t >= a.n_tasks) return;
+      const Task& task = a.tasks[t];
+      switch ((sm.nrows + 31) >> 5) {
+        case 1: task_real<G, 1, false, true>(a, task, sm, lts, lane); break;
 #if SFMM_K2_MAX_R >= 2
-        case 2: task_real<G, 2, CHAIN>(a, task, sm, lts, lane); break;
+        case 2: task_real<G, 2, false, true>(a, task, sm, lts, lane); break;
 #endif
 #if SFMM_K2_MAX_R >= 3
-        case 3: task_real<G, 3, CHAIN>(a, task, sm, lts, lane); break;
+        case 3: task_real<G, 3, false, true>(a, task, sm, lts, lane); break;
 #endif
-        default: task_real<G, SFMM_K2_MAX_R, CHAIN>(a, task, sm, lts, lane); break;
+        default: task_real<G, MAXR, false, true>(a, task, sm, lts, lane); break;
+      }
+      __syncwarp();
+    }
+  } else {
+    for (;;) {
+      int t = 0;
+      if (lane == 0) t = atomicAdd(a.counter, 1);
+      t = __shfl_sync(kFull, t, 0);
+      if (t >= a.n_tasks) return;
+      // by reference: the task's fields are read where they are used instead of
+      // being held in registers through the whole task (entry range, row-partial
+      // slot of split tasks)
+      const Task& task = a.tasks[t];
+      if constexpr (MAXR == 1) {
+        task_real<G, 1, CHAIN, false>(a, task, sm, lts, lane);
+      } else {
+        switch ((task.nrows + 31) >> 5) {
+          case 1: task_real<G, 1, CHAIN, false>(a, task, sm, lts, lane); break;
+#if SFMM_K2_MAX_R >= 2
+          case 2: task_real<G, 2, CHAIN, false>(a, task, sm, lts, lane); break;
+#endif
+#if SFMM_K2_MAX_R >= 3
+          case 3: task_real<G, 3, CHAIN, false>(a, task, sm, lts, lane); break;
+#endif
+          default: task_real<G, SFMM_K2_MAX_R, CHAIN, false>(a, task, sm, lts, lane); break;
+        }
       }
     }
   }
 }
 template <class G>
-constexpr auto k2_real_kernel(bool r1, bool chain) {
-  return chain ? (r1 ? k2_translate_real_t<G, 1, SFMM_K2_R1_MIN_BLOCKS, true>
-                     : k2_translate_real_t<G, SFMM_K2_MAX_R, SFMM_K2_MIN_BLOCKS, true>)
-               : (r1 ? k2_translate_real_t<G, 1, SFMM_K2_R1_MIN_BLOCKS, false>
-                     : k2_translate_real_t<G, SFMM_K2_MAX_R, SFMM_K2_MIN_BLOCKS, false>);
+constexpr auto k2_real_kernel(bool r1, bool chain, bool merged) {
+  // merged plans (plan_build.cpp) have tasks of more than one tile: never r1 or chained
+  if (merged) return k2_translate_real_t<G, SFMM_K2_MAX_R, SFMM_K2_MIN_BLOCKS, false, true>;
+  return chain ? (r1 ? k2_translate_real_t<G, 1, SFMM_K2_R1_MIN_BLOCKS, true, false>
+                     : k2_translate_real_t<G, SFMM_K2_MAX_R, SFMM_K2_MIN_BLOCKS, true, false>)
+               : (r1 ? k2_translate_real_t<G, 1, SFMM_K2_R1_MIN_BLOCKS, false, false>
+                     : k2_translate_real_t<G, SFMM_K2_MAX_R, SFMM_K2_MIN_BLOCKS, false, false>);
 }
 
 // ---------------------------------------------------------------------------
@@ -493,6 +566,11 @@ __device__ __forceinline__ void sym_chunk_cplx(const WarpSmemCplx& sm, const dou
                                                double2 (&ah)[R], double2* __restrict__ st_u,
                                                double2* __restrict__ st_h, int lane) {
   double2 cp = make_double2(0.0, 0.0), ch = make_double2(0.0, 0.0);
+  if (!CHAIN && sm.tile > 0) {  // merged task: as sym_chunk
+    const int col = j0 + lane;
+    if (col < n_c) cp = st_u[col];
+    if (H && col < k_c) ch = st_h[col];
+  }
   const int from = (lane + 1) & 31;
   const int cnt = n_c - j0;  // valid columns of this chunk (may exceed 32)
 #pragma unroll kSymCplxUnroll
@@ -545,6 +623,7 @@ __device__ __forceinline__ void sym_chunk_cplx(const WarpSmemCplx& sm, const dou
 template <int R, bool TAB, bool CHAIN>
 __device__ __forceinline__ void task_cplx(const K2Args& a, const Task& t, WarpSmemCplx& sm,
                                           const double2* tab, int lane) {
+  const int row0 = sm.row0;
   const double2* Q = reinterpret_cast<const double2*>(a.Q);
   const double2* QH = reinterpret_cast<const double2*>(a.QH);
   const BoxRec tb = a.box[t.box];
@@ -553,10 +632,10 @@ __device__ __forceinline__ void task_cplx(const K2Args& a, const Task& t, WarpSm
   int rowi[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    const int row = t.row0 + r * 32 + lane;
+    const int row = row0 + r * 32 + lane;
     rowi[r] = row;
-    const bool valid = row < t.row0 + t.nrows;
-    const int64_t s = tb.slot + (valid ? row : t.row0);
+    const bool valid = row < row0 + sm.nrows;
+    const int64_t s = tb.slot + (valid ? row : row0);
     xi[r] = a.X[s];
     yi[r] = a.Y[s];
     zi[r] = a.Z[s];
@@ -566,7 +645,9 @@ __device__ __forceinline__ void task_cplx(const K2Args& a, const Task& t, WarpSm
     qhr[r] = (valid && row < tb.k) ? QH[tb.skel + row] : make_double2(0.0, 0.0);
   }
   const EntryRange er = a.er[t.box];
-  const bool skel_rows = t.row0 < tb.k;
+  const bool skel_rows = row0 < tb.k;
+  // one staged vector per pair for every row tile: chained or merged layout
+  const bool pair_stage = CHAIN || t.nrows > sm.nrows;
   double2* St = reinterpret_cast<double2*>(a.St);
   int64_t stage = t.stage;
   for (int e = 0; e < er.count; ++e) {
@@ -604,7 +685,7 @@ __device__ __forceinline__ void task_cplx(const K2Args& a, const Task& t, WarpSm
                                         ah, st_u, st_h, lane);
         __syncwarp();
       }
-      stage += (sb.n + (((CHAIN ? tb.k > 0 : skel_rows) && sb.k > 0) ? sb.k : 0) + 31) &
+      stage += (sb.n + (((pair_stage ? tb.k > 0 : skel_rows) && sb.k > 0) ? sb.k : 0) + 31) &
                ~(int64_t)31;
       continue;
     }
@@ -642,7 +723,7 @@ __device__ __forceinline__ void task_cplx(const K2Args& a, const Task& t, WarpSm
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int row = rowi[r];
-    if (row >= t.row0 + t.nrows) continue;
+    if (row >= sm.row0 + sm.nrows) continue;
     const bool skel_row = row < tb.k;
     if (!isfinite(au[r].x) || !isfinite(au[r].y) ||
         (skel_row && (!isfinite(ah[r].x) || !isfinite(ah[r].y))))
@@ -664,13 +745,35 @@ __global__ void __launch_bounds__(kThreads, SFMM_K2C_MIN_BLOCKS) k2_translate_cp
   __syncthreads();
   const int lane = threadIdx.x & 31;
   WarpSmemCplx& sm = smem[threadIdx.x >> 5];
+  if (lane == 0) sm.pend_t = -1;
   for (;;) {
+    // the next tile: a merged task's next one, else a new task (as the real K2)
     int t = 0;
-    if (lane == 0) t = atomicAdd(a.counter, 1);
+    if (lane == 0) {
+      int r0 = 0;
+      if (sm.pend_t >= 0) {
+        t = sm.pend_t;
+        r0 = sm.pend_r0;
+      } else {
+        t = atomicAdd(a.counter, 1);
+      }
+      sm.pend_t = -1;
+      if (t < a.n_tasks) {
+        constexpr int kTile = 32 * SFMM_K2C_MAX_R;
+        const int nr = a.tasks[t].nrows;
+        sm.row0 = a.tasks[t].row0 + r0;
+        sm.nrows = min(kTile, nr - r0);
+        if (!CHAIN) sm.tile = r0 / kTile;
+        if (r0 + kTile < nr) {
+          sm.pend_t = t;
+          sm.pend_r0 = r0 + kTile;
+        }
+      }
+    }
     t = __shfl_sync(kFull, t, 0);
     if (t >= a.n_tasks) return;
     const Task task = a.tasks[t];
-    switch ((task.nrows + 31) >> 5) {
+    switch ((sm.nrows + 31) >> 5) {
       case 1: task_cplx<1, TAB, CHAIN>(a, task, sm, tab, lane); break;
 #if SFMM_K2C_MAX_R >= 3
       case 2: task_cplx<2, TAB, CHAIN>(a, task, sm, tab, lane); break;
@@ -680,6 +783,7 @@ __global__ void __launch_bounds__(kThreads, SFMM_K2C_MIN_BLOCKS) k2_translate_cp
 #endif
       default: task_cplx<SFMM_K2C_MAX_R, TAB, CHAIN>(a, task, sm, tab, lane); break;
     }
+    __syncwarp();
   }
 }
 
@@ -763,10 +867,10 @@ int configure_translate(DevPlan& p, int device) {
                                                       kThreads, 0);
   else if (p.kernel == SFMM_LAPLACE3D)
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per_sm, k2_real_kernel<GenLaplace3d>(p.k2_r1, p.sym_chain), kThreads, 0);
+        &per_sm, k2_real_kernel<GenLaplace3d>(p.k2_r1, p.sym_chain, p.k2_merged), kThreads, 0);
   else
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per_sm, k2_real_kernel<GenLaplace2d>(p.k2_r1, p.sym_chain), kThreads, 0);
+        &per_sm, k2_real_kernel<GenLaplace2d>(p.k2_r1, p.sym_chain, p.k2_merged), kThreads, 0);
   if (e != cudaSuccess) return -1;
   if (per_sm < 1) per_sm = 1;
   p.k2_grid = sms * per_sm;
@@ -822,9 +926,9 @@ void launch_translate(const DevPlan& p, DevState& s, cudaStream_t st, TranslateP
                                            : k2_translate_cplx<false, false>);
       kc<<<grid, kThreads, 0, st>>>(a);
     } else if (p.kernel == SFMM_LAPLACE3D) {
-      k2_real_kernel<GenLaplace3d>(p.k2_r1, p.sym_chain)<<<grid, kThreads, 0, st>>>(a);
+      k2_real_kernel<GenLaplace3d>(p.k2_r1, p.sym_chain, p.k2_merged)<<<grid, kThreads, 0, st>>>(a);
     } else {
-      k2_real_kernel<GenLaplace2d>(p.k2_r1, p.sym_chain)<<<grid, kThreads, 0, st>>>(a);
+      k2_real_kernel<GenLaplace2d>(p.k2_r1, p.sym_chain, p.k2_merged)<<<grid, kThreads, 0, st>>>(a);
     }
   }
   if (part != kInteriorTasks && reduce) launch_stage_reduce(p, s, st);

@@ -92,6 +92,7 @@ struct DevPlan {
   int* err_flag;    // sticky duplicate-point flag
   int k2_grid;      // persistent K2 CTAs
   int k2_r1 = 0;    // every K2 task has <= 32 rows: the 64-register R = 1 kernel
+  int k2_merged = 0;  // some K2 tasks are a box's merged row tiles (plan_build.cpp)
   size_t up_smem, down_smem;
   int k1_bulk = 0;          // real K1 stages T through cp.async.bulk (k1_upward_real_bulk)
   size_t up_bulk_smem = 0;

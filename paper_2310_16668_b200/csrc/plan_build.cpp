@@ -46,6 +46,8 @@ PlanOptions plan_options_from_env() {
   if (const char* v = std::getenv("SFMM_SPLIT")) o.split = std::atoi(v) != 0;
   if (const char* v = std::getenv("SFMM_SPLIT_PART")) o.split_part = std::atof(v);
   if (const char* v = std::getenv("SFMM_SHARD_COMPACT")) o.compact = std::atoi(v) != 0;
+  if (const char* v = std::getenv("SFMM_MERGE_TILES")) o.merge_tiles = std::atoi(v) != 0;
+  if (const char* v = std::getenv("SFMM_MERGE_SHARE")) o.merge_share = std::atof(v);
   return o;
 }
 
@@ -274,7 +276,10 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
     ptime("up_dst");
     // ---- ownership: whole level-1 subtrees per rank ----------
     PlanOptions opt = plan_options_from_env();
-    if (sym_chain >= 0) opt.sym_chain = sym_chain != 0;
+    if (sym_chain >= 0) {  // 0 per tile, 1 chained, 2 per tile with merged tasks
+      opt.sym_chain = sym_chain == 1;
+      opt.merge_tiles = sym_chain == 2;
+    }
     std::vector<uint8_t> unc(nb, 0);
     for (int32_t b = 0; b < nb; ++b)
       unc[b] = opt.skip_cancel && d.box_level[b] >= 2 && hp.box[b].n > 0 &&
@@ -926,7 +931,8 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
       // zero-filled [u: n_b | h: k_b] staging vector (rows outside the tile are
       // never written) that K2b adds to the box in the fixed part order.
       double split_share = 0.0;
-      if (n_ranks == 1 && !hp.cplx && !hp.sym_chain && opt.split && tile <= 32) {
+      if (n_ranks == 1 && !hp.cplx && !hp.sym_chain && opt.split && !opt.merge_tiles &&
+          tile <= 32) {
         double total = 0.0;
         for (int32_t b = 0; b < nb; ++b) {
           if (hp.ent_range[b].count == 0) continue;
@@ -934,6 +940,21 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
             total += 32.0 * ((std::min(tile, hp.box[b].n - r0) + 31) / 32) * (src_of[b] + 8.0);
         }
         split_share = total / (148.0 * 32.0);  // resident warps of the 32-row (R = 1) K2
+      }
+      // Merged tasks: a box of several row tiles whose whole cost stays well
+      // below the per-warp share is ONE task; the kernel runs its tiles in
+      // order and every tile continues the kSYM column sums of one staged
+      // vector per pair (the chained layout's memory, without the chain's
+      // cross-warp waits).
+      double merge_cap = 0.0;
+      if (opt.merge_tiles && !hp.sym_chain && split_share == 0.0) {
+        double total = 0.0;
+        for (int32_t b = 0; b < nb; ++b) {
+          if (hp.ent_range[b].count == 0) continue;
+          for (int32_t r0 = 0; r0 < hp.box[b].n; r0 += tile)
+            total += 32.0 * ((std::min(tile, hp.box[b].n - r0) + 31) / 32) * (src_of[b] + 8.0);
+        }
+        merge_cap = opt.merge_share * total / (148.0 * 16.0);
       }
       // outgoing cross-rank pairs in (b, entry) order, the staged tiles of each
       std::vector<std::pair<int32_t, int32_t>> xpairs;
@@ -975,6 +996,18 @@ int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int
           }
         };
         const int64_t b_stage = cursor;
+        if (merge_cap > 0.0 && hp.box[b].n > tile) {
+          double cost = 0.0;
+          for (int32_t r0 = 0; r0 < hp.box[b].n; r0 += tile)
+            cost += 32.0 * ((std::min(tile, hp.box[b].n - r0) + 31) / 32) * (src + 8.0);
+          if (cost <= merge_cap) {
+            stage_entries(hp.box[b].k > 0);
+            auto& tv = (boundary[b] || !opt.overlap) ? tv_bnd : tv_int;
+            tv.push_back({cost, Task{b, 0, hp.box[b].n, -1, b_stage}});
+            ++hp.n_merged_tasks;
+            continue;
+          }
+        }
         if (hp.sym_chain) stage_entries(hp.box[b].k > 0);
         int32_t tile_index = 0;
         for (int32_t r0 = 0; r0 < hp.box[b].n; r0 += tile, ++tile_index) {

@@ -104,6 +104,7 @@ struct HostPlan {
   std::vector<int64_t> recv_u, recv_h;
   int64_t n_skipped_pairs = 0;                // cancelling pairs not evaluated
   int64_t n_split_parts = 0;                  // later parts of source-range split tasks
+  int64_t n_merged_tasks = 0;                 // boxes whose row tiles run as one task (K2)
   int64_t n_interior_tasks = 0;               // tasks[0, n_interior) read no ghost box
   // sharding: owner rank of every box (whole subtrees at the cut
   // level; kShared: internal boxes above the cut, evaluated on every rank)
@@ -197,7 +198,9 @@ struct HostPlan {
 // level-1 subtrees per rank, as chosen before the skeletons existed by a
 // distributed precompute (subtree_owners) -- instead of the cost-based choice.
 int build_host_plan(const sfmm_plan_desc& d, HostPlan& hp, std::string& err, int n_ranks = 1,
-                    int rank = 0, int sym_chain = -1 /* -1: SFMM_SYM_CHAIN (default 0) */,
+                    int rank = 0, int sym_chain = -1 /* -1: SFMM_SYM_CHAIN / SFMM_MERGE_TILES
+                                                       (default per tile); 0 per tile;
+                                                       1 chained; 2 merged tasks */,
                     const int32_t* l1_owner = nullptr);
 
 // Tree-only ownership for a distributed precompute (no skeletons yet): the
@@ -232,6 +235,14 @@ struct PlanOptions {
   // each other (K2 +19 % at 1e7), so it is used only when the plan would not
   // fit otherwise (sfmm_gpu.cu) or on request (SFMM_SYM_CHAIN=1).
   int sym_chain = 0;
+  // per-tile layout: a box's row tiles as one merged task (its tiles in
+  // order, one staged column-sum vector per pair: the chained layout's
+  // memory without its waits) when the box costs at most merge_share of the
+  // per-warp share of K2.  The low-memory layout tried first when the plan
+  // would not fit (sfmm_gpu.cu); measured 3.8 % slower K2 than per-tile
+  // staging at 1e7 (coarser tasks), so not the default (SFMM_MERGE_TILES=1).
+  bool merge_tiles = false;
+  double merge_share = 0.5;
   // multi-RHS apply: colleague blocks generated once for both directions
   // (the transposed DMMA product of K2m, column sums chained over b's row
   // tiles).  Opt-in (SFMM_MULTI_SYM=1): measured slower on config 4 (DESIGN.md

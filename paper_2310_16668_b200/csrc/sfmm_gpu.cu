@@ -51,21 +51,27 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
     p->device = device;
     DeviceGuard device_guard(device);
     // Per-tile kSYM staging is the fast layout; when the plan would not fit
-    // the free device memory with it, chain the row tiles' column sums into
-    // one vector per pair instead (PlanOptions::sym_chain, ~2/3 less staging)
-    if (!p->hp.sym_chain && p->hp.stage_size > 0 && !std::getenv("SFMM_SYM_CHAIN")) {
+    // the free device memory with it, merge each box's row tiles into one task
+    // with one staged vector per pair (PlanOptions::merge_tiles), and if that
+    // still does not fit, chain the row tiles' column sums (sym_chain)
+    if (!p->hp.sym_chain && p->hp.n_merged_tasks == 0 && p->hp.stage_size > 0 &&
+        !std::getenv("SFMM_SYM_CHAIN") && !std::getenv("SFMM_MERGE_TILES")) {
       size_t free_b = 0, total_b = 0;
       if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
-        const HostPlan& h = p->hp;
-        const double sw = h.cplx ? 2.0 : 1.0;
-        double need = 8.0 * sw * ((double)h.stage_size + 2.0 * h.n_slots + 2.0 * h.n_skel) +
-                      28.0 * h.n_slots + 16.0 * h.n_owned_points + 8.0 * h.n_skel +
-                      24.0 * (double)h.tasks.size() + 4.0 * (double)h.entries.size();
-        if (!(T_dev && !T_compact && n_ranks == 1)) need += 8.0 * sw * (double)h.T_off.back();
-        if (need > 0.92 * (double)free_b) {
-          HostPlan chained;
-          if (build_host_plan(*desc, chained, err, n_ranks, rank, 1, l1_owner) == SFMM_OK)
-            p->hp = std::move(chained);
+        auto need_of = [&](const HostPlan& h) {
+          const double sw = h.cplx ? 2.0 : 1.0;
+          double need = 8.0 * sw * ((double)h.stage_size + 2.0 * h.n_slots + 2.0 * h.n_skel) +
+                        28.0 * h.n_slots + 16.0 * h.n_owned_points + 8.0 * h.n_skel +
+                        24.0 * (double)h.tasks.size() + 4.0 * (double)h.entries.size();
+          if (!(T_dev && !T_compact && n_ranks == 1)) need += 8.0 * sw * (double)h.T_off.back();
+          return need;
+        };
+        const double avail = 0.92 * (double)free_b;
+        for (int layout : {2, 1}) {  // merged tasks, then chained
+          if (need_of(p->hp) <= avail) break;
+          HostPlan lighter;
+          if (build_host_plan(*desc, lighter, err, n_ranks, rank, layout, l1_owner) == SFMM_OK)
+            p->hp = std::move(lighter);
         }
       }
     }
@@ -283,6 +289,9 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
         int32_t max_rows = 0;
         for (const Task& t : hp.tasks) max_rows = std::max(max_rows, t.nrows);
         dp.k2_r1 = !hp.cplx && max_rows <= 32;
+        dp.k2_merged = hp.n_merged_tasks > 0 ? 1 : 0;
+        if (dp.k2_merged && (dp.k2_r1 || hp.sym_chain))
+          throw CudaFail{SFMM_EINVAL, "merged K2 tasks with a 32-row or chained plan"};
       }
       if (configure_translate(dp, device) != 0)
         throw CudaFail{SFMM_ECUDA, "occupancy query failed"};
@@ -792,6 +801,7 @@ int sfmm_gpu_plan_info_get(const sfmm_gpu_plan* p, sfmm_gpu_plan_info* info) {
   info->stage_bytes = (int64_t)(hp.stage_size * (hp.cplx ? 16 : 8));
   info->multi_sym = p->dp.multi_sym;
   info->multi_stage_bytes = p->dp.stage_m_points * kNRHS * (hp.cplx ? 16 : 8);
+  info->merged_tasks = (int32_t)hp.n_merged_tasks;
   if (p->multi) {
     multi_info(p, info);  // the orchestrating plan has no level lists of its own
   } else {

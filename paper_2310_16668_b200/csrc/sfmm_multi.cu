@@ -213,7 +213,9 @@ void multi_info(const sfmm_gpu_plan* p, sfmm_gpu_plan_info* info) {
   info->k2_grid = p->multi->rank[0].plan->dp.k2_grid;
   info->sym_chain = 0;
   info->stage_bytes = 0;
+  info->merged_tasks = 0;
   for (const MultiRank& r : p->multi->rank) {
+    info->merged_tasks += (int32_t)r.plan->hp.n_merged_tasks;
     info->sym_chain |= r.plan->hp.sym_chain ? 1 : 0;
     info->stage_bytes += (int64_t)(r.plan->hp.stage_size * (r.plan->hp.cplx ? 16 : 8));
   }

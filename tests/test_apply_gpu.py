@@ -460,3 +460,30 @@ def test_k1_bulk_copy_path_matches_register_path(dist, tol, leaf, monkeypatch):
     u_ref, _ = rp.apply(q)
     rp.close()
     assert rel_l2(u_bulk, u_ref) <= PARITY
+
+
+@pytest.mark.parametrize("kernel,dist,n,leaf", [(1, "cube", 200000, 128), (1, "sphere", 100000, 64),
+                                                (3, "cube", 60000, 64)])
+def test_merged_tile_tasks(kernel, dist, n, leaf, monkeypatch):
+    """The low-memory staging layout (a box's row tiles as ONE K2 task, its
+    tiles in order, one staged column-sum vector per colleague pair): fewer
+    tasks and less staging than the per-tile layout, the same result to
+    rounding, parity-green vs the reference, bit-identical repeats."""
+    pts = host.generate_points(dist, n, 6)
+    kappa = 10.0 if kernel == 3 else 1.0
+    d = ref_descriptor(kernel, pts, leaf, 1e-6, kappa)
+    q = (host.generate_charges_complex if kernel == 3 else host.generate_charges)(n, 77)
+    monkeypatch.setenv("SFMM_MERGE_TILES", "1")
+    monkeypatch.setenv("SFMM_MERGE_SHARE", "1e9")  # small trees: merge every multi-tile box
+    merged = api.GpuPlan(d)
+    mi = merged.info()
+    u1 = api.fmm_apply(merged, q)
+    assert np.array_equal(u1, api.fmm_apply(merged, q))
+    monkeypatch.setenv("SFMM_MERGE_TILES", "0")
+    plain = api.GpuPlan(d)
+    pi = plain.info()
+    assert pi.merged_tasks == 0 and mi.merged_tasks > 0
+    assert mi.n_tasks < pi.n_tasks and mi.stage_bytes < pi.stage_bytes
+    assert rel_l2(u1, api.fmm_apply(plain, q)) <= 1e-13
+    u_ref, _ = po.oracle_apply(d, q)
+    assert rel_l2(u1, u_ref) <= PARITY
