@@ -354,6 +354,40 @@ __global__ void __launch_bounds__(256) k4_scatter(const int32_t* __restrict__ sl
     k4_point<S>(t, slot, orig, hat, up_dst, U, UH, u);
 }
 
+// K4 in two coalesced-write passes (single-rank plans: every point owned):
+// k4_fold writes each owned point's potential in slot order (same arithmetic
+// as k4_point), k4_gather reads it back in the ORIGINAL order through the
+// inverse map, so the random side is a read (the fold's output still sits in
+// L2) instead of a partial-sector write.
+template <class S>
+__global__ void __launch_bounds__(256) k4_fold(const int32_t* __restrict__ slot,
+                                               const int32_t* __restrict__ hat,
+                                               const int32_t* __restrict__ up_dst, int64_t n,
+                                               const S* __restrict__ U, const S* __restrict__ UH,
+                                               S* __restrict__ V) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    S v = __ldcg(U + __ldg(slot + t));
+    const int32_t h = __ldg(hat + t);
+    if (h >= 0) v = add_s(v, add_s(__ldcg(UH + h), __ldcg(U + __ldg(up_dst + h))));
+    V[t] = v;
+  }
+}
+
+template <class S>
+__global__ void __launch_bounds__(256) k4_gather(const int32_t* __restrict__ pos, int64_t n,
+                                                 const S* __restrict__ V, S* __restrict__ u) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    u[i] = __ldcg(V + __ldg(pos + i));
+}
+
+__global__ void k_invert_orig(const int32_t* __restrict__ orig, int64_t n, int32_t* __restrict__ pos) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x)
+    pos[orig[t]] = (int32_t)t;
+}
+
 __device__ __forceinline__ double shfl_s(double v, int src) { return __shfl_sync(kFull, v, src); }
 __device__ __forceinline__ double2 shfl_s(double2 v, int src) {
   return make_double2(__shfl_sync(kFull, v.x, src), __shfl_sync(kFull, v.y, src));
@@ -822,8 +856,28 @@ void launch_gather(const DevPlan& p, const double* q, DevState& s, cudaStream_t 
                                          p.n_owned_points, q, s.Q, s.QH);
 }
 
+void launch_invert_orig(const DevPlan& p, int32_t* pos, cudaStream_t st) {
+  k_invert_orig<<<grid_for(p.n_owned_points, 256), 256, 0, st>>>(p.leaf_orig, p.n_owned_points, pos);
+}
+
 void launch_scatter(const DevPlan& p, const DevState& s, double* u, cudaStream_t st) {
   const int g = grid_for(p.n_owned_points, 256);
+  if (p.leaf_pos) {  // two passes, the fold staged in Q (free after the upward pass)
+    if (p.cplx) {
+      k4_fold<double2><<<g, 256, 0, st>>>(p.leaf_slot, p.leaf_hat, p.up_dst, p.n_owned_points,
+                                          reinterpret_cast<const double2*>(s.U),
+                                          reinterpret_cast<const double2*>(s.UH),
+                                          reinterpret_cast<double2*>(s.Q));
+      k4_gather<double2><<<g, 256, 0, st>>>(p.leaf_pos, p.n_owned_points,
+                                            reinterpret_cast<const double2*>(s.Q),
+                                            reinterpret_cast<double2*>(u));
+    } else {
+      k4_fold<double><<<g, 256, 0, st>>>(p.leaf_slot, p.leaf_hat, p.up_dst, p.n_owned_points, s.U,
+                                         s.UH, s.Q);
+      k4_gather<double><<<g, 256, 0, st>>>(p.leaf_pos, p.n_owned_points, s.Q, u);
+    }
+    return;
+  }
   if (p.cplx)
     k4_scatter<double2><<<g, 256, 0, st>>>(p.leaf_slot, p.leaf_orig, p.leaf_hat, p.up_dst,
                                            p.n_owned_points, reinterpret_cast<const double2*>(s.U),

@@ -36,6 +36,9 @@ struct DevPlan {
   int32_t* up_dst;     // skeleton entry -> slot of the same point in the parent
   int32_t* leaf_slot;  // owned point (slot order) -> slot
   int32_t* leaf_orig;  // owned point -> original index
+  // single-rank plans with the two-pass K4 (k4_fold + k4_gather): original
+  // index -> owned point (the inverse of leaf_orig), else null
+  int32_t* leaf_pos = nullptr;
   // owned point of an uncompressed leaf (k = n, level >= 2) -> its skeleton
   // entry, else -1: K0 / K4 then also do that leaf's qhat copy / uhat fold
   // (the leaf-level k1_copy / k3_copy fused into the gather / scatter)
@@ -168,6 +171,7 @@ struct SlotBuildArgs {
   const uint8_t* leaf_copy;     // owned leaf is uncompressed (its copies fused into K0/K4)
 };
 void launch_build_slots(const SlotBuildArgs& a, cudaStream_t st);
+void launch_invert_orig(const DevPlan& p, int32_t* pos, cudaStream_t st);
 
 // Persistent-grid size and dynamic shared memory setup (called at plan creation).
 int configure_translate(DevPlan& p, int device);

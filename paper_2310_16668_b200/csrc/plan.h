@@ -343,6 +343,7 @@ struct sfmm_gpu_plan {
     }
     if (dp.n_tasks == 0) --n;
     if (dp.n_recv > 0) ++n;  // k2b_reduce
+    if (dp.leaf_pos && !dp.tree_persist) ++n;  // K4 as k4_fold + k4_gather
     // sharded plans: ghost pack / unpack, column-sum pack
     n += (dp.n_pack > 0 ? 1 : 0) + (dp.n_unpack > 0 ? 1 : 0) + (dp.n_xpairs > 0 ? 1 : 0);
     if (dp.n_interior > 0 && dp.n_interior < dp.n_tasks) ++n;  // SFMM_SHARD_OVERLAP split

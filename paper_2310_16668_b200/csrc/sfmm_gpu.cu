@@ -154,6 +154,19 @@ int create_plan(const sfmm_plan_desc* desc, int device, int n_ranks, int rank,
         a.leaf_hat = dp.leaf_hat;
         launch_build_slots(a, p->stream);
         ck(cudaGetLastError(), "build slots");
+        // single-rank plans whose potentials outgrow L2's reach: K4 as fold +
+        // original-order gather (kernels_tree.cu k4_fold / k4_gather).  A/B
+        // (profiles/r02/k4_gather_ab.txt): 0.252 -> 0.148 ms at 1e7, but
+        // 0.016 -> 0.026 ms at 1e6, where the scatter's lines stay in L2.
+        // SFMM_K4_GATHER=1 / 0 forces it on / off.
+        const char* kg = std::getenv("SFMM_K4_GATHER");
+        const bool big = (double)hp.n_points * 8.0 * sw >= 24e6;
+        if (hp.n_owned_points == hp.n_points && hp.n_points > 0 &&
+            (kg ? kg[0] == '1' : big)) {
+          dp.leaf_pos = p->alloc<int32_t>(hp.n_owned_points);
+          launch_invert_orig(dp, dp.leaf_pos, p->stream);
+          ck(cudaGetLastError(), "invert leaf map");
+        }
         ck(cudaStreamSynchronize(p->stream), "build slots");
       }
       dp.T_off = p->upload(hp.T_off);

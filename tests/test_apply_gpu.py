@@ -487,3 +487,24 @@ def test_merged_tile_tasks(kernel, dist, n, leaf, monkeypatch):
     assert rel_l2(u1, api.fmm_apply(plain, q)) <= 1e-13
     u_ref, _ = po.oracle_apply(d, q)
     assert rel_l2(u1, u_ref) <= PARITY
+
+
+@pytest.mark.parametrize("kernel,dist,n,leaf", [(1, "cube", 50000, 64), (0, "annulus", 30000, 40),
+                                                (3, "sphere", 20000, 50)])
+def test_two_pass_scatter_bit_identical(kernel, dist, n, leaf, monkeypatch):
+    """K4 as k4_fold (slot order) + k4_gather (original order, inverse map):
+    the same arithmetic as the one-pass scatter, so the same bits; one launch
+    more per apply."""
+    pts = host.generate_points(dist, n, 12)
+    kappa = 10.0 if kernel == 3 else 1.0
+    d = ref_descriptor(kernel, pts, leaf, 1e-6, kappa)
+    q = (host.generate_charges_complex if kernel == 3 else host.generate_charges)(n, 88)
+    monkeypatch.setenv("SFMM_K4_GATHER", "1")
+    two = api.GpuPlan(d)
+    u2 = api.fmm_apply(two, q)
+    monkeypatch.setenv("SFMM_K4_GATHER", "0")
+    one = api.GpuPlan(d)
+    assert np.array_equal(u2, api.fmm_apply(one, q))
+    assert two.info().launches_per_apply == one.info().launches_per_apply + 1
+    u_ref, _ = po.oracle_apply(d, q)
+    assert rel_l2(u2, u_ref) <= PARITY
