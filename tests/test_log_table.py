@@ -16,14 +16,15 @@ import pytest
 mpmath = pytest.importorskip("mpmath")
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-INC = os.path.join(ROOT, "paper_2310_16668_b200", "csrc", "log_table.inc")
-SPLIT = 53
+CSRC = os.path.join(ROOT, "paper_2310_16668_b200", "csrc")
+# (file, entries, first right-end entry): fastmath.cuh SFMM_LOG_BITS = 7 / 9
+TABLES = [("log_table.inc", 128, 53), ("log_table512.inc", 512, 213)]
 
 
-def _entries():
+def _entries(inc):
     pat = re.compile(r"\{\s*([-0-9a-fx.p+]+),\s*([-0-9a-fx.p+]+)\s*\}")
     out = []
-    with open(INC) as f:
+    with open(os.path.join(CSRC, inc)) as f:
         for line in f:
             m = pat.search(line)
             if m:
@@ -31,15 +32,16 @@ def _entries():
     return out
 
 
-def test_log_table_is_accurate():
+@pytest.mark.parametrize("inc,size,split", TABLES)
+def test_log_table_is_accurate(inc, size, split):
     mpmath.mp.prec = 160
     ln2 = mpmath.log(2)
-    tab = _entries()
-    assert len(tab) == 128
+    tab = _entries(inc)
+    assert len(tab) == size
     for k, (inv, v) in enumerate(tab):
-        upper = k >= SPLIT
-        c = mpmath.mpf(1) + mpmath.mpf(k + 1 if upper else k) / 128
-        # inv within 2^-24 (relative) of 1/c: |t| < 1/128 + 2^-23 on the entry's interval
+        upper = k >= split
+        c = mpmath.mpf(1) + mpmath.mpf(k + 1 if upper else k) / size
+        # inv within 2^-24 (relative) of 1/c: |t| < 1/size + 2^-23 on the entry's interval
         assert abs(mpmath.mpf(inv) * c - 1) < mpmath.mpf(2) ** -24, k
         exact = -mpmath.log(mpmath.mpf(inv)) - (ln2 if upper else 0)
         if v == 0.0:
