@@ -196,3 +196,22 @@ def test_multi_device_overlapped_exchange(case, monkeypatch):
         u = api.fmm_apply(plan, q)
         assert np.array_equal(api.fmm_apply(plan, q), u)
     assert rel_l2(u, u0) <= 1e-13
+
+
+@pytest.mark.parametrize("case", ["l3d_cube", "h3d_cube"])
+@pytest.mark.parametrize("overlap", ["0", "1"])
+def test_multi_device_merged_tile_tasks(case, overlap, monkeypatch):
+    """The merged-task staging layout on rank plans (cross-rank colleague pairs'
+    column sums packed from one staged vector per pair; interior / boundary
+    task parts with the overlap): same result as the per-tile rank plans."""
+    d, q, _ = _case(case)
+    monkeypatch.setenv("SFMM_SHARD_OVERLAP", overlap)
+    with api.GpuPlan(d, devices=[0, 0, 0, 0]) as plan:
+        u0 = api.fmm_apply(plan, q)
+    monkeypatch.setenv("SFMM_MERGE_TILES", "1")
+    monkeypatch.setenv("SFMM_MERGE_SHARE", "1e9")
+    with api.GpuPlan(d, devices=[0, 0, 0, 0]) as plan:
+        assert plan.info().merged_tasks > 0
+        u = api.fmm_apply(plan, q)
+        assert np.array_equal(api.fmm_apply(plan, q), u)
+    assert rel_l2(u, u0) <= 1e-13
